@@ -1,0 +1,163 @@
+/*
+ * nsreflector.h — C ABI of the B200-native (sm_100a) Newton–Schulz prescribed-index
+ * reflector library, libnsreflector.so.
+ *
+ * WHAT IT COMPUTES (arxiv/paper_2605_24840; P:n = /root/reference/PAPER.md line n):
+ *   For a dense symmetric H (d x d), a shift s in the target spectral gap
+ *   (lambda_k, lambda_{k+1}) and a scale alpha >= ||H - sI||_2, the prescribed-index
+ *   reflector  R_k = I - 2 P_k = sgn(H - sI)   (prop:exact; eq:Pk P:143-145)
+ *   by the scaled Newton–Schulz iteration (eq:NS), written in the
+ *   BASELINE north_star's divide convention:
+ *       X_0 = (H - s I) / alpha,     X_{j+1} = 1.5 X_j - 0.5 X_j (X_j^2).
+ *   Loop convention (reading C2): at step j the library forms
+ *   Y_j = X_j^2, r_j = ||Y_j - I||_F; it stops with CONVERGED when rho_j < tol
+ *   (rho = r_j, or r_j/sqrt(d) in NS_TOL_PER_SQRT_D mode; strict '<', C3/C4), or with
+ *   MAX_STEPS when j == max_steps; otherwise it applies the update.  The returned
+ *   R = X_steps, residual = r_steps, trace = tr R, index_cert = round((d - tr R)/2)
+ *   (half away from zero, C7).  tol = 0 gives fixed-step mode (C5).
+ *
+ * MEMORY, LAYOUT, OWNERSHIP
+ *   - Matrices are FP64, row-major with leading dimension ld >= d (elements).  H is
+ *     symmetric; ONLY ITS UPPER TRIANGLE (i <= j) IS READ.  R is written in full and
+ *     is bitwise symmetric.  R must not alias H.
+ *   - Device pointers: caller-owned CUDA device memory (e.g. torch tensors).  The
+ *     workspace is caller-owned device memory of at least ns_workspace_bytes(...)
+ *     bytes, 256-byte aligned; the library never allocates device memory on the
+ *     hot path.  Work is enqueued on the caller's stream; the call returns after
+ *     the result record is on the host (one stream synchronisation at the end, plus
+ *     bounded look-ahead waits on tiny status records while iterating).
+ *   - `out` / `outs` are HOST memory owned by the caller.
+ *
+ * ERRORS
+ *   Argument violations are detected on the host before any launch and return
+ *   NS_ERR_INVALID_ARG (message via ns_last_error()).  CUDA failures return
+ *   NS_ERR_CUDA.  Numerical outcomes are FLAGS in ns_result_t, never errors
+ *   ("rejection is a value"):  NS_F_CONVERGED, NS_F_MAX_STEPS,
+ *   NS_F_INDEX_MISMATCH (cert != k; R is still sgn(H - sI) for the index the shift
+ *   selects), NS_F_SCALING_SUSPECT (residual rose: alpha < ||H - sI||_2, cor:NS
+ *   P:404-419), NS_F_NONFINITE (NaN/Inf residual; iteration stops at once),
+ *   NS_F_SHIFT_ON_SPECTRUM (|(d - tr R)/2 - cert| > 0.25).
+ *
+ * THREADING: reentrant; at most one call in flight per (stream, workspace).
+ */
+#ifndef NSREFLECTOR_H
+#define NSREFLECTOR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  NS_PREC_FP64 = 0,          /* FP64 DMMA contraction (accuracy path) */
+  NS_PREC_MIXED_BF16X3 = 1,  /* reserved: tcgen05 split-BF16 path (returns NS_ERR_UNSUPPORTED) */
+  NS_PREC_MIXED_TF32X3 = 2   /* reserved: tcgen05 split-TF32 path (returns NS_ERR_UNSUPPORTED) */
+} ns_precision_t;
+
+typedef enum {
+  NS_TOL_ABS = 0,            /* stop when ||X^2 - I||_F < tol */
+  NS_TOL_PER_SQRT_D = 1      /* stop when ||X^2 - I||_F / sqrt(d) < tol */
+} ns_tolmode_t;
+
+typedef enum {
+  NS_OK = 0,
+  NS_ERR_INVALID_ARG = 1,
+  NS_ERR_CUDA = 2,
+  NS_ERR_NCCL = 3,
+  NS_ERR_WORKSPACE = 4,
+  NS_ERR_UNSUPPORTED = 5
+} ns_status_t;
+
+enum {
+  NS_F_CONVERGED = 1,
+  NS_F_MAX_STEPS = 2,
+  NS_F_INDEX_MISMATCH = 4,
+  NS_F_SCALING_SUSPECT = 8,
+  NS_F_NONFINITE = 16,
+  NS_F_SHIFT_ON_SPECTRUM = 32
+};
+
+/* Result record (host).  steps = NS updates applied to the returned R (C2);
+ * residual = ||R^2 - I||_F of the returned R (the check that stopped the loop);
+ * trace = tr R; index_cert = round((d - trace)/2); flags = NS_F_* bits. */
+typedef struct {
+  int32_t steps;
+  int32_t flags;
+  double residual;
+  double trace;
+  int64_t index_cert;
+} ns_result_t;
+
+/* Bytes of device workspace ns_reflector needs for dimension d (batch = 1). */
+size_t ns_workspace_bytes(int64_t d, ns_precision_t prec);
+
+/* Bytes of device workspace ns_reflector_batched needs for `batch` matrices of dimension d. */
+size_t ns_workspace_bytes_batched(int64_t d, int64_t batch, ns_precision_t prec);
+
+/*
+ * ns_reflector — one reflector, run to tolerance (north_star call).
+ *   H      device, d x d, row-major, leading dim ldh >= d; upper triangle read.
+ *   s      shift (finite).      alpha   scale (finite, > 0); X_0 = (H - sI)/alpha.
+ *   k      target index, 0 <= k <= d (the paper's domain is 1..d-1); used
+ *          only for NS_F_INDEX_MISMATCH.
+ *   max_steps >= 0; tol >= 0 (0 = fixed max_steps updates); tm tolerance mode.
+ *   prec   NS_PREC_FP64 (the mixed modes return NS_ERR_UNSUPPORTED in this build).
+ *   R      device, d x d, leading dim ldr >= d; written in full, bitwise symmetric.
+ *   ws     device workspace, ws_bytes >= ns_workspace_bytes(d, prec).
+ *   stream cudaStream_t (as void*); NULL = legacy default stream.
+ *   out    host result record.
+ */
+ns_status_t ns_reflector(const double* H, int64_t d, int64_t ldh, double s, double alpha, int32_t k,
+                         int32_t max_steps, double tol, ns_tolmode_t tm, ns_precision_t prec,
+                         double* R, int64_t ldr, void* ws, size_t ws_bytes, void* stream,
+                         ns_result_t* out);
+
+/*
+ * ns_reflector_host — same computation with HOST H and R (end-to-end entry point):
+ * copies H (host, ldh) to the device workspace, runs ns_reflector, copies R back to
+ * host memory (ldr).  Pinned host buffers give full PCIe bandwidth; pageable works.
+ * The workspace must hold ns_workspace_bytes_host(d, prec) bytes.
+ */
+size_t ns_workspace_bytes_host(int64_t d, ns_precision_t prec);
+ns_status_t ns_reflector_host(const double* H_host, int64_t d, int64_t ldh, double s, double alpha,
+                              int32_t k, int32_t max_steps, double tol, ns_tolmode_t tm,
+                              ns_precision_t prec, double* R_host, int64_t ldr, void* ws,
+                              size_t ws_bytes, void* stream, ns_result_t* out);
+
+/*
+ * ns_reflector_batched — `batch` independent problems (configs[1]: many small H, one
+ * shift each; pass the same H several times via the stride to sweep shifts).
+ *   H      device, H + b*stride_h is problem b's d x d matrix (row-major, ld = d).
+ *   s, alpha, k   HOST arrays [batch].
+ *   R      device, R + b*stride_r receives problem b's reflector (ld = d).
+ *   outs   HOST array [batch] of result records.
+ *   Each problem stops independently (its own steps/flags); problems that stopped
+ *   cost no further contraction work.
+ */
+ns_status_t ns_reflector_batched(const double* H, int64_t d, int64_t batch, int64_t stride_h,
+                                 const double* s, const double* alpha, const int32_t* k,
+                                 int32_t max_steps, double tol, ns_tolmode_t tm, ns_precision_t prec,
+                                 double* R, int64_t stride_r, void* ws, size_t ws_bytes, void* stream,
+                                 ns_result_t* outs);
+
+/*
+ * ns_symm_product — kernel-level entry used by tests: C = A B for symmetric A, B that
+ * commute (so C is symmetric), computed on upper-triangle tiles only and mirrored;
+ * C is bitwise symmetric.  A, B, C device, d x d, leading dim ld (same for all).
+ * mode 0: C = A B.  mode 1: C = 1.5 A - 0.5 (A B) (the NS update epilogue).
+ */
+ns_status_t ns_symm_product(const double* A, const double* B, double* C, int64_t d, int64_t ld,
+                            int32_t mode, void* ws, size_t ws_bytes, void* stream);
+
+/* Library identification: build string with the compile target (e.g. "sm_100a"). */
+const char* ns_build_info(void);
+const char* ns_status_string(ns_status_t st);
+/* Thread-local message for the last non-NS_OK status on this thread ("" if none). */
+const char* ns_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NSREFLECTOR_H */

@@ -23,7 +23,8 @@ are restated here, not imported):
     SCALING_SUSPECT=8  r_{j+1} > r_j (1 + 1e-12) + 1e-10 sqrt(d): with spec(X_0) in
                  [-1,1] every |1 - x^2| shrinks monotonically (prop:NSerr proof,
                  P:456-458), so a rise signals alpha < ||H - sI||_2 (cor:NS P:404-419)
-    NONFINITE=16  r_j is NaN/Inf (stop at once, return X_j)
+    NONFINITE=16  r_j is NaN/Inf (stop at once, return X_j; certificate := -1, so
+                 INDEX_MISMATCH is also set and SHIFT_ON_SPECTRUM is not evaluated)
     SHIFT_ON_SPECTRUM=32  |(d - tr R)/2 - cert| > 0.25 (C7)
 """
 import math
@@ -98,9 +99,12 @@ def ns_reflector(H, s, alpha, k, max_steps, tol, tol_mode=TOL_ABS, trace_residua
         j += 1
     trace = float(np.trace(X))
     half = (d - trace) / 2.0
-    cert = round_half_away(half) if math.isfinite(half) else -1
-    if math.isfinite(half) and abs(half - cert) > 0.25:
-        flags |= SHIFT_ON_SPECTRUM
+    if (flags & NONFINITE) or not math.isfinite(half):
+        cert = -1                      # no certificate for a non-finite iterate (DESIGN.md flags)
+    else:
+        cert = round_half_away(half)
+        if abs(half - cert) > 0.25:
+            flags |= SHIFT_ON_SPECTRUM
     if cert != k:
         flags |= INDEX_MISMATCH
     out = dict(R=X, steps=j, residual=r, trace=trace, cert=cert, flags=flags)

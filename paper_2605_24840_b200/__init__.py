@@ -1,0 +1,209 @@
+"""Thin ctypes binding of libnsreflector.so (include/nsreflector.h).
+
+Argument marshalling only: every step of the Newton–Schulz path runs in the CUDA
+kernels of the shared library.  torch is used for device memory and streams.  There
+is no CPU fallback: importing this package on a machine without the built library
+raises, and calling it with CPU tensors raises.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnsreflector.so")
+
+NS_PREC_FP64, NS_PREC_MIXED_BF16X3, NS_PREC_MIXED_TF32X3 = 0, 1, 2
+NS_TOL_ABS, NS_TOL_PER_SQRT_D = 0, 1
+NS_OK = 0
+NS_F_CONVERGED, NS_F_MAX_STEPS, NS_F_INDEX_MISMATCH = 1, 2, 4
+NS_F_SCALING_SUSPECT, NS_F_NONFINITE, NS_F_SHIFT_ON_SPECTRUM = 8, 16, 32
+
+EXPORTED_SYMBOLS = (
+    "ns_workspace_bytes", "ns_workspace_bytes_batched", "ns_workspace_bytes_host", "ns_reflector",
+    "ns_reflector_host", "ns_reflector_batched", "ns_symm_product", "ns_build_info", "ns_status_string",
+    "ns_last_error",
+)
+
+
+class NsResult(ctypes.Structure):
+    _fields_ = [("steps", ctypes.c_int32), ("flags", ctypes.c_int32), ("residual", ctypes.c_double),
+                ("trace", ctypes.c_double), ("index_cert", ctypes.c_int64)]
+
+    def as_dict(self):
+        return dict(steps=self.steps, flags=self.flags, residual=self.residual, trace=self.trace,
+                    cert=self.index_cert)
+
+
+class NsError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def load_library(path=LIB_PATH):
+    """Load libnsreflector.so (raises if it was not built -- there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise NsError(f"{path} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    c_i64, c_i32, c_dbl, c_vp, c_sz = ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t
+    lib.ns_workspace_bytes.restype = c_sz
+    lib.ns_workspace_bytes.argtypes = [c_i64, ctypes.c_int]
+    lib.ns_workspace_bytes_batched.restype = c_sz
+    lib.ns_workspace_bytes_batched.argtypes = [c_i64, c_i64, ctypes.c_int]
+    lib.ns_workspace_bytes_host.restype = c_sz
+    lib.ns_workspace_bytes_host.argtypes = [c_i64, ctypes.c_int]
+    lib.ns_reflector.restype = ctypes.c_int
+    lib.ns_reflector.argtypes = [c_vp, c_i64, c_i64, c_dbl, c_dbl, c_i32, c_i32, c_dbl, ctypes.c_int, ctypes.c_int,
+                                 c_vp, c_i64, c_vp, c_sz, c_vp, ctypes.POINTER(NsResult)]
+    lib.ns_reflector_host.restype = ctypes.c_int
+    lib.ns_reflector_host.argtypes = lib.ns_reflector.argtypes
+    lib.ns_reflector_batched.restype = ctypes.c_int
+    lib.ns_reflector_batched.argtypes = [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_i32, c_dbl, ctypes.c_int,
+                                         ctypes.c_int, c_vp, c_i64, c_vp, c_sz, c_vp, ctypes.POINTER(NsResult)]
+    lib.ns_symm_product.restype = ctypes.c_int
+    lib.ns_symm_product.argtypes = [c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, c_vp, c_sz, c_vp]
+    lib.ns_build_info.restype = ctypes.c_char_p
+    lib.ns_status_string.restype = ctypes.c_char_p
+    lib.ns_status_string.argtypes = [ctypes.c_int]
+    lib.ns_last_error.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def _check(st):
+    if st != NS_OK:
+        lib = load_library()
+        raise NsError(f"{lib.ns_status_string(st).decode()}: {lib.ns_last_error().decode()}")
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_ptr(stream):
+    torch = _torch()
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _require_cuda_f64(t, name):
+    torch = _torch()
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64):
+        raise NsError(f"{name} must be a CUDA float64 tensor (no CPU fallback)")
+
+
+def ns_workspace_bytes(d, prec=NS_PREC_FP64):
+    return load_library().ns_workspace_bytes(d, prec)
+
+
+def ns_workspace_bytes_batched(d, batch, prec=NS_PREC_FP64):
+    return load_library().ns_workspace_bytes_batched(d, batch, prec)
+
+
+def alloc_workspace(nbytes, device):
+    torch = _torch()
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+def ns_reflector(H, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_ABS, prec=NS_PREC_FP64, R=None, ws=None,
+                 stream=None):
+    """R = sgn(H - sI) by Newton–Schulz on the GPU (C-ABI ns_reflector).  Returns (R, result dict)."""
+    torch = _torch()
+    lib = load_library()
+    _require_cuda_f64(H, "H")
+    d = H.shape[0]
+    if H.dim() != 2 or H.shape[1] != d or H.stride(1) != 1:
+        raise NsError("H must be a square row-major (stride(1)==1) matrix")
+    if R is None:
+        R = torch.empty((d, d), dtype=torch.float64, device=H.device)
+    _require_cuda_f64(R, "R")
+    need = lib.ns_workspace_bytes(d, prec)
+    if ws is None:
+        ws = alloc_workspace(need, H.device)
+    res = NsResult()
+    st = lib.ns_reflector(ctypes.c_void_p(H.data_ptr()), d, H.stride(0), float(s), float(alpha), int(k),
+                          int(max_steps), float(tol), int(tol_mode), int(prec), ctypes.c_void_p(R.data_ptr()),
+                          R.stride(0), ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream),
+                          ctypes.byref(res))
+    _check(st)
+    return R, res.as_dict()
+
+
+def ns_reflector_host(H, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_ABS, prec=NS_PREC_FP64, R=None, ws=None,
+                      stream=None, device=None):
+    """End-to-end entry: host (numpy or pinned CPU torch) H in, host R out (C-ABI ns_reflector_host)."""
+    torch = _torch()
+    lib = load_library()
+    if isinstance(H, np.ndarray):
+        H = torch.from_numpy(np.ascontiguousarray(H, dtype=np.float64))
+    if H.is_cuda or H.dtype != torch.float64:
+        raise NsError("H must be a CPU float64 tensor/array")
+    d = H.shape[0]
+    if R is None:
+        R = torch.empty((d, d), dtype=torch.float64, pin_memory=H.is_pinned())
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+    if ws is None:
+        ws = alloc_workspace(lib.ns_workspace_bytes_host(d, prec), dev)
+    res = NsResult()
+    st = lib.ns_reflector_host(ctypes.c_void_p(H.data_ptr()), d, H.stride(0), float(s), float(alpha), int(k),
+                               int(max_steps), float(tol), int(tol_mode), int(prec), ctypes.c_void_p(R.data_ptr()),
+                               R.stride(0), ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream),
+                               ctypes.byref(res))
+    _check(st)
+    return R, res.as_dict()
+
+
+def ns_reflector_batched(H, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_ABS, prec=NS_PREC_FP64, R=None, ws=None,
+                         stream=None):
+    """Batched reflectors: H (batch, d, d) CUDA float64; s, alpha, k per problem (host sequences)."""
+    torch = _torch()
+    lib = load_library()
+    _require_cuda_f64(H, "H")
+    if H.dim() != 3 or H.shape[1] != H.shape[2] or not H.is_contiguous():
+        raise NsError("H must be a contiguous (batch, d, d) tensor")
+    b, d = H.shape[0], H.shape[1]
+    s_a = np.ascontiguousarray(np.broadcast_to(np.asarray(s, dtype=np.float64), (b,)))
+    a_a = np.ascontiguousarray(np.broadcast_to(np.asarray(alpha, dtype=np.float64), (b,)))
+    k_a = np.ascontiguousarray(np.broadcast_to(np.asarray(k, dtype=np.int32), (b,)))
+    if R is None:
+        R = torch.empty_like(H)
+    _require_cuda_f64(R, "R")
+    if ws is None:
+        ws = alloc_workspace(lib.ns_workspace_bytes_batched(d, b, prec), H.device)
+    outs = (NsResult * b)()
+    st = lib.ns_reflector_batched(ctypes.c_void_p(H.data_ptr()), d, b, H.stride(0), s_a.ctypes.data,
+                                  a_a.ctypes.data, k_a.ctypes.data, int(max_steps), float(tol), int(tol_mode),
+                                  int(prec), ctypes.c_void_p(R.data_ptr()), R.stride(0),
+                                  ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream), outs)
+    _check(st)
+    return R, [o.as_dict() for o in outs]
+
+
+def ns_symm_product(A, B, mode=0, C=None, ws=None, stream=None):
+    """C = A B (mode 0) or 1.5 A - 0.5 A B (mode 1) for commuting symmetric A, B (upper triangles read)."""
+    torch = _torch()
+    lib = load_library()
+    _require_cuda_f64(A, "A")
+    _require_cuda_f64(B, "B")
+    d = A.shape[0]
+    if A.stride(0) != B.stride(0):
+        raise NsError("A and B must share a leading dimension")
+    if C is None:
+        C = torch.empty_like(A)
+    if ws is None:
+        ws = alloc_workspace(lib.ns_workspace_bytes(d, NS_PREC_FP64), A.device)
+    st = lib.ns_symm_product(ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()),
+                             ctypes.c_void_p(C.data_ptr()), d, A.stride(0), int(mode),
+                             ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream))
+    _check(st)
+    return C
+
+
+def build_info():
+    return load_library().ns_build_info().decode()

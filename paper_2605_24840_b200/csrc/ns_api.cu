@@ -1,0 +1,383 @@
+// C-ABI entry points of libnsreflector.so (declared in include/nsreflector.h).
+//
+// Host responsibilities only: argument validation, workspace carve-up, TMA tensor-map
+// encoding, and the step loop that enqueues the device kernels (ns_fp64.cu).  The stop
+// decision is taken on the device (ns_decide_kernel); the host enqueues a bounded number
+// of steps ahead and only reads a 4-byte "problems still running" counter, so kernels
+// enqueued after convergence exit immediately.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/nsreflector.h"
+#include "ns_internal.h"
+
+using namespace nsr;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+ns_status_t fail(ns_status_t st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+#define NS_CUDA(x)                                                                          \
+  do {                                                                                      \
+    cudaError_t e_ = (x);                                                                   \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail(NS_ERR_CUDA, "%s failed: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                                \
+  } while (0)
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Layout {
+  int d = 0, d_pad = 0, n = 0, n_tiles = 0;
+  long long batch = 1;
+  size_t off_xa = 0, off_xb = 0, off_y = 0, off_res = 0, off_tr = 0, off_tiles = 0, off_jobs = 0,
+         off_state = 0, off_active = 0, total = 0;
+};
+
+Layout make_layout(int64_t d, int64_t batch) {
+  Layout L;
+  L.d = static_cast<int>(d);
+  L.d_pad = static_cast<int>((d + kTile - 1) / kTile * kTile);
+  L.n = L.d_pad / kTile;
+  L.n_tiles = L.n * (L.n + 1) / 2;
+  L.batch = batch;
+  const size_t mat = (size_t)L.d_pad * (size_t)L.d_pad * sizeof(double) * (size_t)batch;
+  size_t o = 0;
+  L.off_xa = o; o = align256(o + mat);
+  L.off_xb = o; o = align256(o + mat);
+  L.off_y = o; o = align256(o + mat);
+  L.off_res = o; o = align256(o + sizeof(double) * (size_t)L.n_tiles * batch);
+  L.off_tr = o; o = align256(o + sizeof(double) * (size_t)L.n * batch);
+  L.off_tiles = o; o = align256(o + sizeof(int2) * (size_t)L.n_tiles);
+  L.off_jobs = o; o = align256(o + sizeof(JobParams) * (size_t)batch);
+  L.off_state = o; o = align256(o + sizeof(DevState) * (size_t)batch);
+  L.off_active = o; o = align256(o + 256);
+  L.total = o;
+  return L;
+}
+
+// Upper-triangle tile order: super-blocks of G x G tiles (row-major over the upper
+// triangle of super-blocks), row-major inside each.  Co-resident CTAs then share a
+// few dozen row panels, so each k-slab of a panel is fetched from HBM about once per
+// wave and re-read from L2 by the other CTAs.
+std::vector<int2> make_tiles(int n) {
+  const int G = 8;
+  std::vector<int2> v;
+  v.reserve((size_t)n * (n + 1) / 2);
+  for (int SI = 0; SI < n; SI += G)
+    for (int SJ = SI; SJ < n; SJ += G)
+      for (int I = SI; I < std::min(SI + G, n); ++I)
+        for (int J = std::max(SJ, I); J < std::min(SJ + G, n); ++J) v.push_back(make_int2(I, J));
+  return v;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 3-D map over `batch` row-major d_pad x d_pad FP64 matrices; box = 16 (k) x 128 (rows) x 1,
+// 128-byte swizzle (the consumer's fragment addressing assumes exactly this pattern).
+ns_status_t encode_map(CUtensorMap* m, const double* base, int d_pad, long long batch) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(NS_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)d_pad, (cuuint64_t)d_pad, (cuuint64_t)batch};
+  cuuint64_t strides[2] = {(cuuint64_t)d_pad * 8, (cuuint64_t)d_pad * (cuuint64_t)d_pad * 8};
+  cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)kTile, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(NS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return NS_OK;
+}
+
+struct HostRing {
+  int* slots = nullptr;
+  cudaEvent_t ev[16];
+  bool ok = false;
+};
+
+HostRing& ring() {
+  static thread_local HostRing r;
+  if (!r.ok) {
+    if (cudaHostAlloc(&r.slots, 16 * sizeof(int), cudaHostAllocDefault) != cudaSuccess) return r;
+    for (int i = 0; i < 16; ++i) cudaEventCreateWithFlags(&r.ev[i], cudaEventDisableTiming);
+    r.ok = true;
+  }
+  return r;
+}
+
+ns_status_t check_common(int64_t d, int32_t max_steps, double tol, ns_tolmode_t tm, ns_precision_t prec) {
+  if (d < 1 || d > 65536) return fail(NS_ERR_INVALID_ARG, "d must be in [1, 65536], got %lld", (long long)d);
+  if (max_steps < 0) return fail(NS_ERR_INVALID_ARG, "max_steps must be >= 0");
+  if (!(tol >= 0.0) || !std::isfinite(tol)) return fail(NS_ERR_INVALID_ARG, "tol must be finite and >= 0");
+  if (tm != NS_TOL_ABS && tm != NS_TOL_PER_SQRT_D) return fail(NS_ERR_INVALID_ARG, "bad tolerance mode");
+  if (prec == NS_PREC_MIXED_BF16X3 || prec == NS_PREC_MIXED_TF32X3)
+    return fail(NS_ERR_UNSUPPORTED, "mixed-precision modes are not available in this build");
+  if (prec != NS_PREC_FP64) return fail(NS_ERR_INVALID_ARG, "bad precision");
+  return NS_OK;
+}
+
+// The step loop shared by the single, host and batched entry points.  H: batch matrices
+// at H + b*h_stride (ld ldh).  R likewise.  Returns per-job states in `states`.
+ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ldh, long long h_stride,
+                     const std::vector<JobParams>& jobs, int32_t max_steps, double tol, ns_tolmode_t tm, double* R,
+                     long long ldr, long long r_stride, cudaStream_t st, std::vector<DevState>& states) {
+  const int batch = (int)L.batch;
+  double* Xa = reinterpret_cast<double*>(ws + L.off_xa);
+  double* Xb = reinterpret_cast<double*>(ws + L.off_xb);
+  double* Y = reinterpret_cast<double*>(ws + L.off_y);
+  double* res = reinterpret_cast<double*>(ws + L.off_res);
+  double* trp = reinterpret_cast<double*>(ws + L.off_tr);
+  int2* tiles = reinterpret_cast<int2*>(ws + L.off_tiles);
+  JobParams* djobs = reinterpret_cast<JobParams*>(ws + L.off_jobs);
+  DevState* state = reinterpret_cast<DevState*>(ws + L.off_state);
+  int* n_active = reinterpret_cast<int*>(ws + L.off_active);
+
+  HostRing& rg = ring();
+  if (!rg.ok) return fail(NS_ERR_CUDA, "pinned status ring allocation failed");
+
+  std::vector<int2> tl = make_tiles(L.n);
+  NS_CUDA(cudaMemcpyAsync(tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+  NS_CUDA(cudaMemcpyAsync(djobs, jobs.data(), jobs.size() * sizeof(JobParams), cudaMemcpyHostToDevice, st));
+
+  CUtensorMap tmA, tmB, tmY;
+  ns_status_t s;
+  if ((s = encode_map(&tmA, Xa, L.d_pad, batch)) != NS_OK) return s;
+  if ((s = encode_map(&tmB, Xb, L.d_pad, batch)) != NS_OK) return s;
+  if ((s = encode_map(&tmY, Y, L.d_pad, batch)) != NS_OK) return s;
+
+  NS_CUDA(launch_zero_state(state, batch, n_active, st));
+  NS_CUDA(launch_init(H, ldh, h_stride, Xa, djobs, L.d, L.d_pad, batch, st));
+  NS_CUDA(launch_trace_partials(Xa, L.d, L.d_pad, batch, trp, st));
+
+  LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol};
+  const long long job_stride = (long long)L.d_pad * L.d_pad;
+  // look-ahead: how many steps may be in flight before the host checks the counter
+  const double step_flops = 2.0 * (double)L.n_tiles * kTile * kTile * (double)L.d_pad * batch;
+  const int LA = step_flops > 2e10 ? 2 : 8;
+
+  for (int j = 0; j <= max_steps; ++j) {
+    if (j >= LA) {
+      const int slot = (j - LA) % 16;
+      NS_CUDA(cudaEventSynchronize(rg.ev[slot]));
+      if (rg.slots[slot] == 0) break;
+    }
+    const bool odd = (j & 1) != 0;
+    double* Xc = odd ? Xb : Xa;
+    double* Xn = odd ? Xa : Xb;
+    const CUtensorMap& tmC = odd ? tmB : tmA;
+
+    ProdParams sq{tiles, L.n_tiles, L.d_pad / kBK, L.d, L.d_pad, job_stride, Y, nullptr, res, state, 0};
+    NS_CUDA(launch_product(tmC, tmC, sq, batch, st));
+    NS_CUDA(launch_decide(state, djobs, res, L.n_tiles, trp, L.n, lp, batch, n_active, st));
+    if (j < max_steps) {
+      ProdParams up{tiles, L.n_tiles, L.d_pad / kBK, L.d, L.d_pad, job_stride, Xn, Xc, trp, state, 1};
+      NS_CUDA(launch_product(tmC, tmY, up, batch, st));
+    }
+    const int slot = j % 16;
+    NS_CUDA(cudaMemcpyAsync(&rg.slots[slot], n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+    NS_CUDA(cudaEventRecord(rg.ev[slot], st));
+  }
+  NS_CUDA(launch_copy_out(Xa, Xb, L.d, L.d_pad, state, R, ldr, r_stride, batch, st));
+  states.resize(batch);
+  NS_CUDA(cudaMemcpyAsync(states.data(), state, sizeof(DevState) * batch, cudaMemcpyDeviceToHost, st));
+  NS_CUDA(cudaStreamSynchronize(st));
+  return NS_OK;
+}
+
+void fill_result(const DevState& s, ns_result_t* out) {
+  out->steps = s.j;
+  out->flags = s.flags;
+  out->residual = s.residual;
+  out->trace = s.trace;
+  out->index_cert = s.cert;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t ns_workspace_bytes(int64_t d, ns_precision_t prec) {
+  (void)prec;
+  if (d < 1) return 0;
+  return make_layout(d, 1).total;
+}
+
+size_t ns_workspace_bytes_batched(int64_t d, int64_t batch, ns_precision_t prec) {
+  (void)prec;
+  if (d < 1 || batch < 1) return 0;
+  return make_layout(d, batch).total;
+}
+
+size_t ns_workspace_bytes_host(int64_t d, ns_precision_t prec) { return ns_workspace_bytes(d, prec); }
+
+ns_status_t ns_reflector(const double* H, int64_t d, int64_t ldh, double s, double alpha, int32_t k,
+                         int32_t max_steps, double tol, ns_tolmode_t tm, ns_precision_t prec, double* R, int64_t ldr,
+                         void* ws, size_t ws_bytes, void* stream, ns_result_t* out) {
+  g_last_error.clear();
+  ns_status_t st = check_common(d, max_steps, tol, tm, prec);
+  if (st != NS_OK) return st;
+  if (!H || !R || !ws || !out) return fail(NS_ERR_INVALID_ARG, "null pointer argument");
+  if (ldh < d || ldr < d) return fail(NS_ERR_INVALID_ARG, "leading dimensions must be >= d");
+  if (!std::isfinite(s)) return fail(NS_ERR_INVALID_ARG, "shift s must be finite");
+  if (!(alpha > 0.0) || !std::isfinite(alpha)) return fail(NS_ERR_INVALID_ARG, "alpha must be finite and > 0");
+  if (k < 0 || k > d) return fail(NS_ERR_INVALID_ARG, "k must lie in [0, d]");
+  if (R == H) return fail(NS_ERR_INVALID_ARG, "R must not alias H");
+  if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(NS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+  const Layout L = make_layout(d, 1);
+  if (ws_bytes < L.total)
+    return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
+  std::vector<JobParams> jobs{JobParams{s, alpha, k, 0}};
+  std::vector<DevState> states;
+  st = run_loop(L, static_cast<uint8_t*>(ws), H, ldh, 0, jobs, max_steps, tol, tm, R, ldr, 0,
+                static_cast<cudaStream_t>(stream), states);
+  if (st != NS_OK) return st;
+  fill_result(states[0], out);
+  return NS_OK;
+}
+
+ns_status_t ns_reflector_host(const double* H_host, int64_t d, int64_t ldh, double s, double alpha, int32_t k,
+                              int32_t max_steps, double tol, ns_tolmode_t tm, ns_precision_t prec, double* R_host,
+                              int64_t ldr, void* ws, size_t ws_bytes, void* stream, ns_result_t* out) {
+  g_last_error.clear();
+  ns_status_t st = check_common(d, max_steps, tol, tm, prec);
+  if (st != NS_OK) return st;
+  if (!H_host || !R_host || !ws || !out) return fail(NS_ERR_INVALID_ARG, "null pointer argument");
+  if (ldh < d || ldr < d) return fail(NS_ERR_INVALID_ARG, "leading dimensions must be >= d");
+  if (!std::isfinite(s)) return fail(NS_ERR_INVALID_ARG, "shift s must be finite");
+  if (!(alpha > 0.0) || !std::isfinite(alpha)) return fail(NS_ERR_INVALID_ARG, "alpha must be finite and > 0");
+  if (k < 0 || k > d) return fail(NS_ERR_INVALID_ARG, "k must lie in [0, d]");
+  if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(NS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+  const Layout L = make_layout(d, 1);
+  if (ws_bytes < L.total)
+    return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  // H staged in the Y buffer (dead until the first square), R staged there after the loop.
+  double* stage = reinterpret_cast<double*>(w + L.off_y);
+  NS_CUDA(cudaMemcpy2DAsync(stage, (size_t)d * 8, H_host, (size_t)ldh * 8, (size_t)d * 8, (size_t)d,
+                            cudaMemcpyHostToDevice, cs));
+  std::vector<JobParams> jobs{JobParams{s, alpha, k, 0}};
+  std::vector<DevState> states;
+  st = run_loop(L, w, stage, d, 0, jobs, max_steps, tol, tm, stage, d, 0, cs, states);
+  if (st != NS_OK) return st;
+  NS_CUDA(cudaMemcpy2DAsync(R_host, (size_t)ldr * 8, stage, (size_t)d * 8, (size_t)d * 8, (size_t)d,
+                            cudaMemcpyDeviceToHost, cs));
+  NS_CUDA(cudaStreamSynchronize(cs));
+  fill_result(states[0], out);
+  return NS_OK;
+}
+
+ns_status_t ns_reflector_batched(const double* H, int64_t d, int64_t batch, int64_t stride_h, const double* s,
+                                 const double* alpha, const int32_t* k, int32_t max_steps, double tol,
+                                 ns_tolmode_t tm, ns_precision_t prec, double* R, int64_t stride_r, void* ws,
+                                 size_t ws_bytes, void* stream, ns_result_t* outs) {
+  g_last_error.clear();
+  ns_status_t st = check_common(d, max_steps, tol, tm, prec);
+  if (st != NS_OK) return st;
+  if (batch < 1 || batch > 65535) return fail(NS_ERR_INVALID_ARG, "batch must be in [1, 65535]");
+  if (!H || !R || !ws || !outs || !s || !alpha || !k) return fail(NS_ERR_INVALID_ARG, "null pointer argument");
+  if (stride_h < d * d || stride_r < d * d) return fail(NS_ERR_INVALID_ARG, "strides must be >= d*d");
+  if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(NS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+  std::vector<JobParams> jobs(batch);
+  for (int64_t b = 0; b < batch; ++b) {
+    if (!std::isfinite(s[b])) return fail(NS_ERR_INVALID_ARG, "s[%lld] not finite", (long long)b);
+    if (!(alpha[b] > 0.0) || !std::isfinite(alpha[b]))
+      return fail(NS_ERR_INVALID_ARG, "alpha[%lld] must be finite and > 0", (long long)b);
+    if (k[b] < 0 || k[b] > d) return fail(NS_ERR_INVALID_ARG, "k[%lld] out of [0, d]", (long long)b);
+    jobs[b] = JobParams{s[b], alpha[b], k[b], 0};
+  }
+  const Layout L = make_layout(d, batch);
+  if (ws_bytes < L.total)
+    return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
+  std::vector<DevState> states;
+  st = run_loop(L, static_cast<uint8_t*>(ws), H, d, stride_h, jobs, max_steps, tol, tm, R, d, stride_r,
+                static_cast<cudaStream_t>(stream), states);
+  if (st != NS_OK) return st;
+  for (int64_t b = 0; b < batch; ++b) fill_result(states[b], &outs[b]);
+  return NS_OK;
+}
+
+ns_status_t ns_symm_product(const double* A, const double* B, double* C, int64_t d, int64_t ld, int32_t mode,
+                            void* ws, size_t ws_bytes, void* stream) {
+  g_last_error.clear();
+  if (d < 1 || d > 65536) return fail(NS_ERR_INVALID_ARG, "bad d");
+  if (ld < d) return fail(NS_ERR_INVALID_ARG, "ld must be >= d");
+  if (mode != 0 && mode != 1) return fail(NS_ERR_INVALID_ARG, "mode must be 0 or 1");
+  if (!A || !B || !C || !ws) return fail(NS_ERR_INVALID_ARG, "null pointer argument");
+  if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(NS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+  const Layout L = make_layout(d, 1);
+  if (ws_bytes < L.total) return fail(NS_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  double* Pa = reinterpret_cast<double*>(w + L.off_xa);   // padded A
+  double* Pb = reinterpret_cast<double*>(w + L.off_xb);   // padded B
+  double* Pc = reinterpret_cast<double*>(w + L.off_y);    // padded C
+  int2* tiles = reinterpret_cast<int2*>(w + L.off_tiles);
+  JobParams* djobs = reinterpret_cast<JobParams*>(w + L.off_jobs);
+  std::vector<int2> tl = make_tiles(L.n);
+  NS_CUDA(cudaMemcpyAsync(tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, cs));
+  JobParams unit{0.0, 1.0, 0, 0};
+  NS_CUDA(cudaMemcpyAsync(djobs, &unit, sizeof(unit), cudaMemcpyHostToDevice, cs));
+  // pad (and symmetrise from the upper triangle, s = 0, alpha = 1)
+  NS_CUDA(launch_init(A, ld, 0, Pa, djobs, L.d, L.d_pad, 1, cs));
+  NS_CUDA(launch_init(B, ld, 0, Pb, djobs, L.d, L.d_pad, 1, cs));
+  CUtensorMap tA, tB;
+  ns_status_t s;
+  if ((s = encode_map(&tA, Pa, L.d_pad, 1)) != NS_OK) return s;
+  if ((s = encode_map(&tB, Pb, L.d_pad, 1)) != NS_OK) return s;
+  ProdParams p{tiles, L.n_tiles, L.d_pad / kBK, L.d, L.d_pad, 0, Pc, Pa,
+               reinterpret_cast<double*>(w + (mode == 0 ? L.off_res : L.off_tr)), nullptr, mode};
+  NS_CUDA(launch_product(tA, tB, p, 1, cs));
+  NS_CUDA(cudaMemcpy2DAsync(C, (size_t)ld * 8, Pc, (size_t)L.d_pad * 8, (size_t)d * 8, (size_t)d,
+                            cudaMemcpyDeviceToDevice, cs));
+  NS_CUDA(cudaStreamSynchronize(cs));
+  return NS_OK;
+}
+
+const char* ns_build_info(void) {
+  return "libnsreflector FP64 DMMA/TMA path; target sm_100a; tile 128x128x16, 6-stage TMA ring, 8 DMMA warps";
+}
+
+const char* ns_status_string(ns_status_t st) {
+  switch (st) {
+    case NS_OK: return "NS_OK";
+    case NS_ERR_INVALID_ARG: return "NS_ERR_INVALID_ARG";
+    case NS_ERR_CUDA: return "NS_ERR_CUDA";
+    case NS_ERR_NCCL: return "NS_ERR_NCCL";
+    case NS_ERR_WORKSPACE: return "NS_ERR_WORKSPACE";
+    case NS_ERR_UNSUPPORTED: return "NS_ERR_UNSUPPORTED";
+  }
+  return "NS_ERR_UNKNOWN";
+}
+
+const char* ns_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"

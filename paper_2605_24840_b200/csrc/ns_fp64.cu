@@ -1,0 +1,413 @@
+// FP64 Newton–Schulz kernels for sm_100a (B200).
+//
+// Hot path (BASELINE north_star; eq:NS P:373-379, divide convention C1):
+//   X_0 = (H - sI)/alpha                      ns_init_kernel        (HBM-bound, O(d^2))
+//   Y_j = X_j X_j   + r_j = ||Y_j - I||_F      ns_product_kernel<0>  (symmetric: upper tiles only)
+//   decide: rho_j < tol | j == max_steps       ns_decide_kernel      (1 CTA per problem)
+//   X_{j+1} = 1.5 X_j - 0.5 X_j Y_j  + tr      ns_product_kernel<1>  (Z = X Y is symmetric since
+//                                                                     X and Y commute)
+//   R = X_steps                               ns_copy_out_kernel
+//
+// Contraction core: C_IJ = sum_k P[I,k] Q[J,k] for 128x128 output tiles with I <= J.
+// Both operands are ROW panels of symmetric matrices (Y = X X^T, Z = X Y^T), so one
+// TMA box shape serves both.  FP64 has no tcgen05 kind on sm_100a; the FP64 tensor
+// instruction is warp-level DMMA (mma.sync m8n8k4 .f64, SASS DMMA.8x8x4), fed here by
+// a TMA + mbarrier ring with a dedicated producer warp and 8 DMMA consumer warps.
+// Shared-memory tiles use the TMA 128-byte swizzle; the consumer's k-permutation
+// (k = 4t + s within a 16-wide slab) turns each fragment fetch into a conflict-free
+// 128-bit LDS.  Epilogue: tile staged through shared memory, written row-major and
+// mirrored (bitwise-symmetric output), with per-tile residual / trace partials that
+// the decide kernel reduces in a fixed order (deterministic).
+#include <cmath>
+#include <cstdint>
+
+#include "ns_internal.h"
+#include "ns_ptx.cuh"
+
+namespace nsr {
+
+// --------------------------------------------------------------------------------------
+// X_0 = (H - sI)/alpha from the UPPER triangle of H, zero-padded to d_pad.
+// 32x32 blocks; block (bi,bj) reads H's tile (min,max) and writes its own tile.
+// --------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) ns_init_kernel(const double* __restrict__ H, long long ldh,
+                                                      long long h_stride, double* __restrict__ X,
+                                                      const JobParams* __restrict__ jobs, int d, int d_pad) {
+  __shared__ double t[32][33];
+  const int job = blockIdx.z;
+  const int bi = blockIdx.y, bj = blockIdx.x;
+  const double* Hj = H + (long long)job * h_stride;
+  double* Xj = X + (long long)job * d_pad * (long long)d_pad;
+  const double s = jobs[job].s, alpha = jobs[job].alpha;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const int ri = min(bi, bj), rj = max(bi, bj);           // source tile in the upper triangle
+  for (int y = ty; y < 32; y += 8) {
+    const int gi = ri * 32 + y, gj = rj * 32 + tx;
+    t[y][tx] = (gi < d && gj < d && gi <= gj) ? Hj[(long long)gi * ldh + gj] : 0.0;
+  }
+  __syncthreads();
+  for (int y = ty; y < 32; y += 8) {
+    const int gi = bi * 32 + y, gj = bj * 32 + tx;
+    double v = 0.0;
+    if (gi < d && gj < d) {
+      const double h = (gi <= gj) ? t[gi - ri * 32][gj - rj * 32] : t[gj - ri * 32][gi - rj * 32];
+      v = (gi == gj) ? (h - s) / alpha : h / alpha;
+    }
+    Xj[(long long)gi * d_pad + gj] = v;
+  }
+}
+
+// tr X per 128-row diagonal block (fixed-order block reduction) -> tr_partial[job*n + b].
+__global__ void __launch_bounds__(128) ns_trace_partials_kernel(const double* __restrict__ X, int d, int d_pad,
+                                                                double* __restrict__ tr_partial) {
+  __shared__ double red[4];
+  const int job = blockIdx.y, b = blockIdx.x, n = gridDim.x;
+  const int i = b * kTile + threadIdx.x;
+  double v = (i < d) ? X[(long long)job * d_pad * d_pad + (long long)i * d_pad + i] : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) tr_partial[(long long)job * n + b] = ((red[0] + red[1]) + red[2]) + red[3];
+}
+
+// --------------------------------------------------------------------------------------
+// Symmetric-output product kernel (one 128x128 upper tile per CTA).
+// --------------------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+    ns_product_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
+                      const ProdParams p) {
+  const int job = blockIdx.y;
+  if (p.state != nullptr && p.state[job].done) return;  // uniform per CTA
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  double* sA = reinterpret_cast<double*>(smem);                                   // [stages][128*16]
+  double* sB = reinterpret_cast<double*>(smem + kStages * kTile * kBK * 8);      // [stages][128*16]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  __shared__ double red[kConsumerWarps];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int2 tile = p.tiles[blockIdx.x];
+  const int I = tile.x, J = tile.y;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ---------------- TMA producer (one elected lane) ----------------
+    if (lane == 0) {
+      tma_prefetch_desc(&tmP);
+      tma_prefetch_desc(&tmQ);
+      for (int kt = 0; kt < p.nk; ++kt) {
+        const int s = kt % kStages;
+        const uint32_t use = kt / kStages;
+        if (kt >= kStages) mbar_wait(&empty[s], (use & 1u) ^ 1u);
+        mbar_arrive_expect_tx(&full[s], kStageBytes);
+        tma_load_3d(sA + s * kTile * kBK, &tmP, kt * kBK, I * kTile, job, &full[s]);
+        tma_load_3d(sB + s * kTile * kBK, &tmQ, kt * kBK, J * kTile, job, &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ---------------- DMMA consumers: warp tile 64 (rows of P) x 32 (rows of Q) ----------------
+  const int cw = warp - 1;        // 0..7
+  const int wm = cw >> 2;         // 0..1  -> rows wm*64
+  const int wn = cw & 3;          // 0..3  -> cols wn*32
+  const int g = lane >> 2, t = lane & 3;
+  // byte offsets inside a 128x16-double swizzled tile: row r -> r*128, 16-B chunk c -> (c ^ (r&7))*16;
+  // r & 7 == g for every fragment row below.
+  const uint32_t off_h0 = static_cast<uint32_t>(((2 * t + 0) ^ g) << 4);
+  const uint32_t off_h1 = static_cast<uint32_t>(((2 * t + 1) ^ g) << 4);
+  const uint32_t a_row = static_cast<uint32_t>((wm * 64 + g) * 128);
+  const uint32_t b_row = static_cast<uint32_t>((wn * 32 + g) * 128);
+  const uint32_t sA_u32 = smem_u32(sA), sB_u32 = smem_u32(sB);
+
+  double acc[8][4][2];
+#pragma unroll
+  for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+
+  for (int kt = 0; kt < p.nk; ++kt) {
+    const int s = kt % kStages;
+    mbar_wait(&full[s], static_cast<uint32_t>(kt / kStages) & 1u);
+    const uint32_t aS = sA_u32 + s * (kTile * kBK * 8) + a_row;
+    const uint32_t bS = sB_u32 + s * (kTile * kBK * 8) + b_row;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t off = h ? off_h1 : off_h0;
+      // B fragments for both k-values of this half-slab stay live (16 regs); A fragments are
+      // streamed one m-row at a time so the 128 accumulator registers fit the 168-register
+      // budget of a 9-warp CTA (3 warps share one SMSP's 64 KB register file).
+      double b[4][2];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) lds128(bS + ni * 8 * 128 + off, b[ni][0], b[ni][1]);
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi) {
+        double a0, a1;
+        lds128(aS + mi * 8 * 128 + off, a0, a1);
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a0, b[ni][0]);
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a1, b[ni][1]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  // ---------------- epilogue ----------------
+  // All stages consumed by every consumer warp before the ring is reused as staging.
+  named_bar_sync(1, 32 * kConsumerWarps);
+  double* S = reinterpret_cast<double*>(smem);   // [128][kEpiPitch]
+#pragma unroll
+  for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int r = wm * 64 + mi * 8 + g;
+      const int c = wn * 32 + ni * 8 + 2 * t;
+      S[r * kEpiPitch + c] = acc[mi][ni][0];
+      S[r * kEpiPitch + c + 1] = acc[mi][ni][1];
+    }
+  named_bar_sync(1, 32 * kConsumerWarps);
+
+  const int tid = threadIdx.x - 32;   // 0..255
+  const long long ld = p.ld;
+  const long long base = (long long)job * p.job_stride;
+  double* C = p.C + base;
+  const bool diag = (I == J);
+  double part = 0.0;
+
+  if (MODE == 0) {
+    // Y tile + residual partial: off-diagonal tiles count twice (Y_JI = Y_IJ^T).
+    if (!diag) {
+      for (int idx = tid; idx < kTile * kTile; idx += 256) {
+        const int r = idx >> 7, c = idx & 127;
+        const double v = S[r * kEpiPitch + c];
+        C[(long long)(I * kTile + r) * ld + J * kTile + c] = v;
+        part += v * v;
+      }
+      part *= 2.0;
+      for (int idx = tid; idx < kTile * kTile; idx += 256) {
+        const int r = idx >> 7, c = idx & 127;   // mirror row J*128+r, col I*128+c  <- tile (c, r)
+        C[(long long)(J * kTile + r) * ld + I * kTile + c] = S[c * kEpiPitch + r];
+      }
+    } else {
+      for (int idx = tid; idx < kTile * kTile; idx += 256) {
+        const int r = idx >> 7, c = idx & 127;
+        const double v = (r <= c) ? S[r * kEpiPitch + c] : S[c * kEpiPitch + r];
+        C[(long long)(I * kTile + r) * ld + I * kTile + c] = v;
+        if (r < c) {
+          part += 2.0 * v * v;
+        } else if (r == c) {
+          const double e = (I * kTile + r < p.d) ? v - 1.0 : v;
+          part += e * e;
+        }
+      }
+    }
+  } else {
+    // X_{j+1} = 1.5 X_j - 0.5 Z,  Z = X_j Y_j ; trace partial on diagonal tiles.
+    const double* X = p.Xold + base;
+    if (!diag) {
+      for (int idx = tid; idx < kTile * kTile; idx += 256) {
+        const int r = idx >> 7, c = idx & 127;
+        const long long gidx = (long long)(I * kTile + r) * ld + J * kTile + c;
+        const double v = fma(-0.5, S[r * kEpiPitch + c], 1.5 * X[gidx]);
+        C[gidx] = v;
+        S[r * kEpiPitch + c] = v;
+      }
+      named_bar_sync(1, 32 * kConsumerWarps);
+      for (int idx = tid; idx < kTile * kTile; idx += 256) {
+        const int r = idx >> 7, c = idx & 127;
+        C[(long long)(J * kTile + r) * ld + I * kTile + c] = S[c * kEpiPitch + r];
+      }
+    } else {
+      for (int idx = tid; idx < kTile * kTile; idx += 256) {
+        const int r = idx >> 7, c = idx & 127;
+        if (r <= c) {
+          const long long gidx = (long long)(I * kTile + r) * ld + I * kTile + c;
+          const double v = fma(-0.5, S[r * kEpiPitch + c], 1.5 * X[gidx]);
+          S[r * kEpiPitch + c] = v;
+          if (r == c && I * kTile + r < p.d) part += v;
+        }
+      }
+      named_bar_sync(1, 32 * kConsumerWarps);
+      for (int idx = tid; idx < kTile * kTile; idx += 256) {
+        const int r = idx >> 7, c = idx & 127;
+        C[(long long)(I * kTile + r) * ld + I * kTile + c] = (r <= c) ? S[r * kEpiPitch + c] : S[c * kEpiPitch + r];
+      }
+    }
+  }
+
+  // fixed-order reduction of `part` over the 256 consumer threads
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if (lane == 0) red[cw] = part;
+  named_bar_sync(1, 32 * kConsumerWarps);
+  if (tid == 0) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kConsumerWarps; ++w) s += red[w];
+    if (MODE == 0) {
+      p.partial[(long long)job * p.n_tiles + blockIdx.x] = s;
+    } else if (diag) {
+      p.partial[(long long)job * (p.ld / kTile) + I] = s;
+    }
+  }
+}
+
+// --------------------------------------------------------------------------------------
+// Stop decision for step j (one CTA per problem); fixed-order reductions.
+// --------------------------------------------------------------------------------------
+__device__ __forceinline__ double block_sum_fixed(const double* v, int n, double* red) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += v[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  double tot = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+  return tot;
+}
+
+__global__ void __launch_bounds__(256) ns_decide_kernel(DevState* __restrict__ state, const JobParams* __restrict__ jobs,
+                                                        const double* __restrict__ res_partial, int n_tiles,
+                                                        const double* __restrict__ tr_partial, int n_diag,
+                                                        LoopParams lp, int* n_active) {
+  __shared__ double red[8];
+  const int job = blockIdx.x;
+  DevState* st = state + job;
+  if (st->done) return;
+  const double r2 = block_sum_fixed(res_partial + (long long)job * n_tiles, n_tiles, red);
+  const double tr = block_sum_fixed(tr_partial + (long long)job * n_diag, n_diag, red);
+  if (threadIdx.x != 0) return;
+  const double r = sqrt(r2);
+  int flags = st->flags;
+  int done = 0;
+  const double sqd = sqrt((double)lp.d);
+  if (!isfinite(r)) {
+    flags |= 16;  // NS_F_NONFINITE
+    done = 1;
+  } else {
+    if (st->j > 0 && r > st->r_prev * (1.0 + 1e-12) + 1e-10 * sqd) flags |= 8;  // NS_F_SCALING_SUSPECT
+    const double rho = lp.tol_mode ? r / sqd : r;
+    if (rho < lp.tol) {
+      flags |= 1;  // NS_F_CONVERGED
+      done = 1;
+    } else if (st->j >= lp.max_steps) {
+      flags |= 2;  // NS_F_MAX_STEPS
+      done = 1;
+    }
+  }
+  st->residual = r;
+  st->trace = tr;
+  if (done) {
+    const double half = ((double)lp.d - tr) * 0.5;
+    long long cert = -1;                                   // no certificate for a non-finite iterate
+    if (!(flags & 16) && isfinite(half)) {
+      cert = (long long)floor(fabs(half) + 0.5);
+      if (half < 0) cert = -cert;
+      if (fabs(half - (double)cert) > 0.25) flags |= 32;  // NS_F_SHIFT_ON_SPECTRUM
+    }
+    if (cert != (long long)jobs[job].k) flags |= 4;       // NS_F_INDEX_MISMATCH
+    st->cert = cert;
+    st->flags = flags;
+    st->done = 1;
+    if (n_active) atomicSub(n_active, 1);
+  } else {
+    st->flags = flags;
+    st->r_prev = r;
+    st->j += 1;
+  }
+}
+
+__global__ void ns_zero_state_kernel(DevState* state, int batch, int* n_active) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < batch) {
+    DevState z{};
+    state[i] = z;
+  }
+  if (i == 0 && n_active) *n_active = batch;
+}
+
+// R = X_{steps}: buffer chosen on device from state.j (ping-pong parity).
+__global__ void __launch_bounds__(256) ns_copy_out_kernel(const double* __restrict__ Xa, const double* __restrict__ Xb,
+                                                          int d, int d_pad, const DevState* __restrict__ state,
+                                                          double* __restrict__ R, long long ldr, long long r_stride) {
+  const int job = blockIdx.z;
+  const double* X = ((state[job].j & 1) ? Xb : Xa) + (long long)job * d_pad * d_pad;
+  const int i = blockIdx.y;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < d; c += gridDim.x * blockDim.x)
+    R[(long long)job * r_stride + (long long)i * ldr + c] = X[(long long)i * d_pad + c];
+}
+
+// --------------------------------------------------------------------------------------
+// launchers
+// --------------------------------------------------------------------------------------
+cudaError_t launch_init(const double* H, long long ldh, long long h_stride, double* X, const JobParams* jobs,
+                        int d, int d_pad, int batch, cudaStream_t st) {
+  dim3 grid(d_pad / 32, d_pad / 32, batch);
+  ns_init_kernel<<<grid, 256, 0, st>>>(H, ldh, h_stride, X, jobs, d, d_pad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trace_partials(const double* X, int d, int d_pad, int batch, double* tr_partial,
+                                  cudaStream_t st) {
+  dim3 grid(d_pad / kTile, batch);
+  ns_trace_partials_kernel<<<grid, kTile, 0, st>>>(X, d, d_pad, tr_partial);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_product(const CUtensorMap& tmP, const CUtensorMap& tmQ, const ProdParams& p, int batch,
+                           cudaStream_t st) {
+  static bool attr_done[2] = {false, false};
+  dim3 grid(p.n_tiles, batch);
+  if (p.mode == 0) {
+    if (!attr_done[0]) {
+      cudaFuncSetAttribute(ns_product_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+      attr_done[0] = true;
+    }
+    ns_product_kernel<0><<<grid, kThreads, kSmemBytes, st>>>(tmP, tmQ, p);
+  } else {
+    if (!attr_done[1]) {
+      cudaFuncSetAttribute(ns_product_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+      attr_done[1] = true;
+    }
+    ns_product_kernel<1><<<grid, kThreads, kSmemBytes, st>>>(tmP, tmQ, p);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_decide(DevState* state, const JobParams* jobs, const double* res_partial, int n_tiles,
+                          const double* tr_partial, int n_diag, LoopParams lp, int batch, int* n_active,
+                          cudaStream_t st) {
+  ns_decide_kernel<<<batch, 256, 0, st>>>(state, jobs, res_partial, n_tiles, tr_partial, n_diag, lp, n_active);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy_out(const double* Xa, const double* Xb, int d, int d_pad, const DevState* state,
+                            double* R, long long ldr, long long r_stride, int batch, cudaStream_t st) {
+  const int bx = (d + 255) / 256 < 8 ? (d + 255) / 256 : 8;
+  dim3 grid(bx, d, batch);
+  ns_copy_out_kernel<<<grid, 256, 0, st>>>(Xa, Xb, d, d_pad, state, R, ldr, r_stride);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_zero_state(DevState* state, int batch, int* n_active, cudaStream_t st) {
+  ns_zero_state_kernel<<<(batch + 255) / 256, 256, 0, st>>>(state, batch, n_active);
+  return cudaGetLastError();
+}
+
+}  // namespace nsr

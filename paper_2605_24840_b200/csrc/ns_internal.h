@@ -1,0 +1,76 @@
+// Internal declarations shared by the FP64 kernels (ns_fp64.cu) and the C-ABI host
+// code (ns_api.cu).  Not part of the public ABI.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace nsr {
+
+constexpr int kTile = 128;      // output tile edge (rows of P, rows of Q)
+constexpr int kBK = 16;         // k-slab per pipeline stage: 16 doubles = one 128-B swizzle row
+constexpr int kStages = 6;      // TMA ring depth (6 x 32 KB)
+constexpr int kConsumerWarps = 8;
+constexpr int kThreads = 32 * (1 + kConsumerWarps);   // warp 0 = TMA producer
+constexpr int kStageBytes = 2 * kTile * kBK * 8;      // A + B per stage = 32 KB
+constexpr int kEpiPitch = kTile + 1;                  // staging row pitch (doubles), odd => conflict-free columns
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+
+// Per-problem device state (one per job).  Written only by ns_decide_kernel.
+struct DevState {
+  int32_t j;          // index of the current iterate X_j
+  int32_t flags;      // NS_F_* bits
+  int32_t done;       // 1 once a stop condition fired
+  int32_t pad0;
+  double residual;    // r_j = ||X_j^2 - I||_F of the returned X
+  double r_prev;      // r_{j-1}
+  double trace;       // tr X_j
+  int64_t cert;       // round((d - tr)/2)
+};
+
+// Per-problem scalar inputs (device copy).
+struct JobParams {
+  double s;
+  double alpha;
+  int32_t k;
+  int32_t pad;
+};
+
+struct LoopParams {
+  int d;               // true dimension
+  int d_pad;           // padded dimension (multiple of kTile); workspace leading dim
+  int max_steps;
+  int tol_mode;        // 0 abs, 1 per sqrt(d)
+  double tol;
+};
+
+// Product kernel parameters: C_IJ = sum_k P[I,k] Q[J,k] on upper tiles (I <= J).
+struct ProdParams {
+  const int2* tiles;       // (I, J) tile list, n_tiles entries
+  int n_tiles;
+  int nk;                  // d_pad / kBK
+  int d;                   // true dimension (identity mask in the residual)
+  int ld;                  // d_pad
+  long long job_stride;    // elements between consecutive jobs' matrices
+  double* C;               // mode 0: Y ; mode 1: X_{j+1}
+  const double* Xold;      // mode 1: X_j (read in the epilogue)
+  double* partial;         // mode 0: residual partial per (job, tile); mode 1: trace partial per (job, I) on diag tiles
+  const DevState* state;   // per-job state; CTA exits if state[job].done (nullptr = never)
+  int mode;                // 0 = square/plain product + residual, 1 = NS update + trace
+};
+
+// Host-side launchers (ns_fp64.cu).
+cudaError_t launch_init(const double* H, long long ldh, long long h_stride, double* X, const JobParams* jobs,
+                        int d, int d_pad, int batch, cudaStream_t st);
+cudaError_t launch_trace_partials(const double* X, int d, int d_pad, int batch, double* tr_partial,
+                                  cudaStream_t st);
+cudaError_t launch_product(const CUtensorMap& tmP, const CUtensorMap& tmQ, const ProdParams& p, int batch,
+                           cudaStream_t st);
+cudaError_t launch_decide(DevState* state, const JobParams* jobs, const double* res_partial, int n_tiles,
+                          const double* tr_partial, int n_diag, LoopParams lp, int batch, int* n_active,
+                          cudaStream_t st);
+cudaError_t launch_copy_out(const double* Xa, const double* Xb, int d, int d_pad, const DevState* state,
+                            double* R, long long ldr, long long r_stride, int batch, cudaStream_t st);
+cudaError_t launch_zero_state(DevState* state, int batch, int* n_active, cudaStream_t st);
+
+}  // namespace nsr

@@ -1,0 +1,214 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle on the same seeded inputs.
+
+Tolerances (north_star): ||R_gpu - R_oracle||_F / sqrt(d) <= 1e-10 for FP64, identical step
+count and index certificate (outside the +-1% tie band of reading C9), identical flags.
+Kernel-level tests compare the symmetric product against a plain float64 matmul.
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from oracle import checks, closed_form, ns as ons, scalar  # noqa: E402
+import workloads  # noqa: E402
+
+TOL_R = 1e-10
+
+
+@pytest.fixture(scope="module")
+def nsr():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2605_24840_b200 as m
+    m.load_library()
+    return m
+
+
+def _dev():
+    return torch.device("cuda:0")
+
+
+def _tie_band(hist, tol, steps):
+    """C9: residual at the decision step or the step before within +-1% of tol."""
+    cand = [hist[steps]] + ([hist[steps - 1]] if steps > 0 else [])
+    return any(abs(r - tol) <= 0.01 * tol for r in cand)
+
+
+def _compare(nsr, H, s, alpha, k, max_steps, tol, tm, d=None):
+    d = H.shape[0]
+    o = ons.ns_reflector(H, s, alpha, k, max_steps, tol, tm, trace_residuals=True)
+    Hg = torch.from_numpy(H).to(_dev())
+    R, res = nsr.ns_reflector(Hg, s, alpha, k, max_steps, tol, tm)
+    Rn = R.cpu().numpy()
+    assert np.array_equal(Rn, Rn.T), "R must be bitwise symmetric"
+    tie = _tie_band(o["hist_residual"], tol if tm == 0 else tol * math.sqrt(d), o["steps"]) if tol > 0 else False
+    if tie:
+        assert abs(res["steps"] - o["steps"]) <= 1
+    else:
+        assert res["steps"] == o["steps"], (res, o["steps"])
+        err = checks.frob_per_sqrt_d(Rn, o["R"])
+        if o["flags"] & (ons.SCALING_SUSPECT | ons.NONFINITE):
+            # divergent iterate (alpha < ||H - sI||_2): compare relative to its size
+            err /= max(1.0, np.linalg.norm(o["R"]) / math.sqrt(d))
+        assert err <= TOL_R, err
+        assert res["flags"] == o["flags"], (res["flags"], o["flags"])
+    assert res["cert"] == o["cert"]
+    assert abs(res["trace"] - o["trace"]) <= 1e-9 * max(1.0, abs(o["trace"]))
+    if o["flags"] & ons.CONVERGED:
+        assert res["residual"] < (tol if tm == 0 else tol * math.sqrt(d))
+    return Rn, res, o
+
+
+# ------------------------------------------------------------------ kernel level
+@pytest.mark.parametrize("d", [64, 128, 200, 384, 515])
+def test_symm_product_square(nsr, d):
+    rng = np.random.default_rng(d)
+    A = rng.standard_normal((d, d))
+    A = 0.5 * (A + A.T)
+    Ag = torch.from_numpy(A).to(_dev())
+    C = nsr.ns_symm_product(Ag, Ag, mode=0).cpu().numpy()
+    ref = A @ A
+    assert np.array_equal(C, C.T)
+    assert np.max(np.abs(C - ref)) <= 1e-13 * np.max(np.abs(ref)) * math.sqrt(d)
+
+
+@pytest.mark.parametrize("d", [128, 260])
+def test_symm_product_update(nsr, d):
+    rng = np.random.default_rng(1000 + d)
+    A = rng.standard_normal((d, d))
+    A = 0.5 * (A + A.T) / math.sqrt(d)
+    B = A @ A
+    B = 0.5 * (B + B.T)
+    Ag, Bg = torch.from_numpy(A).to(_dev()), torch.from_numpy(B).to(_dev())
+    C = nsr.ns_symm_product(Ag, Bg, mode=1).cpu().numpy()
+    ref = 1.5 * A - 0.5 * (A @ B)
+    assert np.array_equal(C, C.T)
+    assert np.max(np.abs(C - ref)) <= 1e-14 * math.sqrt(d)
+
+
+# ------------------------------------------------------------------ configs
+@pytest.mark.parametrize("seed", [0, 1, 2, 3, 4])
+def test_cfg0_parity(nsr, seed):
+    p = workloads.cfg0_controlled(seed)
+    R, res, o = _compare(nsr, p.H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    assert res["flags"] == ons.CONVERGED and res["cert"] == 3
+    assert checks.frob_per_sqrt_d(R, closed_form.reflector_explicit_q(p.Q, p.lam, p.s)) <= 1e-13
+
+
+@pytest.mark.parametrize("d,k", [(1, 0), (2, 1), (37, 5), (129, 9), (300, 17)])
+def test_ragged_sizes(nsr, d, k):
+    p = workloads.cfg0_controlled(seed=d, d=d, k=k) if d > 1 else None
+    if p is None:
+        H = np.array([[-0.5]])
+        _compare(nsr, H, 0.25, 1.0, 1, 100, 1e-12, 0)
+        return
+    _compare(nsr, p.H, p.s, p.alpha, p.k, 100, 1e-12, 0)
+
+
+def test_cfg3_recipe_reduced(nsr):
+    p = workloads.cfg3_dense(d=1024, k=64)
+    R, res, o = _compare(nsr, p.H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    cols = np.arange(0, 1024, 31)
+    Rc = closed_form.householder_reflector_columns(p.Vh, p.lam, 0.0, cols)
+    assert np.max(np.abs(R[:, cols] - Rc)) <= 1e-12
+
+
+def test_cfg3_fixed_steps_reduced(nsr):
+    p = workloads.cfg3_dense(d=512, k=32, mode="fixed30")
+    R, res, o = _compare(nsr, p.H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    assert res["steps"] == 30 and res["flags"] == ons.MAX_STEPS
+
+
+def test_cfg2_allen_cahn_small_grid(nsr):
+    """configs[2] recipe on a 32x32 grid (d=1024); s from the oracle's Jacobi midpoint."""
+    from oracle import jacobi
+    prob = workloads.cfg2_allen_cahn(seed=0, n=32)
+    w, V, _ = jacobi.jacobi_eigh(prob.H)
+    s = jacobi.midpoint_shift(w, 5)
+    alpha = workloads.configs.gershgorin_alpha(prob.H, s)
+    R, res, o = _compare(nsr, prob.H, s, alpha, 5, 100, 1e-12, 0)
+    R_eig = jacobi.exact_reflector_from_eig(V, 5)
+    assert checks.frob_per_sqrt_d(R, R_eig) <= 1e-10
+
+
+def test_cfg1_batched_subset(nsr):
+    probs = workloads.cfg1_batched(seed=0, first=0, count=8)
+    H = torch.from_numpy(np.stack([p.H for p in probs])).to(_dev())
+    R, outs = nsr.ns_reflector_batched(H, [p.s for p in probs], [p.alpha for p in probs], [p.k for p in probs],
+                                       100, 1e-12)
+    R = R.cpu().numpy()
+    for i, p in enumerate(probs):
+        o = ons.ns_reflector(p.H, p.s, p.alpha, p.k, 100, 1e-12, 0, trace_residuals=True)
+        if not _tie_band(o["hist_residual"], 1e-12, o["steps"]):
+            assert outs[i]["steps"] == o["steps"], (i, outs[i], o["steps"])
+            assert checks.frob_per_sqrt_d(R[i], o["R"]) <= TOL_R
+            assert outs[i]["flags"] == o["flags"]
+        assert outs[i]["cert"] == p.k
+        # direction error (configs[1]) vs the closed form, prop:direrr P:354-361
+        v = p.extra["probe"]
+        R_cf = closed_form.reflector_explicit_q(p.Q, p.lam, p.s)
+        assert np.linalg.norm((R[i] - R_cf) @ v) <= 1e-12
+
+
+# ------------------------------------------------------------------ edge cases and flags
+def test_edge_cases(nsr):
+    p = workloads.cfg0_controlled(seed=0)
+    _compare(nsr, p.H, p.s, p.alpha, p.k, 0, 1e-12, 0)          # max_steps = 0 -> X_0
+    _compare(nsr, p.H, p.s, p.alpha, p.k, 5, 0.0, 0)            # fixed steps
+    _compare(nsr, p.H, p.s, p.alpha, p.k + 1, 100, 1e-12, 0)    # INDEX_MISMATCH
+    _compare(nsr, p.H, -10.0, 12.0, 0, 100, 1e-12, 0)           # s below the spectrum: k = 0, R = I
+    _compare(nsr, p.H, 10.0, 12.0, 64, 100, 1e-12, 0)           # s above: k = d, R = -I
+    _compare(nsr, p.H, p.s, p.alpha / 4.0, p.k, 100, 1e-12, 0)  # alpha too small -> SCALING_SUSPECT / NONFINITE
+    Hn = p.H.copy()
+    Hn[3, 5] = Hn[5, 3] = np.nan
+    Hg = torch.from_numpy(Hn).to(_dev())
+    R, res = nsr.ns_reflector(Hg, p.s, p.alpha, p.k, 100, 1e-12)
+    assert res["flags"] & ons.NONFINITE and res["steps"] == 0
+
+
+def test_only_upper_triangle_read(nsr):
+    p = workloads.cfg0_controlled(seed=1)
+    Hl = p.H.copy()
+    Hl[np.tril_indices(p.d, -1)] = 1e30      # garbage below the diagonal must be ignored
+    Ha = torch.from_numpy(p.H).to(_dev())
+    Hb = torch.from_numpy(Hl).to(_dev())
+    Ra, ra = nsr.ns_reflector(Ha, p.s, p.alpha, p.k, 100, 1e-12)
+    Rb, rb = nsr.ns_reflector(Hb, p.s, p.alpha, p.k, 100, 1e-12)
+    assert torch.equal(Ra, Rb) and ra == rb
+
+
+def test_host_entry_matches_device(nsr):
+    p = workloads.cfg0_controlled(seed=2, d=200, k=7)
+    Rh, rh = nsr.ns_reflector_host(p.H, p.s, p.alpha, p.k, 100, 1e-12)
+    Rd, rd = nsr.ns_reflector(torch.from_numpy(p.H).to(_dev()), p.s, p.alpha, p.k, 100, 1e-12)
+    assert np.array_equal(Rh.numpy(), Rd.cpu().numpy()) and rh == rd
+
+
+def test_deterministic(nsr):
+    p = workloads.cfg3_dense(d=768, k=48)
+    Hg = torch.from_numpy(p.H).to(_dev())
+    R1, r1 = nsr.ns_reflector(Hg, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    R2, r2 = nsr.ns_reflector(Hg, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    assert torch.equal(R1, R2) and r1 == r2
+
+
+# ------------------------------------------------------------------ full size (bench launch configuration)
+def test_cfg3_full_size_sampled(nsr):
+    """configs[3] at d=16384 exactly as bench.py runs it: steps == scalar-recurrence prediction,
+    cert == 1024, sampled columns == closed form R = Q sgn(Lambda) Q^T (the oracle's column routine)."""
+    p = workloads.cfg3_dense(form=False)
+    H = workloads.configs.householder_form_torch(p.Vh, p.lam, _dev())
+    R, res = nsr.ns_reflector(H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    steps_pred, res_pred, _ = scalar.predict_run((p.lam - p.s) / p.alpha, 100, 1e-10, True)
+    assert res["steps"] == steps_pred and res["cert"] == 1024 and res["flags"] == ons.CONVERGED
+    cols = np.array([0, 1, 4095, 8191, 12000, 16383])
+    Rc = closed_form.householder_reflector_columns(p.Vh, p.lam, 0.0, cols)
+    Rg = R[:, torch.as_tensor(cols, device=_dev())].cpu().numpy()
+    assert np.sqrt(np.mean(np.sum((Rg - Rc) ** 2, axis=0))) <= 1e-10   # estimates ||dR||_F/sqrt(d)
+    assert np.max(np.abs(Rg - Rc)) <= 1e-12
+    blk = R[1000:1300, 9000:9300]
+    assert torch.equal(blk, R[9000:9300, 1000:1300].T)

@@ -1,0 +1,85 @@
+"""CPU-side checks of the C-ABI boundary: the library builds, loads and exports every symbol
+include/nsreflector.h declares; host-side argument validation (no GPU needed: validation
+happens before any CUDA call)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2605_24840_b200 import build
+    build.build()
+    import paper_2605_24840_b200 as nsr
+    return nsr.load_library()
+
+
+def _declared_symbols():
+    with open(os.path.join(ROOT, "include", "nsreflector.h")) as f:
+        src = f.read()
+    return sorted(set(re.findall(r"\b(ns_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_symbols_exported(lib):
+    import paper_2605_24840_b200 as nsr
+    declared = _declared_symbols()
+    assert set(declared) == set(nsr.EXPORTED_SYMBOLS)
+    for name in declared:
+        assert hasattr(lib, name), name
+
+
+def test_build_info_names_target(lib):
+    assert b"sm_100a" in lib.ns_build_info()
+
+
+def test_workspace_sizes(lib):
+    # 3 padded FP64 matrices dominate; d=16384 -> 3 * 2 GiB plus small tails
+    w = lib.ns_workspace_bytes(16384, 0)
+    assert 3 * 16384 * 16384 * 8 <= w < 3 * 16384 * 16384 * 8 + (1 << 20)
+    assert lib.ns_workspace_bytes(100, 0) >= 3 * 128 * 128 * 8      # padded to 128
+    assert lib.ns_workspace_bytes_batched(256, 10, 0) >= 10 * 3 * 256 * 256 * 8
+    assert lib.ns_workspace_bytes(0, 0) == 0
+
+
+def test_argument_validation(lib):
+    import paper_2605_24840_b200 as nsr
+    res = nsr.NsResult()
+    buf = ctypes.create_string_buffer(1 << 16)
+    ws = ctypes.c_void_p((ctypes.addressof(buf) + 255) & ~255)
+    fake = ctypes.c_void_p(0x1000)
+
+    def call(d=64, ldh=64, s=0.0, alpha=1.0, k=3, max_steps=10, tol=1e-12, tm=0, prec=0, R=ctypes.c_void_p(0x2000),
+             ldr=64, ws_bytes=1 << 30):
+        return lib.ns_reflector(fake, d, ldh, s, alpha, k, max_steps, tol, tm, prec, R, ldr, ws, ws_bytes, None,
+                                ctypes.byref(res))
+
+    assert call(d=0) == 1
+    assert call(ldh=10) == 1
+    assert call(alpha=0.0) == 1
+    assert call(alpha=float("nan")) == 1
+    assert call(s=float("inf")) == 1
+    assert call(k=-1) == 1 and call(k=65) == 1
+    assert call(max_steps=-1) == 1
+    assert call(tol=-1.0) == 1
+    assert call(tm=7) == 1
+    assert call(prec=1) == 5                     # mixed modes: NS_ERR_UNSUPPORTED in this build
+    assert call(R=fake) == 1                     # aliasing
+    assert call(ws_bytes=10) == 4                # NS_ERR_WORKSPACE
+    assert b"workspace" in lib.ns_last_error()
+    assert lib.ns_status_string(4) == b"NS_ERR_WORKSPACE"
+
+
+def test_product_path_has_no_oracle_or_fallback():
+    """The product package must not import the oracle nor contain a CPU fallback."""
+    pkg = os.path.join(ROOT, "paper_2605_24840_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                with open(os.path.join(dirpath, fn)) as f:
+                    src = f.read()
+                assert "oracle" not in src.replace("oracle/", ""), fn
+                assert "import numpy.linalg" not in src and "np.linalg" not in src, fn
