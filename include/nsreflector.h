@@ -88,6 +88,8 @@ typedef struct {
   double residual;
   double trace;
   int64_t index_cert;
+  int32_t kernel_launches;   /* device kernels this call launched (incl. early-exit look-ahead steps) */
+  int32_t pad;
 } ns_result_t;
 
 /* Bytes of device workspace ns_reflector needs for dimension d (batch = 1). */
@@ -150,6 +152,23 @@ ns_status_t ns_reflector_batched(const double* H, int64_t d, int64_t batch, int6
  */
 ns_status_t ns_symm_product(const double* A, const double* B, double* C, int64_t d, int64_t ld,
                             int32_t mode, void* ws, size_t ws_bytes, void* stream);
+
+/*
+ * Optional per-thread kernel timing (used by bench.py for the roofline): when enabled,
+ * every contraction launch is bracketed by CUDA events on the caller's stream and,
+ * at the end of each call, the durations of the launches that did work are added to
+ * the thread's accumulators.  Events cost ~microseconds; off by default.
+ */
+typedef struct {
+  int64_t n_square;     /* Y_j = X_j^2 launches that did work (steps + 1 per reflector) */
+  int64_t n_update;     /* X_{j+1} = 1.5 X_j - 0.5 X_j Y_j launches that did work */
+  double ms_square;     /* summed device time of those launches */
+  double ms_update;
+  int64_t n_calls;
+} ns_profile_t;
+void ns_profile_enable(int on);
+void ns_profile_reset(void);
+void ns_profile_get(ns_profile_t* out);
 
 /* Library identification: build string with the compile target (e.g. "sm_100a"). */
 const char* ns_build_info(void);

@@ -22,17 +22,23 @@ NS_F_SCALING_SUSPECT, NS_F_NONFINITE, NS_F_SHIFT_ON_SPECTRUM = 8, 16, 32
 EXPORTED_SYMBOLS = (
     "ns_workspace_bytes", "ns_workspace_bytes_batched", "ns_workspace_bytes_host", "ns_reflector",
     "ns_reflector_host", "ns_reflector_batched", "ns_symm_product", "ns_build_info", "ns_status_string",
-    "ns_last_error",
+    "ns_last_error", "ns_profile_enable", "ns_profile_reset", "ns_profile_get",
 )
 
 
 class NsResult(ctypes.Structure):
     _fields_ = [("steps", ctypes.c_int32), ("flags", ctypes.c_int32), ("residual", ctypes.c_double),
-                ("trace", ctypes.c_double), ("index_cert", ctypes.c_int64)]
+                ("trace", ctypes.c_double), ("index_cert", ctypes.c_int64), ("kernel_launches", ctypes.c_int32),
+                ("pad", ctypes.c_int32)]
 
     def as_dict(self):
         return dict(steps=self.steps, flags=self.flags, residual=self.residual, trace=self.trace,
-                    cert=self.index_cert)
+                    cert=self.index_cert, launches=self.kernel_launches)
+
+
+class NsProfile(ctypes.Structure):
+    _fields_ = [("n_square", ctypes.c_int64), ("n_update", ctypes.c_int64), ("ms_square", ctypes.c_double),
+                ("ms_update", ctypes.c_double), ("n_calls", ctypes.c_int64)]
 
 
 class NsError(RuntimeError):
@@ -71,6 +77,11 @@ def load_library(path=LIB_PATH):
     lib.ns_status_string.restype = ctypes.c_char_p
     lib.ns_status_string.argtypes = [ctypes.c_int]
     lib.ns_last_error.restype = ctypes.c_char_p
+    lib.ns_profile_enable.argtypes = [ctypes.c_int]
+    lib.ns_profile_enable.restype = None
+    lib.ns_profile_reset.restype = None
+    lib.ns_profile_get.argtypes = [ctypes.POINTER(NsProfile)]
+    lib.ns_profile_get.restype = None
     _lib = lib
     return lib
 
@@ -203,6 +214,21 @@ def ns_symm_product(A, B, mode=0, C=None, ws=None, stream=None):
                              ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream))
     _check(st)
     return C
+
+
+def ns_profile_enable(on=True):
+    load_library().ns_profile_enable(1 if on else 0)
+
+
+def ns_profile_reset():
+    load_library().ns_profile_reset()
+
+
+def ns_profile_get():
+    p = NsProfile()
+    load_library().ns_profile_get(ctypes.byref(p))
+    return dict(n_square=p.n_square, n_update=p.n_update, ms_square=p.ms_square, ms_update=p.ms_update,
+                n_calls=p.n_calls)
 
 
 def build_info():

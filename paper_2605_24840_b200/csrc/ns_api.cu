@@ -11,6 +11,7 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <algorithm>
 
 #include "../../include/nsreflector.h"
 #include "ns_internal.h"
@@ -117,6 +118,25 @@ ns_status_t encode_map(CUtensorMap* m, const double* base, int d_pad, long long 
   return NS_OK;
 }
 
+struct Profiler {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  ns_profile_t acc{};
+  cudaEvent_t get(size_t i) {
+    while (pool.size() <= i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[i];
+  }
+};
+
+Profiler& prof() {
+  static thread_local Profiler p;
+  return p;
+}
+
 struct HostRing {
   int* slots = nullptr;
   cudaEvent_t ev[16];
@@ -148,7 +168,8 @@ ns_status_t check_common(int64_t d, int32_t max_steps, double tol, ns_tolmode_t 
 // at H + b*h_stride (ld ldh).  R likewise.  Returns per-job states in `states`.
 ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ldh, long long h_stride,
                      const std::vector<JobParams>& jobs, int32_t max_steps, double tol, ns_tolmode_t tm, double* R,
-                     long long ldr, long long r_stride, cudaStream_t st, std::vector<DevState>& states) {
+                     long long ldr, long long r_stride, cudaStream_t st, std::vector<DevState>& states,
+                     int* launches) {
   const int batch = (int)L.batch;
   double* Xa = reinterpret_cast<double*>(ws + L.off_xa);
   double* Xb = reinterpret_cast<double*>(ws + L.off_xb);
@@ -176,6 +197,9 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
   NS_CUDA(launch_zero_state(state, batch, n_active, st));
   NS_CUDA(launch_init(H, ldh, h_stride, Xa, djobs, L.d, L.d_pad, batch, st));
   NS_CUDA(launch_trace_partials(Xa, L.d, L.d_pad, batch, trp, st));
+  int nl = 3;
+  Profiler& pf = prof();
+  // event slots: 4 per step (square begin/end, update begin/end)
 
   LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol};
   const long long job_stride = (long long)L.d_pad * L.d_pad;
@@ -195,24 +219,51 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
     const CUtensorMap& tmC = odd ? tmB : tmA;
 
     ProdParams sq{tiles, L.n_tiles, L.d_pad / kBK, L.d, L.d_pad, job_stride, Y, nullptr, res, state, 0};
+    if (pf.on) NS_CUDA(cudaEventRecord(pf.get(4 * j + 0), st));
     NS_CUDA(launch_product(tmC, tmC, sq, batch, st));
+    if (pf.on) NS_CUDA(cudaEventRecord(pf.get(4 * j + 1), st));
     NS_CUDA(launch_decide(state, djobs, res, L.n_tiles, trp, L.n, lp, batch, n_active, st));
+    nl += 2;
     if (j < max_steps) {
       ProdParams up{tiles, L.n_tiles, L.d_pad / kBK, L.d, L.d_pad, job_stride, Xn, Xc, trp, state, 1};
+      if (pf.on) NS_CUDA(cudaEventRecord(pf.get(4 * j + 2), st));
       NS_CUDA(launch_product(tmC, tmY, up, batch, st));
+      if (pf.on) NS_CUDA(cudaEventRecord(pf.get(4 * j + 3), st));
+      nl += 1;
     }
     const int slot = j % 16;
     NS_CUDA(cudaMemcpyAsync(&rg.slots[slot], n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
     NS_CUDA(cudaEventRecord(rg.ev[slot], st));
   }
   NS_CUDA(launch_copy_out(Xa, Xb, L.d, L.d_pad, state, R, ldr, r_stride, batch, st));
+  nl += 1;
   states.resize(batch);
   NS_CUDA(cudaMemcpyAsync(states.data(), state, sizeof(DevState) * batch, cudaMemcpyDeviceToHost, st));
   NS_CUDA(cudaStreamSynchronize(st));
+  if (launches) *launches = nl;
+  if (pf.on) {
+    // launches that did work: squares j = 0..max_j, updates j = 0..max_j-1 (max over jobs)
+    int max_j = 0;
+    for (const DevState& d : states) max_j = std::max(max_j, d.j);
+    for (int j = 0; j <= max_j; ++j) {
+      float ms = 0.f;
+      NS_CUDA(cudaEventElapsedTime(&ms, pf.get(4 * j + 0), pf.get(4 * j + 1)));
+      pf.acc.ms_square += ms;
+      pf.acc.n_square += 1;
+      if (j < max_j) {
+        NS_CUDA(cudaEventElapsedTime(&ms, pf.get(4 * j + 2), pf.get(4 * j + 3)));
+        pf.acc.ms_update += ms;
+        pf.acc.n_update += 1;
+      }
+    }
+    pf.acc.n_calls += 1;
+  }
   return NS_OK;
 }
 
-void fill_result(const DevState& s, ns_result_t* out) {
+void fill_result(const DevState& s, int launches, ns_result_t* out) {
+  out->kernel_launches = launches;
+  out->pad = 0;
   out->steps = s.j;
   out->flags = s.flags;
   out->residual = s.residual;
@@ -256,10 +307,11 @@ ns_status_t ns_reflector(const double* H, int64_t d, int64_t ldh, double s, doub
     return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
   std::vector<JobParams> jobs{JobParams{s, alpha, k, 0}};
   std::vector<DevState> states;
+  int nl = 0;
   st = run_loop(L, static_cast<uint8_t*>(ws), H, ldh, 0, jobs, max_steps, tol, tm, R, ldr, 0,
-                static_cast<cudaStream_t>(stream), states);
+                static_cast<cudaStream_t>(stream), states, &nl);
   if (st != NS_OK) return st;
-  fill_result(states[0], out);
+  fill_result(states[0], nl, out);
   return NS_OK;
 }
 
@@ -286,12 +338,13 @@ ns_status_t ns_reflector_host(const double* H_host, int64_t d, int64_t ldh, doub
                             cudaMemcpyHostToDevice, cs));
   std::vector<JobParams> jobs{JobParams{s, alpha, k, 0}};
   std::vector<DevState> states;
-  st = run_loop(L, w, stage, d, 0, jobs, max_steps, tol, tm, stage, d, 0, cs, states);
+  int nl = 0;
+  st = run_loop(L, w, stage, d, 0, jobs, max_steps, tol, tm, stage, d, 0, cs, states, &nl);
   if (st != NS_OK) return st;
   NS_CUDA(cudaMemcpy2DAsync(R_host, (size_t)ldr * 8, stage, (size_t)d * 8, (size_t)d * 8, (size_t)d,
                             cudaMemcpyDeviceToHost, cs));
   NS_CUDA(cudaStreamSynchronize(cs));
-  fill_result(states[0], out);
+  fill_result(states[0], nl, out);
   return NS_OK;
 }
 
@@ -318,10 +371,11 @@ ns_status_t ns_reflector_batched(const double* H, int64_t d, int64_t batch, int6
   if (ws_bytes < L.total)
     return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
   std::vector<DevState> states;
+  int nl = 0;
   st = run_loop(L, static_cast<uint8_t*>(ws), H, d, stride_h, jobs, max_steps, tol, tm, R, d, stride_r,
-                static_cast<cudaStream_t>(stream), states);
+                static_cast<cudaStream_t>(stream), states, &nl);
   if (st != NS_OK) return st;
-  for (int64_t b = 0; b < batch; ++b) fill_result(states[b], &outs[b]);
+  for (int64_t b = 0; b < batch; ++b) fill_result(states[b], nl, &outs[b]);
   return NS_OK;
 }
 
@@ -360,6 +414,12 @@ ns_status_t ns_symm_product(const double* A, const double* B, double* C, int64_t
                             cudaMemcpyDeviceToDevice, cs));
   NS_CUDA(cudaStreamSynchronize(cs));
   return NS_OK;
+}
+
+void ns_profile_enable(int on) { prof().on = (on != 0); }
+void ns_profile_reset(void) { prof().acc = ns_profile_t{}; }
+void ns_profile_get(ns_profile_t* out) {
+  if (out) *out = prof().acc;
 }
 
 const char* ns_build_info(void) {

@@ -129,6 +129,15 @@ def test_householder_closed_form_and_generator():
     assert np.max(np.abs(Rc - R[:, cols])) <= 1e-14
 
 
+def test_householder_fast_formation():
+    """The WY formation used for large-d inputs equals the inside-out rank-2 recipe (C13)."""
+    lam, Vh = workloads.householder_spectrum(1, 300, 20, 0.05, 16)
+    H1 = workloads.householder_form_numpy(Vh, lam)
+    H2 = workloads.householder_form_fast(Vh, lam)
+    assert np.array_equal(H2, H2.T)
+    assert np.max(np.abs(H1 - H2)) <= 1e-14
+
+
 def test_cfg3_recipe_reduced_size():
     """cfg3 recipe at d=1024, k=64 (C13): steps == prediction (both tol readings, C3); R == closed form."""
     p = workloads.cfg3_dense(d=1024, k=64)
