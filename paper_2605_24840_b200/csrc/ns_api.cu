@@ -76,7 +76,7 @@ Layout make_layout(int64_t d, int64_t batch) {
 // few dozen row panels, so each k-slab of a panel is fetched from HBM about once per
 // wave and re-read from L2 by the other CTAs.
 std::vector<int2> make_tiles(int n) {
-  const int G = 8;
+  const int G = 12;
   std::vector<int2> v;
   v.reserve((size_t)n * (n + 1) / 2);
   for (int SI = 0; SI < n; SI += G)

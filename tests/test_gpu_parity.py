@@ -212,3 +212,27 @@ def test_cfg3_full_size_sampled(nsr):
     assert np.max(np.abs(Rg - Rc)) <= 1e-12
     blk = R[1000:1300, 9000:9300]
     assert torch.equal(blk, R[9000:9300, 1000:1300].T)
+
+
+def test_cfg2_full_size_golden(nsr, golden_dir):
+    """configs[2] at full size (64x64 grid, d=4096), seed 0 (the stiffest, gamma ~ 1e-5):
+    s and alpha from the oracle's Jacobi (tests/golden/cfg2_seed0.json, written by
+    tools/make_golden_cfg2.py from oracle/ only); steps, certificate, flags and sampled
+    columns of the oracle's NS reflector and Jacobi I - 2P_5 must match."""
+    import json
+    import os
+    g = json.load(open(os.path.join(golden_dir, "cfg2_seed0.json")))
+    cols = np.load(os.path.join(golden_dir, "cfg2_seed0_cols.npz"))
+    prob = workloads.cfg2_allen_cahn(seed=0, s=g["s"])
+    assert abs(prob.alpha - g["alpha"]) <= 1e-12 * g["alpha"]
+    Hg = torch.from_numpy(prob.H).to(_dev())
+    R, res = nsr.ns_reflector(Hg, g["s"], g["alpha"], 5, 100, 1e-12, 0)
+    hist = g["ns"]["hist_residual"]
+    if not _tie_band(hist, 1e-12, g["ns"]["steps"]):
+        assert res["steps"] == g["ns"]["steps"] and res["flags"] == g["ns"]["flags"]
+    assert res["cert"] == g["ns"]["cert"] == 5
+    c = torch.as_tensor(cols["cols"], device=_dev())
+    Rc = R[:, c].cpu().numpy()
+    assert np.sqrt(np.mean(np.sum((Rc - cols["R_ns"]) ** 2, axis=0))) <= TOL_R     # estimates ||dR||_F/sqrt(d)
+    assert np.sqrt(np.mean(np.sum((Rc - cols["R_eig"]) ** 2, axis=0))) <= TOL_R
+    assert torch.equal(R, R.T)
