@@ -145,13 +145,19 @@ ns_status_t ns_reflector_batched(const double* H, int64_t d, int64_t batch, int6
                                  ns_result_t* outs);
 
 /*
- * ns_symm_product — kernel-level entry used by tests: C = A B for symmetric A, B that
- * commute (so C is symmetric), computed on upper-triangle tiles only and mirrored;
- * C is bitwise symmetric.  A, B, C device, d x d, leading dim ld (same for all).
- * mode 0: C = A B.  mode 1: C = 1.5 A - 0.5 (A B) (the NS update epilogue).
+ * ns_symm_product — kernel-level entry used by tests (the contraction core alone).
+ * A and B are symmetric (only their upper triangles are read); A, B, C device, d x d,
+ * leading dim ld (same for all).
+ * mode 0: C = A B for commuting A, B (C symmetric): upper-triangle tiles only, mirrored,
+ *         C bitwise symmetric.
+ * mode 1: C = 1.5 A - 0.5 (A B) (the NS update epilogue), same tiling.
+ * mode 2: C = A B, every tile (no symmetry assumed for the result).
+ * prec NS_PREC_FP64: FP64 DMMA kernel; NS_PREC_MIXED_BF16X3: tcgen05 BF16x3 kernel (FP32
+ * accumulation; A and B are split into BF16 hi/lo planes first).
+ * The workspace must hold ns_workspace_bytes(d, prec) bytes.
  */
 ns_status_t ns_symm_product(const double* A, const double* B, double* C, int64_t d, int64_t ld,
-                            int32_t mode, void* ws, size_t ws_bytes, void* stream);
+                            int32_t mode, ns_precision_t prec, void* ws, size_t ws_bytes, void* stream);
 
 /*
  * Optional per-thread kernel timing (used by bench.py for the roofline): when enabled,

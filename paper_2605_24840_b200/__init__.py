@@ -72,7 +72,7 @@ def load_library(path=LIB_PATH):
     lib.ns_reflector_batched.argtypes = [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_i32, c_dbl, ctypes.c_int,
                                          ctypes.c_int, c_vp, c_i64, c_vp, c_sz, c_vp, ctypes.POINTER(NsResult)]
     lib.ns_symm_product.restype = ctypes.c_int
-    lib.ns_symm_product.argtypes = [c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, c_vp, c_sz, c_vp]
+    lib.ns_symm_product.argtypes = [c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, ctypes.c_int, c_vp, c_sz, c_vp]
     lib.ns_build_info.restype = ctypes.c_char_p
     lib.ns_status_string.restype = ctypes.c_char_p
     lib.ns_status_string.argtypes = [ctypes.c_int]
@@ -196,8 +196,9 @@ def ns_reflector_batched(H, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_ABS, pr
     return R, [o.as_dict() for o in outs]
 
 
-def ns_symm_product(A, B, mode=0, C=None, ws=None, stream=None):
-    """C = A B (mode 0) or 1.5 A - 0.5 A B (mode 1) for commuting symmetric A, B (upper triangles read)."""
+def ns_symm_product(A, B, mode=0, C=None, ws=None, stream=None, prec=NS_PREC_FP64):
+    """C = A B (mode 0, symmetric tiles), 1.5 A - 0.5 A B (mode 1) or A B on every tile (mode 2);
+    A, B symmetric (upper triangles read).  prec selects the FP64 DMMA or BF16x3 tcgen05 core."""
     torch = _torch()
     lib = load_library()
     _require_cuda_f64(A, "A")
@@ -208,9 +209,9 @@ def ns_symm_product(A, B, mode=0, C=None, ws=None, stream=None):
     if C is None:
         C = torch.empty_like(A)
     if ws is None:
-        ws = alloc_workspace(lib.ns_workspace_bytes(d, NS_PREC_FP64), A.device)
+        ws = alloc_workspace(lib.ns_workspace_bytes(d, prec), A.device)
     st = lib.ns_symm_product(ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()),
-                             ctypes.c_void_p(C.data_ptr()), d, A.stride(0), int(mode),
+                             ctypes.c_void_p(C.data_ptr()), d, A.stride(0), int(mode), int(prec),
                              ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream))
     _check(st)
     return C

@@ -45,11 +45,12 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 struct Layout {
   int d = 0, d_pad = 0, n = 0, n_tiles = 0;
   long long batch = 1;
+  bool mixed = false;
   size_t off_xa = 0, off_xb = 0, off_y = 0, off_res = 0, off_tr = 0, off_tiles = 0, off_jobs = 0,
-         off_state = 0, off_active = 0, total = 0;
+         off_state = 0, off_active = 0, off_px = 0, off_py = 0, off_full = 0, total = 0;
 };
 
-Layout make_layout(int64_t d, int64_t batch) {
+Layout make_layout(int64_t d, int64_t batch, bool mixed = false) {
   Layout L;
   L.d = static_cast<int>(d);
   L.d_pad = static_cast<int>((d + kTile - 1) / kTile * kTile);
@@ -67,8 +68,26 @@ Layout make_layout(int64_t d, int64_t batch) {
   L.off_jobs = o; o = align256(o + sizeof(JobParams) * (size_t)batch);
   L.off_state = o; o = align256(o + sizeof(DevState) * (size_t)batch);
   L.off_active = o; o = align256(o + 256);
+  L.off_full = o; o = align256(o + sizeof(int2) * (size_t)L.n * L.n);   // full tile list (dense products)
+  L.mixed = mixed;
+  if (mixed) {
+    const size_t planes = (size_t)L.d_pad * L.d_pad * 2 * sizeof(uint16_t) * (size_t)batch;
+    L.off_px = o; o = align256(o + planes);     // bf16 hi/lo planes of the current iterate
+    L.off_py = o; o = align256(o + planes);     // bf16 hi/lo planes of Y
+  }
   L.total = o;
   return L;
+}
+
+std::vector<int2> make_tiles_full(int n) {
+  std::vector<int2> v;
+  v.reserve((size_t)n * n);
+  const int G = 12;
+  for (int SI = 0; SI < n; SI += G)
+    for (int SJ = 0; SJ < n; SJ += G)
+      for (int I = SI; I < std::min(SI + G, n); ++I)
+        for (int J = SJ; J < std::min(SJ + G, n); ++J) v.push_back(make_int2(I, J));
+  return v;
 }
 
 // Upper-triangle tile order: super-blocks of G x G tiles (row-major over the upper
@@ -115,6 +134,22 @@ ns_status_t encode_map(CUtensorMap* m, const double* base, int d_pad, long long 
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(NS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return NS_OK;
+}
+
+// 3-D map over `nplanes` row-major d_pad x d_pad BF16 planes; box = 64 (k) x 128 (rows) x 1, 128-B swizzle
+// (the layout the UMMA shared-memory descriptors in ns_mixed.cu describe).
+ns_status_t encode_map_bf16(CUtensorMap* m, const uint16_t* base, int d_pad, long long nplanes) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(NS_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)d_pad, (cuuint64_t)d_pad, (cuuint64_t)nplanes};
+  cuuint64_t strides[2] = {(cuuint64_t)d_pad * 2, (cuuint64_t)d_pad * (cuuint64_t)d_pad * 2};
+  cuuint32_t box[3] = {(cuuint32_t)kMxBK, (cuuint32_t)kTile, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<uint16_t*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(NS_ERR_CUDA, "cuTensorMapEncodeTiled (bf16) failed (%d)", (int)r);
   return NS_OK;
 }
 
@@ -276,9 +311,8 @@ void fill_result(const DevState& s, int launches, ns_result_t* out) {
 extern "C" {
 
 size_t ns_workspace_bytes(int64_t d, ns_precision_t prec) {
-  (void)prec;
   if (d < 1) return 0;
-  return make_layout(d, 1).total;
+  return make_layout(d, 1, prec != NS_PREC_FP64).total;
 }
 
 size_t ns_workspace_bytes_batched(int64_t d, int64_t batch, ns_precision_t prec) {
@@ -380,36 +414,50 @@ ns_status_t ns_reflector_batched(const double* H, int64_t d, int64_t batch, int6
 }
 
 ns_status_t ns_symm_product(const double* A, const double* B, double* C, int64_t d, int64_t ld, int32_t mode,
-                            void* ws, size_t ws_bytes, void* stream) {
+                            ns_precision_t prec, void* ws, size_t ws_bytes, void* stream) {
   g_last_error.clear();
   if (d < 1 || d > 65536) return fail(NS_ERR_INVALID_ARG, "bad d");
   if (ld < d) return fail(NS_ERR_INVALID_ARG, "ld must be >= d");
-  if (mode != 0 && mode != 1) return fail(NS_ERR_INVALID_ARG, "mode must be 0 or 1");
+  if (mode < 0 || mode > 2) return fail(NS_ERR_INVALID_ARG, "mode must be 0, 1 or 2");
+  if (prec != NS_PREC_FP64 && prec != NS_PREC_MIXED_BF16X3) return fail(NS_ERR_UNSUPPORTED, "precision not available");
   if (!A || !B || !C || !ws) return fail(NS_ERR_INVALID_ARG, "null pointer argument");
   if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(NS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
-  const Layout L = make_layout(d, 1);
-  if (ws_bytes < L.total) return fail(NS_ERR_WORKSPACE, "workspace too small");
+  const bool mixed = (prec == NS_PREC_MIXED_BF16X3);
+  const Layout L = make_layout(d, 1, mixed);
+  if (ws_bytes < L.total) return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   uint8_t* w = static_cast<uint8_t*>(ws);
   double* Pa = reinterpret_cast<double*>(w + L.off_xa);   // padded A
   double* Pb = reinterpret_cast<double*>(w + L.off_xb);   // padded B
   double* Pc = reinterpret_cast<double*>(w + L.off_y);    // padded C
-  int2* tiles = reinterpret_cast<int2*>(w + L.off_tiles);
+  int2* tiles = reinterpret_cast<int2*>(w + (mode == 2 ? L.off_full : L.off_tiles));
   JobParams* djobs = reinterpret_cast<JobParams*>(w + L.off_jobs);
-  std::vector<int2> tl = make_tiles(L.n);
+  std::vector<int2> tl = (mode == 2) ? make_tiles_full(L.n) : make_tiles(L.n);
   NS_CUDA(cudaMemcpyAsync(tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, cs));
   JobParams unit{0.0, 1.0, 0, 0};
   NS_CUDA(cudaMemcpyAsync(djobs, &unit, sizeof(unit), cudaMemcpyHostToDevice, cs));
   // pad (and symmetrise from the upper triangle, s = 0, alpha = 1)
   NS_CUDA(launch_init(A, ld, 0, Pa, djobs, L.d, L.d_pad, 1, cs));
   NS_CUDA(launch_init(B, ld, 0, Pb, djobs, L.d, L.d_pad, 1, cs));
-  CUtensorMap tA, tB;
+  double* partial = reinterpret_cast<double*>(w + (mode == 0 ? L.off_res : L.off_tr));
   ns_status_t s;
-  if ((s = encode_map(&tA, Pa, L.d_pad, 1)) != NS_OK) return s;
-  if ((s = encode_map(&tB, Pb, L.d_pad, 1)) != NS_OK) return s;
-  ProdParams p{tiles, L.n_tiles, L.d_pad / kBK, L.d, L.d_pad, 0, Pc, Pa,
-               reinterpret_cast<double*>(w + (mode == 0 ? L.off_res : L.off_tr)), nullptr, mode};
-  NS_CUDA(launch_product(tA, tB, p, 1, cs));
+  if (!mixed) {
+    CUtensorMap tA, tB;
+    if ((s = encode_map(&tA, Pa, L.d_pad, 1)) != NS_OK) return s;
+    if ((s = encode_map(&tB, Pb, L.d_pad, 1)) != NS_OK) return s;
+    ProdParams p{tiles, (int)tl.size(), L.d_pad / kBK, L.d, L.d_pad, 0, Pc, Pa, partial, nullptr, mode};
+    NS_CUDA(launch_product(tA, tB, p, 1, cs));
+  } else {
+    uint16_t* planesA = reinterpret_cast<uint16_t*>(w + L.off_px);
+    uint16_t* planesB = reinterpret_cast<uint16_t*>(w + L.off_py);
+    NS_CUDA(launch_split_planes(Pa, planesA, L.d_pad, 1, cs));
+    NS_CUDA(launch_split_planes(Pb, planesB, L.d_pad, 1, cs));
+    CUtensorMap tA, tB;
+    if ((s = encode_map_bf16(&tA, planesA, L.d_pad, 2)) != NS_OK) return s;
+    if ((s = encode_map_bf16(&tB, planesB, L.d_pad, 2)) != NS_OK) return s;
+    MxParams p{tiles, (int)tl.size(), L.d_pad / kMxBK, L.d, L.d_pad, 0, Pc, Pa, nullptr, partial, nullptr, mode};
+    NS_CUDA(launch_mx_product(tA, tB, p, 1, cs));
+  }
   NS_CUDA(cudaMemcpy2DAsync(C, (size_t)ld * 8, Pc, (size_t)L.d_pad * 8, (size_t)d * 8, (size_t)d,
                             cudaMemcpyDeviceToDevice, cs));
   NS_CUDA(cudaStreamSynchronize(cs));

@@ -188,7 +188,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool diag = (I == J);
   double part = 0.0;
 
-  if (MODE == 0) {
+  if (MODE == 2) {
+    // dense product tile, no symmetry assumed: C_IJ only
+    for (int idx = tid; idx < kTile * kTile; idx += 256) {
+      const int r = idx >> 7, c = idx & 127;
+      C[(long long)(I * kTile + r) * ld + J * kTile + c] = S[r * kEpiPitch + c];
+    }
+  } else if (MODE == 0) {
     // Y tile + residual partial: off-diagonal tiles count twice (Y_JI = Y_IJ^T).
     if (!diag) {
       for (int idx = tid; idx < kTile * kTile; idx += 256) {
@@ -249,6 +255,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
+  if (MODE == 2) return;
   // fixed-order reduction of `part` over the 256 consumer threads
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
@@ -372,9 +379,15 @@ cudaError_t launch_trace_partials(const double* X, int d, int d_pad, int batch, 
 
 cudaError_t launch_product(const CUtensorMap& tmP, const CUtensorMap& tmQ, const ProdParams& p, int batch,
                            cudaStream_t st) {
-  static bool attr_done[2] = {false, false};
+  static bool attr_done[3] = {false, false, false};
   dim3 grid(p.n_tiles, batch);
-  if (p.mode == 0) {
+  if (p.mode == 2) {
+    if (!attr_done[2]) {
+      cudaFuncSetAttribute(ns_product_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+      attr_done[2] = true;
+    }
+    ns_product_kernel<2><<<grid, kThreads, kSmemBytes, st>>>(tmP, tmQ, p);
+  } else if (p.mode == 0) {
     if (!attr_done[0]) {
       cudaFuncSetAttribute(ns_product_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
       attr_done[0] = true;

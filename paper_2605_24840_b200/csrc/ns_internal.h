@@ -59,6 +59,34 @@ struct ProdParams {
   int mode;                // 0 = square/plain product + residual, 1 = NS update + trace
 };
 
+// ---------------- mixed path (tcgen05 BF16x3, ns_mixed.cu) ----------------
+constexpr int kMxBK = 64;                       // bf16 per k-block: 128 B = one swizzle row
+constexpr int kMxStages = 6;
+constexpr int kMxThreads = 192;                 // warp 0 TMA, warp 1 MMA, warps 2..5 epilogue
+constexpr int kMxStageBytes = 2 * kTile * kMxBK * 2;   // 32 KB
+constexpr int kMxSmemBytes = kMxStages * kMxStageBytes + 1024 + 256;
+
+// C_IJ = sum over the 3 split terms of P'_I Q'_J^T with P' = [P_hi P_lo P_hi], Q' = [Q_lo Q_hi Q_hi]
+// (small terms first), FP32 accumulation in TMEM.  Planes: [job][hi|lo][d_pad][d_pad] bf16.
+struct MxParams {
+  const int2* tiles;
+  int n_tiles;
+  int nkb;                 // d_pad / kMxBK
+  int d;
+  int ld;                  // d_pad
+  long long job_stride;    // FP64 elements between jobs' matrices
+  double* C;               // FP64 output (mode 0: Y, 1: X_{j+1}, 2: W dense)
+  const double* Xold;      // mode 1
+  uint16_t* Cplanes;       // bf16 planes of C (modes 0, 1), nullptr = skip
+  double* partial;         // mode 0 residual partial per tile; mode 1 trace partial per diag block
+  const DevState* state;
+  int mode;                // 0 square (+res, mirror), 1 update (+trace, mirror), 2 dense tile (no mirror)
+};
+
+cudaError_t launch_split_planes(const double* X, uint16_t* planes, int d_pad, int batch, cudaStream_t st);
+cudaError_t launch_mx_product(const CUtensorMap& tmP, const CUtensorMap& tmQ, const MxParams& p, int batch,
+                              cudaStream_t st);
+
 // Host-side launchers (ns_fp64.cu).
 cudaError_t launch_init(const double* H, long long ldh, long long h_stride, double* X, const JobParams* jobs,
                         int d, int d_pad, int batch, cudaStream_t st);

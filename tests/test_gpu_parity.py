@@ -236,3 +236,25 @@ def test_cfg2_full_size_golden(nsr, golden_dir):
     assert np.sqrt(np.mean(np.sum((Rc - cols["R_ns"]) ** 2, axis=0))) <= TOL_R     # estimates ||dR||_F/sqrt(d)
     assert np.sqrt(np.mean(np.sum((Rc - cols["R_eig"]) ** 2, axis=0))) <= TOL_R
     assert torch.equal(R, R.T)
+
+
+# ------------------------------------------------------------------ tcgen05 BF16x3 contraction core
+@pytest.mark.parametrize("d,mode", [(128, 0), (256, 0), (300, 0), (515, 1), (384, 2), (200, 2)])
+def test_mixed_product_kernel(nsr, d, mode):
+    """BF16x3 (hi*lo + lo*hi + hi*hi, FP32 accumulate in TMEM) against float64: relative error
+    at the split-BF16 level (~2^-16), bitwise-symmetric output for modes 0/1."""
+    rng = np.random.default_rng(77 + d)
+    A = rng.standard_normal((d, d))
+    A = 0.5 * (A + A.T) / math.sqrt(d)
+    B = A @ A if mode != 2 else rng.standard_normal((d, d))
+    B = 0.5 * (B + B.T)
+    Ag, Bg = torch.from_numpy(A).to(_dev()), torch.from_numpy(B).to(_dev())
+    C = nsr.ns_symm_product(Ag, Bg, mode=mode, prec=nsr.NS_PREC_MIXED_BF16X3).cpu().numpy()
+    ref = A @ B if mode != 1 else 1.5 * A - 0.5 * (A @ B)
+    err = np.max(np.abs(C - ref)) / np.max(np.abs(A @ B))
+    assert err <= 2e-5, err
+    assert err >= 1e-12, "suspiciously exact: is the FP64 kernel running?"
+    if mode != 2:
+        assert np.array_equal(C, C.T)
+    C64 = nsr.ns_symm_product(Ag, Bg, mode=mode).cpu().numpy()
+    assert np.max(np.abs(C64 - ref)) <= 1e-13 * np.max(np.abs(ref)) * math.sqrt(d)
