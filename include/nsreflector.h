@@ -52,7 +52,7 @@ extern "C" {
 
 typedef enum {
   NS_PREC_FP64 = 0,          /* FP64 DMMA contraction (accuracy path) */
-  NS_PREC_MIXED_BF16X3 = 1,  /* reserved: tcgen05 split-BF16 path (returns NS_ERR_UNSUPPORTED) */
+  NS_PREC_MIXED_BF16X3 = 1,  /* tcgen05 BF16x3 steps -> switch -> re-anchor -> FP64 steps (C16) */
   NS_PREC_MIXED_TF32X3 = 2   /* reserved: tcgen05 split-TF32 path (returns NS_ERR_UNSUPPORTED) */
 } ns_precision_t;
 
@@ -89,8 +89,30 @@ typedef struct {
   double trace;
   int64_t index_cert;
   int32_t kernel_launches;   /* device kernels this call launched (incl. early-exit look-ahead steps) */
-  int32_t pad;
+  int32_t switch_step;       /* mixed path: j at which the low-precision phase ended (-1 = none) */
+  double pre_polish_residual;/* mixed path: low-precision ||X_switch^2 - I||_F (0 if no switch) */
 } ns_result_t;
+
+/*
+ * Tuning / diagnostic options (ns_reflector_ex).  ns_options_default() fills the
+ * library defaults, which ns_reflector uses.
+ *   switch_tol     mixed path: the BF16x3 phase ends at the first j with
+ *                  ||X_j^2 - I||_F / sqrt(d) < switch_tol (default 1e-4, reading C16).
+ *   cg_iters       mixed path: conjugate-gradient iterations of the re-anchor solve
+ *                  |A|E + E|A| = sym(X~ [A, X~]) (default 24; 0 = polish without re-anchor).
+ *   stop_at_switch mixed path: return the pre-polish iterate X_switch as R (no re-anchor,
+ *                  no FP64 steps); flags then carry neither CONVERGED nor MAX_STEPS.
+ *   lookahead      steps enqueued before the host reads the stop flag (0 = default).
+ */
+typedef struct {
+  double switch_tol;
+  int32_t cg_iters;
+  int32_t stop_at_switch;
+  int32_t lookahead;
+  int32_t reserved[3];
+} ns_options_t;
+
+void ns_options_default(ns_options_t* opts);
 
 /* Bytes of device workspace ns_reflector needs for dimension d (batch = 1). */
 size_t ns_workspace_bytes(int64_t d, ns_precision_t prec);
@@ -105,7 +127,9 @@ size_t ns_workspace_bytes_batched(int64_t d, int64_t batch, ns_precision_t prec)
  *   k      target index, 0 <= k <= d (the paper's domain is 1..d-1); used
  *          only for NS_F_INDEX_MISMATCH.
  *   max_steps >= 0; tol >= 0 (0 = fixed max_steps updates); tm tolerance mode.
- *   prec   NS_PREC_FP64 (the mixed modes return NS_ERR_UNSUPPORTED in this build).
+ *   prec   NS_PREC_FP64, or NS_PREC_MIXED_BF16X3: BF16x3 tcgen05 steps until the switch
+ *          threshold, one FP64 re-anchor solve, FP64 steps to tol (single problem only;
+ *          NS_PREC_MIXED_TF32X3 returns NS_ERR_UNSUPPORTED).
  *   R      device, d x d, leading dim ldr >= d; written in full, bitwise symmetric.
  *   ws     device workspace, ws_bytes >= ns_workspace_bytes(d, prec).
  *   stream cudaStream_t (as void*); NULL = legacy default stream.
@@ -115,6 +139,12 @@ ns_status_t ns_reflector(const double* H, int64_t d, int64_t ldh, double s, doub
                          int32_t max_steps, double tol, ns_tolmode_t tm, ns_precision_t prec,
                          double* R, int64_t ldr, void* ws, size_t ws_bytes, void* stream,
                          ns_result_t* out);
+
+/* ns_reflector with explicit options (NULL = defaults). */
+ns_status_t ns_reflector_ex(const double* H, int64_t d, int64_t ldh, double s, double alpha, int32_t k,
+                            int32_t max_steps, double tol, ns_tolmode_t tm, ns_precision_t prec,
+                            double* R, int64_t ldr, void* ws, size_t ws_bytes, void* stream,
+                            const ns_options_t* opts, ns_result_t* out);
 
 /*
  * ns_reflector_host — same computation with HOST H and R (end-to-end entry point):

@@ -22,18 +22,25 @@ NS_F_SCALING_SUSPECT, NS_F_NONFINITE, NS_F_SHIFT_ON_SPECTRUM = 8, 16, 32
 EXPORTED_SYMBOLS = (
     "ns_workspace_bytes", "ns_workspace_bytes_batched", "ns_workspace_bytes_host", "ns_reflector",
     "ns_reflector_host", "ns_reflector_batched", "ns_symm_product", "ns_build_info", "ns_status_string",
-    "ns_last_error", "ns_profile_enable", "ns_profile_reset", "ns_profile_get",
+    "ns_last_error", "ns_profile_enable", "ns_profile_reset", "ns_profile_get", "ns_options_default",
+    "ns_reflector_ex",
 )
 
 
 class NsResult(ctypes.Structure):
     _fields_ = [("steps", ctypes.c_int32), ("flags", ctypes.c_int32), ("residual", ctypes.c_double),
                 ("trace", ctypes.c_double), ("index_cert", ctypes.c_int64), ("kernel_launches", ctypes.c_int32),
-                ("pad", ctypes.c_int32)]
+                ("switch_step", ctypes.c_int32), ("pre_polish_residual", ctypes.c_double)]
 
     def as_dict(self):
         return dict(steps=self.steps, flags=self.flags, residual=self.residual, trace=self.trace,
-                    cert=self.index_cert, launches=self.kernel_launches)
+                    cert=self.index_cert, launches=self.kernel_launches, switch_step=self.switch_step,
+                    pre_polish_residual=self.pre_polish_residual)
+
+
+class NsOptions(ctypes.Structure):
+    _fields_ = [("switch_tol", ctypes.c_double), ("cg_iters", ctypes.c_int32), ("stop_at_switch", ctypes.c_int32),
+                ("lookahead", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
 
 
 class NsProfile(ctypes.Structure):
@@ -66,6 +73,11 @@ def load_library(path=LIB_PATH):
     lib.ns_reflector.restype = ctypes.c_int
     lib.ns_reflector.argtypes = [c_vp, c_i64, c_i64, c_dbl, c_dbl, c_i32, c_i32, c_dbl, ctypes.c_int, ctypes.c_int,
                                  c_vp, c_i64, c_vp, c_sz, c_vp, ctypes.POINTER(NsResult)]
+    lib.ns_reflector_ex.restype = ctypes.c_int
+    lib.ns_reflector_ex.argtypes = [c_vp, c_i64, c_i64, c_dbl, c_dbl, c_i32, c_i32, c_dbl, ctypes.c_int, ctypes.c_int,
+                                    c_vp, c_i64, c_vp, c_sz, c_vp, ctypes.POINTER(NsOptions), ctypes.POINTER(NsResult)]
+    lib.ns_options_default.restype = None
+    lib.ns_options_default.argtypes = [ctypes.POINTER(NsOptions)]
     lib.ns_reflector_host.restype = ctypes.c_int
     lib.ns_reflector_host.argtypes = lib.ns_reflector.argtypes
     lib.ns_reflector_batched.restype = ctypes.c_int
@@ -122,9 +134,19 @@ def alloc_workspace(nbytes, device):
     return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
 
 
+def ns_options(**kw):
+    """ns_options_t with library defaults, fields overridden by keyword (switch_tol, cg_iters, ...)."""
+    o = NsOptions()
+    load_library().ns_options_default(ctypes.byref(o))
+    for k_, v in kw.items():
+        setattr(o, k_, v)
+    return o
+
+
 def ns_reflector(H, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_ABS, prec=NS_PREC_FP64, R=None, ws=None,
-                 stream=None):
-    """R = sgn(H - sI) by Newton–Schulz on the GPU (C-ABI ns_reflector).  Returns (R, result dict)."""
+                 stream=None, options=None):
+    """R = sgn(H - sI) by Newton–Schulz on the GPU (C-ABI ns_reflector / ns_reflector_ex when options
+    are given).  Returns (R, result dict)."""
     torch = _torch()
     lib = load_library()
     _require_cuda_f64(H, "H")
@@ -138,10 +160,13 @@ def ns_reflector(H, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_ABS, prec=NS_PR
     if ws is None:
         ws = alloc_workspace(need, H.device)
     res = NsResult()
-    st = lib.ns_reflector(ctypes.c_void_p(H.data_ptr()), d, H.stride(0), float(s), float(alpha), int(k),
-                          int(max_steps), float(tol), int(tol_mode), int(prec), ctypes.c_void_p(R.data_ptr()),
-                          R.stride(0), ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream),
-                          ctypes.byref(res))
+    args = (ctypes.c_void_p(H.data_ptr()), d, H.stride(0), float(s), float(alpha), int(k), int(max_steps), float(tol),
+            int(tol_mode), int(prec), ctypes.c_void_p(R.data_ptr()), R.stride(0), ctypes.c_void_p(ws.data_ptr()),
+            ws.numel(), _stream_ptr(stream))
+    if options is None:
+        st = lib.ns_reflector(*args, ctypes.byref(res))
+    else:
+        st = lib.ns_reflector_ex(*args, ctypes.byref(options), ctypes.byref(res))
     _check(st)
     return R, res.as_dict()
 

@@ -47,7 +47,8 @@ struct Layout {
   long long batch = 1;
   bool mixed = false;
   size_t off_xa = 0, off_xb = 0, off_y = 0, off_res = 0, off_tr = 0, off_tiles = 0, off_jobs = 0,
-         off_state = 0, off_active = 0, off_px = 0, off_py = 0, off_full = 0, total = 0;
+         off_state = 0, off_active = 0, off_px = 0, off_py = 0, off_full = 0, off_pxb = 0, off_ahat = 0,
+         off_r = 0, off_p = 0, off_cgpart = 0, off_cgsc = 0, total = 0;
 };
 
 Layout make_layout(int64_t d, int64_t batch, bool mixed = false) {
@@ -72,8 +73,16 @@ Layout make_layout(int64_t d, int64_t batch, bool mixed = false) {
   L.mixed = mixed;
   if (mixed) {
     const size_t planes = (size_t)L.d_pad * L.d_pad * 2 * sizeof(uint16_t) * (size_t)batch;
-    L.off_px = o; o = align256(o + planes);     // bf16 hi/lo planes of the current iterate
-    L.off_py = o; o = align256(o + planes);     // bf16 hi/lo planes of Y
+    L.off_px = o; o = align256(o + planes);     // bf16 hi/lo planes of X_j (even j) / CG direction P
+    L.off_pxb = o; o = align256(o + planes);    // bf16 hi/lo planes of X_j (odd j)
+    L.off_py = o; o = align256(o + planes);     // bf16 hi/lo planes of Y / |A|
+    L.off_ahat = o; o = align256(o + mat);      // A = X_0 kept in FP64 for the re-anchor; later E
+    L.off_r = o; o = align256(o + mat);         // CG residual R
+    L.off_p = o; o = align256(o + mat);         // CG direction P
+    const int nb = L.d_pad / 32;
+    const size_t npart = std::max<size_t>((size_t)nb * (nb + 1) / 2, (size_t)kEwBlocks);
+    L.off_cgpart = o; o = align256(o + sizeof(double) * npart);
+    L.off_cgsc = o; o = align256(o + sizeof(CgScalars));
   }
   L.total = o;
   return L;
@@ -193,9 +202,8 @@ ns_status_t check_common(int64_t d, int32_t max_steps, double tol, ns_tolmode_t 
   if (max_steps < 0) return fail(NS_ERR_INVALID_ARG, "max_steps must be >= 0");
   if (!(tol >= 0.0) || !std::isfinite(tol)) return fail(NS_ERR_INVALID_ARG, "tol must be finite and >= 0");
   if (tm != NS_TOL_ABS && tm != NS_TOL_PER_SQRT_D) return fail(NS_ERR_INVALID_ARG, "bad tolerance mode");
-  if (prec == NS_PREC_MIXED_BF16X3 || prec == NS_PREC_MIXED_TF32X3)
-    return fail(NS_ERR_UNSUPPORTED, "mixed-precision modes are not available in this build");
-  if (prec != NS_PREC_FP64) return fail(NS_ERR_INVALID_ARG, "bad precision");
+  if (prec == NS_PREC_MIXED_TF32X3) return fail(NS_ERR_UNSUPPORTED, "the TF32x3 mode is not available in this build");
+  if (prec != NS_PREC_FP64 && prec != NS_PREC_MIXED_BF16X3) return fail(NS_ERR_INVALID_ARG, "bad precision");
   return NS_OK;
 }
 
@@ -296,9 +304,186 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
   return NS_OK;
 }
 
+struct Opts {
+  double switch_tol = 1e-4;
+  int cg_iters = 24;
+  int stop_at_switch = 0;
+  int lookahead = 0;
+};
+
+Opts to_opts(const ns_options_t* o) {
+  Opts r;
+  if (o) {
+    r.switch_tol = o->switch_tol;
+    r.cg_iters = o->cg_iters;
+    r.stop_at_switch = o->stop_at_switch;
+    r.lookahead = o->lookahead;
+  }
+  return r;
+}
+
+// Mixed path (single problem): BF16x3 tcgen05 steps -> switch -> re-anchor -> FP64 steps.
+ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long ldh, const JobParams& jp,
+                      int32_t max_steps, double tol, ns_tolmode_t tm, double* R, long long ldr, cudaStream_t st,
+                      const Opts& opt, DevState& out_state, int* launches) {
+  double* Xa = reinterpret_cast<double*>(ws + L.off_xa);
+  double* Xb = reinterpret_cast<double*>(ws + L.off_xb);
+  double* Y = reinterpret_cast<double*>(ws + L.off_y);
+  double* Ahat = reinterpret_cast<double*>(ws + L.off_ahat);
+  double* Rc = reinterpret_cast<double*>(ws + L.off_r);
+  double* Pc = reinterpret_cast<double*>(ws + L.off_p);
+  double* res = reinterpret_cast<double*>(ws + L.off_res);
+  double* trp = reinterpret_cast<double*>(ws + L.off_tr);
+  double* cgpart = reinterpret_cast<double*>(ws + L.off_cgpart);
+  CgScalars* cgsc = reinterpret_cast<CgScalars*>(ws + L.off_cgsc);
+  uint16_t* PXa = reinterpret_cast<uint16_t*>(ws + L.off_px);
+  uint16_t* PXb = reinterpret_cast<uint16_t*>(ws + L.off_pxb);
+  uint16_t* PY = reinterpret_cast<uint16_t*>(ws + L.off_py);
+  int2* tiles = reinterpret_cast<int2*>(ws + L.off_tiles);
+  int2* full = reinterpret_cast<int2*>(ws + L.off_full);
+  JobParams* djobs = reinterpret_cast<JobParams*>(ws + L.off_jobs);
+  DevState* state = reinterpret_cast<DevState*>(ws + L.off_state);
+  int* n_active = reinterpret_cast<int*>(ws + L.off_active);
+  HostRing& rg = ring();
+  if (!rg.ok) return fail(NS_ERR_CUDA, "pinned status ring allocation failed");
+  const size_t mat_bytes = (size_t)L.d_pad * L.d_pad * sizeof(double);
+
+  std::vector<int2> tl = make_tiles(L.n), tf = make_tiles_full(L.n);
+  NS_CUDA(cudaMemcpyAsync(tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+  NS_CUDA(cudaMemcpyAsync(full, tf.data(), tf.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+  NS_CUDA(cudaMemcpyAsync(djobs, &jp, sizeof(JobParams), cudaMemcpyHostToDevice, st));
+
+  CUtensorMap tmA, tmB, tmY, tmAh, tmPXa, tmPXb, tmPY;
+  ns_status_t s;
+  if ((s = encode_map(&tmA, Xa, L.d_pad, 1)) != NS_OK) return s;
+  if ((s = encode_map(&tmB, Xb, L.d_pad, 1)) != NS_OK) return s;
+  if ((s = encode_map(&tmY, Y, L.d_pad, 1)) != NS_OK) return s;
+  if ((s = encode_map(&tmAh, Ahat, L.d_pad, 1)) != NS_OK) return s;
+  if ((s = encode_map_bf16(&tmPXa, PXa, L.d_pad, 2)) != NS_OK) return s;
+  if ((s = encode_map_bf16(&tmPXb, PXb, L.d_pad, 2)) != NS_OK) return s;
+  if ((s = encode_map_bf16(&tmPY, PY, L.d_pad, 2)) != NS_OK) return s;
+
+  int nl = 0;
+  NS_CUDA(launch_zero_state(state, 1, n_active, st));
+  NS_CUDA(launch_init(H, ldh, 0, Xa, djobs, L.d, L.d_pad, 1, st));
+  NS_CUDA(cudaMemcpyAsync(Ahat, Xa, mat_bytes, cudaMemcpyDeviceToDevice, st));
+  NS_CUDA(launch_trace_partials(Xa, L.d, L.d_pad, 1, trp, st));
+  NS_CUDA(launch_split_planes(Xa, PXa, L.d_pad, 1, st));
+  nl += 4;
+
+  // ---------------- phase 1: BF16x3 steps until the switch threshold ----------------
+  LoopParams lp_low{L.d, L.d_pad, max_steps, (int)tm, tol, opt.switch_tol > 0 ? opt.switch_tol : 1e-300};
+  const int LA = opt.lookahead > 0 ? std::min(opt.lookahead, 15) : 2;
+  const long long js = (long long)L.d_pad * L.d_pad;
+  for (int j = 0; j <= max_steps; ++j) {
+    if (j >= LA) {
+      const int slot = (j - LA) % 16;
+      NS_CUDA(cudaEventSynchronize(rg.ev[slot]));
+      if (rg.slots[slot] == 0) break;
+    }
+    const bool odd = (j & 1) != 0;
+    double* Xc = odd ? Xb : Xa;
+    double* Xn = odd ? Xa : Xb;
+    const CUtensorMap& tPc = odd ? tmPXb : tmPXa;
+    uint16_t* PXn = odd ? PXa : PXb;
+    MxParams sq{tiles, L.n_tiles, L.d_pad / kMxBK, L.d, L.d_pad, js, Y, nullptr, PY, res, state, 0};
+    NS_CUDA(launch_mx_product(tPc, tPc, sq, 1, st));
+    NS_CUDA(launch_decide(state, djobs, res, L.n_tiles, trp, L.n, lp_low, 1, n_active, st));
+    nl += 2;
+    if (j < max_steps) {
+      MxParams up{tiles, L.n_tiles, L.d_pad / kMxBK, L.d, L.d_pad, js, Xn, Xc, PXn, trp, state, 1};
+      NS_CUDA(launch_mx_product(tPc, tmPY, up, 1, st));
+      nl += 1;
+    }
+    NS_CUDA(cudaMemcpyAsync(&rg.slots[j % 16], n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+    NS_CUDA(cudaEventRecord(rg.ev[j % 16], st));
+  }
+  DevState hs;
+  NS_CUDA(cudaMemcpyAsync(&hs, state, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+  NS_CUDA(cudaStreamSynchronize(st));
+
+  if (!hs.done && !opt.stop_at_switch && hs.sw) {
+    const int j0 = hs.j;
+    double* Xt = (j0 & 1) ? Xb : Xa;                // X~ = X_switch
+    double* Xo = (j0 & 1) ? Xa : Xb;                // free FP64 buffer
+    const CUtensorMap& tXt = (j0 & 1) ? tmB : tmA;
+    const CUtensorMap& tXo = (j0 & 1) ? tmA : tmB;
+    const int nk = L.d_pad / kBK;
+    if (opt.cg_iters > 0) {
+      // M = A X~  (FP64 DMMA, every tile) -> Y
+      ProdParams pm{full, L.n * L.n, nk, L.d, L.d_pad, 0, Y, nullptr, nullptr, nullptr, 2};
+      NS_CUDA(launch_product(tmAh, tXt, pm, 1, st));
+      // C = M - M^T -> Xo ; |A| = sym(M) -> bf16 planes PY
+      NS_CUDA(launch_commutator(Y, Xo, PY, L.d_pad, st));
+      // F' = X~ C^T = -X~ C  (FP64 DMMA, every tile) -> Y
+      ProdParams pf{full, L.n * L.n, nk, L.d, L.d_pad, 0, Y, nullptr, nullptr, nullptr, 2};
+      NS_CUDA(launch_product(tXt, tXo, pf, 1, st));
+      // F = sym(X~ C); R = P = F; E = 0 (E lives in A's buffer, A is no longer needed)
+      int np = 0;
+      double* E = Ahat;
+      NS_CUDA(launch_cg_init(Y, Rc, Pc, E, cgpart, L.d_pad, st, &np));
+      NS_CUDA(launch_cg_scalar(cgsc, cgpart, np, 0, st));
+      NS_CUDA(launch_split_planes(Pc, PXa, L.d_pad, 1, st));
+      nl += 6;
+      for (int it = 0; it < opt.cg_iters; ++it) {
+        // W = |A| P (BF16x3 tcgen05, every tile) -> Xo
+        MxParams pw{full, L.n * L.n, L.d_pad / kMxBK, L.d, L.d_pad, 0, Xo, nullptr, nullptr, nullptr, nullptr, 2};
+        NS_CUDA(launch_mx_product(tmPY, tmPXa, pw, 1, st));
+        NS_CUDA(launch_cg_pw(Pc, Xo, cgpart, L.d_pad, st));
+        NS_CUDA(launch_cg_scalar(cgsc, cgpart, kEwBlocks, 1, st));
+        NS_CUDA(launch_cg_update(E, Rc, Pc, Xo, cgsc, cgpart, L.d_pad, st, &np));
+        NS_CUDA(launch_cg_scalar(cgsc, cgpart, np, 2, st));
+        nl += 5;
+        if (it + 1 < opt.cg_iters) {
+          NS_CUDA(launch_cg_direction(Pc, Rc, cgsc, PXa, L.d_pad, st));
+          nl += 1;
+        }
+      }
+      NS_CUDA(launch_apply_correction(Xt, E, L.d_pad, st));
+      nl += 1;
+    }
+    NS_CUDA(launch_trace_partials(Xt, L.d, L.d_pad, 1, trp, st));
+    nl += 1;
+
+    // ---------------- phase 2: FP64 steps from j0 to tolerance ----------------
+    LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0};
+    const int one = 1;
+    NS_CUDA(cudaMemcpyAsync(n_active, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+    for (int j = j0; j <= max_steps; ++j) {
+      if (j >= j0 + LA) {
+        const int slot = (j - LA) % 16;
+        NS_CUDA(cudaEventSynchronize(rg.ev[slot]));
+        if (rg.slots[slot] == 0) break;
+      }
+      const bool odd = (j & 1) != 0;
+      double* Xc = odd ? Xb : Xa;
+      double* Xn = odd ? Xa : Xb;
+      const CUtensorMap& tmC = odd ? tmB : tmA;
+      ProdParams sq{tiles, L.n_tiles, nk, L.d, L.d_pad, js, Y, nullptr, res, state, 0};
+      NS_CUDA(launch_product(tmC, tmC, sq, 1, st));
+      NS_CUDA(launch_decide(state, djobs, res, L.n_tiles, trp, L.n, lp, 1, n_active, st));
+      nl += 2;
+      if (j < max_steps) {
+        ProdParams up{tiles, L.n_tiles, nk, L.d, L.d_pad, js, Xn, Xc, trp, state, 1};
+        NS_CUDA(launch_product(tmC, tmY, up, 1, st));
+        nl += 1;
+      }
+      NS_CUDA(cudaMemcpyAsync(&rg.slots[j % 16], n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+      NS_CUDA(cudaEventRecord(rg.ev[j % 16], st));
+    }
+  }
+  NS_CUDA(launch_copy_out(Xa, Xb, L.d, L.d_pad, state, R, ldr, 0, 1, st));
+  nl += 1;
+  NS_CUDA(cudaMemcpyAsync(&out_state, state, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+  NS_CUDA(cudaStreamSynchronize(st));
+  if (launches) *launches = nl;
+  return NS_OK;
+}
+
 void fill_result(const DevState& s, int launches, ns_result_t* out) {
   out->kernel_launches = launches;
-  out->pad = 0;
+  out->switch_step = s.sw_step;
+  out->pre_polish_residual = s.sw ? s.sw_residual : 0.0;
   out->steps = s.j;
   out->flags = s.flags;
   out->residual = s.residual;
@@ -323,9 +508,19 @@ size_t ns_workspace_bytes_batched(int64_t d, int64_t batch, ns_precision_t prec)
 
 size_t ns_workspace_bytes_host(int64_t d, ns_precision_t prec) { return ns_workspace_bytes(d, prec); }
 
-ns_status_t ns_reflector(const double* H, int64_t d, int64_t ldh, double s, double alpha, int32_t k,
-                         int32_t max_steps, double tol, ns_tolmode_t tm, ns_precision_t prec, double* R, int64_t ldr,
-                         void* ws, size_t ws_bytes, void* stream, ns_result_t* out) {
+void ns_options_default(ns_options_t* o) {
+  if (!o) return;
+  *o = ns_options_t{};
+  o->switch_tol = 1e-4;
+  o->cg_iters = 24;
+  o->stop_at_switch = 0;
+  o->lookahead = 0;
+}
+
+ns_status_t ns_reflector_ex(const double* H, int64_t d, int64_t ldh, double s, double alpha, int32_t k,
+                            int32_t max_steps, double tol, ns_tolmode_t tm, ns_precision_t prec, double* R,
+                            int64_t ldr, void* ws, size_t ws_bytes, void* stream, const ns_options_t* opts,
+                            ns_result_t* out) {
   g_last_error.clear();
   ns_status_t st = check_common(d, max_steps, tol, tm, prec);
   if (st != NS_OK) return st;
@@ -336,17 +531,35 @@ ns_status_t ns_reflector(const double* H, int64_t d, int64_t ldh, double s, doub
   if (k < 0 || k > d) return fail(NS_ERR_INVALID_ARG, "k must lie in [0, d]");
   if (R == H) return fail(NS_ERR_INVALID_ARG, "R must not alias H");
   if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(NS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
-  const Layout L = make_layout(d, 1);
+  const bool mixed = (prec == NS_PREC_MIXED_BF16X3);
+  const Layout L = make_layout(d, 1, mixed);
   if (ws_bytes < L.total)
     return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
+  const Opts o = to_opts(opts);
+  if (mixed && (!(o.switch_tol >= 0.0) || o.cg_iters < 0)) return fail(NS_ERR_INVALID_ARG, "bad mixed options");
   std::vector<JobParams> jobs{JobParams{s, alpha, k, 0}};
-  std::vector<DevState> states;
   int nl = 0;
+  if (mixed) {
+    DevState ds;
+    st = run_mixed(L, static_cast<uint8_t*>(ws), H, ldh, jobs[0], max_steps, tol, tm, R, ldr,
+                   static_cast<cudaStream_t>(stream), o, ds, &nl);
+    if (st != NS_OK) return st;
+    fill_result(ds, nl, out);
+    return NS_OK;
+  }
+  std::vector<DevState> states;
   st = run_loop(L, static_cast<uint8_t*>(ws), H, ldh, 0, jobs, max_steps, tol, tm, R, ldr, 0,
                 static_cast<cudaStream_t>(stream), states, &nl);
   if (st != NS_OK) return st;
   fill_result(states[0], nl, out);
   return NS_OK;
+}
+
+ns_status_t ns_reflector(const double* H, int64_t d, int64_t ldh, double s, double alpha, int32_t k,
+                         int32_t max_steps, double tol, ns_tolmode_t tm, ns_precision_t prec, double* R, int64_t ldr,
+                         void* ws, size_t ws_bytes, void* stream, ns_result_t* out) {
+  return ns_reflector_ex(H, d, ldh, s, alpha, k, max_steps, tol, tm, prec, R, ldr, ws, ws_bytes, stream, nullptr,
+                         out);
 }
 
 ns_status_t ns_reflector_host(const double* H_host, int64_t d, int64_t ldh, double s, double alpha, int32_t k,
@@ -361,7 +574,8 @@ ns_status_t ns_reflector_host(const double* H_host, int64_t d, int64_t ldh, doub
   if (!(alpha > 0.0) || !std::isfinite(alpha)) return fail(NS_ERR_INVALID_ARG, "alpha must be finite and > 0");
   if (k < 0 || k > d) return fail(NS_ERR_INVALID_ARG, "k must lie in [0, d]");
   if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(NS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
-  const Layout L = make_layout(d, 1);
+  const bool mixed = (prec == NS_PREC_MIXED_BF16X3);
+  const Layout L = make_layout(d, 1, mixed);
   if (ws_bytes < L.total)
     return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
@@ -371,9 +585,12 @@ ns_status_t ns_reflector_host(const double* H_host, int64_t d, int64_t ldh, doub
   NS_CUDA(cudaMemcpy2DAsync(stage, (size_t)d * 8, H_host, (size_t)ldh * 8, (size_t)d * 8, (size_t)d,
                             cudaMemcpyHostToDevice, cs));
   std::vector<JobParams> jobs{JobParams{s, alpha, k, 0}};
-  std::vector<DevState> states;
+  std::vector<DevState> states(1);
   int nl = 0;
-  st = run_loop(L, w, stage, d, 0, jobs, max_steps, tol, tm, stage, d, 0, cs, states, &nl);
+  if (mixed)
+    st = run_mixed(L, w, stage, d, jobs[0], max_steps, tol, tm, stage, d, cs, Opts{}, states[0], &nl);
+  else
+    st = run_loop(L, w, stage, d, 0, jobs, max_steps, tol, tm, stage, d, 0, cs, states, &nl);
   if (st != NS_OK) return st;
   NS_CUDA(cudaMemcpy2DAsync(R_host, (size_t)ldr * 8, stage, (size_t)d * 8, (size_t)d * 8, (size_t)d,
                             cudaMemcpyDeviceToHost, cs));
@@ -389,6 +606,7 @@ ns_status_t ns_reflector_batched(const double* H, int64_t d, int64_t batch, int6
   g_last_error.clear();
   ns_status_t st = check_common(d, max_steps, tol, tm, prec);
   if (st != NS_OK) return st;
+  if (prec != NS_PREC_FP64) return fail(NS_ERR_UNSUPPORTED, "the batched entry runs the FP64 path only");
   if (batch < 1 || batch > 65535) return fail(NS_ERR_INVALID_ARG, "batch must be in [1, 65535]");
   if (!H || !R || !ws || !outs || !s || !alpha || !k) return fail(NS_ERR_INVALID_ARG, "null pointer argument");
   if (stride_h < d * d || stride_r < d * d) return fail(NS_ERR_INVALID_ARG, "strides must be >= d*d");

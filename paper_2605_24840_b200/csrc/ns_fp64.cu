@@ -297,6 +297,7 @@ __global__ void __launch_bounds__(256) ns_decide_kernel(DevState* __restrict__ s
   const int job = blockIdx.x;
   DevState* st = state + job;
   if (st->done) return;
+  if (lp.switch_tol > 0.0 && st->sw) return;   // low-precision phase already left (look-ahead launch)
   const double r2 = block_sum_fixed(res_partial + (long long)job * n_tiles, n_tiles, red);
   const double tr = block_sum_fixed(tr_partial + (long long)job * n_diag, n_diag, red);
   if (threadIdx.x != 0) return;
@@ -316,6 +317,16 @@ __global__ void __launch_bounds__(256) ns_decide_kernel(DevState* __restrict__ s
     } else if (st->j >= lp.max_steps) {
       flags |= 2;  // NS_F_MAX_STEPS
       done = 1;
+    } else if (lp.switch_tol > 0.0 && !st->sw && r / sqd < lp.switch_tol) {
+      // mixed path: leave the low-precision phase at this j (re-anchor + FP64 from here, C16)
+      st->sw = 1;
+      st->sw_step = st->j;
+      st->sw_residual = r;
+      st->residual = r;
+      st->trace = tr;
+      st->flags = flags;
+      if (n_active) atomicSub(n_active, 1);
+      return;
     }
   }
   st->residual = r;
@@ -344,6 +355,7 @@ __global__ void ns_zero_state_kernel(DevState* state, int batch, int* n_active) 
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < batch) {
     DevState z{};
+    z.sw_step = -1;
     state[i] = z;
   }
   if (i == 0 && n_active) *n_active = batch;

@@ -21,11 +21,14 @@ struct DevState {
   int32_t j;          // index of the current iterate X_j
   int32_t flags;      // NS_F_* bits
   int32_t done;       // 1 once a stop condition fired
-  int32_t pad0;
+  int32_t sw;         // mixed path: 1 once the low-precision phase hit the switch threshold
   double residual;    // r_j = ||X_j^2 - I||_F of the returned X
   double r_prev;      // r_{j-1}
   double trace;       // tr X_j
   int64_t cert;       // round((d - tr)/2)
+  double sw_residual; // mixed path: low-precision residual at the switch
+  int32_t sw_step;    // mixed path: j at the switch (-1 = none)
+  int32_t pad1;
 };
 
 // Per-problem scalar inputs (device copy).
@@ -42,7 +45,29 @@ struct LoopParams {
   int max_steps;
   int tol_mode;        // 0 abs, 1 per sqrt(d)
   double tol;
+  double switch_tol;   // mixed path: leave the low-precision phase when r/sqrt(d) < switch_tol (0 = never)
 };
+
+// ---------------- re-anchor (ns_reanchor.cu) ----------------
+// Device scalars of the conjugate-gradient solve |A|E + E|A| = F.
+struct CgScalars {
+  double rr;      // <R, R>
+  double pw;      // <P, W>,  W = |A| P
+  double alpha;
+  double beta;
+};
+constexpr int kEwBlocks = 148 * 8;   // fixed grid of the elementwise CG kernels (fixed-order partial sums)
+
+cudaError_t launch_commutator(const double* M, double* C, uint16_t* abs_planes, int d_pad, cudaStream_t st);
+cudaError_t launch_cg_init(const double* Fp, double* R, double* P, double* E, double* partial, int d_pad,
+                           cudaStream_t st, int* n_partial);
+cudaError_t launch_cg_pw(const double* P, const double* W, double* partial, int d_pad, cudaStream_t st);
+cudaError_t launch_cg_scalar(CgScalars* sc, const double* partial, int n_partial, int which, cudaStream_t st);
+cudaError_t launch_cg_update(double* E, double* R, const double* P, const double* W, const CgScalars* sc,
+                             double* partial, int d_pad, cudaStream_t st, int* n_partial);
+cudaError_t launch_cg_direction(double* P, const double* R, const CgScalars* sc, uint16_t* p_planes, int d_pad,
+                                cudaStream_t st);
+cudaError_t launch_apply_correction(double* X, const double* E, int d_pad, cudaStream_t st);
 
 // Product kernel parameters: C_IJ = sum_k P[I,k] Q[J,k] on upper tiles (I <= J).
 struct ProdParams {
@@ -62,7 +87,10 @@ struct ProdParams {
 // ---------------- mixed path (tcgen05 BF16x3, ns_mixed.cu) ----------------
 constexpr int kMxBK = 64;                       // bf16 per k-block: 128 B = one swizzle row
 constexpr int kMxStages = 6;
-constexpr int kMxThreads = 192;                 // warp 0 TMA, warp 1 MMA, warps 2..5 epilogue
+constexpr int kMxEpiWarps = 8;
+constexpr int kMxEpiThreads = 32 * kMxEpiWarps;
+constexpr int kMxThreads = 64 + kMxEpiThreads;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
+constexpr int kMxChunkKb = 16;                  // k-blocks (x64) per FP32 accumulation chunk = K 1024
 constexpr int kMxStageBytes = 2 * kTile * kMxBK * 2;   // 32 KB
 constexpr int kMxSmemBytes = kMxStages * kMxStageBytes + 1024 + 256;
 

@@ -9,9 +9,12 @@
 // FP64 kernel (Y + residual, NS update + trace, bitwise-symmetric mirrored writes), and also
 // re-emits the BF16 planes of its output for the next product.
 //
-// CTA = 6 warps: warp 0 TMA producer, warp 1 MMA issuer (one elected lane; owns the TMEM
-// allocation), warps 2..5 epilogue (warp w reads TMEM lane quadrant w % 4).  128x128 output tile,
-// UMMA M=128 N=128 K=16, 6-stage ring of 32 KB (A and B: 128 rows x 64 bf16, 128-B swizzle).
+// CTA = 10 warps: warp 0 TMA producer, warp 1 MMA issuer (one elected lane; owns the TMEM
+// allocation), warps 2..9 epilogue (warp w reads TMEM lane quadrant w % 4, column half (w-2)/4).
+// 128x128 output tile, UMMA M=128 N=128 K=16, 6-stage ring of 32 KB (A and B: 128 rows x 64 bf16,
+// 128-B swizzle).  The extended K (3d) is cut into chunks of kMxChunkKb*64; each chunk accumulates
+// in FP32 into one of two 128-column TMEM buffers while the epilogue folds the previous chunk into
+// FP64 registers, so FP32 accumulation error is bounded by the chunk length (C16 accuracy budget).
 #include <cuda_bf16.h>
 
 #include <cmath>
@@ -48,7 +51,7 @@ __global__ void __launch_bounds__(kMxThreads, 1)
     ns_mx_product_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
                          const MxParams p) {
   const int job = blockIdx.y;
-  if (p.state != nullptr && p.state[job].done) return;
+  if (p.state != nullptr && (p.state[job].done || p.state[job].sw)) return;   // low-precision phase over
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -56,24 +59,29 @@ __global__ void __launch_bounds__(kMxThreads, 1)
   uint8_t* sB = smem + kMxStages * kTile * kMxBK * 2;        // [stages][128 x 64 bf16]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kMxStages * kMxStageBytes);
   uint64_t* empty = full + kMxStages;
-  uint64_t* tmem_full = empty + kMxStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
-  __shared__ double red[4];
+  uint64_t* tfull = empty + kMxStages;     // [2] accumulator chunk ready (MMA -> epilogue)
+  uint64_t* tempty = tfull + 2;            // [2] accumulator drained (epilogue -> MMA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  __shared__ double red[kMxEpiWarps];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int2 tile = p.tiles[blockIdx.x];
   const int I = tile.x, J = tile.y;
   const int nkb_total = 3 * p.nkb;
+  const int n_chunks = (nkb_total + kMxChunkKb - 1) / kMxChunkKb;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kMxStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], kMxEpiWarps);
+    }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 128);
+  if (warp == 1) tmem_alloc(tmem_slot, 2 * kTile);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -99,35 +107,58 @@ __global__ void __launch_bounds__(kMxThreads, 1)
     // idesc: D=F32 (bits 4-5 = 1), A=B=BF16 (bits 7-9, 10-12 = 1), K-major, N=128 (>>3 at 17), M=128 (>>4 at 24)
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTile >> 3) << 17) |
                            ((uint32_t)(kTile >> 4) << 24);
-    for (int kb = 0; kb < nkb_total; ++kb) {
-      const int s = kb % kMxStages;
-      mbar_wait(&full[s], static_cast<uint32_t>(kb / kMxStages) & 1u);
+    // K is cut into chunks of kMxChunkKb k-blocks; each chunk accumulates in FP32 into one of two TMEM
+    // buffers, and the epilogue warps fold finished chunks into FP64 registers (FP32 accumulation error
+    // then grows with the chunk length, not with 3*d).
+    for (int c = 0; c < n_chunks; ++c) {
+      const int b = c & 1;
+      if (c >= 2) mbar_wait(&tempty[b], static_cast<uint32_t>((c >> 1) - 1) & 1u);
       tc_fence_after();
-      if (lane == 0) {
-        const uint32_t a0 = smem_u32(sA + s * kTile * kMxBK * 2);
-        const uint32_t b0 = smem_u32(sB + s * kTile * kMxBK * 2);
+      const uint32_t acc = tmem + (uint32_t)(b * kTile);
+      const int kb0 = c * kMxChunkKb, kb1 = min(nkb_total, kb0 + kMxChunkKb);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        const int s = kb % kMxStages;
+        mbar_wait(&full[s], static_cast<uint32_t>(kb / kMxStages) & 1u);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a0 = smem_u32(sA + s * kTile * kMxBK * 2);
+          const uint32_t b0 = smem_u32(sB + s * kTile * kMxBK * 2);
 #pragma unroll
-        for (int k = 0; k < kMxBK / 16; ++k)
-          umma_bf16(tmem, sdesc_k128(a0 + k * 32), sdesc_k128(b0 + k * 32), idesc, (kb | k) != 0);
-        umma_commit(&empty[s]);
-        if (kb == nkb_total - 1) umma_commit(tmem_full);
+          for (int k = 0; k < kMxBK / 16; ++k)
+            umma_bf16(acc, sdesc_k128(a0 + k * 32), sdesc_k128(b0 + k * 32), idesc, (kb != kb0) || (k != 0));
+          umma_commit(&empty[s]);
+          if (kb == kb1 - 1) umma_commit(&tfull[b]);
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
   } else {
-    // ---------------- epilogue: TMEM -> FP64 -> smem staging -> global ----------------
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
-    const int q = warp & 3;                 // TMEM lane quadrant of this warp
-    const int r = q * 32 + lane;            // tile row owned by this thread
-    double* S = reinterpret_cast<double*>(smem);   // [128][kEpiPitch]; the ring is idle once tmem_full fired
-#pragma unroll 1
-    for (int c0 = 0; c0 < kTile; c0 += 32) {
-      uint32_t v[32];
-      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
+    // ---------------- epilogue: fold FP32 chunks into FP64 registers ----------------
+    const int q = warp & 3;                        // TMEM lane quadrant of this warp
+    const int h = (warp - 2) >> 2;                 // column half: 0 -> cols 0..63, 1 -> 64..127
+    const int r = q * 32 + lane;                   // tile row owned by this thread
+    double accd[64];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) S[r * kEpiPitch + c0 + i] = (double)__uint_as_float(v[i]);
+    for (int i = 0; i < 64; ++i) accd[i] = 0.0;
+    for (int c = 0; c < n_chunks; ++c) {
+      const int b = c & 1;
+      mbar_wait(&tfull[b], static_cast<uint32_t>(c >> 1) & 1u);
+      tc_fence_after();
+#pragma unroll
+      for (int c0 = 0; c0 < 64; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * kTile + h * 64 + c0), v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) accd[c0 + i] += (double)__uint_as_float(v[i]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[b]);
     }
+    // the ring is idle once the last chunk landed: stage the FP64 tile for the coalesced passes
+    double* S = reinterpret_cast<double*>(smem);   // [128][kEpiPitch]
+#pragma unroll
+    for (int i = 0; i < 64; ++i) S[r * kEpiPitch + h * 64 + i] = accd[i];
   }
   // all roles: ring no longer in use (epilogue wrote S only after the last MMA completed)
   tc_fence_before();
@@ -135,7 +166,7 @@ __global__ void __launch_bounds__(kMxThreads, 1)
 
   if (warp >= 2) {
     double* S = reinterpret_cast<double*>(smem);
-    const int tid = threadIdx.x - 64;       // 0..127
+    const int tid = threadIdx.x - 64;       // 0..255
     const long long ld = p.ld;
     const long long base = (long long)job * p.job_stride;
     double* C = p.C + base;
@@ -154,25 +185,25 @@ __global__ void __launch_bounds__(kMxThreads, 1)
       }
     };
     if (MODE == 2) {
-      for (int idx = tid; idx < kTile * kTile; idx += 128) {
+      for (int idx = tid; idx < kTile * kTile; idx += kMxEpiThreads) {
         const int rr = idx >> 7, cc = idx & 127;
         put((long long)(I * kTile + rr) * ld + J * kTile + cc, S[rr * kEpiPitch + cc]);
       }
     } else if (MODE == 0) {
       if (!diag) {
-        for (int idx = tid; idx < kTile * kTile; idx += 128) {
+        for (int idx = tid; idx < kTile * kTile; idx += kMxEpiThreads) {
           const int rr = idx >> 7, cc = idx & 127;
           const double v = S[rr * kEpiPitch + cc];
           put((long long)(I * kTile + rr) * ld + J * kTile + cc, v);
           part += v * v;
         }
         part *= 2.0;
-        for (int idx = tid; idx < kTile * kTile; idx += 128) {
+        for (int idx = tid; idx < kTile * kTile; idx += kMxEpiThreads) {
           const int rr = idx >> 7, cc = idx & 127;
           put((long long)(J * kTile + rr) * ld + I * kTile + cc, S[cc * kEpiPitch + rr]);
         }
       } else {
-        for (int idx = tid; idx < kTile * kTile; idx += 128) {
+        for (int idx = tid; idx < kTile * kTile; idx += kMxEpiThreads) {
           const int rr = idx >> 7, cc = idx & 127;
           const double v = (rr <= cc) ? S[rr * kEpiPitch + cc] : S[cc * kEpiPitch + rr];
           put((long long)(I * kTile + rr) * ld + I * kTile + cc, v);
@@ -187,20 +218,20 @@ __global__ void __launch_bounds__(kMxThreads, 1)
     } else {  // MODE 1: X_{j+1} = 1.5 X_j - 0.5 Z
       const double* X = p.Xold + base;
       if (!diag) {
-        for (int idx = tid; idx < kTile * kTile; idx += 128) {
+        for (int idx = tid; idx < kTile * kTile; idx += kMxEpiThreads) {
           const int rr = idx >> 7, cc = idx & 127;
           const long long g = (long long)(I * kTile + rr) * ld + J * kTile + cc;
           const double v = fma(-0.5, S[rr * kEpiPitch + cc], 1.5 * X[g]);
           put(g, v);
           S[rr * kEpiPitch + cc] = v;
         }
-        named_bar_sync(1, 128);
-        for (int idx = tid; idx < kTile * kTile; idx += 128) {
+        named_bar_sync(1, kMxEpiThreads);
+        for (int idx = tid; idx < kTile * kTile; idx += kMxEpiThreads) {
           const int rr = idx >> 7, cc = idx & 127;
           put((long long)(J * kTile + rr) * ld + I * kTile + cc, S[cc * kEpiPitch + rr]);
         }
       } else {
-        for (int idx = tid; idx < kTile * kTile; idx += 128) {
+        for (int idx = tid; idx < kTile * kTile; idx += kMxEpiThreads) {
           const int rr = idx >> 7, cc = idx & 127;
           if (rr <= cc) {
             const long long g = (long long)(I * kTile + rr) * ld + I * kTile + cc;
@@ -209,8 +240,8 @@ __global__ void __launch_bounds__(kMxThreads, 1)
             if (rr == cc && I * kTile + rr < p.d) part += v;
           }
         }
-        named_bar_sync(1, 128);
-        for (int idx = tid; idx < kTile * kTile; idx += 128) {
+        named_bar_sync(1, kMxEpiThreads);
+        for (int idx = tid; idx < kTile * kTile; idx += kMxEpiThreads) {
           const int rr = idx >> 7, cc = idx & 127;
           put((long long)(I * kTile + rr) * ld + I * kTile + cc,
               (rr <= cc) ? S[rr * kEpiPitch + cc] : S[cc * kEpiPitch + rr]);
@@ -221,16 +252,18 @@ __global__ void __launch_bounds__(kMxThreads, 1)
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
       if (lane == 0) red[warp - 2] = part;
-      named_bar_sync(1, 128);
+      named_bar_sync(1, kMxEpiThreads);
       if (tid == 0) {
-        const double s = ((red[0] + red[1]) + red[2]) + red[3];
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < kMxEpiWarps; ++w) s += red[w];
         if (MODE == 0) p.partial[(long long)job * p.n_tiles + blockIdx.x] = s;
         else if (diag) p.partial[(long long)job * (p.ld / kTile) + I] = s;
       }
     }
   }
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, 128);
+  if (warp == 1) tmem_dealloc(tmem, 2 * kTile);
 }
 
 cudaError_t launch_split_planes(const double* X, uint16_t* planes, int d_pad, int batch, cudaStream_t st) {

@@ -258,3 +258,74 @@ def test_mixed_product_kernel(nsr, d, mode):
         assert np.array_equal(C, C.T)
     C64 = nsr.ns_symm_product(Ag, Bg, mode=mode).cpu().numpy()
     assert np.max(np.abs(C64 - ref)) <= 1e-13 * np.max(np.abs(ref)) * math.sqrt(d)
+
+
+# ------------------------------------------------------------------ mixed path (a6-a8)
+def _mixed(nsr, p, **opts):
+    Hg = torch.from_numpy(p.H).to(_dev()) if p.H is not None else p.extra["Hg"]
+    o = nsr.ns_options(**opts) if opts else None
+    R, res = nsr.ns_reflector(Hg, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode, prec=nsr.NS_PREC_MIXED_BF16X3,
+                              options=o)
+    return R, res
+
+
+@pytest.mark.parametrize("d,k", [(512, 32), (1024, 64)])
+def test_mixed_cfg3_recipe(nsr, d, k):
+    """north_star: mixed before polish <= 1e-4, after polish <= 1e-10 of the oracle, identical steps and cert."""
+    p = workloads.cfg3_dense(d=d, k=k)
+    o = ons.ns_reflector(p.H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode, trace_residuals=True)
+    Rpre, rpre = _mixed(nsr, p, stop_at_switch=1)
+    pre = checks.frob_per_sqrt_d(Rpre.cpu().numpy(), o["R"])
+    assert pre <= 1e-4, pre
+    R, res = _mixed(nsr, p)
+    err = checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"])
+    print(f"mixed d={d}: switch j={res['switch_step']} pre={pre:.3e} post={err:.3e} steps={res['steps']}")
+    assert res["switch_step"] == rpre["steps"] and 0 < res["switch_step"] < o["steps"]
+    assert res["steps"] == o["steps"] and res["cert"] == o["cert"] == p.k
+    assert res["flags"] == o["flags"] == ons.CONVERGED
+    assert err <= TOL_R, err
+    assert torch.equal(R, R.T)
+
+
+def test_mixed_fixed30(nsr):
+    p = workloads.cfg3_dense(d=512, k=32, mode="fixed30")
+    o = ons.ns_reflector(p.H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    R, res = _mixed(nsr, p)
+    assert res["steps"] == 30 and res["flags"] == o["flags"] == ons.MAX_STEPS
+    assert checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= TOL_R
+
+
+def test_mixed_without_reanchor_floors(nsr):
+    """C16: polishing alone (cg_iters = 0) converges to sgn(X_switch), not sgn(A): the error floors
+    far above 1e-10 -- the reason the re-anchor exists."""
+    p = workloads.cfg3_dense(d=512, k=32)
+    o = ons.ns_reflector(p.H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    R, res = _mixed(nsr, p, cg_iters=0)
+    err = checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"])
+    R2, _ = _mixed(nsr, p)
+    err2 = checks.frob_per_sqrt_d(R2.cpu().numpy(), o["R"])
+    print(f"polish only {err:.3e}, with re-anchor {err2:.3e}")
+    assert err > 1e-9 and err2 < err / 100
+
+
+def test_mixed_cfg0(nsr):
+    p = workloads.cfg0_controlled(seed=0)
+    o = ons.ns_reflector(p.H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    R, res = _mixed(nsr, p)
+    assert res["steps"] == o["steps"] and res["cert"] == 3
+    assert checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= TOL_R
+
+
+def test_mixed_cfg3_full_size_sampled(nsr):
+    """configs[3] mixed mode at d=16384: steps == prediction, cert 1024, sampled columns vs closed form."""
+    p = workloads.cfg3_dense(form=False)
+    p.extra["Hg"] = workloads.householder_form_fast(p.Vh, p.lam, device=_dev())
+    R, res = _mixed(nsr, p)
+    steps_pred = scalar.predict_run((p.lam - p.s) / p.alpha, 100, 1e-10, True)[0]
+    assert res["steps"] == steps_pred and res["cert"] == 1024 and res["flags"] == ons.CONVERGED
+    cols = np.array([0, 3, 5000, 16383])
+    Rc = closed_form.householder_reflector_columns(p.Vh, p.lam, 0.0, cols)
+    Rg = R[:, torch.as_tensor(cols, device=_dev())].cpu().numpy()
+    err = np.sqrt(np.mean(np.sum((Rg - Rc) ** 2, axis=0)))
+    print(f"mixed d=16384: switch j={res['switch_step']} err~{err:.3e}")
+    assert err <= 1e-10
