@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="tol", choices=["tol", "fixed30"])
+    ap.add_argument("--prec", default="fp64", choices=["fp64", "mixed"],
+                    help="fp64: DMMA path (headline); mixed: BF16x3 tcgen05 -> re-anchor -> FP64 (configs[3] mixed)")
+    ap.add_argument("--no-mixed", action="store_true", help="skip the secondary mixed-mode measurement")
     ap.add_argument("--d", type=int, default=16384)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -175,8 +178,14 @@ def run_ours(args):
     wsbuf = nsr.alloc_workspace(nsr.ns_workspace_bytes(d), dev)
     stream = torch.cuda.current_stream(dev)
 
-    def call():
-        return nsr.ns_reflector(H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode, R=R, ws=wsbuf, stream=stream)
+    prec = nsr.NS_PREC_FP64 if args.prec == "fp64" else nsr.NS_PREC_MIXED_BF16X3
+    if prec != nsr.NS_PREC_FP64:
+        wsbuf = nsr.alloc_workspace(nsr.ns_workspace_bytes(d, prec), dev)
+
+    def call(pr=None):
+        pr = prec if pr is None else pr
+        return nsr.ns_reflector(H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode, R=R, ws=wsbuf, stream=stream,
+                                prec=pr)
 
     for _ in range(max(3, args.warmup)):
         _, res = call()
@@ -239,7 +248,8 @@ def run_ours(args):
         Hh = H.cpu().pin_memory()
         Rh = torch.empty((d, d), dtype=torch.float64).pin_memory()
         wsh = wsbuf
-        nsr.ns_reflector_host(Hh, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode, R=Rh, ws=wsh, stream=stream)
+        nsr.ns_reflector_host(Hh, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode, R=Rh, ws=wsh, stream=stream,
+                              prec=prec)
         if pg:
             pg.barrier()
         torch.cuda.synchronize(dev)
@@ -248,7 +258,7 @@ def run_ours(args):
         f0.record(stream)
         for _ in range(args.steps):
             _, rh = nsr.ns_reflector_host(Hh, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode, R=Rh, ws=wsh,
-                                          stream=stream)
+                                          stream=stream, prec=prec)
         f1.record(stream)
         torch.cuda.synchronize(dev)
         ems = f0.elapsed_time(f1)
@@ -260,6 +270,25 @@ def run_ours(args):
                "unit": "TFLOP/s", "h2d_bytes_per_step": d * d * 8, "d2h_bytes_per_step": d * d * 8,
                "ms_per_step": ems / args.steps, "entry": "ns_reflector_host (pinned host H, R)"}
         del Hh, Rh
+
+    # ---- secondary: the same reflector through the mixed BF16x3 -> re-anchor -> FP64 mode
+    mixed = None
+    if args.prec == "fp64" and not args.no_mixed:
+        wsbuf = nsr.alloc_workspace(nsr.ns_workspace_bytes(d, nsr.NS_PREC_MIXED_BF16X3), dev)
+        _, rm = call(nsr.NS_PREC_MIXED_BF16X3)
+        torch.cuda.synchronize(dev)
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            _, rm = call(nsr.NS_PREC_MIXED_BF16X3)
+        g1.record(stream)
+        torch.cuda.synchronize(dev)
+        mms = g0.elapsed_time(g1) / args.steps
+        mixed = {"time_to_R_ms": mms, "value": (2 * rm["steps"] + 1) * float(d) ** 3 / (mms * 1e-3) / 1e12,
+                 "unit": "TFLOP/s (FP64-equivalent algorithmic)", "steps": rm["steps"], "switch_step": rm["switch_step"],
+                 "pre_polish_residual": rm["pre_polish_residual"], "cert": rm["cert"], "flags": rm["flags"],
+                 "speedup_vs_fp64": (ms / args.steps) / mms, "launches": rm["launches"]}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -283,6 +312,7 @@ def run_ours(args):
             "result": {"steps": steps_ns, "cert": results[-1]["cert"], "flags": results[-1]["flags"],
                        "residual": results[-1]["residual"]},
             "gpu_launches": launches, "clocks": clocks, "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
+            "mixed_mode": mixed, "precision": args.prec,
         }
         print(json.dumps(line), flush=True)
     if pg:
