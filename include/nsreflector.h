@@ -175,6 +175,36 @@ ns_status_t ns_reflector_batched(const double* H, int64_t d, int64_t batch, int6
                                  ns_result_t* outs);
 
 /*
+ * ---------------- multi-GPU (one process per GPU, NCCL over NVLink/NVSwitch) ----------------
+ * configs[4] (d = 49152) on P GPUs.  Every rank keeps the full FP64 iterate and
+ * computes only its share of the upper 128x128 tiles of each symmetric product (tile t of the
+ * library's upper-tile order belongs to rank t % P); after each product the ranks exchange their
+ * tiles with one ncclAllGather and the per-rank residual sums with a second (P doubles, summed in
+ * rank order so every rank takes the identical stop decision).
+ *
+ * ns_comm_get_unique_id  rank 0 creates the 128-byte NCCL id (ship it to the other ranks, e.g.
+ *                        with torch.distributed.broadcast).
+ * ns_comm_init           every rank, with its CUDA device current; collective (blocks until all
+ *                        ranks joined).  nranks >= 1 (1 = single-GPU communicator).
+ * ns_shard_plan          host-only: the (I, J) tile pairs rank `rank` computes for dimension d
+ *                        (tiles_ij[2*i], tiles_ij[2*i+1]); returns the count via n_out; writes at
+ *                        most `cap` pairs.  Lets callers/tests check balance and coverage.
+ * ns_reflector_sharded   same arguments and result as ns_reflector (FP64 only); H (full, upper
+ *                        triangle read) and R (full) are device buffers on every rank; all ranks
+ *                        must call it with identical scalars.  The workspace must hold
+ *                        ns_workspace_bytes_sharded(d, nranks) bytes.
+ */
+typedef struct ns_comm ns_comm_t;
+ns_status_t ns_comm_get_unique_id(uint8_t id[128]);
+ns_status_t ns_comm_init(int rank, int nranks, const uint8_t id[128], ns_comm_t** comm);
+ns_status_t ns_comm_destroy(ns_comm_t* comm);
+ns_status_t ns_shard_plan(int64_t d, int nranks, int rank, int32_t* tiles_ij, int32_t cap, int32_t* n_out);
+size_t ns_workspace_bytes_sharded(int64_t d, int nranks);
+ns_status_t ns_reflector_sharded(ns_comm_t* comm, const double* H, int64_t d, int64_t ldh, double s, double alpha,
+                                 int32_t k, int32_t max_steps, double tol, ns_tolmode_t tm, double* R, int64_t ldr,
+                                 void* ws, size_t ws_bytes, void* stream, ns_result_t* out);
+
+/*
  * ns_symm_product — kernel-level entry used by tests (the contraction core alone).
  * A and B are symmetric (only their upper triangles are read); A, B, C device, d x d,
  * leading dim ld (same for all).

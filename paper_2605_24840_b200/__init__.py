@@ -23,7 +23,8 @@ EXPORTED_SYMBOLS = (
     "ns_workspace_bytes", "ns_workspace_bytes_batched", "ns_workspace_bytes_host", "ns_reflector",
     "ns_reflector_host", "ns_reflector_batched", "ns_symm_product", "ns_build_info", "ns_status_string",
     "ns_last_error", "ns_profile_enable", "ns_profile_reset", "ns_profile_get", "ns_options_default",
-    "ns_reflector_ex",
+    "ns_reflector_ex", "ns_comm_get_unique_id", "ns_comm_init", "ns_comm_destroy", "ns_shard_plan",
+    "ns_workspace_bytes_sharded", "ns_reflector_sharded",
 )
 
 
@@ -94,6 +95,19 @@ def load_library(path=LIB_PATH):
     lib.ns_profile_reset.restype = None
     lib.ns_profile_get.argtypes = [ctypes.POINTER(NsProfile)]
     lib.ns_profile_get.restype = None
+    lib.ns_comm_get_unique_id.restype = ctypes.c_int
+    lib.ns_comm_get_unique_id.argtypes = [ctypes.c_char_p]
+    lib.ns_comm_init.restype = ctypes.c_int
+    lib.ns_comm_init.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(c_vp)]
+    lib.ns_comm_destroy.restype = ctypes.c_int
+    lib.ns_comm_destroy.argtypes = [c_vp]
+    lib.ns_shard_plan.restype = ctypes.c_int
+    lib.ns_shard_plan.argtypes = [c_i64, ctypes.c_int, ctypes.c_int, c_vp, c_i32, ctypes.POINTER(c_i32)]
+    lib.ns_workspace_bytes_sharded.restype = c_sz
+    lib.ns_workspace_bytes_sharded.argtypes = [c_i64, ctypes.c_int]
+    lib.ns_reflector_sharded.restype = ctypes.c_int
+    lib.ns_reflector_sharded.argtypes = [c_vp, c_vp, c_i64, c_i64, c_dbl, c_dbl, c_i32, c_i32, c_dbl, ctypes.c_int,
+                                         c_vp, c_i64, c_vp, c_sz, c_vp, ctypes.POINTER(NsResult)]
     _lib = lib
     return lib
 
@@ -255,6 +269,57 @@ def ns_profile_get():
     load_library().ns_profile_get(ctypes.byref(p))
     return dict(n_square=p.n_square, n_update=p.n_update, ms_square=p.ms_square, ms_update=p.ms_update,
                 n_calls=p.n_calls)
+
+
+def ns_comm_get_unique_id():
+    """128-byte NCCL unique id (rank 0 creates it; broadcast it to the other ranks)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().ns_comm_get_unique_id(buf))
+    return buf.raw
+
+
+def ns_comm_init(rank, nranks, uid):
+    """NCCL communicator for the sharded path (collective across ranks; current CUDA device)."""
+    h = ctypes.c_void_p()
+    _check(load_library().ns_comm_init(int(rank), int(nranks), bytes(uid), ctypes.byref(h)))
+    return h
+
+
+def ns_comm_destroy(comm):
+    _check(load_library().ns_comm_destroy(comm))
+
+
+def ns_shard_plan(d, nranks, rank):
+    """(n, 2) int32 array of the (I, J) upper tiles rank `rank` computes (host-only)."""
+    lib = load_library()
+    n = ctypes.c_int32()
+    _check(lib.ns_shard_plan(int(d), int(nranks), int(rank), None, 0, ctypes.byref(n)))
+    out = np.zeros((max(n.value, 1), 2), dtype=np.int32)
+    _check(lib.ns_shard_plan(int(d), int(nranks), int(rank), out.ctypes.data, n.value, ctypes.byref(n)))
+    return out[:n.value]
+
+
+def ns_workspace_bytes_sharded(d, nranks):
+    return load_library().ns_workspace_bytes_sharded(d, nranks)
+
+
+def ns_reflector_sharded(comm, H, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_ABS, R=None, ws=None, stream=None,
+                         nranks=None):
+    """Multi-GPU reflector (every rank passes the full H; every rank receives the full R)."""
+    torch = _torch()
+    lib = load_library()
+    _require_cuda_f64(H, "H")
+    d = H.shape[0]
+    if R is None:
+        R = torch.empty((d, d), dtype=torch.float64, device=H.device)
+    if ws is None:
+        ws = alloc_workspace(lib.ns_workspace_bytes_sharded(d, nranks or 1), H.device)
+    res = NsResult()
+    st = lib.ns_reflector_sharded(comm, ctypes.c_void_p(H.data_ptr()), d, H.stride(0), float(s), float(alpha), int(k),
+                                  int(max_steps), float(tol), int(tol_mode), ctypes.c_void_p(R.data_ptr()), R.stride(0),
+                                  ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream), ctypes.byref(res))
+    _check(st)
+    return R, res.as_dict()
 
 
 def build_info():

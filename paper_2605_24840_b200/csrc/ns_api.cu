@@ -15,6 +15,7 @@
 
 #include "../../include/nsreflector.h"
 #include "ns_internal.h"
+#include <nccl.h>
 
 using namespace nsr;
 
@@ -480,6 +481,130 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
   return NS_OK;
 }
 
+// ---------------- sharded (multi-GPU) path ----------------
+struct ShardLayout {
+  Layout base;
+  int nranks = 1, rank = 0, n_my = 0, n_my_max = 0;
+  size_t off_my = 0, off_send = 0, off_recv = 0, off_rsend = 0, off_rrecv = 0, total = 0;
+};
+
+ShardLayout make_shard_layout(int64_t d, int nranks, int rank) {
+  ShardLayout S;
+  S.base = make_layout(d, 1, false);
+  S.nranks = nranks;
+  S.rank = rank;
+  const int nt = S.base.n_tiles;
+  S.n_my_max = (nt + nranks - 1) / nranks;
+  S.n_my = (nt - rank + nranks - 1) / nranks;   // tiles t = rank, rank + P, ...
+  size_t o = S.base.total;
+  const size_t tile_bytes = (size_t)kTile * kTile * sizeof(double);
+  S.off_my = o; o = align256(o + sizeof(int2) * (size_t)S.n_my_max);
+  S.off_send = o; o = align256(o + tile_bytes * (size_t)S.n_my_max);
+  S.off_recv = o; o = align256(o + tile_bytes * (size_t)S.n_my_max * (size_t)nranks);
+  S.off_rsend = o; o = align256(o + sizeof(double));
+  S.off_rrecv = o; o = align256(o + sizeof(double) * (size_t)nranks);
+  S.total = o;
+  return S;
+}
+
+std::vector<int2> shard_tiles(const std::vector<int2>& all, int nranks, int rank) {
+  std::vector<int2> v;
+  for (size_t t = (size_t)rank; t < all.size(); t += (size_t)nranks) v.push_back(all[t]);
+  return v;
+}
+
+#define NS_NCCL(x)                                                                                  \
+  do {                                                                                              \
+    ncclResult_t r_ = (x);                                                                          \
+    if (r_ != ncclSuccess) return fail(NS_ERR_NCCL, "%s failed: %s", #x, ncclGetErrorString(r_)); \
+  } while (0)
+
+ns_status_t run_sharded(ncclComm_t comm, const ShardLayout& SL, uint8_t* ws, const double* H, long long ldh,
+                        const JobParams& jp, int32_t max_steps, double tol, ns_tolmode_t tm, double* R, long long ldr,
+                        cudaStream_t st, DevState& out_state, int* launches) {
+  const Layout& L = SL.base;
+  double* Xa = reinterpret_cast<double*>(ws + L.off_xa);
+  double* Xb = reinterpret_cast<double*>(ws + L.off_xb);
+  double* Y = reinterpret_cast<double*>(ws + L.off_y);
+  double* res = reinterpret_cast<double*>(ws + L.off_res);
+  double* trp = reinterpret_cast<double*>(ws + L.off_tr);
+  int2* tiles = reinterpret_cast<int2*>(ws + L.off_tiles);
+  int2* my = reinterpret_cast<int2*>(ws + SL.off_my);
+  double* send = reinterpret_cast<double*>(ws + SL.off_send);
+  double* recv = reinterpret_cast<double*>(ws + SL.off_recv);
+  double* rsend = reinterpret_cast<double*>(ws + SL.off_rsend);
+  double* rrecv = reinterpret_cast<double*>(ws + SL.off_rrecv);
+  JobParams* djobs = reinterpret_cast<JobParams*>(ws + L.off_jobs);
+  DevState* state = reinterpret_cast<DevState*>(ws + L.off_state);
+  int* n_active = reinterpret_cast<int*>(ws + L.off_active);
+  HostRing& rg = ring();
+  if (!rg.ok) return fail(NS_ERR_CUDA, "pinned status ring allocation failed");
+
+  std::vector<int2> tl = make_tiles(L.n);
+  std::vector<int2> mt = shard_tiles(tl, SL.nranks, SL.rank);
+  NS_CUDA(cudaMemcpyAsync(tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+  if (!mt.empty()) NS_CUDA(cudaMemcpyAsync(my, mt.data(), mt.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+  NS_CUDA(cudaMemcpyAsync(djobs, &jp, sizeof(JobParams), cudaMemcpyHostToDevice, st));
+  CUtensorMap tmA, tmB, tmY;
+  ns_status_t s;
+  if ((s = encode_map(&tmA, Xa, L.d_pad, 1)) != NS_OK) return s;
+  if ((s = encode_map(&tmB, Xb, L.d_pad, 1)) != NS_OK) return s;
+  if ((s = encode_map(&tmY, Y, L.d_pad, 1)) != NS_OK) return s;
+
+  const size_t per_rank = (size_t)SL.n_my_max * kTile * kTile;   // doubles per rank in the gather
+  const int n_my = (int)mt.size();
+  int nl = 0;
+  NS_CUDA(launch_zero_state(state, 1, n_active, st));
+  NS_CUDA(launch_init(H, ldh, 0, Xa, djobs, L.d, L.d_pad, 1, st));
+  NS_CUDA(launch_trace_partials(Xa, L.d, L.d_pad, 1, trp, st));
+  nl += 3;
+  LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0};
+  const int LA = 2;
+  const long long js = (long long)L.d_pad * L.d_pad;
+  for (int j = 0; j <= max_steps; ++j) {
+    if (j >= LA) {
+      const int slot = (j - LA) % 16;
+      NS_CUDA(cudaEventSynchronize(rg.ev[slot]));
+      if (rg.slots[slot] == 0) break;   // identical on every rank: decisions use identical bits
+    }
+    const bool odd = (j & 1) != 0;
+    double* Xc = odd ? Xb : Xa;
+    double* Xn = odd ? Xa : Xb;
+    const CUtensorMap& tmC = odd ? tmB : tmA;
+    // 1-4: own Y tiles, residual sum, exchange
+    ProdParams sq{my, n_my, L.d_pad / kBK, L.d, L.d_pad, js, Y, nullptr, res, state, 0};
+    if (n_my) NS_CUDA(launch_product(tmC, tmC, sq, 1, st));
+    NS_CUDA(launch_shard_sum(res, n_my, rsend, st));
+    NS_CUDA(launch_pack_tiles(Y, my, n_my, send, L.d_pad, st));
+    NS_NCCL(ncclAllGather(send, recv, per_rank, ncclDouble, comm, st));
+    NS_NCCL(ncclAllGather(rsend, rrecv, 1, ncclDouble, comm, st));
+    NS_CUDA(launch_unpack_tiles(Y, tiles, L.n_tiles, recv, (long long)per_rank, SL.n_my_max, SL.nranks, SL.rank,
+                                L.d_pad, st));
+    // 5: decide (identical on all ranks)
+    NS_CUDA(launch_decide(state, djobs, res, 0, trp, L.n, lp, 1, n_active, st, rrecv, SL.nranks));
+    nl += 5;
+    // 6: own X_{j+1} tiles, exchange, trace
+    if (j < max_steps) {
+      ProdParams up{my, n_my, L.d_pad / kBK, L.d, L.d_pad, js, Xn, Xc, trp, state, 1};
+      if (n_my) NS_CUDA(launch_product(tmC, tmY, up, 1, st));
+      NS_CUDA(launch_pack_tiles(Xn, my, n_my, send, L.d_pad, st));
+      NS_NCCL(ncclAllGather(send, recv, per_rank, ncclDouble, comm, st));
+      NS_CUDA(launch_unpack_tiles(Xn, tiles, L.n_tiles, recv, (long long)per_rank, SL.n_my_max, SL.nranks,
+                                  SL.rank, L.d_pad, st));
+      NS_CUDA(launch_trace_partials(Xn, L.d, L.d_pad, 1, trp, st));
+      nl += 4;
+    }
+    NS_CUDA(cudaMemcpyAsync(&rg.slots[j % 16], n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+    NS_CUDA(cudaEventRecord(rg.ev[j % 16], st));
+  }
+  NS_CUDA(launch_copy_out(Xa, Xb, L.d, L.d_pad, state, R, ldr, 0, 1, st));
+  nl += 1;
+  NS_CUDA(cudaMemcpyAsync(&out_state, state, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+  NS_CUDA(cudaStreamSynchronize(st));
+  if (launches) *launches = nl;
+  return NS_OK;
+}
+
 void fill_result(const DevState& s, int launches, ns_result_t* out) {
   out->kernel_launches = launches;
   out->switch_step = s.sw_step;
@@ -679,6 +804,92 @@ ns_status_t ns_symm_product(const double* A, const double* B, double* C, int64_t
   NS_CUDA(cudaMemcpy2DAsync(C, (size_t)ld * 8, Pc, (size_t)L.d_pad * 8, (size_t)d * 8, (size_t)d,
                             cudaMemcpyDeviceToDevice, cs));
   NS_CUDA(cudaStreamSynchronize(cs));
+  return NS_OK;
+}
+
+struct ns_comm {
+  ncclComm_t comm;
+  int rank;
+  int nranks;
+};
+
+ns_status_t ns_comm_get_unique_id(uint8_t id[128]) {
+  g_last_error.clear();
+  if (!id) return fail(NS_ERR_INVALID_ARG, "null id");
+  static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id size");
+  ncclUniqueId u;
+  NS_NCCL(ncclGetUniqueId(&u));
+  memcpy(id, &u, 128);
+  return NS_OK;
+}
+
+ns_status_t ns_comm_init(int rank, int nranks, const uint8_t id[128], ns_comm_t** comm) {
+  g_last_error.clear();
+  if (!id || !comm) return fail(NS_ERR_INVALID_ARG, "null argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(NS_ERR_INVALID_ARG, "bad rank/nranks");
+  ncclUniqueId u;
+  memcpy(&u, id, 128);
+  ns_comm_t* c = new ns_comm_t{nullptr, rank, nranks};
+  ncclResult_t r = ncclCommInitRank(&c->comm, nranks, u, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(NS_ERR_NCCL, "ncclCommInitRank failed: %s", ncclGetErrorString(r));
+  }
+  *comm = c;
+  return NS_OK;
+}
+
+ns_status_t ns_comm_destroy(ns_comm_t* comm) {
+  g_last_error.clear();
+  if (!comm) return NS_OK;
+  ncclResult_t r = ncclCommDestroy(comm->comm);
+  delete comm;
+  if (r != ncclSuccess) return fail(NS_ERR_NCCL, "ncclCommDestroy failed: %s", ncclGetErrorString(r));
+  return NS_OK;
+}
+
+ns_status_t ns_shard_plan(int64_t d, int nranks, int rank, int32_t* tiles_ij, int32_t cap, int32_t* n_out) {
+  g_last_error.clear();
+  if (d < 1 || d > 65536 || nranks < 1 || rank < 0 || rank >= nranks || !n_out)
+    return fail(NS_ERR_INVALID_ARG, "bad arguments");
+  const Layout L = make_layout(d, 1, false);
+  std::vector<int2> mt = shard_tiles(make_tiles(L.n), nranks, rank);
+  *n_out = (int32_t)mt.size();
+  for (int32_t i = 0; i < (int32_t)mt.size() && i < cap && tiles_ij; ++i) {
+    tiles_ij[2 * i] = mt[i].x;
+    tiles_ij[2 * i + 1] = mt[i].y;
+  }
+  return NS_OK;
+}
+
+size_t ns_workspace_bytes_sharded(int64_t d, int nranks) {
+  if (d < 1 || nranks < 1) return 0;
+  return make_shard_layout(d, nranks, 0).total;
+}
+
+ns_status_t ns_reflector_sharded(ns_comm_t* comm, const double* H, int64_t d, int64_t ldh, double s, double alpha,
+                                 int32_t k, int32_t max_steps, double tol, ns_tolmode_t tm, double* R, int64_t ldr,
+                                 void* ws, size_t ws_bytes, void* stream, ns_result_t* out) {
+  g_last_error.clear();
+  if (!comm) return fail(NS_ERR_INVALID_ARG, "null communicator");
+  ns_status_t st = check_common(d, max_steps, tol, tm, NS_PREC_FP64);
+  if (st != NS_OK) return st;
+  if (!H || !R || !ws || !out) return fail(NS_ERR_INVALID_ARG, "null pointer argument");
+  if (ldh < d || ldr < d) return fail(NS_ERR_INVALID_ARG, "leading dimensions must be >= d");
+  if (!std::isfinite(s)) return fail(NS_ERR_INVALID_ARG, "shift s must be finite");
+  if (!(alpha > 0.0) || !std::isfinite(alpha)) return fail(NS_ERR_INVALID_ARG, "alpha must be finite and > 0");
+  if (k < 0 || k > d) return fail(NS_ERR_INVALID_ARG, "k must lie in [0, d]");
+  if (R == H) return fail(NS_ERR_INVALID_ARG, "R must not alias H");
+  if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(NS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+  const ShardLayout SL = make_shard_layout(d, comm->nranks, comm->rank);
+  if (ws_bytes < SL.total)
+    return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, SL.total);
+  DevState ds;
+  int nl = 0;
+  st = run_sharded(comm->comm, SL, static_cast<uint8_t*>(ws), H, ldh, JobParams{s, alpha, k, 0}, max_steps, tol, tm,
+                   R, ldr, static_cast<cudaStream_t>(stream), ds, &nl);
+  if (st != NS_OK) return st;
+  fill_result(ds, nl, out);
   return NS_OK;
 }
 

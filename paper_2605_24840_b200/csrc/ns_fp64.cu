@@ -292,15 +292,20 @@ __device__ __forceinline__ double block_sum_fixed(const double* v, int n, double
 __global__ void __launch_bounds__(256) ns_decide_kernel(DevState* __restrict__ state, const JobParams* __restrict__ jobs,
                                                         const double* __restrict__ res_partial, int n_tiles,
                                                         const double* __restrict__ tr_partial, int n_diag,
-                                                        LoopParams lp, int* n_active) {
+                                                        LoopParams lp, int* n_active,
+                                                        const double* __restrict__ res_ranks, int nranks) {
   __shared__ double red[8];
   const int job = blockIdx.x;
   DevState* st = state + job;
   if (st->done) return;
   if (lp.switch_tol > 0.0 && st->sw) return;   // low-precision phase already left (look-ahead launch)
-  const double r2 = block_sum_fixed(res_partial + (long long)job * n_tiles, n_tiles, red);
+  double r2 = block_sum_fixed(res_partial + (long long)job * n_tiles, n_tiles, red);
   const double tr = block_sum_fixed(tr_partial + (long long)job * n_diag, n_diag, red);
   if (threadIdx.x != 0) return;
+  if (res_ranks != nullptr) {   // sharded: per-rank sums gathered over NCCL, summed in rank order
+    r2 = 0.0;
+    for (int q = 0; q < nranks; ++q) r2 += res_ranks[q];
+  }
   const double r = sqrt(r2);
   int flags = st->flags;
   int done = 0;
@@ -417,8 +422,9 @@ cudaError_t launch_product(const CUtensorMap& tmP, const CUtensorMap& tmQ, const
 
 cudaError_t launch_decide(DevState* state, const JobParams* jobs, const double* res_partial, int n_tiles,
                           const double* tr_partial, int n_diag, LoopParams lp, int batch, int* n_active,
-                          cudaStream_t st) {
-  ns_decide_kernel<<<batch, 256, 0, st>>>(state, jobs, res_partial, n_tiles, tr_partial, n_diag, lp, n_active);
+                          cudaStream_t st, const double* res_ranks, int nranks) {
+  ns_decide_kernel<<<batch, 256, 0, st>>>(state, jobs, res_partial, n_tiles, tr_partial, n_diag, lp, n_active,
+                                          res_ranks, nranks);
   return cudaGetLastError();
 }
 

@@ -124,7 +124,14 @@ cudaError_t launch_product(const CUtensorMap& tmP, const CUtensorMap& tmQ, const
                            cudaStream_t st);
 cudaError_t launch_decide(DevState* state, const JobParams* jobs, const double* res_partial, int n_tiles,
                           const double* tr_partial, int n_diag, LoopParams lp, int batch, int* n_active,
-                          cudaStream_t st);
+                          cudaStream_t st, const double* res_ranks = nullptr, int nranks = 0);
+
+// ---------------- sharded path (ns_shard.cu) ----------------
+cudaError_t launch_pack_tiles(const double* M, const int2* my_tiles, int n_my, double* send, int d_pad,
+                              cudaStream_t st);
+cudaError_t launch_unpack_tiles(double* M, const int2* all_tiles, int n_tiles, const double* recv, long long per_rank,
+                                int n_my_max, int nranks, int my_rank, int d_pad, cudaStream_t st);
+cudaError_t launch_shard_sum(const double* v, int n, double* out, cudaStream_t st);
 cudaError_t launch_copy_out(const double* Xa, const double* Xb, int d, int d_pad, const DevState* state,
                             double* R, long long ldr, long long r_stride, int batch, cudaStream_t st);
 cudaError_t launch_zero_state(DevState* state, int batch, int* n_active, cudaStream_t st);

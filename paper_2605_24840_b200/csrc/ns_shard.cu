@@ -1,0 +1,105 @@
+// Multi-GPU Newton–Schulz for large d (BASELINE configs[4]):
+// one process per GPU, NCCL over NVLink/NVSwitch.
+//
+// Partitioning: every rank keeps the full iterate X (replicated, 8 d_pad^2 bytes) but computes only
+// its share of the n(n+1)/2 upper 128x128 output tiles of each symmetric product:
+// rank r owns tiles t of the L2-ordered upper-tile list with t % P == r (balanced to one tile).
+// Per NS step:
+//   1. Y tiles (own) <- X X               ns_product_kernel<0> on the rank's tile list
+//   2. residual partials -> one double    ns_shard_sum_kernel (fixed order)
+//   3. pack own Y tiles, ncclAllGather     (tile-major buffer; every rank receives all tiles)
+//      + ncclAllGather of the P residual sums (summed in rank order: identical bits on all ranks)
+//   4. unpack the other ranks' tiles into Y, mirrored (Y_JI = Y_IJ^T)
+//   5. decide (identical on all ranks)
+//   6. X_{j+1} tiles (own) <- 1.5 X - 0.5 X Y, pack, all-gather, unpack; tr X_{j+1} locally.
+// Communication per step: 2 all-gathers of d^2/2 doubles (each rank receives (P-1)/P of them)
+// + 2 x P doubles; compute per rank 2 d^3 / P.  At d = 49152, P = 8: ~19 GB/step received vs
+// ~0.85 s of DMMA work per step (~3% on NVLink 5 before overlap).
+#include <cstdint>
+
+#include "ns_internal.h"
+#include "ns_ptx.cuh"
+
+namespace nsr {
+
+// Copy the rank's tiles (local list entries 0..n_my-1) of the d_pad x d_pad matrix M into the
+// tile-major send buffer (tile t -> send[t * 128*128 ...], row-major inside the tile).
+__global__ void __launch_bounds__(256) ns_pack_tiles_kernel(const double* __restrict__ M, const int2* __restrict__ my_tiles,
+                                                            double* __restrict__ send, int d_pad) {
+  const int2 tl = my_tiles[blockIdx.x];
+  const double* src = M + (long long)tl.x * kTile * d_pad + (long long)tl.y * kTile;
+  double* dst = send + (long long)blockIdx.x * kTile * kTile;
+  for (int i = threadIdx.x; i < kTile * kTile / 2; i += 256) {
+    const int r = (2 * i) >> 7, c = (2 * i) & 127;
+    const double2 v = *reinterpret_cast<const double2*>(src + (long long)r * d_pad + c);
+    *reinterpret_cast<double2*>(dst + (long long)r * kTile + c) = v;
+  }
+}
+
+// Scatter every other rank's gathered tiles into M, with the mirrored block for off-diagonal tiles.
+// grid = (n_my_max, P).  Global tile index of (local slot s, rank q) is s * P + q.
+__global__ void __launch_bounds__(256) ns_unpack_tiles_kernel(double* __restrict__ M, const int2* __restrict__ all_tiles,
+                                                              int n_tiles, const double* __restrict__ recv,
+                                                              long long per_rank, int nranks, int my_rank, int d_pad) {
+  __shared__ double t[32][33];
+  const int q = blockIdx.y, slot = blockIdx.x;
+  if (q == my_rank) return;
+  const long long gt = (long long)slot * nranks + q;
+  if (gt >= n_tiles) return;
+  const int2 tl = all_tiles[gt];
+  const double* src = recv + (long long)q * per_rank + (long long)slot * kTile * kTile;
+  double* dst = M + (long long)tl.x * kTile * d_pad + (long long)tl.y * kTile;
+  for (int i = threadIdx.x; i < kTile * kTile / 2; i += 256) {
+    const int r = (2 * i) >> 7, c = (2 * i) & 127;
+    *reinterpret_cast<double2*>(dst + (long long)r * d_pad + c) = *reinterpret_cast<const double2*>(src + r * kTile + c);
+  }
+  if (tl.x == tl.y) return;
+  // mirror: M[J*128 + c][I*128 + r] = tile[r][c], through 32x32 smem transposes
+  double* mdst = M + (long long)tl.y * kTile * d_pad + (long long)tl.x * kTile;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int bi = 0; bi < 4; ++bi)
+    for (int bj = 0; bj < 4; ++bj) {
+      __syncthreads();
+      for (int y = ty; y < 32; y += 8) t[y][tx] = src[(bi * 32 + y) * kTile + bj * 32 + tx];
+      __syncthreads();
+      for (int y = ty; y < 32; y += 8) mdst[(long long)(bj * 32 + y) * d_pad + bi * 32 + tx] = t[tx][y];
+    }
+}
+
+// out[0] = sum_{i < n} v[i] in a fixed order (one block).
+__global__ void __launch_bounds__(256) ns_shard_sum_kernel(const double* __restrict__ v, int n, double* out) {
+  __shared__ double red[8];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += 256) s += v[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    out[0] = t;
+  }
+}
+
+cudaError_t launch_pack_tiles(const double* M, const int2* my_tiles, int n_my, double* send, int d_pad,
+                              cudaStream_t st) {
+  if (n_my > 0) ns_pack_tiles_kernel<<<n_my, 256, 0, st>>>(M, my_tiles, send, d_pad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_tiles(double* M, const int2* all_tiles, int n_tiles, const double* recv, long long per_rank,
+                                int n_my_max, int nranks, int my_rank, int d_pad, cudaStream_t st) {
+  if (nranks > 1 && n_my_max > 0) {
+    dim3 grid(n_my_max, nranks);
+    ns_unpack_tiles_kernel<<<grid, 256, 0, st>>>(M, all_tiles, n_tiles, recv, per_rank, nranks, my_rank, d_pad);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shard_sum(const double* v, int n, double* out, cudaStream_t st) {
+  ns_shard_sum_kernel<<<1, 256, 0, st>>>(v, n, out);
+  return cudaGetLastError();
+}
+
+}  // namespace nsr

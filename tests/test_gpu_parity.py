@@ -329,3 +329,40 @@ def test_mixed_cfg3_full_size_sampled(nsr):
     err = np.sqrt(np.mean(np.sum((Rg - Rc) ** 2, axis=0)))
     print(f"mixed d=16384: switch j={res['switch_step']} err~{err:.3e}")
     assert err <= 1e-10
+
+
+# ------------------------------------------------------------------ sharded path (a10), single-rank communicator
+@pytest.fixture(scope="module")
+def comm1(nsr):
+    uid = nsr.ns_comm_get_unique_id()
+    c = nsr.ns_comm_init(0, 1, uid)
+    yield c
+    nsr.ns_comm_destroy(c)
+
+
+def test_sharded_p1_matches_single_and_oracle(nsr, comm1):
+    p = workloads.cfg3_dense(d=1024, k=64)
+    Hg = torch.from_numpy(p.H).to(_dev())
+    Rs, rs = nsr.ns_reflector_sharded(comm1, Hg, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    Rd, rd = nsr.ns_reflector(Hg, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    assert torch.equal(Rs, Rd)
+    for key in ("steps", "flags", "residual", "trace", "cert"):
+        assert rs[key] == rd[key], key
+    o = ons.ns_reflector(p.H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    assert rs["steps"] == o["steps"] and rs["cert"] == o["cert"]
+    assert checks.frob_per_sqrt_d(Rs.cpu().numpy(), o["R"]) <= TOL_R
+
+
+def test_sharded_cfg4_subproblem(nsr, comm1):
+    """configs[4] oracle sub-problem (C14): d=4096, k=341, 32 Householders, margins +-0.02."""
+    p = workloads.cfg4_sharded(d=4096, k=341, form=False)
+    Hg = workloads.householder_form_fast(p.Vh, p.lam, device=_dev())
+    R, res = nsr.ns_reflector_sharded(comm1, Hg, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    steps_pred = scalar.predict_run((p.lam - p.s) / p.alpha, 100, 1e-10, True)[0]
+    assert res["steps"] == steps_pred and res["cert"] == 341 and res["flags"] == ons.CONVERGED
+    cols = np.array([0, 17, 2048, 4095])
+    Rc = closed_form.householder_reflector_columns(p.Vh, p.lam, 0.0, cols)
+    Rg = R[:, torch.as_tensor(cols, device=_dev())].cpu().numpy()
+    assert np.max(np.abs(Rg - Rc)) <= 1e-12
+    o = ons.ns_reflector(Hg.cpu().numpy(), p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    assert o["steps"] == res["steps"] and checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= TOL_R
