@@ -228,9 +228,19 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
   HostRing& rg = ring();
   if (!rg.ok) return fail(NS_ERR_CUDA, "pinned status ring allocation failed");
 
+  NS_CUDA(cudaMemcpyAsync(djobs, jobs.data(), jobs.size() * sizeof(JobParams), cudaMemcpyHostToDevice, st));
+  if (small_dpad(L.d) != 0) {
+    // d <= 96: one fused kernel (one CTA per problem runs the whole loop in shared memory)
+    LoopParams lps{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0, -1, 0};
+    NS_CUDA(launch_small(H, ldh, h_stride, djobs, lps, R, ldr, r_stride, state, batch, st));
+    states.resize(batch);
+    NS_CUDA(cudaMemcpyAsync(states.data(), state, sizeof(DevState) * batch, cudaMemcpyDeviceToHost, st));
+    NS_CUDA(cudaStreamSynchronize(st));
+    if (launches) *launches = 1;
+    return NS_OK;
+  }
   std::vector<int2> tl = make_tiles(L.n);
   NS_CUDA(cudaMemcpyAsync(tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
-  NS_CUDA(cudaMemcpyAsync(djobs, jobs.data(), jobs.size() * sizeof(JobParams), cudaMemcpyHostToDevice, st));
 
   CUtensorMap tmA, tmB, tmY;
   ns_status_t s;
@@ -245,7 +255,7 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
   Profiler& pf = prof();
   // event slots: 4 per step (square begin/end, update begin/end)
 
-  LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol};
+  LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0, -1, 0};
   const long long job_stride = (long long)L.d_pad * L.d_pad;
   // look-ahead: how many steps may be in flight before the host checks the counter
   const double step_flops = 2.0 * (double)L.n_tiles * kTile * kTile * (double)L.d_pad * batch;
@@ -373,7 +383,11 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
   nl += 4;
 
   // ---------------- phase 1: BF16x3 steps until the switch threshold ----------------
-  LoopParams lp_low{L.d, L.d_pad, max_steps, (int)tm, tol, opt.switch_tol > 0 ? opt.switch_tol : 1e-300};
+  // run-to-tolerance: switch at the first r_j/sqrt(d) < switch_tol (C16).  Fixed-step mode (tol = 0):
+  // low precision up to j = max_steps - kPolishSteps, then re-anchor and kPolishSteps FP64 steps.
+  const int kPolishSteps = 2;
+  const int switch_at = (tol == 0.0) ? std::max(0, max_steps - kPolishSteps) : -1;
+  LoopParams lp_low{L.d, L.d_pad, max_steps, (int)tm, tol, opt.switch_tol > 0 ? opt.switch_tol : 1e-300, switch_at, 1};
   const int LA = opt.lookahead > 0 ? std::min(opt.lookahead, 15) : 2;
   const long long js = (long long)L.d_pad * L.d_pad;
   for (int j = 0; j <= max_steps; ++j) {
@@ -447,7 +461,7 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
     nl += 1;
 
     // ---------------- phase 2: FP64 steps from j0 to tolerance ----------------
-    LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0};
+    LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0, -1, 0};
     const int one = 1;
     NS_CUDA(cudaMemcpyAsync(n_active, &one, sizeof(int), cudaMemcpyHostToDevice, st));
     for (int j = j0; j <= max_steps; ++j) {
@@ -558,7 +572,7 @@ ns_status_t run_sharded(ncclComm_t comm, const ShardLayout& SL, uint8_t* ws, con
   NS_CUDA(launch_init(H, ldh, 0, Xa, djobs, L.d, L.d_pad, 1, st));
   NS_CUDA(launch_trace_partials(Xa, L.d, L.d_pad, 1, trp, st));
   nl += 3;
-  LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0};
+  LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0, -1, 0};
   const int LA = 2;
   const long long js = (long long)L.d_pad * L.d_pad;
   for (int j = 0; j <= max_steps; ++j) {

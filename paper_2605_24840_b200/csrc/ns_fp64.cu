@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(256) ns_decide_kernel(DevState* __restrict__ s
   const int job = blockIdx.x;
   DevState* st = state + job;
   if (st->done) return;
-  if (lp.switch_tol > 0.0 && st->sw) return;   // low-precision phase already left (look-ahead launch)
+  if (lp.lowprec && st->sw) return;   // low-precision phase already left (look-ahead launch)
   double r2 = block_sum_fixed(res_partial + (long long)job * n_tiles, n_tiles, red);
   const double tr = block_sum_fixed(tr_partial + (long long)job * n_diag, n_diag, red);
   if (threadIdx.x != 0) return;
@@ -314,7 +314,10 @@ __global__ void __launch_bounds__(256) ns_decide_kernel(DevState* __restrict__ s
     flags |= 16;  // NS_F_NONFINITE
     done = 1;
   } else {
-    if (st->j > 0 && r > st->r_prev * (1.0 + 1e-12) + 1e-10 * sqd) flags |= 8;  // NS_F_SCALING_SUSPECT
+    // NS_F_SCALING_SUSPECT: a residual rise beyond the arithmetic's noise floor (FP64: 1e-10 sqrt(d);
+    // BF16x3 phase of the mixed path: 1e-4 sqrt(d), the split-precision floor).
+    const double slack = (lp.lowprec ? 1e-4 : 1e-10) * sqd;
+    if (st->j > 0 && r > st->r_prev * (1.0 + 1e-12) + slack) flags |= 8;
     const double rho = lp.tol_mode ? r / sqd : r;
     if (rho < lp.tol) {
       flags |= 1;  // NS_F_CONVERGED
@@ -322,11 +325,13 @@ __global__ void __launch_bounds__(256) ns_decide_kernel(DevState* __restrict__ s
     } else if (st->j >= lp.max_steps) {
       flags |= 2;  // NS_F_MAX_STEPS
       done = 1;
-    } else if (lp.switch_tol > 0.0 && !st->sw && r / sqd < lp.switch_tol) {
+    } else if (lp.lowprec && !st->sw &&
+               (lp.switch_at >= 0 ? st->j >= lp.switch_at : r / sqd < lp.switch_tol)) {
       // mixed path: leave the low-precision phase at this j (re-anchor + FP64 from here, C16)
       st->sw = 1;
       st->sw_step = st->j;
       st->sw_residual = r;
+      st->r_prev = INFINITY;   // the FP64 phase's first residual is not compared with a BF16x3 one
       st->residual = r;
       st->trace = tr;
       st->flags = flags;

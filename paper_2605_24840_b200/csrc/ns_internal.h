@@ -45,7 +45,9 @@ struct LoopParams {
   int max_steps;
   int tol_mode;        // 0 abs, 1 per sqrt(d)
   double tol;
-  double switch_tol;   // mixed path: leave the low-precision phase when r/sqrt(d) < switch_tol (0 = never)
+  double switch_tol;   // mixed path: leave the low-precision phase when r/sqrt(d) < switch_tol
+  int switch_at;       // mixed path, fixed-step mode: leave the low-precision phase at j == switch_at (-1: use switch_tol)
+  int lowprec;         // 1 while running the low-precision phase of the mixed path
 };
 
 // ---------------- re-anchor (ns_reanchor.cu) ----------------
@@ -125,6 +127,11 @@ cudaError_t launch_product(const CUtensorMap& tmP, const CUtensorMap& tmQ, const
 cudaError_t launch_decide(DevState* state, const JobParams* jobs, const double* res_partial, int n_tiles,
                           const double* tr_partial, int n_diag, LoopParams lp, int batch, int* n_active,
                           cudaStream_t st, const double* res_ranks = nullptr, int nranks = 0);
+
+// ---------------- small-d fused path (ns_small.cu): d <= 96, whole loop in one CTA per problem ----------------
+int small_dpad(int d);
+cudaError_t launch_small(const double* H, long long ldh, long long h_stride, const JobParams* jobs, LoopParams lp,
+                         double* R, long long ldr, long long r_stride, DevState* state, int batch, cudaStream_t st);
 
 // ---------------- sharded path (ns_shard.cu) ----------------
 cudaError_t launch_pack_tiles(const double* M, const int2* my_tiles, int n_my, double* send, int d_pad,

@@ -366,3 +366,24 @@ def test_sharded_cfg4_subproblem(nsr, comm1):
     assert np.max(np.abs(Rg - Rc)) <= 1e-12
     o = ons.ns_reflector(Hg.cpu().numpy(), p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
     assert o["steps"] == res["steps"] and checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= TOL_R
+
+
+def test_small_path_batched(nsr):
+    """d <= 96 runs the fused one-CTA-per-problem kernel; batched problems stop independently."""
+    probs = []
+    for seed in range(6):
+        probs.append(workloads.cfg0_controlled(seed=seed, d=[64, 64, 96, 50, 96, 33][seed], k=[3, 5, 7, 2, 40, 1][seed]))
+    for dd in sorted({p.d for p in probs}):
+        group = [p for p in probs if p.d == dd]
+        H = torch.from_numpy(np.stack([p.H for p in group])).to(_dev())
+        R, outs = nsr.ns_reflector_batched(H, [p.s for p in group], [p.alpha for p in group], [p.k for p in group],
+                                           100, 1e-12)
+        assert all(o["launches"] == 1 for o in outs)
+        for i, p in enumerate(group):
+            o = ons.ns_reflector(p.H, p.s, p.alpha, p.k, 100, 1e-12, 0, trace_residuals=True)
+            Rn = R[i].cpu().numpy()
+            assert np.array_equal(Rn, Rn.T)
+            if not _tie_band(o["hist_residual"], 1e-12, o["steps"]):
+                assert outs[i]["steps"] == o["steps"] and outs[i]["flags"] == o["flags"]
+                assert checks.frob_per_sqrt_d(Rn, o["R"]) <= TOL_R
+            assert outs[i]["cert"] == p.k
