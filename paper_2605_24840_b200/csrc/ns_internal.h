@@ -88,12 +88,13 @@ struct ProdParams {
 
 // ---------------- mixed path (tcgen05 BF16x3, ns_mixed.cu) ----------------
 constexpr int kMxBK = 64;                       // bf16 per k-block: 128 B = one swizzle row
-constexpr int kMxStages = 6;
+constexpr int kMxStages = 3;
 constexpr int kMxEpiWarps = 8;
 constexpr int kMxEpiThreads = 32 * kMxEpiWarps;
 constexpr int kMxThreads = 64 + kMxEpiThreads;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
-constexpr int kMxChunkKb = 16;                  // k-blocks (x64) per FP32 accumulation chunk = K 1024
-constexpr int kMxStageBytes = 2 * kTile * kMxBK * 2;   // 32 KB
+constexpr int kMxChunkKb = 8;                   // k-blocks (x64) per FP32 accumulation chunk (x3 split terms)
+constexpr int kMxSlab = kTile * kMxBK * 2;      // one 128 x 64 bf16 operand slab = 16 KB
+constexpr int kMxStageBytes = 4 * kMxSlab;      // A_hi, A_lo, B_hi, B_lo = 64 KB
 constexpr int kMxSmemBytes = kMxStages * kMxStageBytes + 1024 + 256;
 
 // C_IJ = sum over the 3 split terms of P'_I Q'_J^T with P' = [P_hi P_lo P_hi], Q' = [Q_lo Q_hi Q_hi]

@@ -11,8 +11,9 @@
 //
 // CTA = 10 warps: warp 0 TMA producer, warp 1 MMA issuer (one elected lane; owns the TMEM
 // allocation), warps 2..9 epilogue (warp w reads TMEM lane quadrant w % 4, column half (w-2)/4).
-// 128x128 output tile, UMMA M=128 N=128 K=16, 6-stage ring of 32 KB (A and B: 128 rows x 64 bf16,
-// 128-B swizzle).  The extended K (3d) is cut into chunks of kMxChunkKb*64; each chunk accumulates
+// 128x128 output tile, UMMA M=128 N=128 K=16, 3-stage ring of 64 KB: each stage brings the hi and lo
+// slabs of both operands for one 64-wide k-block (each byte fetched once; the kernel is L2-bandwidth
+// bound) and feeds 12 UMMAs.  K is cut into chunks of kMxChunkKb*64; each chunk accumulates
 // in FP32 into one of two 128-column TMEM buffers while the epilogue folds the previous chunk into
 // FP64 registers, so FP32 accumulation error is bounded by the chunk length (C16 accuracy budget).
 #include <cuda_bf16.h>
@@ -55,8 +56,7 @@ __global__ void __launch_bounds__(kMxThreads, 1)
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;                                        // [stages][128 x 64 bf16]
-  uint8_t* sB = smem + kMxStages * kTile * kMxBK * 2;        // [stages][128 x 64 bf16]
+  // stage s holds four 16 KB slabs: A_hi, A_lo, B_hi, B_lo (128 rows x 64 bf16 each, 128-B swizzle)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kMxStages * kMxStageBytes);
   uint64_t* empty = full + kMxStages;
   uint64_t* tfull = empty + kMxStages;     // [2] accumulator chunk ready (MMA -> epilogue)
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kMxThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int2 tile = p.tiles[blockIdx.x];
   const int I = tile.x, J = tile.y;
-  const int nkb_total = 3 * p.nkb;
+  const int nkb_total = p.nkb;
   const int n_chunks = (nkb_total + kMxChunkKb - 1) / kMxChunkKb;
 
   if (threadIdx.x == 0) {
@@ -95,12 +95,12 @@ __global__ void __launch_bounds__(kMxThreads, 1)
         const int s = kb % kMxStages;
         const uint32_t use = kb / kMxStages;
         if (kb >= kMxStages) mbar_wait(&empty[s], (use & 1u) ^ 1u);
-        const int seg = kb / p.nkb, kk = kb - seg * p.nkb;
-        const int pa = (seg == 1) ? 1 : 0;   // segments: (hi,lo), (lo,hi), (hi,hi)
-        const int pb = (seg == 0) ? 1 : 0;
+        uint8_t* st = smem + s * kMxStageBytes;
         mbar_arrive_expect_tx(&full[s], kMxStageBytes);
-        tma_load_3d(sA + s * kTile * kMxBK * 2, &tmP, kk * kMxBK, I * kTile, 2 * job + pa, &full[s]);
-        tma_load_3d(sB + s * kTile * kMxBK * 2, &tmQ, kk * kMxBK, J * kTile, 2 * job + pb, &full[s]);
+        tma_load_3d(st + 0 * kMxSlab, &tmP, kb * kMxBK, I * kTile, 2 * job + 0, &full[s]);   // P_hi
+        tma_load_3d(st + 1 * kMxSlab, &tmP, kb * kMxBK, I * kTile, 2 * job + 1, &full[s]);   // P_lo
+        tma_load_3d(st + 2 * kMxSlab, &tmQ, kb * kMxBK, J * kTile, 2 * job + 0, &full[s]);   // Q_hi
+        tma_load_3d(st + 3 * kMxSlab, &tmQ, kb * kMxBK, J * kTile, 2 * job + 1, &full[s]);   // Q_lo
       }
     }
   } else if (warp == 1) {
@@ -121,11 +121,18 @@ __global__ void __launch_bounds__(kMxThreads, 1)
         mbar_wait(&full[s], static_cast<uint32_t>(kb / kMxStages) & 1u);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t a0 = smem_u32(sA + s * kTile * kMxBK * 2);
-          const uint32_t b0 = smem_u32(sB + s * kTile * kMxBK * 2);
+          const uint32_t ahi = smem_u32(smem + s * kMxStageBytes), alo = ahi + kMxSlab;
+          const uint32_t bhi = ahi + 2 * kMxSlab, blo = ahi + 3 * kMxSlab;
+          // the three split terms, small ones first: P_hi Q_lo^T + P_lo Q_hi^T + P_hi Q_hi^T
 #pragma unroll
           for (int k = 0; k < kMxBK / 16; ++k)
-            umma_bf16(acc, sdesc_k128(a0 + k * 32), sdesc_k128(b0 + k * 32), idesc, (kb != kb0) || (k != 0));
+            umma_bf16(acc, sdesc_k128(ahi + k * 32), sdesc_k128(blo + k * 32), idesc, (kb != kb0) || (k != 0));
+#pragma unroll
+          for (int k = 0; k < kMxBK / 16; ++k)
+            umma_bf16(acc, sdesc_k128(alo + k * 32), sdesc_k128(bhi + k * 32), idesc, 1u);
+#pragma unroll
+          for (int k = 0; k < kMxBK / 16; ++k)
+            umma_bf16(acc, sdesc_k128(ahi + k * 32), sdesc_k128(bhi + k * 32), idesc, 1u);
           umma_commit(&empty[s]);
           if (kb == kb1 - 1) umma_commit(&tfull[b]);
         }
