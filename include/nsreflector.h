@@ -103,6 +103,8 @@ typedef struct {
  *   stop_at_switch mixed path: return the pre-polish iterate X_switch as R (no re-anchor,
  *                  no FP64 steps); flags then carry neither CONVERGED nor MAX_STEPS.
  *   lookahead      steps enqueued before the host reads the stop flag (0 = default).
+ *   filter_a/b     the step X_{j+1} = a X_j + b X_j^3 (generic odd sign-preserving
+ *                  filters; with tol = 0 and max_steps = m it is the fixed-depth filter phi_m).
  */
 typedef struct {
   double switch_tol;
@@ -110,6 +112,8 @@ typedef struct {
   int32_t stop_at_switch;
   int32_t lookahead;
   int32_t reserved[3];
+  double filter_a;   /* odd cubic filter step X <- filter_a X + filter_b X^3 (eq:signpreserving P:278-289); */
+  double filter_b;   /* Newton–Schulz = (1.5, -0.5) (default).  FP64 paths only; mixed requires the default. */
 } ns_options_t;
 
 void ns_options_default(ns_options_t* opts);
@@ -173,6 +177,37 @@ ns_status_t ns_reflector_batched(const double* H, int64_t d, int64_t batch, int6
                                  int32_t max_steps, double tol, ns_tolmode_t tm, ns_precision_t prec,
                                  double* R, int64_t stride_r, void* ws, size_t ws_bytes, void* stream,
                                  ns_result_t* outs);
+
+/*
+ * ---------------- shift / scale setup (the step before the path) ----------------
+ * ns_scale_bound: alpha_out = ||H - sI||_inf = max_i (|H_ii - s| + sum_{j!=i} |H_ij|), the
+ *   Gershgorin / infinity-norm surrogate for ||H - sI||_2 (alg:ssr step 5 P:676-678; default
+ *   realization P:710-712; scaling discussion P:720-736).  Always >= ||H - sI||_2, so
+ *   (H - sI)/alpha_out has its spectrum in [-1, 1] (lem:NSsign).  Device H (upper triangle read),
+ *   device workspace >= ns_workspace_bytes_setup(d) bytes; alpha_out is host memory.  Also bounds the
+ *   endpoint drift of prop:reuse_refresh: |lambda_i(H') - lambda_i(H)| <= ||H' - H||_inf (Weyl).
+ * ns_shift_certificate (host only): prop:reuse_refresh.  Given endpoint estimates
+ *   lam_k_hat, lam_k1_hat with error <= eps, a shift s and a next-step drift bound delta:
+ *     margin_hat  = min(s - lam_k_hat, lam_k1_hat - s)
+ *     admissible  = margin_hat > eps           (true margin >= margin_lb = margin_hat - eps)
+ *     reuse_ok    = delta < margin_hat - eps   (true margin at the next iterate >= reuse_margin_lb)
+ *     midpoint    = (lam_k_hat + lam_k1_hat)/2, midpoint_ok = (lam_k1_hat - lam_k_hat)/2 > eps
+ */
+size_t ns_workspace_bytes_setup(int64_t d);
+ns_status_t ns_scale_bound(const double* H, int64_t d, int64_t ldh, double s, void* ws, size_t ws_bytes,
+                           void* stream, double* alpha_out);
+typedef struct {
+  double margin_hat;
+  double margin_lb;
+  double reuse_margin_lb;
+  double midpoint;
+  int32_t admissible;
+  int32_t reuse_ok;
+  int32_t midpoint_ok;
+  int32_t pad;
+} ns_shift_cert_t;
+ns_status_t ns_shift_certificate(double lam_k_hat, double lam_k1_hat, double eps, double s, double delta,
+                                 ns_shift_cert_t* out);
 
 /*
  * ---------------- multi-GPU (one process per GPU, NCCL over NVLink/NVSwitch) ----------------

@@ -24,7 +24,8 @@ EXPORTED_SYMBOLS = (
     "ns_reflector_host", "ns_reflector_batched", "ns_symm_product", "ns_build_info", "ns_status_string",
     "ns_last_error", "ns_profile_enable", "ns_profile_reset", "ns_profile_get", "ns_options_default",
     "ns_reflector_ex", "ns_comm_get_unique_id", "ns_comm_init", "ns_comm_destroy", "ns_shard_plan",
-    "ns_workspace_bytes_sharded", "ns_reflector_sharded",
+    "ns_workspace_bytes_sharded", "ns_reflector_sharded", "ns_workspace_bytes_setup", "ns_scale_bound",
+    "ns_shift_certificate",
 )
 
 
@@ -41,12 +42,19 @@ class NsResult(ctypes.Structure):
 
 class NsOptions(ctypes.Structure):
     _fields_ = [("switch_tol", ctypes.c_double), ("cg_iters", ctypes.c_int32), ("stop_at_switch", ctypes.c_int32),
-                ("lookahead", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
+                ("lookahead", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3), ("filter_a", ctypes.c_double),
+                ("filter_b", ctypes.c_double)]
 
 
 class NsProfile(ctypes.Structure):
     _fields_ = [("n_square", ctypes.c_int64), ("n_update", ctypes.c_int64), ("ms_square", ctypes.c_double),
                 ("ms_update", ctypes.c_double), ("n_calls", ctypes.c_int64)]
+
+
+class NsShiftCert(ctypes.Structure):
+    _fields_ = [("margin_hat", ctypes.c_double), ("margin_lb", ctypes.c_double), ("reuse_margin_lb", ctypes.c_double),
+                ("midpoint", ctypes.c_double), ("admissible", ctypes.c_int32), ("reuse_ok", ctypes.c_int32),
+                ("midpoint_ok", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
 class NsError(RuntimeError):
@@ -108,6 +116,12 @@ def load_library(path=LIB_PATH):
     lib.ns_reflector_sharded.restype = ctypes.c_int
     lib.ns_reflector_sharded.argtypes = [c_vp, c_vp, c_i64, c_i64, c_dbl, c_dbl, c_i32, c_i32, c_dbl, ctypes.c_int,
                                          c_vp, c_i64, c_vp, c_sz, c_vp, ctypes.POINTER(NsResult)]
+    lib.ns_workspace_bytes_setup.restype = c_sz
+    lib.ns_workspace_bytes_setup.argtypes = [c_i64]
+    lib.ns_scale_bound.restype = ctypes.c_int
+    lib.ns_scale_bound.argtypes = [c_vp, c_i64, c_i64, c_dbl, c_vp, c_sz, c_vp, ctypes.POINTER(c_dbl)]
+    lib.ns_shift_certificate.restype = ctypes.c_int
+    lib.ns_shift_certificate.argtypes = [c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, ctypes.POINTER(NsShiftCert)]
     _lib = lib
     return lib
 
@@ -320,6 +334,29 @@ def ns_reflector_sharded(comm, H, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_A
                                   ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream), ctypes.byref(res))
     _check(st)
     return R, res.as_dict()
+
+
+def ns_scale_bound(H, s, ws=None, stream=None):
+    """||H - sI||_inf on the device (Gershgorin alpha; upper triangle read)."""
+    lib = load_library()
+    _require_cuda_f64(H, "H")
+    d = H.shape[0]
+    if ws is None:
+        ws = alloc_workspace(lib.ns_workspace_bytes_setup(d), H.device)
+    out = ctypes.c_double()
+    _check(lib.ns_scale_bound(ctypes.c_void_p(H.data_ptr()), d, H.stride(0), float(s), ctypes.c_void_p(ws.data_ptr()),
+                              ws.numel(), _stream_ptr(stream), ctypes.byref(out)))
+    return out.value
+
+
+def ns_shift_certificate(lam_k_hat, lam_k1_hat, eps, s, delta=0.0):
+    """prop:reuse_refresh certificate (host-only C function)."""
+    c = NsShiftCert()
+    _check(load_library().ns_shift_certificate(float(lam_k_hat), float(lam_k1_hat), float(eps), float(s),
+                                               float(delta), ctypes.byref(c)))
+    return dict(margin_hat=c.margin_hat, margin_lb=c.margin_lb, reuse_margin_lb=c.reuse_margin_lb,
+                midpoint=c.midpoint, admissible=bool(c.admissible), reuse_ok=bool(c.reuse_ok),
+                midpoint_ok=bool(c.midpoint_ok))
 
 
 def build_info():

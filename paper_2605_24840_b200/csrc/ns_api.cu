@@ -208,12 +208,33 @@ ns_status_t check_common(int64_t d, int32_t max_steps, double tol, ns_tolmode_t 
   return NS_OK;
 }
 
+struct Opts {
+  double switch_tol = 1e-4;
+  int cg_iters = 24;
+  int stop_at_switch = 0;
+  int lookahead = 0;
+  double ca = 1.5, cb = -0.5;
+};
+
+Opts to_opts(const ns_options_t* o) {
+  Opts r;
+  if (o) {
+    r.switch_tol = o->switch_tol;
+    r.cg_iters = o->cg_iters;
+    r.stop_at_switch = o->stop_at_switch;
+    r.lookahead = o->lookahead;
+    r.ca = o->filter_a;
+    r.cb = o->filter_b;
+  }
+  return r;
+}
+
 // The step loop shared by the single, host and batched entry points.  H: batch matrices
 // at H + b*h_stride (ld ldh).  R likewise.  Returns per-job states in `states`.
 ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ldh, long long h_stride,
                      const std::vector<JobParams>& jobs, int32_t max_steps, double tol, ns_tolmode_t tm, double* R,
                      long long ldr, long long r_stride, cudaStream_t st, std::vector<DevState>& states,
-                     int* launches) {
+                     int* launches, const Opts& opt = Opts{}) {
   const int batch = (int)L.batch;
   double* Xa = reinterpret_cast<double*>(ws + L.off_xa);
   double* Xb = reinterpret_cast<double*>(ws + L.off_xb);
@@ -231,7 +252,7 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
   NS_CUDA(cudaMemcpyAsync(djobs, jobs.data(), jobs.size() * sizeof(JobParams), cudaMemcpyHostToDevice, st));
   if (small_dpad(L.d) != 0) {
     // d <= 96: one fused kernel (one CTA per problem runs the whole loop in shared memory)
-    LoopParams lps{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0, -1, 0};
+    LoopParams lps{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0, -1, 0, opt.ca, opt.cb};
     NS_CUDA(launch_small(H, ldh, h_stride, djobs, lps, R, ldr, r_stride, state, batch, st));
     states.resize(batch);
     NS_CUDA(cudaMemcpyAsync(states.data(), state, sizeof(DevState) * batch, cudaMemcpyDeviceToHost, st));
@@ -279,7 +300,7 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
     NS_CUDA(launch_decide(state, djobs, res, L.n_tiles, trp, L.n, lp, batch, n_active, st));
     nl += 2;
     if (j < max_steps) {
-      ProdParams up{tiles, L.n_tiles, L.d_pad / kBK, L.d, L.d_pad, job_stride, Xn, Xc, trp, state, 1};
+      ProdParams up{tiles, L.n_tiles, L.d_pad / kBK, L.d, L.d_pad, job_stride, Xn, Xc, trp, state, 1, opt.ca, opt.cb};
       if (pf.on) NS_CUDA(cudaEventRecord(pf.get(4 * j + 2), st));
       NS_CUDA(launch_product(tmC, tmY, up, batch, st));
       if (pf.on) NS_CUDA(cudaEventRecord(pf.get(4 * j + 3), st));
@@ -313,24 +334,6 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
     pf.acc.n_calls += 1;
   }
   return NS_OK;
-}
-
-struct Opts {
-  double switch_tol = 1e-4;
-  int cg_iters = 24;
-  int stop_at_switch = 0;
-  int lookahead = 0;
-};
-
-Opts to_opts(const ns_options_t* o) {
-  Opts r;
-  if (o) {
-    r.switch_tol = o->switch_tol;
-    r.cg_iters = o->cg_iters;
-    r.stop_at_switch = o->stop_at_switch;
-    r.lookahead = o->lookahead;
-  }
-  return r;
 }
 
 // Mixed path (single problem): BF16x3 tcgen05 steps -> switch -> re-anchor -> FP64 steps.
@@ -654,6 +657,8 @@ void ns_options_default(ns_options_t* o) {
   o->cg_iters = 24;
   o->stop_at_switch = 0;
   o->lookahead = 0;
+  o->filter_a = 1.5;
+  o->filter_b = -0.5;
 }
 
 ns_status_t ns_reflector_ex(const double* H, int64_t d, int64_t ldh, double s, double alpha, int32_t k,
@@ -676,6 +681,9 @@ ns_status_t ns_reflector_ex(const double* H, int64_t d, int64_t ldh, double s, d
     return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
   const Opts o = to_opts(opts);
   if (mixed && (!(o.switch_tol >= 0.0) || o.cg_iters < 0)) return fail(NS_ERR_INVALID_ARG, "bad mixed options");
+  if (!std::isfinite(o.ca) || !std::isfinite(o.cb)) return fail(NS_ERR_INVALID_ARG, "filter coefficients must be finite");
+  if (mixed && (o.ca != 1.5 || o.cb != -0.5))
+    return fail(NS_ERR_UNSUPPORTED, "the mixed path runs the Newton-Schulz step (1.5, -0.5) only");
   std::vector<JobParams> jobs{JobParams{s, alpha, k, 0}};
   int nl = 0;
   if (mixed) {
@@ -688,7 +696,7 @@ ns_status_t ns_reflector_ex(const double* H, int64_t d, int64_t ldh, double s, d
   }
   std::vector<DevState> states;
   st = run_loop(L, static_cast<uint8_t*>(ws), H, ldh, 0, jobs, max_steps, tol, tm, R, ldr, 0,
-                static_cast<cudaStream_t>(stream), states, &nl);
+                static_cast<cudaStream_t>(stream), states, &nl, o);
   if (st != NS_OK) return st;
   fill_result(states[0], nl, out);
   return NS_OK;
@@ -904,6 +912,43 @@ ns_status_t ns_reflector_sharded(ns_comm_t* comm, const double* H, int64_t d, in
                    R, ldr, static_cast<cudaStream_t>(stream), ds, &nl);
   if (st != NS_OK) return st;
   fill_result(ds, nl, out);
+  return NS_OK;
+}
+
+size_t ns_workspace_bytes_setup(int64_t d) { return d < 1 ? 0 : align256(sizeof(double) * (size_t)(d + 1)); }
+
+ns_status_t ns_scale_bound(const double* H, int64_t d, int64_t ldh, double s, void* ws, size_t ws_bytes,
+                           void* stream, double* alpha_out) {
+  g_last_error.clear();
+  if (!H || !ws || !alpha_out) return fail(NS_ERR_INVALID_ARG, "null pointer argument");
+  if (d < 1 || d > 65536 || ldh < d) return fail(NS_ERR_INVALID_ARG, "bad d / ldh");
+  if (!std::isfinite(s)) return fail(NS_ERR_INVALID_ARG, "shift must be finite");
+  if (ws_bytes < ns_workspace_bytes_setup(d)) return fail(NS_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  double* part = static_cast<double*>(ws);
+  double* dout = part + d;
+  NS_CUDA(launch_scale_bound(H, ldh, (int)d, s, part, dout, cs));
+  NS_CUDA(cudaMemcpyAsync(alpha_out, dout, sizeof(double), cudaMemcpyDeviceToHost, cs));
+  NS_CUDA(cudaStreamSynchronize(cs));
+  return NS_OK;
+}
+
+ns_status_t ns_shift_certificate(double lam_k_hat, double lam_k1_hat, double eps, double s, double delta,
+                                 ns_shift_cert_t* out) {
+  g_last_error.clear();
+  if (!out) return fail(NS_ERR_INVALID_ARG, "null output");
+  if (!std::isfinite(lam_k_hat) || !std::isfinite(lam_k1_hat) || !std::isfinite(s) || !(eps >= 0.0) ||
+      !(delta >= 0.0) || !std::isfinite(eps) || !std::isfinite(delta))
+    return fail(NS_ERR_INVALID_ARG, "estimates must be finite, eps and delta >= 0");
+  ns_shift_cert_t c{};
+  c.margin_hat = std::min(s - lam_k_hat, lam_k1_hat - s);
+  c.admissible = c.margin_hat > eps ? 1 : 0;
+  c.margin_lb = c.margin_hat - eps;
+  c.reuse_ok = (c.admissible && delta < c.margin_hat - eps) ? 1 : 0;
+  c.reuse_margin_lb = c.margin_hat - eps - delta;
+  c.midpoint = 0.5 * (lam_k_hat + lam_k1_hat);
+  c.midpoint_ok = (0.5 * (lam_k1_hat - lam_k_hat) > eps) ? 1 : 0;
+  *out = c;
   return NS_OK;
 }
 

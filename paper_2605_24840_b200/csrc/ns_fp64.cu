@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int idx = tid; idx < kTile * kTile; idx += 256) {
         const int r = idx >> 7, c = idx & 127;
         const long long gidx = (long long)(I * kTile + r) * ld + J * kTile + c;
-        const double v = fma(-0.5, S[r * kEpiPitch + c], 1.5 * X[gidx]);
+        const double v = fma(p.cb, S[r * kEpiPitch + c], p.ca * X[gidx]);
         C[gidx] = v;
         S[r * kEpiPitch + c] = v;
       }
@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int r = idx >> 7, c = idx & 127;
         if (r <= c) {
           const long long gidx = (long long)(I * kTile + r) * ld + I * kTile + c;
-          const double v = fma(-0.5, S[r * kEpiPitch + c], 1.5 * X[gidx]);
+          const double v = fma(p.cb, S[r * kEpiPitch + c], p.ca * X[gidx]);
           S[r * kEpiPitch + c] = v;
           if (r == c && I * kTile + r < p.d) part += v;
         }

@@ -48,6 +48,8 @@ struct LoopParams {
   double switch_tol;   // mixed path: leave the low-precision phase when r/sqrt(d) < switch_tol
   int switch_at;       // mixed path, fixed-step mode: leave the low-precision phase at j == switch_at (-1: use switch_tol)
   int lowprec;         // 1 while running the low-precision phase of the mixed path
+  double ca = 1.5;     // filter step coefficients (small fused kernel)
+  double cb = -0.5;
 };
 
 // ---------------- re-anchor (ns_reanchor.cu) ----------------
@@ -84,6 +86,8 @@ struct ProdParams {
   double* partial;         // mode 0: residual partial per (job, tile); mode 1: trace partial per (job, I) on diag tiles
   const DevState* state;   // per-job state; CTA exits if state[job].done (nullptr = never)
   int mode;                // 0 = square/plain product + residual, 1 = NS update + trace
+  double ca = 1.5;         // mode 1: X_{j+1} = ca X_j + cb X_j Y_j  (odd cubic filter step; NS: 1.5, -0.5)
+  double cb = -0.5;
 };
 
 // ---------------- mixed path (tcgen05 BF16x3, ns_mixed.cu) ----------------
@@ -133,6 +137,10 @@ cudaError_t launch_decide(DevState* state, const JobParams* jobs, const double* 
 int small_dpad(int d);
 cudaError_t launch_small(const double* H, long long ldh, long long h_stride, const JobParams* jobs, LoopParams lp,
                          double* R, long long ldr, long long r_stride, DevState* state, int batch, cudaStream_t st);
+
+// ---------------- shift/scale setup (ns_setup.cu) ----------------
+cudaError_t launch_scale_bound(const double* H, long long ldh, int d, double s, double* part, double* out,
+                               cudaStream_t st);
 
 // ---------------- sharded path (ns_shard.cu) ----------------
 cudaError_t launch_pack_tiles(const double* M, const int2* my_tiles, int n_my, double* send, int d_pad,

@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
     small_product<DP>(X, Y, Z);                     // Z = X_j Y_j
     for (int e = threadIdx.x; e < DP * DP; e += kSmallThreads) {
       const int i = e / DP, c = e % DP;
-      X[i * P + c] = fma(-0.5, Z[i * P + c], 1.5 * X[i * P + c]);
+      X[i * P + c] = fma(lp.cb, Z[i * P + c], lp.ca * X[i * P + c]);
     }
     __syncthreads();
     r_prev = r;

@@ -387,3 +387,47 @@ def test_small_path_batched(nsr):
                 assert outs[i]["steps"] == o["steps"] and outs[i]["flags"] == o["flags"]
                 assert checks.frob_per_sqrt_d(Rn, o["R"]) <= TOL_R
             assert outs[i]["cert"] == p.k
+
+
+# ------------------------------------------------------------------ N1 / N3: setup and filter variants
+def test_scale_bound_on_device(nsr):
+    from oracle import setup
+    rng = np.random.default_rng(11)
+    for d in (1, 37, 300, 1030):
+        A = rng.standard_normal((d, d))
+        A = 0.5 * (A + A.T)
+        s = float(rng.uniform(-1, 1))
+        got = nsr.ns_scale_bound(torch.from_numpy(A).to(_dev()), s)
+        ref = setup.inf_norm_shifted(A, s)
+        assert abs(got - ref) <= 1e-12 * ref, (d, got, ref)
+    prob = workloads.cfg2_allen_cahn(seed=0, n=32)
+    got = nsr.ns_scale_bound(torch.from_numpy(prob.H).to(_dev()), -0.5)
+    assert abs(got - setup.inf_norm_shifted(prob.H, -0.5)) <= 1e-12 * got
+
+
+@pytest.mark.parametrize("d", [64, 300])
+@pytest.mark.parametrize("coef", [(1.5, -0.5), (1.875, -0.875)])
+def test_fixed_depth_filters(nsr, d, coef):
+    """Fixed-depth filtered reflectors phi_m(alpha(H - sI)), m = 2, 4, 6: tol = 0,
+    max_steps = m; generic odd cubic step via ns_options.filter_a/b."""
+    from oracle import setup
+    p = workloads.cfg0_controlled(seed=4, d=d, k=max(1, d // 20))
+    Hg = torch.from_numpy(p.H).to(_dev())
+    for m in (2, 4, 6):
+        R, res = nsr.ns_reflector(Hg, p.s, p.alpha, p.k, m, 0.0, options=nsr.ns_options(filter_a=coef[0],
+                                                                                        filter_b=coef[1]))
+        Xo = setup.filter_fixed_depth(p.H, p.s, p.alpha, m, *coef)
+        assert res["steps"] == m and res["flags"] & ons.MAX_STEPS
+        assert checks.frob_per_sqrt_d(R.cpu().numpy(), Xo) <= 1e-13
+        mu = (p.lam - p.s) / p.alpha
+        Xcf = closed_form.spectral_matrix(p.Q, setup.filter_scalar(mu, m, *coef))
+        assert checks.frob_per_sqrt_d(R.cpu().numpy(), Xcf) <= 1e-13
+
+
+def test_raw_sign_shift_zero(nsr):
+    """prop:raw: s = 0 gives sgn(H); cfg0's spectrum has 0 inside the target gap."""
+    p = workloads.cfg0_controlled(seed=2)
+    a = float(np.max(np.abs(p.lam)))
+    R, res = nsr.ns_reflector(torch.from_numpy(p.H).to(_dev()), 0.0, a, 3, 100, 1e-12)
+    assert res["cert"] == 3
+    assert checks.frob_per_sqrt_d(R.cpu().numpy(), closed_form.reflector_explicit_q(p.Q, p.lam, 0.0)) <= 1e-13

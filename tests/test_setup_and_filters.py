@@ -1,0 +1,77 @@
+"""N1 (shift/scale setup) and N3 (filter variants): oracle pins on CPU, and the C library's
+host-only certificate against the oracle's transcription of prop:reuse_refresh."""
+import numpy as np
+import pytest
+
+from oracle import closed_form, setup, scalar
+import workloads
+
+
+def test_inf_norm_pins():
+    # diagonal: max |h_ii - s| ; Gershgorin: >= spectral norm; equals numpy's inf-norm
+    assert setup.inf_norm_shifted(np.diag([-3.0, 1.0, 2.5]), 0.5) == 3.5
+    rng = np.random.default_rng(3)
+    for d in (5, 40, 130):
+        A = rng.standard_normal((d, d))
+        A = 0.5 * (A + A.T)
+        s = float(rng.uniform(-1, 1))
+        v = setup.inf_norm_shifted(A, s)
+        assert v >= np.linalg.norm(A - s * np.eye(d), 2) - 1e-12
+        assert abs(v - np.linalg.norm(A - s * np.eye(d), np.inf)) <= 1e-12 * v
+
+
+def test_certificate_pins():
+    c = setup.shift_certificate(-1.0, 1.0, 0.1, 0.0, 0.5)
+    assert c["margin_hat"] == 1.0 and c["admissible"] and abs(c["margin_lb"] - 0.9) < 1e-15
+    assert c["reuse_ok"] and abs(c["reuse_margin_lb"] - 0.4) < 1e-15 and c["midpoint"] == 0.0
+    assert not setup.shift_certificate(-1.0, 1.0, 0.1, 0.0, 0.95)["reuse_ok"]
+    assert not setup.shift_certificate(-1.0, 1.0, 1.0, 0.0)["admissible"]      # m_hat == eps: not strict
+    assert not setup.shift_certificate(0.0, 0.1, 0.06, 0.05)["midpoint_ok"]
+    # brute force: any true endpoints within eps of the estimates, drifted by <= delta, keep s inside
+    rng = np.random.default_rng(0)
+    for _ in range(2000):
+        lk, lk1 = sorted(rng.uniform(-1, 1, 2))
+        eps, delta = rng.uniform(0, 0.2, 2)
+        s = rng.uniform(lk - 0.1, lk1 + 0.1)
+        c = setup.shift_certificate(lk, lk1, eps, s, delta)
+        tk = lk + rng.uniform(-eps, eps)
+        tk1 = lk1 + rng.uniform(-eps, eps)
+        if c["admissible"]:
+            assert tk < s < tk1 and min(s - tk, tk1 - s) >= c["margin_lb"] - 1e-15
+        if c["reuse_ok"]:
+            nk, nk1 = tk + rng.uniform(-delta, delta), tk1 + rng.uniform(-delta, delta)
+            assert nk < s < nk1 and min(s - nk, nk1 - s) >= c["reuse_margin_lb"] - 1e-15
+
+
+def test_c_certificate_matches_oracle():
+    from paper_2605_24840_b200 import build
+    build.build()
+    import paper_2605_24840_b200 as nsr
+    rng = np.random.default_rng(1)
+    for _ in range(500):
+        lk, lk1 = sorted(rng.uniform(-2, 2, 2))
+        eps, delta = rng.uniform(0, 0.5, 2)
+        s = rng.uniform(-2.5, 2.5)
+        a = setup.shift_certificate(lk, lk1, eps, s, delta)
+        b = nsr.ns_shift_certificate(lk, lk1, eps, s, delta)
+        assert a == b
+
+
+def test_filter_oracle_pins():
+    """Odd cubic filters: diagonal exactness and the closed form Q diag(phi^m(mu)) Q^T; NS is (1.5, -0.5)."""
+    h = np.array([-0.9, -0.2, 0.3, 0.7])
+    for (a, b) in ((1.5, -0.5), (1.875, -0.875), (1.0, 0.0)):
+        for m in (0, 2, 4, 6):
+            X = setup.filter_fixed_depth(np.diag(h), 0.1, 1.0, m, a, b)
+            assert np.max(np.abs(np.diag(X) - setup.filter_scalar(h - 0.1, m, a, b))) <= 1e-15
+    assert np.array_equal(setup.filter_scalar(0.5, 3, 1.5, -0.5), scalar.p_m(0.5, 3))
+    p = workloads.cfg0_controlled(seed=1)
+    for m in (2, 4, 6):
+        X = setup.filter_fixed_depth(p.H, p.s, p.alpha, m, 1.875, -0.875)
+        mu = (p.lam - p.s) / p.alpha
+        Xcf = closed_form.spectral_matrix(p.Q, setup.filter_scalar(mu, m, 1.875, -0.875))
+        assert np.max(np.abs(X - Xcf)) <= 1e-13
+    # sign preservation of the alternative filter on [-1, 1] (eq:signpreserving)
+    t = np.linspace(-1, 1, 2001)
+    t = t[t != 0]
+    assert np.all(np.sign(setup.filter_scalar(t, 5, 1.875, -0.875)) == np.sign(t))
