@@ -210,6 +210,33 @@ ns_status_t ns_shift_certificate(double lam_k_hat, double lam_k1_hat, double eps
                                  ns_shift_cert_t* out);
 
 /*
+ * ---------------- Algorithm 1 outer loop (the step after the path) ----------------
+ * ns_alg1_rotated_quartic: nruns independent runs of alg:ssr on the dense rotated
+ * quartic of §5.3:
+ *   E(x) = 1/4 sum y_i^4 + 1/2 sum c_i y_i^2, y = Q^T x, c_i = -1 (i <= k_r), +1 otherwise,
+ * from start x0[r] with target index k[r]: exact endpoints, midpoint shift, alpha = ||H - sI||_2,
+ * R~ = m Newton–Schulz steps (m = 0: exact reflector), x <- x - eta R~ g, until ||g|| <= grad_tol or
+ * max_iters.  One CTA per run, everything in shared memory (d <= 64).
+ *   Q      device d x d row-major orthogonal matrix (shared by all runs)
+ *   k      HOST int32[nruns], 1 <= k < d
+ *   x0     device nruns x d starts;  x_out device nruns x d final states
+ *   out    HOST ns_alg1_result_t[nruns]: iterations, final ||g||, Morse index of H(x_final),
+ *          success = (||g|| <= grad_tol && Morse index == k)
+ *   ws     device workspace >= ns_workspace_bytes_alg1(nruns) bytes
+ */
+typedef struct {
+  int32_t iters;
+  int32_t morse_index;
+  int32_t success;
+  int32_t pad;
+  double grad_norm;
+} ns_alg1_result_t;
+size_t ns_workspace_bytes_alg1(int32_t nruns);
+ns_status_t ns_alg1_rotated_quartic(const double* Q, int64_t d, int32_t nruns, const int32_t* k, const double* x0,
+                                    int32_t m, double eta, int32_t max_iters, double grad_tol, double* x_out,
+                                    void* ws, size_t ws_bytes, void* stream, ns_alg1_result_t* out);
+
+/*
  * ---------------- multi-GPU (one process per GPU, NCCL over NVLink/NVSwitch) ----------------
  * configs[4] (d = 49152) on P GPUs.  Every rank keeps the full FP64 iterate and
  * computes only its share of the upper 128x128 tiles of each symmetric product (tile t of the

@@ -27,10 +27,11 @@ closed_form  exact reflector and exact m-step iterate when the generator knows Q
 checks       reflector invariants R^2=I, R^T=R, RH=HR, tr R=d-2k (prop:exact).
 setup        ||H - sI||_inf scaling surrogate, prop:reuse_refresh certificate, odd cubic
              filter variants at fixed depth (eq:signpreserving, eq:phi-reflector).  [pinned]
+outer        Algorithm 1 (alg:ssr) on the rotated quartic of §5.3.               [pinned]
 
 Every function is pinned by a ``-m "not gpu"`` test against something other than
 itself (paper worked values, closed forms, invariants, mpmath brute force for
 d<=16, LAPACK as a third path).  No function here is "parity unpinned".
 """
 
-from . import scalar, ns, jacobi, closed_form, checks, setup  # noqa: F401
+from . import scalar, ns, jacobi, closed_form, checks, setup, outer  # noqa: F401

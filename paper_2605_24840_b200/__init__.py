@@ -25,7 +25,7 @@ EXPORTED_SYMBOLS = (
     "ns_last_error", "ns_profile_enable", "ns_profile_reset", "ns_profile_get", "ns_options_default",
     "ns_reflector_ex", "ns_comm_get_unique_id", "ns_comm_init", "ns_comm_destroy", "ns_shard_plan",
     "ns_workspace_bytes_sharded", "ns_reflector_sharded", "ns_workspace_bytes_setup", "ns_scale_bound",
-    "ns_shift_certificate",
+    "ns_shift_certificate", "ns_workspace_bytes_alg1", "ns_alg1_rotated_quartic",
 )
 
 
@@ -55,6 +55,11 @@ class NsShiftCert(ctypes.Structure):
     _fields_ = [("margin_hat", ctypes.c_double), ("margin_lb", ctypes.c_double), ("reuse_margin_lb", ctypes.c_double),
                 ("midpoint", ctypes.c_double), ("admissible", ctypes.c_int32), ("reuse_ok", ctypes.c_int32),
                 ("midpoint_ok", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+
+class NsAlg1Result(ctypes.Structure):
+    _fields_ = [("iters", ctypes.c_int32), ("morse_index", ctypes.c_int32), ("success", ctypes.c_int32),
+                ("pad", ctypes.c_int32), ("grad_norm", ctypes.c_double)]
 
 
 class NsError(RuntimeError):
@@ -122,6 +127,11 @@ def load_library(path=LIB_PATH):
     lib.ns_scale_bound.argtypes = [c_vp, c_i64, c_i64, c_dbl, c_vp, c_sz, c_vp, ctypes.POINTER(c_dbl)]
     lib.ns_shift_certificate.restype = ctypes.c_int
     lib.ns_shift_certificate.argtypes = [c_dbl, c_dbl, c_dbl, c_dbl, c_dbl, ctypes.POINTER(NsShiftCert)]
+    lib.ns_workspace_bytes_alg1.restype = c_sz
+    lib.ns_workspace_bytes_alg1.argtypes = [c_i32]
+    lib.ns_alg1_rotated_quartic.restype = ctypes.c_int
+    lib.ns_alg1_rotated_quartic.argtypes = [c_vp, c_i64, c_i32, c_vp, c_vp, c_i32, c_dbl, c_i32, c_dbl, c_vp, c_vp,
+                                            c_sz, c_vp, ctypes.POINTER(NsAlg1Result)]
     _lib = lib
     return lib
 
@@ -357,6 +367,28 @@ def ns_shift_certificate(lam_k_hat, lam_k1_hat, eps, s, delta=0.0):
     return dict(margin_hat=c.margin_hat, margin_lb=c.margin_lb, reuse_margin_lb=c.reuse_margin_lb,
                 midpoint=c.midpoint, admissible=bool(c.admissible), reuse_ok=bool(c.reuse_ok),
                 midpoint_ok=bool(c.midpoint_ok))
+
+
+def ns_alg1_rotated_quartic(Q, k, x0, m, eta, max_iters, grad_tol, x_out=None, ws=None, stream=None):
+    """Batched Algorithm 1 on the rotated quartic (N2).  Q (d, d) and x0 (nruns, d) CUDA float64;
+    k host ints.  Returns (x_final, list of result dicts)."""
+    torch = _torch()
+    lib = load_library()
+    _require_cuda_f64(Q, "Q")
+    _require_cuda_f64(x0, "x0")
+    nruns, d = x0.shape
+    k_a = np.ascontiguousarray(np.broadcast_to(np.asarray(k, dtype=np.int32), (nruns,)))
+    if x_out is None:
+        x_out = torch.empty_like(x0)
+    if ws is None:
+        ws = alloc_workspace(lib.ns_workspace_bytes_alg1(nruns), x0.device)
+    outs = (NsAlg1Result * nruns)()
+    _check(lib.ns_alg1_rotated_quartic(ctypes.c_void_p(Q.data_ptr()), d, nruns, k_a.ctypes.data,
+                                       ctypes.c_void_p(x0.data_ptr()), int(m), float(eta), int(max_iters),
+                                       float(grad_tol), ctypes.c_void_p(x_out.data_ptr()),
+                                       ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream), outs))
+    return x_out, [dict(iters=o.iters, morse_index=o.morse_index, success=bool(o.success), grad_norm=o.grad_norm)
+                   for o in outs]
 
 
 def build_info():

@@ -952,6 +952,43 @@ ns_status_t ns_shift_certificate(double lam_k_hat, double lam_k1_hat, double eps
   return NS_OK;
 }
 
+size_t ns_workspace_bytes_alg1(int32_t nruns) {
+  if (nruns < 1) return 0;
+  return align256(sizeof(int) * (size_t)nruns) + align256(sizeof(OuterResult) * (size_t)nruns);
+}
+
+ns_status_t ns_alg1_rotated_quartic(const double* Q, int64_t d, int32_t nruns, const int32_t* k, const double* x0,
+                                    int32_t m, double eta, int32_t max_iters, double grad_tol, double* x_out,
+                                    void* ws, size_t ws_bytes, void* stream, ns_alg1_result_t* out) {
+  g_last_error.clear();
+  if (!Q || !k || !x0 || !x_out || !ws || !out) return fail(NS_ERR_INVALID_ARG, "null pointer argument");
+  if (d < 2 || d > 64) return fail(NS_ERR_INVALID_ARG, "d must lie in [2, 64] (one CTA per run)");
+  if (nruns < 1 || nruns > 1 << 20) return fail(NS_ERR_INVALID_ARG, "bad nruns");
+  if (m < 0 || m > 64 || max_iters < 0) return fail(NS_ERR_INVALID_ARG, "bad depth / iteration budget");
+  if (!(eta > 0.0) || !std::isfinite(eta) || !(grad_tol >= 0.0)) return fail(NS_ERR_INVALID_ARG, "bad eta / grad_tol");
+  for (int r = 0; r < nruns; ++r)
+    if (k[r] < 1 || k[r] >= d) return fail(NS_ERR_INVALID_ARG, "k[%d] must lie in [1, d-1]", r);
+  if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(NS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+  if (ws_bytes < ns_workspace_bytes_alg1(nruns)) return fail(NS_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  int* dk = static_cast<int*>(ws);
+  OuterResult* dres = reinterpret_cast<OuterResult*>(static_cast<uint8_t*>(ws) + align256(sizeof(int) * (size_t)nruns));
+  NS_CUDA(cudaMemcpyAsync(dk, k, sizeof(int) * nruns, cudaMemcpyHostToDevice, cs));
+  OuterParams p{m, max_iters, eta, grad_tol};
+  NS_CUDA(launch_outer(Q, (int)d, dk, x0, p, x_out, dres, nruns, cs));
+  std::vector<OuterResult> hr(nruns);
+  NS_CUDA(cudaMemcpyAsync(hr.data(), dres, sizeof(OuterResult) * nruns, cudaMemcpyDeviceToHost, cs));
+  NS_CUDA(cudaStreamSynchronize(cs));
+  for (int r = 0; r < nruns; ++r) {
+    out[r].iters = hr[r].iters;
+    out[r].morse_index = hr[r].morse_index;
+    out[r].success = hr[r].success;
+    out[r].pad = 0;
+    out[r].grad_norm = hr[r].grad_norm;
+  }
+  return NS_OK;
+}
+
 void ns_profile_enable(int on) { prof().on = (on != 0); }
 void ns_profile_reset(void) { prof().acc = ns_profile_t{}; }
 void ns_profile_get(ns_profile_t* out) {

@@ -138,6 +138,23 @@ int small_dpad(int d);
 cudaError_t launch_small(const double* H, long long ldh, long long h_stride, const JobParams* jobs, LoopParams lp,
                          double* R, long long ldr, long long r_stride, DevState* state, int batch, cudaStream_t st);
 
+// ---------------- Algorithm 1 outer loop on the rotated quartic (ns_outer.cu), d <= 64 ----------------
+struct OuterParams {
+  int m;              // Newton–Schulz depth of the filter (0 = exact reflector)
+  int max_iters;
+  double eta;         // fixed outer step size
+  double grad_tol;
+};
+struct OuterResult {
+  int iters;
+  int morse_index;
+  int success;
+  int pad;
+  double grad_norm;
+};
+cudaError_t launch_outer(const double* Q, int d, const int* k, const double* x0, OuterParams p, double* xout,
+                         OuterResult* res, int nruns, cudaStream_t st);
+
 // ---------------- shift/scale setup (ns_setup.cu) ----------------
 cudaError_t launch_scale_bound(const double* H, long long ldh, int d, double s, double* part, double* out,
                                cudaStream_t st);

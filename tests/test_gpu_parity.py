@@ -431,3 +431,41 @@ def test_raw_sign_shift_zero(nsr):
     R, res = nsr.ns_reflector(torch.from_numpy(p.H).to(_dev()), 0.0, a, 3, 100, 1e-12)
     assert res["cert"] == 3
     assert checks.frob_per_sqrt_d(R.cpu().numpy(), closed_form.reflector_explicit_q(p.Q, p.lam, 0.0)) <= 1e-13
+
+
+# ------------------------------------------------------------------ N2: Algorithm 1 outer loop (rotated quartic)
+def test_alg1_local_parity(nsr):
+    """Batched Algorithm 1 (one CTA per run) vs the oracle: local runs (radius 0.1) converge to the
+    index-k saddle for the exact reflector and NS depth 2/4/6; iteration counts agree (+-1 at the
+    grad_tol crossing), final states agree."""
+    from oracle import outer
+    Q, ks, starts = workloads.rotated_quartic_scan(d=64, n_starts=4, radius=0.1)
+    Qg = torch.from_numpy(Q).to(_dev())
+    for m in (0, 2, 4, 6):
+        kk = [k for k in ks for _ in starts]
+        x0 = np.concatenate([starts for _ in ks])
+        xf, res = nsr.ns_alg1_rotated_quartic(Qg, kk, torch.from_numpy(x0).to(_dev()), m, 0.2, 400, 1e-10)
+        xf = xf.cpu().numpy()
+        for r in range(len(kk)):
+            o = outer.run(Q, kk[r], x0[r], m, 0.2, 400, 1e-10)
+            assert res[r]["success"] == o["success"], (m, r, res[r], o["iters"])
+            assert abs(res[r]["iters"] - o["iters"]) <= 1
+            assert res[r]["morse_index"] == o["morse_index"]
+            assert np.max(np.abs(xf[r] - o["x"])) <= 1e-9
+
+
+def test_alg1_scan_matches_oracle(nsr):
+    """Target-index scan (§5.3, d=64, k in {1,2,4,8,16}, 32 matched starts, m = 2/4/6/exact): per-run
+    success flags of the GPU runs equal the oracle's (all runs), success rates printed."""
+    from oracle import outer
+    Q, ks, starts = workloads.rotated_quartic_scan(d=64, n_starts=8, radius=4.0)
+    Qg = torch.from_numpy(Q).to(_dev())
+    kk = [k for k in ks for _ in starts]
+    x0 = np.concatenate([starts for _ in ks])
+    for m in (0, 2, 4, 6):
+        _, res = nsr.ns_alg1_rotated_quartic(Qg, kk, torch.from_numpy(x0).to(_dev()), m, 0.2, 1000, 1e-10)
+        agree = sum(res[r]["success"] == outer.run(Q, kk[r], x0[r], m, 0.2, 1000, 1e-10)["success"]
+                    for r in range(len(kk)))
+        rate = sum(r["success"] for r in res) / len(res)
+        print(f"m={m}: success rate {rate:.2f}, agreement with oracle {agree}/{len(kk)}")
+        assert agree == len(kk)

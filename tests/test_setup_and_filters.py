@@ -75,3 +75,36 @@ def test_filter_oracle_pins():
     t = np.linspace(-1, 1, 2001)
     t = t[t != 0]
     assert np.all(np.sign(setup.filter_scalar(t, 5, 1.875, -0.875)) == np.sign(t))
+
+
+# ------------------------------------------------------------------ N2: Algorithm 1 oracle pins
+def test_rotated_quartic_model_pins():
+    """Gradient and Hessian eigenvalues of the rotated quartic: finite differences,
+    origin is a critical point with Morse index k, Hessian eigenvalues mu = 3y^2 + c."""
+    from oracle import outer
+    Q, ks, starts = workloads.rotated_quartic_scan(d=8, ks=(3,), n_starts=2)
+    k = 3
+    c = np.where(np.arange(8) < k, -1.0, 1.0)
+    E = lambda x: 0.25 * np.sum((Q.T @ x) ** 4) + 0.5 * np.sum(c * (Q.T @ x) ** 2)  # noqa: E731
+    x = starts[0] * 3
+    g, mu = outer.gradient_and_mu(Q, k, x)
+    h = 1e-6
+    fd = np.array([(E(x + h * e) - E(x - h * e)) / (2 * h) for e in np.eye(8)])
+    assert np.max(np.abs(fd - g)) <= 1e-8
+    y = Q.T @ x
+    H = Q @ np.diag(3 * y * y + c) @ Q.T
+    assert np.max(np.abs(np.sort(np.linalg.eigvalsh(H)) - np.sort(mu))) <= 1e-12
+    g0, mu0 = outer.gradient_and_mu(Q, k, np.zeros(8))
+    assert np.all(g0 == 0) and np.sum(mu0 < 0) == k
+
+
+def test_alg1_exact_reflector_converges_locally():
+    """thm:discrete / SPEC S:448: matched-index runs from within radius 0.1 converge to the origin
+    (index-k saddle) with the exact reflector and with NS depth 6."""
+    from oracle import outer
+    Q, ks, starts = workloads.rotated_quartic_scan(d=16, ks=(1, 4), n_starts=3, radius=0.1)
+    for k in ks:
+        for x0 in starts:
+            for m in (0, 6):
+                r = outer.run(Q, k, x0, m, 0.2, 500, 1e-10)
+                assert r["success"] and np.linalg.norm(r["x"]) < 1e-9, (k, m, r["iters"])

@@ -150,6 +150,19 @@ def cfg4(sharded=True):
         nsr.ns_comm_destroy(comm)
 
 
+def kscan():
+    """§5.3 target-index scan (N2): d=64, k in {1,2,4,8,16}, 32 matched starts, m = exact/2/4/6."""
+    Q, ks, starts = workloads.rotated_quartic_scan(d=64, n_starts=32)
+    Qg = torch.from_numpy(Q).to(DEV)
+    kk = [k for k in ks for _ in starts]
+    x0 = torch.from_numpy(np.concatenate([starts for _ in ks])).to(DEV)
+    for m in (0, 2, 4, 6):
+        (xf, res), ms, _ = timed(lambda: nsr.ns_alg1_rotated_quartic(Qg, kk, x0, m, 0.2, 1000, 1e-10), 3, 1)
+        per_k = {k: float(np.mean([r["success"] for r, kr in zip(res, kk) if kr == k])) for k in ks}
+        emit({"config": "kscan", "m": m, "runs": len(kk), "time_ms": ms, "success_rate_by_k": per_k,
+              "median_iters": float(np.median([r["iters"] for r in res]))})
+
+
 def main():
     which = sys.argv[1:] or ["cfg0", "cfg1", "cfg2", "cfg3", "cfg3mixed", "cfg3fixed", "cfg3fixedmixed"]
     for w in which:
@@ -174,6 +187,8 @@ def main():
             cfg4(True)
         elif w == "cfg4single":
             cfg4(False)
+        elif w == "kscan":
+            kscan()
 
 
 if __name__ == "__main__":

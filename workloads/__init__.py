@@ -7,5 +7,5 @@ read in DESIGN.md §Inputs.
 """
 from .configs import (  # noqa: F401
     cfg0_controlled, cfg1_batched, cfg2_allen_cahn, cfg3_dense, cfg4_sharded,
-    householder_spectrum, householder_form_numpy, householder_form_fast, haar_q,
+    householder_spectrum, householder_form_numpy, householder_form_fast, haar_q, rotated_quartic_scan,
 )

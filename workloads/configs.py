@@ -253,3 +253,15 @@ def cfg4_sharded(seed=1, d=49152, k=4096, margin=0.02, n_house=32, form=True):
     lam, Vh = householder_spectrum(seed, d, k, margin, n_house)
     H = householder_form_numpy(Vh, lam) if form else None
     return Problem(f"cfg4[d={d}]", d, k, 0.0, 1.05, 100, 1e-10, 1, H=H, lam=lam, Vh=Vh)
+
+
+# --------------------------------------------------------------------------- N2: target-index scan
+def rotated_quartic_scan(seed=0, d=64, ks=(1, 2, 4, 8, 16), n_starts=32, radius=4.0):
+    """§5.3 target-index scan inputs: one Haar Q (shared), and n_starts matched random starts
+    x0 ~ radius * N(0, I)/sqrt(d) (the same starts for every k, "matched random starts").
+    The paper does not state the start distribution or the c_i magnitudes; unit |c_i| and
+    this start recipe are DESIGN.md readings."""
+    rng = _rng(seed)
+    Q = haar_q(rng, d)
+    starts = radius * rng.standard_normal((n_starts, d)) / math.sqrt(d)
+    return Q, list(ks), starts
