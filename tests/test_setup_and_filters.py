@@ -86,11 +86,11 @@ def test_rotated_quartic_model_pins():
     k = 3
     c = np.where(np.arange(8) < k, -1.0, 1.0)
     E = lambda x: 0.25 * np.sum((Q.T @ x) ** 4) + 0.5 * np.sum(c * (Q.T @ x) ** 2)  # noqa: E731
-    x = starts[0] * 3
+    x = starts[0]
     g, mu = outer.gradient_and_mu(Q, k, x)
     h = 1e-6
     fd = np.array([(E(x + h * e) - E(x - h * e)) / (2 * h) for e in np.eye(8)])
-    assert np.max(np.abs(fd - g)) <= 1e-8
+    assert np.max(np.abs(fd - g)) <= 1e-5 * max(1.0, np.linalg.norm(g))   # S:481 tolerance
     y = Q.T @ x
     H = Q @ np.diag(3 * y * y + c) @ Q.T
     assert np.max(np.abs(np.sort(np.linalg.eigvalsh(H)) - np.sort(mu))) <= 1e-12
