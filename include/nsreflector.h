@@ -261,6 +261,10 @@ ns_status_t ns_comm_get_unique_id(uint8_t id[128]);
 ns_status_t ns_comm_init(int rank, int nranks, const uint8_t id[128], ns_comm_t** comm);
 ns_status_t ns_comm_destroy(ns_comm_t* comm);
 ns_status_t ns_shard_plan(int64_t d, int nranks, int rank, int32_t* tiles_ij, int32_t cap, int32_t* n_out);
+/* Exchange chunking of the sharded path: each rank's tile list is cut into n_chunks chunks of
+ * chunk_slots slots (padded to the largest rank); chunk c of rank q carries the rank's local tiles
+ * c*chunk_slots .. c*chunk_slots + chunk_slots - 1, i.e. global upper tiles (c*chunk_slots + s)*P + q. */
+ns_status_t ns_shard_chunks(int64_t d, int nranks, int32_t* n_chunks, int32_t* chunk_slots);
 size_t ns_workspace_bytes_sharded(int64_t d, int nranks);
 ns_status_t ns_reflector_sharded(ns_comm_t* comm, const double* H, int64_t d, int64_t ldh, double s, double alpha,
                                  int32_t k, int32_t max_steps, double tol, ns_tolmode_t tm, double* R, int64_t ldr,

@@ -24,7 +24,7 @@ EXPORTED_SYMBOLS = (
     "ns_reflector_host", "ns_reflector_batched", "ns_symm_product", "ns_build_info", "ns_status_string",
     "ns_last_error", "ns_profile_enable", "ns_profile_reset", "ns_profile_get", "ns_options_default",
     "ns_reflector_ex", "ns_comm_get_unique_id", "ns_comm_init", "ns_comm_destroy", "ns_shard_plan",
-    "ns_workspace_bytes_sharded", "ns_reflector_sharded", "ns_workspace_bytes_setup", "ns_scale_bound",
+    "ns_workspace_bytes_sharded", "ns_reflector_sharded", "ns_shard_chunks", "ns_workspace_bytes_setup", "ns_scale_bound",
     "ns_shift_certificate", "ns_workspace_bytes_alg1", "ns_alg1_rotated_quartic",
 )
 
@@ -116,6 +116,8 @@ def load_library(path=LIB_PATH):
     lib.ns_comm_destroy.argtypes = [c_vp]
     lib.ns_shard_plan.restype = ctypes.c_int
     lib.ns_shard_plan.argtypes = [c_i64, ctypes.c_int, ctypes.c_int, c_vp, c_i32, ctypes.POINTER(c_i32)]
+    lib.ns_shard_chunks.restype = ctypes.c_int
+    lib.ns_shard_chunks.argtypes = [c_i64, ctypes.c_int, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)]
     lib.ns_workspace_bytes_sharded.restype = c_sz
     lib.ns_workspace_bytes_sharded.argtypes = [c_i64, ctypes.c_int]
     lib.ns_reflector_sharded.restype = ctypes.c_int
@@ -321,6 +323,13 @@ def ns_shard_plan(d, nranks, rank):
     out = np.zeros((max(n.value, 1), 2), dtype=np.int32)
     _check(lib.ns_shard_plan(int(d), int(nranks), int(rank), out.ctypes.data, n.value, ctypes.byref(n)))
     return out[:n.value]
+
+
+def ns_shard_chunks(d, nranks):
+    """(n_chunks, chunk_slots) of the sharded exchange (host-only)."""
+    a, b = ctypes.c_int32(), ctypes.c_int32()
+    _check(load_library().ns_shard_chunks(int(d), int(nranks), ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
 
 
 def ns_workspace_bytes_sharded(d, nranks):

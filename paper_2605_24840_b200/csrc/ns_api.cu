@@ -501,7 +501,7 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
 // ---------------- sharded (multi-GPU) path ----------------
 struct ShardLayout {
   Layout base;
-  int nranks = 1, rank = 0, n_my = 0, n_my_max = 0;
+  int nranks = 1, rank = 0, n_my = 0, n_my_max = 0, n_chunks = 1, cs = 0;
   size_t off_my = 0, off_send = 0, off_recv = 0, off_rsend = 0, off_rrecv = 0, total = 0;
 };
 
@@ -513,11 +513,13 @@ ShardLayout make_shard_layout(int64_t d, int nranks, int rank) {
   const int nt = S.base.n_tiles;
   S.n_my_max = (nt + nranks - 1) / nranks;
   S.n_my = (nt - rank + nranks - 1) / nranks;   // tiles t = rank, rank + P, ...
+  S.n_chunks = std::max(1, std::min(8, S.n_my_max));
+  S.cs = (S.n_my_max + S.n_chunks - 1) / S.n_chunks;   // slots per chunk (padded, equal on all ranks)
   size_t o = S.base.total;
   const size_t tile_bytes = (size_t)kTile * kTile * sizeof(double);
   S.off_my = o; o = align256(o + sizeof(int2) * (size_t)S.n_my_max);
-  S.off_send = o; o = align256(o + tile_bytes * (size_t)S.n_my_max);
-  S.off_recv = o; o = align256(o + tile_bytes * (size_t)S.n_my_max * (size_t)nranks);
+  S.off_send = o; o = align256(o + tile_bytes * (size_t)S.n_chunks * S.cs);
+  S.off_recv = o; o = align256(o + tile_bytes * (size_t)S.n_chunks * S.cs * (size_t)nranks);
   S.off_rsend = o; o = align256(o + sizeof(double));
   S.off_rrecv = o; o = align256(o + sizeof(double) * (size_t)nranks);
   S.total = o;
@@ -536,9 +538,16 @@ std::vector<int2> shard_tiles(const std::vector<int2>& all, int nranks, int rank
     if (r_ != ncclSuccess) return fail(NS_ERR_NCCL, "%s failed: %s", #x, ncclGetErrorString(r_)); \
   } while (0)
 
-ns_status_t run_sharded(ncclComm_t comm, const ShardLayout& SL, uint8_t* ws, const double* H, long long ldh,
+struct CommCtx {
+  ncclComm_t comm;
+  cudaStream_t cst;                    // communication stream (pack / all-gather / unpack)
+  std::vector<cudaEvent_t> ev;         // chunk-ready events (compute -> comm), + 1 "exchange done" (comm -> compute)
+};
+
+ns_status_t run_sharded(CommCtx& cc, const ShardLayout& SL, uint8_t* ws, const double* H, long long ldh,
                         const JobParams& jp, int32_t max_steps, double tol, ns_tolmode_t tm, double* R, long long ldr,
                         cudaStream_t st, DevState& out_state, int* launches) {
+  ncclComm_t comm = cc.comm;
   const Layout& L = SL.base;
   double* Xa = reinterpret_cast<double*>(ws + L.off_xa);
   double* Xb = reinterpret_cast<double*>(ws + L.off_xb);
@@ -568,16 +577,48 @@ ns_status_t run_sharded(ncclComm_t comm, const ShardLayout& SL, uint8_t* ws, con
   if ((s = encode_map(&tmB, Xb, L.d_pad, 1)) != NS_OK) return s;
   if ((s = encode_map(&tmY, Y, L.d_pad, 1)) != NS_OK) return s;
 
-  const size_t per_rank = (size_t)SL.n_my_max * kTile * kTile;   // doubles per rank in the gather
+  const size_t tile_elems = (size_t)kTile * kTile;
+  const size_t chunk_elems = (size_t)SL.cs * tile_elems;          // doubles per rank per chunk
   const int n_my = (int)mt.size();
+  while (cc.ev.size() < (size_t)SL.n_chunks + 1) {
+    cudaEvent_t e;
+    NS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cc.ev.push_back(e);
+  }
   int nl = 0;
+  // One symmetric product on the rank's tiles, chunk by chunk, with the exchange of chunk c on the
+  // communication stream overlapping the computation of chunk c+1.
+  auto product_and_exchange = [&](const CUtensorMap& tP, const CUtensorMap& tQ, double* C, const double* Xold,
+                                  double* partial, int mode) -> ns_status_t {
+    for (int c = 0; c < SL.n_chunks; ++c) {
+      const int s0 = c * SL.cs;
+      const int cnt = std::max(0, std::min(SL.cs, n_my - s0));
+      if (cnt > 0) {
+        ProdParams pp{my + s0, cnt, L.d_pad / kBK, L.d, L.d_pad, (long long)L.d_pad * L.d_pad, C, Xold,
+                      partial + s0, state, mode};
+        NS_CUDA(launch_product(tP, tQ, pp, 1, st));
+        nl += 1;
+      }
+      NS_CUDA(cudaEventRecord(cc.ev[c], st));
+      NS_CUDA(cudaStreamWaitEvent(cc.cst, cc.ev[c], 0));
+      if (cnt > 0) NS_CUDA(launch_pack_tiles(C, my + s0, cnt, send + (size_t)s0 * tile_elems, L.d_pad, cc.cst));
+      NS_NCCL(ncclAllGather(send + (size_t)s0 * tile_elems, recv + (size_t)c * SL.nranks * chunk_elems, chunk_elems,
+                            ncclDouble, comm, cc.cst));
+      NS_CUDA(launch_unpack_tiles(C, tiles, L.n_tiles, recv + (size_t)c * SL.nranks * chunk_elems, SL.cs, s0,
+                                  SL.nranks, SL.rank, L.d_pad, cc.cst));
+      nl += 2;
+    }
+    NS_CUDA(cudaEventRecord(cc.ev[SL.n_chunks], cc.cst));
+    NS_CUDA(cudaStreamWaitEvent(st, cc.ev[SL.n_chunks], 0));
+    return NS_OK;
+  };
+
   NS_CUDA(launch_zero_state(state, 1, n_active, st));
   NS_CUDA(launch_init(H, ldh, 0, Xa, djobs, L.d, L.d_pad, 1, st));
   NS_CUDA(launch_trace_partials(Xa, L.d, L.d_pad, 1, trp, st));
   nl += 3;
   LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0, -1, 0};
   const int LA = 2;
-  const long long js = (long long)L.d_pad * L.d_pad;
   for (int j = 0; j <= max_steps; ++j) {
     if (j >= LA) {
       const int slot = (j - LA) % 16;
@@ -588,28 +629,19 @@ ns_status_t run_sharded(ncclComm_t comm, const ShardLayout& SL, uint8_t* ws, con
     double* Xc = odd ? Xb : Xa;
     double* Xn = odd ? Xa : Xb;
     const CUtensorMap& tmC = odd ? tmB : tmA;
-    // 1-4: own Y tiles, residual sum, exchange
-    ProdParams sq{my, n_my, L.d_pad / kBK, L.d, L.d_pad, js, Y, nullptr, res, state, 0};
-    if (n_my) NS_CUDA(launch_product(tmC, tmC, sq, 1, st));
+    // own Y tiles (chunked, exchange overlapped) + residual sum of the rank's tiles
+    ns_status_t e1 = product_and_exchange(tmC, tmC, Y, nullptr, res, 0);
+    if (e1 != NS_OK) return e1;
     NS_CUDA(launch_shard_sum(res, n_my, rsend, st));
-    NS_CUDA(launch_pack_tiles(Y, my, n_my, send, L.d_pad, st));
-    NS_NCCL(ncclAllGather(send, recv, per_rank, ncclDouble, comm, st));
     NS_NCCL(ncclAllGather(rsend, rrecv, 1, ncclDouble, comm, st));
-    NS_CUDA(launch_unpack_tiles(Y, tiles, L.n_tiles, recv, (long long)per_rank, SL.n_my_max, SL.nranks, SL.rank,
-                                L.d_pad, st));
-    // 5: decide (identical on all ranks)
+    // decide (identical on all ranks)
     NS_CUDA(launch_decide(state, djobs, res, 0, trp, L.n, lp, 1, n_active, st, rrecv, SL.nranks));
-    nl += 5;
-    // 6: own X_{j+1} tiles, exchange, trace
+    nl += 2;
     if (j < max_steps) {
-      ProdParams up{my, n_my, L.d_pad / kBK, L.d, L.d_pad, js, Xn, Xc, trp, state, 1};
-      if (n_my) NS_CUDA(launch_product(tmC, tmY, up, 1, st));
-      NS_CUDA(launch_pack_tiles(Xn, my, n_my, send, L.d_pad, st));
-      NS_NCCL(ncclAllGather(send, recv, per_rank, ncclDouble, comm, st));
-      NS_CUDA(launch_unpack_tiles(Xn, tiles, L.n_tiles, recv, (long long)per_rank, SL.n_my_max, SL.nranks,
-                                  SL.rank, L.d_pad, st));
+      ns_status_t e2 = product_and_exchange(tmC, tmY, Xn, Xc, trp, 1);
+      if (e2 != NS_OK) return e2;
       NS_CUDA(launch_trace_partials(Xn, L.d, L.d_pad, 1, trp, st));
-      nl += 4;
+      nl += 1;
     }
     NS_CUDA(cudaMemcpyAsync(&rg.slots[j % 16], n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
     NS_CUDA(cudaEventRecord(rg.ev[j % 16], st));
@@ -833,6 +865,7 @@ struct ns_comm {
   ncclComm_t comm;
   int rank;
   int nranks;
+  CommCtx ctx;
 };
 
 ns_status_t ns_comm_get_unique_id(uint8_t id[128]) {
@@ -851,11 +884,17 @@ ns_status_t ns_comm_init(int rank, int nranks, const uint8_t id[128], ns_comm_t*
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(NS_ERR_INVALID_ARG, "bad rank/nranks");
   ncclUniqueId u;
   memcpy(&u, id, 128);
-  ns_comm_t* c = new ns_comm_t{nullptr, rank, nranks};
+  ns_comm_t* c = new ns_comm_t{nullptr, rank, nranks, CommCtx{}};
   ncclResult_t r = ncclCommInitRank(&c->comm, nranks, u, rank);
   if (r != ncclSuccess) {
     delete c;
     return fail(NS_ERR_NCCL, "ncclCommInitRank failed: %s", ncclGetErrorString(r));
+  }
+  c->ctx.comm = c->comm;
+  if (cudaStreamCreateWithFlags(&c->ctx.cst, cudaStreamNonBlocking) != cudaSuccess) {
+    ncclCommDestroy(c->comm);
+    delete c;
+    return fail(NS_ERR_CUDA, "communication stream creation failed");
   }
   *comm = c;
   return NS_OK;
@@ -864,6 +903,8 @@ ns_status_t ns_comm_init(int rank, int nranks, const uint8_t id[128], ns_comm_t*
 ns_status_t ns_comm_destroy(ns_comm_t* comm) {
   g_last_error.clear();
   if (!comm) return NS_OK;
+  for (cudaEvent_t e : comm->ctx.ev) cudaEventDestroy(e);
+  if (comm->ctx.cst) cudaStreamDestroy(comm->ctx.cst);
   ncclResult_t r = ncclCommDestroy(comm->comm);
   delete comm;
   if (r != ncclSuccess) return fail(NS_ERR_NCCL, "ncclCommDestroy failed: %s", ncclGetErrorString(r));
@@ -881,6 +922,15 @@ ns_status_t ns_shard_plan(int64_t d, int nranks, int rank, int32_t* tiles_ij, in
     tiles_ij[2 * i] = mt[i].x;
     tiles_ij[2 * i + 1] = mt[i].y;
   }
+  return NS_OK;
+}
+
+ns_status_t ns_shard_chunks(int64_t d, int nranks, int32_t* n_chunks, int32_t* chunk_slots) {
+  g_last_error.clear();
+  if (d < 1 || d > 65536 || nranks < 1 || !n_chunks || !chunk_slots) return fail(NS_ERR_INVALID_ARG, "bad arguments");
+  const ShardLayout SL = make_shard_layout(d, nranks, 0);
+  *n_chunks = SL.n_chunks;
+  *chunk_slots = SL.cs;
   return NS_OK;
 }
 
@@ -908,7 +958,7 @@ ns_status_t ns_reflector_sharded(ns_comm_t* comm, const double* H, int64_t d, in
     return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, SL.total);
   DevState ds;
   int nl = 0;
-  st = run_sharded(comm->comm, SL, static_cast<uint8_t*>(ws), H, ldh, JobParams{s, alpha, k, 0}, max_steps, tol, tm,
+  st = run_sharded(comm->ctx, SL, static_cast<uint8_t*>(ws), H, ldh, JobParams{s, alpha, k, 0}, max_steps, tol, tm,
                    R, ldr, static_cast<cudaStream_t>(stream), ds, &nl);
   if (st != NS_OK) return st;
   fill_result(ds, nl, out);

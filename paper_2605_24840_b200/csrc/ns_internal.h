@@ -162,8 +162,8 @@ cudaError_t launch_scale_bound(const double* H, long long ldh, int d, double s, 
 // ---------------- sharded path (ns_shard.cu) ----------------
 cudaError_t launch_pack_tiles(const double* M, const int2* my_tiles, int n_my, double* send, int d_pad,
                               cudaStream_t st);
-cudaError_t launch_unpack_tiles(double* M, const int2* all_tiles, int n_tiles, const double* recv, long long per_rank,
-                                int n_my_max, int nranks, int my_rank, int d_pad, cudaStream_t st);
+cudaError_t launch_unpack_tiles(double* M, const int2* all_tiles, int n_tiles, const double* recv_chunk, int cs,
+                                int slot0, int nranks, int my_rank, int d_pad, cudaStream_t st);
 cudaError_t launch_shard_sum(const double* v, int n, double* out, cudaStream_t st);
 cudaError_t launch_copy_out(const double* Xa, const double* Xb, int d, int d_pad, const DevState* state,
                             double* R, long long ldr, long long r_stride, int batch, cudaStream_t st);

@@ -7,9 +7,12 @@
 // Per NS step:
 //   1. Y tiles (own) <- X X               ns_product_kernel<0> on the rank's tile list
 //   2. residual partials -> one double    ns_shard_sum_kernel (fixed order)
-//   3. pack own Y tiles, ncclAllGather     (tile-major buffer; every rank receives all tiles)
-//      + ncclAllGather of the P residual sums (summed in rank order: identical bits on all ranks)
-//   4. unpack the other ranks' tiles into Y, mirrored (Y_JI = Y_IJ^T)
+//   3. the rank's tile list is cut into C chunks; as soon as chunk c's product kernel finishes (event
+//      on the compute stream) a communication stream packs its tiles, all-gathers them (NCCL) and
+//      unpacks the other ranks' copies into Y (mirrored) while chunk c+1 is being computed, so the
+//      exchange overlaps the contraction chunk by chunk; + ncclAllGather of the P residual sums
+//      (summed in rank order: identical bits on all ranks)
+//   4. the compute stream waits for the last unpack before anything reads the full Y
 //   5. decide (identical on all ranks)
 //   6. X_{j+1} tiles (own) <- 1.5 X - 0.5 X Y, pack, all-gather, unpack; tr X_{j+1} locally.
 // Communication per step: 2 all-gathers of d^2/2 doubles (each rank receives (P-1)/P of them)
@@ -36,18 +39,19 @@ __global__ void __launch_bounds__(256) ns_pack_tiles_kernel(const double* __rest
   }
 }
 
-// Scatter every other rank's gathered tiles into M, with the mirrored block for off-diagonal tiles.
-// grid = (n_my_max, P).  Global tile index of (local slot s, rank q) is s * P + q.
+// Scatter every other rank's gathered tiles of one chunk into M, with the mirrored block for
+// off-diagonal tiles.  grid = (cs, P): slot s of rank q in chunk c holds the rank's local tile
+// slot0 + s, i.e. global upper tile (slot0 + s) * P + q (absent if >= n_tiles).
 __global__ void __launch_bounds__(256) ns_unpack_tiles_kernel(double* __restrict__ M, const int2* __restrict__ all_tiles,
-                                                              int n_tiles, const double* __restrict__ recv,
-                                                              long long per_rank, int nranks, int my_rank, int d_pad) {
+                                                              int n_tiles, const double* __restrict__ recv_chunk,
+                                                              int cs, int slot0, int nranks, int my_rank, int d_pad) {
   __shared__ double t[32][33];
   const int q = blockIdx.y, slot = blockIdx.x;
   if (q == my_rank) return;
-  const long long gt = (long long)slot * nranks + q;
+  const long long gt = (long long)(slot0 + slot) * nranks + q;
   if (gt >= n_tiles) return;
   const int2 tl = all_tiles[gt];
-  const double* src = recv + (long long)q * per_rank + (long long)slot * kTile * kTile;
+  const double* src = recv_chunk + ((long long)q * cs + slot) * kTile * kTile;
   double* dst = M + (long long)tl.x * kTile * d_pad + (long long)tl.y * kTile;
   for (int i = threadIdx.x; i < kTile * kTile / 2; i += 256) {
     const int r = (2 * i) >> 7, c = (2 * i) & 127;
@@ -88,11 +92,11 @@ cudaError_t launch_pack_tiles(const double* M, const int2* my_tiles, int n_my, d
   return cudaGetLastError();
 }
 
-cudaError_t launch_unpack_tiles(double* M, const int2* all_tiles, int n_tiles, const double* recv, long long per_rank,
-                                int n_my_max, int nranks, int my_rank, int d_pad, cudaStream_t st) {
-  if (nranks > 1 && n_my_max > 0) {
-    dim3 grid(n_my_max, nranks);
-    ns_unpack_tiles_kernel<<<grid, 256, 0, st>>>(M, all_tiles, n_tiles, recv, per_rank, nranks, my_rank, d_pad);
+cudaError_t launch_unpack_tiles(double* M, const int2* all_tiles, int n_tiles, const double* recv_chunk, int cs,
+                                int slot0, int nranks, int my_rank, int d_pad, cudaStream_t st) {
+  if (nranks > 1 && cs > 0) {
+    dim3 grid(cs, nranks);
+    ns_unpack_tiles_kernel<<<grid, 256, 0, st>>>(M, all_tiles, n_tiles, recv_chunk, cs, slot0, nranks, my_rank, d_pad);
   }
   return cudaGetLastError();
 }

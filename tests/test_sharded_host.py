@@ -2,10 +2,11 @@
 
 * ns_shard_plan (the C library's tile assignment) covers every upper tile exactly once and is
   balanced to one tile.
-* A world_size-2 gloo run replays the library's exchange protocol (own tiles -> tile-major
-  send buffer padded to n_my_max -> all_gather -> unpack slot s of rank q = global tile s*P + q,
-  mirrored) with numpy products, and reproduces the unsharded Newton–Schulz step on every rank
-  bitwise-identically (identical stop decisions need identical bits).
+* A world_size-2 gloo run replays the library's exchange protocol (ns_shard_chunks: own tiles cut
+  into chunks -> tile-major send buffer -> one all_gather per chunk -> unpack slot s of rank q of
+  chunk c = global tile (c*cs + s)*P + q, mirrored) with numpy products, and reproduces the
+  unsharded Newton–Schulz step on every rank bitwise-identically (identical stop decisions need
+  identical bits).
 """
 import os
 import socket
@@ -66,23 +67,36 @@ def _worker(rank, world, port, d, q):
         X = np.zeros((dp, dp))
         X[:d, :d] = A
         plans = [nsr.ns_shard_plan(d, world, r) for r in range(world)]
-        n_my_max = max(len(p) for p in plans)
+        n_chunks, cs = nsr.ns_shard_chunks(d, world)
+        all_tiles = [None] * sum(len(p) for p in plans)
+        for q_, pl in enumerate(plans):            # global tile t = local slot * P + rank
+            for s_, tl in enumerate(pl):
+                all_tiles[s_ * world + q_] = tuple(int(v) for v in tl)
         mine = plans[rank]
 
         def exchange(M):
-            send = np.zeros((n_my_max, T, T))
-            for s_, (I, J) in enumerate(mine):
-                send[s_] = M[I * T:(I + 1) * T, J * T:(J + 1) * T]
-            out = [torch.zeros(n_my_max * T * T, dtype=torch.float64) for _ in range(world)]
-            dist.all_gather(out, torch.from_numpy(send.reshape(-1)))
-            for qq in range(world):
-                if qq == rank:
-                    continue
-                recv = out[qq].numpy().reshape(n_my_max, T, T)
-                for s_, (I, J) in enumerate(plans[qq]):
-                    M[I * T:(I + 1) * T, J * T:(J + 1) * T] = recv[s_]
-                    if I != J:
-                        M[J * T:(J + 1) * T, I * T:(I + 1) * T] = recv[s_].T
+            # the library's protocol: chunk c = local slots [c*cs, (c+1)*cs), one all_gather per chunk,
+            # gathered slot s of rank q = global tile (c*cs + s)*P + q, unpacked with its mirror
+            for c in range(n_chunks):
+                send = np.zeros((cs, T, T))
+                for s_ in range(cs):
+                    if c * cs + s_ < len(mine):
+                        I, J = mine[c * cs + s_]
+                        send[s_] = M[I * T:(I + 1) * T, J * T:(J + 1) * T]
+                out = [torch.zeros(cs * T * T, dtype=torch.float64) for _ in range(world)]
+                dist.all_gather(out, torch.from_numpy(send.reshape(-1)))
+                for qq in range(world):
+                    if qq == rank:
+                        continue
+                    recv = out[qq].numpy().reshape(cs, T, T)
+                    for s_ in range(cs):
+                        gt = (c * cs + s_) * world + qq
+                        if gt >= len(all_tiles):
+                            continue
+                        I, J = all_tiles[gt]
+                        M[I * T:(I + 1) * T, J * T:(J + 1) * T] = recv[s_]
+                        if I != J:
+                            M[J * T:(J + 1) * T, I * T:(I + 1) * T] = recv[s_].T
             return M
 
         def own_product(P_, Q_, update):
@@ -126,7 +140,7 @@ def _worker(rank, world, port, d, q):
         q.put((rank, f"error: {e!r}", False))
 
 
-@pytest.mark.parametrize("d", [300, 520])
+@pytest.mark.parametrize("d", [300, 520, 2000])
 def test_gloo_two_rank_exchange(nsr, d):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
