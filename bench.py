@@ -43,9 +43,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="tol", choices=["tol", "fixed30"])
-    ap.add_argument("--prec", default="fp64", choices=["fp64", "mixed"],
-                    help="fp64: DMMA path (headline); mixed: BF16x3 tcgen05 -> re-anchor -> FP64 (configs[3] mixed)")
-    ap.add_argument("--no-mixed", action="store_true", help="skip the secondary mixed-mode measurement")
+    ap.add_argument("--prec", default="fp64", choices=["fp64", "mixed", "ozaki"],
+                    help="fp64: DMMA path (headline); mixed: BF16x3 tcgen05 -> re-anchor -> FP64 (configs[3] mixed); "
+                         "ozaki: FP64 products emulated on the INT8 tensor cores")
+    ap.add_argument("--no-mixed", action="store_true", help="skip the secondary mixed / Ozaki measurements")
     ap.add_argument("--d", type=int, default=16384)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -178,7 +179,7 @@ def run_ours(args):
     wsbuf = nsr.alloc_workspace(nsr.ns_workspace_bytes(d), dev)
     stream = torch.cuda.current_stream(dev)
 
-    prec = nsr.NS_PREC_FP64 if args.prec == "fp64" else nsr.NS_PREC_MIXED_BF16X3
+    prec = {"fp64": nsr.NS_PREC_FP64, "mixed": nsr.NS_PREC_MIXED_BF16X3, "ozaki": nsr.NS_PREC_FP64_OZAKI}[args.prec]
     if prec != nsr.NS_PREC_FP64:
         wsbuf = nsr.alloc_workspace(nsr.ns_workspace_bytes(d, prec), dev)
 
@@ -271,24 +272,32 @@ def run_ours(args):
                "ms_per_step": ems / args.steps, "entry": "ns_reflector_host (pinned host H, R)"}
         del Hh, Rh
 
-    # ---- secondary: the same reflector through the mixed BF16x3 -> re-anchor -> FP64 mode
-    mixed = None
-    if args.prec == "fp64" and not args.no_mixed:
-        wsbuf = nsr.alloc_workspace(nsr.ns_workspace_bytes(d, nsr.NS_PREC_MIXED_BF16X3), dev)
-        _, rm = call(nsr.NS_PREC_MIXED_BF16X3)
+    # ---- secondary: the same reflector through the mixed BF16x3 -> re-anchor -> FP64 mode and the
+    # Ozaki-split FP64 emulation on the INT8 tensor cores (same metric, FP64-equivalent algorithmic flops)
+    mixed = ozaki = None
+
+    def secondary(pr):
+        nonlocal wsbuf
+        wsbuf = nsr.alloc_workspace(nsr.ns_workspace_bytes(d, pr), dev)
+        _, rm = call(pr)
         torch.cuda.synchronize(dev)
         g0 = torch.cuda.Event(enable_timing=True)
         g1 = torch.cuda.Event(enable_timing=True)
         g0.record(stream)
         for _ in range(args.steps):
-            _, rm = call(nsr.NS_PREC_MIXED_BF16X3)
+            _, rm = call(pr)
         g1.record(stream)
         torch.cuda.synchronize(dev)
         mms = g0.elapsed_time(g1) / args.steps
-        mixed = {"time_to_R_ms": mms, "value": (2 * rm["steps"] + 1) * float(d) ** 3 / (mms * 1e-3) / 1e12,
-                 "unit": "TFLOP/s (FP64-equivalent algorithmic)", "steps": rm["steps"], "switch_step": rm["switch_step"],
-                 "pre_polish_residual": rm["pre_polish_residual"], "cert": rm["cert"], "flags": rm["flags"],
-                 "speedup_vs_fp64": (ms / args.steps) / mms, "launches": rm["launches"]}
+        return {"time_to_R_ms": mms, "value": (2 * rm["steps"] + 1) * float(d) ** 3 / (mms * 1e-3) / 1e12,
+                "unit": "TFLOP/s (FP64-equivalent algorithmic)", "steps": rm["steps"], "switch_step": rm["switch_step"],
+                "pre_polish_residual": rm["pre_polish_residual"], "cert": rm["cert"], "flags": rm["flags"],
+                "speedup_vs_fp64": (ms / args.steps) / mms, "launches": rm["launches"]}
+
+    if args.prec == "fp64" and not args.no_mixed:
+        mixed = secondary(nsr.NS_PREC_MIXED_BF16X3)
+        if d <= 16640:
+            ozaki = secondary(nsr.NS_PREC_FP64_OZAKI)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -312,7 +321,7 @@ def run_ours(args):
             "result": {"steps": steps_ns, "cert": results[-1]["cert"], "flags": results[-1]["flags"],
                        "residual": results[-1]["residual"]},
             "gpu_launches": launches, "clocks": clocks, "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
-            "mixed_mode": mixed, "precision": args.prec,
+            "mixed_mode": mixed, "ozaki_mode": ozaki, "precision": args.prec,
         }
         print(json.dumps(line), flush=True)
     if pg:

@@ -53,7 +53,9 @@ extern "C" {
 typedef enum {
   NS_PREC_FP64 = 0,          /* FP64 DMMA contraction (accuracy path) */
   NS_PREC_MIXED_BF16X3 = 1,  /* tcgen05 BF16x3 steps -> switch -> re-anchor -> FP64 steps (C16) */
-  NS_PREC_MIXED_TF32X3 = 2   /* reserved: tcgen05 split-TF32 path (returns NS_ERR_UNSUPPORTED) */
+  NS_PREC_MIXED_TF32X3 = 2,  /* reserved: tcgen05 split-TF32 path (returns NS_ERR_UNSUPPORTED) */
+  NS_PREC_FP64_OZAKI = 3     /* FP64-accurate products emulated on tcgen05 INT8 (Ozaki split, 7 slices);
+                                SURVEY N4; single problem, d <= 16384 (INT32 group sums stay exact) */
 } ns_precision_t;
 
 typedef enum {

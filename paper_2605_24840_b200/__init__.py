@@ -13,7 +13,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libnsreflector.so")
 
-NS_PREC_FP64, NS_PREC_MIXED_BF16X3, NS_PREC_MIXED_TF32X3 = 0, 1, 2
+NS_PREC_FP64, NS_PREC_MIXED_BF16X3, NS_PREC_MIXED_TF32X3, NS_PREC_FP64_OZAKI = 0, 1, 2, 3
 NS_TOL_ABS, NS_TOL_PER_SQRT_D = 0, 1
 NS_OK = 0
 NS_F_CONVERGED, NS_F_MAX_STEPS, NS_F_INDEX_MISMATCH = 1, 2, 4

@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libnsreflector.so")
-SOURCES = ["ns_api.cu", "ns_fp64.cu", "ns_mixed.cu", "ns_reanchor.cu", "ns_shard.cu", "ns_small.cu", "ns_setup.cu", "ns_outer.cu"]
+SOURCES = ["ns_api.cu", "ns_fp64.cu", "ns_mixed.cu", "ns_reanchor.cu", "ns_shard.cu", "ns_small.cu", "ns_setup.cu", "ns_outer.cu", "ns_ozaki.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 

@@ -49,10 +49,11 @@ struct Layout {
   bool mixed = false;
   size_t off_xa = 0, off_xb = 0, off_y = 0, off_res = 0, off_tr = 0, off_tiles = 0, off_jobs = 0,
          off_state = 0, off_active = 0, off_px = 0, off_py = 0, off_full = 0, off_pxb = 0, off_ahat = 0,
-         off_r = 0, off_p = 0, off_cgpart = 0, off_cgsc = 0, total = 0;
+         off_r = 0, off_p = 0, off_cgpart = 0, off_cgsc = 0, off_ozx = 0, off_ozy = 0, off_oex = 0, off_oey = 0,
+         off_ores = 0, off_otr = 0, off_otiles = 0, total = 0;
 };
 
-Layout make_layout(int64_t d, int64_t batch, bool mixed = false) {
+Layout make_layout(int64_t d, int64_t batch, bool mixed = false, bool ozaki = false) {
   Layout L;
   L.d = static_cast<int>(d);
   L.d_pad = static_cast<int>((d + kTile - 1) / kTile * kTile);
@@ -72,6 +73,16 @@ Layout make_layout(int64_t d, int64_t batch, bool mixed = false) {
   L.off_active = o; o = align256(o + 256);
   L.off_full = o; o = align256(o + sizeof(int2) * (size_t)L.n * L.n);   // full tile list (dense products)
   L.mixed = mixed;
+  if (ozaki) {
+    const size_t nn = (size_t)L.d_pad * L.d_pad;
+    L.off_ozx = o; o = align256(o + nn * kOzSlices * (size_t)batch);     // int8 slices of X_j
+    L.off_ozy = o; o = align256(o + nn * kOzSlices * (size_t)batch);     // int8 slices of Y_j
+    L.off_oex = o; o = align256(o + sizeof(int) * (size_t)L.d_pad * batch);
+    L.off_oey = o; o = align256(o + sizeof(int) * (size_t)L.d_pad * batch);
+    L.off_ores = o; o = align256(o + sizeof(double) * (size_t)L.n * (L.n + 1) * batch);   // 128x64 tiles
+    L.off_otr = o; o = align256(o + sizeof(double) * (size_t)2 * L.n * batch);
+    L.off_otiles = o; o = align256(o + sizeof(int2) * (size_t)2 * L.n * L.n);           // sym or full 128x64 list
+  }
   if (mixed) {
     const size_t planes = (size_t)L.d_pad * L.d_pad * 2 * sizeof(uint16_t) * (size_t)batch;
     L.off_px = o; o = align256(o + planes);     // bf16 hi/lo planes of X_j (even j) / CG direction P
@@ -87,6 +98,18 @@ Layout make_layout(int64_t d, int64_t batch, bool mixed = false) {
   }
   L.total = o;
   return L;
+}
+
+// 128 x 64 tiles (I: 128-row block, J2: 64-column block).  Symmetric: every tile touching the upper
+// triangle (J2*64 + 63 >= I*128), L2-grouped like make_tiles; dense: all.
+std::vector<int2> make_tiles_oz(int n, bool sym) {
+  std::vector<int2> v;
+  const int G = 12;
+  for (int SI = 0; SI < n; SI += G)
+    for (int SJ = sym ? 2 * SI : 0; SJ < 2 * n; SJ += 2 * G)
+      for (int I = SI; I < std::min(SI + G, n); ++I)
+        for (int J2 = std::max(SJ, sym ? 2 * I : 0); J2 < std::min(SJ + 2 * G, 2 * n); ++J2) v.push_back(make_int2(I, J2));
+  return v;
 }
 
 std::vector<int2> make_tiles_full(int n) {
@@ -147,6 +170,21 @@ ns_status_t encode_map(CUtensorMap* m, const double* base, int d_pad, long long 
   return NS_OK;
 }
 
+// 3-D map over `nplanes` row-major d_pad x d_pad int8 slices; box = 64 (k) x rows x 1, 64-byte swizzle.
+ns_status_t encode_map_i8(CUtensorMap* m, const int8_t* base, int d_pad, long long nplanes, int box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(NS_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)d_pad, (cuuint64_t)d_pad, (cuuint64_t)nplanes};
+  cuuint64_t strides[2] = {(cuuint64_t)d_pad, (cuuint64_t)d_pad * (cuuint64_t)d_pad};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(NS_ERR_CUDA, "cuTensorMapEncodeTiled (int8) failed (%d)", (int)r);
+  return NS_OK;
+}
+
 // 3-D map over `nplanes` row-major d_pad x d_pad BF16 planes; box = 64 (k) x 128 (rows) x 1, 128-B swizzle
 // (the layout the UMMA shared-memory descriptors in ns_mixed.cu describe).
 ns_status_t encode_map_bf16(CUtensorMap* m, const uint16_t* base, int d_pad, long long nplanes) {
@@ -204,7 +242,8 @@ ns_status_t check_common(int64_t d, int32_t max_steps, double tol, ns_tolmode_t 
   if (!(tol >= 0.0) || !std::isfinite(tol)) return fail(NS_ERR_INVALID_ARG, "tol must be finite and >= 0");
   if (tm != NS_TOL_ABS && tm != NS_TOL_PER_SQRT_D) return fail(NS_ERR_INVALID_ARG, "bad tolerance mode");
   if (prec == NS_PREC_MIXED_TF32X3) return fail(NS_ERR_UNSUPPORTED, "the TF32x3 mode is not available in this build");
-  if (prec != NS_PREC_FP64 && prec != NS_PREC_MIXED_BF16X3) return fail(NS_ERR_INVALID_ARG, "bad precision");
+  if (prec != NS_PREC_FP64 && prec != NS_PREC_MIXED_BF16X3 && prec != NS_PREC_FP64_OZAKI)
+    return fail(NS_ERR_INVALID_ARG, "bad precision");
   return NS_OK;
 }
 
@@ -333,6 +372,73 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
     }
     pf.acc.n_calls += 1;
   }
+  return NS_OK;
+}
+
+// Ozaki path (single problem): the FP64 loop with every product on the INT8 tensor cores.
+ns_status_t run_ozaki(const Layout& L, uint8_t* ws, const double* H, long long ldh, const JobParams& jp,
+                      int32_t max_steps, double tol, ns_tolmode_t tm, double* R, long long ldr, cudaStream_t st,
+                      const Opts& opt, DevState& out_state, int* launches) {
+  double* Xa = reinterpret_cast<double*>(ws + L.off_xa);
+  double* Xb = reinterpret_cast<double*>(ws + L.off_xb);
+  double* Y = reinterpret_cast<double*>(ws + L.off_y);
+  double* res = reinterpret_cast<double*>(ws + L.off_ores);
+  double* trp = reinterpret_cast<double*>(ws + L.off_otr);
+  int8_t* slX = reinterpret_cast<int8_t*>(ws + L.off_ozx);
+  int8_t* slY = reinterpret_cast<int8_t*>(ws + L.off_ozy);
+  int* eX = reinterpret_cast<int*>(ws + L.off_oex);
+  int* eY = reinterpret_cast<int*>(ws + L.off_oey);
+  int2* otiles = reinterpret_cast<int2*>(ws + L.off_otiles);
+  JobParams* djobs = reinterpret_cast<JobParams*>(ws + L.off_jobs);
+  DevState* state = reinterpret_cast<DevState*>(ws + L.off_state);
+  int* n_active = reinterpret_cast<int*>(ws + L.off_active);
+  HostRing& rg = ring();
+  if (!rg.ok) return fail(NS_ERR_CUDA, "pinned status ring allocation failed");
+  std::vector<int2> ot = make_tiles_oz(L.n, true);
+  const int nt = (int)ot.size(), ndiag = 2 * L.n;
+  NS_CUDA(cudaMemcpyAsync(otiles, ot.data(), ot.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+  NS_CUDA(cudaMemcpyAsync(djobs, &jp, sizeof(JobParams), cudaMemcpyHostToDevice, st));
+  CUtensorMap tXa, tXb, tY;
+  ns_status_t s;
+  if ((s = encode_map_i8(&tXa, slX, L.d_pad, kOzSlices, kTile)) != NS_OK) return s;
+  if ((s = encode_map_i8(&tXb, slX, L.d_pad, kOzSlices, 64)) != NS_OK) return s;
+  if ((s = encode_map_i8(&tY, slY, L.d_pad, kOzSlices, 64)) != NS_OK) return s;
+  int nl = 0;
+  NS_CUDA(launch_zero_state(state, 1, n_active, st));
+  NS_CUDA(launch_init(H, ldh, 0, Xa, djobs, L.d, L.d_pad, 1, st));
+  NS_CUDA(cudaMemsetAsync(trp, 0, sizeof(double) * ndiag, st));
+  NS_CUDA(launch_trace_partials(Xa, L.d, L.d_pad, 1, trp, st));
+  nl += 3;
+  LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0, -1, 0};
+  const int LA = 2;
+  for (int j = 0; j <= max_steps; ++j) {
+    if (j >= LA) {
+      const int slot = (j - LA) % 16;
+      NS_CUDA(cudaEventSynchronize(rg.ev[slot]));
+      if (rg.slots[slot] == 0) break;
+    }
+    const bool odd = (j & 1) != 0;
+    double* Xc = odd ? Xb : Xa;
+    double* Xn = odd ? Xa : Xb;
+    NS_CUDA(launch_ozaki_slice(Xc, slX, eX, L.d_pad, 1, st));
+    OzParams sq{otiles, nt, L.d_pad / 64, L.d, L.d_pad, 0, Y, nullptr, eX, eX, res, state, 0};
+    NS_CUDA(launch_ozaki_product(tXa, tXb, sq, 1, st));
+    NS_CUDA(launch_decide(state, djobs, res, nt, trp, ndiag, lp, 1, n_active, st));
+    nl += 3;
+    if (j < max_steps) {
+      NS_CUDA(launch_ozaki_slice(Y, slY, eY, L.d_pad, 1, st));
+      OzParams up{otiles, nt, L.d_pad / 64, L.d, L.d_pad, 0, Xn, Xc, eX, eY, trp, state, 1, opt.ca, opt.cb};
+      NS_CUDA(launch_ozaki_product(tXa, tY, up, 1, st));
+      nl += 2;
+    }
+    NS_CUDA(cudaMemcpyAsync(&rg.slots[j % 16], n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+    NS_CUDA(cudaEventRecord(rg.ev[j % 16], st));
+  }
+  NS_CUDA(launch_copy_out(Xa, Xb, L.d, L.d_pad, state, R, ldr, 0, 1, st));
+  nl += 1;
+  NS_CUDA(cudaMemcpyAsync(&out_state, state, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+  NS_CUDA(cudaStreamSynchronize(st));
+  if (launches) *launches = nl;
   return NS_OK;
 }
 
@@ -671,7 +777,7 @@ extern "C" {
 
 size_t ns_workspace_bytes(int64_t d, ns_precision_t prec) {
   if (d < 1) return 0;
-  return make_layout(d, 1, prec != NS_PREC_FP64).total;
+  return make_layout(d, 1, prec == NS_PREC_MIXED_BF16X3, prec == NS_PREC_FP64_OZAKI).total;
 }
 
 size_t ns_workspace_bytes_batched(int64_t d, int64_t batch, ns_precision_t prec) {
@@ -708,7 +814,9 @@ ns_status_t ns_reflector_ex(const double* H, int64_t d, int64_t ldh, double s, d
   if (R == H) return fail(NS_ERR_INVALID_ARG, "R must not alias H");
   if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(NS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
   const bool mixed = (prec == NS_PREC_MIXED_BF16X3);
-  const Layout L = make_layout(d, 1, mixed);
+  const bool ozaki = (prec == NS_PREC_FP64_OZAKI);
+  if (ozaki && d > kOzMaxD) return fail(NS_ERR_UNSUPPORTED, "the Ozaki path needs d <= %d", kOzMaxD);
+  const Layout L = make_layout(d, 1, mixed, ozaki);
   if (ws_bytes < L.total)
     return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
   const Opts o = to_opts(opts);
@@ -718,10 +826,12 @@ ns_status_t ns_reflector_ex(const double* H, int64_t d, int64_t ldh, double s, d
     return fail(NS_ERR_UNSUPPORTED, "the mixed path runs the Newton-Schulz step (1.5, -0.5) only");
   std::vector<JobParams> jobs{JobParams{s, alpha, k, 0}};
   int nl = 0;
-  if (mixed) {
+  if (mixed || ozaki) {
     DevState ds;
-    st = run_mixed(L, static_cast<uint8_t*>(ws), H, ldh, jobs[0], max_steps, tol, tm, R, ldr,
-                   static_cast<cudaStream_t>(stream), o, ds, &nl);
+    st = mixed ? run_mixed(L, static_cast<uint8_t*>(ws), H, ldh, jobs[0], max_steps, tol, tm, R, ldr,
+                           static_cast<cudaStream_t>(stream), o, ds, &nl)
+               : run_ozaki(L, static_cast<uint8_t*>(ws), H, ldh, jobs[0], max_steps, tol, tm, R, ldr,
+                           static_cast<cudaStream_t>(stream), o, ds, &nl);
     if (st != NS_OK) return st;
     fill_result(ds, nl, out);
     return NS_OK;
@@ -754,7 +864,9 @@ ns_status_t ns_reflector_host(const double* H_host, int64_t d, int64_t ldh, doub
   if (k < 0 || k > d) return fail(NS_ERR_INVALID_ARG, "k must lie in [0, d]");
   if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(NS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
   const bool mixed = (prec == NS_PREC_MIXED_BF16X3);
-  const Layout L = make_layout(d, 1, mixed);
+  const bool ozaki = (prec == NS_PREC_FP64_OZAKI);
+  if (ozaki && d > kOzMaxD) return fail(NS_ERR_UNSUPPORTED, "the Ozaki path needs d <= %d", kOzMaxD);
+  const Layout L = make_layout(d, 1, mixed, ozaki);
   if (ws_bytes < L.total)
     return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
@@ -768,6 +880,8 @@ ns_status_t ns_reflector_host(const double* H_host, int64_t d, int64_t ldh, doub
   int nl = 0;
   if (mixed)
     st = run_mixed(L, w, stage, d, jobs[0], max_steps, tol, tm, stage, d, cs, Opts{}, states[0], &nl);
+  else if (ozaki)
+    st = run_ozaki(L, w, stage, d, jobs[0], max_steps, tol, tm, stage, d, cs, Opts{}, states[0], &nl);
   else
     st = run_loop(L, w, stage, d, 0, jobs, max_steps, tol, tm, stage, d, 0, cs, states, &nl);
   if (st != NS_OK) return st;
@@ -816,11 +930,14 @@ ns_status_t ns_symm_product(const double* A, const double* B, double* C, int64_t
   if (d < 1 || d > 65536) return fail(NS_ERR_INVALID_ARG, "bad d");
   if (ld < d) return fail(NS_ERR_INVALID_ARG, "ld must be >= d");
   if (mode < 0 || mode > 2) return fail(NS_ERR_INVALID_ARG, "mode must be 0, 1 or 2");
-  if (prec != NS_PREC_FP64 && prec != NS_PREC_MIXED_BF16X3) return fail(NS_ERR_UNSUPPORTED, "precision not available");
+  if (prec != NS_PREC_FP64 && prec != NS_PREC_MIXED_BF16X3 && prec != NS_PREC_FP64_OZAKI)
+    return fail(NS_ERR_UNSUPPORTED, "precision not available");
+  if (prec == NS_PREC_FP64_OZAKI && d > kOzMaxD) return fail(NS_ERR_UNSUPPORTED, "Ozaki products need d <= %d", kOzMaxD);
   if (!A || !B || !C || !ws) return fail(NS_ERR_INVALID_ARG, "null pointer argument");
   if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(NS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
   const bool mixed = (prec == NS_PREC_MIXED_BF16X3);
-  const Layout L = make_layout(d, 1, mixed);
+  const bool ozaki = (prec == NS_PREC_FP64_OZAKI);
+  const Layout L = make_layout(d, 1, mixed, ozaki);
   if (ws_bytes < L.total) return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   uint8_t* w = static_cast<uint8_t*>(ws);
@@ -838,7 +955,23 @@ ns_status_t ns_symm_product(const double* A, const double* B, double* C, int64_t
   NS_CUDA(launch_init(B, ld, 0, Pb, djobs, L.d, L.d_pad, 1, cs));
   double* partial = reinterpret_cast<double*>(w + (mode == 0 ? L.off_res : L.off_tr));
   ns_status_t s;
-  if (!mixed) {
+  if (ozaki) {
+    int8_t* slA = reinterpret_cast<int8_t*>(w + L.off_ozx);
+    int8_t* slB = reinterpret_cast<int8_t*>(w + L.off_ozy);
+    int* eA = reinterpret_cast<int*>(w + L.off_oex);
+    int* eB = reinterpret_cast<int*>(w + L.off_oey);
+    int2* otiles = reinterpret_cast<int2*>(w + L.off_otiles);
+    std::vector<int2> ot = make_tiles_oz(L.n, mode != 2);
+    NS_CUDA(cudaMemcpyAsync(otiles, ot.data(), ot.size() * sizeof(int2), cudaMemcpyHostToDevice, cs));
+    NS_CUDA(launch_ozaki_slice(Pa, slA, eA, L.d_pad, 1, cs));
+    NS_CUDA(launch_ozaki_slice(Pb, slB, eB, L.d_pad, 1, cs));
+    CUtensorMap tA, tB;
+    if ((s = encode_map_i8(&tA, slA, L.d_pad, kOzSlices, kTile)) != NS_OK) return s;
+    if ((s = encode_map_i8(&tB, slB, L.d_pad, kOzSlices, 64)) != NS_OK) return s;
+    double* opart = reinterpret_cast<double*>(w + (mode == 0 ? L.off_ores : L.off_otr));
+    OzParams p{otiles, (int)ot.size(), L.d_pad / 64, L.d, L.d_pad, 0, Pc, Pa, eA, eB, opart, nullptr, mode};
+    NS_CUDA(launch_ozaki_product(tA, tB, p, 1, cs));
+  } else if (!mixed) {
     CUtensorMap tA, tB;
     if ((s = encode_map(&tA, Pa, L.d_pad, 1)) != NS_OK) return s;
     if ((s = encode_map(&tB, Pb, L.d_pad, 1)) != NS_OK) return s;

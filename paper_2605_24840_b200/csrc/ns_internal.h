@@ -155,6 +155,37 @@ struct OuterResult {
 cudaError_t launch_outer(const double* Q, int d, const int* k, const double* x0, OuterParams p, double* xout,
                          OuterResult* res, int nruns, cudaStream_t st);
 
+// ---------------- Ozaki-split FP64 products on INT8 tensor cores (ns_ozaki.cu) ----------------
+constexpr int kOzSlices = 8;                           // 8 x 7-bit slices per operand row (~2^-56 of the row max)
+constexpr int kOzMaxD = 16640;                         // 8 * d_pad * 127^2 < 2^31: exact INT32 group sums
+constexpr int kOzStages = 2;
+constexpr int kOzThreads = 192;                        // warp 0 TMA, warp 1 MMA, warps 2..5 epilogue
+constexpr int kOzSlabA = kTile * 64;                   // 128 rows x 64 int8
+constexpr int kOzSlabB = 64 * 64;                      // 64 rows x 64 int8
+constexpr int kOzStageBytes = kOzSlices * (kOzSlabA + kOzSlabB);
+constexpr int kOzSmemBytes = kOzStages * kOzStageBytes + 1024 + 256;
+
+struct OzParams {
+  const int2* tiles;       // (I: 128-row block, J2: 64-column block)
+  int n_tiles;
+  int nkb;                 // d_pad / 64
+  int d;
+  int ld;                  // d_pad
+  long long job_stride;
+  double* C;
+  const double* Xold;      // mode 1
+  const int* expP;         // row exponents of P (per job, d_pad)
+  const int* expQ;         // row exponents of Q
+  double* partial;         // mode 0: per tile; mode 1: per 64-column block J2 (2n entries per job)
+  const DevState* state;
+  int mode;                // 0 square (+res, mirror), 1 update (+trace, mirror), 2 dense
+  double ca = 1.5;
+  double cb = -0.5;
+};
+cudaError_t launch_ozaki_slice(const double* X, int8_t* slices, int* expo, int d_pad, int batch, cudaStream_t st);
+cudaError_t launch_ozaki_product(const CUtensorMap& tmA, const CUtensorMap& tmB, const OzParams& p, int batch,
+                                 cudaStream_t st);
+
 // ---------------- shift/scale setup (ns_setup.cu) ----------------
 cudaError_t launch_scale_bound(const double* H, long long ldh, int d, double s, double* part, double* out,
                                cudaStream_t st);

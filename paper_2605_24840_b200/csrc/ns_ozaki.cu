@@ -1,0 +1,263 @@
+// FP64-accurate products on the INT8 tensor cores (tcgen05 kind::i8) by the Ozaki splitting
+// (SURVEY §8(f) N4 -- an arithmetic variant, not in the paper).
+//
+// Every operand row i is scaled by its own power of two, x_ij = 2^{e_i} * sum_{s=1..S} 2^{-7s} q^s_ij
+// with integer slices q^s in [-127, 127] (exact bit extraction in FP64: e_i = frexp exponent of the
+// row max, r = x 2^{7 - e_i}, q = trunc(r), r = (r - q) 2^7, ...).  Then
+//     (P Q^T)_ij = 2^{e_i + f_j} sum_{g=2}^{S+1} 2^{-7g} sum_{s+t=g} (Q^s_P Q^t_Q^T)_ij  (+ truncation below 2^{-7(S+1)})
+// where each slice product is EXACT in INT32 (|sum| <= 7 * d * 127^2 < 2^31 for d <= 19000) and the
+// seven group sums are accumulated in seven INT32 TMEM accumulators.  The epilogue converts them to
+// FP64 exactly, weights them by powers of two (smallest first), applies the row/column exponents and
+// rounds once: the result is accurate to ~2^-49 of |row_i| |row_j|, i.e. FP64-class.
+//
+// CTA tile 128 x 64 (UMMA M=128, N=64, K=32), 7 accumulators x 64 columns = 448 TMEM columns.
+// Stage = one 64-wide k-block of all 7 slices of both operands (7 x 8 KB + 7 x 4 KB, 64-B swizzle),
+// feeding 28 slice pairs x 2 UMMAs; 2 stages.  Warp 0 TMA, warp 1 MMA, warps 2..5 epilogue.
+// Symmetric outputs: tiles (I, J2) with J2*64 + 63 >= I*128; every element with j >= i is produced
+// by exactly one tile, which writes it and its mirror (bitwise-symmetric output).
+#include <cmath>
+#include <cstdint>
+
+#include "ns_internal.h"
+#include "ns_ptx.cuh"
+
+namespace nsr {
+
+// per-row exponent e_i (row max < 2^{e_i}) and S int8 slices; one block per row, grid.y = job
+__global__ void __launch_bounds__(256) ns_ozaki_slice_kernel(const double* __restrict__ X, int8_t* __restrict__ slices,
+                                                             int* __restrict__ expo, int d_pad) {
+  __shared__ double red[8];
+  const int row = blockIdx.x, job = blockIdx.y;
+  const long long nn = (long long)d_pad * d_pad;
+  const double* x = X + (long long)job * nn + (long long)row * d_pad;
+  double m = 0.0;
+  for (int j = threadIdx.x; j < d_pad; j += 256) m = fmax(m, fabs(x[j]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  double mm = 0.0;
+  for (int w = 0; w < 8; ++w) mm = fmax(mm, red[w]);
+  int e = 0;
+  if (mm > 0.0 && isfinite(mm)) frexp(mm, &e);   // mm = f 2^e, f in [0.5, 1)  =>  |x_ij| < 2^e
+  if (threadIdx.x == 0) expo[(long long)job * d_pad + row] = e;
+  int8_t* out = slices + (long long)job * kOzSlices * nn + (long long)row * d_pad;
+  for (int j = threadIdx.x; j < d_pad; j += 256) {
+    double r = ldexp(x[j], 7 - e);               // |r| < 128, exact
+#pragma unroll
+    for (int s = 0; s < kOzSlices; ++s) {
+      const double q = trunc(r);
+      out[(long long)s * nn + j] = (int8_t)q;
+      r = (r - q) * 128.0;                       // exact
+    }
+  }
+}
+
+__device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// K-major operand, 64-byte swizzle: rows of 64 B, 8-row atoms 512 B apart (SBO), version 1.
+__device__ __forceinline__ uint64_t sdesc_k64(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | (1ull << 16) | (32ull << 32) | (1ull << 46) | (4ull << 61);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kOzThreads, 1)
+    ns_ozaki_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                            const OzParams p) {
+  const int job = blockIdx.y;
+  if (p.state != nullptr && p.state[job].done) return;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOzStages * kOzStageBytes);
+  uint64_t* empty = full + kOzStages;
+  uint64_t* tmem_full = empty + kOzStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  __shared__ double red[4];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int2 tile = p.tiles[blockIdx.x];
+  const int I = tile.x, J2 = tile.y;     // 128-row block, 64-column block
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kOzStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+      for (int kb = 0; kb < p.nkb; ++kb) {
+        const int s = kb % kOzStages;
+        if (kb >= kOzStages) mbar_wait(&empty[s], ((kb / kOzStages) & 1u) ^ 1u);
+        uint8_t* st = smem + s * kOzStageBytes;
+        mbar_arrive_expect_tx(&full[s], kOzStageBytes);
+#pragma unroll
+        for (int q = 0; q < kOzSlices; ++q)
+          tma_load_3d(st + q * kOzSlabA, &tmA, kb * 64, I * kTile, job * kOzSlices + q, &full[s]);
+#pragma unroll
+        for (int q = 0; q < kOzSlices; ++q)
+          tma_load_3d(st + kOzSlices * kOzSlabA + q * kOzSlabB, &tmB, kb * 64, J2 * 64, job * kOzSlices + q,
+                      &full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    // idesc: D=S32 (bits 4-5 = 2), A=B=signed int8 (bits 7-9, 10-12 = 1), K-major, N=64, M=128
+    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(64 >> 3) << 17) |
+                           ((uint32_t)(kTile >> 4) << 24);
+    for (int kb = 0; kb < p.nkb; ++kb) {
+      const int s = kb % kOzStages;
+      mbar_wait(&full[s], static_cast<uint32_t>(kb / kOzStages) & 1u);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t a0 = smem_u32(smem + s * kOzStageBytes);
+        const uint32_t b0 = a0 + kOzSlices * kOzSlabA;
+#pragma unroll
+        for (int g = 2; g <= kOzSlices + 1; ++g) {
+          const uint32_t acc = tmem + (uint32_t)((g - 2) * 64);
+#pragma unroll
+          for (int sa = 1; sa < g; ++sa) {
+            const int sb = g - sa;
+            if (sa > kOzSlices || sb > kOzSlices) continue;
+            const uint32_t aa = a0 + (sa - 1) * kOzSlabA, bb = b0 + (sb - 1) * kOzSlabB;
+            const bool first = (kb == 0) && (sa == ((g - 1 > kOzSlices) ? g - kOzSlices : 1));
+            umma_i8(acc, sdesc_k64(aa), sdesc_k64(bb), idesc, first ? 0u : 1u);
+            umma_i8(acc, sdesc_k64(aa + 32), sdesc_k64(bb + 32), idesc, 1u);
+          }
+        }
+        umma_commit(&empty[s]);
+        if (kb == p.nkb - 1) umma_commit(tmem_full);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---------------- epilogue: 7 INT32 group sums -> FP64 (exact), weighted, scaled ----------------
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    double acc[64];
+#pragma unroll
+    for (int c = 0; c < 64; ++c) acc[c] = 0.0;
+#pragma unroll 1
+    for (int g = kOzSlices + 1; g >= 2; --g) {       // smallest weights first
+      const double w = ldexp(1.0, -7 * g);
+#pragma unroll
+      for (int c0 = 0; c0 < 64; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((g - 2) * 64 + c0), v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[c0 + i] = fma((double)(int)v[i], w, acc[c0 + i]);
+      }
+    }
+    const int er = p.expP[(long long)job * p.ld + I * kTile + r];
+    double* S = reinterpret_cast<double*>(smem);   // [128][65]; ring idle after tmem_full
+#pragma unroll
+    for (int c = 0; c < 64; ++c) S[r * 65 + c] = ldexp(acc[c], er + p.expQ[(long long)job * p.ld + J2 * 64 + c]);
+  }
+  tc_fence_before();
+  __syncthreads();
+
+  if (warp >= 2) {
+    double* S = reinterpret_cast<double*>(smem);
+    const int tid = threadIdx.x - 64;   // 0..127
+    const long long ld = p.ld;
+    const long long base = (long long)job * p.job_stride;
+    double* C = p.C + base;
+    const int i0 = I * kTile, j0 = J2 * 64;
+    double part = 0.0;
+    if (MODE == 2) {
+      for (int idx = tid; idx < kTile * 64; idx += 128) {
+        const int rr = idx >> 6, cc = idx & 63;
+        C[(long long)(i0 + rr) * ld + j0 + cc] = S[rr * 65 + cc];
+      }
+    } else {
+      const double* X = p.Xold + base;
+      // pass A: elements with j >= i (row-major, coalesced); update / residual / trace
+      for (int idx = tid; idx < kTile * 64; idx += 128) {
+        const int rr = idx >> 6, cc = idx & 63;
+        const int gi = i0 + rr, gj = j0 + cc;
+        if (gj < gi) continue;
+        double v = S[rr * 65 + cc];
+        const long long g = (long long)gi * ld + gj;
+        if (MODE == 1) {
+          v = fma(p.cb, v, p.ca * X[g]);
+          S[rr * 65 + cc] = v;
+          if (gi == gj && gi < p.d) part += v;
+        } else {
+          if (gj > gi) part += 2.0 * v * v;
+          else {
+            const double e = (gi < p.d) ? v - 1.0 : v;
+            part += e * e;
+          }
+        }
+        C[g] = v;
+      }
+      named_bar_sync(1, 128);
+      // pass B: mirrors C[j][i] (threads along i: coalesced)
+      for (int idx = tid; idx < kTile * 64; idx += 128) {
+        const int cc = idx >> 7, rr = idx & 127;
+        const int gi = i0 + rr, gj = j0 + cc;
+        if (gj <= gi) continue;
+        C[(long long)gj * ld + gi] = S[rr * 65 + cc];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if (lane == 0) red[warp - 2] = part;
+      named_bar_sync(1, 128);
+      if (tid == 0) {
+        const double s = ((red[0] + red[1]) + red[2]) + red[3];
+        if (MODE == 0) p.partial[(long long)job * p.n_tiles + blockIdx.x] = s;
+        else if (j0 <= i0 + kTile - 1 && j0 + 63 >= i0) p.partial[(long long)job * (2 * (p.ld / kTile)) + J2] = s;
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+cudaError_t launch_ozaki_slice(const double* X, int8_t* slices, int* expo, int d_pad, int batch, cudaStream_t st) {
+  dim3 grid(d_pad, batch);
+  ns_ozaki_slice_kernel<<<grid, 256, 0, st>>>(X, slices, expo, d_pad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ozaki_product(const CUtensorMap& tmA, const CUtensorMap& tmB, const OzParams& p, int batch,
+                                 cudaStream_t st) {
+  static bool attr[3] = {false, false, false};
+  dim3 grid(p.n_tiles, batch);
+  switch (p.mode) {
+    case 0:
+      if (!attr[0]) { cudaFuncSetAttribute(ns_ozaki_product_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOzSmemBytes); attr[0] = true; }
+      ns_ozaki_product_kernel<0><<<grid, kOzThreads, kOzSmemBytes, st>>>(tmA, tmB, p);
+      break;
+    case 1:
+      if (!attr[1]) { cudaFuncSetAttribute(ns_ozaki_product_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOzSmemBytes); attr[1] = true; }
+      ns_ozaki_product_kernel<1><<<grid, kOzThreads, kOzSmemBytes, st>>>(tmA, tmB, p);
+      break;
+    default:
+      if (!attr[2]) { cudaFuncSetAttribute(ns_ozaki_product_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOzSmemBytes); attr[2] = true; }
+      ns_ozaki_product_kernel<2><<<grid, kOzThreads, kOzSmemBytes, st>>>(tmA, tmB, p);
+      break;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace nsr

@@ -469,3 +469,60 @@ def test_alg1_scan_matches_oracle(nsr):
         rate = sum(r["success"] for r in res) / len(res)
         print(f"m={m}: success rate {rate:.2f}, agreement with oracle {agree}/{len(kk)}")
         assert agree == len(kk)
+
+
+# ------------------------------------------------------------------ N4: Ozaki-split FP64 on INT8 tensor cores
+@pytest.mark.parametrize("d,mode", [(128, 0), (300, 0), (515, 1), (256, 2), (200, 2), (1024, 0)])
+def test_ozaki_product_kernel(nsr, d, mode):
+    """7-slice Ozaki products on tcgen05 kind::i8: FP64-class accuracy (relative to |row||col|)."""
+    rng = np.random.default_rng(99 + d)
+    A = rng.standard_normal((d, d))
+    A = 0.5 * (A + A.T) / math.sqrt(d)
+    B = A @ A if mode != 2 else rng.standard_normal((d, d))
+    B = 0.5 * (B + B.T)
+    Ag, Bg = torch.from_numpy(A).to(_dev()), torch.from_numpy(B).to(_dev())
+    C = nsr.ns_symm_product(Ag, Bg, mode=mode, prec=nsr.NS_PREC_FP64_OZAKI).cpu().numpy()
+    ref = A @ B if mode != 1 else 1.5 * A - 0.5 * (A @ B)
+    scale = np.max(np.abs(A)) * np.max(np.abs(B)) * d
+    err = np.max(np.abs(C - ref)) / scale
+    print(f"ozaki d={d} mode={mode}: max err / (max|A| max|B| d) = {err:.2e}")
+    assert err <= 1e-14, err
+    if mode != 2:
+        assert np.array_equal(C, C.T)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_ozaki_cfg0(nsr, seed):
+    p = workloads.cfg0_controlled(seed)
+    o = ons.ns_reflector(p.H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode, trace_residuals=True)
+    R, res = nsr.ns_reflector(torch.from_numpy(p.H).to(_dev()), p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode,
+                              prec=nsr.NS_PREC_FP64_OZAKI)
+    assert res["steps"] == o["steps"] and res["cert"] == 3 and res["flags"] == o["flags"]
+    assert checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= TOL_R
+
+
+def test_ozaki_cfg3_recipe(nsr):
+    p = workloads.cfg3_dense(d=1024, k=64)
+    o = ons.ns_reflector(p.H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    R, res = nsr.ns_reflector(torch.from_numpy(p.H).to(_dev()), p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode,
+                              prec=nsr.NS_PREC_FP64_OZAKI)
+    err = checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"])
+    print(f"ozaki cfg3 d=1024: steps {res['steps']} (oracle {o['steps']}), err {err:.2e}")
+    assert res["steps"] == o["steps"] and res["cert"] == 64 and res["flags"] == ons.CONVERGED
+    assert err <= TOL_R
+    assert torch.equal(R, R.T)
+
+
+def test_ozaki_cfg3_full_size_sampled(nsr):
+    """configs[3] at d=16384 through the Ozaki path: steps == prediction, cert, closed-form columns."""
+    p = workloads.cfg3_dense(form=False)
+    H = workloads.householder_form_fast(p.Vh, p.lam, device=_dev())
+    R, res = nsr.ns_reflector(H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode, prec=nsr.NS_PREC_FP64_OZAKI)
+    steps_pred = scalar.predict_run((p.lam - p.s) / p.alpha, 100, 1e-10, True)[0]
+    assert res["steps"] == steps_pred and res["cert"] == 1024 and res["flags"] == ons.CONVERGED
+    cols = np.array([0, 7, 8000, 16383])
+    Rc = closed_form.householder_reflector_columns(p.Vh, p.lam, 0.0, cols)
+    Rg = R[:, torch.as_tensor(cols, device=_dev())].cpu().numpy()
+    err = np.sqrt(np.mean(np.sum((Rg - Rc) ** 2, axis=0)))
+    print(f"ozaki d=16384: err~{err:.3e}")
+    assert err <= TOL_R      # north_star bar; 8 slices of 7 bits give ~1e-13 per entry at this d

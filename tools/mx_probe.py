@@ -13,7 +13,8 @@ def main():
     dev = torch.device("cuda:0")
     A = torch.randn(d, d, dtype=torch.float64, device=dev)
     A = (A + A.T) * (0.5 / d ** 0.5)
-    for prec, name in ((nsr.NS_PREC_MIXED_BF16X3, "bf16x3"), (nsr.NS_PREC_FP64, "fp64")):
+    for prec, name in ((nsr.NS_PREC_FP64_OZAKI, "ozaki_i8"), (nsr.NS_PREC_MIXED_BF16X3, "bf16x3"),
+                       (nsr.NS_PREC_FP64, "fp64")):
         ws = nsr.alloc_workspace(nsr.ns_workspace_bytes(d, prec), dev)
         C = torch.empty_like(A)
         for mode in (0, 2):
