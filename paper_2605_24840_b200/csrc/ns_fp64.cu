@@ -83,8 +83,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  double* sA = reinterpret_cast<double*>(smem);                                   // [stages][128*16]
-  double* sB = reinterpret_cast<double*>(smem + kStages * kTile * kBK * 8);      // [stages][128*16]
+  double* sA = reinterpret_cast<double*>(smem);                                           // [stages*kSPS][128*16]
+  double* sB = reinterpret_cast<double*>(smem + kStages * kSPS * kTile * kBK * 8);       // [stages*kSPS][128*16]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
   __shared__ double red[kConsumerWarps];
@@ -107,13 +107,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       tma_prefetch_desc(&tmP);
       tma_prefetch_desc(&tmQ);
-      for (int kt = 0; kt < p.nk; ++kt) {
+      const int nst = p.nk / kSPS;
+      for (int kt = 0; kt < nst; ++kt) {
         const int s = kt % kStages;
         const uint32_t use = kt / kStages;
         if (kt >= kStages) mbar_wait(&empty[s], (use & 1u) ^ 1u);
         mbar_arrive_expect_tx(&full[s], kStageBytes);
-        tma_load_3d(sA + s * kTile * kBK, &tmP, kt * kBK, I * kTile, job, &full[s]);
-        tma_load_3d(sB + s * kTile * kBK, &tmQ, kt * kBK, J * kTile, job, &full[s]);
+#pragma unroll
+        for (int u = 0; u < kSPS; ++u) {
+          tma_load_3d(sA + (s * kSPS + u) * kTile * kBK, &tmP, (kt * kSPS + u) * kBK, I * kTile, job, &full[s]);
+          tma_load_3d(sB + (s * kSPS + u) * kTile * kBK, &tmQ, (kt * kSPS + u) * kBK, J * kTile, job, &full[s]);
+        }
       }
     }
     return;
@@ -138,13 +142,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 
-  for (int kt = 0; kt < p.nk; ++kt) {
+  const int nst = p.nk / kSPS;
+  for (int kt = 0; kt < nst; ++kt) {
     const int s = kt % kStages;
     mbar_wait(&full[s], static_cast<uint32_t>(kt / kStages) & 1u);
-    const uint32_t aS = sA_u32 + s * (kTile * kBK * 8) + a_row;
-    const uint32_t bS = sB_u32 + s * (kTile * kBK * 8) + b_row;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int hh = 0; hh < 2 * kSPS; ++hh) {
+    const int h = hh & 1;
+    const uint32_t aS = sA_u32 + (s * kSPS + (hh >> 1)) * (kTile * kBK * 8) + a_row;
+    const uint32_t bS = sB_u32 + (s * kSPS + (hh >> 1)) * (kTile * kBK * 8) + b_row;
+    {
       const uint32_t off = h ? off_h1 : off_h0;
       // B fragments for both k-values of this half-slab stay live (16 regs); A fragments are
       // streamed one m-row at a time so the 128 accumulator registers fit the 168-register
@@ -161,6 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a1, b[ni][1]);
       }
+    }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);

@@ -9,10 +9,11 @@ namespace nsr {
 
 constexpr int kTile = 128;      // output tile edge (rows of P, rows of Q)
 constexpr int kBK = 16;         // k-slab per pipeline stage: 16 doubles = one 128-B swizzle row
-constexpr int kStages = 6;      // TMA ring depth (6 x 32 KB)
+constexpr int kSPS = 2;         // 16-wide k-slabs per pipeline stage (one mbarrier wait per 2 slabs)
+constexpr int kStages = 3;      // TMA ring depth (3 x 64 KB)
 constexpr int kConsumerWarps = 8;
 constexpr int kThreads = 32 * (1 + kConsumerWarps);   // warp 0 = TMA producer
-constexpr int kStageBytes = 2 * kTile * kBK * 8;      // A + B per stage = 32 KB
+constexpr int kStageBytes = kSPS * 2 * kTile * kBK * 8;   // A + B per stage = 64 KB
 constexpr int kEpiPitch = kTile + 1;                  // staging row pitch (doubles), odd => conflict-free columns
 constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 
