@@ -222,6 +222,7 @@ Profiler& prof() {
 
 struct HostRing {
   int* slots = nullptr;
+  DevState* pstate = nullptr;   // pinned landing slot for single-problem results
   cudaEvent_t ev[16];
   bool ok = false;
 };
@@ -230,6 +231,7 @@ HostRing& ring() {
   static thread_local HostRing r;
   if (!r.ok) {
     if (cudaHostAlloc(&r.slots, 16 * sizeof(int), cudaHostAllocDefault) != cudaSuccess) return r;
+    if (cudaHostAlloc(&r.pstate, sizeof(DevState), cudaHostAllocDefault) != cudaSuccess) r.pstate = nullptr;
     for (int i = 0; i < 16; ++i) cudaEventCreateWithFlags(&r.ev[i], cudaEventDisableTiming);
     r.ok = true;
   }
@@ -288,17 +290,27 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
   HostRing& rg = ring();
   if (!rg.ok) return fail(NS_ERR_CUDA, "pinned status ring allocation failed");
 
-  NS_CUDA(cudaMemcpyAsync(djobs, jobs.data(), jobs.size() * sizeof(JobParams), cudaMemcpyHostToDevice, st));
   if (small_dpad(L.d) != 0) {
-    // d <= 96: one fused kernel (one CTA per problem runs the whole loop in shared memory)
+    // d <= 96: one fused kernel (one CTA per problem runs the whole loop in shared memory); a single
+    // problem passes its scalars by value and returns its state through pinned memory (no staging).
     LoopParams lps{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0, -1, 0, opt.ca, opt.cb};
-    NS_CUDA(launch_small(H, ldh, h_stride, djobs, lps, R, ldr, r_stride, state, batch, st));
+    if (batch > 1)
+      NS_CUDA(cudaMemcpyAsync(djobs, jobs.data(), jobs.size() * sizeof(JobParams), cudaMemcpyHostToDevice, st));
+    NS_CUDA(launch_small(H, ldh, h_stride, batch > 1 ? djobs : nullptr, jobs[0], lps, R, ldr, r_stride, state, batch,
+                         st));
     states.resize(batch);
-    NS_CUDA(cudaMemcpyAsync(states.data(), state, sizeof(DevState) * batch, cudaMemcpyDeviceToHost, st));
-    NS_CUDA(cudaStreamSynchronize(st));
+    if (batch == 1 && rg.pstate) {
+      NS_CUDA(cudaMemcpyAsync(rg.pstate, state, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+      NS_CUDA(cudaStreamSynchronize(st));
+      states[0] = *rg.pstate;
+    } else {
+      NS_CUDA(cudaMemcpyAsync(states.data(), state, sizeof(DevState) * batch, cudaMemcpyDeviceToHost, st));
+      NS_CUDA(cudaStreamSynchronize(st));
+    }
     if (launches) *launches = 1;
     return NS_OK;
   }
+  NS_CUDA(cudaMemcpyAsync(djobs, jobs.data(), jobs.size() * sizeof(JobParams), cudaMemcpyHostToDevice, st));
   std::vector<int2> tl = make_tiles(L.n);
   NS_CUDA(cudaMemcpyAsync(tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
 

@@ -20,7 +20,7 @@ namespace nsr {
 template <int DP>
 __global__ void __launch_bounds__(kSmallThreads, 1)
     ns_small_kernel(const double* __restrict__ H, long long ldh, long long h_stride, const JobParams* __restrict__ jobs,
-                    LoopParams lp, double* __restrict__ R, long long ldr, long long r_stride,
+                    JobParams job0, LoopParams lp, double* __restrict__ R, long long ldr, long long r_stride,
                     DevState* __restrict__ state) {
   constexpr int P = DP + 4;
   extern __shared__ __align__(16) double sm[];
@@ -30,7 +30,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
   __shared__ double red[kSmallThreads / 32];
   const int job = blockIdx.x;
   const double* Hj = H + (long long)job * h_stride;
-  const double s = jobs[job].s, alpha = jobs[job].alpha;
+  const JobParams jp = jobs ? jobs[job] : job0;   // batch of one: parameters by value (no H2D copy)
+  const double s = jp.s, alpha = jp.alpha;
   const int d = lp.d;
   // X_0 = (H - sI)/alpha from the upper triangle, zero padded
   for (int e = threadIdx.x; e < DP * DP; e += kSmallThreads) {
@@ -101,7 +102,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
       if (half < 0) cert = -cert;
       if (fabs(half - (double)cert) > 0.25) flags |= 32;
     }
-    if (cert != (long long)jobs[job].k) flags |= 4;
+    if (cert != (long long)jp.k) flags |= 4;
     st.cert = cert;
     st.flags = flags;
     state[job] = st;
@@ -110,21 +111,23 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
 
 int small_dpad(int d) { return d <= 32 ? 32 : d <= 64 ? 64 : d <= 96 ? 96 : 0; }
 
-cudaError_t launch_small(const double* H, long long ldh, long long h_stride, const JobParams* jobs, LoopParams lp,
-                         double* R, long long ldr, long long r_stride, DevState* state, int batch, cudaStream_t st) {
+cudaError_t launch_small(const double* H, long long ldh, long long h_stride, const JobParams* jobs, JobParams job0,
+                         LoopParams lp, double* R, long long ldr, long long r_stride, DevState* state, int batch,
+                         cudaStream_t st) {
+  static bool attr[3] = {false, false, false};
   const int dp = small_dpad(lp.d);
   const size_t smem = (size_t)3 * dp * (dp + 4) * sizeof(double);
   switch (dp) {
     case 32:
-      ns_small_kernel<32><<<batch, kSmallThreads, smem, st>>>(H, ldh, h_stride, jobs, lp, R, ldr, r_stride, state);
+      ns_small_kernel<32><<<batch, kSmallThreads, smem, st>>>(H, ldh, h_stride, jobs, job0, lp, R, ldr, r_stride, state);
       break;
     case 64:
-      cudaFuncSetAttribute(ns_small_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      ns_small_kernel<64><<<batch, kSmallThreads, smem, st>>>(H, ldh, h_stride, jobs, lp, R, ldr, r_stride, state);
+      if (!attr[1]) { cudaFuncSetAttribute(ns_small_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr[1] = true; }
+      ns_small_kernel<64><<<batch, kSmallThreads, smem, st>>>(H, ldh, h_stride, jobs, job0, lp, R, ldr, r_stride, state);
       break;
     case 96:
-      cudaFuncSetAttribute(ns_small_kernel<96>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      ns_small_kernel<96><<<batch, kSmallThreads, smem, st>>>(H, ldh, h_stride, jobs, lp, R, ldr, r_stride, state);
+      if (!attr[2]) { cudaFuncSetAttribute(ns_small_kernel<96>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr[2] = true; }
+      ns_small_kernel<96><<<batch, kSmallThreads, smem, st>>>(H, ldh, h_stride, jobs, job0, lp, R, ldr, r_stride, state);
       break;
     default:
       return cudaErrorInvalidValue;

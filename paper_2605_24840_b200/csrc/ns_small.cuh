@@ -22,14 +22,19 @@ __device__ __forceinline__ void small_product(const double* __restrict__ A, cons
   for (int f = warp; f < NF * NF; f += kSmallThreads / 32) {
     const int fi = f / NF, fj = f % NF;
     if (fi > fj) continue;                 // upper fragments only; mirrored below
-    double c0 = 0.0, c1 = 0.0;
+    // four independent accumulator chains over k (the DMMA latency, not its throughput, bounds a
+    // single 8x8 fragment at this size), summed in a fixed order
+    double c[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
     const double* a = A + (fi * 8 + g) * P + t;
     const double* b = B + (fj * 8 + g) * P + t;
-#pragma unroll 8
-    for (int k = 0; k < DP; k += 4) dmma_8x8x4(c0, c1, a[k], b[k]);
-    const int r = fi * 8 + g, c = fj * 8 + 2 * t;
-    C[r * P + c] = c0;
-    C[r * P + c + 1] = c1;
+#pragma unroll
+    for (int k = 0; k < DP; k += 16) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dmma_8x8x4(c[u][0], c[u][1], a[k + 4 * u], b[k + 4 * u]);
+    }
+    const int r = fi * 8 + g, cc = fj * 8 + 2 * t;
+    C[r * P + cc] = (c[0][0] + c[1][0]) + (c[2][0] + c[3][0]);
+    C[r * P + cc + 1] = (c[0][1] + c[1][1]) + (c[2][1] + c[3][1]);
   }
   __syncthreads();
   // mirror: lower triangle (and the lower half of diagonal fragments) from the upper values
