@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 #include <algorithm>
@@ -127,8 +128,17 @@ std::vector<int2> make_tiles_full(int n) {
 // triangle of super-blocks), row-major inside each.  Co-resident CTAs then share a
 // few dozen row panels, so each k-slab of a panel is fetched from HBM about once per
 // wave and re-read from L2 by the other CTAs.
+int tile_group() {
+  static int g = [] {
+    const char* e = getenv("NS_TILE_GROUP");   // experiment knob: super-block edge of the tile order
+    int v = e ? atoi(e) : 0;
+    return v > 0 ? v : 8;
+  }();
+  return g;
+}
+
 std::vector<int2> make_tiles(int n) {
-  const int G = 12;
+  const int G = tile_group();
   std::vector<int2> v;
   v.reserve((size_t)n * (n + 1) / 2);
   for (int SI = 0; SI < n; SI += G)
