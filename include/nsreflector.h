@@ -53,7 +53,7 @@ extern "C" {
 typedef enum {
   NS_PREC_FP64 = 0,          /* FP64 DMMA contraction (accuracy path) */
   NS_PREC_MIXED_BF16X3 = 1,  /* tcgen05 BF16x3 steps -> switch -> re-anchor -> FP64 steps (C16) */
-  NS_PREC_MIXED_TF32X3 = 2,  /* reserved: tcgen05 split-TF32 path (returns NS_ERR_UNSUPPORTED) */
+  NS_PREC_MIXED_TF32X3 = 2,  /* as MIXED_BF16X3 with TF32 hi/lo splits (tcgen05 kind::tf32; more margin, half rate) */
   NS_PREC_FP64_OZAKI = 3     /* FP64-accurate products emulated on tcgen05 INT8 (Ozaki split, 7 slices);
                                 SURVEY N4; single problem, d <= 16384 (INT32 group sums stay exact) */
 } ns_precision_t;
@@ -135,7 +135,8 @@ size_t ns_workspace_bytes_batched(int64_t d, int64_t batch, ns_precision_t prec)
  *   max_steps >= 0; tol >= 0 (0 = fixed max_steps updates); tm tolerance mode.
  *   prec   NS_PREC_FP64, or NS_PREC_MIXED_BF16X3: BF16x3 tcgen05 steps until the switch
  *          threshold, one FP64 re-anchor solve, FP64 steps to tol (single problem only;
- *          NS_PREC_MIXED_TF32X3 returns NS_ERR_UNSUPPORTED).
+ *          NS_PREC_MIXED_TF32X3 the same with TF32 splits; NS_PREC_FP64_OZAKI: FP64 products emulated
+ *          on the INT8 tensor cores, d <= 16640).
  *   R      device, d x d, leading dim ldr >= d; written in full, bitwise symmetric.
  *   ws     device workspace, ws_bytes >= ns_workspace_bytes(d, prec).
  *   stream cudaStream_t (as void*); NULL = legacy default stream.

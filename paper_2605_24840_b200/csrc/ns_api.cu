@@ -54,7 +54,7 @@ struct Layout {
          off_ores = 0, off_otr = 0, off_otiles = 0, total = 0;
 };
 
-Layout make_layout(int64_t d, int64_t batch, bool mixed = false, bool ozaki = false) {
+Layout make_layout(int64_t d, int64_t batch, bool mixed = false, bool ozaki = false, bool tf32 = false) {
   Layout L;
   L.d = static_cast<int>(d);
   L.d_pad = static_cast<int>((d + kTile - 1) / kTile * kTile);
@@ -85,7 +85,7 @@ Layout make_layout(int64_t d, int64_t batch, bool mixed = false, bool ozaki = fa
     L.off_otiles = o; o = align256(o + sizeof(int2) * (size_t)2 * L.n * L.n);           // sym or full 128x64 list
   }
   if (mixed) {
-    const size_t planes = (size_t)L.d_pad * L.d_pad * 2 * sizeof(uint16_t) * (size_t)batch;
+    const size_t planes = (size_t)L.d_pad * L.d_pad * 2 * (tf32 ? 4 : 2) * (size_t)batch;   // hi + lo
     L.off_px = o; o = align256(o + planes);     // bf16 hi/lo planes of X_j (even j) / CG direction P
     L.off_pxb = o; o = align256(o + planes);    // bf16 hi/lo planes of X_j (odd j)
     L.off_py = o; o = align256(o + planes);     // bf16 hi/lo planes of Y / |A|
@@ -197,14 +197,16 @@ ns_status_t encode_map_i8(CUtensorMap* m, const int8_t* base, int d_pad, long lo
 
 // 3-D map over `nplanes` row-major d_pad x d_pad BF16 planes; box = 64 (k) x 128 (rows) x 1, 128-B swizzle
 // (the layout the UMMA shared-memory descriptors in ns_mixed.cu describe).
-ns_status_t encode_map_bf16(CUtensorMap* m, const uint16_t* base, int d_pad, long long nplanes) {
+ns_status_t encode_map_bf16(CUtensorMap* m, const void* base, int d_pad, long long nplanes, bool tf32 = false) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(NS_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  const cuuint64_t esz = tf32 ? 4 : 2;
   cuuint64_t dims[3] = {(cuuint64_t)d_pad, (cuuint64_t)d_pad, (cuuint64_t)nplanes};
-  cuuint64_t strides[2] = {(cuuint64_t)d_pad * 2, (cuuint64_t)d_pad * (cuuint64_t)d_pad * 2};
-  cuuint32_t box[3] = {(cuuint32_t)kMxBK, (cuuint32_t)kTile, 1};
+  cuuint64_t strides[2] = {(cuuint64_t)d_pad * esz, (cuuint64_t)d_pad * (cuuint64_t)d_pad * esz};
+  cuuint32_t box[3] = {(cuuint32_t)(128 / esz), (cuuint32_t)kTile, 1};   // 128-byte rows: 64 bf16 or 32 tf32
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<uint16_t*>(base), dims, strides, box, estr,
+  CUresult r = enc(m, tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                   const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(NS_ERR_CUDA, "cuTensorMapEncodeTiled (bf16) failed (%d)", (int)r);
@@ -253,8 +255,8 @@ ns_status_t check_common(int64_t d, int32_t max_steps, double tol, ns_tolmode_t 
   if (max_steps < 0) return fail(NS_ERR_INVALID_ARG, "max_steps must be >= 0");
   if (!(tol >= 0.0) || !std::isfinite(tol)) return fail(NS_ERR_INVALID_ARG, "tol must be finite and >= 0");
   if (tm != NS_TOL_ABS && tm != NS_TOL_PER_SQRT_D) return fail(NS_ERR_INVALID_ARG, "bad tolerance mode");
-  if (prec == NS_PREC_MIXED_TF32X3) return fail(NS_ERR_UNSUPPORTED, "the TF32x3 mode is not available in this build");
-  if (prec != NS_PREC_FP64 && prec != NS_PREC_MIXED_BF16X3 && prec != NS_PREC_FP64_OZAKI)
+  if (prec != NS_PREC_FP64 && prec != NS_PREC_MIXED_BF16X3 && prec != NS_PREC_MIXED_TF32X3 &&
+      prec != NS_PREC_FP64_OZAKI)
     return fail(NS_ERR_INVALID_ARG, "bad precision");
   return NS_OK;
 }
@@ -467,7 +469,8 @@ ns_status_t run_ozaki(const Layout& L, uint8_t* ws, const double* H, long long l
 // Mixed path (single problem): BF16x3 tcgen05 steps -> switch -> re-anchor -> FP64 steps.
 ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long ldh, const JobParams& jp,
                       int32_t max_steps, double tol, ns_tolmode_t tm, double* R, long long ldr, cudaStream_t st,
-                      const Opts& opt, DevState& out_state, int* launches) {
+                      const Opts& opt, DevState& out_state, int* launches, bool tf32 = false) {
+  const int mx_nkb = L.d_pad / (tf32 ? 32 : kMxBK);
   double* Xa = reinterpret_cast<double*>(ws + L.off_xa);
   double* Xb = reinterpret_cast<double*>(ws + L.off_xb);
   double* Y = reinterpret_cast<double*>(ws + L.off_y);
@@ -478,9 +481,9 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
   double* trp = reinterpret_cast<double*>(ws + L.off_tr);
   double* cgpart = reinterpret_cast<double*>(ws + L.off_cgpart);
   CgScalars* cgsc = reinterpret_cast<CgScalars*>(ws + L.off_cgsc);
-  uint16_t* PXa = reinterpret_cast<uint16_t*>(ws + L.off_px);
-  uint16_t* PXb = reinterpret_cast<uint16_t*>(ws + L.off_pxb);
-  uint16_t* PY = reinterpret_cast<uint16_t*>(ws + L.off_py);
+  void* PXa = ws + L.off_px;
+  void* PXb = ws + L.off_pxb;
+  void* PY = ws + L.off_py;
   int2* tiles = reinterpret_cast<int2*>(ws + L.off_tiles);
   int2* full = reinterpret_cast<int2*>(ws + L.off_full);
   JobParams* djobs = reinterpret_cast<JobParams*>(ws + L.off_jobs);
@@ -501,16 +504,16 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
   if ((s = encode_map(&tmB, Xb, L.d_pad, 1)) != NS_OK) return s;
   if ((s = encode_map(&tmY, Y, L.d_pad, 1)) != NS_OK) return s;
   if ((s = encode_map(&tmAh, Ahat, L.d_pad, 1)) != NS_OK) return s;
-  if ((s = encode_map_bf16(&tmPXa, PXa, L.d_pad, 2)) != NS_OK) return s;
-  if ((s = encode_map_bf16(&tmPXb, PXb, L.d_pad, 2)) != NS_OK) return s;
-  if ((s = encode_map_bf16(&tmPY, PY, L.d_pad, 2)) != NS_OK) return s;
+  if ((s = encode_map_bf16(&tmPXa, PXa, L.d_pad, 2, tf32)) != NS_OK) return s;
+  if ((s = encode_map_bf16(&tmPXb, PXb, L.d_pad, 2, tf32)) != NS_OK) return s;
+  if ((s = encode_map_bf16(&tmPY, PY, L.d_pad, 2, tf32)) != NS_OK) return s;
 
   int nl = 0;
   NS_CUDA(launch_zero_state(state, 1, n_active, st));
   NS_CUDA(launch_init(H, ldh, 0, Xa, djobs, L.d, L.d_pad, 1, st));
   NS_CUDA(cudaMemcpyAsync(Ahat, Xa, mat_bytes, cudaMemcpyDeviceToDevice, st));
   NS_CUDA(launch_trace_partials(Xa, L.d, L.d_pad, 1, trp, st));
-  NS_CUDA(launch_split_planes(Xa, PXa, L.d_pad, 1, st));
+  NS_CUDA(launch_split_planes(Xa, PXa, L.d_pad, 1, st, tf32));
   nl += 4;
 
   // ---------------- phase 1: BF16x3 steps until the switch threshold ----------------
@@ -531,13 +534,13 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
     double* Xc = odd ? Xb : Xa;
     double* Xn = odd ? Xa : Xb;
     const CUtensorMap& tPc = odd ? tmPXb : tmPXa;
-    uint16_t* PXn = odd ? PXa : PXb;
-    MxParams sq{tiles, L.n_tiles, L.d_pad / kMxBK, L.d, L.d_pad, js, Y, nullptr, PY, res, state, 0};
+    void* PXn = odd ? PXa : PXb;
+    MxParams sq{tiles, L.n_tiles, mx_nkb, L.d, L.d_pad, js, Y, nullptr, PY, res, state, 0, tf32 ? 1 : 0};
     NS_CUDA(launch_mx_product(tPc, tPc, sq, 1, st));
     NS_CUDA(launch_decide(state, djobs, res, L.n_tiles, trp, L.n, lp_low, 1, n_active, st));
     nl += 2;
     if (j < max_steps) {
-      MxParams up{tiles, L.n_tiles, L.d_pad / kMxBK, L.d, L.d_pad, js, Xn, Xc, PXn, trp, state, 1};
+      MxParams up{tiles, L.n_tiles, mx_nkb, L.d, L.d_pad, js, Xn, Xc, PXn, trp, state, 1, tf32 ? 1 : 0};
       NS_CUDA(launch_mx_product(tPc, tmPY, up, 1, st));
       nl += 1;
     }
@@ -560,7 +563,7 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
       ProdParams pm{full, L.n * L.n, nk, L.d, L.d_pad, 0, Y, nullptr, nullptr, nullptr, 2};
       NS_CUDA(launch_product(tmAh, tXt, pm, 1, st));
       // C = M - M^T -> Xo ; |A| = sym(M) -> bf16 planes PY
-      NS_CUDA(launch_commutator(Y, Xo, PY, L.d_pad, st));
+      NS_CUDA(launch_commutator(Y, Xo, PY, L.d_pad, st, tf32));
       // F' = X~ C^T = -X~ C  (FP64 DMMA, every tile) -> Y
       ProdParams pf{full, L.n * L.n, nk, L.d, L.d_pad, 0, Y, nullptr, nullptr, nullptr, 2};
       NS_CUDA(launch_product(tXt, tXo, pf, 1, st));
@@ -569,11 +572,11 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
       double* E = Ahat;
       NS_CUDA(launch_cg_init(Y, Rc, Pc, E, cgpart, L.d_pad, st, &np));
       NS_CUDA(launch_cg_scalar(cgsc, cgpart, np, 0, st));
-      NS_CUDA(launch_split_planes(Pc, PXa, L.d_pad, 1, st));
+      NS_CUDA(launch_split_planes(Pc, PXa, L.d_pad, 1, st, tf32));
       nl += 6;
       for (int it = 0; it < opt.cg_iters; ++it) {
         // W = |A| P (BF16x3 tcgen05, every tile) -> Xo
-        MxParams pw{full, L.n * L.n, L.d_pad / kMxBK, L.d, L.d_pad, 0, Xo, nullptr, nullptr, nullptr, nullptr, 2};
+        MxParams pw{full, L.n * L.n, mx_nkb, L.d, L.d_pad, 0, Xo, nullptr, nullptr, nullptr, nullptr, 2, tf32 ? 1 : 0};
         NS_CUDA(launch_mx_product(tmPY, tmPXa, pw, 1, st));
         NS_CUDA(launch_cg_pw(Pc, Xo, cgpart, L.d_pad, st));
         NS_CUDA(launch_cg_scalar(cgsc, cgpart, kEwBlocks, 1, st));
@@ -581,7 +584,7 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
         NS_CUDA(launch_cg_scalar(cgsc, cgpart, np, 2, st));
         nl += 5;
         if (it + 1 < opt.cg_iters) {
-          NS_CUDA(launch_cg_direction(Pc, Rc, cgsc, PXa, L.d_pad, st));
+          NS_CUDA(launch_cg_direction(Pc, Rc, cgsc, PXa, L.d_pad, st, tf32));
           nl += 1;
         }
       }
@@ -799,7 +802,8 @@ extern "C" {
 
 size_t ns_workspace_bytes(int64_t d, ns_precision_t prec) {
   if (d < 1) return 0;
-  return make_layout(d, 1, prec == NS_PREC_MIXED_BF16X3, prec == NS_PREC_FP64_OZAKI).total;
+  return make_layout(d, 1, prec == NS_PREC_MIXED_BF16X3 || prec == NS_PREC_MIXED_TF32X3, prec == NS_PREC_FP64_OZAKI,
+                     prec == NS_PREC_MIXED_TF32X3).total;
 }
 
 size_t ns_workspace_bytes_batched(int64_t d, int64_t batch, ns_precision_t prec) {
@@ -835,10 +839,11 @@ ns_status_t ns_reflector_ex(const double* H, int64_t d, int64_t ldh, double s, d
   if (k < 0 || k > d) return fail(NS_ERR_INVALID_ARG, "k must lie in [0, d]");
   if (R == H) return fail(NS_ERR_INVALID_ARG, "R must not alias H");
   if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(NS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
-  const bool mixed = (prec == NS_PREC_MIXED_BF16X3);
+  const bool tf32 = (prec == NS_PREC_MIXED_TF32X3);
+  const bool mixed = (prec == NS_PREC_MIXED_BF16X3) || tf32;
   const bool ozaki = (prec == NS_PREC_FP64_OZAKI);
   if (ozaki && d > kOzMaxD) return fail(NS_ERR_UNSUPPORTED, "the Ozaki path needs d <= %d", kOzMaxD);
-  const Layout L = make_layout(d, 1, mixed, ozaki);
+  const Layout L = make_layout(d, 1, mixed, ozaki, tf32);
   if (ws_bytes < L.total)
     return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
   const Opts o = to_opts(opts);
@@ -851,7 +856,7 @@ ns_status_t ns_reflector_ex(const double* H, int64_t d, int64_t ldh, double s, d
   if (mixed || ozaki) {
     DevState ds;
     st = mixed ? run_mixed(L, static_cast<uint8_t*>(ws), H, ldh, jobs[0], max_steps, tol, tm, R, ldr,
-                           static_cast<cudaStream_t>(stream), o, ds, &nl)
+                           static_cast<cudaStream_t>(stream), o, ds, &nl, tf32)
                : run_ozaki(L, static_cast<uint8_t*>(ws), H, ldh, jobs[0], max_steps, tol, tm, R, ldr,
                            static_cast<cudaStream_t>(stream), o, ds, &nl);
     if (st != NS_OK) return st;
@@ -885,10 +890,11 @@ ns_status_t ns_reflector_host(const double* H_host, int64_t d, int64_t ldh, doub
   if (!(alpha > 0.0) || !std::isfinite(alpha)) return fail(NS_ERR_INVALID_ARG, "alpha must be finite and > 0");
   if (k < 0 || k > d) return fail(NS_ERR_INVALID_ARG, "k must lie in [0, d]");
   if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(NS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
-  const bool mixed = (prec == NS_PREC_MIXED_BF16X3);
+  const bool tf32 = (prec == NS_PREC_MIXED_TF32X3);
+  const bool mixed = (prec == NS_PREC_MIXED_BF16X3) || tf32;
   const bool ozaki = (prec == NS_PREC_FP64_OZAKI);
   if (ozaki && d > kOzMaxD) return fail(NS_ERR_UNSUPPORTED, "the Ozaki path needs d <= %d", kOzMaxD);
-  const Layout L = make_layout(d, 1, mixed, ozaki);
+  const Layout L = make_layout(d, 1, mixed, ozaki, tf32);
   if (ws_bytes < L.total)
     return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
@@ -901,7 +907,7 @@ ns_status_t ns_reflector_host(const double* H_host, int64_t d, int64_t ldh, doub
   std::vector<DevState> states(1);
   int nl = 0;
   if (mixed)
-    st = run_mixed(L, w, stage, d, jobs[0], max_steps, tol, tm, stage, d, cs, Opts{}, states[0], &nl);
+    st = run_mixed(L, w, stage, d, jobs[0], max_steps, tol, tm, stage, d, cs, Opts{}, states[0], &nl, tf32);
   else if (ozaki)
     st = run_ozaki(L, w, stage, d, jobs[0], max_steps, tol, tm, stage, d, cs, Opts{}, states[0], &nl);
   else
@@ -952,14 +958,16 @@ ns_status_t ns_symm_product(const double* A, const double* B, double* C, int64_t
   if (d < 1 || d > 65536) return fail(NS_ERR_INVALID_ARG, "bad d");
   if (ld < d) return fail(NS_ERR_INVALID_ARG, "ld must be >= d");
   if (mode < 0 || mode > 2) return fail(NS_ERR_INVALID_ARG, "mode must be 0, 1 or 2");
-  if (prec != NS_PREC_FP64 && prec != NS_PREC_MIXED_BF16X3 && prec != NS_PREC_FP64_OZAKI)
+  if (prec != NS_PREC_FP64 && prec != NS_PREC_MIXED_BF16X3 && prec != NS_PREC_MIXED_TF32X3 &&
+      prec != NS_PREC_FP64_OZAKI)
     return fail(NS_ERR_UNSUPPORTED, "precision not available");
   if (prec == NS_PREC_FP64_OZAKI && d > kOzMaxD) return fail(NS_ERR_UNSUPPORTED, "Ozaki products need d <= %d", kOzMaxD);
   if (!A || !B || !C || !ws) return fail(NS_ERR_INVALID_ARG, "null pointer argument");
   if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(NS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
-  const bool mixed = (prec == NS_PREC_MIXED_BF16X3);
+  const bool tf32 = (prec == NS_PREC_MIXED_TF32X3);
+  const bool mixed = (prec == NS_PREC_MIXED_BF16X3) || tf32;
   const bool ozaki = (prec == NS_PREC_FP64_OZAKI);
-  const Layout L = make_layout(d, 1, mixed, ozaki);
+  const Layout L = make_layout(d, 1, mixed, ozaki, tf32);
   if (ws_bytes < L.total) return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   uint8_t* w = static_cast<uint8_t*>(ws);
@@ -1000,14 +1008,15 @@ ns_status_t ns_symm_product(const double* A, const double* B, double* C, int64_t
     ProdParams p{tiles, (int)tl.size(), L.d_pad / kBK, L.d, L.d_pad, 0, Pc, Pa, partial, nullptr, mode};
     NS_CUDA(launch_product(tA, tB, p, 1, cs));
   } else {
-    uint16_t* planesA = reinterpret_cast<uint16_t*>(w + L.off_px);
-    uint16_t* planesB = reinterpret_cast<uint16_t*>(w + L.off_py);
-    NS_CUDA(launch_split_planes(Pa, planesA, L.d_pad, 1, cs));
-    NS_CUDA(launch_split_planes(Pb, planesB, L.d_pad, 1, cs));
+    void* planesA = w + L.off_px;
+    void* planesB = w + L.off_py;
+    NS_CUDA(launch_split_planes(Pa, planesA, L.d_pad, 1, cs, tf32));
+    NS_CUDA(launch_split_planes(Pb, planesB, L.d_pad, 1, cs, tf32));
     CUtensorMap tA, tB;
-    if ((s = encode_map_bf16(&tA, planesA, L.d_pad, 2)) != NS_OK) return s;
-    if ((s = encode_map_bf16(&tB, planesB, L.d_pad, 2)) != NS_OK) return s;
-    MxParams p{tiles, (int)tl.size(), L.d_pad / kMxBK, L.d, L.d_pad, 0, Pc, Pa, nullptr, partial, nullptr, mode};
+    if ((s = encode_map_bf16(&tA, planesA, L.d_pad, 2, tf32)) != NS_OK) return s;
+    if ((s = encode_map_bf16(&tB, planesB, L.d_pad, 2, tf32)) != NS_OK) return s;
+    MxParams p{tiles, (int)tl.size(), L.d_pad / (tf32 ? 32 : kMxBK), L.d, L.d_pad, 0, Pc, Pa, nullptr, partial,
+               nullptr, mode, tf32 ? 1 : 0};
     NS_CUDA(launch_mx_product(tA, tB, p, 1, cs));
   }
   NS_CUDA(cudaMemcpy2DAsync(C, (size_t)ld * 8, Pc, (size_t)L.d_pad * 8, (size_t)d * 8, (size_t)d,

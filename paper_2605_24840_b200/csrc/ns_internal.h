@@ -63,15 +63,16 @@ struct CgScalars {
 };
 constexpr int kEwBlocks = 148 * 8;   // fixed grid of the elementwise CG kernels (fixed-order partial sums)
 
-cudaError_t launch_commutator(const double* M, double* C, uint16_t* abs_planes, int d_pad, cudaStream_t st);
+cudaError_t launch_commutator(const double* M, double* C, void* abs_planes, int d_pad, cudaStream_t st,
+                              bool tf32 = false);
 cudaError_t launch_cg_init(const double* Fp, double* R, double* P, double* E, double* partial, int d_pad,
                            cudaStream_t st, int* n_partial);
 cudaError_t launch_cg_pw(const double* P, const double* W, double* partial, int d_pad, cudaStream_t st);
 cudaError_t launch_cg_scalar(CgScalars* sc, const double* partial, int n_partial, int which, cudaStream_t st);
 cudaError_t launch_cg_update(double* E, double* R, const double* P, const double* W, const CgScalars* sc,
                              double* partial, int d_pad, cudaStream_t st, int* n_partial);
-cudaError_t launch_cg_direction(double* P, const double* R, const CgScalars* sc, uint16_t* p_planes, int d_pad,
-                                cudaStream_t st);
+cudaError_t launch_cg_direction(double* P, const double* R, const CgScalars* sc, void* p_planes, int d_pad,
+                                cudaStream_t st, bool tf32 = false);
 cudaError_t launch_apply_correction(double* X, const double* E, int d_pad, cudaStream_t st);
 
 // Product kernel parameters: C_IJ = sum_k P[I,k] Q[J,k] on upper tiles (I <= J).
@@ -113,13 +114,15 @@ struct MxParams {
   long long job_stride;    // FP64 elements between jobs' matrices
   double* C;               // FP64 output (mode 0: Y, 1: X_{j+1}, 2: W dense)
   const double* Xold;      // mode 1
-  uint16_t* Cplanes;       // bf16 planes of C (modes 0, 1), nullptr = skip
+  void* Cplanes;           // hi/lo planes of C (bf16 or tf32-as-fp32; modes 0, 1), nullptr = skip
   double* partial;         // mode 0 residual partial per tile; mode 1 trace partial per diag block
   const DevState* state;
   int mode;                // 0 square (+res, mirror), 1 update (+trace, mirror), 2 dense tile (no mirror)
+  int tf32 = 0;            // 0: BF16x3 (kind::f16), 1: TF32x3 (kind::tf32); nkb = d_pad / (tf32 ? 32 : 64)
 };
 
-cudaError_t launch_split_planes(const double* X, uint16_t* planes, int d_pad, int batch, cudaStream_t st);
+cudaError_t launch_split_planes(const double* X, void* planes, int d_pad, int batch, cudaStream_t st,
+                                bool tf32 = false);
 cudaError_t launch_mx_product(const CUtensorMap& tmP, const CUtensorMap& tmQ, const MxParams& p, int batch,
                               cudaStream_t st);
 

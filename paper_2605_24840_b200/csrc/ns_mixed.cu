@@ -34,23 +34,59 @@ __device__ __forceinline__ void split_bf16(double x, uint16_t& hi, uint16_t& lo)
   lo = __bfloat16_as_ushort(l);
 }
 
-__global__ void __launch_bounds__(256) ns_split_planes_kernel(const double* __restrict__ X,
-                                                              uint16_t* __restrict__ planes, long long n_per_job,
-                                                              int batch) {
-  const long long total = n_per_job * batch;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    const long long job = i / n_per_job, e = i - job * n_per_job;
-    uint16_t hi, lo;
-    split_bf16(X[i], hi, lo);
-    planes[job * 2 * n_per_job + e] = hi;
-    planes[job * 2 * n_per_job + n_per_job + e] = lo;
+// TF32 split: hi = tf32(x) (10 explicit mantissa bits, stored as an fp32 bit pattern), lo = tf32(x - hi).
+__device__ __forceinline__ uint32_t to_tf32_bits(float f) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(f));
+  return r;
+}
+__device__ __forceinline__ void split_tf32(double x, uint32_t& hi, uint32_t& lo) {
+  hi = to_tf32_bits((float)x);
+  lo = to_tf32_bits((float)(x - (double)__uint_as_float(hi)));
+}
+
+template <bool TF32>
+__device__ __forceinline__ void split_plane(double x, void* planes, long long i, long long n) {
+  if (TF32) {
+    uint32_t h, l;
+    split_tf32(x, h, l);
+    static_cast<uint32_t*>(planes)[i] = h;
+    static_cast<uint32_t*>(planes)[n + i] = l;
+  } else {
+    uint16_t h, l;
+    split_bf16(x, h, l);
+    static_cast<uint16_t*>(planes)[i] = h;
+    static_cast<uint16_t*>(planes)[n + i] = l;
   }
 }
 
-template <int MODE>
+template <bool TF32>
+__global__ void __launch_bounds__(256) ns_split_planes_kernel(const double* __restrict__ X, void* __restrict__ planes,
+                                                              long long n_per_job, int batch) {
+  const long long total = n_per_job * batch;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long job = i / n_per_job, e = i - job * n_per_job;
+    void* base = TF32 ? (void*)(static_cast<uint32_t*>(planes) + job * 2 * n_per_job)
+                      : (void*)(static_cast<uint16_t*>(planes) + job * 2 * n_per_job);
+    split_plane<TF32>(X[i], base, e, n_per_job);
+  }
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+template <int MODE, bool TF32>
 __global__ void __launch_bounds__(kMxThreads, 1)
     ns_mx_product_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
                          const MxParams p) {
+  constexpr int kKB = TF32 ? 32 : kMxBK;   // elements per 128-byte k-block row
   const int job = blockIdx.y;
   if (p.state != nullptr && (p.state[job].done || p.state[job].sw)) return;   // low-precision phase over
 
@@ -68,7 +104,8 @@ __global__ void __launch_bounds__(kMxThreads, 1)
   const int2 tile = p.tiles[blockIdx.x];
   const int I = tile.x, J = tile.y;
   const int nkb_total = p.nkb;
-  const int n_chunks = (nkb_total + kMxChunkKb - 1) / kMxChunkKb;
+  constexpr int kChunk = TF32 ? kMxChunkKb / 2 : kMxChunkKb;   // same K per FP32 chunk in elements x bytes
+  const int n_chunks = (nkb_total + kChunk - 1) / kChunk;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kMxStages; ++s) {
@@ -97,15 +134,16 @@ __global__ void __launch_bounds__(kMxThreads, 1)
         if (kb >= kMxStages) mbar_wait(&empty[s], (use & 1u) ^ 1u);
         uint8_t* st = smem + s * kMxStageBytes;
         mbar_arrive_expect_tx(&full[s], kMxStageBytes);
-        tma_load_3d(st + 0 * kMxSlab, &tmP, kb * kMxBK, I * kTile, 2 * job + 0, &full[s]);   // P_hi
-        tma_load_3d(st + 1 * kMxSlab, &tmP, kb * kMxBK, I * kTile, 2 * job + 1, &full[s]);   // P_lo
-        tma_load_3d(st + 2 * kMxSlab, &tmQ, kb * kMxBK, J * kTile, 2 * job + 0, &full[s]);   // Q_hi
-        tma_load_3d(st + 3 * kMxSlab, &tmQ, kb * kMxBK, J * kTile, 2 * job + 1, &full[s]);   // Q_lo
+        tma_load_3d(st + 0 * kMxSlab, &tmP, kb * kKB, I * kTile, 2 * job + 0, &full[s]);   // P_hi
+        tma_load_3d(st + 1 * kMxSlab, &tmP, kb * kKB, I * kTile, 2 * job + 1, &full[s]);   // P_lo
+        tma_load_3d(st + 2 * kMxSlab, &tmQ, kb * kKB, J * kTile, 2 * job + 0, &full[s]);   // Q_hi
+        tma_load_3d(st + 3 * kMxSlab, &tmQ, kb * kKB, J * kTile, 2 * job + 1, &full[s]);   // Q_lo
       }
     }
   } else if (warp == 1) {
-    // idesc: D=F32 (bits 4-5 = 1), A=B=BF16 (bits 7-9, 10-12 = 1), K-major, N=128 (>>3 at 17), M=128 (>>4 at 24)
-    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTile >> 3) << 17) |
+    // idesc: D=F32 (bits 4-5 = 1), A=B=BF16 (1) or TF32 (2) (bits 7-9, 10-12), K-major, N=128, M=128
+    constexpr uint32_t fmt = TF32 ? 2u : 1u;
+    const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(kTile >> 3) << 17) |
                            ((uint32_t)(kTile >> 4) << 24);
     // K is cut into chunks of kMxChunkKb k-blocks; each chunk accumulates in FP32 into one of two TMEM
     // buffers, and the epilogue warps fold finished chunks into FP64 registers (FP32 accumulation error
@@ -115,7 +153,7 @@ __global__ void __launch_bounds__(kMxThreads, 1)
       if (c >= 2) mbar_wait(&tempty[b], static_cast<uint32_t>((c >> 1) - 1) & 1u);
       tc_fence_after();
       const uint32_t acc = tmem + (uint32_t)(b * kTile);
-      const int kb0 = c * kMxChunkKb, kb1 = min(nkb_total, kb0 + kMxChunkKb);
+      const int kb0 = c * kChunk, kb1 = min(nkb_total, kb0 + kChunk);
       for (int kb = kb0; kb < kb1; ++kb) {
         const int s = kb % kMxStages;
         mbar_wait(&full[s], static_cast<uint32_t>(kb / kMxStages) & 1u);
@@ -124,15 +162,22 @@ __global__ void __launch_bounds__(kMxThreads, 1)
           const uint32_t ahi = smem_u32(smem + s * kMxStageBytes), alo = ahi + kMxSlab;
           const uint32_t bhi = ahi + 2 * kMxSlab, blo = ahi + 3 * kMxSlab;
           // the three split terms, small ones first: P_hi Q_lo^T + P_lo Q_hi^T + P_hi Q_hi^T
+          // 4 UMMAs per 128-byte k-block row (K = 16 bf16 or 8 tf32 = 32 bytes each)
 #pragma unroll
-          for (int k = 0; k < kMxBK / 16; ++k)
-            umma_bf16(acc, sdesc_k128(ahi + k * 32), sdesc_k128(blo + k * 32), idesc, (kb != kb0) || (k != 0));
+          for (int k = 0; k < 4; ++k) {
+            if (TF32) umma_tf32(acc, sdesc_k128(ahi + k * 32), sdesc_k128(blo + k * 32), idesc, (kb != kb0) || (k != 0));
+            else umma_bf16(acc, sdesc_k128(ahi + k * 32), sdesc_k128(blo + k * 32), idesc, (kb != kb0) || (k != 0));
+          }
 #pragma unroll
-          for (int k = 0; k < kMxBK / 16; ++k)
-            umma_bf16(acc, sdesc_k128(alo + k * 32), sdesc_k128(bhi + k * 32), idesc, 1u);
+          for (int k = 0; k < 4; ++k) {
+            if (TF32) umma_tf32(acc, sdesc_k128(alo + k * 32), sdesc_k128(bhi + k * 32), idesc, 1u);
+            else umma_bf16(acc, sdesc_k128(alo + k * 32), sdesc_k128(bhi + k * 32), idesc, 1u);
+          }
 #pragma unroll
-          for (int k = 0; k < kMxBK / 16; ++k)
-            umma_bf16(acc, sdesc_k128(ahi + k * 32), sdesc_k128(bhi + k * 32), idesc, 1u);
+          for (int k = 0; k < 4; ++k) {
+            if (TF32) umma_tf32(acc, sdesc_k128(ahi + k * 32), sdesc_k128(bhi + k * 32), idesc, 1u);
+            else umma_bf16(acc, sdesc_k128(ahi + k * 32), sdesc_k128(bhi + k * 32), idesc, 1u);
+          }
           umma_commit(&empty[s]);
           if (kb == kb1 - 1) umma_commit(&tfull[b]);
         }
@@ -178,18 +223,14 @@ __global__ void __launch_bounds__(kMxThreads, 1)
     const long long base = (long long)job * p.job_stride;
     double* C = p.C + base;
     const long long nplane = (long long)p.ld * p.ld;
-    uint16_t* Ph = p.Cplanes ? p.Cplanes + (long long)job * 2 * nplane : nullptr;
-    uint16_t* Pl = Ph ? Ph + nplane : nullptr;
+    void* Ph = nullptr;
+    if (p.Cplanes) Ph = TF32 ? (void*)(static_cast<uint32_t*>(p.Cplanes) + (long long)job * 2 * nplane)
+                             : (void*)(static_cast<uint16_t*>(p.Cplanes) + (long long)job * 2 * nplane);
     const bool diag = (I == J);
     double part = 0.0;
     auto put = [&](long long gidx, double v) {
       C[gidx] = v;
-      if (Ph) {
-        uint16_t h, l;
-        split_bf16(v, h, l);
-        Ph[gidx] = h;
-        Pl[gidx] = l;
-      }
+      if (Ph) split_plane<TF32>(v, Ph, gidx, nplane);
     };
     if (MODE == 2) {
       for (int idx = tid; idx < kTile * kTile; idx += kMxEpiThreads) {
@@ -273,33 +314,38 @@ __global__ void __launch_bounds__(kMxThreads, 1)
   if (warp == 1) tmem_dealloc(tmem, 2 * kTile);
 }
 
-cudaError_t launch_split_planes(const double* X, uint16_t* planes, int d_pad, int batch, cudaStream_t st) {
+cudaError_t launch_split_planes(const double* X, void* planes, int d_pad, int batch, cudaStream_t st, bool tf32) {
   const long long n = (long long)d_pad * d_pad;
   long long blocks = (n * batch + 255) / 256;
   if (blocks > 148 * 64) blocks = 148 * 64;
-  ns_split_planes_kernel<<<(unsigned)blocks, 256, 0, st>>>(X, planes, n, batch);
+  if (tf32) ns_split_planes_kernel<true><<<(unsigned)blocks, 256, 0, st>>>(X, planes, n, batch);
+  else ns_split_planes_kernel<false><<<(unsigned)blocks, 256, 0, st>>>(X, planes, n, batch);
+  return cudaGetLastError();
+}
+
+template <int MODE, bool TF32>
+static cudaError_t launch_mx_t(const CUtensorMap& tmP, const CUtensorMap& tmQ, const MxParams& p, int batch,
+                               cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(ns_mx_product_kernel<MODE, TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMxSmemBytes);
+    attr = true;
+  }
+  dim3 grid(p.n_tiles, batch);
+  ns_mx_product_kernel<MODE, TF32><<<grid, kMxThreads, kMxSmemBytes, st>>>(tmP, tmQ, p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_mx_product(const CUtensorMap& tmP, const CUtensorMap& tmQ, const MxParams& p, int batch,
                               cudaStream_t st) {
-  static bool attr[3] = {false, false, false};
-  dim3 grid(p.n_tiles, batch);
-  switch (p.mode) {
-    case 0:
-      if (!attr[0]) { cudaFuncSetAttribute(ns_mx_product_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMxSmemBytes); attr[0] = true; }
-      ns_mx_product_kernel<0><<<grid, kMxThreads, kMxSmemBytes, st>>>(tmP, tmQ, p);
-      break;
-    case 1:
-      if (!attr[1]) { cudaFuncSetAttribute(ns_mx_product_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMxSmemBytes); attr[1] = true; }
-      ns_mx_product_kernel<1><<<grid, kMxThreads, kMxSmemBytes, st>>>(tmP, tmQ, p);
-      break;
-    default:
-      if (!attr[2]) { cudaFuncSetAttribute(ns_mx_product_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMxSmemBytes); attr[2] = true; }
-      ns_mx_product_kernel<2><<<grid, kMxThreads, kMxSmemBytes, st>>>(tmP, tmQ, p);
-      break;
+  if (p.tf32) {
+    if (p.mode == 0) return launch_mx_t<0, true>(tmP, tmQ, p, batch, st);
+    if (p.mode == 1) return launch_mx_t<1, true>(tmP, tmQ, p, batch, st);
+    return launch_mx_t<2, true>(tmP, tmQ, p, batch, st);
   }
-  return cudaGetLastError();
+  if (p.mode == 0) return launch_mx_t<0, false>(tmP, tmQ, p, batch, st);
+  if (p.mode == 1) return launch_mx_t<1, false>(tmP, tmQ, p, batch, st);
+  return launch_mx_t<2, false>(tmP, tmQ, p, batch, st);
 }
 
 }  // namespace nsr

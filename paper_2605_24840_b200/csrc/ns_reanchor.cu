@@ -32,6 +32,28 @@ __device__ __forceinline__ void split_bf16_r(double x, uint16_t& hi, uint16_t& l
   lo = __bfloat16_as_ushort(l);
 }
 
+__device__ __forceinline__ uint32_t tf32_bits_r(float f) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(f));
+  return r;
+}
+
+// hi/lo planes of one element (bf16 or tf32-as-fp32 layout), plane stride n
+template <bool TF32>
+__device__ __forceinline__ void put_planes(double x, void* planes, long long i, long long n) {
+  if (TF32) {
+    const uint32_t h = tf32_bits_r((float)x);
+    const uint32_t l = tf32_bits_r((float)(x - (double)__uint_as_float(h)));
+    static_cast<uint32_t*>(planes)[i] = h;
+    static_cast<uint32_t*>(planes)[n + i] = l;
+  } else {
+    uint16_t h, l;
+    split_bf16_r(x, h, l);
+    static_cast<uint16_t*>(planes)[i] = h;
+    static_cast<uint16_t*>(planes)[n + i] = l;
+  }
+}
+
 // fixed-order block reduction of one double per thread (blockDim = 256) -> out[blockIdx]
 __device__ __forceinline__ void block_partial(double v, double* out) {
   __shared__ double red[8];
@@ -60,8 +82,9 @@ __device__ __forceinline__ void tile_pair(int b, int nb, int& bi, int& bj) {
 }
 
 // C = M - M^T,  |A| = (M + M^T)/2 -> bf16 hi/lo planes (the CG operator's left factor).
+template <bool TF32>
 __global__ void __launch_bounds__(256) ns_commutator_kernel(const double* __restrict__ M, double* __restrict__ C,
-                                                            uint16_t* __restrict__ abs_planes, int d_pad) {
+                                                            void* __restrict__ abs_planes, int d_pad) {
   __shared__ double ta[32][33], tb[32][33];
   const int nb = d_pad / 32;
   int bi, bj;
@@ -79,16 +102,11 @@ __global__ void __launch_bounds__(256) ns_commutator_kernel(const double* __rest
     const long long g1 = (long long)(bi * 32 + y) * d_pad + bj * 32 + tx;
     const long long g2 = (long long)(bj * 32 + y) * d_pad + bi * 32 + tx;
     C[g1] = mij - mji;
-    uint16_t h, l;
-    split_bf16_r(0.5 * (mij + mji), h, l);
-    abs_planes[g1] = h;
-    abs_planes[np + g1] = l;
+    put_planes<TF32>(0.5 * (mij + mji), abs_planes, g1, np);
     if (bi != bj) {
       const double nij = tb[y][tx], nji = ta[tx][y];   // element (bj*32+y, bi*32+tx)
       C[g2] = nij - nji;
-      split_bf16_r(0.5 * (nij + nji), h, l);
-      abs_planes[g2] = h;
-      abs_planes[np + g2] = l;
+      put_planes<TF32>(0.5 * (nij + nji), abs_planes, g2, np);
     }
   }
 }
@@ -192,17 +210,15 @@ __global__ void __launch_bounds__(256) ns_cg_update_kernel(double* __restrict__ 
 }
 
 // P = R + beta P, and the bf16 hi/lo planes of the new P (right factor of W = |A| P).
+template <bool TF32>
 __global__ void __launch_bounds__(256) ns_cg_direction_kernel(double* __restrict__ P, const double* __restrict__ R,
                                                               const CgScalars* __restrict__ sc,
-                                                              uint16_t* __restrict__ planes, long long n) {
+                                                              void* __restrict__ planes, long long n) {
   const double beta = sc->beta;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const double p = fma(beta, P[i], R[i]);
     P[i] = p;
-    uint16_t h, l;
-    split_bf16_r(p, h, l);
-    planes[i] = h;
-    planes[n + i] = l;
+    put_planes<TF32>(p, planes, i, n);
   }
 }
 
@@ -218,8 +234,9 @@ static int n_pairs(int d_pad) {
   return nb * (nb + 1) / 2;
 }
 
-cudaError_t launch_commutator(const double* M, double* C, uint16_t* abs_planes, int d_pad, cudaStream_t st) {
-  ns_commutator_kernel<<<n_pairs(d_pad), 256, 0, st>>>(M, C, abs_planes, d_pad);
+cudaError_t launch_commutator(const double* M, double* C, void* abs_planes, int d_pad, cudaStream_t st, bool tf32) {
+  if (tf32) ns_commutator_kernel<true><<<n_pairs(d_pad), 256, 0, st>>>(M, C, abs_planes, d_pad);
+  else ns_commutator_kernel<false><<<n_pairs(d_pad), 256, 0, st>>>(M, C, abs_planes, d_pad);
   return cudaGetLastError();
 }
 
@@ -247,9 +264,10 @@ cudaError_t launch_cg_update(double* E, double* R, const double* P, const double
   return cudaGetLastError();
 }
 
-cudaError_t launch_cg_direction(double* P, const double* R, const CgScalars* sc, uint16_t* p_planes, int d_pad,
-                                cudaStream_t st) {
-  ns_cg_direction_kernel<<<kEwBlocks, 256, 0, st>>>(P, R, sc, p_planes, (long long)d_pad * d_pad);
+cudaError_t launch_cg_direction(double* P, const double* R, const CgScalars* sc, void* p_planes, int d_pad,
+                                cudaStream_t st, bool tf32) {
+  if (tf32) ns_cg_direction_kernel<true><<<kEwBlocks, 256, 0, st>>>(P, R, sc, p_planes, (long long)d_pad * d_pad);
+  else ns_cg_direction_kernel<false><<<kEwBlocks, 256, 0, st>>>(P, R, sc, p_planes, (long long)d_pad * d_pad);
   return cudaGetLastError();
 }
 

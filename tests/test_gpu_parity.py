@@ -526,3 +526,30 @@ def test_ozaki_cfg3_full_size_sampled(nsr):
     err = np.sqrt(np.mean(np.sum((Rg - Rc) ** 2, axis=0)))
     print(f"ozaki d=16384: err~{err:.3e}")
     assert err <= TOL_R      # north_star bar; 8 slices of 7 bits give ~1e-13 per entry at this d
+
+
+# ------------------------------------------------------------------ TF32x3 variant of the mixed path
+@pytest.mark.parametrize("d,mode", [(256, 0), (300, 1), (384, 2)])
+def test_tf32x3_product_kernel(nsr, d, mode):
+    rng = np.random.default_rng(5 + d)
+    A = rng.standard_normal((d, d))
+    A = 0.5 * (A + A.T) / math.sqrt(d)
+    B = A @ A if mode != 2 else rng.standard_normal((d, d))
+    B = 0.5 * (B + B.T)
+    Ag, Bg = torch.from_numpy(A).to(_dev()), torch.from_numpy(B).to(_dev())
+    C = nsr.ns_symm_product(Ag, Bg, mode=mode, prec=nsr.NS_PREC_MIXED_TF32X3).cpu().numpy()
+    ref = A @ B if mode != 1 else 1.5 * A - 0.5 * (A @ B)
+    err = np.max(np.abs(C - ref)) / np.max(np.abs(A @ B))
+    print(f"tf32x3 d={d} mode={mode}: {err:.2e}")
+    assert 1e-12 <= err <= 5e-6, err     # bounded by the FP32 chunk accumulation, like BF16x3
+
+
+def test_tf32x3_mixed_cfg3_recipe(nsr):
+    p = workloads.cfg3_dense(d=1024, k=64)
+    o = ons.ns_reflector(p.H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    R, res = nsr.ns_reflector(torch.from_numpy(p.H).to(_dev()), p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode,
+                              prec=nsr.NS_PREC_MIXED_TF32X3)
+    err = checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"])
+    print(f"tf32x3 mixed d=1024: switch {res['switch_step']} steps {res['steps']} err {err:.2e}")
+    assert res["steps"] == o["steps"] and res["cert"] == 64 and res["flags"] == ons.CONVERGED
+    assert err <= TOL_R

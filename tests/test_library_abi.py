@@ -66,7 +66,8 @@ def test_argument_validation(lib):
     assert call(max_steps=-1) == 1
     assert call(tol=-1.0) == 1
     assert call(tm=7) == 1
-    assert call(prec=2) == 5                     # TF32x3 mode: NS_ERR_UNSUPPORTED in this build
+    assert call(prec=7) == 1                     # unknown precision
+    assert call(prec=3, d=20000, ldh=20000, ldr=20000, k=3) == 5   # Ozaki: d <= 16640 (NS_ERR_UNSUPPORTED)
     assert call(R=fake) == 1                     # aliasing
     assert call(ws_bytes=10) == 4                # NS_ERR_WORKSPACE
     assert b"workspace" in lib.ns_last_error()

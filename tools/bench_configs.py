@@ -113,7 +113,8 @@ def cfg3(mode="tol", prec=nsr.NS_PREC_FP64, reps=3):
     Rg = R[:, torch.as_tensor(cols, device=DEV)].cpu().numpy()
     err = float(np.sqrt(np.mean(np.sum((Rg - Rc) ** 2, axis=0))))
     tf = (2 * res["steps"] + 1) * float(p.d) ** 3 / (ms * 1e-3) / 1e12
-    emit({"config": "cfg3", "mode": mode, "prec": {0: "fp64", 1: "mixed_bf16x3", 3: "fp64_ozaki_int8"}[prec], "d": p.d,
+    emit({"config": "cfg3", "mode": mode, "prec": {0: "fp64", 1: "mixed_bf16x3", 2: "mixed_tf32x3",
+                                                   3: "fp64_ozaki_int8"}[prec], "d": p.d,
           "time_to_R_ms": ms, "steps": res["steps"], "cert": res["cert"], "flags": res["flags"],
           "switch_step": res["switch_step"], "tflops": tf, "frac_fp64_peak": tf / PEAK, "err_vs_closed_form": err,
           "launches": res["launches"]})
@@ -183,6 +184,8 @@ def main():
             cfg3("fixed30", nsr.NS_PREC_FP64, reps=1)
         elif w == "cfg3fixedmixed":
             cfg3("fixed30", nsr.NS_PREC_MIXED_BF16X3, reps=1)
+        elif w == "cfg3tf32":
+            cfg3("tol", nsr.NS_PREC_MIXED_TF32X3)
         elif w == "cfg3ozaki":
             cfg3("tol", nsr.NS_PREC_FP64_OZAKI)
         elif w == "cfg3fixedozaki":
