@@ -553,3 +553,32 @@ def test_tf32x3_mixed_cfg3_recipe(nsr):
     print(f"tf32x3 mixed d=1024: switch {res['switch_step']} steps {res['steps']} err {err:.2e}")
     assert res["steps"] == o["steps"] and res["cert"] == 64 and res["flags"] == ons.CONVERGED
     assert err <= TOL_R
+
+
+# ------------------------------------------------------------------ extra edges for every precision path
+@pytest.mark.parametrize("prec_name", ["NS_PREC_MIXED_BF16X3", "NS_PREC_MIXED_TF32X3", "NS_PREC_FP64_OZAKI"])
+@pytest.mark.parametrize("d,k", [(100, 7), (300, 20)])
+def test_precision_paths_ragged(nsr, prec_name, d, k):
+    """Ragged d (padding to 128) through the mixed and Ozaki paths: oracle parity, steps, certificate."""
+    p = workloads.cfg3_dense(d=d, k=k, n_house=8)
+    o = ons.ns_reflector(p.H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode, trace_residuals=True)
+    R, res = nsr.ns_reflector(torch.from_numpy(p.H).to(_dev()), p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode,
+                              prec=getattr(nsr, prec_name))
+    assert res["cert"] == k and res["flags"] == o["flags"]
+    if not _tie_band(o["hist_residual"], p.tol * math.sqrt(d), o["steps"]):
+        assert res["steps"] == o["steps"]
+    assert checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= TOL_R
+    assert torch.equal(R, R.T)
+
+
+def test_cfg2_seed1_golden(nsr, golden_dir):
+    import json
+    import os
+    g = json.load(open(os.path.join(golden_dir, "cfg2_seed1.json")))
+    cols = np.load(os.path.join(golden_dir, "cfg2_seed1_cols.npz"))
+    prob = workloads.cfg2_allen_cahn(seed=1, s=g["s"])
+    R, res = nsr.ns_reflector(torch.from_numpy(prob.H).to(_dev()), g["s"], g["alpha"], 5, 100, 1e-12, 0)
+    assert res["steps"] == g["ns"]["steps"] == 24 and res["cert"] == 5 and res["flags"] == g["ns"]["flags"]
+    Rc = R[:, torch.as_tensor(cols["cols"], device=_dev())].cpu().numpy()
+    assert np.sqrt(np.mean(np.sum((Rc - cols["R_ns"]) ** 2, axis=0))) <= TOL_R
+    assert np.sqrt(np.mean(np.sum((Rc - cols["R_eig"]) ** 2, axis=0))) <= TOL_R
