@@ -102,29 +102,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncthreads();
 
-  if (warp == 0) {
-    // ---------------- TMA producer (one elected lane) ----------------
-    if (lane == 0) {
-      tma_prefetch_desc(&tmP);
-      tma_prefetch_desc(&tmQ);
-      const int nst = p.nk / kSPS;
-      for (int kt = 0; kt < nst; ++kt) {
-        const int s = kt % kStages;
-        const uint32_t use = kt / kStages;
-        if (kt >= kStages) mbar_wait(&empty[s], (use & 1u) ^ 1u);
-        mbar_arrive_expect_tx(&full[s], kStageBytes);
+  // ---------------- TMA ring, driven by thread 0 between its own DMMA work ----------------
+  // 8 warps only (2 per SMSP) so each thread may use up to 255 registers; thread 0 fills the first
+  // kStages stages up front and, each time all warps have released a stage (empty barrier),
+  // refills that slot with the stage kStages ahead.
+  const int nst = p.nk / kSPS;
+  auto issue = [&](int kt) {
+    const int s = kt % kStages;
+    mbar_arrive_expect_tx(&full[s], kStageBytes);
 #pragma unroll
-        for (int u = 0; u < kSPS; ++u) {
-          tma_load_3d(sA + (s * kSPS + u) * kTile * kBK, &tmP, (kt * kSPS + u) * kBK, I * kTile, job, &full[s]);
-          tma_load_3d(sB + (s * kSPS + u) * kTile * kBK, &tmQ, (kt * kSPS + u) * kBK, J * kTile, job, &full[s]);
-        }
-      }
+    for (int u = 0; u < kSPS; ++u) {
+      tma_load_3d(sA + (s * kSPS + u) * kTile * kBK, &tmP, (kt * kSPS + u) * kBK, I * kTile, job, &full[s]);
+      tma_load_3d(sB + (s * kSPS + u) * kTile * kBK, &tmQ, (kt * kSPS + u) * kBK, J * kTile, job, &full[s]);
     }
-    return;
+  };
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmP);
+    tma_prefetch_desc(&tmQ);
+    for (int kt = 0; kt < kStages && kt < nst; ++kt) issue(kt);
   }
 
-  // ---------------- DMMA consumers: warp tile 64 (rows of P) x 32 (rows of Q) ----------------
-  const int cw = warp - 1;        // 0..7
+  // ---------------- DMMA: warp tile 64 (rows of P) x 32 (rows of Q) ----------------
+  const int cw = warp;            // 0..7
   const int wm = cw >> 2;         // 0..1  -> rows wm*64
   const int wn = cw & 3;          // 0..3  -> cols wn*32
   const int g = lane >> 2, t = lane & 3;
@@ -142,33 +141,34 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 
-  const int nst = p.nk / kSPS;
   for (int kt = 0; kt < nst; ++kt) {
     const int s = kt % kStages;
+    if (threadIdx.x == 0 && kt >= 1 && kt - 1 + kStages < nst) {
+      // every warp released stage kt-1: refill its slot with stage kt-1+kStages
+      const int sp = (kt - 1) % kStages;
+      mbar_wait(&empty[sp], static_cast<uint32_t>((kt - 1) / kStages) & 1u);
+      issue(kt - 1 + kStages);
+    }
     mbar_wait(&full[s], static_cast<uint32_t>(kt / kStages) & 1u);
 #pragma unroll
     for (int hh = 0; hh < 2 * kSPS; ++hh) {
-    const int h = hh & 1;
-    const uint32_t aS = sA_u32 + (s * kSPS + (hh >> 1)) * (kTile * kBK * 8) + a_row;
-    const uint32_t bS = sB_u32 + (s * kSPS + (hh >> 1)) * (kTile * kBK * 8) + b_row;
-    {
+      const int h = hh & 1;
+      const uint32_t aS = sA_u32 + (s * kSPS + (hh >> 1)) * (kTile * kBK * 8) + a_row;
+      const uint32_t bS = sB_u32 + (s * kSPS + (hh >> 1)) * (kTile * kBK * 8) + b_row;
       const uint32_t off = h ? off_h1 : off_h0;
-      // B fragments for both k-values of this half-slab stay live (16 regs); A fragments are
-      // streamed one m-row at a time so the 128 accumulator registers fit the 168-register
-      // budget of a 9-warp CTA (3 warps share one SMSP's 64 KB register file).
-      double b[4][2];
+      // all fragments of this half-slab first, then the DMMAs k-step-major: the two updates of an
+      // accumulator are 32 DMMAs apart
+      double a[8][2], b[4][2];
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) lds128(bS + ni * 8 * 128 + off, b[ni][0], b[ni][1]);
 #pragma unroll
-      for (int mi = 0; mi < 8; ++mi) {
-        double a0, a1;
-        lds128(aS + mi * 8 * 128 + off, a0, a1);
+      for (int mi = 0; mi < 8; ++mi) lds128(aS + mi * 8 * 128 + off, a[mi][0], a[mi][1]);
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a0, b[ni][0]);
+      for (int e = 0; e < 2; ++e)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a1, b[ni][1]);
-      }
-    }
+        for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi][e], b[ni][e]);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   named_bar_sync(1, 32 * kConsumerWarps);
 
-  const int tid = threadIdx.x - 32;   // 0..255
+  const int tid = threadIdx.x;        // 0..255
   const long long ld = p.ld;
   const long long base = (long long)job * p.job_stride;
   double* C = p.C + base;

@@ -12,7 +12,7 @@ constexpr int kBK = 16;         // k-slab per pipeline stage: 16 doubles = one 1
 constexpr int kSPS = 2;         // 16-wide k-slabs per pipeline stage (one mbarrier wait per 2 slabs)
 constexpr int kStages = 3;      // TMA ring depth (3 x 64 KB)
 constexpr int kConsumerWarps = 8;
-constexpr int kThreads = 32 * (1 + kConsumerWarps);   // warp 0 = TMA producer
+constexpr int kThreads = 32 * kConsumerWarps;         // 8 DMMA warps; warp 0 lane 0 also drives the TMA ring
 constexpr int kStageBytes = kSPS * 2 * kTile * kBK * 8;   // A + B per stage = 64 KB
 constexpr int kEpiPitch = kTile + 1;                  // staging row pitch (doubles), odd => conflict-free columns
 constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
