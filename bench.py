@@ -296,7 +296,7 @@ def run_ours(args):
 
     if args.prec == "fp64" and not args.no_mixed:
         mixed = secondary(nsr.NS_PREC_MIXED_BF16X3)
-        if d <= 16640:
+        if d <= 65536:
             ozaki = secondary(nsr.NS_PREC_FP64_OZAKI)
 
     cpu = None

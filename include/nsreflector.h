@@ -136,7 +136,7 @@ size_t ns_workspace_bytes_batched(int64_t d, int64_t batch, ns_precision_t prec)
  *   prec   NS_PREC_FP64, or NS_PREC_MIXED_BF16X3: BF16x3 tcgen05 steps until the switch
  *          threshold, one FP64 re-anchor solve, FP64 steps to tol (single problem only;
  *          NS_PREC_MIXED_TF32X3 the same with TF32 splits; NS_PREC_FP64_OZAKI: FP64 products emulated
- *          on the INT8 tensor cores, d <= 16640).
+ *          on the INT8 tensor cores, d <= 65536).
  *   R      device, d x d, leading dim ldr >= d; written in full, bitwise symmetric.
  *   ws     device workspace, ws_bytes >= ns_workspace_bytes(d, prec).
  *   stream cudaStream_t (as void*); NULL = legacy default stream.

@@ -161,8 +161,9 @@ cudaError_t launch_outer(const double* Q, int d, const int* k, const double* x0,
                          OuterResult* res, int nruns, cudaStream_t st);
 
 // ---------------- Ozaki-split FP64 products on INT8 tensor cores (ns_ozaki.cu) ----------------
-constexpr int kOzSlices = 8;                           // 8 x 7-bit slices per operand row (~2^-56 of the row max)
-constexpr int kOzMaxD = 16640;                         // 8 * d_pad * 127^2 < 2^31: exact INT32 group sums
+constexpr int kOzSlices = 7;                           // balanced base-256 int8 digits per entry (54 bits)
+constexpr int kOzChunkKb = 256;                        // k-blocks (x64) per INT32 chunk: exact for any d
+constexpr int kOzMaxD = 65536;
 constexpr int kOzStages = 2;
 constexpr int kOzThreads = 192;                        // warp 0 TMA, warp 1 MMA, warps 2..5 epilogue
 constexpr int kOzSlabA = kTile * 64;                   // 128 rows x 64 int8

@@ -1,18 +1,19 @@
 // FP64-accurate products on the INT8 tensor cores (tcgen05 kind::i8) by the Ozaki splitting
 // (SURVEY §8(f) N4 -- an arithmetic variant, not in the paper).
 //
-// Every operand row i is scaled by its own power of two, x_ij = 2^{e_i} * sum_{s=1..S} 2^{-7s} q^s_ij
-// with integer slices q^s in [-127, 127] (exact bit extraction in FP64: e_i = frexp exponent of the
-// row max, r = x 2^{7 - e_i}, q = trunc(r), r = (r - q) 2^7, ...).  Then
-//     (P Q^T)_ij = 2^{e_i + f_j} sum_{g=2}^{S+1} 2^{-7g} sum_{s+t=g} (Q^s_P Q^t_Q^T)_ij  (+ truncation below 2^{-7(S+1)})
-// where each slice product is EXACT in INT32 (|sum| <= 7 * d * 127^2 < 2^31 for d <= 19000) and the
-// seven group sums are accumulated in seven INT32 TMEM accumulators.  The epilogue converts them to
-// FP64 exactly, weights them by powers of two (smallest first), applies the row/column exponents and
-// rounds once: the result is accurate to ~2^-49 of |row_i| |row_j|, i.e. FP64-class.
+// Every operand row i is scaled by its own power of two and cut exactly into 7 signed 8-bit slices:
+// N_ij = rint(x_ij 2^{54-e_i}) (e_i = frexp exponent of the row max, so |N| < 2^54) is written in
+// balanced base 256, N = sum_{s=0..6} D^s 256^{6-s}, D^s in [-128, 127] (|D^0| <= 64).  Then
+//     (P Q^T)_ij ~= 2^{e_i + f_j - 12} sum_{g=0}^{6} 2^{-8g} sum_{s+t=g} (D_P^s D_Q^t^T)_ij
+// keeping the 28 slice pairs with s + t <= 6 (the dropped ones lie below ~2^-50 of |row| |col| per term;
+// balanced digits keep the tails of small entries small -- floor-based unsigned tails do not).  Each
+// slice product is EXACT in INT32; the seven group sums live in seven INT32 TMEM accumulators and are
+// folded into FP64 registers every 16384 of K (7 x 16384 x 128^2 < 2^31, so any d), with exact
+// conversions and power-of-two weights; one rounding per fold.
 //
 // CTA tile 128 x 64 (UMMA M=128, N=64, K=32), 7 accumulators x 64 columns = 448 TMEM columns.
-// Stage = one 64-wide k-block of all 7 slices of both operands (7 x 8 KB + 7 x 4 KB, 64-B swizzle),
-// feeding 28 slice pairs x 2 UMMAs; 2 stages.  Warp 0 TMA, warp 1 MMA, warps 2..5 epilogue.
+// Stage = one 64-wide k-block of the 7 slices of both operands (7 x 8 KB + 7 x 4 KB, 64-B swizzle)
+// feeding 28 pairs x 2 UMMAs; 2 stages.  Warp 0 TMA, warp 1 MMA, warps 2..5 epilogue.
 // Symmetric outputs: tiles (I, J2) with J2*64 + 63 >= I*128; every element with j >= i is produced
 // by exactly one tile, which writes it and its mirror (bitwise-symmetric output).
 #include <cmath>
@@ -43,13 +44,17 @@ __global__ void __launch_bounds__(256) ns_ozaki_slice_kernel(const double* __res
   if (threadIdx.x == 0) expo[(long long)job * d_pad + row] = e;
   int8_t* out = slices + (long long)job * kOzSlices * nn + (long long)row * d_pad;
   for (int j = threadIdx.x; j < d_pad; j += 256) {
-    double r = ldexp(x[j], 7 - e);               // |r| < 128, exact
+    // N = x 2^{54-e} rounded to an integer (|N| < 2^54), written in balanced base 256:
+    // N = sum_s D_s 256^{6-s}, D_1..D_6 in [-128, 127], |D_0| <= 64.  A small |x| has zero leading
+    // digits, so every slice-pair product stays relative to the operands' own magnitudes.
+    long long N = (long long)rint(ldexp(x[j], 54 - e));
 #pragma unroll
-    for (int s = 0; s < kOzSlices; ++s) {
-      const double q = trunc(r);
-      out[(long long)s * nn + j] = (int8_t)q;
-      r = (r - q) * 128.0;                       // exact
+    for (int q = kOzSlices - 1; q >= 1; --q) {
+      const long long D = ((N + 128) & 255) - 128;
+      out[(long long)q * nn + j] = (int8_t)D;
+      N = (N - D) >> 8;                          // exact
     }
+    out[j] = (int8_t)N;
   }
 }
 
@@ -78,20 +83,23 @@ __global__ void __launch_bounds__(kOzThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOzStages * kOzStageBytes);
   uint64_t* empty = full + kOzStages;
-  uint64_t* tmem_full = empty + kOzStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tfull = empty + kOzStages;     // chunk accumulated (MMA -> epilogue)
+  uint64_t* tempty = tfull + 1;            // chunk folded into FP64 (epilogue -> MMA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
   __shared__ double red[4];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int2 tile = p.tiles[blockIdx.x];
   const int I = tile.x, J2 = tile.y;     // 128-row block, 64-column block
+  const int n_chunks = (p.nkb + kOzChunkKb - 1) / kOzChunkKb;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kOzStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 4);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -119,58 +127,69 @@ __global__ void __launch_bounds__(kOzThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // idesc: D=S32 (bits 4-5 = 2), A=B=signed int8 (bits 7-9, 10-12 = 1), K-major, N=64, M=128
-    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(64 >> 3) << 17) |
-                           ((uint32_t)(kTile >> 4) << 24);
-    for (int kb = 0; kb < p.nkb; ++kb) {
-      const int s = kb % kOzStages;
-      mbar_wait(&full[s], static_cast<uint32_t>(kb / kOzStages) & 1u);
+    // idesc: D=S32 (bits 4-5 = 2), A/B signed int8 (bits 7-9 / 10-12 = 1), K-major, N=64, M=128.
+    const uint32_t idesc_base = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(64 >> 3) << 17) |
+                                ((uint32_t)(kTile >> 4) << 24);
+    for (int c = 0; c < n_chunks; ++c) {
+      if (c >= 1) mbar_wait(tempty, static_cast<uint32_t>(c - 1) & 1u);   // accumulators folded
       tc_fence_after();
-      if (lane == 0) {
-        const uint32_t a0 = smem_u32(smem + s * kOzStageBytes);
-        const uint32_t b0 = a0 + kOzSlices * kOzSlabA;
+      const int kb0 = c * kOzChunkKb, kb1 = min(p.nkb, kb0 + kOzChunkKb);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        const int s = kb % kOzStages;
+        mbar_wait(&full[s], static_cast<uint32_t>(kb / kOzStages) & 1u);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a0 = smem_u32(smem + s * kOzStageBytes);
+          const uint32_t b0 = a0 + kOzSlices * kOzSlabA;
 #pragma unroll
-        for (int g = 2; g <= kOzSlices + 1; ++g) {
-          const uint32_t acc = tmem + (uint32_t)((g - 2) * 64);
+          for (int g = 0; g < kOzSlices; ++g) {          // group g: slice pairs (sa, sb) with sa + sb = g
+            const uint32_t acc = tmem + (uint32_t)(g * 64);
 #pragma unroll
-          for (int sa = 1; sa < g; ++sa) {
-            const int sb = g - sa;
-            if (sa > kOzSlices || sb > kOzSlices) continue;
-            const uint32_t aa = a0 + (sa - 1) * kOzSlabA, bb = b0 + (sb - 1) * kOzSlabB;
-            const bool first = (kb == 0) && (sa == ((g - 1 > kOzSlices) ? g - kOzSlices : 1));
-            umma_i8(acc, sdesc_k64(aa), sdesc_k64(bb), idesc, first ? 0u : 1u);
-            umma_i8(acc, sdesc_k64(aa + 32), sdesc_k64(bb + 32), idesc, 1u);
+            for (int sa = 0; sa <= g; ++sa) {
+              const int sb = g - sa;
+              const uint32_t idesc = idesc_base;
+              const uint32_t aa = a0 + sa * kOzSlabA, bb = b0 + sb * kOzSlabB;
+              const bool first = (kb == kb0) && (sa == 0);
+              umma_i8(acc, sdesc_k64(aa), sdesc_k64(bb), idesc, first ? 0u : 1u);
+              umma_i8(acc, sdesc_k64(aa + 32), sdesc_k64(bb + 32), idesc, 1u);
+            }
           }
+          umma_commit(&empty[s]);
+          if (kb == kb1 - 1) umma_commit(tfull);
         }
-        umma_commit(&empty[s]);
-        if (kb == p.nkb - 1) umma_commit(tmem_full);
+        __syncwarp();
       }
-      __syncwarp();
     }
   } else {
-    // ---------------- epilogue: 7 INT32 group sums -> FP64 (exact), weighted, scaled ----------------
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
+    // ---------------- epilogue: fold each chunk's 7 INT32 group sums into FP64 (exact weights) ----------------
     const int q = warp & 3;
     const int r = q * 32 + lane;
     double acc[64];
 #pragma unroll
     for (int c = 0; c < 64; ++c) acc[c] = 0.0;
+    for (int ch = 0; ch < n_chunks; ++ch) {
+      mbar_wait(tfull, static_cast<uint32_t>(ch) & 1u);
+      tc_fence_after();
 #pragma unroll 1
-    for (int g = kOzSlices + 1; g >= 2; --g) {       // smallest weights first
-      const double w = ldexp(1.0, -7 * g);
+      for (int g = kOzSlices - 1; g >= 0; --g) {      // smallest weights first
+        const double w = ldexp(1.0, -8 * g);
 #pragma unroll
-      for (int c0 = 0; c0 < 64; c0 += 16) {
-        uint32_t v[16];
-        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((g - 2) * 64 + c0), v);
+        for (int c0 = 0; c0 < 64; c0 += 16) {
+          uint32_t v[16];
+          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(g * 64 + c0), v);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) acc[c0 + i] = fma((double)(int)v[i], w, acc[c0 + i]);
+          for (int i = 0; i < 16; ++i) acc[c0 + i] = fma((double)(int)v[i], w, acc[c0 + i]);
+        }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);
     }
     const int er = p.expP[(long long)job * p.ld + I * kTile + r];
-    double* S = reinterpret_cast<double*>(smem);   // [128][65]; ring idle after tmem_full
+    double* S = reinterpret_cast<double*>(smem);   // [128][65]; ring idle after the last chunk
 #pragma unroll
-    for (int c = 0; c < 64; ++c) S[r * 65 + c] = ldexp(acc[c], er + p.expQ[(long long)job * p.ld + J2 * 64 + c]);
+    for (int c = 0; c < 64; ++c)
+      S[r * 65 + c] = ldexp(acc[c], er + p.expQ[(long long)job * p.ld + J2 * 64 + c] - 12);
   }
   tc_fence_before();
   __syncthreads();

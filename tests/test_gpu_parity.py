@@ -472,7 +472,7 @@ def test_alg1_scan_matches_oracle(nsr):
 
 
 # ------------------------------------------------------------------ N4: Ozaki-split FP64 on INT8 tensor cores
-@pytest.mark.parametrize("d,mode", [(128, 0), (300, 0), (515, 1), (256, 2), (200, 2), (1024, 0)])
+@pytest.mark.parametrize("d,mode", [(128, 0), (300, 0), (515, 1), (256, 2), (200, 2), (1024, 0), (4500, 1), (16500, 0)])
 def test_ozaki_product_kernel(nsr, d, mode):
     """7-slice Ozaki products on tcgen05 kind::i8: FP64-class accuracy (relative to |row||col|)."""
     rng = np.random.default_rng(99 + d)
@@ -489,6 +489,42 @@ def test_ozaki_product_kernel(nsr, d, mode):
     assert err <= 1e-14, err
     if mode != 2:
         assert np.array_equal(C, C.T)
+
+
+def test_ozaki_product_edge_values(nsr):
+    """Slicing edge cases: rows whose max is an exact power of two (r = -128 + tiny), all-negative rows,
+    zero rows, entries 2^-60 below the row max (dropped below the last slice), mixed row scales."""
+    d = 384
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((d, d))
+    A = 0.5 * (A + A.T)
+
+    def setrow(i, v):
+        A[i, :] = v
+        A[:, i] = v
+
+    setrow(5, -1.0)
+    A[5, 7] = A[7, 5] = -(2.0 ** 3)          # row max a power of two: r = -64, the rest -8
+    setrow(11, 2.0 ** -60)
+    A[11, 0] = A[0, 11] = 1.0                # 2^-60 lies below the last slice of row 11
+    A[21, :] = -(2.0 ** -30)                 # tiny negative entries: balanced digits stay small
+    A[:, 21] = -(2.0 ** -30)
+    setrow(9, 0.0)
+    A[13, :] *= 2.0 ** 40
+    A[:, 13] *= 2.0 ** 40
+    A[17, :] *= 2.0 ** -40
+    A[:, 17] *= 2.0 ** -40
+    B = rng.standard_normal((d, d))
+    B = 0.5 * (B + B.T)
+    Ag, Bg = torch.from_numpy(A).to(_dev()), torch.from_numpy(B).to(_dev())
+    C = nsr.ns_symm_product(Ag, Bg, mode=2, prec=nsr.NS_PREC_FP64_OZAKI).cpu().numpy()
+    ref = A @ B
+    # accuracy is relative to |row of A| x |col of B| (per-row exponents)
+    scale = np.max(np.abs(A), axis=1)[:, None] * np.max(np.abs(B), axis=0)[None, :] * d
+    nz = scale > 0
+    err = np.max(np.abs(C - ref)[nz] / scale[nz])
+    assert err <= 1e-14, err
+    assert np.all(C[9, :] == 0.0)            # zero row: exponent 0, all digits 0
 
 
 @pytest.mark.parametrize("seed", [0, 1])
@@ -525,7 +561,7 @@ def test_ozaki_cfg3_full_size_sampled(nsr):
     Rg = R[:, torch.as_tensor(cols, device=_dev())].cpu().numpy()
     err = np.sqrt(np.mean(np.sum((Rg - Rc) ** 2, axis=0)))
     print(f"ozaki d=16384: err~{err:.3e}")
-    assert err <= TOL_R      # north_star bar; 8 slices of 7 bits give ~1e-13 per entry at this d
+    assert err <= TOL_R      # north_star bar; 7 balanced int8 digits (54 bits) per entry
 
 
 # ------------------------------------------------------------------ TF32x3 variant of the mixed path

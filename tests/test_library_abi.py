@@ -67,7 +67,7 @@ def test_argument_validation(lib):
     assert call(tol=-1.0) == 1
     assert call(tm=7) == 1
     assert call(prec=7) == 1                     # unknown precision
-    assert call(prec=3, d=20000, ldh=20000, ldr=20000, k=3) == 5   # Ozaki: d <= 16640 (NS_ERR_UNSUPPORTED)
+    assert call(prec=3, d=70000, ldh=70000, ldr=70000, k=3) == 1   # d <= 65536 on every path (Ozaki chunks INT32 sums)
     assert call(R=fake) == 1                     # aliasing
     assert call(ws_bytes=10) == 4                # NS_ERR_WORKSPACE
     assert b"workspace" in lib.ns_last_error()
