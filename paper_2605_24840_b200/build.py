@@ -32,7 +32,8 @@ def build(force=False, verbose=False):
     nccl = _nccl_dir()
     link = ["-I" + os.path.join(nccl, "include"), "-L" + os.path.join(nccl, "lib"), "-l:libnccl.so.2",
             "-Xlinker", "-rpath=" + os.path.join(nccl, "lib")]
-    cmd = [NVCC] + FLAGS + ["-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES] + link
+    extra = os.environ.get("NS_NVCC_EXTRA", "").split()   # developer experiments (e.g. -DNS_OZ_A_TMEM=0)
+    cmd = [NVCC] + FLAGS + extra + ["-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES] + link
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:

@@ -11,9 +11,11 @@
 // folded into FP64 registers every 16384 of K (7 x 16384 x 128^2 < 2^31, so any d), with exact
 // conversions and power-of-two weights; one rounding per fold.
 //
-// CTA tile 128 x 64 (UMMA M=128, N=64, K=32), 7 accumulators x 64 columns = 448 TMEM columns.
-// Stage = one 64-wide k-block of the 7 slices of both operands (7 x 8 KB + 7 x 4 KB, 64-B swizzle)
-// feeding 28 pairs x 2 UMMAs; 2 stages.  Warp 0 TMA, warp 1 MMA, warps 2..5 epilogue.
+// CTA tile 128 x 64, 7 accumulators x 64 columns = 448 TMEM columns.  Stage = one 64-wide k-block of
+// the 7 digits of both operands (7 x 8 KB + 7 x 4 KB, 64-B swizzle), 2 stages; warp 0 TMA, warp 1 MMA,
+// warps 2..5 epilogue.  The B digit slabs lie back to back, so the pairs (sa, sb0..sb0+n-1) are ONE
+// UMMA (M=128, N=64n <= 256, K=32) writing n adjacent group accumulators: 10 UMMAs per K=32 half
+// instead of 28 (ncu: with 28 N=64 UMMAs the issuing warp, not the tensor pipe, was the limit).
 // Symmetric outputs: tiles (I, J2) with J2*64 + 63 >= I*128; every element with j >= i is produced
 // by exactly one tile, which writes it and its mirror (bitwise-symmetric output).
 #include <cmath>
@@ -127,9 +129,8 @@ __global__ void __launch_bounds__(kOzThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // idesc: D=S32 (bits 4-5 = 2), A/B signed int8 (bits 7-9 / 10-12 = 1), K-major, N=64, M=128.
-    const uint32_t idesc_base = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(64 >> 3) << 17) |
-                                ((uint32_t)(kTile >> 4) << 24);
+    // idesc: D=S32 (bits 4-5 = 2), A/B signed int8 (bits 7-9 / 10-12 = 1), K-major, M=128 (N set per MMA).
+    const uint32_t idesc_base = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTile >> 4) << 24);
     for (int c = 0; c < n_chunks; ++c) {
       if (c >= 1) mbar_wait(tempty, static_cast<uint32_t>(c - 1) & 1u);   // accumulators folded
       tc_fence_after();
@@ -141,17 +142,22 @@ __global__ void __launch_bounds__(kOzThreads, 1)
         if (lane == 0) {
           const uint32_t a0 = smem_u32(smem + s * kOzStageBytes);
           const uint32_t b0 = a0 + kOzSlices * kOzSlabA;
+          const uint32_t first = (kb == kb0) ? 0u : 1u;
+          // Digit pairs (sa, sb), sb = sb0 .. sb0+n-1, share the A digit: the B digit slabs are stored
+          // back to back (64 rows each), so rows [64 sb0, 64 (sb0+n)) form ONE K-major operand of N = 64 n
+          // whose output columns are exactly the group accumulators sa+sb0 .. sa+sb0+n-1.  28 pairs
+          // become 10 UMMAs (N = 64..256) per K=32 half, with the same MACs: fewer issues and A re-reads.
 #pragma unroll
-          for (int g = 0; g < kOzSlices; ++g) {          // group g: slice pairs (sa, sb) with sa + sb = g
-            const uint32_t acc = tmem + (uint32_t)(g * 64);
+          for (int h = 0; h < 2; ++h) {
 #pragma unroll
-            for (int sa = 0; sa <= g; ++sa) {
-              const int sb = g - sa;
-              const uint32_t idesc = idesc_base;
-              const uint32_t aa = a0 + sa * kOzSlabA, bb = b0 + sb * kOzSlabB;
-              const bool first = (kb == kb0) && (sa == 0);
-              umma_i8(acc, sdesc_k64(aa), sdesc_k64(bb), idesc, first ? 0u : 1u);
-              umma_i8(acc, sdesc_k64(aa + 32), sdesc_k64(bb + 32), idesc, 1u);
+            for (int sa = 0; sa < kOzSlices; ++sa) {
+#pragma unroll
+              for (int sb0 = 0; sb0 < kOzSlices - sa; sb0 += 4) {
+                const int n = min(4, kOzSlices - sa - sb0);
+                const uint32_t idesc = idesc_base | ((uint32_t)(64 * n >> 3) << 17);
+                umma_i8(tmem + (uint32_t)(64 * (sa + sb0)), sdesc_k64(a0 + sa * kOzSlabA + 32 * h),
+                        sdesc_k64(b0 + sb0 * kOzSlabB + 32 * h), idesc, (sa == 0 && h == 0) ? first : 1u);
+              }
             }
           }
           umma_commit(&empty[s]);
