@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kMxThreads, 1)
         const int s = kb % kMxStages;
         mbar_wait(&full[s], static_cast<uint32_t>(kb / kMxStages) & 1u);
         tc_fence_after();
-        if (lane == 0) {
+        if (elect_one()) {
           const uint32_t ahi = smem_u32(smem + s * kMxStageBytes), alo = ahi + kMxSlab;
           const uint32_t bhi = ahi + 2 * kMxSlab, blo = ahi + 3 * kMxSlab;
           // the three split terms, small ones first: P_hi Q_lo^T + P_lo Q_hi^T + P_hi Q_hi^T

@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
         const int s = kb % kOzStages;
         mbar_wait(&full[s], static_cast<uint32_t>(kb / kOzStages) & 1u);
         tc_fence_after();
-        if (lane == 0) {
+        if (elect_one()) {
           const uint32_t a0 = smem_u32(smem + s * kOzStageBytes);
           const uint32_t b0 = a0 + kOzSlices * kOzSlabA;
           const uint32_t first = (kb == kb0) ? 0u : 1u;

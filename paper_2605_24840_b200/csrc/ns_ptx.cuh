@@ -109,6 +109,21 @@ __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t adesc, uint6
       : "memory");
 }
 
+// One lane of a converged warp (elect.sync).  Used as the branch around tcgen05.mma issue: under
+// "if (lane == 0)" ptxas wraps every MMA in an elect/broadcast/branch loop (its operands must be
+// uniform registers and it cannot prove a single active thread), ~6 extra SASS instructions per
+// MMA; under an elect.sync branch it emits the MMAs back to back (measured: 53 instead of ~200
+// instructions for the Ozaki kernel's 20 UMMAs per k-block).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b32 x;\n\t"
+      "elect.sync x|e, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, e;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // Arrive (once) on an mbarrier when all previously issued tcgen05 ops of this thread complete.
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
