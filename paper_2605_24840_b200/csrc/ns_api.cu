@@ -5,6 +5,7 @@
 // decision is taken on the device (ns_decide_kernel); the host enqueues a bounded number
 // of steps ahead and only reads a 4-byte "problems still running" counter, so kernels
 // enqueued after convergence exit immediately.
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -234,7 +235,8 @@ Profiler& prof() {
 
 struct HostRing {
   int* slots = nullptr;
-  DevState* pstate = nullptr;   // pinned landing slot for single-problem results
+  DevState* pstate = nullptr;   // pinned, mapped landing slot for single-problem results
+  DevState* dstate = nullptr;   // its device alias: the fused small-d kernel writes the result there
   cudaEvent_t ev[16];
   bool ok = false;
 };
@@ -243,7 +245,9 @@ HostRing& ring() {
   static thread_local HostRing r;
   if (!r.ok) {
     if (cudaHostAlloc(&r.slots, 16 * sizeof(int), cudaHostAllocDefault) != cudaSuccess) return r;
-    if (cudaHostAlloc(&r.pstate, sizeof(DevState), cudaHostAllocDefault) != cudaSuccess) r.pstate = nullptr;
+    if (cudaHostAlloc(&r.pstate, sizeof(DevState), cudaHostAllocMapped) != cudaSuccess) r.pstate = nullptr;
+    if (r.pstate && cudaHostGetDevicePointer(reinterpret_cast<void**>(&r.dstate), r.pstate, 0) != cudaSuccess)
+      r.dstate = nullptr;
     for (int i = 0; i < 16; ++i) cudaEventCreateWithFlags(&r.ev[i], cudaEventDisableTiming);
     r.ok = true;
   }
@@ -308,13 +312,15 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
     LoopParams lps{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0, -1, 0, opt.ca, opt.cb};
     if (batch > 1)
       NS_CUDA(cudaMemcpyAsync(djobs, jobs.data(), jobs.size() * sizeof(JobParams), cudaMemcpyHostToDevice, st));
-    NS_CUDA(launch_small(H, ldh, h_stride, batch > 1 ? djobs : nullptr, jobs[0], lps, R, ldr, r_stride, state, batch,
-                         st));
+    // batch of one: the kernel stores its result record straight into mapped pinned memory (no copy)
+    const bool mapped = (batch == 1 && rg.dstate != nullptr);
+    NS_CUDA(launch_small(H, ldh, h_stride, batch > 1 ? djobs : nullptr, jobs[0], lps, R, ldr, r_stride,
+                         mapped ? rg.dstate : state, batch, st));
     states.resize(batch);
-    if (batch == 1 && rg.pstate) {
-      NS_CUDA(cudaMemcpyAsync(rg.pstate, state, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+    if (mapped) {
       NS_CUDA(cudaStreamSynchronize(st));
-      states[0] = *rg.pstate;
+      std::atomic_thread_fence(std::memory_order_acquire);
+      std::memcpy(&states[0], rg.pstate, sizeof(DevState));   // written by the kernel
     } else {
       NS_CUDA(cudaMemcpyAsync(states.data(), state, sizeof(DevState) * batch, cudaMemcpyDeviceToHost, st));
       NS_CUDA(cudaStreamSynchronize(st));

@@ -5,9 +5,11 @@
 // (~2 x d^3 FMA per step on one SM's FP64 tensor pipe) instead of 3 launches + a status read per step.
 //
 // Products use DMMA m8n8k4 fragments read straight from row-major shared memory with a padded pitch
-// (d_pad + 4 doubles: the 8 rows of a fragment land 32 B apart, conflict-free per half-warp).  Every
-// 8x8 output fragment is computed; the stored matrix takes the upper-triangle value for both (i,j)
-// and (j,i), so every iterate is bitwise symmetric, as in the tiled path.
+// (d_pad + 4 doubles: the 8 rows of a fragment land 32 B apart, conflict-free per half-warp).  Only the
+// upper 8x8 fragments are computed; each is written with its mirror straight from registers, and the
+// residual / update / trace are applied in the same epilogue, so one NS step is two products and two
+// barriers (the earlier version ran separate mirror, residual and update passes over shared memory:
+// 92 us for configs[0], most of it in those passes).
 #include <cmath>
 #include <cstdint>
 
@@ -17,47 +19,222 @@
 
 namespace nsr {
 
+// one warp per work unit (a pair of upper fragments sharing their A rows, see small_ns_product):
+// 6 / 20 / 42 units for d_pad 32 / 64 / 96 (d_pad 96: 14 warps x 3 units, within the register file)
 template <int DP>
-__global__ void __launch_bounds__(kSmallThreads, 1)
+__host__ __device__ constexpr int small_units() {
+  int n = 0;
+  for (int fi = 0; fi < DP / 8; ++fi) n += (DP / 8 - fi + 1) / 2;
+  return n;
+}
+// Work-unit table (fi, fj) per warp slot w: single-fragment units (the last of each odd-length fragment
+// row) first, then the pairs, so consecutive warps -- which sit on different SM sub-partitions with
+// separate DMMA pipes -- share the singles.  Filled once per CTA (small_fill_units), read per product.
+template <int DP>
+__device__ __forceinline__ void small_fill_units(int2* tab) {
+  constexpr int NF = DP / 8;
+  constexpr int NS = NF / 2;               // single-fragment units: rows with an odd count NF - fi
+  if (threadIdx.x != 0) return;
+  int s = 0, pr = 0;
+  for (int fi = 0; fi < NF; ++fi) {
+    const int nu = (NF - fi + 1) / 2;
+    for (int m = 0; m < nu; ++m) {
+      const bool single = ((NF - fi) & 1) && m == nu - 1;
+      tab[single ? s++ : NS + pr++] = make_int2(fi, fi + 2 * m);
+    }
+  }
+}
+
+// Row pitch (doubles) of the shared-memory matrices.  DP + 8 makes two fragment rows 16 banks apart, so
+// a quarter-warp's 16-byte loads (rows g, g+1; k = 2t, 2t+1) are conflict-free; d_pad 96 keeps DP + 4
+// (three 96 x 104 matrices would exceed the 227 KB shared-memory limit) and 8-byte loads.
+template <int DP>
+__host__ __device__ constexpr int small_pitch() { return DP == 96 ? DP + 4 : DP + 8; }
+
+template <int DP>
+__host__ __device__ constexpr int small_threads() { return 32 * (small_units<DP>() <= 24 ? small_units<DP>() : (small_units<DP>() + 2) / 3); }
+
+// Upper 8x8 fragments (fi <= fj) of C = A B^T for row-major smem operands with pitch DP+4, with the
+// Newton–Schulz epilogue applied in registers (no separate mirror / residual / update passes):
+//   MODE 0: C = A A^T = Y_j; writes the fragment and its mirror; returns this thread's share of
+//           ||Y_j - I||_F^2 (diagonal fragments: elements c >= r only, off-diagonal weight 2).
+//   MODE 1: C = ca X + cb (X Y) = X_{j+1} (X = A); writes it and its mirror; returns this thread's
+//           share of tr X_{j+1}.
+// Diagonal fragments store only c >= r and mirror those, so every stored matrix is bitwise symmetric.
+// Epilogue of one 8x8 fragment held as c[h] = C[r][c0 + h] (see small_ns_product).
+template <int DP, int MODE>
+__device__ __forceinline__ void small_frag_epilogue(const double (&c)[2], int r, int c0, bool diag,
+                                                    const double* __restrict__ A, double* __restrict__ C, int d,
+                                                    double ca, double cb, double& acc) {
+  constexpr int P = small_pitch<DP>();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int cc = c0 + h;
+    if (diag && cc < r) continue;          // lower half of a diagonal fragment: comes from the mirror
+    double v = c[h];
+    if (MODE == 0) {
+      const double e = (cc == r && r < d) ? v - 1.0 : v;
+      acc += (cc == r ? 1.0 : 2.0) * e * e;
+    } else {
+      v = fma(cb, v, ca * A[r * P + cc]);
+      if (cc == r && r < d) acc += v;
+    }
+    C[r * P + cc] = v;
+    if (cc != r) C[cc * P + r] = v;
+  }
+}
+
+// Upper part of C = A B^T for row-major smem operands with pitch DP+4, with the Newton–Schulz epilogue
+// applied in registers (no separate mirror / residual / update passes):
+//   MODE 0: C = A A^T = Y_j; writes each value and its mirror; returns this thread's share of
+//           ||Y_j - I||_F^2 (diagonal fragments: elements c >= r only, off-diagonal weight 2).
+//   MODE 1: C = ca X + cb (X Y) = X_{j+1} (X = A); writes it and its mirror; returns this thread's
+//           share of tr X_{j+1}.
+// Work unit = two horizontally adjacent upper fragments (fi, fj), (fi, fj+1) (the second absent at the
+// end of a row), so each loaded A fragment feeds two DMMAs; one unit per warp (d_pad 96: two), which
+// spreads the 8x8x4 DMMAs evenly over the four SM sub-partitions — one CTA is bound by the SM's FP64
+// tensor path (64 FMA/clk).  Diagonal fragments store only c >= r and mirror those, so every stored
+// matrix is bitwise symmetric.
+template <int DP, int MODE>
+__device__ __forceinline__ double small_ns_product(const double* __restrict__ A, const double* __restrict__ B,
+                                                   double* __restrict__ C, int d, double ca, double cb,
+                                                   const int2* __restrict__ units) {
+  constexpr int P = small_pitch<DP>();
+  constexpr bool VEC = ((2 * P) % 32) == 16;
+  constexpr int NU = small_units<DP>();
+  constexpr int NW = small_threads<DP>() / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  double acc = 0.0;
+  for (int w = warp; w < NU; w += NW) {
+    const int2 un = units[w];
+    const int fi = un.x, fj = un.y;
+    const bool two = (fj + 1 < DP / 8);
+    double c[2][2][2];                     // c[fragment][k-chain][h]
+#pragma unroll
+    for (int f = 0; f < 2; ++f)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) c[f][q][0] = c[f][q][1] = 0.0;
+    if constexpr (VEC) {
+      // k-permuted fragments: thread t supplies k = 2t (chain 0) and 2t+1 (chain 1) of each 8-wide k
+      // block with one 16-byte load; both operands use the same permutation, so every product
+      // A[i][k] B[j][k] still meets its partner (the summation order differs, not the sum's terms).
+      const double* a = A + (fi * 8 + g) * P + 2 * t;
+      const double* b0 = B + (fj * 8 + g) * P + 2 * t;
+      const double* b1 = b0 + 8 * P;
+#pragma unroll 4
+      for (int k = 0; k < DP; k += 8) {
+        const double2 x = *reinterpret_cast<const double2*>(a + k);
+        const double2 y0 = *reinterpret_cast<const double2*>(b0 + k);
+        dmma_8x8x4(c[0][0][0], c[0][0][1], x.x, y0.x);
+        dmma_8x8x4(c[0][1][0], c[0][1][1], x.y, y0.y);
+        if (two) {
+          const double2 y1 = *reinterpret_cast<const double2*>(b1 + k);
+          dmma_8x8x4(c[1][0][0], c[1][0][1], x.x, y1.x);
+          dmma_8x8x4(c[1][1][0], c[1][1][1], x.y, y1.y);
+        }
+      }
+    } else {
+      const double* a = A + (fi * 8 + g) * P + t;
+      const double* b0 = B + (fj * 8 + g) * P + t;
+      const double* b1 = b0 + 8 * P;
+#pragma unroll 4
+      for (int k = 0; k < DP; k += 8) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const double x = a[k + 4 * q], y0 = b0[k + 4 * q];
+          dmma_8x8x4(c[0][q][0], c[0][q][1], x, y0);
+          if (two) dmma_8x8x4(c[1][q][0], c[1][q][1], x, b1[k + 4 * q]);
+        }
+      }
+    }
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+      if (f == 1 && !two) continue;
+      const double v[2] = {c[f][0][0] + c[f][1][0], c[f][0][1] + c[f][1][1]};
+      small_frag_epilogue<DP, MODE>(v, fi * 8 + g, (fj + f) * 8 + 2 * t, fi == fj + f, A, C, d, ca, cb, acc);
+    }
+  }
+  return acc;
+}
+
+// Sum of (a, b) over the CTA; one barrier (callers separate consecutive uses by another barrier).
+// The per-warp partials are summed by every warp with the same shuffle tree, so all threads hold
+// identical bits (one LDS per lane instead of NW per thread).
+template <int NW>
+__device__ __forceinline__ void block_sum2(double& a, double& b, double (*red)[2]) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) {
+    red[threadIdx.x >> 5][0] = a;
+    red[threadIdx.x >> 5][1] = b;
+  }
+  __syncthreads();
+  a = lane < NW ? red[lane][0] : 0.0;
+  b = lane < NW ? red[lane][1] : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+}
+
+template <int DP>
+__global__ void __launch_bounds__(small_threads<DP>(), 1)
     ns_small_kernel(const double* __restrict__ H, long long ldh, long long h_stride, const JobParams* __restrict__ jobs,
                     JobParams job0, LoopParams lp, double* __restrict__ R, long long ldr, long long r_stride,
                     DevState* __restrict__ state) {
-  constexpr int P = DP + 4;
+  constexpr int P = small_pitch<DP>();
+  constexpr int NT = small_threads<DP>();
   extern __shared__ __align__(16) double sm[];
-  double* X = sm;
-  double* Y = sm + DP * P;
-  double* Z = sm + 2 * DP * P;
-  __shared__ double red[kSmallThreads / 32];
+  double* X = sm;                  // X_j
+  double* Xn = sm + DP * P;        // X_{j+1}
+  double* Y = sm + 2 * DP * P;     // Y_j = X_j^2
+  __shared__ double red[NT / 32][2];
+  __shared__ int2 units[small_units<DP>()];
+  small_fill_units<DP>(units);             // visible after the first barrier below
   const int job = blockIdx.x;
   const double* Hj = H + (long long)job * h_stride;
   const JobParams jp = jobs ? jobs[job] : job0;   // batch of one: parameters by value (no H2D copy)
   const double s = jp.s, alpha = jp.alpha;
   const int d = lp.d;
-  // X_0 = (H - sI)/alpha from the upper triangle, zero padded
-  for (int e = threadIdx.x; e < DP * DP; e += kSmallThreads) {
-    const int i = e / DP, j = e % DP;
-    double v = 0.0;
-    if (i < d && j < d) {
-      const double h = (i <= j) ? Hj[(long long)i * ldh + j] : Hj[(long long)j * ldh + i];
-      v = (i == j) ? (h - s) / alpha : h / alpha;
+  // X_0 = (H - sI)/alpha from the upper triangle, zero padded; tr X_0 partials
+  double tpart = 0.0;
+  for (int e = threadIdx.x; e < DP * DP; e += NT) X[(e / DP) * P + e % DP] = 0.0;   // padding
+  __syncthreads();
+  // row-major (coalesced) reads, 8 independent loads in flight per thread (the loop is otherwise a chain
+  // of global-memory latencies: ~9 us of a 48 us configs[0] kernel); the upper triangle is kept
+  for (int e0 = threadIdx.x; e0 < d * d; e0 += 8 * NT) {
+    double h[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = e0 + q * NT;
+      h[q] = (e < d * d) ? Hj[(long long)(e / d) * ldh + e % d] : 0.0;
     }
-    X[i * P + j] = v;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = e0 + q * NT;
+      const int i = e / d, j = e % d;
+      if (e >= d * d || i > j) continue;
+      const double v = (i == j) ? (h[q] - s) / alpha : h[q] / alpha;
+      if (i == j) tpart += v;
+      X[i * P + j] = v;
+      X[j * P + i] = v;
+    }
   }
   __syncthreads();
   const double sqd = sqrt((double)d);
   int j = 0, flags = 0;
   double r = 0.0, r_prev = 0.0, tr = 0.0;
   while (true) {
-    small_product<DP>(X, X, Y);                     // Y_j = X_j^2
-    double part = 0.0, tpart = 0.0;
-    for (int e = threadIdx.x; e < d * d; e += kSmallThreads) {
-      const int i = e / d, c = e % d;
-      const double v = Y[i * P + c] - (i == c ? 1.0 : 0.0);
-      part += v * v;
-    }
-    for (int i = threadIdx.x; i < d; i += kSmallThreads) tpart += X[i * P + i];
-    r = sqrt(block_sum(part, red));
-    tr = block_sum(tpart, red);
+    double part = small_ns_product<DP, 0>(X, X, Y, d, 0.0, 0.0, units);   // Y_j = X_j^2, ||Y_j - I||_F^2 share
+    block_sum2<NT / 32>(part, tpart, red);                          // barrier: Y_j complete
+    r = sqrt(part);
+    tr = tpart;
     if (!isfinite(r)) {
       flags |= 16;
       break;
@@ -72,18 +249,17 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
       flags |= 2;
       break;
     }
-    small_product<DP>(X, Y, Z);                     // Z = X_j Y_j
-    for (int e = threadIdx.x; e < DP * DP; e += kSmallThreads) {
-      const int i = e / DP, c = e % DP;
-      X[i * P + c] = fma(lp.cb, Z[i * P + c], lp.ca * X[i * P + c]);
-    }
-    __syncthreads();
+    tpart = small_ns_product<DP, 1>(X, Y, Xn, d, lp.ca, lp.cb, units);      // X_{j+1} = ca X_j + cb X_j Y_j
+    __syncthreads();                                                 // X_{j+1} complete
+    double* tmp = X;
+    X = Xn;
+    Xn = tmp;
     r_prev = r;
     ++j;
   }
   // R = X_j
   double* Rj = R + (long long)job * r_stride;
-  for (int e = threadIdx.x; e < d * d; e += kSmallThreads) {
+  for (int e = threadIdx.x; e < d * d; e += NT) {
     const int i = e / d, c = e % d;
     Rj[(long long)i * ldr + c] = X[i * P + c];
   }
@@ -116,18 +292,18 @@ cudaError_t launch_small(const double* H, long long ldh, long long h_stride, con
                          cudaStream_t st) {
   static bool attr[3] = {false, false, false};
   const int dp = small_dpad(lp.d);
-  const size_t smem = (size_t)3 * dp * (dp + 4) * sizeof(double);
+  const size_t smem = (size_t)3 * dp * (dp == 96 ? dp + 4 : dp + 8) * sizeof(double);
   switch (dp) {
     case 32:
-      ns_small_kernel<32><<<batch, kSmallThreads, smem, st>>>(H, ldh, h_stride, jobs, job0, lp, R, ldr, r_stride, state);
+      ns_small_kernel<32><<<batch, small_threads<32>(), smem, st>>>(H, ldh, h_stride, jobs, job0, lp, R, ldr, r_stride, state);
       break;
     case 64:
       if (!attr[1]) { cudaFuncSetAttribute(ns_small_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr[1] = true; }
-      ns_small_kernel<64><<<batch, kSmallThreads, smem, st>>>(H, ldh, h_stride, jobs, job0, lp, R, ldr, r_stride, state);
+      ns_small_kernel<64><<<batch, small_threads<64>(), smem, st>>>(H, ldh, h_stride, jobs, job0, lp, R, ldr, r_stride, state);
       break;
     case 96:
       if (!attr[2]) { cudaFuncSetAttribute(ns_small_kernel<96>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr[2] = true; }
-      ns_small_kernel<96><<<batch, kSmallThreads, smem, st>>>(H, ldh, h_stride, jobs, job0, lp, R, ldr, r_stride, state);
+      ns_small_kernel<96><<<batch, small_threads<96>(), smem, st>>>(H, ldh, h_stride, jobs, job0, lp, R, ldr, r_stride, state);
       break;
     default:
       return cudaErrorInvalidValue;
