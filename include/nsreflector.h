@@ -105,6 +105,9 @@ typedef struct {
  *   stop_at_switch mixed path: return the pre-polish iterate X_switch as R (no re-anchor,
  *                  no FP64 steps); flags then carry neither CONVERGED nor MAX_STEPS.
  *   lookahead      steps enqueued before the host reads the stop flag (0 = default).
+ *   polish         mixed path: arithmetic of the re-anchor's two dense products and of the
+ *                  polishing steps: 0 = FP64 DMMA (default), 1 = FP64 emulated on the INT8 tensor
+ *                  cores (the Ozaki products of NS_PREC_FP64_OZAKI).
  *   filter_a/b     the step X_{j+1} = a X_j + b X_j^3 (generic odd sign-preserving
  *                  filters; with tol = 0 and max_steps = m it is the fixed-depth filter phi_m).
  */
@@ -113,7 +116,8 @@ typedef struct {
   int32_t cg_iters;
   int32_t stop_at_switch;
   int32_t lookahead;
-  int32_t reserved[3];
+  int32_t polish;
+  int32_t reserved[2];
   double filter_a;   /* odd cubic filter step X <- filter_a X + filter_b X^3 (eq:signpreserving P:278-289); */
   double filter_b;   /* Newton–Schulz = (1.5, -0.5) (default).  FP64 paths only; mixed requires the default. */
 } ns_options_t;

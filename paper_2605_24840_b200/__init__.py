@@ -42,7 +42,7 @@ class NsResult(ctypes.Structure):
 
 class NsOptions(ctypes.Structure):
     _fields_ = [("switch_tol", ctypes.c_double), ("cg_iters", ctypes.c_int32), ("stop_at_switch", ctypes.c_int32),
-                ("lookahead", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3), ("filter_a", ctypes.c_double),
+                ("lookahead", ctypes.c_int32), ("polish", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2), ("filter_a", ctypes.c_double),
                 ("filter_b", ctypes.c_double)]
 
 

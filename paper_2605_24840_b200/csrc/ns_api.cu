@@ -117,7 +117,11 @@ std::vector<int2> make_tiles_oz(int n, bool sym) {
 std::vector<int2> make_tiles_full(int n) {
   std::vector<int2> v;
   v.reserve((size_t)n * n);
-  const int G = 12;
+  static const int G = [] {
+    const char* e = getenv("NS_TILE_GROUP_FULL");   // experiment knob, like NS_TILE_GROUP
+    const int g = e ? atoi(e) : 0;
+    return g > 0 ? g : 12;
+  }();
   for (int SI = 0; SI < n; SI += G)
     for (int SJ = 0; SJ < n; SJ += G)
       for (int I = SI; I < std::min(SI + G, n); ++I)
@@ -270,6 +274,7 @@ struct Opts {
   int cg_iters = 24;
   int stop_at_switch = 0;
   int lookahead = 0;
+  int polish = 0;                 // mixed path: 0 = FP64 DMMA re-anchor / polish, 1 = Ozaki INT8
   double ca = 1.5, cb = -0.5;
 };
 
@@ -280,6 +285,7 @@ Opts to_opts(const ns_options_t* o) {
     r.cg_iters = o->cg_iters;
     r.stop_at_switch = o->stop_at_switch;
     r.lookahead = o->lookahead;
+    r.polish = o->polish;
     r.ca = o->filter_a;
     r.cb = o->filter_b;
   }
@@ -564,22 +570,53 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
     const CUtensorMap& tXt = (j0 & 1) ? tmB : tmA;
     const CUtensorMap& tXo = (j0 & 1) ? tmA : tmB;
     const int nk = L.d_pad / kBK;
+    // polish = 1: the FP64-class products below run as Ozaki INT8 products (same operands / outputs)
+    const bool oz = (opt.polish == 1);
+    int8_t* slX = reinterpret_cast<int8_t*>(ws + L.off_ozx);
+    int8_t* slY = reinterpret_cast<int8_t*>(ws + L.off_ozy);
+    int* eX = reinterpret_cast<int*>(ws + L.off_oex);
+    int* eY = reinterpret_cast<int*>(ws + L.off_oey);
+    double* ores = reinterpret_cast<double*>(ws + L.off_ores);
+    double* otr = reinterpret_cast<double*>(ws + L.off_otr);
+    int2* otiles = reinterpret_cast<int2*>(ws + L.off_otiles);
+    CUtensorMap tOa, tOb, tOy;
+    if (oz) {
+      if ((s = encode_map_i8(&tOa, slX, L.d_pad, kOzSlices, kTile)) != NS_OK) return s;
+      if ((s = encode_map_i8(&tOb, slX, L.d_pad, kOzSlices, 64)) != NS_OK) return s;
+      if ((s = encode_map_i8(&tOy, slY, L.d_pad, kOzSlices, 64)) != NS_OK) return s;
+    }
+    const std::vector<int2> ot_full = oz ? make_tiles_oz(L.n, false) : std::vector<int2>();
+    // C = P Q^T over every tile (P, Q row panels), FP64 DMMA or Ozaki
+    auto dense = [&](const double* P, const CUtensorMap& tP, const double* Q, const CUtensorMap& tQ,
+                     double* C) -> ns_status_t {
+      if (oz) {
+        NS_CUDA(launch_ozaki_slice(P, slX, eX, L.d_pad, 1, st));
+        NS_CUDA(launch_ozaki_slice(Q, slY, eY, L.d_pad, 1, st));
+        OzParams pp{otiles, (int)ot_full.size(), L.d_pad / 64, L.d, L.d_pad, 0, C, nullptr, eX, eY, nullptr, nullptr, 2};
+        NS_CUDA(launch_ozaki_product(tOa, tOy, pp, 1, st));
+        nl += 3;
+      } else {
+        ProdParams pp{full, L.n * L.n, nk, L.d, L.d_pad, 0, C, nullptr, nullptr, nullptr, 2};
+        NS_CUDA(launch_product(tP, tQ, pp, 1, st));
+        nl += 1;
+      }
+      return NS_OK;
+    };
+    if (oz) NS_CUDA(cudaMemcpyAsync(otiles, ot_full.data(), ot_full.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
     if (opt.cg_iters > 0) {
-      // M = A X~  (FP64 DMMA, every tile) -> Y
-      ProdParams pm{full, L.n * L.n, nk, L.d, L.d_pad, 0, Y, nullptr, nullptr, nullptr, 2};
-      NS_CUDA(launch_product(tmAh, tXt, pm, 1, st));
+      // M = A X~  (every tile) -> Y
+      if ((s = dense(Ahat, tmAh, Xt, tXt, Y)) != NS_OK) return s;
       // C = M - M^T -> Xo ; |A| = sym(M) -> bf16 planes PY
       NS_CUDA(launch_commutator(Y, Xo, PY, L.d_pad, st, tf32));
-      // F' = X~ C^T = -X~ C  (FP64 DMMA, every tile) -> Y
-      ProdParams pf{full, L.n * L.n, nk, L.d, L.d_pad, 0, Y, nullptr, nullptr, nullptr, 2};
-      NS_CUDA(launch_product(tXt, tXo, pf, 1, st));
+      // F' = X~ C^T = -X~ C  (every tile) -> Y
+      if ((s = dense(Xt, tXt, Xo, tXo, Y)) != NS_OK) return s;
       // F = sym(X~ C); R = P = F; E = 0 (E lives in A's buffer, A is no longer needed)
       int np = 0;
       double* E = Ahat;
       NS_CUDA(launch_cg_init(Y, Rc, Pc, E, cgpart, L.d_pad, st, &np));
       NS_CUDA(launch_cg_scalar(cgsc, cgpart, np, 0, st));
       NS_CUDA(launch_split_planes(Pc, PXa, L.d_pad, 1, st, tf32));
-      nl += 6;
+      nl += 4;
       for (int it = 0; it < opt.cg_iters; ++it) {
         // W = |A| P (BF16x3 tcgen05, every tile) -> Xo
         MxParams pw{full, L.n * L.n, mx_nkb, L.d, L.d_pad, 0, Xo, nullptr, nullptr, nullptr, nullptr, 2, tf32 ? 1 : 0};
@@ -597,13 +634,45 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
       NS_CUDA(launch_apply_correction(Xt, E, L.d_pad, st));
       nl += 1;
     }
-    NS_CUDA(launch_trace_partials(Xt, L.d, L.d_pad, 1, trp, st));
-    nl += 1;
-
-    // ---------------- phase 2: FP64 steps from j0 to tolerance ----------------
+    // ---------------- phase 2: FP64-class steps from j0 to tolerance ----------------
     LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0, -1, 0};
     const int one = 1;
     NS_CUDA(cudaMemcpyAsync(n_active, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+    if (oz) {
+      // Ozaki steps (as run_ozaki): symmetric 128x64 tile list, its residual / trace partial layouts
+      const std::vector<int2> ot = make_tiles_oz(L.n, true);
+      const int nt = (int)ot.size(), ndiag = 2 * L.n;
+      NS_CUDA(cudaMemcpyAsync(otiles, ot.data(), ot.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+      NS_CUDA(cudaMemsetAsync(otr, 0, sizeof(double) * ndiag, st));
+      NS_CUDA(launch_trace_partials(Xt, L.d, L.d_pad, 1, otr, st));
+      nl += 1;
+      for (int j = j0; j <= max_steps; ++j) {
+        if (j >= j0 + LA) {
+          const int slot = (j - LA) % 16;
+          NS_CUDA(cudaEventSynchronize(rg.ev[slot]));
+          if (rg.slots[slot] == 0) break;
+        }
+        const bool odd = (j & 1) != 0;
+        double* Xc = odd ? Xb : Xa;
+        double* Xn = odd ? Xa : Xb;
+        NS_CUDA(launch_ozaki_slice(Xc, slX, eX, L.d_pad, 1, st));
+        OzParams sq{otiles, nt, L.d_pad / 64, L.d, L.d_pad, 0, Y, nullptr, eX, eX, ores, state, 0};
+        NS_CUDA(launch_ozaki_product(tOa, tOb, sq, 1, st));
+        NS_CUDA(launch_decide(state, djobs, ores, nt, otr, ndiag, lp, 1, n_active, st));
+        nl += 3;
+        if (j < max_steps) {
+          NS_CUDA(launch_ozaki_slice(Y, slY, eY, L.d_pad, 1, st));
+          OzParams up{otiles, nt, L.d_pad / 64, L.d, L.d_pad, 0, Xn, Xc, eX, eY, otr, state, 1, opt.ca, opt.cb};
+          NS_CUDA(launch_ozaki_product(tOa, tOy, up, 1, st));
+          nl += 2;
+        }
+        NS_CUDA(cudaMemcpyAsync(&rg.slots[j % 16], n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+        NS_CUDA(cudaEventRecord(rg.ev[j % 16], st));
+      }
+    }
+    if (!oz) {
+    NS_CUDA(launch_trace_partials(Xt, L.d, L.d_pad, 1, trp, st));
+    nl += 1;
     for (int j = j0; j <= max_steps; ++j) {
       if (j >= j0 + LA) {
         const int slot = (j - LA) % 16;
@@ -625,6 +694,7 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
       }
       NS_CUDA(cudaMemcpyAsync(&rg.slots[j % 16], n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
       NS_CUDA(cudaEventRecord(rg.ev[j % 16], st));
+    }
     }
   }
   NS_CUDA(launch_copy_out(Xa, Xb, L.d, L.d_pad, state, R, ldr, 0, 1, st));
@@ -808,8 +878,9 @@ extern "C" {
 
 size_t ns_workspace_bytes(int64_t d, ns_precision_t prec) {
   if (d < 1) return 0;
-  return make_layout(d, 1, prec == NS_PREC_MIXED_BF16X3 || prec == NS_PREC_MIXED_TF32X3, prec == NS_PREC_FP64_OZAKI,
-                     prec == NS_PREC_MIXED_TF32X3).total;
+  const bool mixed = prec == NS_PREC_MIXED_BF16X3 || prec == NS_PREC_MIXED_TF32X3;
+  // the mixed layout carries the Ozaki buffers too (options.polish = 1)
+  return make_layout(d, 1, mixed, prec == NS_PREC_FP64_OZAKI || mixed, prec == NS_PREC_MIXED_TF32X3).total;
 }
 
 size_t ns_workspace_bytes_batched(int64_t d, int64_t batch, ns_precision_t prec) {
@@ -849,11 +920,12 @@ ns_status_t ns_reflector_ex(const double* H, int64_t d, int64_t ldh, double s, d
   const bool mixed = (prec == NS_PREC_MIXED_BF16X3) || tf32;
   const bool ozaki = (prec == NS_PREC_FP64_OZAKI);
   if (ozaki && d > kOzMaxD) return fail(NS_ERR_UNSUPPORTED, "the Ozaki path needs d <= %d", kOzMaxD);
-  const Layout L = make_layout(d, 1, mixed, ozaki, tf32);
+  const Layout L = make_layout(d, 1, mixed, ozaki || mixed, tf32);
   if (ws_bytes < L.total)
     return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
   const Opts o = to_opts(opts);
-  if (mixed && (!(o.switch_tol >= 0.0) || o.cg_iters < 0)) return fail(NS_ERR_INVALID_ARG, "bad mixed options");
+  if (mixed && (!(o.switch_tol >= 0.0) || o.cg_iters < 0 || o.polish < 0 || o.polish > 1))
+    return fail(NS_ERR_INVALID_ARG, "bad mixed options");
   if (!std::isfinite(o.ca) || !std::isfinite(o.cb)) return fail(NS_ERR_INVALID_ARG, "filter coefficients must be finite");
   if (mixed && (o.ca != 1.5 || o.cb != -0.5))
     return fail(NS_ERR_UNSUPPORTED, "the mixed path runs the Newton-Schulz step (1.5, -0.5) only");
@@ -900,7 +972,7 @@ ns_status_t ns_reflector_host(const double* H_host, int64_t d, int64_t ldh, doub
   const bool mixed = (prec == NS_PREC_MIXED_BF16X3) || tf32;
   const bool ozaki = (prec == NS_PREC_FP64_OZAKI);
   if (ozaki && d > kOzMaxD) return fail(NS_ERR_UNSUPPORTED, "the Ozaki path needs d <= %d", kOzMaxD);
-  const Layout L = make_layout(d, 1, mixed, ozaki, tf32);
+  const Layout L = make_layout(d, 1, mixed, ozaki || mixed, tf32);
   if (ws_bytes < L.total)
     return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
@@ -973,7 +1045,7 @@ ns_status_t ns_symm_product(const double* A, const double* B, double* C, int64_t
   const bool tf32 = (prec == NS_PREC_MIXED_TF32X3);
   const bool mixed = (prec == NS_PREC_MIXED_BF16X3) || tf32;
   const bool ozaki = (prec == NS_PREC_FP64_OZAKI);
-  const Layout L = make_layout(d, 1, mixed, ozaki, tf32);
+  const Layout L = make_layout(d, 1, mixed, ozaki || mixed, tf32);
   if (ws_bytes < L.total) return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   uint8_t* w = static_cast<uint8_t*>(ws);

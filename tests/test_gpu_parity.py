@@ -269,15 +269,16 @@ def _mixed(nsr, p, **opts):
     return R, res
 
 
-@pytest.mark.parametrize("d,k", [(512, 32), (1024, 64)])
-def test_mixed_cfg3_recipe(nsr, d, k):
-    """north_star: mixed before polish <= 1e-4, after polish <= 1e-10 of the oracle, identical steps and cert."""
+@pytest.mark.parametrize("d,k,polish", [(512, 32, 0), (1024, 64, 0), (1024, 64, 1), (700, 40, 1)])
+def test_mixed_cfg3_recipe(nsr, d, k, polish):
+    """north_star: mixed before polish <= 1e-4, after polish <= 1e-10 of the oracle, identical steps and cert.
+    polish = 1: re-anchor products and polishing steps on the Ozaki INT8 products."""
     p = workloads.cfg3_dense(d=d, k=k)
     o = ons.ns_reflector(p.H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode, trace_residuals=True)
     Rpre, rpre = _mixed(nsr, p, stop_at_switch=1)
     pre = checks.frob_per_sqrt_d(Rpre.cpu().numpy(), o["R"])
     assert pre <= 1e-4, pre
-    R, res = _mixed(nsr, p)
+    R, res = _mixed(nsr, p, polish=polish)
     err = checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"])
     print(f"mixed d={d}: switch j={res['switch_step']} pre={pre:.3e} post={err:.3e} steps={res['steps']}")
     assert res["switch_step"] == rpre["steps"] and 0 < res["switch_step"] < o["steps"]
@@ -287,10 +288,11 @@ def test_mixed_cfg3_recipe(nsr, d, k):
     assert torch.equal(R, R.T)
 
 
-def test_mixed_fixed30(nsr):
+@pytest.mark.parametrize("polish", [0, 1])
+def test_mixed_fixed30(nsr, polish):
     p = workloads.cfg3_dense(d=512, k=32, mode="fixed30")
     o = ons.ns_reflector(p.H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
-    R, res = _mixed(nsr, p)
+    R, res = _mixed(nsr, p, polish=polish)
     assert res["steps"] == 30 and res["flags"] == o["flags"] == ons.MAX_STEPS
     assert checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= TOL_R
 
@@ -316,18 +318,19 @@ def test_mixed_cfg0(nsr):
     assert checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= TOL_R
 
 
-def test_mixed_cfg3_full_size_sampled(nsr):
+@pytest.mark.parametrize("polish", [0, 1])
+def test_mixed_cfg3_full_size_sampled(nsr, polish):
     """configs[3] mixed mode at d=16384: steps == prediction, cert 1024, sampled columns vs closed form."""
     p = workloads.cfg3_dense(form=False)
     p.extra["Hg"] = workloads.householder_form_fast(p.Vh, p.lam, device=_dev())
-    R, res = _mixed(nsr, p)
+    R, res = _mixed(nsr, p, polish=polish)
     steps_pred = scalar.predict_run((p.lam - p.s) / p.alpha, 100, 1e-10, True)[0]
     assert res["steps"] == steps_pred and res["cert"] == 1024 and res["flags"] == ons.CONVERGED
     cols = np.array([0, 3, 5000, 16383])
     Rc = closed_form.householder_reflector_columns(p.Vh, p.lam, 0.0, cols)
     Rg = R[:, torch.as_tensor(cols, device=_dev())].cpu().numpy()
     err = np.sqrt(np.mean(np.sum((Rg - Rc) ** 2, axis=0)))
-    print(f"mixed d=16384: switch j={res['switch_step']} err~{err:.3e}")
+    print(f"mixed d=16384 polish={polish}: switch j={res['switch_step']} err~{err:.3e}")
     assert err <= 1e-10
 
 

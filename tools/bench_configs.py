@@ -101,20 +101,22 @@ def cfg2(seed=0):
           "tflops": (2 * res["steps"] + 1) * 4096.0 ** 3 / (ms * 1e-3) / 1e12, "err_vs_oracle_cols": err})
 
 
-def cfg3(mode="tol", prec=nsr.NS_PREC_FP64, reps=3):
+def cfg3(mode="tol", prec=nsr.NS_PREC_FP64, reps=3, polish=0):
     p = workloads.cfg3_dense(form=False, mode=mode)
     H = workloads.householder_form_fast(p.Vh, p.lam, device=DEV)
     R = torch.empty_like(H)
     ws = nsr.alloc_workspace(nsr.ns_workspace_bytes(p.d, prec), DEV)
+    opts = nsr.ns_options(polish=polish) if polish else None
     (R, res), ms, _ = timed(lambda: nsr.ns_reflector(H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode, R=R, ws=ws,
-                                                     prec=prec), reps, 1)
+                                                     prec=prec, options=opts), reps, 1)
     cols = np.array([0, 1, 9999, 16383])
     Rc = closed_form.householder_reflector_columns(p.Vh, p.lam, 0.0, cols)
     Rg = R[:, torch.as_tensor(cols, device=DEV)].cpu().numpy()
     err = float(np.sqrt(np.mean(np.sum((Rg - Rc) ** 2, axis=0))))
     tf = (2 * res["steps"] + 1) * float(p.d) ** 3 / (ms * 1e-3) / 1e12
     emit({"config": "cfg3", "mode": mode, "prec": {0: "fp64", 1: "mixed_bf16x3", 2: "mixed_tf32x3",
-                                                   3: "fp64_ozaki_int8"}[prec], "d": p.d,
+                                                   3: "fp64_ozaki_int8"}[prec] + ("+ozaki_polish" if polish else ""),
+          "d": p.d,
           "time_to_R_ms": ms, "steps": res["steps"], "cert": res["cert"], "flags": res["flags"],
           "switch_step": res["switch_step"], "tflops": tf, "frac_fp64_peak": tf / PEAK, "err_vs_closed_form": err,
           "launches": res["launches"]})
@@ -184,6 +186,10 @@ def main():
             cfg3("fixed30", nsr.NS_PREC_FP64, reps=1)
         elif w == "cfg3fixedmixed":
             cfg3("fixed30", nsr.NS_PREC_MIXED_BF16X3, reps=1)
+        elif w == "cfg3mixedoz":
+            cfg3("tol", nsr.NS_PREC_MIXED_BF16X3, polish=1)
+        elif w == "cfg3fixedmixedoz":
+            cfg3("fixed30", nsr.NS_PREC_MIXED_BF16X3, reps=1, polish=1)
         elif w == "cfg3tf32":
             cfg3("tol", nsr.NS_PREC_MIXED_TF32X3)
         elif w == "cfg3ozaki":
