@@ -18,6 +18,9 @@
 // instead of 28 (ncu: with 28 N=64 UMMAs the issuing warp, not the tensor pipe, was the limit).
 // Symmetric outputs: tiles (I, J2) with J2*64 + 63 >= I*128; every element with j >= i is produced
 // by exactly one tile, which writes it and its mirror (bitwise-symmetric output).
+// Persistent launch (one CTA per SM walking the tile list): the producer prefetches the next tile and
+// the MMA warp starts it while the epilogue writes the previous one from registers.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 
@@ -78,21 +81,22 @@ __device__ __forceinline__ uint64_t sdesc_k64(uint32_t saddr) {
 template <int MODE>
 __global__ void __launch_bounds__(kOzThreads, 1)
     ns_ozaki_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                            const OzParams p) {
-  const int job = blockIdx.y;
-  if (p.state != nullptr && p.state[job].done) return;
+                            const OzParams p, int n_items) {
+  // Persistent: CTA b processes work items b, b + gridDim.x, ... (item = job * n_tiles + tile).  The
+  // stage ring, the chunk handshake and their phase bits run on across tiles, so the producer streams
+  // the next tile's k-blocks while the epilogue drains this one, and the MMA warp starts the next tile
+  // as soon as the accumulators are in registers (the epilogue writes C straight from registers:
+  // there is no staging buffer to wait for).
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOzStages * kOzStageBytes);
   uint64_t* empty = full + kOzStages;
   uint64_t* tfull = empty + kOzStages;     // chunk accumulated (MMA -> epilogue)
-  uint64_t* tempty = tfull + 1;            // chunk folded into FP64 (epilogue -> MMA)
+  uint64_t* tempty = tfull + 1;            // chunk folded into FP64 registers (epilogue -> MMA)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
   __shared__ double red[4];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int2 tile = p.tiles[blockIdx.x];
-  const int I = tile.x, J2 = tile.y;     // 128-row block, 64-column block
   const int n_chunks = (p.nkb + kOzChunkKb - 1) / kOzChunkKb;
 
   if (threadIdx.x == 0) {
@@ -114,146 +118,149 @@ __global__ void __launch_bounds__(kOzThreads, 1)
     if (lane == 0) {
       tma_prefetch_desc(&tmA);
       tma_prefetch_desc(&tmB);
-      for (int kb = 0; kb < p.nkb; ++kb) {
-        const int s = kb % kOzStages;
-        if (kb >= kOzStages) mbar_wait(&empty[s], ((kb / kOzStages) & 1u) ^ 1u);
-        uint8_t* st = smem + s * kOzStageBytes;
-        mbar_arrive_expect_tx(&full[s], kOzStageBytes);
+      uint32_t kbg = 0;                    // k-blocks issued by this CTA so far (ring position)
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int job = item / p.n_tiles;
+        if (p.state != nullptr && p.state[job].done) continue;
+        const int2 tile = p.tiles[item - job * p.n_tiles];
+        for (int kb = 0; kb < p.nkb; ++kb, ++kbg) {
+          const int s = kbg % kOzStages;
+          if (kbg >= kOzStages) mbar_wait(&empty[s], ((kbg / kOzStages) & 1u) ^ 1u);
+          uint8_t* st = smem + s * kOzStageBytes;
+          mbar_arrive_expect_tx(&full[s], kOzStageBytes);
 #pragma unroll
-        for (int q = 0; q < kOzSlices; ++q)
-          tma_load_3d(st + q * kOzSlabA, &tmA, kb * 64, I * kTile, job * kOzSlices + q, &full[s]);
+          for (int q = 0; q < kOzSlices; ++q)
+            tma_load_3d(st + q * kOzSlabA, &tmA, kb * 64, tile.x * kTile, job * kOzSlices + q, &full[s]);
 #pragma unroll
-        for (int q = 0; q < kOzSlices; ++q)
-          tma_load_3d(st + kOzSlices * kOzSlabA + q * kOzSlabB, &tmB, kb * 64, J2 * 64, job * kOzSlices + q,
-                      &full[s]);
+          for (int q = 0; q < kOzSlices; ++q)
+            tma_load_3d(st + kOzSlices * kOzSlabA + q * kOzSlabB, &tmB, kb * 64, tile.y * 64, job * kOzSlices + q,
+                        &full[s]);
+        }
       }
     }
   } else if (warp == 1) {
     // idesc: D=S32 (bits 4-5 = 2), A/B signed int8 (bits 7-9 / 10-12 = 1), K-major, M=128 (N set per MMA).
     const uint32_t idesc_base = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTile >> 4) << 24);
-    for (int c = 0; c < n_chunks; ++c) {
-      if (c >= 1) mbar_wait(tempty, static_cast<uint32_t>(c - 1) & 1u);   // accumulators folded
-      tc_fence_after();
-      const int kb0 = c * kOzChunkKb, kb1 = min(p.nkb, kb0 + kOzChunkKb);
-      for (int kb = kb0; kb < kb1; ++kb) {
-        const int s = kb % kOzStages;
-        mbar_wait(&full[s], static_cast<uint32_t>(kb / kOzStages) & 1u);
+    uint32_t kbg = 0, cg = 0;              // k-blocks / chunks consumed by this CTA so far
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int job = item / p.n_tiles;
+      if (p.state != nullptr && p.state[job].done) continue;
+      for (int c = 0; c < n_chunks; ++c, ++cg) {
+        if (cg >= 1) mbar_wait(tempty, (cg - 1) & 1u);   // accumulators folded by the epilogue
         tc_fence_after();
-        if (elect_one()) {
-          const uint32_t a0 = smem_u32(smem + s * kOzStageBytes);
-          const uint32_t b0 = a0 + kOzSlices * kOzSlabA;
-          const uint32_t first = (kb == kb0) ? 0u : 1u;
-          // Digit pairs (sa, sb), sb = sb0 .. sb0+n-1, share the A digit: the B digit slabs are stored
-          // back to back (64 rows each), so rows [64 sb0, 64 (sb0+n)) form ONE K-major operand of N = 64 n
-          // whose output columns are exactly the group accumulators sa+sb0 .. sa+sb0+n-1.  28 pairs
-          // become 10 UMMAs (N = 64..256) per K=32 half, with the same MACs: fewer issues and A re-reads.
+        const int kb0 = c * kOzChunkKb, kb1 = min(p.nkb, kb0 + kOzChunkKb);
+        for (int kb = kb0; kb < kb1; ++kb, ++kbg) {
+          const int s = kbg % kOzStages;
+          mbar_wait(&full[s], (kbg / kOzStages) & 1u);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t a0 = smem_u32(smem + s * kOzStageBytes);
+            const uint32_t b0 = a0 + kOzSlices * kOzSlabA;
+            const uint32_t first = (kb == kb0) ? 0u : 1u;
+            // Digit pairs (sa, sb), sb = sb0 .. sb0+n-1, share the A digit: the B digit slabs are stored
+            // back to back (64 rows each), so rows [64 sb0, 64 (sb0+n)) form ONE K-major operand of
+            // N = 64 n whose output columns are exactly the group accumulators sa+sb0 .. sa+sb0+n-1.
+            // 28 pairs become 10 UMMAs (N = 64..256) per K=32 half, with the same MACs.
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < 2; ++h) {
 #pragma unroll
-            for (int sa = 0; sa < kOzSlices; ++sa) {
+              for (int sa = 0; sa < kOzSlices; ++sa) {
 #pragma unroll
-              for (int sb0 = 0; sb0 < kOzSlices - sa; sb0 += 4) {
-                const int n = min(4, kOzSlices - sa - sb0);
-                const uint32_t idesc = idesc_base | ((uint32_t)(64 * n >> 3) << 17);
-                umma_i8(tmem + (uint32_t)(64 * (sa + sb0)), sdesc_k64(a0 + sa * kOzSlabA + 32 * h),
-                        sdesc_k64(b0 + sb0 * kOzSlabB + 32 * h), idesc, (sa == 0 && h == 0) ? first : 1u);
+                for (int sb0 = 0; sb0 < kOzSlices - sa; sb0 += 4) {
+                  const int n = min(4, kOzSlices - sa - sb0);
+                  const uint32_t idesc = idesc_base | ((uint32_t)(64 * n >> 3) << 17);
+                  umma_i8(tmem + (uint32_t)(64 * (sa + sb0)), sdesc_k64(a0 + sa * kOzSlabA + 32 * h),
+                          sdesc_k64(b0 + sb0 * kOzSlabB + 32 * h), idesc, (sa == 0 && h == 0) ? first : 1u);
+                }
               }
             }
+            umma_commit(&empty[s]);
+            if (kb == kb1 - 1) umma_commit(tfull);
           }
-          umma_commit(&empty[s]);
-          if (kb == kb1 - 1) umma_commit(tfull);
+          __syncwarp();
         }
-        __syncwarp();
       }
     }
   } else {
-    // ---------------- epilogue: fold each chunk's 7 INT32 group sums into FP64 (exact weights) ----------------
+    // ---------------- epilogue warps 2..5: TMEM lane quadrant q = warp % 4, tile row r ----------------
     const int q = warp & 3;
     const int r = q * 32 + lane;
-    double acc[64];
+    const int tid = threadIdx.x - 64;      // 0..127
+    uint32_t cg = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int job = item / p.n_tiles;
+      if (p.state != nullptr && p.state[job].done) continue;
+      const int2 tile = p.tiles[item - job * p.n_tiles];
+      double acc[64];
 #pragma unroll
-    for (int c = 0; c < 64; ++c) acc[c] = 0.0;
-    for (int ch = 0; ch < n_chunks; ++ch) {
-      mbar_wait(tfull, static_cast<uint32_t>(ch) & 1u);
-      tc_fence_after();
+      for (int c = 0; c < 64; ++c) acc[c] = 0.0;
+      for (int ch = 0; ch < n_chunks; ++ch, ++cg) {
+        mbar_wait(tfull, cg & 1u);
+        tc_fence_after();
 #pragma unroll 1
-      for (int g = kOzSlices - 1; g >= 0; --g) {      // smallest weights first
-        const double w = ldexp(1.0, -8 * g);
+        for (int g = kOzSlices - 1; g >= 0; --g) {      // smallest weights first
+          const double w = ldexp(1.0, -8 * g);
 #pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 16) {
-          uint32_t v[16];
-          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(g * 64 + c0), v);
+          for (int c0 = 0; c0 < 64; c0 += 16) {
+            uint32_t v[16];
+            tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(g * 64 + c0), v);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) acc[c0 + i] = fma((double)(int)v[i], w, acc[c0 + i]);
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(tempty);
-    }
-    const int er = p.expP[(long long)job * p.ld + I * kTile + r];
-    double* S = reinterpret_cast<double*>(smem);   // [128][65]; ring idle after the last chunk
-#pragma unroll
-    for (int c = 0; c < 64; ++c)
-      S[r * 65 + c] = ldexp(acc[c], er + p.expQ[(long long)job * p.ld + J2 * 64 + c] - 12);
-  }
-  tc_fence_before();
-  __syncthreads();
-
-  if (warp >= 2) {
-    double* S = reinterpret_cast<double*>(smem);
-    const int tid = threadIdx.x - 64;   // 0..127
-    const long long ld = p.ld;
-    const long long base = (long long)job * p.job_stride;
-    double* C = p.C + base;
-    const int i0 = I * kTile, j0 = J2 * 64;
-    double part = 0.0;
-    if (MODE == 2) {
-      for (int idx = tid; idx < kTile * 64; idx += 128) {
-        const int rr = idx >> 6, cc = idx & 63;
-        C[(long long)(i0 + rr) * ld + j0 + cc] = S[rr * 65 + cc];
-      }
-    } else {
-      const double* X = p.Xold + base;
-      // pass A: elements with j >= i (row-major, coalesced); update / residual / trace
-      for (int idx = tid; idx < kTile * 64; idx += 128) {
-        const int rr = idx >> 6, cc = idx & 63;
-        const int gi = i0 + rr, gj = j0 + cc;
-        if (gj < gi) continue;
-        double v = S[rr * 65 + cc];
-        const long long g = (long long)gi * ld + gj;
-        if (MODE == 1) {
-          v = fma(p.cb, v, p.ca * X[g]);
-          S[rr * 65 + cc] = v;
-          if (gi == gj && gi < p.d) part += v;
-        } else {
-          if (gj > gi) part += 2.0 * v * v;
-          else {
-            const double e = (gi < p.d) ? v - 1.0 : v;
-            part += e * e;
+            for (int i = 0; i < 16; ++i) acc[c0 + i] = fma((double)(int)v[i], w, acc[c0 + i]);
           }
         }
-        C[g] = v;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty);   // TMEM free: the MMA warp may start the next chunk / tile
       }
-      named_bar_sync(1, 128);
-      // pass B: mirrors C[j][i] (threads along i: coalesced)
-      for (int idx = tid; idx < kTile * 64; idx += 128) {
-        const int cc = idx >> 7, rr = idx & 127;
-        const int gi = i0 + rr, gj = j0 + cc;
-        if (gj <= gi) continue;
-        C[(long long)gj * ld + gi] = S[rr * 65 + cc];
-      }
+      // ---- write-out from registers (row r of the tile, 64 columns) ----
+      const long long base = (long long)job * p.job_stride;
+      const long long ld = p.ld;
+      double* C = p.C + base;
+      const int i0 = tile.x * kTile, j0 = tile.y * 64, gi = i0 + r;
+      const int er = p.expP[(long long)job * ld + gi];
+      const int* ecol = p.expQ + (long long)job * ld + j0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      if (lane == 0) red[warp - 2] = part;
-      named_bar_sync(1, 128);
-      if (tid == 0) {
-        const double s = ((red[0] + red[1]) + red[2]) + red[3];
-        if (MODE == 0) p.partial[(long long)job * p.n_tiles + blockIdx.x] = s;
-        else if (j0 <= i0 + kTile - 1 && j0 + 63 >= i0) p.partial[(long long)job * (2 * (p.ld / kTile)) + J2] = s;
+      for (int c = 0; c < 64; ++c) acc[c] = ldexp(acc[c], er + ecol[c] - 12);
+      double part = 0.0;
+      if (MODE == 2) {
+        double2* row = reinterpret_cast<double2*>(C + (long long)gi * ld + j0);
+#pragma unroll
+        for (int c = 0; c < 64; c += 2) row[c >> 1] = make_double2(acc[c], acc[c + 1]);
+      } else {
+        const double* X = p.Xold + base;
+        // element (gi, gj) is owned by this tile iff gj >= gi; it is written with its mirror (gj, gi)
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+          const int gj = j0 + c;
+          if (gj < gi) continue;
+          double v = acc[c];
+          if (MODE == 1) {
+            v = fma(p.cb, v, p.ca * X[(long long)gi * ld + gj]);
+            if (gi == gj && gi < p.d) part += v;
+          } else {
+            if (gj > gi) part += 2.0 * v * v;
+            else {
+              const double e = (gi < p.d) ? v - 1.0 : v;
+              part += e * e;
+            }
+          }
+          C[(long long)gi * ld + gj] = v;
+          if (gj > gi) C[(long long)gj * ld + gi] = v;   // lanes = consecutive gi: coalesced
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (lane == 0) red[warp - 2] = part;
+        named_bar_sync(1, 128);
+        if (tid == 0) {
+          const double sum = ((red[0] + red[1]) + red[2]) + red[3];
+          if (MODE == 0) p.partial[(long long)job * p.n_tiles + (item - job * p.n_tiles)] = sum;
+          else if (j0 <= i0 + kTile - 1 && j0 + 63 >= i0) p.partial[(long long)job * (2 * (p.ld / kTile)) + tile.y] = sum;
+        }
+        named_bar_sync(1, 128);              // red[] is reused by the next tile
       }
     }
   }
+  tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
@@ -267,19 +274,27 @@ cudaError_t launch_ozaki_slice(const double* X, int8_t* slices, int* expo, int d
 cudaError_t launch_ozaki_product(const CUtensorMap& tmA, const CUtensorMap& tmB, const OzParams& p, int batch,
                                  cudaStream_t st) {
   static bool attr[3] = {false, false, false};
-  dim3 grid(p.n_tiles, batch);
+  static int n_sm = 0;
+  if (n_sm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (n_sm <= 0) n_sm = 148;
+  }
+  const int n_items = p.n_tiles * batch;
+  const dim3 grid(std::min(n_items, n_sm));   // persistent: one CTA per SM
   switch (p.mode) {
     case 0:
       if (!attr[0]) { cudaFuncSetAttribute(ns_ozaki_product_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOzSmemBytes); attr[0] = true; }
-      ns_ozaki_product_kernel<0><<<grid, kOzThreads, kOzSmemBytes, st>>>(tmA, tmB, p);
+      ns_ozaki_product_kernel<0><<<grid, kOzThreads, kOzSmemBytes, st>>>(tmA, tmB, p, n_items);
       break;
     case 1:
       if (!attr[1]) { cudaFuncSetAttribute(ns_ozaki_product_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOzSmemBytes); attr[1] = true; }
-      ns_ozaki_product_kernel<1><<<grid, kOzThreads, kOzSmemBytes, st>>>(tmA, tmB, p);
+      ns_ozaki_product_kernel<1><<<grid, kOzThreads, kOzSmemBytes, st>>>(tmA, tmB, p, n_items);
       break;
     default:
       if (!attr[2]) { cudaFuncSetAttribute(ns_ozaki_product_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOzSmemBytes); attr[2] = true; }
-      ns_ozaki_product_kernel<2><<<grid, kOzThreads, kOzSmemBytes, st>>>(tmA, tmB, p);
+      ns_ozaki_product_kernel<2><<<grid, kOzThreads, kOzSmemBytes, st>>>(tmA, tmB, p, n_items);
       break;
   }
   return cudaGetLastError();
