@@ -412,9 +412,12 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
 }
 
 // Ozaki path (single problem): the FP64 loop with every product on the INT8 tensor cores.
-ns_status_t run_ozaki(const Layout& L, uint8_t* ws, const double* H, long long ldh, const JobParams& jp,
-                      int32_t max_steps, double tol, ns_tolmode_t tm, double* R, long long ldr, cudaStream_t st,
-                      const Opts& opt, DevState& out_state, int* launches) {
+// Ozaki path: L.batch problems (H + b*h_stride, R + b*r_stride), every product on the INT8 tensor cores.
+ns_status_t run_ozaki_batch(const Layout& L, uint8_t* ws, const double* H, long long ldh, long long h_stride,
+                            const std::vector<JobParams>& jobs, int32_t max_steps, double tol, ns_tolmode_t tm,
+                            double* R, long long ldr, long long r_stride, cudaStream_t st, const Opts& opt,
+                            std::vector<DevState>& states, int* launches) {
+  const int batch = (int)L.batch;
   double* Xa = reinterpret_cast<double*>(ws + L.off_xa);
   double* Xb = reinterpret_cast<double*>(ws + L.off_xb);
   double* Y = reinterpret_cast<double*>(ws + L.off_y);
@@ -432,21 +435,22 @@ ns_status_t run_ozaki(const Layout& L, uint8_t* ws, const double* H, long long l
   if (!rg.ok) return fail(NS_ERR_CUDA, "pinned status ring allocation failed");
   std::vector<int2> ot = make_tiles_oz(L.n, true);
   const int nt = (int)ot.size(), ndiag = 2 * L.n;
+  const long long js = (long long)L.d_pad * L.d_pad;
   NS_CUDA(cudaMemcpyAsync(otiles, ot.data(), ot.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
-  NS_CUDA(cudaMemcpyAsync(djobs, &jp, sizeof(JobParams), cudaMemcpyHostToDevice, st));
+  NS_CUDA(cudaMemcpyAsync(djobs, jobs.data(), jobs.size() * sizeof(JobParams), cudaMemcpyHostToDevice, st));
   CUtensorMap tXa, tXb, tY;
   ns_status_t s;
-  if ((s = encode_map_i8(&tXa, slX, L.d_pad, kOzSlices, kTile)) != NS_OK) return s;
-  if ((s = encode_map_i8(&tXb, slX, L.d_pad, kOzSlices, 64)) != NS_OK) return s;
-  if ((s = encode_map_i8(&tY, slY, L.d_pad, kOzSlices, 64)) != NS_OK) return s;
+  if ((s = encode_map_i8(&tXa, slX, L.d_pad, kOzSlices * batch, kTile)) != NS_OK) return s;
+  if ((s = encode_map_i8(&tXb, slX, L.d_pad, kOzSlices * batch, 64)) != NS_OK) return s;
+  if ((s = encode_map_i8(&tY, slY, L.d_pad, kOzSlices * batch, 64)) != NS_OK) return s;
   int nl = 0;
-  NS_CUDA(launch_zero_state(state, 1, n_active, st));
-  NS_CUDA(launch_init(H, ldh, 0, Xa, djobs, L.d, L.d_pad, 1, st));
-  NS_CUDA(cudaMemsetAsync(trp, 0, sizeof(double) * ndiag, st));
-  NS_CUDA(launch_trace_partials(Xa, L.d, L.d_pad, 1, trp, st));
+  NS_CUDA(launch_zero_state(state, batch, n_active, st));
+  NS_CUDA(launch_init(H, ldh, h_stride, Xa, djobs, L.d, L.d_pad, batch, st));
+  NS_CUDA(cudaMemsetAsync(trp, 0, sizeof(double) * ndiag * batch, st));
+  NS_CUDA(launch_trace_partials(Xa, L.d, L.d_pad, batch, trp, st, ndiag));
   nl += 3;
   LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0, -1, 0};
-  const int LA = 2;
+  const int LA = batch > 1 ? 8 : 2;
   for (int j = 0; j <= max_steps; ++j) {
     if (j >= LA) {
       const int slot = (j - LA) % 16;
@@ -456,26 +460,37 @@ ns_status_t run_ozaki(const Layout& L, uint8_t* ws, const double* H, long long l
     const bool odd = (j & 1) != 0;
     double* Xc = odd ? Xb : Xa;
     double* Xn = odd ? Xa : Xb;
-    NS_CUDA(launch_ozaki_slice(Xc, slX, eX, L.d_pad, 1, st));
-    OzParams sq{otiles, nt, L.d_pad / 64, L.d, L.d_pad, 0, Y, nullptr, eX, eX, res, state, 0};
-    NS_CUDA(launch_ozaki_product(tXa, tXb, sq, 1, st));
-    NS_CUDA(launch_decide(state, djobs, res, nt, trp, ndiag, lp, 1, n_active, st));
+    NS_CUDA(launch_ozaki_slice(Xc, slX, eX, L.d_pad, batch, st));
+    OzParams sq{otiles, nt, L.d_pad / 64, L.d, L.d_pad, js, Y, nullptr, eX, eX, res, state, 0};
+    NS_CUDA(launch_ozaki_product(tXa, tXb, sq, batch, st));
+    NS_CUDA(launch_decide(state, djobs, res, nt, trp, ndiag, lp, batch, n_active, st));
     nl += 3;
     if (j < max_steps) {
-      NS_CUDA(launch_ozaki_slice(Y, slY, eY, L.d_pad, 1, st));
-      OzParams up{otiles, nt, L.d_pad / 64, L.d, L.d_pad, 0, Xn, Xc, eX, eY, trp, state, 1, opt.ca, opt.cb};
-      NS_CUDA(launch_ozaki_product(tXa, tY, up, 1, st));
+      NS_CUDA(launch_ozaki_slice(Y, slY, eY, L.d_pad, batch, st));
+      OzParams up{otiles, nt, L.d_pad / 64, L.d, L.d_pad, js, Xn, Xc, eX, eY, trp, state, 1, opt.ca, opt.cb};
+      NS_CUDA(launch_ozaki_product(tXa, tY, up, batch, st));
       nl += 2;
     }
     NS_CUDA(cudaMemcpyAsync(&rg.slots[j % 16], n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
     NS_CUDA(cudaEventRecord(rg.ev[j % 16], st));
   }
-  NS_CUDA(launch_copy_out(Xa, Xb, L.d, L.d_pad, state, R, ldr, 0, 1, st));
+  NS_CUDA(launch_copy_out(Xa, Xb, L.d, L.d_pad, state, R, ldr, r_stride, batch, st));
   nl += 1;
-  NS_CUDA(cudaMemcpyAsync(&out_state, state, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+  states.resize(batch);
+  NS_CUDA(cudaMemcpyAsync(states.data(), state, sizeof(DevState) * batch, cudaMemcpyDeviceToHost, st));
   NS_CUDA(cudaStreamSynchronize(st));
   if (launches) *launches = nl;
   return NS_OK;
+}
+
+ns_status_t run_ozaki(const Layout& L, uint8_t* ws, const double* H, long long ldh, const JobParams& jp,
+                      int32_t max_steps, double tol, ns_tolmode_t tm, double* R, long long ldr, cudaStream_t st,
+                      const Opts& opt, DevState& out_state, int* launches) {
+  std::vector<DevState> states;
+  const ns_status_t s = run_ozaki_batch(L, ws, H, ldh, 0, std::vector<JobParams>{jp}, max_steps, tol, tm, R, ldr, 0,
+                                        st, opt, states, launches);
+  if (s == NS_OK) out_state = states[0];
+  return s;
 }
 
 // Mixed path (single problem): BF16x3 tcgen05 steps -> switch -> re-anchor -> FP64 steps.
@@ -884,9 +899,8 @@ size_t ns_workspace_bytes(int64_t d, ns_precision_t prec) {
 }
 
 size_t ns_workspace_bytes_batched(int64_t d, int64_t batch, ns_precision_t prec) {
-  (void)prec;
   if (d < 1 || batch < 1) return 0;
-  return make_layout(d, batch).total;
+  return make_layout(d, batch, false, prec == NS_PREC_FP64_OZAKI).total;
 }
 
 size_t ns_workspace_bytes_host(int64_t d, ns_precision_t prec) { return ns_workspace_bytes(d, prec); }
@@ -1005,7 +1019,8 @@ ns_status_t ns_reflector_batched(const double* H, int64_t d, int64_t batch, int6
   g_last_error.clear();
   ns_status_t st = check_common(d, max_steps, tol, tm, prec);
   if (st != NS_OK) return st;
-  if (prec != NS_PREC_FP64) return fail(NS_ERR_UNSUPPORTED, "the batched entry runs the FP64 path only");
+  if (prec != NS_PREC_FP64 && prec != NS_PREC_FP64_OZAKI)
+    return fail(NS_ERR_UNSUPPORTED, "the batched entry runs the FP64 and Ozaki paths only");
   if (batch < 1 || batch > 65535) return fail(NS_ERR_INVALID_ARG, "batch must be in [1, 65535]");
   if (!H || !R || !ws || !outs || !s || !alpha || !k) return fail(NS_ERR_INVALID_ARG, "null pointer argument");
   if (stride_h < d * d || stride_r < d * d) return fail(NS_ERR_INVALID_ARG, "strides must be >= d*d");
@@ -1018,13 +1033,18 @@ ns_status_t ns_reflector_batched(const double* H, int64_t d, int64_t batch, int6
     if (k[b] < 0 || k[b] > d) return fail(NS_ERR_INVALID_ARG, "k[%lld] out of [0, d]", (long long)b);
     jobs[b] = JobParams{s[b], alpha[b], k[b], 0};
   }
-  const Layout L = make_layout(d, batch);
+  const bool ozaki = (prec == NS_PREC_FP64_OZAKI);
+  const Layout L = make_layout(d, batch, false, ozaki);
   if (ws_bytes < L.total)
     return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
   std::vector<DevState> states;
   int nl = 0;
-  st = run_loop(L, static_cast<uint8_t*>(ws), H, d, stride_h, jobs, max_steps, tol, tm, R, d, stride_r,
-                static_cast<cudaStream_t>(stream), states, &nl);
+  if (ozaki)
+    st = run_ozaki_batch(L, static_cast<uint8_t*>(ws), H, d, stride_h, jobs, max_steps, tol, tm, R, d, stride_r,
+                         static_cast<cudaStream_t>(stream), Opts{}, states, &nl);
+  else
+    st = run_loop(L, static_cast<uint8_t*>(ws), H, d, stride_h, jobs, max_steps, tol, tm, R, d, stride_r,
+                  static_cast<cudaStream_t>(stream), states, &nl);
   if (st != NS_OK) return st;
   for (int64_t b = 0; b < batch; ++b) fill_result(states[b], nl, &outs[b]);
   return NS_OK;

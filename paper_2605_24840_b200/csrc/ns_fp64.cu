@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(256) ns_init_kernel(const double* __restrict__
 
 // tr X per 128-row diagonal block (fixed-order block reduction) -> tr_partial[job*n + b].
 __global__ void __launch_bounds__(128) ns_trace_partials_kernel(const double* __restrict__ X, int d, int d_pad,
-                                                                double* __restrict__ tr_partial) {
+                                                                double* __restrict__ tr_partial, int job_stride) {
   __shared__ double red[4];
   const int job = blockIdx.y, b = blockIdx.x, n = gridDim.x;
   const int i = b * kTile + threadIdx.x;
@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(128) ns_trace_partials_kernel(const double* __
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
   __syncthreads();
-  if (threadIdx.x == 0) tr_partial[(long long)job * n + b] = ((red[0] + red[1]) + red[2]) + red[3];
+  if (threadIdx.x == 0) tr_partial[(long long)job * (job_stride > 0 ? job_stride : n) + b] = ((red[0] + red[1]) + red[2]) + red[3];
 }
 
 // --------------------------------------------------------------------------------------
@@ -141,8 +141,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 
+  // MODE 1 reads the 128x128 tile of X_j in its epilogue: ask L2 for it a few stages before the end of
+  // the k loop (at small d -- the batched configs -- that read was an exposed HBM latency per CTA)
+  const int pf_kt = nst > 8 ? nst - 8 : 0;
   for (int kt = 0; kt < nst; ++kt) {
     const int s = kt % kStages;
+    if (MODE == 1 && kt == pf_kt) {
+      const double* Xt = p.Xold + (long long)job * p.job_stride + (long long)(I * kTile) * p.ld + J * kTile;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int l = threadIdx.x * 4 + u;     // 1024 lines of 128 B: row l >> 3, 16-double chunk l & 7
+        prefetch_l2(Xt + (long long)(l >> 3) * p.ld + (l & 7) * 16);
+      }
+    }
     if (threadIdx.x == 0 && kt >= 1 && kt - 1 + kStages < nst) {
       // every warp released stage kt-1: refill its slot with stage kt-1+kStages
       const int sp = (kt - 1) % kStages;
@@ -233,12 +244,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     // X_{j+1} = 1.5 X_j - 0.5 Z,  Z = X_j Y_j ; trace partial on diagonal tiles.
     const double* X = p.Xold + base;
     if (!diag) {
-      for (int idx = tid; idx < kTile * kTile; idx += 256) {
-        const int r = idx >> 7, c = idx & 127;
-        const long long gidx = (long long)(I * kTile + r) * ld + J * kTile + c;
-        const double v = fma(p.cb, S[r * kEpiPitch + c], p.ca * X[gidx]);
-        C[gidx] = v;
-        S[r * kEpiPitch + c] = v;
+      // X_j is read 8 elements at a time before any store (C may alias X as far as the compiler knows,
+      // so a load per iteration would otherwise wait out a full memory latency: ~35% of a configs[1]
+      // update launch in the ncu source view)
+      for (int idx0 = tid; idx0 < kTile * kTile; idx0 += 8 * 256) {
+        double xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int idx = idx0 + u * 256, r = idx >> 7, c = idx & 127;
+          xv[u] = X[(long long)(I * kTile + r) * ld + J * kTile + c];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int idx = idx0 + u * 256, r = idx >> 7, c = idx & 127;
+          const long long gidx = (long long)(I * kTile + r) * ld + J * kTile + c;
+          const double v = fma(p.cb, S[r * kEpiPitch + c], p.ca * xv[u]);
+          C[gidx] = v;
+          S[r * kEpiPitch + c] = v;
+        }
       }
       named_bar_sync(1, 32 * kConsumerWarps);
       for (int idx = tid; idx < kTile * kTile; idx += 256) {
@@ -246,13 +269,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         C[(long long)(J * kTile + r) * ld + I * kTile + c] = S[c * kEpiPitch + r];
       }
     } else {
-      for (int idx = tid; idx < kTile * kTile; idx += 256) {
-        const int r = idx >> 7, c = idx & 127;
-        if (r <= c) {
-          const long long gidx = (long long)(I * kTile + r) * ld + I * kTile + c;
-          const double v = fma(p.cb, S[r * kEpiPitch + c], p.ca * X[gidx]);
-          S[r * kEpiPitch + c] = v;
-          if (r == c && I * kTile + r < p.d) part += v;
+      for (int idx0 = tid; idx0 < kTile * kTile; idx0 += 8 * 256) {
+        double xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int idx = idx0 + u * 256, r = idx >> 7, c = idx & 127;
+          xv[u] = (r <= c) ? X[(long long)(I * kTile + r) * ld + I * kTile + c] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int idx = idx0 + u * 256, r = idx >> 7, c = idx & 127;
+          if (r <= c) {
+            const double v = fma(p.cb, S[r * kEpiPitch + c], p.ca * xv[u]);
+            S[r * kEpiPitch + c] = v;
+            if (r == c && I * kTile + r < p.d) part += v;
+          }
         }
       }
       named_bar_sync(1, 32 * kConsumerWarps);
@@ -401,9 +432,9 @@ cudaError_t launch_init(const double* H, long long ldh, long long h_stride, doub
 }
 
 cudaError_t launch_trace_partials(const double* X, int d, int d_pad, int batch, double* tr_partial,
-                                  cudaStream_t st) {
+                                  cudaStream_t st, int job_stride) {
   dim3 grid(d_pad / kTile, batch);
-  ns_trace_partials_kernel<<<grid, kTile, 0, st>>>(X, d, d_pad, tr_partial);
+  ns_trace_partials_kernel<<<grid, kTile, 0, st>>>(X, d, d_pad, tr_partial, job_stride);
   return cudaGetLastError();
 }
 

@@ -130,7 +130,7 @@ cudaError_t launch_mx_product(const CUtensorMap& tmP, const CUtensorMap& tmQ, co
 cudaError_t launch_init(const double* H, long long ldh, long long h_stride, double* X, const JobParams* jobs,
                         int d, int d_pad, int batch, cudaStream_t st);
 cudaError_t launch_trace_partials(const double* X, int d, int d_pad, int batch, double* tr_partial,
-                                  cudaStream_t st);
+                                  cudaStream_t st, int job_stride = 0);
 cudaError_t launch_product(const CUtensorMap& tmP, const CUtensorMap& tmQ, const ProdParams& p, int batch,
                            cudaStream_t st);
 cudaError_t launch_decide(DevState* state, const JobParams* jobs, const double* res_partial, int n_tiles,
@@ -165,11 +165,11 @@ constexpr int kOzSlices = 7;                           // balanced base-256 int8
 constexpr int kOzChunkKb = 256;                        // k-blocks (x64) per INT32 chunk: exact for any d
 constexpr int kOzMaxD = 65536;
 constexpr int kOzStages = 2;
-constexpr int kOzThreads = 192;                        // warp 0 TMA, warp 1 MMA, warps 2..5 epilogue
+constexpr int kOzThreads = 320;                        // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
 constexpr int kOzSlabA = kTile * 64;                   // 128 rows x 64 int8
 constexpr int kOzSlabB = 64 * 64;                      // 64 rows x 64 int8
 constexpr int kOzStageBytes = kOzSlices * (kOzSlabA + kOzSlabB);
-constexpr int kOzSmemBytes = kOzStages * kOzStageBytes + 1024 + 256;
+constexpr int kOzSmemBytes = kOzStages * kOzStageBytes + 1024 + 256 + 8 * 32 * 17 * 8;   // + epilogue staging
 
 struct OzParams {
   const int2* tiles;       // (I: 128-row block, J2: 64-column block)

@@ -13,7 +13,7 @@
 //
 // CTA tile 128 x 64, 7 accumulators x 64 columns = 448 TMEM columns.  Stage = one 64-wide k-block of
 // the 7 digits of both operands (7 x 8 KB + 7 x 4 KB, 64-B swizzle), 2 stages; warp 0 TMA, warp 1 MMA,
-// warps 2..5 epilogue.  The B digit slabs lie back to back, so the pairs (sa, sb0..sb0+n-1) are ONE
+// warps 2..9 epilogue.  The B digit slabs lie back to back, so the pairs (sa, sb0..sb0+n-1) are ONE
 // UMMA (M=128, N=64n <= 256, K=32) writing n adjacent group accumulators: 10 UMMAs per K=32 half
 // instead of 28 (ncu: with 28 N=64 UMMAs the issuing warp, not the tensor pipe, was the limit).
 // Symmetric outputs: tiles (I, J2) with J2*64 + 63 >= I*128; every element with j >= i is produced
@@ -63,6 +63,34 @@ __global__ void __launch_bounds__(256) ns_ozaki_slice_kernel(const double* __res
   }
 }
 
+// The same exponent and digits with one warp per row (8 rows per block): for small d_pad (the batched
+// configs) a 256-thread block per 256-element row was mostly block scheduling and barrier overhead.
+__global__ void __launch_bounds__(256) ns_ozaki_slice_rows_kernel(const double* __restrict__ X,
+                                                                  int8_t* __restrict__ slices, int* __restrict__ expo,
+                                                                  int d_pad) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), job = blockIdx.y, lane = threadIdx.x & 31;
+  const long long nn = (long long)d_pad * d_pad;
+  const double* x = X + (long long)job * nn + (long long)row * d_pad;
+  double m = 0.0;
+  for (int j = lane; j < d_pad; j += 32) m = fmax(m, fabs(x[j]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  int e = 0;
+  if (m > 0.0 && isfinite(m)) frexp(m, &e);
+  if (lane == 0) expo[(long long)job * d_pad + row] = e;
+  int8_t* out = slices + (long long)job * kOzSlices * nn + (long long)row * d_pad;
+  for (int j = lane; j < d_pad; j += 32) {
+    long long N = (long long)rint(ldexp(x[j], 54 - e));
+#pragma unroll
+    for (int q = kOzSlices - 1; q >= 1; --q) {
+      const long long D = ((N + 128) & 255) - 128;
+      out[(long long)q * nn + j] = (int8_t)D;
+      N = (N - D) >> 8;
+    }
+    out[j] = (int8_t)N;
+  }
+}
+
 __device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                         uint32_t accumulate) {
   asm volatile(
@@ -94,7 +122,8 @@ __global__ void __launch_bounds__(kOzThreads, 1)
   uint64_t* tfull = empty + kOzStages;     // chunk accumulated (MMA -> epilogue)
   uint64_t* tempty = tfull + 1;            // chunk folded into FP64 registers (epilogue -> MMA)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
-  __shared__ double red[4];
+  double* stage_base = reinterpret_cast<double*>(smem + kOzStages * kOzStageBytes + 256);   // 4 x [32][17]
+  __shared__ double red[8];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_chunks = (p.nkb + kOzChunkKb - 1) / kOzChunkKb;
@@ -105,7 +134,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 4);
+    mbar_init(tempty, 8);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -182,81 +211,106 @@ __global__ void __launch_bounds__(kOzThreads, 1)
       }
     }
   } else {
-    // ---------------- epilogue warps 2..5: TMEM lane quadrant q = warp % 4, tile row r ----------------
-    const int q = warp & 3;
+    // ---------------- epilogue warps 2..9: TMEM lane quadrant q = warp % 4, column half hc ----------------
+    const int q = warp & 3, hc = (warp - 2) >> 2;
     const int r = q * 32 + lane;
-    const int tid = threadIdx.x - 64;      // 0..127
+    const int ew = warp - 2;               // 0..7
     uint32_t cg = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int job = item / p.n_tiles;
       if (p.state != nullptr && p.state[job].done) continue;
       const int2 tile = p.tiles[item - job * p.n_tiles];
-      double acc[64];
+      double acc[32];
 #pragma unroll
-      for (int c = 0; c < 64; ++c) acc[c] = 0.0;
+      for (int c = 0; c < 32; ++c) acc[c] = 0.0;
       for (int ch = 0; ch < n_chunks; ++ch, ++cg) {
         mbar_wait(tfull, cg & 1u);
         tc_fence_after();
 #pragma unroll 1
         for (int g = kOzSlices - 1; g >= 0; --g) {      // smallest weights first
           const double w = ldexp(1.0, -8 * g);
+          uint32_t v[32];
+          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(g * 64 + hc * 32), v);   // one wait per group
 #pragma unroll
-          for (int c0 = 0; c0 < 64; c0 += 16) {
-            uint32_t v[16];
-            tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(g * 64 + c0), v);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) acc[c0 + i] = fma((double)(int)v[i], w, acc[c0 + i]);
-          }
+          for (int i = 0; i < 32; ++i) acc[i] = fma((double)(int)v[i], w, acc[i]);
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty);   // TMEM free: the MMA warp may start the next chunk / tile
       }
-      // ---- write-out from registers (row r of the tile, 64 columns) ----
+      // ---- write-out from registers (row r of the tile, columns 32 hc .. 32 hc + 31) ----
       const long long base = (long long)job * p.job_stride;
       const long long ld = p.ld;
       double* C = p.C + base;
-      const int i0 = tile.x * kTile, j0 = tile.y * 64, gi = i0 + r;
+      const int i0 = tile.x * kTile, j0 = tile.y * 64 + hc * 32, gi = i0 + r;
       const int er = p.expP[(long long)job * ld + gi];
       const int* ecol = p.expQ + (long long)job * ld + j0;
 #pragma unroll
-      for (int c = 0; c < 64; ++c) acc[c] = ldexp(acc[c], er + ecol[c] - 12);
+      for (int c = 0; c < 32; ++c) {
+        // times 2^(er + ec - 12): one multiply by the power of two built from its bits (ldexp only when
+        // that power is outside the normal range, i.e. for extreme operand scales)
+        const int ex = er + ecol[c] - 12;
+        acc[c] = (ex >= -1022 && ex <= 1023) ? acc[c] * __hiloint2double((ex + 1023) << 20, 0) : ldexp(acc[c], ex);
+      }
       double part = 0.0;
-      if (MODE == 2) {
-        double2* row = reinterpret_cast<double2*>(C + (long long)gi * ld + j0);
+      const double* X = p.Xold + base;
+      double* stg = stage_base + ew * (32 * 17);   // this warp's 32 x 16 staging block (pitch 17)
+      // 16-column blocks: values (MODE 1: from X_j, read 16 at a time ahead of any store) are computed
+      // per thread (= row), mirrors go straight out (lanes = consecutive rows of the mirror: coalesced),
+      // and the row-major part is transposed through the staging block so every store instruction
+      // writes two full 128-byte row segments.
 #pragma unroll
-        for (int c = 0; c < 64; c += 2) row[c >> 1] = make_double2(acc[c], acc[c + 1]);
-      } else {
-        const double* X = p.Xold + base;
-        // element (gi, gj) is owned by this tile iff gj >= gi; it is written with its mirror (gj, gi)
+      for (int cb = 0; cb < 2; ++cb) {
+        double xbuf[16];
+        if (MODE == 1) {
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          const int gj = j0 + c;
-          if (gj < gi) continue;
-          double v = acc[c];
-          if (MODE == 1) {
-            v = fma(p.cb, v, p.ca * X[(long long)gi * ld + gj]);
-            if (gi == gj && gi < p.d) part += v;
-          } else {
-            if (gj > gi) part += 2.0 * v * v;
-            else {
-              const double e = (gi < p.d) ? v - 1.0 : v;
-              part += e * e;
-            }
+          for (int u = 0; u < 16; ++u) {
+            const int gj = j0 + 16 * cb + u;
+            xbuf[u] = (gj >= gi) ? X[(long long)gi * ld + gj] : 0.0;
           }
-          C[(long long)gi * ld + gj] = v;
-          if (gj > gi) C[(long long)gj * ld + gi] = v;   // lanes = consecutive gi: coalesced
         }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int c = 16 * cb + u, gj = j0 + c;
+          double v = acc[c];
+          if (MODE != 2 && gj >= gi) {          // element owned by this tile (written with its mirror)
+            if (MODE == 1) {
+              v = fma(p.cb, v, p.ca * xbuf[u]);
+              if (gi == gj && gi < p.d) part += v;
+            } else {
+              if (gj > gi) part += 2.0 * v * v;
+              else {
+                const double e = (gi < p.d) ? v - 1.0 : v;
+                part += e * e;
+              }
+            }
+            if (gj > gi) C[(long long)gj * ld + gi] = v;
+          }
+          stg[lane * 17 + u] = v;
+        }
+        __syncwarp();
+#pragma unroll 4
+        for (int rr = 0; rr < 32; rr += 2) {
+          const int row = rr + (lane >> 4), col = lane & 15;
+          const int gi2 = i0 + q * 32 + row, gj2 = j0 + 16 * cb + col;
+          if (MODE == 2 || gj2 >= gi2) C[(long long)gi2 * ld + gj2] = stg[row * 17 + col];
+        }
+        __syncwarp();
+      }
+      if (MODE != 2) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        if (lane == 0) red[warp - 2] = part;
-        named_bar_sync(1, 128);
-        if (tid == 0) {
-          const double sum = ((red[0] + red[1]) + red[2]) + red[3];
+        if (lane == 0) red[ew] = part;
+        named_bar_sync(1, 256);
+        if (ew == 0 && lane == 0) {
+          double sum = 0.0;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) sum += red[w];
+          const int i0t = tile.x * kTile, j0t = tile.y * 64;
           if (MODE == 0) p.partial[(long long)job * p.n_tiles + (item - job * p.n_tiles)] = sum;
-          else if (j0 <= i0 + kTile - 1 && j0 + 63 >= i0) p.partial[(long long)job * (2 * (p.ld / kTile)) + tile.y] = sum;
+          else if (j0t <= i0t + kTile - 1 && j0t + 63 >= i0t) p.partial[(long long)job * (2 * (p.ld / kTile)) + tile.y] = sum;
         }
-        named_bar_sync(1, 128);              // red[] is reused by the next tile
+        named_bar_sync(1, 256);              // red[] is reused by the next tile
       }
     }
   }
@@ -266,8 +320,13 @@ __global__ void __launch_bounds__(kOzThreads, 1)
 }
 
 cudaError_t launch_ozaki_slice(const double* X, int8_t* slices, int* expo, int d_pad, int batch, cudaStream_t st) {
-  dim3 grid(d_pad, batch);
-  ns_ozaki_slice_kernel<<<grid, 256, 0, st>>>(X, slices, expo, d_pad);
+  if (d_pad <= 2048) {
+    dim3 grid(d_pad / 8, batch);
+    ns_ozaki_slice_rows_kernel<<<grid, 256, 0, st>>>(X, slices, expo, d_pad);
+  } else {
+    dim3 grid(d_pad, batch);
+    ns_ozaki_slice_kernel<<<grid, 256, 0, st>>>(X, slices, expo, d_pad);
+  }
   return cudaGetLastError();
 }
 

@@ -135,11 +135,14 @@ def test_cfg2_allen_cahn_small_grid(nsr):
     assert checks.frob_per_sqrt_d(R, R_eig) <= 1e-10
 
 
-def test_cfg1_batched_subset(nsr):
+@pytest.mark.parametrize("prec", [0, 3])
+def test_cfg1_batched_subset(nsr, prec):
+    """configs[1] problems through the batched entry (FP64 DMMA, or every product on the Ozaki INT8 path):
+    oracle steps / flags / reflector outside the tie band, certificate, direction error."""
     probs = workloads.cfg1_batched(seed=0, first=0, count=8)
     H = torch.from_numpy(np.stack([p.H for p in probs])).to(_dev())
     R, outs = nsr.ns_reflector_batched(H, [p.s for p in probs], [p.alpha for p in probs], [p.k for p in probs],
-                                       100, 1e-12)
+                                       100, 1e-12, prec=prec)
     R = R.cpu().numpy()
     for i, p in enumerate(probs):
         o = ons.ns_reflector(p.H, p.s, p.alpha, p.k, 100, 1e-12, 0, trace_residuals=True)

@@ -59,15 +59,15 @@ def cfg0():
               "tflops": (2 * res["steps"] + 1) * 64 ** 3 / (ms * 1e-3) / 1e12})
 
 
-def cfg1(n_mat=2048):
+def cfg1(n_mat=2048, prec=nsr.NS_PREC_FP64):
     t0 = time.time()
     probs = workloads.cfg1_batched(seed=0, n_matrices=2048, count=n_mat)
     gen_s = time.time() - t0
     H = torch.from_numpy(np.stack([p.H for p in probs])).to(DEV)
-    ws = nsr.alloc_workspace(nsr.ns_workspace_bytes_batched(256, len(probs)), DEV)
+    ws = nsr.alloc_workspace(nsr.ns_workspace_bytes_batched(256, len(probs), prec), DEV)
     R = torch.empty_like(H)
     s_, a_, k_ = [p.s for p in probs], [p.alpha for p in probs], [p.k for p in probs]
-    (R, outs), ms, _ = timed(lambda: nsr.ns_reflector_batched(H, s_, a_, k_, 100, 1e-12, R=R, ws=ws), 3, 1)
+    (R, outs), ms, _ = timed(lambda: nsr.ns_reflector_batched(H, s_, a_, k_, 100, 1e-12, R=R, ws=ws, prec=prec), 3, 1)
     steps = np.array([o["steps"] for o in outs])
     pred = np.array([scalar.predict_run((p.lam - p.s) / p.alpha, 100, 1e-12, False)[0] for p in probs])
     certs_ok = all(o["cert"] == p.k for o, p in zip(outs, probs))
@@ -78,7 +78,8 @@ def cfg1(n_mat=2048):
                                     @ probs[i].extra["probe"])) for i in range(0, len(probs), max(1, len(probs) // 64)))
     mid = steps[0::3]
     off = np.minimum(steps[1::3], steps[2::3])
-    emit({"config": "cfg1", "problems": len(probs), "d": 256, "time_ms": ms, "reflectors_per_s": len(probs) / (ms * 1e-3),
+    emit({"config": "cfg1", "prec": {0: "fp64", 3: "fp64_ozaki_int8"}[prec], "problems": len(probs), "d": 256,
+          "time_ms": ms, "reflectors_per_s": len(probs) / (ms * 1e-3),
           "tflops": flops / (ms * 1e-3) / 1e12, "steps_sum": int(steps.sum()), "steps_min": int(steps.min()),
           "steps_max": int(steps.max()), "steps_equal_prediction": int(np.sum(steps == pred)),
           "steps_off_by_one": int(np.sum(np.abs(steps - pred) == 1)), "certs_ok": certs_ok,
@@ -175,6 +176,8 @@ def main():
             cfg1()
         elif w == "cfg1small":
             cfg1(64)
+        elif w == "cfg1ozaki":
+            cfg1(prec=nsr.NS_PREC_FP64_OZAKI)
         elif w == "cfg2":
             cfg2(0)
             cfg2(1)
