@@ -67,9 +67,11 @@ Layout make_layout(int64_t d, int64_t batch, bool mixed = false, bool ozaki = fa
   L.off_xa = o; o = align256(o + mat);
   L.off_xb = o; o = align256(o + mat);
   L.off_y = o; o = align256(o + mat);
-  L.off_res = o; o = align256(o + sizeof(double) * (size_t)L.n_tiles * batch);
-  L.off_tr = o; o = align256(o + sizeof(double) * (size_t)L.n * batch);
-  L.off_tiles = o; o = align256(o + sizeof(int2) * (size_t)L.n_tiles);
+  // residual / trace partials and the tile list sized for 64-tiles too (d_pad <= k64MaxDpad)
+  const size_t n64 = 2 * (size_t)L.n, nt_max = std::max<size_t>(L.n_tiles, n64 * (n64 + 1) / 2);
+  L.off_res = o; o = align256(o + sizeof(double) * nt_max * batch);
+  L.off_tr = o; o = align256(o + sizeof(double) * n64 * batch);
+  L.off_tiles = o; o = align256(o + sizeof(int2) * nt_max);
   L.off_jobs = o; o = align256(o + sizeof(JobParams) * (size_t)batch);
   L.off_state = o; o = align256(o + sizeof(DevState) * (size_t)batch);
   L.off_active = o; o = align256(o + 256);
@@ -171,12 +173,12 @@ EncodeTiledFn get_encode() {
 
 // 3-D map over `batch` row-major d_pad x d_pad FP64 matrices; box = 16 (k) x 128 (rows) x 1,
 // 128-byte swizzle (the consumer's fragment addressing assumes exactly this pattern).
-ns_status_t encode_map(CUtensorMap* m, const double* base, int d_pad, long long batch) {
+ns_status_t encode_map(CUtensorMap* m, const double* base, int d_pad, long long batch, int box_rows = kTile) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(NS_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   cuuint64_t dims[3] = {(cuuint64_t)d_pad, (cuuint64_t)d_pad, (cuuint64_t)batch};
   cuuint64_t strides[2] = {(cuuint64_t)d_pad * 8, (cuuint64_t)d_pad * (cuuint64_t)d_pad * 8};
-  cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)kTile, 1};
+  cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -335,18 +337,27 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
     return NS_OK;
   }
   NS_CUDA(cudaMemcpyAsync(djobs, jobs.data(), jobs.size() * sizeof(JobParams), cudaMemcpyHostToDevice, st));
-  std::vector<int2> tl = make_tiles(L.n);
+  // d_pad <= k64MaxDpad: 64x64 upper tiles (ns_product64_kernel), otherwise 128x128
+  const bool t64 = L.d_pad <= k64MaxDpad;
+  const int tile_rows = t64 ? k64Tile : kTile;
+  const int nb = L.d_pad / tile_rows;                 // tile blocks per dimension (= diagonal partials)
+  std::vector<int2> tl = make_tiles(nb);
+  const int n_t = (int)tl.size();
   NS_CUDA(cudaMemcpyAsync(tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+  auto product = [&](const CUtensorMap& a, const CUtensorMap& b, const ProdParams& pp) {
+    return t64 ? launch_product64(a, b, pp, batch, st) : launch_product(a, b, pp, batch, st);
+  };
 
   CUtensorMap tmA, tmB, tmY;
   ns_status_t s;
-  if ((s = encode_map(&tmA, Xa, L.d_pad, batch)) != NS_OK) return s;
-  if ((s = encode_map(&tmB, Xb, L.d_pad, batch)) != NS_OK) return s;
-  if ((s = encode_map(&tmY, Y, L.d_pad, batch)) != NS_OK) return s;
+  if ((s = encode_map(&tmA, Xa, L.d_pad, batch, tile_rows)) != NS_OK) return s;
+  if ((s = encode_map(&tmB, Xb, L.d_pad, batch, tile_rows)) != NS_OK) return s;
+  if ((s = encode_map(&tmY, Y, L.d_pad, batch, tile_rows)) != NS_OK) return s;
 
   NS_CUDA(launch_zero_state(state, batch, n_active, st));
   NS_CUDA(launch_init(H, ldh, h_stride, Xa, djobs, L.d, L.d_pad, batch, st));
-  NS_CUDA(launch_trace_partials(Xa, L.d, L.d_pad, batch, trp, st));
+  if (t64) NS_CUDA(cudaMemsetAsync(trp, 0, sizeof(double) * nb * batch, st));
+  NS_CUDA(launch_trace_partials(Xa, L.d, L.d_pad, batch, trp, st, nb));   // 128-block sums, stride nb
   int nl = 3;
   Profiler& pf = prof();
   // event slots: 4 per step (square begin/end, update begin/end)
@@ -368,16 +379,16 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
     double* Xn = odd ? Xa : Xb;
     const CUtensorMap& tmC = odd ? tmB : tmA;
 
-    ProdParams sq{tiles, L.n_tiles, L.d_pad / kBK, L.d, L.d_pad, job_stride, Y, nullptr, res, state, 0};
+    ProdParams sq{tiles, n_t, L.d_pad / kBK, L.d, L.d_pad, job_stride, Y, nullptr, res, state, 0};
     if (pf.on) NS_CUDA(cudaEventRecord(pf.get(4 * j + 0), st));
-    NS_CUDA(launch_product(tmC, tmC, sq, batch, st));
+    NS_CUDA(product(tmC, tmC, sq));
     if (pf.on) NS_CUDA(cudaEventRecord(pf.get(4 * j + 1), st));
-    NS_CUDA(launch_decide(state, djobs, res, L.n_tiles, trp, L.n, lp, batch, n_active, st));
+    NS_CUDA(launch_decide(state, djobs, res, n_t, trp, nb, lp, batch, n_active, st));
     nl += 2;
     if (j < max_steps) {
-      ProdParams up{tiles, L.n_tiles, L.d_pad / kBK, L.d, L.d_pad, job_stride, Xn, Xc, trp, state, 1, opt.ca, opt.cb};
+      ProdParams up{tiles, n_t, L.d_pad / kBK, L.d, L.d_pad, job_stride, Xn, Xc, trp, state, 1, opt.ca, opt.cb};
       if (pf.on) NS_CUDA(cudaEventRecord(pf.get(4 * j + 2), st));
-      NS_CUDA(launch_product(tmC, tmY, up, batch, st));
+      NS_CUDA(product(tmC, tmY, up));
       if (pf.on) NS_CUDA(cudaEventRecord(pf.get(4 * j + 3), st));
       nl += 1;
     }

@@ -313,6 +313,186 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // --------------------------------------------------------------------------------------
+// 64x64-tile variant for small and batched problems (d_pad <= 1024): the upper triangle in 64-tiles
+// wastes less on diagonal tiles (d = 256: 10 tiles of 64^2 instead of 3 of 128^2 per product, 17%
+// fewer MACs), gives 4x more CTAs to a single mid-size problem, and with 96 KB of shared memory and
+// 128 threads two CTAs share an SM, so one CTA's epilogue overlaps the other's DMMA loop.
+// Same scheme as ns_product_kernel: TMA ring (box 16 x 64, 128-B swizzle), thread 0 refills, 4 DMMA
+// warps with 32x32 warp tiles and the k-permuted conflict-free LDS.128 fragments, staged epilogue.
+// --------------------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(k64Threads, 2)
+    ns_product64_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
+                        const ProdParams p) {
+  const int job = blockIdx.y;
+  if (p.state != nullptr && p.state[job].done) return;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  double* sA = reinterpret_cast<double*>(smem);                                      // [stages*kSPS][64*16]
+  double* sB = reinterpret_cast<double*>(smem + k64Stages * kSPS * k64Tile * kBK * 8);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + k64Stages * k64StageBytes);
+  uint64_t* empty = full + k64Stages;
+  __shared__ double red[k64Threads / 32];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int2 tile = p.tiles[blockIdx.x];
+  const int I = tile.x, J = tile.y;        // 64-blocks
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < k64Stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], k64Threads / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int nst = p.nk / kSPS;
+  auto issue = [&](int kt) {
+    const int s = kt % k64Stages;
+    mbar_arrive_expect_tx(&full[s], k64StageBytes);
+#pragma unroll
+    for (int u = 0; u < kSPS; ++u) {
+      tma_load_3d(sA + (s * kSPS + u) * k64Tile * kBK, &tmP, (kt * kSPS + u) * kBK, I * k64Tile, job, &full[s]);
+      tma_load_3d(sB + (s * kSPS + u) * k64Tile * kBK, &tmQ, (kt * kSPS + u) * kBK, J * k64Tile, job, &full[s]);
+    }
+  };
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmP);
+    tma_prefetch_desc(&tmQ);
+    for (int kt = 0; kt < k64Stages && kt < nst; ++kt) issue(kt);
+  }
+  const int wm = warp >> 1, wn = warp & 1;   // warp tile rows wm*32, cols wn*32
+  const int g = lane >> 2, t = lane & 3;
+  const uint32_t off_h0 = static_cast<uint32_t>(((2 * t + 0) ^ g) << 4);
+  const uint32_t off_h1 = static_cast<uint32_t>(((2 * t + 1) ^ g) << 4);
+  const uint32_t a_row = static_cast<uint32_t>((wm * 32 + g) * 128);
+  const uint32_t b_row = static_cast<uint32_t>((wn * 32 + g) * 128);
+  const uint32_t sA_u32 = smem_u32(sA), sB_u32 = smem_u32(sB);
+  double acc[4][4][2];
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+  const int pf_kt = nst > 8 ? nst - 8 : 0;
+  for (int kt = 0; kt < nst; ++kt) {
+    const int s = kt % k64Stages;
+    if (MODE == 1 && kt == pf_kt) {           // X_j tile for the epilogue: ask L2 early
+      const double* Xt = p.Xold + (long long)job * p.job_stride + (long long)(I * k64Tile) * p.ld + J * k64Tile;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int l = threadIdx.x * 4 + u;     // 512 lines of 64 B: row l >> 3 (0..63), 8-double chunk l & 7
+        prefetch_l2(Xt + (long long)(l >> 3) * p.ld + (l & 7) * 8);
+      }
+    }
+    if (threadIdx.x == 0 && kt >= 1 && kt - 1 + k64Stages < nst) {
+      const int sp = (kt - 1) % k64Stages;
+      mbar_wait(&empty[sp], static_cast<uint32_t>((kt - 1) / k64Stages) & 1u);
+      issue(kt - 1 + k64Stages);
+    }
+    mbar_wait(&full[s], static_cast<uint32_t>(kt / k64Stages) & 1u);
+#pragma unroll
+    for (int hh = 0; hh < 2 * kSPS; ++hh) {
+      const int h = hh & 1;
+      const uint32_t aS = sA_u32 + (s * kSPS + (hh >> 1)) * (k64Tile * kBK * 8) + a_row;
+      const uint32_t bS = sB_u32 + (s * kSPS + (hh >> 1)) * (k64Tile * kBK * 8) + b_row;
+      const uint32_t off = h ? off_h1 : off_h0;
+      double a[4][2], b[4][2];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) lds128(bS + ni * 8 * 128 + off, b[ni][0], b[ni][1]);
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) lds128(aS + mi * 8 * 128 + off, a[mi][0], a[mi][1]);
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi][e], b[ni][e]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  // ---------------- epilogue (ring reused as staging once every warp is past the loop) ----------------
+  __syncthreads();
+  constexpr int EP = k64Tile + 1;
+  double* S = reinterpret_cast<double*>(smem);   // [64][65]
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int r = wm * 32 + mi * 8 + g, c = wn * 32 + ni * 8 + 2 * t;
+      S[r * EP + c] = acc[mi][ni][0];
+      S[r * EP + c + 1] = acc[mi][ni][1];
+    }
+  __syncthreads();
+  const int tid = threadIdx.x;
+  const long long ld = p.ld;
+  const long long base = (long long)job * p.job_stride;
+  double* C = p.C + base;
+  const bool diag = (I == J);
+  const int i0 = I * k64Tile, j0 = J * k64Tile;
+  double part = 0.0;
+  constexpr int NE = k64Tile * k64Tile;          // 4096 elements, 32 per thread
+  if (MODE == 1) {
+    const double* X = p.Xold + base;
+    for (int idx0 = tid; idx0 < NE; idx0 += 8 * k64Threads) {
+      double xv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = idx0 + u * k64Threads, r = idx >> 6, c = idx & 63;
+        xv[u] = (!diag || r <= c) ? X[(long long)(i0 + r) * ld + j0 + c] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = idx0 + u * k64Threads, r = idx >> 6, c = idx & 63;
+        if (!diag || r <= c) {
+          const double v = fma(p.cb, S[r * EP + c], p.ca * xv[u]);
+          S[r * EP + c] = v;
+          if (diag && r == c && i0 + r < p.d) part += v;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (!diag) {
+    for (int idx = tid; idx < NE; idx += k64Threads) {
+      const int r = idx >> 6, c = idx & 63;
+      const double v = S[r * EP + c];
+      C[(long long)(i0 + r) * ld + j0 + c] = v;
+      if (MODE == 0) part += v * v;
+    }
+    if (MODE == 0) part *= 2.0;
+    for (int idx = tid; idx < NE; idx += k64Threads) {
+      const int r = idx >> 6, c = idx & 63;   // mirror row j0+r, col i0+c <- tile (c, r)
+      C[(long long)(j0 + r) * ld + i0 + c] = S[c * EP + r];
+    }
+  } else {
+    for (int idx = tid; idx < NE; idx += k64Threads) {
+      const int r = idx >> 6, c = idx & 63;
+      const double v = (r <= c) ? S[r * EP + c] : S[c * EP + r];
+      C[(long long)(i0 + r) * ld + i0 + c] = v;
+      if (MODE == 0) {
+        if (r < c) {
+          part += 2.0 * v * v;
+        } else if (r == c) {
+          const double e = (i0 + r < p.d) ? v - 1.0 : v;
+          part += e * e;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if (lane == 0) red[warp] = part;
+  __syncthreads();
+  if (tid == 0) {
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < k64Threads / 32; ++w) sum += red[w];
+    if (MODE == 0) p.partial[(long long)job * p.n_tiles + blockIdx.x] = sum;
+    else if (diag) p.partial[(long long)job * (p.ld / k64Tile) + I] = sum;
+  }
+}
+
+// --------------------------------------------------------------------------------------
 // Stop decision for step j (one CTA per problem); fixed-order reductions.
 // --------------------------------------------------------------------------------------
 __device__ __forceinline__ double block_sum_fixed(const double* v, int n, double* red) {
@@ -435,6 +615,20 @@ cudaError_t launch_trace_partials(const double* X, int d, int d_pad, int batch, 
                                   cudaStream_t st, int job_stride) {
   dim3 grid(d_pad / kTile, batch);
   ns_trace_partials_kernel<<<grid, kTile, 0, st>>>(X, d, d_pad, tr_partial, job_stride);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_product64(const CUtensorMap& tmP, const CUtensorMap& tmQ, const ProdParams& p, int batch,
+                             cudaStream_t st) {
+  static bool attr[2] = {false, false};
+  dim3 grid(p.n_tiles, batch);
+  if (p.mode == 0) {
+    if (!attr[0]) { cudaFuncSetAttribute(ns_product64_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, k64SmemBytes); attr[0] = true; }
+    ns_product64_kernel<0><<<grid, k64Threads, k64SmemBytes, st>>>(tmP, tmQ, p);
+  } else {
+    if (!attr[1]) { cudaFuncSetAttribute(ns_product64_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, k64SmemBytes); attr[1] = true; }
+    ns_product64_kernel<1><<<grid, k64Threads, k64SmemBytes, st>>>(tmP, tmQ, p);
+  }
   return cudaGetLastError();
 }
 

@@ -16,6 +16,13 @@ constexpr int kThreads = 32 * kConsumerWarps;         // 8 DMMA warps; warp 0 la
 constexpr int kStageBytes = kSPS * 2 * kTile * kBK * 8;   // A + B per stage = 64 KB
 constexpr int kEpiPitch = kTile + 1;                  // staging row pitch (doubles), odd => conflict-free columns
 constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+// 64x64-tile variant (small / batched problems): 4 DMMA warps, 3 stages of 32 KB, 2 CTAs per SM
+constexpr int k64Tile = 64;
+constexpr int k64Threads = 128;
+constexpr int k64Stages = 3;
+constexpr int k64StageBytes = kSPS * 2 * k64Tile * kBK * 8;   // 32 KB
+constexpr int k64SmemBytes = k64Stages * k64StageBytes + 1024 + 256;
+constexpr int k64MaxDpad = 1024;                              // d_pad <= this uses the 64-tile kernel
 
 // Per-problem device state (one per job).  Written only by ns_decide_kernel.
 struct DevState {
@@ -131,6 +138,8 @@ cudaError_t launch_init(const double* H, long long ldh, long long h_stride, doub
                         int d, int d_pad, int batch, cudaStream_t st);
 cudaError_t launch_trace_partials(const double* X, int d, int d_pad, int batch, double* tr_partial,
                                   cudaStream_t st, int job_stride = 0);
+cudaError_t launch_product64(const CUtensorMap& tmP, const CUtensorMap& tmQ, const ProdParams& p, int batch,
+                             cudaStream_t st);
 cudaError_t launch_product(const CUtensorMap& tmP, const CUtensorMap& tmQ, const ProdParams& p, int batch,
                            cudaStream_t st);
 cudaError_t launch_decide(DevState* state, const JobParams* jobs, const double* res_partial, int n_tiles,
