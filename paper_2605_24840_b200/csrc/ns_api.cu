@@ -338,7 +338,11 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
   }
   NS_CUDA(cudaMemcpyAsync(djobs, jobs.data(), jobs.size() * sizeof(JobParams), cudaMemcpyHostToDevice, st));
   // d_pad <= k64MaxDpad: 64x64 upper tiles (ns_product64_kernel), otherwise 128x128
-  const bool t64 = L.d_pad <= k64MaxDpad;
+  static const bool t64_on = [] {
+    const char* e = getenv("NS_TILE64");   // experiment knob: 0 forces 128-tiles everywhere
+    return !(e && e[0] == '0');
+  }();
+  const bool t64 = t64_on && L.d_pad <= k64MaxDpad;
   const int tile_rows = t64 ? k64Tile : kTile;
   const int nb = L.d_pad / tile_rows;                 // tile blocks per dimension (= diagonal partials)
   std::vector<int2> tl = make_tiles(nb);

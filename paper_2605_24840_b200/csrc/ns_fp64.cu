@@ -181,6 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi][e], b[ni][e]);
     }
+    fence_proxy_async();                 // generic reads of the slot before the TMA refill (see 64-tile kernel)
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // warps with 32x32 warp tiles and the k-permuted conflict-free LDS.128 fragments, staged epilogue.
 // --------------------------------------------------------------------------------------
 template <int MODE>
-__global__ void __launch_bounds__(k64Threads, 2)
+__global__ void __launch_bounds__(k64Threads, k64Stages == 2 ? 3 : 2)
     ns_product64_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
                         const ProdParams p) {
   const int job = blockIdx.y;
@@ -407,6 +408,10 @@ __global__ void __launch_bounds__(k64Threads, 2)
 #pragma unroll
           for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi][e], b[ni][e]);
     }
+    // the slot is refilled by TMA (async proxy) once every warp has arrived: order this warp's generic-
+    // proxy reads of it before the release (without the fence, 3 CTAs/SM with a 2-stage ring produced
+    // nondeterministic results -- a refill overtaking the last LDS of the slot)
+    fence_proxy_async();
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }

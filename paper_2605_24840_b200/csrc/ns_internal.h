@@ -19,9 +19,15 @@ constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barrie
 // 64x64-tile variant (small / batched problems): 4 DMMA warps, 3 stages of 32 KB, 2 CTAs per SM
 constexpr int k64Tile = 64;
 constexpr int k64Threads = 128;
-constexpr int k64Stages = 3;
+#ifndef NS_K64_STAGES
+#define NS_K64_STAGES 2
+#endif
+constexpr int k64Stages = NS_K64_STAGES;
 constexpr int k64StageBytes = kSPS * 2 * k64Tile * kBK * 8;   // 32 KB
-constexpr int k64SmemBytes = k64Stages * k64StageBytes + 1024 + 256;
+#ifndef NS_K64_PAD
+#define NS_K64_PAD 0
+#endif
+constexpr int k64SmemBytes = k64Stages * k64StageBytes + 1024 + 256 + NS_K64_PAD;
 constexpr int k64MaxDpad = 1024;                              // d_pad <= this uses the 64-tile kernel
 
 // Per-problem device state (one per job).  Written only by ns_decide_kernel.

@@ -199,6 +199,19 @@ def test_deterministic(nsr):
     assert torch.equal(R1, R2) and r1 == r2
 
 
+def test_deterministic_batched_full_occupancy(nsr):
+    """Many batched problems keep every SM busy with several 64-tile CTAs (the regime where a missing
+    generic->async proxy fence once let a TMA refill overtake a shared-memory read): bitwise repeatable."""
+    probs = workloads.cfg1_batched(seed=0, n_matrices=2048, count=512)
+    H = torch.from_numpy(np.stack([p.H for p in probs])).to(_dev())
+    args = ([p.s for p in probs], [p.alpha for p in probs], [p.k for p in probs], 100, 1e-12)
+    R1, o1 = nsr.ns_reflector_batched(H, *args)
+    R1 = R1.clone()
+    for _ in range(2):
+        R2, o2 = nsr.ns_reflector_batched(H, *args)
+        assert torch.equal(R1, R2) and o1 == o2
+
+
 # ------------------------------------------------------------------ full size (bench launch configuration)
 def test_cfg3_full_size_sampled(nsr):
     """configs[3] at d=16384 exactly as bench.py runs it: steps == scalar-recurrence prediction,
