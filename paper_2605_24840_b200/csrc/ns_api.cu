@@ -67,7 +67,7 @@ Layout make_layout(int64_t d, int64_t batch, bool mixed = false, bool ozaki = fa
   L.off_xa = o; o = align256(o + mat);
   L.off_xb = o; o = align256(o + mat);
   L.off_y = o; o = align256(o + mat);
-  // residual / trace partials and the tile list sized for 64-tiles too (d_pad <= k64MaxDpad)
+  // residual / trace partials and the tile list sized for 64-tiles too (use_tile64)
   const size_t n64 = 2 * (size_t)L.n, nt_max = std::max<size_t>(L.n_tiles, n64 * (n64 + 1) / 2);
   L.off_res = o; o = align256(o + sizeof(double) * nt_max * batch);
   L.off_tr = o; o = align256(o + sizeof(double) * n64 * batch);
@@ -122,7 +122,7 @@ std::vector<int2> make_tiles_full(int n) {
   static const int G = [] {
     const char* e = getenv("NS_TILE_GROUP_FULL");   // experiment knob, like NS_TILE_GROUP
     const int g = e ? atoi(e) : 0;
-    return g > 0 ? g : 12;
+    return g > 0 ? g : 6;
   }();
   for (int SI = 0; SI < n; SI += G)
     for (int SJ = 0; SJ < n; SJ += G)
@@ -294,6 +294,31 @@ Opts to_opts(const ns_options_t* o) {
   return r;
 }
 
+// 64x64 or 128x128 product tiles for the FP64 step loop.  Wave model: a 128-tile costs T per SM
+// (one CTA per SM); three 64-tile CTAs share an SM and finish a wave of 3 x n_SM tiles in ~0.75 T.
+// 64-tiles are taken when they need >= 5% less time (small d, batches, and sizes where 128-tiles
+// leave a mostly empty last wave -- d = 3000: 26.5 ms vs 18.1 ms, d = 8192: -6.7%), else 128-tiles
+// (d = 16384: 56 waves either way; the 128 kernel is the profiled headline kernel).
+// NS_TILE64=0/1 forces one kind (experiments).
+bool use_tile64(int d_pad, long long batch) {
+  static const int force = [] {
+    const char* e = getenv("NS_TILE64");
+    return e ? atoi(e) : -1;
+  }();
+  if (force == 0 || force == 1) return force == 1;
+  static int n_sm = 0;
+  if (n_sm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n_sm <= 0) n_sm = 148;
+  }
+  const long long n = d_pad / kTile, m = d_pad / k64Tile;
+  const long long t128 = n * (n + 1) / 2 * batch, t64 = m * (m + 1) / 2 * batch;
+  const double w128 = (double)((t128 + n_sm - 1) / n_sm);
+  const double w64 = 0.75 * (double)((t64 + 3 * n_sm - 1) / (3 * n_sm));
+  return w64 <= 0.95 * w128;
+}
+
 // The step loop shared by the single, host and batched entry points.  H: batch matrices
 // at H + b*h_stride (ld ldh).  R likewise.  Returns per-job states in `states`.
 ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ldh, long long h_stride,
@@ -337,12 +362,7 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
     return NS_OK;
   }
   NS_CUDA(cudaMemcpyAsync(djobs, jobs.data(), jobs.size() * sizeof(JobParams), cudaMemcpyHostToDevice, st));
-  // d_pad <= k64MaxDpad: 64x64 upper tiles (ns_product64_kernel), otherwise 128x128
-  static const bool t64_on = [] {
-    const char* e = getenv("NS_TILE64");   // experiment knob: 0 forces 128-tiles everywhere
-    return !(e && e[0] == '0');
-  }();
-  const bool t64 = t64_on && L.d_pad <= k64MaxDpad;
+  const bool t64 = use_tile64(L.d_pad, batch);
   const int tile_rows = t64 ? k64Tile : kTile;
   const int nb = L.d_pad / tile_rows;                 // tile blocks per dimension (= diagonal partials)
   std::vector<int2> tl = make_tiles(nb);

@@ -28,7 +28,6 @@ constexpr int k64StageBytes = kSPS * 2 * k64Tile * kBK * 8;   // 32 KB
 #define NS_K64_PAD 0
 #endif
 constexpr int k64SmemBytes = k64Stages * k64StageBytes + 1024 + 256 + NS_K64_PAD;
-constexpr int k64MaxDpad = 1024;                              // d_pad <= this uses the 64-tile kernel
 
 // Per-problem device state (one per job).  Written only by ns_decide_kernel.
 struct DevState {

@@ -360,8 +360,9 @@ def comm1(nsr):
 
 
 def test_sharded_p1_matches_single_and_oracle(nsr, comm1):
-    # d_pad > 1024: the single path uses the same 128x128 tiles as the sharded one, so results are bitwise equal
-    p = workloads.cfg3_dense(d=1152, k=72)
+    # d = 2048: the single path picks the same 128x128 tiles as the sharded one (use_tile64's wave
+    # model), so results are bitwise equal
+    p = workloads.cfg3_dense(d=2048, k=128)
     Hg = torch.from_numpy(p.H).to(_dev())
     Rs, rs = nsr.ns_reflector_sharded(comm1, Hg, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
     Rd, rd = nsr.ns_reflector(Hg, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
