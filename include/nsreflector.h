@@ -311,6 +311,16 @@ void ns_profile_get(ns_profile_t* out);
 
 /* Library identification: build string with the compile target (e.g. "sm_100a"). */
 const char* ns_build_info(void);
+
+/*
+ * Diagnostics (tools/mx_timeline.py): when `device_buffer` is non-NULL, the 2-SM split-precision
+ * kernel launched by ns_symm_product (prec NS_PREC_MIXED_*) writes 12 uint64 per CTA into it
+ * (%globaltimer at start, when the accumulators are in registers, at the end; SM id; leader MMA warp
+ * cycles waiting for operands, its loop cycles, producer cycles waiting for free stages, MMA cycles
+ * waiting for TMEM; epilogue cycles waiting for / folding accumulator chunks).  The buffer must hold
+ * 12 x CTAs entries; NULL turns the stamps off (default).
+ */
+void ns_debug_mx_trace(void* device_buffer);
 const char* ns_status_string(ns_status_t st);
 /* Thread-local message for the last non-NS_OK status on this thread ("" if none). */
 const char* ns_last_error(void);

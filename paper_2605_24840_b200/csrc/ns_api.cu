@@ -116,6 +116,31 @@ std::vector<int2> make_tiles_oz(int n, bool sym) {
   return v;
 }
 
+// Tile pairs for the 2-SM split-precision kernel: (I2, J) = rows [256 I2, +256) x cols [128 J, +128);
+// sym: only pairs touching the upper triangle (J >= 2 I2).  Super-blocks as in make_tiles.
+std::vector<int2> make_tiles_pairs(int n, bool sym) {
+  const int n2 = (n + 1) / 2, G = 8;
+  std::vector<int2> v;
+  for (int SI = 0; SI < n2; SI += G / 2)
+    for (int SJ = sym ? 2 * SI : 0; SJ < n; SJ += G)
+      for (int I2 = SI; I2 < std::min(SI + G / 2, n2); ++I2)
+        for (int J = std::max(SJ, sym ? 2 * I2 : 0); J < std::min(SJ + G, n); ++J) v.push_back(make_int2(I2, J));
+  return v;
+}
+
+// Diagnostics: when set, the 2-SM split-precision kernel launched by ns_symm_product records per-CTA
+// %globaltimer stamps (start, accumulators done, end, SM id) -- tools/mx_timeline.py.
+unsigned long long* g_mx_trace = nullptr;
+
+// 2-SM (cta_group::2) split-precision products on by default; NS_MX2=0 selects the one-SM kernel.
+bool use_mx2() {
+  static const bool on = [] {
+    const char* e = getenv("NS_MX2");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 std::vector<int2> make_tiles_full(int n) {
   std::vector<int2> v;
   v.reserve((size_t)n * n);
@@ -204,13 +229,14 @@ ns_status_t encode_map_i8(CUtensorMap* m, const int8_t* base, int d_pad, long lo
 
 // 3-D map over `nplanes` row-major d_pad x d_pad BF16 planes; box = 64 (k) x 128 (rows) x 1, 128-B swizzle
 // (the layout the UMMA shared-memory descriptors in ns_mixed.cu describe).
-ns_status_t encode_map_bf16(CUtensorMap* m, const void* base, int d_pad, long long nplanes, bool tf32 = false) {
+ns_status_t encode_map_bf16(CUtensorMap* m, const void* base, int d_pad, long long nplanes, bool tf32 = false,
+                            int box_rows = kTile) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(NS_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   const cuuint64_t esz = tf32 ? 4 : 2;
   cuuint64_t dims[3] = {(cuuint64_t)d_pad, (cuuint64_t)d_pad, (cuuint64_t)nplanes};
   cuuint64_t strides[2] = {(cuuint64_t)d_pad * esz, (cuuint64_t)d_pad * (cuuint64_t)d_pad * esz};
-  cuuint32_t box[3] = {(cuuint32_t)(128 / esz), (cuuint32_t)kTile, 1};   // 128-byte rows: 64 bf16 or 32 tf32
+  cuuint32_t box[3] = {(cuuint32_t)(128 / esz), (cuuint32_t)box_rows, 1};   // 128-byte rows: 64 bf16 or 32 tf32
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
                    const_cast<void*>(base), dims, strides, box, estr,
@@ -1085,6 +1111,8 @@ ns_status_t ns_reflector_batched(const double* H, int64_t d, int64_t batch, int6
   return NS_OK;
 }
 
+void ns_debug_mx_trace(void* device_buffer) { g_mx_trace = static_cast<unsigned long long*>(device_buffer); }
+
 ns_status_t ns_symm_product(const double* A, const double* B, double* C, int64_t d, int64_t ld, int32_t mode,
                             ns_precision_t prec, void* ws, size_t ws_bytes, void* stream) {
   g_last_error.clear();
@@ -1146,11 +1174,19 @@ ns_status_t ns_symm_product(const double* A, const double* B, double* C, int64_t
     NS_CUDA(launch_split_planes(Pa, planesA, L.d_pad, 1, cs, tf32));
     NS_CUDA(launch_split_planes(Pb, planesB, L.d_pad, 1, cs, tf32));
     CUtensorMap tA, tB;
+    const bool mx2 = use_mx2();
     if ((s = encode_map_bf16(&tA, planesA, L.d_pad, 2, tf32)) != NS_OK) return s;
-    if ((s = encode_map_bf16(&tB, planesB, L.d_pad, 2, tf32)) != NS_OK) return s;
-    MxParams p{tiles, (int)tl.size(), L.d_pad / (tf32 ? 32 : kMxBK), L.d, L.d_pad, 0, Pc, Pa, nullptr, partial,
+    if ((s = encode_map_bf16(&tB, planesB, L.d_pad, 2, tf32, mx2 ? 64 : kTile)) != NS_OK) return s;
+    int nt = (int)tl.size();
+    if (mx2) {
+      const std::vector<int2> pl = make_tiles_pairs(L.n, mode != 2);
+      NS_CUDA(cudaMemcpyAsync(tiles, pl.data(), pl.size() * sizeof(int2), cudaMemcpyHostToDevice, cs));
+      nt = 2 * (int)pl.size();
+    }
+    MxParams p{tiles, nt, L.d_pad / (tf32 ? 32 : kMxBK), L.d, L.d_pad, 0, Pc, Pa, nullptr, partial,
                nullptr, mode, tf32 ? 1 : 0};
-    NS_CUDA(launch_mx_product(tA, tB, p, 1, cs));
+    p.trace = g_mx_trace;                  // diagnostics only (ns_debug_mx_trace)
+    NS_CUDA(mx2 ? launch_mx2_product(tA, tB, p, 1, cs) : launch_mx_product(tA, tB, p, 1, cs));
   }
   NS_CUDA(cudaMemcpy2DAsync(C, (size_t)ld * 8, Pc, (size_t)L.d_pad * 8, (size_t)d * 8, (size_t)d,
                             cudaMemcpyDeviceToDevice, cs));

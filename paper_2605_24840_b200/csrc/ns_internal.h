@@ -110,10 +110,20 @@ constexpr int kMxStages = 3;
 constexpr int kMxEpiWarps = 8;
 constexpr int kMxEpiThreads = 32 * kMxEpiWarps;
 constexpr int kMxThreads = 64 + kMxEpiThreads;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
-constexpr int kMxChunkKb = 8;                   // k-blocks (x64) per FP32 accumulation chunk (x3 split terms)
+#ifndef NS_MX_CHUNK_KB
+#define NS_MX_CHUNK_KB 16
+#endif
+constexpr int kMxChunkKb = NS_MX_CHUNK_KB;      // k-blocks (x64) per FP32 accumulation chunk (x3 split terms)
 constexpr int kMxSlab = kTile * kMxBK * 2;      // one 128 x 64 bf16 operand slab = 16 KB
 constexpr int kMxStageBytes = 4 * kMxSlab;      // A_hi, A_lo, B_hi, B_lo = 64 KB
 constexpr int kMxSmemBytes = kMxStages * kMxStageBytes + 1024 + 256;
+// 2-SM variant (cta_group::2): a CTA pair computes a 256 x 128 tile with M=256 UMMAs; each CTA stages
+// its own 128 rows of P and 64 of the 128 rows of Q (the two Q halves form one N=128 operand)
+constexpr int kMx2Stages = 4;
+constexpr int kMx2SlabA = kTile * kMxBK * 2;     // 128 x 64 bf16 = 16 KB
+constexpr int kMx2SlabB = 64 * kMxBK * 2;        // 64 x 64 bf16 = 8 KB
+constexpr int kMx2StageBytes = 2 * kMx2SlabA + 2 * kMx2SlabB;   // 48 KB per CTA
+constexpr int kMx2SmemBytes = kMx2Stages * kMx2StageBytes + 1024 + 256;
 
 // C_IJ = sum over the 3 split terms of P'_I Q'_J^T with P' = [P_hi P_lo P_hi], Q' = [Q_lo Q_hi Q_hi]
 // (small terms first), FP32 accumulation in TMEM.  Planes: [job][hi|lo][d_pad][d_pad] bf16.
@@ -131,12 +141,17 @@ struct MxParams {
   const DevState* state;
   int mode;                // 0 square (+res, mirror), 1 update (+trace, mirror), 2 dense tile (no mirror)
   int tf32 = 0;            // 0: BF16x3 (kind::f16), 1: TF32x3 (kind::tf32); nkb = d_pad / (tf32 ? 32 : 64)
+  unsigned long long* trace = nullptr;   // diagnostics: per-CTA %globaltimer stamps (start, mainloop done, end)
 };
 
 cudaError_t launch_split_planes(const double* X, void* planes, int d_pad, int batch, cudaStream_t st,
                                 bool tf32 = false);
 cudaError_t launch_mx_product(const CUtensorMap& tmP, const CUtensorMap& tmQ, const MxParams& p, int batch,
                               cudaStream_t st);
+// 2-SM launch: p.tiles holds (I2, J) pairs (256-row block, 128-column block), p.n_tiles = 2 x pairs;
+// tmQ must be a 64-row-box map of the Q planes
+cudaError_t launch_mx2_product(const CUtensorMap& tmP, const CUtensorMap& tmQ64, const MxParams& p, int batch,
+                               cudaStream_t st);
 
 // Host-side launchers (ns_fp64.cu).
 cudaError_t launch_init(const double* H, long long ldh, long long h_stride, double* X, const JobParams* jobs,
