@@ -108,7 +108,11 @@ Layout make_layout(int64_t d, int64_t batch, bool mixed = false, bool ozaki = fa
 // triangle (J2*64 + 63 >= I*128), L2-grouped like make_tiles; dense: all.
 std::vector<int2> make_tiles_oz(int n, bool sym) {
   std::vector<int2> v;
-  const int G = 12;
+  static const int G = [] {
+    const char* e = getenv("NS_TILE_GROUP_OZ");   // experiment knob (super-block edge in 128-row blocks)
+    const int g = e ? atoi(e) : 0;
+    return g > 0 ? g : 12;
+  }();
   for (int SI = 0; SI < n; SI += G)
     for (int SJ = sym ? 2 * SI : 0; SJ < 2 * n; SJ += 2 * G)
       for (int I = SI; I < std::min(SI + G, n); ++I)

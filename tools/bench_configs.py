@@ -125,7 +125,7 @@ def cfg3(mode="tol", prec=nsr.NS_PREC_FP64, reps=3, polish=0):
     torch.cuda.empty_cache()
 
 
-def cfg4(sharded=True):
+def cfg4(sharded=True, prec=nsr.NS_PREC_FP64):
     p = workloads.cfg4_sharded(form=False)
     H = workloads.householder_form_fast(p.Vh, p.lam, device=DEV)
     R = torch.empty_like(H)
@@ -135,8 +135,9 @@ def cfg4(sharded=True):
         ws = nsr.alloc_workspace(nsr.ns_workspace_bytes_sharded(p.d, 1), DEV)
         fn = lambda: nsr.ns_reflector_sharded(comm, H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode, R=R, ws=ws)  # noqa: E731
     else:
-        ws = nsr.alloc_workspace(nsr.ns_workspace_bytes(p.d), DEV)
-        fn = lambda: nsr.ns_reflector(H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode, R=R, ws=ws)  # noqa: E731
+        ws = nsr.alloc_workspace(nsr.ns_workspace_bytes(p.d, prec), DEV)
+        fn = lambda: nsr.ns_reflector(H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode, R=R, ws=ws,  # noqa: E731
+                                      prec=prec)
     (R, res), ms, _ = timed(fn, 1, 0)
     pred = scalar.predict_run((p.lam - p.s) / p.alpha, 100, 1e-10, True)[0]
     cols = np.array([0, 4095, 4096, 30000, 49151])
@@ -146,7 +147,8 @@ def cfg4(sharded=True):
     probe = torch.randn(p.d, dtype=torch.float64, device=DEV)
     inv = float(torch.linalg.vector_norm(R @ (R @ probe) - probe) / torch.linalg.vector_norm(probe))
     tf = (2 * res["steps"] + 1) * float(p.d) ** 3 / (ms * 1e-3) / 1e12
-    emit({"config": "cfg4", "path": "sharded P=1" if sharded else "single", "d": p.d, "time_to_R_s": ms / 1e3,
+    emit({"config": "cfg4", "path": ("sharded P=1" if sharded else "single") + (" ozaki" if prec == 3 else ""),
+          "d": p.d, "time_to_R_s": ms / 1e3,
           "steps": res["steps"], "predicted_steps": pred, "cert": res["cert"], "flags": res["flags"], "tflops": tf,
           "frac_fp64_peak": tf / PEAK, "err_vs_closed_form_cols": err, "probe_R2v_minus_v": inv,
           "trace_residual": abs(res["trace"] - (p.d - 2 * p.k)), "launches": res["launches"]})
@@ -203,6 +205,8 @@ def main():
             cfg4(True)
         elif w == "cfg4single":
             cfg4(False)
+        elif w == "cfg4ozaki":
+            cfg4(False, nsr.NS_PREC_FP64_OZAKI)
         elif w == "kscan":
             kscan()
 
