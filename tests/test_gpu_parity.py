@@ -5,6 +5,7 @@ count and index certificate (outside the +-1% tie band of reading C9), identical
 Kernel-level tests compare the symmetric product against a plain float64 matmul.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -639,3 +640,23 @@ def test_cfg2_seed1_golden(nsr, golden_dir):
     Rc = R[:, torch.as_tensor(cols["cols"], device=_dev())].cpu().numpy()
     assert np.sqrt(np.mean(np.sum((Rc - cols["R_ns"]) ** 2, axis=0))) <= TOL_R
     assert np.sqrt(np.mean(np.sum((Rc - cols["R_eig"]) ** 2, axis=0))) <= TOL_R
+
+
+# ------------------------------------------------------------------ kernel-selection alternatives
+@pytest.mark.parametrize("env", [{"NS_MX2": "0"}, {"NS_TILE64": "0"}, {"NS_TILE64": "1"}])
+def test_alternative_kernels(nsr, env):
+    """The one-SM split-precision kernel (NS_MX2=0) and the forced 128- / 64-tile FP64 kernels give the
+    same answers as the defaults (the knobs are read once per process: run in a subprocess)."""
+    import json
+    import subprocess
+    import sys
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "_alt_kernels_check.py")],
+                       capture_output=True, text=True, env=e, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    for key, v in out.items():
+        if key.startswith("mixed"):
+            assert 1e-12 <= v <= 2e-5, (key, v)
+        else:
+            assert v[0] <= TOL_R and v[1], (key, v)
