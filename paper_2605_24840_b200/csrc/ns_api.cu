@@ -52,7 +52,7 @@ struct Layout {
   size_t off_xa = 0, off_xb = 0, off_y = 0, off_res = 0, off_tr = 0, off_tiles = 0, off_jobs = 0,
          off_state = 0, off_active = 0, off_px = 0, off_py = 0, off_full = 0, off_pxb = 0, off_ahat = 0,
          off_r = 0, off_p = 0, off_cgpart = 0, off_cgsc = 0, off_ozx = 0, off_ozy = 0, off_oex = 0, off_oey = 0,
-         off_ores = 0, off_otr = 0, off_otiles = 0, total = 0;
+         off_ores = 0, off_otr = 0, off_otiles = 0, off_ptiles = 0, off_pfull = 0, total = 0;
 };
 
 Layout make_layout(int64_t d, int64_t batch, bool mixed = false, bool ozaki = false, bool tf32 = false) {
@@ -99,6 +99,8 @@ Layout make_layout(int64_t d, int64_t batch, bool mixed = false, bool ozaki = fa
     const size_t npart = std::max<size_t>((size_t)nb * (nb + 1) / 2, (size_t)kEwBlocks);
     L.off_cgpart = o; o = align256(o + sizeof(double) * npart);
     L.off_cgsc = o; o = align256(o + sizeof(CgScalars));
+    L.off_ptiles = o; o = align256(o + sizeof(int2) * (size_t)L.n * L.n);   // 2-SM pair list, upper
+    L.off_pfull = o; o = align256(o + sizeof(int2) * (size_t)L.n * L.n);    // 2-SM pair list, dense
   }
   L.total = o;
   return L;
@@ -589,8 +591,23 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
   NS_CUDA(cudaMemcpyAsync(tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
   NS_CUDA(cudaMemcpyAsync(full, tf.data(), tf.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
   NS_CUDA(cudaMemcpyAsync(djobs, &jp, sizeof(JobParams), cudaMemcpyHostToDevice, st));
+  // split-precision products: 2-SM kernel on 256 x 128 pair tiles (BF16x3 default: 2.08 vs 2.10 s at cfg3)
+  // or the one-SM kernel (TF32x3: 2.92 s vs 3.01 s with the pair kernel)
+  const bool mx2 = use_mx2() && !tf32;
+  int2* ptiles = reinterpret_cast<int2*>(ws + L.off_ptiles);
+  int2* pfull = reinterpret_cast<int2*>(ws + L.off_pfull);
+  const std::vector<int2> ps = mx2 ? make_tiles_pairs(L.n, true) : std::vector<int2>();
+  const std::vector<int2> pf = mx2 ? make_tiles_pairs(L.n, false) : std::vector<int2>();
+  if (mx2) {
+    NS_CUDA(cudaMemcpyAsync(ptiles, ps.data(), ps.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+    NS_CUDA(cudaMemcpyAsync(pfull, pf.data(), pf.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+  }
+  const int2* mx_sym = mx2 ? ptiles : tiles;
+  const int2* mx_full = mx2 ? pfull : full;
+  const int mx_nsym = mx2 ? 2 * (int)ps.size() : L.n_tiles;     // CTAs (= residual partials) per product
+  const int mx_nfull = mx2 ? 2 * (int)pf.size() : L.n * L.n;
 
-  CUtensorMap tmA, tmB, tmY, tmAh, tmPXa, tmPXb, tmPY;
+  CUtensorMap tmA, tmB, tmY, tmAh, tmPXa, tmPXb, tmPY, tqPXa, tqPXb, tqPY;   // tq*: Q-operand maps
   ns_status_t s;
   if ((s = encode_map(&tmA, Xa, L.d_pad, 1)) != NS_OK) return s;
   if ((s = encode_map(&tmB, Xb, L.d_pad, 1)) != NS_OK) return s;
@@ -599,6 +616,13 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
   if ((s = encode_map_bf16(&tmPXa, PXa, L.d_pad, 2, tf32)) != NS_OK) return s;
   if ((s = encode_map_bf16(&tmPXb, PXb, L.d_pad, 2, tf32)) != NS_OK) return s;
   if ((s = encode_map_bf16(&tmPY, PY, L.d_pad, 2, tf32)) != NS_OK) return s;
+  const int qrows = mx2 ? 64 : kTile;
+  if ((s = encode_map_bf16(&tqPXa, PXa, L.d_pad, 2, tf32, qrows)) != NS_OK) return s;
+  if ((s = encode_map_bf16(&tqPXb, PXb, L.d_pad, 2, tf32, qrows)) != NS_OK) return s;
+  if ((s = encode_map_bf16(&tqPY, PY, L.d_pad, 2, tf32, qrows)) != NS_OK) return s;
+  auto mx_product = [&](const CUtensorMap& tP, const CUtensorMap& tQ, const MxParams& mp) {
+    return mx2 ? launch_mx2_product(tP, tQ, mp, 1, st) : launch_mx_product(tP, tQ, mp, 1, st);
+  };
 
   int nl = 0;
   NS_CUDA(launch_zero_state(state, 1, n_active, st));
@@ -626,14 +650,15 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
     double* Xc = odd ? Xb : Xa;
     double* Xn = odd ? Xa : Xb;
     const CUtensorMap& tPc = odd ? tmPXb : tmPXa;
+    const CUtensorMap& tQc = odd ? tqPXb : tqPXa;
     void* PXn = odd ? PXa : PXb;
-    MxParams sq{tiles, L.n_tiles, mx_nkb, L.d, L.d_pad, js, Y, nullptr, PY, res, state, 0, tf32 ? 1 : 0};
-    NS_CUDA(launch_mx_product(tPc, tPc, sq, 1, st));
-    NS_CUDA(launch_decide(state, djobs, res, L.n_tiles, trp, L.n, lp_low, 1, n_active, st));
+    MxParams sq{mx_sym, mx_nsym, mx_nkb, L.d, L.d_pad, js, Y, nullptr, PY, res, state, 0, tf32 ? 1 : 0};
+    NS_CUDA(mx_product(tPc, tQc, sq));
+    NS_CUDA(launch_decide(state, djobs, res, mx_nsym, trp, L.n, lp_low, 1, n_active, st));
     nl += 2;
     if (j < max_steps) {
-      MxParams up{tiles, L.n_tiles, mx_nkb, L.d, L.d_pad, js, Xn, Xc, PXn, trp, state, 1, tf32 ? 1 : 0};
-      NS_CUDA(launch_mx_product(tPc, tmPY, up, 1, st));
+      MxParams up{mx_sym, mx_nsym, mx_nkb, L.d, L.d_pad, js, Xn, Xc, PXn, trp, state, 1, tf32 ? 1 : 0};
+      NS_CUDA(mx_product(tPc, tqPY, up));
       nl += 1;
     }
     NS_CUDA(cudaMemcpyAsync(&rg.slots[j % 16], n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -699,8 +724,8 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
       nl += 4;
       for (int it = 0; it < opt.cg_iters; ++it) {
         // W = |A| P (BF16x3 tcgen05, every tile) -> Xo
-        MxParams pw{full, L.n * L.n, mx_nkb, L.d, L.d_pad, 0, Xo, nullptr, nullptr, nullptr, nullptr, 2, tf32 ? 1 : 0};
-        NS_CUDA(launch_mx_product(tmPY, tmPXa, pw, 1, st));
+        MxParams pw{mx_full, mx_nfull, mx_nkb, L.d, L.d_pad, 0, Xo, nullptr, nullptr, nullptr, nullptr, 2, tf32 ? 1 : 0};
+        NS_CUDA(mx_product(tmPY, tqPXa, pw));
         NS_CUDA(launch_cg_pw(Pc, Xo, cgpart, L.d_pad, st));
         NS_CUDA(launch_cg_scalar(cgsc, cgpart, kEwBlocks, 1, st));
         NS_CUDA(launch_cg_update(E, Rc, Pc, Xo, cgsc, cgpart, L.d_pad, st, &np));
@@ -1178,7 +1203,7 @@ ns_status_t ns_symm_product(const double* A, const double* B, double* C, int64_t
     NS_CUDA(launch_split_planes(Pa, planesA, L.d_pad, 1, cs, tf32));
     NS_CUDA(launch_split_planes(Pb, planesB, L.d_pad, 1, cs, tf32));
     CUtensorMap tA, tB;
-    const bool mx2 = use_mx2();
+    const bool mx2 = use_mx2() && !tf32;
     if ((s = encode_map_bf16(&tA, planesA, L.d_pad, 2, tf32)) != NS_OK) return s;
     if ((s = encode_map_bf16(&tB, planesB, L.d_pad, 2, tf32, mx2 ? 64 : kTile)) != NS_OK) return s;
     int nt = (int)tl.size();
