@@ -159,10 +159,10 @@ __global__ void __launch_bounds__(kOzThreads, 1)
           mbar_arrive_expect_tx(&full[s], kOzStageBytes);
 #pragma unroll
           for (int q = 0; q < kOzSlices; ++q)
-            tma_load_3d(st + q * kOzSlabA, &tmA, kb * 64, tile.x * kTile, job * kOzSlices + q, &full[s]);
+            tma_load_3d(st + q * kOzSlabA, &tmA, (p.kb0 + kb) * 64, tile.x * kTile, job * kOzSlices + q, &full[s]);
 #pragma unroll
           for (int q = 0; q < kOzSlices; ++q)
-            tma_load_3d(st + kOzSlices * kOzSlabA + q * kOzSlabB, &tmB, kb * 64, tile.y * 64, job * kOzSlices + q,
+            tma_load_3d(st + kOzSlices * kOzSlabA + q * kOzSlabB, &tmB, (p.kb0 + kb) * 64, tile.y * 64, job * kOzSlices + q,
                         &full[s]);
         }
       }
@@ -259,10 +259,26 @@ __global__ void __launch_bounds__(kOzThreads, 1)
       // per thread (= row), mirrors go straight out (lanes = consecutive rows of the mirror: coalesced),
       // and the row-major part is transposed through the staging block so every store instruction
       // writes two full 128-byte row segments.
+      // K segments (d > 16384): segments before the last store raw partial sums of the owned elements in
+      // C; the last adds them back and runs the mode epilogue (launches are stream-ordered)
+      const bool fin = (p.pm == 0 || p.pm == 3);
+      if (p.pm >= 2) {
+#pragma unroll
+        for (int cb = 0; cb < 2; ++cb) {
+          double pbuf[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const int gj = j0 + 16 * cb + u;
+            pbuf[u] = (MODE == 2 || gj >= gi) ? C[(long long)gi * ld + gj] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 16; ++u) acc[16 * cb + u] += pbuf[u];
+        }
+      }
 #pragma unroll
       for (int cb = 0; cb < 2; ++cb) {
         double xbuf[16];
-        if (MODE == 1) {
+        if (MODE == 1 && fin) {
 #pragma unroll
           for (int u = 0; u < 16; ++u) {
             const int gj = j0 + 16 * cb + u;
@@ -273,7 +289,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
         for (int u = 0; u < 16; ++u) {
           const int c = 16 * cb + u, gj = j0 + c;
           double v = acc[c];
-          if (MODE != 2 && gj >= gi) {          // element owned by this tile (written with its mirror)
+          if (MODE != 2 && gj >= gi && fin) {   // element owned by this tile (written with its mirror)
             if (MODE == 1) {
               v = fma(p.cb, v, p.ca * xbuf[u]);
               if (gi == gj && gi < p.d) part += v;
@@ -297,7 +313,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
         }
         __syncwarp();
       }
-      if (MODE != 2) {
+      if (MODE != 2 && fin) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
         if (lane == 0) red[ew] = part;
@@ -339,6 +355,21 @@ cudaError_t launch_ozaki_product(const CUtensorMap& tmA, const CUtensorMap& tmB,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     if (n_sm <= 0) n_sm = 148;
+  }
+  if (p.pm == 0 && p.nkb > kOzSegKb) {
+    // K segments of kOzSegKb k-blocks, one launch each: every segment streams a K range that the
+    // concurrently working CTAs share in L2 (whole-K tiles at d = 49152 drifted apart: 40% L2 hits,
+    // HBM-bound); partial sums go through C (stream-ordered launches)
+    const int nseg = (p.nkb + kOzSegKb - 1) / kOzSegKb;
+    for (int sgi = 0; sgi < nseg; ++sgi) {
+      OzParams q = p;
+      q.kb0 = sgi * kOzSegKb;
+      q.nkb = std::min(kOzSegKb, p.nkb - q.kb0);
+      q.pm = (sgi == 0) ? 1 : (sgi == nseg - 1 ? 3 : 2);
+      const cudaError_t e = launch_ozaki_product(tmA, tmB, q, batch, st);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
   }
   const int n_items = p.n_tiles * batch;
   const dim3 grid(std::min(n_items, n_sm));   // persistent: one CTA per SM

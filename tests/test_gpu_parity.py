@@ -494,7 +494,8 @@ def test_alg1_scan_matches_oracle(nsr):
 
 
 # ------------------------------------------------------------------ N4: Ozaki-split FP64 on INT8 tensor cores
-@pytest.mark.parametrize("d,mode", [(128, 0), (300, 0), (515, 1), (256, 2), (200, 2), (1024, 0), (4500, 1), (16500, 0)])
+@pytest.mark.parametrize("d,mode", [(128, 0), (300, 0), (515, 1), (256, 2), (200, 2), (1024, 0), (4500, 1), (16500, 0),
+                                    (16448, 1)])
 def test_ozaki_product_kernel(nsr, d, mode):
     """7-slice Ozaki products on tcgen05 kind::i8: FP64-class accuracy (relative to |row||col|)."""
     rng = np.random.default_rng(99 + d)
