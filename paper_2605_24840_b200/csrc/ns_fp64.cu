@@ -625,13 +625,13 @@ cudaError_t launch_trace_partials(const double* X, int d, int d_pad, int batch, 
 
 cudaError_t launch_product64(const CUtensorMap& tmP, const CUtensorMap& tmQ, const ProdParams& p, int batch,
                              cudaStream_t st) {
-  static bool attr[2] = {false, false};
+  static unsigned long long attr[2] = {0, 0};
   dim3 grid(p.n_tiles, batch);
   if (p.mode == 0) {
-    if (!attr[0]) { cudaFuncSetAttribute(ns_product64_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, k64SmemBytes); attr[0] = true; }
+    smem_attr(ns_product64_kernel<0>, k64SmemBytes, attr[0]);
     ns_product64_kernel<0><<<grid, k64Threads, k64SmemBytes, st>>>(tmP, tmQ, p);
   } else {
-    if (!attr[1]) { cudaFuncSetAttribute(ns_product64_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, k64SmemBytes); attr[1] = true; }
+    smem_attr(ns_product64_kernel<1>, k64SmemBytes, attr[1]);
     ns_product64_kernel<1><<<grid, k64Threads, k64SmemBytes, st>>>(tmP, tmQ, p);
   }
   return cudaGetLastError();
@@ -639,25 +639,16 @@ cudaError_t launch_product64(const CUtensorMap& tmP, const CUtensorMap& tmQ, con
 
 cudaError_t launch_product(const CUtensorMap& tmP, const CUtensorMap& tmQ, const ProdParams& p, int batch,
                            cudaStream_t st) {
-  static bool attr_done[3] = {false, false, false};
+  static unsigned long long attr[3] = {0, 0, 0};
   dim3 grid(p.n_tiles, batch);
   if (p.mode == 2) {
-    if (!attr_done[2]) {
-      cudaFuncSetAttribute(ns_product_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-      attr_done[2] = true;
-    }
+    smem_attr(ns_product_kernel<2>, kSmemBytes, attr[2]);
     ns_product_kernel<2><<<grid, kThreads, kSmemBytes, st>>>(tmP, tmQ, p);
   } else if (p.mode == 0) {
-    if (!attr_done[0]) {
-      cudaFuncSetAttribute(ns_product_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-      attr_done[0] = true;
-    }
+    smem_attr(ns_product_kernel<0>, kSmemBytes, attr[0]);
     ns_product_kernel<0><<<grid, kThreads, kSmemBytes, st>>>(tmP, tmQ, p);
   } else {
-    if (!attr_done[1]) {
-      cudaFuncSetAttribute(ns_product_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-      attr_done[1] = true;
-    }
+    smem_attr(ns_product_kernel<1>, kSmemBytes, attr[1]);
     ns_product_kernel<1><<<grid, kThreads, kSmemBytes, st>>>(tmP, tmQ, p);
   }
   return cudaGetLastError();

@@ -158,6 +158,17 @@ cudaError_t launch_init(const double* H, long long ldh, long long h_stride, doub
                         int d, int d_pad, int batch, cudaStream_t st);
 cudaError_t launch_trace_partials(const double* X, int d, int d_pad, int batch, double* tr_partial,
                                   cudaStream_t st, int job_stride = 0);
+// Raise a kernel's dynamic shared-memory limit once per device: `mask` is that kernel's static set of
+// devices already configured (one process may drive several GPUs; the setting is per device).
+template <typename F>
+inline void smem_attr(F* fn, int bytes, unsigned long long& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (mask & bit) return;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess) mask |= bit;
+}
+
 cudaError_t launch_product64(const CUtensorMap& tmP, const CUtensorMap& tmQ, const ProdParams& p, int batch,
                              cudaStream_t st);
 cudaError_t launch_product(const CUtensorMap& tmP, const CUtensorMap& tmQ, const ProdParams& p, int batch,

@@ -548,11 +548,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMxThreads, 1)
 template <int MODE, bool TF32>
 static cudaError_t launch_mx2_t(const CUtensorMap& tmP, const CUtensorMap& tmQ, const MxParams& p, int batch,
                                 cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(ns_mx2_product_kernel<MODE, TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMx2SmemBytes);
-    attr = true;
-  }
+  static unsigned long long attr = 0;
+  smem_attr(ns_mx2_product_kernel<MODE, TF32>, kMx2SmemBytes, attr);
   dim3 grid(p.n_tiles, batch);   // n_tiles = 2 x pairs: one cluster of 2 per pair
   ns_mx2_product_kernel<MODE, TF32><<<grid, kMxThreads, kMx2SmemBytes, st>>>(tmP, tmQ, p);
   return cudaGetLastError();
@@ -582,11 +579,8 @@ cudaError_t launch_split_planes(const double* X, void* planes, int d_pad, int ba
 template <int MODE, bool TF32>
 static cudaError_t launch_mx_t(const CUtensorMap& tmP, const CUtensorMap& tmQ, const MxParams& p, int batch,
                                cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(ns_mx_product_kernel<MODE, TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMxSmemBytes);
-    attr = true;
-  }
+  static unsigned long long attr = 0;
+  smem_attr(ns_mx_product_kernel<MODE, TF32>, kMxSmemBytes, attr);
   dim3 grid(p.n_tiles, batch);
   ns_mx_product_kernel<MODE, TF32><<<grid, kMxThreads, kMxSmemBytes, st>>>(tmP, tmQ, p);
   return cudaGetLastError();

@@ -348,7 +348,7 @@ cudaError_t launch_ozaki_slice(const double* X, int8_t* slices, int* expo, int d
 
 cudaError_t launch_ozaki_product(const CUtensorMap& tmA, const CUtensorMap& tmB, const OzParams& p, int batch,
                                  cudaStream_t st) {
-  static bool attr[3] = {false, false, false};
+  static unsigned long long attr[3] = {0, 0, 0};
   static int n_sm = 0;
   if (n_sm == 0) {
     int dev = 0;
@@ -375,15 +375,15 @@ cudaError_t launch_ozaki_product(const CUtensorMap& tmA, const CUtensorMap& tmB,
   const dim3 grid(std::min(n_items, n_sm));   // persistent: one CTA per SM
   switch (p.mode) {
     case 0:
-      if (!attr[0]) { cudaFuncSetAttribute(ns_ozaki_product_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOzSmemBytes); attr[0] = true; }
+      smem_attr(ns_ozaki_product_kernel<0>, kOzSmemBytes, attr[0]);
       ns_ozaki_product_kernel<0><<<grid, kOzThreads, kOzSmemBytes, st>>>(tmA, tmB, p, n_items);
       break;
     case 1:
-      if (!attr[1]) { cudaFuncSetAttribute(ns_ozaki_product_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOzSmemBytes); attr[1] = true; }
+      smem_attr(ns_ozaki_product_kernel<1>, kOzSmemBytes, attr[1]);
       ns_ozaki_product_kernel<1><<<grid, kOzThreads, kOzSmemBytes, st>>>(tmA, tmB, p, n_items);
       break;
     default:
-      if (!attr[2]) { cudaFuncSetAttribute(ns_ozaki_product_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOzSmemBytes); attr[2] = true; }
+      smem_attr(ns_ozaki_product_kernel<2>, kOzSmemBytes, attr[2]);
       ns_ozaki_product_kernel<2><<<grid, kOzThreads, kOzSmemBytes, st>>>(tmA, tmB, p, n_items);
       break;
   }

@@ -290,7 +290,7 @@ int small_dpad(int d) { return d <= 32 ? 32 : d <= 64 ? 64 : d <= 96 ? 96 : 0; }
 cudaError_t launch_small(const double* H, long long ldh, long long h_stride, const JobParams* jobs, JobParams job0,
                          LoopParams lp, double* R, long long ldr, long long r_stride, DevState* state, int batch,
                          cudaStream_t st) {
-  static bool attr[3] = {false, false, false};
+  static unsigned long long attr[3] = {0, 0, 0};
   const int dp = small_dpad(lp.d);
   const size_t smem = (size_t)3 * dp * (dp == 96 ? dp + 4 : dp + 8) * sizeof(double);
   switch (dp) {
@@ -298,11 +298,11 @@ cudaError_t launch_small(const double* H, long long ldh, long long h_stride, con
       ns_small_kernel<32><<<batch, small_threads<32>(), smem, st>>>(H, ldh, h_stride, jobs, job0, lp, R, ldr, r_stride, state);
       break;
     case 64:
-      if (!attr[1]) { cudaFuncSetAttribute(ns_small_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr[1] = true; }
+      smem_attr(ns_small_kernel<64>, (int)smem, attr[1]);
       ns_small_kernel<64><<<batch, small_threads<64>(), smem, st>>>(H, ldh, h_stride, jobs, job0, lp, R, ldr, r_stride, state);
       break;
     case 96:
-      if (!attr[2]) { cudaFuncSetAttribute(ns_small_kernel<96>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr[2] = true; }
+      smem_attr(ns_small_kernel<96>, (int)smem, attr[2]);
       ns_small_kernel<96><<<batch, small_threads<96>(), smem, st>>>(H, ldh, h_stride, jobs, job0, lp, R, ldr, r_stride, state);
       break;
     default:
