@@ -261,13 +261,31 @@ ns_status_t ns_alg1_rotated_quartic(const double* Q, int64_t d, int32_t nruns, c
  * ns_reflector_sharded   same arguments and result as ns_reflector (FP64 only); H (full, upper
  *                        triangle read) and R (full) are device buffers on every rank; all ranks
  *                        must call it with identical scalars.  The workspace must hold
- *                        ns_workspace_bytes_sharded(d, nranks) bytes.
+ *                        ns_workspace_bytes_sharded(d, nranks) bytes.  Exchange: every rank's
+ *                        workspace is mapped into every process (CUDA IPC, collective, cached per
+ *                        workspace) and the product kernels store their tiles straight into all
+ *                        ranks' buffers (one small all-reduce per product as the barrier); if any
+ *                        rank cannot map (e.g. VMM memory) or NS_SHARD_P2P=0, tiles are exchanged with
+ *                        chunked NCCL all-gathers overlapped with the contraction.
  */
 typedef struct ns_comm ns_comm_t;
 ns_status_t ns_comm_get_unique_id(uint8_t id[128]);
 ns_status_t ns_comm_init(int rank, int nranks, const uint8_t id[128], ns_comm_t** comm);
 ns_status_t ns_comm_destroy(ns_comm_t* comm);
 ns_status_t ns_shard_plan(int64_t d, int nranks, int rank, int32_t* tiles_ij, int32_t cap, int32_t* n_out);
+
+/*
+ * ns_symm_product_shard — the sharded path's peer-memory exchange primitive at kernel level (tests):
+ * rank `rank` of `nranks` computes its share of the upper 128x128 tiles of C = A B (mode 0) or of
+ * C = 1.5 A - 0.5 A B (mode 1) and its epilogue stores every tile and its mirror into ALL n_dst
+ * destination matrices C_list[0..n_dst-1] (device pointers, d x d, ld = d; in ns_reflector_sharded
+ * these are the ranks' buffers mapped through CUDA IPC over NVLink).  Calling it for every rank of a
+ * plan fills every destination with the full, bitwise-symmetric product.  d must be a multiple of 128;
+ * A, B symmetric, ld = d.  C_list is a HOST array.  Workspace: ns_workspace_bytes(d, NS_PREC_FP64).
+ */
+ns_status_t ns_symm_product_shard(const double* A, const double* B, double* const* C_list, int32_t n_dst, int64_t d,
+                                  int32_t mode, int32_t rank, int32_t nranks, void* ws, size_t ws_bytes,
+                                  void* stream);
 /* Exchange chunking of the sharded path: each rank's tile list is cut into n_chunks chunks of
  * chunk_slots slots (padded to the largest rank); chunk c of rank q carries the rank's local tiles
  * c*chunk_slots .. c*chunk_slots + chunk_slots - 1, i.e. global upper tiles (c*chunk_slots + s)*P + q. */

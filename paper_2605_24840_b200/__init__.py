@@ -26,6 +26,7 @@ EXPORTED_SYMBOLS = (
     "ns_reflector_ex", "ns_comm_get_unique_id", "ns_comm_init", "ns_comm_destroy", "ns_shard_plan",
     "ns_workspace_bytes_sharded", "ns_reflector_sharded", "ns_shard_chunks", "ns_workspace_bytes_setup", "ns_scale_bound",
     "ns_shift_certificate", "ns_workspace_bytes_alg1", "ns_alg1_rotated_quartic", "ns_debug_mx_trace",
+    "ns_symm_product_shard",
 )
 
 
@@ -99,6 +100,8 @@ def load_library(path=LIB_PATH):
                                          ctypes.c_int, c_vp, c_i64, c_vp, c_sz, c_vp, ctypes.POINTER(NsResult)]
     lib.ns_symm_product.restype = ctypes.c_int
     lib.ns_symm_product.argtypes = [c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, ctypes.c_int, c_vp, c_sz, c_vp]
+    lib.ns_symm_product_shard.restype = ctypes.c_int
+    lib.ns_symm_product_shard.argtypes = [c_vp, c_vp, c_vp, c_i32, c_i64, c_i32, c_i32, c_i32, c_vp, c_sz, c_vp]
     lib.ns_build_info.restype = ctypes.c_char_p
     lib.ns_status_string.restype = ctypes.c_char_p
     lib.ns_status_string.argtypes = [ctypes.c_int]
@@ -281,6 +284,24 @@ def ns_symm_product(A, B, mode=0, C=None, ws=None, stream=None, prec=NS_PREC_FP6
     _check(st)
     return C
 
+
+
+def ns_symm_product_shard(A, B, C_list, rank, nranks, mode=0, ws=None, stream=None):
+    """Peer-memory exchange primitive (C-ABI ns_symm_product_shard): rank `rank`'s tiles of the
+    symmetric product, each stored into every matrix of C_list (CUDA float64, d x d, d % 128 == 0)."""
+    lib = load_library()
+    _require_cuda_f64(A, "A")
+    _require_cuda_f64(B, "B")
+    d = A.shape[0]
+    for C in C_list:
+        _require_cuda_f64(C, "C")
+    if ws is None:
+        ws = alloc_workspace(lib.ns_workspace_bytes(d, NS_PREC_FP64), A.device)
+    arr = (ctypes.c_void_p * len(C_list))(*[C.data_ptr() for C in C_list])
+    st = lib.ns_symm_product_shard(ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()), arr, len(C_list), d,
+                                   int(mode), int(rank), int(nranks), ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                                   _stream_ptr(stream))
+    _check(st)
 
 def ns_profile_enable(on=True):
     load_library().ns_profile_enable(1 if on else 0)

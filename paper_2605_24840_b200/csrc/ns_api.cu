@@ -814,7 +814,7 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
 struct ShardLayout {
   Layout base;
   int nranks = 1, rank = 0, n_my = 0, n_my_max = 0, n_chunks = 1, cs = 0;
-  size_t off_my = 0, off_send = 0, off_recv = 0, off_rsend = 0, off_rrecv = 0, total = 0;
+  size_t off_my = 0, off_send = 0, off_recv = 0, off_rsend = 0, off_rrecv = 0, off_ptrs = 0, off_ipc = 0, total = 0;
 };
 
 ShardLayout make_shard_layout(int64_t d, int nranks, int rank) {
@@ -834,6 +834,8 @@ ShardLayout make_shard_layout(int64_t d, int nranks, int rank) {
   S.off_recv = o; o = align256(o + tile_bytes * (size_t)S.n_chunks * S.cs * (size_t)nranks);
   S.off_rsend = o; o = align256(o + sizeof(double));
   S.off_rrecv = o; o = align256(o + sizeof(double) * (size_t)nranks);
+  S.off_ptrs = o; o = align256(o + sizeof(double*) * 6 * (size_t)nranks);   // peer bases: Y, Xa, Xb, res, tr0, tr1
+  S.off_ipc = o; o = align256(o + 128 * ((size_t)nranks + 1));              // IPC handle exchange
   S.total = o;
   return S;
 }
@@ -854,7 +856,106 @@ struct CommCtx {
   ncclComm_t comm;
   cudaStream_t cst;                    // communication stream (pack / all-gather / unpack)
   std::vector<cudaEvent_t> ev;         // chunk-ready events (compute -> comm), + 1 "exchange done" (comm -> compute)
+  // peer-memory exchange: every rank's workspace mapped into this process (CUDA IPC over NVLink)
+  const void* peer_ws_key = nullptr;   // workspace the mappings below belong to
+  std::vector<uint8_t*> peer_ws;       // [rank] -> that rank's workspace (own entry: local pointer)
+  std::vector<void*> opened;           // IPC mappings to close
+  bool p2p = false;
 };
+
+typedef CUresult (*AddrRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+AddrRangeFn get_addr_range() {
+  static AddrRangeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<AddrRangeFn>(p);
+  }
+  return fn;
+}
+
+void close_peers(CommCtx& cc) {
+  for (void* p : cc.opened) cudaIpcCloseMemHandle(p);
+  cc.opened.clear();
+  cc.peer_ws.clear();
+  cc.peer_ws_key = nullptr;
+  cc.p2p = false;
+}
+
+// Map every rank's workspace into this process (collective).  The exchange runs through NCCL on the
+// device; all ranks take the peer-memory path only if every rank could export and open the mappings
+// (torch's caching allocator memory can be IPC-exported; VMM/expandable segments cannot), else the
+// NCCL all-gather path is used everywhere.  NS_SHARD_P2P=0 forces the NCCL path.
+ns_status_t setup_peers(CommCtx& cc, int rank, int nranks, uint8_t* ws, uint8_t* scratch, cudaStream_t st) {
+  if (cc.peer_ws_key == ws) return NS_OK;
+  close_peers(cc);
+  static const bool allow = [] {
+    const char* e = getenv("NS_SHARD_P2P");
+    return !(e && e[0] == '0');
+  }();
+  cc.peer_ws.assign(nranks, nullptr);
+  cc.peer_ws[rank] = ws;
+  if (nranks == 1) {
+    cc.p2p = allow;
+    cc.peer_ws_key = ws;
+    return NS_OK;
+  }
+  struct Rec {
+    cudaIpcMemHandle_t h;
+    unsigned long long off;
+    int ok;
+    int pad[13];
+  };
+  static_assert(sizeof(Rec) == 128, "IPC record size");
+  Rec mine{};
+  mine.ok = allow ? 1 : 0;
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  AddrRangeFn rng = get_addr_range();
+  if (mine.ok && (!rng || rng(&base, &size, reinterpret_cast<CUdeviceptr>(ws)) != CUDA_SUCCESS)) mine.ok = 0;
+  if (mine.ok && cudaIpcGetMemHandle(&mine.h, reinterpret_cast<void*>(base)) != cudaSuccess) {
+    cudaGetLastError();
+    mine.ok = 0;
+  }
+  mine.off = mine.ok ? (unsigned long long)(reinterpret_cast<uintptr_t>(ws) - (uintptr_t)base) : 0ull;
+  NS_CUDA(cudaMemcpyAsync(scratch, &mine, sizeof(Rec), cudaMemcpyHostToDevice, st));
+  NS_NCCL(ncclAllGather(scratch, scratch + sizeof(Rec), sizeof(Rec), ncclUint8, cc.comm, st));
+  std::vector<Rec> all(nranks);
+  NS_CUDA(cudaMemcpyAsync(all.data(), scratch + sizeof(Rec), sizeof(Rec) * nranks, cudaMemcpyDeviceToHost, st));
+  NS_CUDA(cudaStreamSynchronize(st));
+  int ok = 1;
+  for (const Rec& r : all) ok &= r.ok;
+  if (ok) {
+    for (int r = 0; r < nranks && ok; ++r) {
+      if (r == rank) continue;
+      void* p = nullptr;
+      if (cudaIpcOpenMemHandle(&p, all[r].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        ok = 0;
+        break;
+      }
+      cc.opened.push_back(p);
+      cc.peer_ws[r] = static_cast<uint8_t*>(p) + all[r].off;
+    }
+  }
+  // agree on the outcome (an open can fail on one rank only)
+  double* flag = reinterpret_cast<double*>(scratch);
+  const double mine_ok = ok ? 1.0 : 0.0;
+  NS_CUDA(cudaMemcpyAsync(flag, &mine_ok, sizeof(double), cudaMemcpyHostToDevice, st));
+  NS_NCCL(ncclAllReduce(flag, flag, 1, ncclDouble, ncclMin, cc.comm, st));
+  double all_ok = 0.0;
+  NS_CUDA(cudaMemcpyAsync(&all_ok, flag, sizeof(double), cudaMemcpyDeviceToHost, st));
+  NS_CUDA(cudaStreamSynchronize(st));
+  cc.p2p = (all_ok == 1.0);
+  if (!cc.p2p) {
+    for (void* p : cc.opened) cudaIpcCloseMemHandle(p);
+    cc.opened.clear();
+  }
+  cc.peer_ws_key = ws;
+  return NS_OK;
+}
 
 ns_status_t run_sharded(CommCtx& cc, const ShardLayout& SL, uint8_t* ws, const double* H, long long ldh,
                         const JobParams& jp, int32_t max_steps, double tol, ns_tolmode_t tm, double* R, long long ldr,
@@ -925,6 +1026,46 @@ ns_status_t run_sharded(CommCtx& cc, const ShardLayout& SL, uint8_t* ws, const d
     return NS_OK;
   };
 
+  // Peer-memory exchange (default): the product kernel's epilogue stores each tile (+ mirror, + its
+  // residual / trace partial) straight into every rank's buffers through the IPC mappings, so the
+  // exchange rides on the contraction tile by tile; one tiny NCCL all-reduce per product is the
+  // cross-rank barrier (all peers' stores done) before anything reads the full matrix.
+  ns_status_t ps = setup_peers(cc, SL.rank, SL.nranks, ws, ws + SL.off_ipc, st);
+  if (ps != NS_OK) return ps;
+  const bool p2p = cc.p2p;
+  // [6][P]: Y, Xa, Xb, res, tr (even steps), tr (odd steps).  The trace partials alternate by step
+  // parity: a fast rank's update j (writing tr X_{j+1}) may overlap a slow rank's decide j (reading tr X_j).
+  double** dptr = reinterpret_cast<double**>(ws + SL.off_ptrs);
+  if (p2p) {
+    std::vector<double*> h(6 * (size_t)SL.nranks);
+    for (int r = 0; r < SL.nranks; ++r) {
+      uint8_t* w = cc.peer_ws[r];
+      h[0 * SL.nranks + r] = reinterpret_cast<double*>(w + L.off_y);
+      h[1 * SL.nranks + r] = reinterpret_cast<double*>(w + L.off_xa);
+      h[2 * SL.nranks + r] = reinterpret_cast<double*>(w + L.off_xb);
+      h[3 * SL.nranks + r] = reinterpret_cast<double*>(w + L.off_res);
+      h[4 * SL.nranks + r] = reinterpret_cast<double*>(w + L.off_tr);
+      h[5 * SL.nranks + r] = reinterpret_cast<double*>(w + L.off_tr) + L.n;
+    }
+    NS_CUDA(cudaMemcpyAsync(dptr, h.data(), h.size() * sizeof(double*), cudaMemcpyHostToDevice, st));
+  }
+  auto product_p2p = [&](const CUtensorMap& tP, const CUtensorMap& tQ, double* C, int which_c, const double* Xold,
+                         double* partial, int which_part, int mode) -> ns_status_t {
+    if (n_my > 0) {
+      ProdParams pp{my, n_my, L.d_pad / kBK, L.d, L.d_pad, (long long)L.d_pad * L.d_pad, C, Xold, partial, state, mode};
+      pp.dst = dptr + (size_t)which_c * SL.nranks;
+      pp.dst_part = dptr + (size_t)which_part * SL.nranks;
+      pp.n_dst = SL.nranks;
+      pp.gt_off = SL.rank;
+      pp.gt_stride = SL.nranks;
+      pp.n_tiles_total = L.n_tiles;
+      NS_CUDA(launch_product(tP, tQ, pp, 1, st));
+      nl += 1;
+    }
+    if (SL.nranks > 1) NS_NCCL(ncclAllReduce(rsend, rsend, 1, ncclDouble, ncclSum, comm, st));   // barrier
+    return NS_OK;
+  };
+
   NS_CUDA(launch_zero_state(state, 1, n_active, st));
   NS_CUDA(launch_init(H, ldh, 0, Xa, djobs, L.d, L.d_pad, 1, st));
   NS_CUDA(launch_trace_partials(Xa, L.d, L.d_pad, 1, trp, st));
@@ -941,19 +1082,32 @@ ns_status_t run_sharded(CommCtx& cc, const ShardLayout& SL, uint8_t* ws, const d
     double* Xc = odd ? Xb : Xa;
     double* Xn = odd ? Xa : Xb;
     const CUtensorMap& tmC = odd ? tmB : tmA;
-    // own Y tiles (chunked, exchange overlapped) + residual sum of the rank's tiles
-    ns_status_t e1 = product_and_exchange(tmC, tmC, Y, nullptr, res, 0);
-    if (e1 != NS_OK) return e1;
-    NS_CUDA(launch_shard_sum(res, n_my, rsend, st));
-    NS_NCCL(ncclAllGather(rsend, rrecv, 1, ncclDouble, comm, st));
-    // decide (identical on all ranks)
-    NS_CUDA(launch_decide(state, djobs, res, 0, trp, L.n, lp, 1, n_active, st, rrecv, SL.nranks));
-    nl += 2;
-    if (j < max_steps) {
-      ns_status_t e2 = product_and_exchange(tmC, tmY, Xn, Xc, trp, 1);
-      if (e2 != NS_OK) return e2;
-      NS_CUDA(launch_trace_partials(Xn, L.d, L.d_pad, 1, trp, st));
+    if (p2p) {
+      // Y tiles of this rank into every rank's Y (+ residual partials into every rank's res, global slots)
+      ns_status_t e1 = product_p2p(tmC, tmC, Y, 0, nullptr, res, 3, 0);
+      if (e1 != NS_OK) return e1;
+      NS_CUDA(launch_decide(state, djobs, res, L.n_tiles, trp + (odd ? L.n : 0), L.n, lp, 1, n_active, st));
       nl += 1;
+      if (j < max_steps) {
+        // X_{j+1} tiles into every rank's X_{j+1}; the diagonal tiles' trace partials likewise (other parity)
+        ns_status_t e2 = product_p2p(tmC, tmY, Xn, odd ? 1 : 2, Xc, trp + (odd ? 0 : L.n), odd ? 4 : 5, 1);
+        if (e2 != NS_OK) return e2;
+      }
+    } else {
+      // own Y tiles (chunked, exchange overlapped) + residual sum of the rank's tiles
+      ns_status_t e1 = product_and_exchange(tmC, tmC, Y, nullptr, res, 0);
+      if (e1 != NS_OK) return e1;
+      NS_CUDA(launch_shard_sum(res, n_my, rsend, st));
+      NS_NCCL(ncclAllGather(rsend, rrecv, 1, ncclDouble, comm, st));
+      // decide (identical on all ranks)
+      NS_CUDA(launch_decide(state, djobs, res, 0, trp, L.n, lp, 1, n_active, st, rrecv, SL.nranks));
+      nl += 2;
+      if (j < max_steps) {
+        ns_status_t e2 = product_and_exchange(tmC, tmY, Xn, Xc, trp, 1);
+        if (e2 != NS_OK) return e2;
+        NS_CUDA(launch_trace_partials(Xn, L.d, L.d_pad, 1, trp, st));
+        nl += 1;
+      }
     }
     NS_CUDA(cudaMemcpyAsync(&rg.slots[j % 16], n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
     NS_CUDA(cudaEventRecord(rg.ev[j % 16], st));
@@ -1265,11 +1419,55 @@ ns_status_t ns_comm_init(int rank, int nranks, const uint8_t id[128], ns_comm_t*
 ns_status_t ns_comm_destroy(ns_comm_t* comm) {
   g_last_error.clear();
   if (!comm) return NS_OK;
+  close_peers(comm->ctx);
   for (cudaEvent_t e : comm->ctx.ev) cudaEventDestroy(e);
   if (comm->ctx.cst) cudaStreamDestroy(comm->ctx.cst);
   ncclResult_t r = ncclCommDestroy(comm->comm);
   delete comm;
   if (r != ncclSuccess) return fail(NS_ERR_NCCL, "ncclCommDestroy failed: %s", ncclGetErrorString(r));
+  return NS_OK;
+}
+
+ns_status_t ns_symm_product_shard(const double* A, const double* B, double* const* C_list, int32_t n_dst, int64_t d,
+                                  int32_t mode, int32_t rank, int32_t nranks, void* ws, size_t ws_bytes, void* stream) {
+  g_last_error.clear();
+  if (d < kTile || d > 65536 || d % kTile != 0) return fail(NS_ERR_INVALID_ARG, "d must be a multiple of 128 in [128, 65536]");
+  if (mode < 0 || mode > 1) return fail(NS_ERR_INVALID_ARG, "mode must be 0 or 1");
+  if (nranks < 1 || rank < 0 || rank >= nranks || n_dst < 1 || n_dst > 64)
+    return fail(NS_ERR_INVALID_ARG, "bad rank / nranks / n_dst");
+  if (!A || !B || !C_list || !ws) return fail(NS_ERR_INVALID_ARG, "null pointer argument");
+  for (int q = 0; q < n_dst; ++q)
+    if (!C_list[q]) return fail(NS_ERR_INVALID_ARG, "null destination");
+  if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(NS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+  const Layout L = make_layout(d, 1, false);
+  if (ws_bytes < L.total) return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  int2* tiles = reinterpret_cast<int2*>(w + L.off_tiles);
+  double** dst = reinterpret_cast<double**>(w + L.off_full);                 // n_dst C bases, n_dst partial bases
+  double* part = reinterpret_cast<double*>(w + L.off_res);
+  const std::vector<int2> mt = shard_tiles(make_tiles(L.n), nranks, rank);
+  if (mt.empty()) return NS_OK;
+  std::vector<double*> h(2 * (size_t)n_dst);
+  for (int q = 0; q < n_dst; ++q) {
+    h[q] = C_list[q];
+    h[n_dst + q] = part;
+  }
+  NS_CUDA(cudaMemcpyAsync(tiles, mt.data(), mt.size() * sizeof(int2), cudaMemcpyHostToDevice, cs));
+  NS_CUDA(cudaMemcpyAsync(dst, h.data(), h.size() * sizeof(double*), cudaMemcpyHostToDevice, cs));
+  CUtensorMap tA, tB;
+  ns_status_t s;
+  if ((s = encode_map(&tA, A, L.d_pad, 1)) != NS_OK) return s;
+  if ((s = encode_map(&tB, B, L.d_pad, 1)) != NS_OK) return s;
+  ProdParams pp{tiles, (int)mt.size(), L.d_pad / kBK, L.d, L.d_pad, 0, C_list[0], A, part, nullptr, mode};
+  pp.dst = dst;
+  pp.dst_part = dst + n_dst;
+  pp.n_dst = n_dst;
+  pp.gt_off = rank;
+  pp.gt_stride = nranks;
+  pp.n_tiles_total = L.n_tiles;
+  NS_CUDA(launch_product(tA, tB, pp, 1, cs));
+  NS_CUDA(cudaStreamSynchronize(cs));
   return NS_OK;
 }
 

@@ -296,6 +296,31 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   if (MODE == 2) return;
+  if (p.n_dst > 0) {
+    // peer-memory exchange: the same tile (and mirror) into every other destination; S holds the final
+    // values (MODE 1 updated it in place; diagonal tiles are valid on and above the diagonal)
+    named_bar_sync(1, 32 * kConsumerWarps);
+    for (int q = 0; q < p.n_dst; ++q) {
+      double* Cq = p.dst[q] + base;
+      if (Cq == C) continue;
+      if (!diag) {
+        for (int idx = tid; idx < kTile * kTile; idx += 256) {
+          const int r = idx >> 7, c = idx & 127;
+          Cq[(long long)(I * kTile + r) * ld + J * kTile + c] = S[r * kEpiPitch + c];
+        }
+        for (int idx = tid; idx < kTile * kTile; idx += 256) {
+          const int r = idx >> 7, c = idx & 127;
+          Cq[(long long)(J * kTile + r) * ld + I * kTile + c] = S[c * kEpiPitch + r];
+        }
+      } else {
+        for (int idx = tid; idx < kTile * kTile; idx += 256) {
+          const int r = idx >> 7, c = idx & 127;
+          Cq[(long long)(I * kTile + r) * ld + I * kTile + c] = (r <= c) ? S[r * kEpiPitch + c] : S[c * kEpiPitch + r];
+        }
+      }
+    }
+    __threadfence_system();                // this thread's remote stores performed before the CTA retires
+  }
   // fixed-order reduction of `part` over the 256 consumer threads
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
@@ -305,7 +330,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     double s = 0.0;
 #pragma unroll
     for (int w = 0; w < kConsumerWarps; ++w) s += red[w];
-    if (MODE == 0) {
+    if (p.n_dst > 0) {
+      const long long gt = (long long)p.gt_off + (long long)blockIdx.x * p.gt_stride;
+      for (int q = 0; q < p.n_dst; ++q) {
+        if (MODE == 0) p.dst_part[q][(long long)job * p.n_tiles_total + gt] = s;
+        else if (diag) p.dst_part[q][(long long)job * (p.ld / kTile) + I] = s;
+      }
+      __threadfence_system();
+    } else if (MODE == 0) {
       p.partial[(long long)job * p.n_tiles + blockIdx.x] = s;
     } else if (diag) {
       p.partial[(long long)job * (p.ld / kTile) + I] = s;

@@ -102,6 +102,14 @@ struct ProdParams {
   int mode;                // 0 = square/plain product + residual, 1 = NS update + trace
   double ca = 1.5;         // mode 1: X_{j+1} = ca X_j + cb X_j Y_j  (odd cubic filter step; NS: 1.5, -0.5)
   double cb = -0.5;
+  // Peer-memory exchange (sharded path, modes 0/1): the epilogue also stores its tile, mirror and partial
+  // into n_dst destination buffers (device arrays of base pointers, e.g. every rank's Y through CUDA IPC
+  // peer mappings over NVLink); partial slots use the global tile index gt_off + blockIdx.x * gt_stride
+  // in arrays of n_tiles_total per job.  n_dst = 0: local stores only.
+  double* const* dst = nullptr;
+  double* const* dst_part = nullptr;
+  int n_dst = 0;
+  int gt_off = 0, gt_stride = 1, n_tiles_total = 0;
 };
 
 // ---------------- mixed path (tcgen05 BF16x3, ns_mixed.cu) ----------------

@@ -1,10 +1,15 @@
 // Multi-GPU Newton–Schulz for large d (BASELINE configs[4]):
-// one process per GPU, NCCL over NVLink/NVSwitch.
+// one process per GPU.
 //
 // Partitioning: every rank keeps the full iterate X (replicated, 8 d_pad^2 bytes) but computes only
 // its share of the n(n+1)/2 upper 128x128 output tiles of each symmetric product:
 // rank r owns tiles t of the L2-ordered upper-tile list with t % P == r (balanced to one tile).
-// Per NS step:
+//
+// Default exchange (ns_api.cu run_sharded + ns_fp64.cu epilogue): every rank's workspace is mapped
+// into every process through CUDA IPC, and the product kernel's epilogue stores each tile, its mirror
+// and its residual / trace partial into all ranks' buffers over NVLink as the tile finishes; a
+// one-double ncclAllReduce per product is the barrier.  This file holds the kernels of the fallback
+// exchange (NCCL all-gather, used when a rank cannot map its peers):
 //   1. Y tiles (own) <- X X               ns_product_kernel<0> on the rank's tile list
 //   2. residual partials -> one double    ns_shard_sum_kernel (fixed order)
 //   3. the rank's tile list is cut into C chunks; as soon as chunk c's product kernel finishes (event

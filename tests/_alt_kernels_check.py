@@ -28,4 +28,13 @@ for d, k in ((1024, 64), (2048, 128)):
     o = ons.ns_reflector(p.H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
     R, res = nsr.ns_reflector(torch.from_numpy(p.H).cuda(), p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
     out[f"fp64_{d}"] = [checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]), res["steps"] == o["steps"]]
+if os.environ.get("NS_SHARD_P2P") == "0":
+    # the NCCL all-gather exchange of the sharded path on a one-rank communicator: = single path bitwise
+    p = workloads.cfg3_dense(d=2048, k=128)
+    Hg = torch.from_numpy(p.H).cuda()
+    c = nsr.ns_comm_init(0, 1, nsr.ns_comm_get_unique_id())
+    Rs, rs = nsr.ns_reflector_sharded(c, Hg, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    nsr.ns_comm_destroy(c)
+    Rd, rd = nsr.ns_reflector(Hg, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    out["fp64_sharded_nccl"] = [0.0 if torch.equal(Rs, Rd) else 1.0, rs["steps"] == rd["steps"]]
 print(json.dumps(out))

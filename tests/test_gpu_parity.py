@@ -644,7 +644,7 @@ def test_cfg2_seed1_golden(nsr, golden_dir):
 
 
 # ------------------------------------------------------------------ kernel-selection alternatives
-@pytest.mark.parametrize("env", [{"NS_MX2": "0"}, {"NS_TILE64": "0"}, {"NS_TILE64": "1"}])
+@pytest.mark.parametrize("env", [{"NS_MX2": "0"}, {"NS_TILE64": "0"}, {"NS_TILE64": "1"}, {"NS_SHARD_P2P": "0"}])
 def test_alternative_kernels(nsr, env):
     """The one-SM split-precision kernel (NS_MX2=0) and the forced 128- / 64-tile FP64 kernels give the
     same answers as the defaults (the knobs are read once per process: run in a subprocess)."""
@@ -661,3 +661,21 @@ def test_alternative_kernels(nsr, env):
             assert 1e-12 <= v <= 2e-5, (key, v)
         else:
             assert v[0] <= TOL_R and v[1], (key, v)
+
+
+# ------------------------------------------------------------------ sharded path: peer-memory exchange
+@pytest.mark.parametrize("d,mode,P", [(512, 0, 2), (640, 1, 3), (768, 0, 4)])
+def test_peer_exchange_products(nsr, d, mode, P):
+    """The sharded path's fused exchange: every virtual rank's product kernel stores its tiles into all
+    P destination matrices; after all ranks, each destination equals the single-GPU product bitwise."""
+    rng = np.random.default_rng(11 + d)
+    A = rng.standard_normal((d, d))
+    A = 0.5 * (A + A.T) / math.sqrt(d)
+    B = A @ A
+    Ag, Bg = torch.from_numpy(A).to(_dev()), torch.from_numpy(B).to(_dev())
+    Cs = [torch.full((d, d), float("nan"), dtype=torch.float64, device=_dev()) for _ in range(P)]
+    for r in range(P):
+        nsr.ns_symm_product_shard(Ag, Bg, Cs, r, P, mode=mode)
+    ref = nsr.ns_symm_product(Ag, Bg, mode=mode)
+    for C in Cs:
+        assert torch.equal(C, ref)
