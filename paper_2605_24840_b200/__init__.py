@@ -152,10 +152,17 @@ def _torch():
     return torch
 
 
-def _stream_ptr(stream):
+def _stream_ptr(stream, device=None):
+    """cudaStream_t of `stream`, or of torch's current stream on `device` (the raw-handle query avoids
+    building a torch.cuda.Stream object: ~3 us per call on the small-d latency path)."""
     torch = _torch()
-    s = torch.cuda.current_stream() if stream is None else stream
-    return ctypes.c_void_p(s.cuda_stream)
+    if stream is not None:
+        return ctypes.c_void_p(stream.cuda_stream)
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        idx = device.index if device is not None and device.index is not None else torch.cuda.current_device()
+        return ctypes.c_void_p(raw(idx))
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
 def _require_cuda_f64(t, name):
@@ -199,13 +206,12 @@ def ns_reflector(H, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_ABS, prec=NS_PR
     if R is None:
         R = torch.empty((d, d), dtype=torch.float64, device=H.device)
     _require_cuda_f64(R, "R")
-    need = lib.ns_workspace_bytes(d, prec)
     if ws is None:
-        ws = alloc_workspace(need, H.device)
+        ws = alloc_workspace(lib.ns_workspace_bytes(d, prec), H.device)   # (the library checks a given size)
     res = NsResult()
     args = (ctypes.c_void_p(H.data_ptr()), d, H.stride(0), float(s), float(alpha), int(k), int(max_steps), float(tol),
             int(tol_mode), int(prec), ctypes.c_void_p(R.data_ptr()), R.stride(0), ctypes.c_void_p(ws.data_ptr()),
-            ws.numel(), _stream_ptr(stream))
+            ws.numel(), _stream_ptr(stream, H.device))
     if options is None:
         st = lib.ns_reflector(*args, ctypes.byref(res))
     else:
