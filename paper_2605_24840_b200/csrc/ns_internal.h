@@ -238,6 +238,7 @@ struct OzParams {
   int kb0 = 0;             // first k-block of this launch (K segments, see launch_ozaki_product)
   int pm = 0;              // 0 whole K; K segments: 1 first (C = raw sums), 2 middle (C += raw), 3 last (C + raw -> epilogue)
 };
+constexpr int kOzBadRow = 1 << 20;   // row exponent marking a non-finite row (its products become NaN)
 constexpr int kOzSegKb = 256;   // k-blocks per K segment (K = 16384): one launch per segment for larger d
 cudaError_t launch_ozaki_slice(const double* X, int8_t* slices, int* expo, int d_pad, int batch, cudaStream_t st);
 cudaError_t launch_ozaki_product(const CUtensorMap& tmA, const CUtensorMap& tmB, const OzParams& p, int batch,

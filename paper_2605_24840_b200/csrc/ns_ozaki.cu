@@ -37,16 +37,29 @@ __global__ void __launch_bounds__(256) ns_ozaki_slice_kernel(const double* __res
   const long long nn = (long long)d_pad * d_pad;
   const double* x = X + (long long)job * nn + (long long)row * d_pad;
   double m = 0.0;
-  for (int j = threadIdx.x; j < d_pad; j += 256) m = fmax(m, fabs(x[j]));
+  for (int j = threadIdx.x; j < d_pad; j += 256) {
+    const double a = fabs(x[j]);
+    m = (a > m || a != a) ? a : m;               // NaN / Inf propagate (fmax would drop a NaN)
+  }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  for (int o = 16; o > 0; o >>= 1) {
+    const double b = __shfl_xor_sync(0xffffffffu, m, o);
+    m = (b > m || b != b) ? b : m;
+  }
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
   double mm = 0.0;
-  for (int w = 0; w < 8; ++w) mm = fmax(mm, red[w]);
+  for (int w = 0; w < 8; ++w) mm = (red[w] > mm || red[w] != red[w]) ? red[w] : mm;
   int e = 0;
-  if (mm > 0.0 && isfinite(mm)) frexp(mm, &e);   // mm = f 2^e, f in [0.5, 1)  =>  |x_ij| < 2^e
+  if (!isfinite(mm)) e = kOzBadRow;                  // non-finite row: the products of this row come out NaN
+  else if (mm > 0.0) frexp(mm, &e);                 // mm = f 2^e, f in [0.5, 1)  =>  |x_ij| < 2^e
   if (threadIdx.x == 0) expo[(long long)job * d_pad + row] = e;
+  if (e == kOzBadRow) {
+    int8_t* o0 = slices + (long long)job * kOzSlices * nn + (long long)row * d_pad;
+    for (int j = threadIdx.x; j < d_pad; j += 256)
+      for (int q = 0; q < kOzSlices; ++q) o0[(long long)q * nn + j] = 0;
+    return;
+  }
   int8_t* out = slices + (long long)job * kOzSlices * nn + (long long)row * d_pad;
   for (int j = threadIdx.x; j < d_pad; j += 256) {
     // N = x 2^{54-e} rounded to an integer (|N| < 2^54), written in balanced base 256:
@@ -72,13 +85,25 @@ __global__ void __launch_bounds__(256) ns_ozaki_slice_rows_kernel(const double* 
   const long long nn = (long long)d_pad * d_pad;
   const double* x = X + (long long)job * nn + (long long)row * d_pad;
   double m = 0.0;
-  for (int j = lane; j < d_pad; j += 32) m = fmax(m, fabs(x[j]));
+  for (int j = lane; j < d_pad; j += 32) {
+    const double a = fabs(x[j]);
+    m = (a > m || a != a) ? a : m;
+  }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  for (int o = 16; o > 0; o >>= 1) {
+    const double b = __shfl_xor_sync(0xffffffffu, m, o);
+    m = (b > m || b != b) ? b : m;
+  }
   int e = 0;
-  if (m > 0.0 && isfinite(m)) frexp(m, &e);
+  if (!isfinite(m)) e = kOzBadRow;
+  else if (m > 0.0) frexp(m, &e);
   if (lane == 0) expo[(long long)job * d_pad + row] = e;
   int8_t* out = slices + (long long)job * kOzSlices * nn + (long long)row * d_pad;
+  if (e == kOzBadRow) {
+    for (int j = lane; j < d_pad; j += 32)
+      for (int q = 0; q < kOzSlices; ++q) out[(long long)q * nn + j] = 0;
+    return;
+  }
   for (int j = lane; j < d_pad; j += 32) {
     long long N = (long long)rint(ldexp(x[j], 54 - e));
 #pragma unroll
@@ -250,7 +275,9 @@ __global__ void __launch_bounds__(kOzThreads, 1)
         // times 2^(er + ec - 12): one multiply by the power of two built from its bits (ldexp only when
         // that power is outside the normal range, i.e. for extreme operand scales)
         const int ex = er + ecol[c] - 12;
-        acc[c] = (ex >= -1022 && ex <= 1023) ? acc[c] * __hiloint2double((ex + 1023) << 20, 0) : ldexp(acc[c], ex);
+        acc[c] = (ex >= -1022 && ex <= 1023) ? acc[c] * __hiloint2double((ex + 1023) << 20, 0)
+                 : (er == kOzBadRow || ecol[c] == kOzBadRow) ? __longlong_as_double(0x7ff8000000000000LL)   // NaN
+                                                             : ldexp(acc[c], ex);
       }
       double part = 0.0;
       const double* X = p.Xold + base;

@@ -679,3 +679,29 @@ def test_peer_exchange_products(nsr, d, mode, P):
     ref = nsr.ns_symm_product(Ag, Bg, mode=mode)
     for C in Cs:
         assert torch.equal(C, ref)
+
+
+# ------------------------------------------------------------------ edge cases on every precision path
+@pytest.mark.parametrize("prec", [1, 2, 3])
+def test_edge_cases_other_precisions(nsr, prec):
+    """Non-finite input, a too-small scale, fixed-step runs and s outside the spectrum on the mixed
+    (BF16x3, TF32x3) and Ozaki paths: same flags / certificates as the oracle, no hang, R symmetric."""
+    p = workloads.cfg3_dense(d=384, k=24)
+    Hg = torch.from_numpy(p.H).to(_dev())
+    # NaN in H -> NONFINITE at step 0, certificate -1 (flag definitions in DESIGN)
+    Hn = p.H.copy()
+    Hn[3, 5] = Hn[5, 3] = np.nan
+    R, res = nsr.ns_reflector(torch.from_numpy(Hn).to(_dev()), p.s, p.alpha, p.k, 100, 1e-10, 1, prec=prec)
+    assert res["flags"] & ons.NONFINITE and res["steps"] == 0 and res["cert"] == -1
+    # s below / above the whole spectrum: R = +I / -I, k = 0 / d
+    for s_, k_, sign in ((-2.0, 0, 1.0), (2.0, p.d, -1.0)):
+        R, res = nsr.ns_reflector(Hg, s_, 3.1, k_, 100, 1e-10, 1, prec=prec)
+        assert res["cert"] == k_ and res["flags"] & ons.CONVERGED
+        assert np.max(np.abs(R.cpu().numpy() - sign * np.eye(p.d))) <= 1e-9
+    # fixed 6 steps: the oracle's X_6 (mixed: low-precision steps then re-anchor + polish -> compare loosely)
+    o = ons.ns_reflector(p.H, p.s, p.alpha, p.k, 6, 0.0, 1)
+    R, res = nsr.ns_reflector(Hg, p.s, p.alpha, p.k, 6, 0.0, 1, prec=prec)
+    assert res["steps"] == 6 and res["flags"] & ons.MAX_STEPS
+    Rn = R.cpu().numpy()
+    assert np.array_equal(Rn, Rn.T)
+    assert checks.frob_per_sqrt_d(Rn, o["R"]) <= (1e-10 if prec == 3 else 1e-4)
