@@ -705,3 +705,22 @@ def test_edge_cases_other_precisions(nsr, prec):
     Rn = R.cpu().numpy()
     assert np.array_equal(Rn, Rn.T)
     assert checks.frob_per_sqrt_d(Rn, o["R"]) <= (1e-10 if prec == 3 else 1e-4)
+
+
+@pytest.mark.parametrize("prec", [0, 3])
+def test_batched_nonfinite_problem_is_isolated(nsr, prec):
+    """One problem of a batch carries a NaN: it stops with NONFINITE at step 0; the others are unaffected."""
+    probs = workloads.cfg1_batched(seed=0, first=0, count=6)
+    Hs = np.stack([p.H for p in probs])
+    Hs[2, 7, 9] = Hs[2, 9, 7] = np.nan
+    R, outs = nsr.ns_reflector_batched(torch.from_numpy(Hs).to(_dev()), [p.s for p in probs],
+                                       [p.alpha for p in probs], [p.k for p in probs], 100, 1e-12, prec=prec)
+    R = R.cpu().numpy()
+    assert outs[2]["flags"] & ons.NONFINITE and outs[2]["steps"] == 0
+    for i, p in enumerate(probs):
+        if i == 2:
+            continue
+        o = ons.ns_reflector(p.H, p.s, p.alpha, p.k, 100, 1e-12, 0, trace_residuals=True)
+        if not _tie_band(o["hist_residual"], 1e-12, o["steps"]):
+            assert outs[i]["steps"] == o["steps"]
+        assert outs[i]["cert"] == p.k and checks.frob_per_sqrt_d(R[i], o["R"]) <= TOL_R
