@@ -186,6 +186,13 @@ std::vector<int2> make_tiles(int n) {
   return v;
 }
 
+// Ozaki tile list and the number of per-tile residual partials it yields: 128x128 tiles walked by CTA
+// clusters of 2 (each CTA one 64-column half, A digits multicast; default) or 128x64 single-CTA tiles.
+std::vector<int2> oz_tile_list(int n, bool sym) {
+  return use_oz_mc() ? (sym ? make_tiles(n) : make_tiles_full(n)) : make_tiles_oz(n, sym);
+}
+int oz_partials(const std::vector<int2>& ot) { return (use_oz_mc() ? 2 : 1) * (int)ot.size(); }
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -500,8 +507,8 @@ ns_status_t run_ozaki_batch(const Layout& L, uint8_t* ws, const double* H, long 
   int* n_active = reinterpret_cast<int*>(ws + L.off_active);
   HostRing& rg = ring();
   if (!rg.ok) return fail(NS_ERR_CUDA, "pinned status ring allocation failed");
-  std::vector<int2> ot = make_tiles_oz(L.n, true);
-  const int nt = (int)ot.size(), ndiag = 2 * L.n;
+  std::vector<int2> ot = oz_tile_list(L.n, true);
+  const int nt = (int)ot.size(), npart = oz_partials(ot), ndiag = 2 * L.n;
   const long long js = (long long)L.d_pad * L.d_pad;
   NS_CUDA(cudaMemcpyAsync(otiles, ot.data(), ot.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
   NS_CUDA(cudaMemcpyAsync(djobs, jobs.data(), jobs.size() * sizeof(JobParams), cudaMemcpyHostToDevice, st));
@@ -530,7 +537,7 @@ ns_status_t run_ozaki_batch(const Layout& L, uint8_t* ws, const double* H, long 
     NS_CUDA(launch_ozaki_slice(Xc, slX, eX, L.d_pad, batch, st));
     OzParams sq{otiles, nt, L.d_pad / 64, L.d, L.d_pad, js, Y, nullptr, eX, eX, res, state, 0};
     NS_CUDA(launch_ozaki_product(tXa, tXb, sq, batch, st));
-    NS_CUDA(launch_decide(state, djobs, res, nt, trp, ndiag, lp, batch, n_active, st));
+    NS_CUDA(launch_decide(state, djobs, res, npart, trp, ndiag, lp, batch, n_active, st));
     nl += 3;
     if (j < max_steps) {
       NS_CUDA(launch_ozaki_slice(Y, slY, eY, L.d_pad, batch, st));
@@ -690,7 +697,7 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
       if ((s = encode_map_i8(&tOb, slX, L.d_pad, kOzSlices, 64)) != NS_OK) return s;
       if ((s = encode_map_i8(&tOy, slY, L.d_pad, kOzSlices, 64)) != NS_OK) return s;
     }
-    const std::vector<int2> ot_full = oz ? make_tiles_oz(L.n, false) : std::vector<int2>();
+    const std::vector<int2> ot_full = oz ? oz_tile_list(L.n, false) : std::vector<int2>();
     // C = P Q^T over every tile (P, Q row panels), FP64 DMMA or Ozaki
     auto dense = [&](const double* P, const CUtensorMap& tP, const double* Q, const CUtensorMap& tQ,
                      double* C) -> ns_status_t {
@@ -745,8 +752,8 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
     NS_CUDA(cudaMemcpyAsync(n_active, &one, sizeof(int), cudaMemcpyHostToDevice, st));
     if (oz) {
       // Ozaki steps (as run_ozaki): symmetric 128x64 tile list, its residual / trace partial layouts
-      const std::vector<int2> ot = make_tiles_oz(L.n, true);
-      const int nt = (int)ot.size(), ndiag = 2 * L.n;
+      const std::vector<int2> ot = oz_tile_list(L.n, true);
+      const int nt = (int)ot.size(), npart = oz_partials(ot), ndiag = 2 * L.n;
       NS_CUDA(cudaMemcpyAsync(otiles, ot.data(), ot.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
       NS_CUDA(cudaMemsetAsync(otr, 0, sizeof(double) * ndiag, st));
       NS_CUDA(launch_trace_partials(Xt, L.d, L.d_pad, 1, otr, st));
@@ -763,7 +770,7 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
         NS_CUDA(launch_ozaki_slice(Xc, slX, eX, L.d_pad, 1, st));
         OzParams sq{otiles, nt, L.d_pad / 64, L.d, L.d_pad, 0, Y, nullptr, eX, eX, ores, state, 0};
         NS_CUDA(launch_ozaki_product(tOa, tOb, sq, 1, st));
-        NS_CUDA(launch_decide(state, djobs, ores, nt, otr, ndiag, lp, 1, n_active, st));
+        NS_CUDA(launch_decide(state, djobs, ores, npart, otr, ndiag, lp, 1, n_active, st));
         nl += 3;
         if (j < max_steps) {
           NS_CUDA(launch_ozaki_slice(Y, slY, eY, L.d_pad, 1, st));
@@ -1335,7 +1342,7 @@ ns_status_t ns_symm_product(const double* A, const double* B, double* C, int64_t
     int* eA = reinterpret_cast<int*>(w + L.off_oex);
     int* eB = reinterpret_cast<int*>(w + L.off_oey);
     int2* otiles = reinterpret_cast<int2*>(w + L.off_otiles);
-    std::vector<int2> ot = make_tiles_oz(L.n, mode != 2);
+    std::vector<int2> ot = oz_tile_list(L.n, mode != 2);
     NS_CUDA(cudaMemcpyAsync(otiles, ot.data(), ot.size() * sizeof(int2), cudaMemcpyHostToDevice, cs));
     NS_CUDA(launch_ozaki_slice(Pa, slA, eA, L.d_pad, 1, cs));
     NS_CUDA(launch_ozaki_slice(Pb, slB, eB, L.d_pad, 1, cs));

@@ -240,6 +240,7 @@ struct OzParams {
 };
 constexpr int kOzBadRow = 1 << 20;   // row exponent marking a non-finite row (its products become NaN)
 constexpr int kOzSegKb = 256;   // k-blocks per K segment (K = 16384): one launch per segment for larger d
+bool use_oz_mc();   // Ozaki products on CTA clusters of 2 (A digits multicast); NS_OZ_MC=0 disables
 cudaError_t launch_ozaki_slice(const double* X, int8_t* slices, int* expo, int d_pad, int batch, cudaStream_t st);
 cudaError_t launch_ozaki_product(const CUtensorMap& tmA, const CUtensorMap& tmB, const OzParams& p, int batch,
                                  cudaStream_t st);

@@ -116,6 +116,26 @@ __global__ void __launch_bounds__(256) ns_ozaki_slice_rows_kernel(const double* 
   }
 }
 
+// TMA load delivered to the same shared-memory offset in every CTA of `mask` (cluster multicast); each
+// destination CTA's barrier at `bar`'s offset receives the bytes.
+__device__ __forceinline__ void tma_load_3d_mc(void* dst, const void* tmap, int c0, int c1, int c2, uint64_t* bar,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+// arrive (once) on the barrier at this offset in every CTA of `mask` when this thread's prior tcgen05
+// operations complete
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
 __device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                         uint32_t accumulate) {
   asm volatile(
@@ -131,7 +151,7 @@ __device__ __forceinline__ uint64_t sdesc_k64(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | (1ull << 16) | (32ull << 32) | (1ull << 46) | (4ull << 61);
 }
 
-template <int MODE>
+template <int MODE, bool MC>
 __global__ void __launch_bounds__(kOzThreads, 1)
     ns_ozaki_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                             const OzParams p, int n_items) {
@@ -152,11 +172,21 @@ __global__ void __launch_bounds__(kOzThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_chunks = (p.nkb + kOzChunkKb - 1) / kOzChunkKb;
+  // MC (cluster of 2): work items are 128 x 128 tiles walked per cluster; CTA `rank` takes the 64-column
+  // half 2 J + rank.  The 7 A digit slabs of a k-block are shared: each CTA loads about half of them with
+  // TMA multicast into both CTAs' shared memory (half the A traffic from L2 per CTA).
+  const int rank = MC ? (int)cluster_ctarank() : 0;
+  const int item0 = MC ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int istride = MC ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  auto tile_of = [&](int item, int job) -> int2 {
+    const int2 t = p.tiles[item - job * p.n_tiles];
+    return MC ? make_int2(t.x, 2 * t.y + rank) : t;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kOzStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC ? 2 : 1);   // MC: both CTAs' MMA warps release a slot (their A halves are shared)
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, 8);
@@ -165,6 +195,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
+  if (MC) cluster_sync_all();              // peer barriers initialised before any multicast / remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -173,18 +204,26 @@ __global__ void __launch_bounds__(kOzThreads, 1)
       tma_prefetch_desc(&tmA);
       tma_prefetch_desc(&tmB);
       uint32_t kbg = 0;                    // k-blocks issued by this CTA so far (ring position)
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      for (int item = item0; item < n_items; item += istride) {
         const int job = item / p.n_tiles;
         if (p.state != nullptr && p.state[job].done) continue;
-        const int2 tile = p.tiles[item - job * p.n_tiles];
+        const int2 tile = tile_of(item, job);
         for (int kb = 0; kb < p.nkb; ++kb, ++kbg) {
           const int s = kbg % kOzStages;
           if (kbg >= kOzStages) mbar_wait(&empty[s], ((kbg / kOzStages) & 1u) ^ 1u);
           uint8_t* st = smem + s * kOzStageBytes;
           mbar_arrive_expect_tx(&full[s], kOzStageBytes);
+          if (MC) {
 #pragma unroll
-          for (int q = 0; q < kOzSlices; ++q)
-            tma_load_3d(st + q * kOzSlabA, &tmA, (p.kb0 + kb) * 64, tile.x * kTile, job * kOzSlices + q, &full[s]);
+            for (int q = 0; q < kOzSlices; ++q)
+              if ((q & 1) == rank)
+                tma_load_3d_mc(st + q * kOzSlabA, &tmA, (p.kb0 + kb) * 64, tile.x * kTile, job * kOzSlices + q,
+                               &full[s], 0x3);
+          } else {
+#pragma unroll
+            for (int q = 0; q < kOzSlices; ++q)
+              tma_load_3d(st + q * kOzSlabA, &tmA, (p.kb0 + kb) * 64, tile.x * kTile, job * kOzSlices + q, &full[s]);
+          }
 #pragma unroll
           for (int q = 0; q < kOzSlices; ++q)
             tma_load_3d(st + kOzSlices * kOzSlabA + q * kOzSlabB, &tmB, (p.kb0 + kb) * 64, tile.y * 64, job * kOzSlices + q,
@@ -196,7 +235,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
     // idesc: D=S32 (bits 4-5 = 2), A/B signed int8 (bits 7-9 / 10-12 = 1), K-major, M=128 (N set per MMA).
     const uint32_t idesc_base = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTile >> 4) << 24);
     uint32_t kbg = 0, cg = 0;              // k-blocks / chunks consumed by this CTA so far
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    for (int item = item0; item < n_items; item += istride) {
       const int job = item / p.n_tiles;
       if (p.state != nullptr && p.state[job].done) continue;
       for (int c = 0; c < n_chunks; ++c, ++cg) {
@@ -228,7 +267,8 @@ __global__ void __launch_bounds__(kOzThreads, 1)
                 }
               }
             }
-            umma_commit(&empty[s]);
+            if (MC) umma_commit_mc(&empty[s], 0x3);   // release the slot in both CTAs
+            else umma_commit(&empty[s]);
             if (kb == kb1 - 1) umma_commit(tfull);
           }
           __syncwarp();
@@ -241,10 +281,10 @@ __global__ void __launch_bounds__(kOzThreads, 1)
     const int r = q * 32 + lane;
     const int ew = warp - 2;               // 0..7
     uint32_t cg = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    for (int item = item0; item < n_items; item += istride) {
       const int job = item / p.n_tiles;
       if (p.state != nullptr && p.state[job].done) continue;
-      const int2 tile = p.tiles[item - job * p.n_tiles];
+      const int2 tile = tile_of(item, job);
       double acc[32];
 #pragma unroll
       for (int c = 0; c < 32; ++c) acc[c] = 0.0;
@@ -350,7 +390,8 @@ __global__ void __launch_bounds__(kOzThreads, 1)
 #pragma unroll
           for (int w = 0; w < 8; ++w) sum += red[w];
           const int i0t = tile.x * kTile, j0t = tile.y * 64;
-          if (MODE == 0) p.partial[(long long)job * p.n_tiles + (item - job * p.n_tiles)] = sum;
+          if (MODE == 0)
+            p.partial[(long long)job * (MC ? 2 * p.n_tiles : p.n_tiles) + (item - job * p.n_tiles) * (MC ? 2 : 1) + rank] = sum;
           else if (j0t <= i0t + kTile - 1 && j0t + 63 >= i0t) p.partial[(long long)job * (2 * (p.ld / kTile)) + tile.y] = sum;
         }
         named_bar_sync(1, 256);              // red[] is reused by the next tile
@@ -359,7 +400,17 @@ __global__ void __launch_bounds__(kOzThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (MC) cluster_sync_all();              // no multicast into, or arrive on, a CTA that has left
   if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+// Cluster-of-2 Ozaki products (A digits multicast) on by default; NS_OZ_MC=0 selects single CTAs.
+bool use_oz_mc() {
+  static const bool on = [] {
+    const char* e = getenv("NS_OZ_MC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 cudaError_t launch_ozaki_slice(const double* X, int8_t* slices, int* expo, int d_pad, int batch, cudaStream_t st) {
@@ -375,7 +426,7 @@ cudaError_t launch_ozaki_slice(const double* X, int8_t* slices, int* expo, int d
 
 cudaError_t launch_ozaki_product(const CUtensorMap& tmA, const CUtensorMap& tmB, const OzParams& p, int batch,
                                  cudaStream_t st) {
-  static unsigned long long attr[3] = {0, 0, 0};
+  static unsigned long long attr[3] = {0, 0, 0}, attr_mc[3] = {0, 0, 0};
   static int n_sm = 0;
   if (n_sm == 0) {
     int dev = 0;
@@ -399,19 +450,46 @@ cudaError_t launch_ozaki_product(const CUtensorMap& tmA, const CUtensorMap& tmB,
     return cudaSuccess;
   }
   const int n_items = p.n_tiles * batch;
+  if (use_oz_mc()) {
+    // clusters of 2 CTAs on 128 x 128 tiles (p.tiles holds (I, J) of 128-column blocks); persistent
+    const int n_cl = std::min(n_items, n_sm / 2);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * n_cl);
+    cfg.blockDim = dim3(kOzThreads);
+    cfg.dynamicSmemBytes = kOzSmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    switch (p.mode) {
+      case 0:
+        smem_attr(ns_ozaki_product_kernel<0, true>, kOzSmemBytes, attr_mc[0]);
+        return cudaLaunchKernelEx(&cfg, ns_ozaki_product_kernel<0, true>, tmA, tmB, p, n_items);
+      case 1:
+        smem_attr(ns_ozaki_product_kernel<1, true>, kOzSmemBytes, attr_mc[1]);
+        return cudaLaunchKernelEx(&cfg, ns_ozaki_product_kernel<1, true>, tmA, tmB, p, n_items);
+      default:
+        smem_attr(ns_ozaki_product_kernel<2, true>, kOzSmemBytes, attr_mc[2]);
+        return cudaLaunchKernelEx(&cfg, ns_ozaki_product_kernel<2, true>, tmA, tmB, p, n_items);
+    }
+  }
   const dim3 grid(std::min(n_items, n_sm));   // persistent: one CTA per SM
   switch (p.mode) {
     case 0:
-      smem_attr(ns_ozaki_product_kernel<0>, kOzSmemBytes, attr[0]);
-      ns_ozaki_product_kernel<0><<<grid, kOzThreads, kOzSmemBytes, st>>>(tmA, tmB, p, n_items);
+      smem_attr(ns_ozaki_product_kernel<0, false>, kOzSmemBytes, attr[0]);
+      ns_ozaki_product_kernel<0, false><<<grid, kOzThreads, kOzSmemBytes, st>>>(tmA, tmB, p, n_items);
       break;
     case 1:
-      smem_attr(ns_ozaki_product_kernel<1>, kOzSmemBytes, attr[1]);
-      ns_ozaki_product_kernel<1><<<grid, kOzThreads, kOzSmemBytes, st>>>(tmA, tmB, p, n_items);
+      smem_attr(ns_ozaki_product_kernel<1, false>, kOzSmemBytes, attr[1]);
+      ns_ozaki_product_kernel<1, false><<<grid, kOzThreads, kOzSmemBytes, st>>>(tmA, tmB, p, n_items);
       break;
     default:
-      smem_attr(ns_ozaki_product_kernel<2>, kOzSmemBytes, attr[2]);
-      ns_ozaki_product_kernel<2><<<grid, kOzThreads, kOzSmemBytes, st>>>(tmA, tmB, p, n_items);
+      smem_attr(ns_ozaki_product_kernel<2, false>, kOzSmemBytes, attr[2]);
+      ns_ozaki_product_kernel<2, false><<<grid, kOzThreads, kOzSmemBytes, st>>>(tmA, tmB, p, n_items);
       break;
   }
   return cudaGetLastError();
