@@ -290,6 +290,20 @@ ns_status_t ns_symm_product_shard(const double* A, const double* B, double* cons
  * chunk_slots slots (padded to the largest rank); chunk c of rank q carries the rank's local tiles
  * c*chunk_slots .. c*chunk_slots + chunk_slots - 1, i.e. global upper tiles (c*chunk_slots + s)*P + q. */
 ns_status_t ns_shard_chunks(int64_t d, int nranks, int32_t* n_chunks, int32_t* chunk_slots);
+/*
+ * ns_reflector_sharded_emulated — the sharded algorithm with `nranks` ranks emulated on ONE GPU
+ * (tests; multi-GPU behaviour without multiple GPUs): nranks workspace replicas, each rank's product
+ * kernels launched in turn with the multi-GPU path's peer-store epilogue (destinations: every
+ * replica), each replica deciding on its own data.  No kernel waits on another.  Returns
+ * NS_ERR_CUDA ("emulated ranks diverged") if the replicas' final states differ in any bit.  Same
+ * arguments and result as ns_reflector (FP64); device H and R; workspace >=
+ * ns_workspace_bytes_sharded_emulated(d, nranks).
+ */
+size_t ns_workspace_bytes_sharded_emulated(int64_t d, int nranks);
+ns_status_t ns_reflector_sharded_emulated(int32_t nranks, const double* H, int64_t d, int64_t ldh, double s,
+                                          double alpha, int32_t k, int32_t max_steps, double tol, ns_tolmode_t tm,
+                                          double* R, int64_t ldr, void* ws, size_t ws_bytes, void* stream,
+                                          ns_result_t* out);
 size_t ns_workspace_bytes_sharded(int64_t d, int nranks);
 ns_status_t ns_reflector_sharded(ns_comm_t* comm, const double* H, int64_t d, int64_t ldh, double s, double alpha,
                                  int32_t k, int32_t max_steps, double tol, ns_tolmode_t tm, double* R, int64_t ldr,

@@ -26,7 +26,7 @@ EXPORTED_SYMBOLS = (
     "ns_reflector_ex", "ns_comm_get_unique_id", "ns_comm_init", "ns_comm_destroy", "ns_shard_plan",
     "ns_workspace_bytes_sharded", "ns_reflector_sharded", "ns_shard_chunks", "ns_workspace_bytes_setup", "ns_scale_bound",
     "ns_shift_certificate", "ns_workspace_bytes_alg1", "ns_alg1_rotated_quartic", "ns_debug_mx_trace",
-    "ns_symm_product_shard",
+    "ns_symm_product_shard", "ns_workspace_bytes_sharded_emulated", "ns_reflector_sharded_emulated",
 )
 
 
@@ -100,6 +100,11 @@ def load_library(path=LIB_PATH):
                                          ctypes.c_int, c_vp, c_i64, c_vp, c_sz, c_vp, ctypes.POINTER(NsResult)]
     lib.ns_symm_product.restype = ctypes.c_int
     lib.ns_symm_product.argtypes = [c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, ctypes.c_int, c_vp, c_sz, c_vp]
+    lib.ns_workspace_bytes_sharded_emulated.restype = c_sz
+    lib.ns_workspace_bytes_sharded_emulated.argtypes = [c_i64, ctypes.c_int]
+    lib.ns_reflector_sharded_emulated.restype = ctypes.c_int
+    lib.ns_reflector_sharded_emulated.argtypes = [c_i32, c_vp, c_i64, c_i64, c_dbl, c_dbl, c_i32, c_i32, c_dbl,
+                                                  ctypes.c_int, c_vp, c_i64, c_vp, c_sz, c_vp, c_vp]
     lib.ns_symm_product_shard.restype = ctypes.c_int
     lib.ns_symm_product_shard.argtypes = [c_vp, c_vp, c_vp, c_i32, c_i64, c_i32, c_i32, c_i32, c_vp, c_sz, c_vp]
     lib.ns_build_info.restype = ctypes.c_char_p
@@ -290,6 +295,26 @@ def ns_symm_product(A, B, mode=0, C=None, ws=None, stream=None, prec=NS_PREC_FP6
     _check(st)
     return C
 
+
+
+def ns_reflector_sharded_emulated(nranks, H, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_ABS, R=None, ws=None,
+                                  stream=None):
+    """The sharded algorithm with `nranks` ranks emulated on one GPU (C-ABI ns_reflector_sharded_emulated)."""
+    torch = _torch()
+    lib = load_library()
+    _require_cuda_f64(H, "H")
+    d = H.shape[0]
+    if R is None:
+        R = torch.empty((d, d), dtype=torch.float64, device=H.device)
+    if ws is None:
+        ws = alloc_workspace(lib.ns_workspace_bytes_sharded_emulated(d, nranks), H.device)
+    res = NsResult()
+    st = lib.ns_reflector_sharded_emulated(int(nranks), ctypes.c_void_p(H.data_ptr()), d, H.stride(0), float(s),
+                                           float(alpha), int(k), int(max_steps), float(tol), int(tol_mode),
+                                           ctypes.c_void_p(R.data_ptr()), R.stride(0), ctypes.c_void_p(ws.data_ptr()),
+                                           ws.numel(), _stream_ptr(stream, H.device), ctypes.byref(res))
+    _check(st)
+    return R, res.as_dict()
 
 
 def ns_symm_product_shard(A, B, C_list, rank, nranks, mode=0, ws=None, stream=None):

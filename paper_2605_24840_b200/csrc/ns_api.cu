@@ -1127,6 +1127,115 @@ ns_status_t run_sharded(CommCtx& cc, const ShardLayout& SL, uint8_t* ws, const d
   return NS_OK;
 }
 
+// The sharded algorithm with P ranks emulated on ONE GPU (tests): P workspace replicas side by side,
+// each rank's product kernel launched in turn on one stream with the same peer-store epilogue as the
+// multi-GPU path (destinations: all replicas), every replica running its own decide.  No kernel waits
+// on another (stream order replaces the cross-rank barrier), so this is safe on one device; it checks
+// the partitioning, the global partial slots, the trace-parity buffers and that all ranks take
+// identical decisions (their final states must agree bit for bit).
+ns_status_t run_sharded_emulated(int64_t d, int P, uint8_t* ws, size_t stride, const double* H, long long ldh,
+                                 const JobParams& jp, int32_t max_steps, double tol, ns_tolmode_t tm, double* R,
+                                 long long ldr, cudaStream_t st, DevState& out_state, int* launches) {
+  std::vector<ShardLayout> sl;
+  std::vector<uint8_t*> w(P);
+  for (int r = 0; r < P; ++r) {
+    sl.push_back(make_shard_layout(d, P, r));
+    w[r] = ws + (size_t)r * stride;
+  }
+  const Layout& L = sl[0].base;
+  auto ptr = [&](int r, size_t off) { return reinterpret_cast<double*>(w[r] + off); };
+  HostRing& rg = ring();
+  if (!rg.ok) return fail(NS_ERR_CUDA, "pinned status ring allocation failed");
+  const std::vector<int2> tl = make_tiles(L.n);
+  std::vector<std::vector<int2>> mt(P);
+  std::vector<CUtensorMap> tA(P), tB(P), tY(P);
+  ns_status_t s;
+  // peer pointer table [6][P] (Y, Xa, Xb, res, tr even, tr odd), identical for every replica; replica 0 holds it
+  double** dptr = reinterpret_cast<double**>(w[0] + sl[0].off_ptrs);
+  std::vector<double*> h(6 * (size_t)P);
+  for (int r = 0; r < P; ++r) {
+    h[0 * P + r] = ptr(r, L.off_y);
+    h[1 * P + r] = ptr(r, L.off_xa);
+    h[2 * P + r] = ptr(r, L.off_xb);
+    h[3 * P + r] = ptr(r, L.off_res);
+    h[4 * P + r] = ptr(r, L.off_tr);
+    h[5 * P + r] = ptr(r, L.off_tr) + L.n;
+  }
+  NS_CUDA(cudaMemcpyAsync(dptr, h.data(), h.size() * sizeof(double*), cudaMemcpyHostToDevice, st));
+  int nl = 0;
+  for (int r = 0; r < P; ++r) {
+    mt[r] = shard_tiles(tl, P, r);
+    int2* my = reinterpret_cast<int2*>(w[r] + sl[r].off_my);
+    if (!mt[r].empty()) NS_CUDA(cudaMemcpyAsync(my, mt[r].data(), mt[r].size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+    NS_CUDA(cudaMemcpyAsync(w[r] + L.off_jobs, &jp, sizeof(JobParams), cudaMemcpyHostToDevice, st));
+    if ((s = encode_map(&tA[r], ptr(r, L.off_xa), L.d_pad, 1)) != NS_OK) return s;
+    if ((s = encode_map(&tB[r], ptr(r, L.off_xb), L.d_pad, 1)) != NS_OK) return s;
+    if ((s = encode_map(&tY[r], ptr(r, L.off_y), L.d_pad, 1)) != NS_OK) return s;
+    DevState* state = reinterpret_cast<DevState*>(w[r] + L.off_state);
+    int* n_active = reinterpret_cast<int*>(w[r] + L.off_active);
+    NS_CUDA(launch_zero_state(state, 1, n_active, st));
+    NS_CUDA(launch_init(H, ldh, 0, ptr(r, L.off_xa), reinterpret_cast<JobParams*>(w[r] + L.off_jobs), L.d, L.d_pad, 1, st));
+    NS_CUDA(launch_trace_partials(ptr(r, L.off_xa), L.d, L.d_pad, 1, ptr(r, L.off_tr), st));
+    nl += 3;
+  }
+  auto products = [&](bool odd, int mode) -> ns_status_t {
+    for (int r = 0; r < P; ++r) {
+      if (mt[r].empty()) continue;
+      const CUtensorMap& tC = odd ? tB[r] : tA[r];
+      double* Xc = ptr(r, odd ? L.off_xb : L.off_xa);
+      double* C = (mode == 0) ? ptr(r, L.off_y) : ptr(r, odd ? L.off_xa : L.off_xb);
+      ProdParams pp{reinterpret_cast<int2*>(w[r] + sl[r].off_my), (int)mt[r].size(), L.d_pad / kBK, L.d, L.d_pad,
+                    (long long)L.d_pad * L.d_pad, C, mode == 1 ? Xc : nullptr,
+                    mode == 0 ? ptr(r, L.off_res) : ptr(r, L.off_tr) + (odd ? 0 : L.n),
+                    reinterpret_cast<DevState*>(w[r] + L.off_state), mode};
+      const int which_c = (mode == 0) ? 0 : (odd ? 1 : 2);
+      const int which_p = (mode == 0) ? 3 : (odd ? 4 : 5);
+      pp.dst = dptr + (size_t)which_c * P;
+      pp.dst_part = dptr + (size_t)which_p * P;
+      pp.n_dst = P;
+      pp.gt_off = r;
+      pp.gt_stride = P;
+      pp.n_tiles_total = L.n_tiles;
+      NS_CUDA(launch_product(tC, mode == 0 ? tC : tY[r], pp, 1, st));
+      nl += 1;
+    }
+    return NS_OK;
+  };
+  LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0, -1, 0};
+  const int LA = 2;
+  for (int j = 0; j <= max_steps; ++j) {
+    if (j >= LA) {
+      const int slot = (j - LA) % 16;
+      NS_CUDA(cudaEventSynchronize(rg.ev[slot]));
+      if (rg.slots[slot] == 0) break;
+    }
+    const bool odd = (j & 1) != 0;
+    if ((s = products(odd, 0)) != NS_OK) return s;
+    for (int r = 0; r < P; ++r) {
+      NS_CUDA(launch_decide(reinterpret_cast<DevState*>(w[r] + L.off_state), reinterpret_cast<JobParams*>(w[r] + L.off_jobs),
+                            ptr(r, L.off_res), L.n_tiles, ptr(r, L.off_tr) + (odd ? L.n : 0), L.n, lp, 1,
+                            reinterpret_cast<int*>(w[r] + L.off_active), st));
+      nl += 1;
+    }
+    if (j < max_steps && (s = products(odd, 1)) != NS_OK) return s;
+    NS_CUDA(cudaMemcpyAsync(&rg.slots[j % 16], w[0] + L.off_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+    NS_CUDA(cudaEventRecord(rg.ev[j % 16], st));
+  }
+  NS_CUDA(launch_copy_out(ptr(0, L.off_xa), ptr(0, L.off_xb), L.d, L.d_pad, reinterpret_cast<DevState*>(w[0] + L.off_state),
+                          R, ldr, 0, 1, st));
+  nl += 1;
+  std::vector<DevState> states(P);
+  for (int r = 0; r < P; ++r)
+    NS_CUDA(cudaMemcpyAsync(&states[r], w[r] + L.off_state, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+  NS_CUDA(cudaStreamSynchronize(st));
+  for (int r = 1; r < P; ++r)
+    if (memcmp(&states[r], &states[0], sizeof(DevState)) != 0)
+      return fail(NS_ERR_CUDA, "emulated ranks diverged (rank %d state differs from rank 0)", r);
+  out_state = states[0];
+  if (launches) *launches = nl;
+  return NS_OK;
+}
+
 void fill_result(const DevState& s, int launches, ns_result_t* out) {
   out->kernel_launches = launches;
   out->switch_step = s.sw_step;
@@ -1475,6 +1584,37 @@ ns_status_t ns_symm_product_shard(const double* A, const double* B, double* cons
   pp.n_tiles_total = L.n_tiles;
   NS_CUDA(launch_product(tA, tB, pp, 1, cs));
   NS_CUDA(cudaStreamSynchronize(cs));
+  return NS_OK;
+}
+
+size_t ns_workspace_bytes_sharded_emulated(int64_t d, int nranks) {
+  if (d < 1 || nranks < 1) return 0;
+  return align256(make_shard_layout(d, nranks, 0).total) * (size_t)nranks;
+}
+
+ns_status_t ns_reflector_sharded_emulated(int32_t nranks, const double* H, int64_t d, int64_t ldh, double s,
+                                          double alpha, int32_t k, int32_t max_steps, double tol, ns_tolmode_t tm,
+                                          double* R, int64_t ldr, void* ws, size_t ws_bytes, void* stream,
+                                          ns_result_t* out) {
+  g_last_error.clear();
+  ns_status_t st = check_common(d, max_steps, tol, tm, NS_PREC_FP64);
+  if (st != NS_OK) return st;
+  if (nranks < 1 || nranks > 64) return fail(NS_ERR_INVALID_ARG, "nranks must be in [1, 64]");
+  if (!H || !R || !ws || !out) return fail(NS_ERR_INVALID_ARG, "null pointer argument");
+  if (ldh < d || ldr < d) return fail(NS_ERR_INVALID_ARG, "leading dimensions must be >= d");
+  if (!std::isfinite(s)) return fail(NS_ERR_INVALID_ARG, "shift s must be finite");
+  if (!(alpha > 0.0) || !std::isfinite(alpha)) return fail(NS_ERR_INVALID_ARG, "alpha must be finite and > 0");
+  if (k < 0 || k > d) return fail(NS_ERR_INVALID_ARG, "k must lie in [0, d]");
+  if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(NS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+  const size_t stride = align256(make_shard_layout(d, nranks, 0).total);
+  if (ws_bytes < stride * (size_t)nranks)
+    return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, stride * (size_t)nranks);
+  DevState ds;
+  int nl = 0;
+  st = run_sharded_emulated(d, nranks, static_cast<uint8_t*>(ws), stride, H, ldh, JobParams{s, alpha, k, 0},
+                            max_steps, tol, tm, R, ldr, static_cast<cudaStream_t>(stream), ds, &nl);
+  if (st != NS_OK) return st;
+  fill_result(ds, nl, out);
   return NS_OK;
 }
 

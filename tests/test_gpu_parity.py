@@ -681,6 +681,31 @@ def test_peer_exchange_products(nsr, d, mode, P):
         assert torch.equal(C, ref)
 
 
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_sharded_emulated_ranks_match_single(nsr, P):
+    """The whole sharded run with P ranks emulated on one GPU (P workspace replicas, each rank's product
+    kernels storing into every replica, every replica deciding on its own): all replicas end in the
+    same state (the library checks this bit for bit) and R equals the single-GPU result bitwise
+    (d = 2048: both use 128x128 tiles)."""
+    p = workloads.cfg3_dense(d=2048, k=128)
+    Hg = torch.from_numpy(p.H).to(_dev())
+    Re, re_ = nsr.ns_reflector_sharded_emulated(P, Hg, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    Rd, rd = nsr.ns_reflector(Hg, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    assert torch.equal(Re, Rd)
+    for key in ("steps", "flags", "residual", "trace", "cert"):
+        assert re_[key] == rd[key], key
+
+
+def test_sharded_emulated_ragged_vs_oracle(nsr):
+    """Ragged d (not a tile multiple) with more ranks than some tile rows: parity with the oracle."""
+    p = workloads.cfg3_dense(d=1000, k=77)
+    Hg = torch.from_numpy(p.H).to(_dev())
+    R, res = nsr.ns_reflector_sharded_emulated(5, Hg, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    o = ons.ns_reflector(p.H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    assert res["steps"] == o["steps"] and res["cert"] == o["cert"] == 77
+    assert checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= TOL_R
+
+
 # ------------------------------------------------------------------ edge cases on every precision path
 @pytest.mark.parametrize("prec", [1, 2, 3])
 def test_edge_cases_other_precisions(nsr, prec):
