@@ -20,6 +20,7 @@
 // the decide kernel reduces in a fixed order (deterministic).
 #include <cmath>
 #include <cstdint>
+#include <type_traits>
 
 #include "ns_internal.h"
 #include "ns_ptx.cuh"
@@ -397,74 +398,136 @@ __global__ void __launch_bounds__(k64Threads, k64Stages == 2 ? 3 : 2)
   const int g = lane >> 2, t = lane & 3;
   const uint32_t off_h0 = static_cast<uint32_t>(((2 * t + 0) ^ g) << 4);
   const uint32_t off_h1 = static_cast<uint32_t>(((2 * t + 1) ^ g) << 4);
-  const uint32_t a_row = static_cast<uint32_t>((wm * 32 + g) * 128);
-  const uint32_t b_row = static_cast<uint32_t>((wn * 32 + g) * 128);
   const uint32_t sA_u32 = smem_u32(sA), sB_u32 = smem_u32(sB);
-  double acc[4][4][2];
-#pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+  const bool diag = (I == J);
   const int pf_kt = nst > 8 ? nst - 8 : 0;
-  for (int kt = 0; kt < nst; ++kt) {
-    const int s = kt % k64Stages;
-    if (MODE == 1 && kt == pf_kt) {           // X_j tile for the epilogue: ask L2 early
-      const double* Xt = p.Xold + (long long)job * p.job_stride + (long long)(I * k64Tile) * p.ld + J * k64Tile;
+  // K loop: ring bookkeeping around a per-warp compute step on stage s
+  auto mainloop = [&](auto&& compute) {
+    for (int kt = 0; kt < nst; ++kt) {
+      const int s = kt % k64Stages;
+      if (MODE == 1 && kt == pf_kt) {           // X_j tile for the epilogue: ask L2 early
+        const double* Xt = p.Xold + (long long)job * p.job_stride + (long long)(I * k64Tile) * p.ld + J * k64Tile;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int l = threadIdx.x * 4 + u;     // 512 lines of 64 B: row l >> 3 (0..63), 8-double chunk l & 7
-        prefetch_l2(Xt + (long long)(l >> 3) * p.ld + (l & 7) * 8);
+        for (int u = 0; u < 4; ++u) {
+          const int l = threadIdx.x * 4 + u;     // 512 lines of 64 B: row l >> 3 (0..63), 8-double chunk l & 7
+          prefetch_l2(Xt + (long long)(l >> 3) * p.ld + (l & 7) * 8);
+        }
       }
+      if (threadIdx.x == 0 && kt >= 1 && kt - 1 + k64Stages < nst) {
+        const int sp = (kt - 1) % k64Stages;
+        mbar_wait(&empty[sp], static_cast<uint32_t>((kt - 1) / k64Stages) & 1u);
+        issue(kt - 1 + k64Stages);
+      }
+      mbar_wait(&full[s], static_cast<uint32_t>(kt / k64Stages) & 1u);
+      compute(s);
+      // the slot is refilled by TMA (async proxy) once every warp has arrived: order this warp's generic-
+      // proxy reads of it before the release (without the fence, 3 CTAs/SM with a 2-stage ring produced
+      // nondeterministic results -- a refill overtaking the last LDS of the slot)
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
     }
-    if (threadIdx.x == 0 && kt >= 1 && kt - 1 + k64Stages < nst) {
-      const int sp = (kt - 1) % k64Stages;
-      mbar_wait(&empty[sp], static_cast<uint32_t>((kt - 1) / k64Stages) & 1u);
-      issue(kt - 1 + k64Stages);
+  };
+  constexpr int EP = k64Tile + 1;
+  double* S = reinterpret_cast<double*>(smem);   // [64][65] epilogue staging (reuses the ring)
+  if (!diag) {
+    const uint32_t a_row = static_cast<uint32_t>((wm * 32 + g) * 128);
+    const uint32_t b_row = static_cast<uint32_t>((wn * 32 + g) * 128);
+    double acc[4][4][2];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+    mainloop([&](int s) {
+#pragma unroll
+      for (int hh = 0; hh < 2 * kSPS; ++hh) {
+        const int h = hh & 1;
+        const uint32_t aS = sA_u32 + (s * kSPS + (hh >> 1)) * (k64Tile * kBK * 8) + a_row;
+        const uint32_t bS = sB_u32 + (s * kSPS + (hh >> 1)) * (k64Tile * kBK * 8) + b_row;
+        const uint32_t off = h ? off_h1 : off_h0;
+        double a[4][2], b[4][2];
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) lds128(bS + ni * 8 * 128 + off, b[ni][0], b[ni][1]);
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) lds128(aS + mi * 8 * 128 + off, a[mi][0], a[mi][1]);
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi][e], b[ni][e]);
+      }
+    });
+    __syncthreads();
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const int r = wm * 32 + mi * 8 + g, c = wn * 32 + ni * 8 + 2 * t;
+        S[r * EP + c] = acc[mi][ni][0];
+        S[r * EP + c + 1] = acc[mi][ni][1];
+      }
+  } else {
+    // Diagonal tile: only the 36 upper-triangle 8x8 blocks (rb <= cb) of the 8x8 block grid are needed
+    // (the epilogue reads r <= c and mirrors).  Warp W takes block rows W and 7 - W: (8 - W) + (W + 1)
+    // = 9 blocks for every warp, so the four SM sub-partitions stay balanced (the 32x32 warp quadrants
+    // would leave one warp idle and one at full load).  Batched d = 256: 17% fewer DMMAs per product.
+    auto diag_warp = [&](auto WC) {
+      constexpr int W = decltype(WC)::value;
+      constexpr int R0 = W, R1 = 7 - W, N0 = 8 - W, N1 = W + 1;
+      double c0[N0][2], c1[N1][2];
+#pragma unroll
+      for (int i = 0; i < N0; ++i) c0[i][0] = c0[i][1] = 0.0;
+#pragma unroll
+      for (int i = 0; i < N1; ++i) c1[i][0] = c1[i][1] = 0.0;
+      mainloop([&](int s) {
+#pragma unroll
+        for (int hh = 0; hh < 2 * kSPS; ++hh) {
+          const int h = hh & 1;
+          const uint32_t aS = sA_u32 + (s * kSPS + (hh >> 1)) * (k64Tile * kBK * 8) + g * 128;
+          const uint32_t bS = sB_u32 + (s * kSPS + (hh >> 1)) * (k64Tile * kBK * 8) + g * 128;
+          const uint32_t off = h ? off_h1 : off_h0;
+          double a0[2], a1[2], b[8][2];
+#pragma unroll
+          for (int cb = W; cb < 8; ++cb) lds128(bS + cb * 8 * 128 + off, b[cb][0], b[cb][1]);
+          lds128(aS + R0 * 8 * 128 + off, a0[0], a0[1]);
+          lds128(aS + R1 * 8 * 128 + off, a1[0], a1[1]);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+#pragma unroll
+            for (int i = 0; i < N0; ++i) dmma_8x8x4(c0[i][0], c0[i][1], a0[e], b[R0 + i][e]);
+#pragma unroll
+            for (int i = 0; i < N1; ++i) dmma_8x8x4(c1[i][0], c1[i][1], a1[e], b[R1 + i][e]);
+          }
+        }
+      });
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < N0; ++i) {
+        const int r = R0 * 8 + g, c = (R0 + i) * 8 + 2 * t;
+        S[r * EP + c] = c0[i][0];
+        S[r * EP + c + 1] = c0[i][1];
+      }
+#pragma unroll
+      for (int i = 0; i < N1; ++i) {
+        const int r = R1 * 8 + g, c = (R1 + i) * 8 + 2 * t;
+        S[r * EP + c] = c1[i][0];
+        S[r * EP + c + 1] = c1[i][1];
+      }
+    };
+    switch (warp) {
+      case 0: diag_warp(std::integral_constant<int, 0>{}); break;
+      case 1: diag_warp(std::integral_constant<int, 1>{}); break;
+      case 2: diag_warp(std::integral_constant<int, 2>{}); break;
+      default: diag_warp(std::integral_constant<int, 3>{}); break;
     }
-    mbar_wait(&full[s], static_cast<uint32_t>(kt / k64Stages) & 1u);
-#pragma unroll
-    for (int hh = 0; hh < 2 * kSPS; ++hh) {
-      const int h = hh & 1;
-      const uint32_t aS = sA_u32 + (s * kSPS + (hh >> 1)) * (k64Tile * kBK * 8) + a_row;
-      const uint32_t bS = sB_u32 + (s * kSPS + (hh >> 1)) * (k64Tile * kBK * 8) + b_row;
-      const uint32_t off = h ? off_h1 : off_h0;
-      double a[4][2], b[4][2];
-#pragma unroll
-      for (int ni = 0; ni < 4; ++ni) lds128(bS + ni * 8 * 128 + off, b[ni][0], b[ni][1]);
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi) lds128(aS + mi * 8 * 128 + off, a[mi][0], a[mi][1]);
-#pragma unroll
-      for (int e = 0; e < 2; ++e)
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi][e], b[ni][e]);
-    }
-    // the slot is refilled by TMA (async proxy) once every warp has arrived: order this warp's generic-
-    // proxy reads of it before the release (without the fence, 3 CTAs/SM with a 2-stage ring produced
-    // nondeterministic results -- a refill overtaking the last LDS of the slot)
-    fence_proxy_async();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
   }
   // ---------------- epilogue (ring reused as staging once every warp is past the loop) ----------------
-  __syncthreads();
-  constexpr int EP = k64Tile + 1;
-  double* S = reinterpret_cast<double*>(smem);   // [64][65]
-#pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
-      const int r = wm * 32 + mi * 8 + g, c = wn * 32 + ni * 8 + 2 * t;
-      S[r * EP + c] = acc[mi][ni][0];
-      S[r * EP + c + 1] = acc[mi][ni][1];
-    }
   __syncthreads();
   const int tid = threadIdx.x;
   const long long ld = p.ld;
   const long long base = (long long)job * p.job_stride;
   double* C = p.C + base;
-  const bool diag = (I == J);
   const int i0 = I * k64Tile, j0 = J * k64Tile;
   double part = 0.0;
   constexpr int NE = k64Tile * k64Tile;          // 4096 elements, 32 per thread
