@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(k64Threads, k64Stages == 2 ? 3 : 2)
   };
   constexpr int EP = k64Tile + 1;
   double* S = reinterpret_cast<double*>(smem);   // [64][65] epilogue staging (reuses the ring)
-  if (!diag) {
+  if (!diag || !p.diag_tri) {
     const uint32_t a_row = static_cast<uint32_t>((wm * 32 + g) * 128);
     const uint32_t b_row = static_cast<uint32_t>((wn * 32 + g) * 128);
     double acc[4][4][2];
@@ -718,9 +718,19 @@ cudaError_t launch_trace_partials(const double* X, int d, int d_pad, int batch, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_product64(const CUtensorMap& tmP, const CUtensorMap& tmQ, const ProdParams& p, int batch,
+static int diag_tri_env() {
+  static const int v = [] {
+    const char* e = getenv("NS_DIAG_TRI");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return v;
+}
+
+cudaError_t launch_product64(const CUtensorMap& tmP, const CUtensorMap& tmQ, const ProdParams& p_in, int batch,
                              cudaStream_t st) {
   static unsigned long long attr[2] = {0, 0};
+  ProdParams p = p_in;
+  p.diag_tri = diag_tri_env();
   dim3 grid(p.n_tiles, batch);
   if (p.mode == 0) {
     smem_attr(ns_product64_kernel<0>, k64SmemBytes, attr[0]);

@@ -110,6 +110,7 @@ struct ProdParams {
   double* const* dst_part = nullptr;
   int n_dst = 0;
   int gt_off = 0, gt_stride = 1, n_tiles_total = 0;
+  int diag_tri = 1;        // 64x64-tile kernel: diagonal tiles compute only their upper 8x8 blocks (NS_DIAG_TRI=0: full)
 };
 
 // ---------------- mixed path (tcgen05 BF16x3, ns_mixed.cu) ----------------
