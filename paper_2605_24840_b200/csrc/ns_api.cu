@@ -52,7 +52,7 @@ struct Layout {
   size_t off_xa = 0, off_xb = 0, off_y = 0, off_res = 0, off_tr = 0, off_tiles = 0, off_jobs = 0,
          off_state = 0, off_active = 0, off_px = 0, off_py = 0, off_full = 0, off_pxb = 0, off_ahat = 0,
          off_r = 0, off_p = 0, off_cgpart = 0, off_cgsc = 0, off_ozx = 0, off_ozy = 0, off_oex = 0, off_oey = 0,
-         off_ores = 0, off_otr = 0, off_otiles = 0, off_ptiles = 0, off_pfull = 0, total = 0;
+         off_ores = 0, off_otr = 0, off_otiles = 0, off_ptiles = 0, off_pfull = 0, off_jlist = 0, total = 0;
 };
 
 Layout make_layout(int64_t d, int64_t batch, bool mixed = false, bool ozaki = false, bool tf32 = false) {
@@ -75,6 +75,7 @@ Layout make_layout(int64_t d, int64_t batch, bool mixed = false, bool ozaki = fa
   L.off_jobs = o; o = align256(o + sizeof(JobParams) * (size_t)batch);
   L.off_state = o; o = align256(o + sizeof(DevState) * (size_t)batch);
   L.off_active = o; o = align256(o + 256);
+  L.off_jlist = o; o = align256(o + sizeof(int) * ((size_t)batch + 1));   // active-job list + its count
   L.off_full = o; o = align256(o + sizeof(int2) * (size_t)L.n * L.n);   // full tile list (dense products)
   L.mixed = mixed;
   if (ozaki) {
@@ -407,8 +408,18 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
   std::vector<int2> tl = make_tiles(nb);
   const int n_t = (int)tl.size();
   NS_CUDA(cudaMemcpyAsync(tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
-  auto product = [&](const CUtensorMap& a, const CUtensorMap& b, const ProdParams& pp) {
-    return t64 ? launch_product64(a, b, pp, batch, st) : launch_product(a, b, pp, batch, st);
+  // batched: CTA rows follow the compacted active-job list; the grid covers a host-side upper bound of
+  // its length (the newest completed n_active readback: the count only decreases)
+  int* jlist = reinterpret_cast<int*>(ws + L.off_jlist);
+  const bool compact = batch > 1;
+  int rows = batch;
+  auto product = [&](const CUtensorMap& a, const CUtensorMap& b, ProdParams pp) {
+    if (compact && rows < batch) {   // while every job may be active, rows map 1:1 (no list indirection)
+      pp.job_list = jlist;
+      pp.n_job_list = jlist + batch;
+    }
+    const int gy = std::max(rows, 1);
+    return t64 ? launch_product64(a, b, pp, gy, st) : launch_product(a, b, pp, gy, st);
   };
 
   CUtensorMap tmA, tmB, tmY;
@@ -418,10 +429,11 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
   if ((s = encode_map(&tmY, Y, L.d_pad, batch, tile_rows)) != NS_OK) return s;
 
   NS_CUDA(launch_zero_state(state, batch, n_active, st));
+  if (compact) NS_CUDA(launch_compact(state, batch, jlist, jlist + batch, st));
   NS_CUDA(launch_init(H, ldh, h_stride, Xa, djobs, L.d, L.d_pad, batch, st));
   if (t64) NS_CUDA(cudaMemsetAsync(trp, 0, sizeof(double) * nb * batch, st));
   NS_CUDA(launch_trace_partials(Xa, L.d, L.d_pad, batch, trp, st, nb));   // 128-block sums, stride nb
-  int nl = 3;
+  int nl = compact ? 4 : 3;
   Profiler& pf = prof();
   // event slots: 4 per step (square begin/end, update begin/end)
 
@@ -436,6 +448,13 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
       const int slot = (j - LA) % 16;
       NS_CUDA(cudaEventSynchronize(rg.ev[slot]));
       if (rg.slots[slot] == 0) break;
+      rows = std::min(rows, rg.slots[slot]);
+      if (compact)   // a newer readback may already be in: tighter bound, no wait
+        for (int q = j - 1; q > j - LA; --q)
+          if (cudaEventQuery(rg.ev[q % 16]) == cudaSuccess) {
+            rows = std::min(rows, rg.slots[q % 16]);
+            break;
+          }
     }
     const bool odd = (j & 1) != 0;
     double* Xc = odd ? Xb : Xa;
@@ -448,6 +467,10 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
     if (pf.on) NS_CUDA(cudaEventRecord(pf.get(4 * j + 1), st));
     NS_CUDA(launch_decide(state, djobs, res, n_t, trp, nb, lp, batch, n_active, st));
     nl += 2;
+    if (compact) {
+      NS_CUDA(launch_compact(state, batch, jlist, jlist + batch, st));
+      nl += 1;
+    }
     if (j < max_steps) {
       ProdParams up{tiles, n_t, L.d_pad / kBK, L.d, L.d_pad, job_stride, Xn, Xc, trp, state, 1, opt.ca, opt.cb};
       if (pf.on) NS_CUDA(cudaEventRecord(pf.get(4 * j + 2), st));

@@ -18,6 +18,7 @@
 // 128-bit LDS.  Epilogue: tile staged through shared memory, written row-major and
 // mirrored (bitwise-symmetric output), with per-tile residual / trace partials that
 // the decide kernel reduces in a fixed order (deterministic).
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <type_traits>
@@ -29,32 +30,38 @@ namespace nsr {
 
 // --------------------------------------------------------------------------------------
 // X_0 = (H - sI)/alpha from the UPPER triangle of H, zero-padded to d_pad.
-// 32x32 blocks; block (bi,bj) reads H's tile (min,max) and writes its own tile.
+// 64x64 blocks, 16 independent loads per thread in flight; block (bi,bj) reads H's tile (min,max)
+// and writes its own tile (transposed through shared memory below the diagonal).
 // --------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) ns_init_kernel(const double* __restrict__ H, long long ldh,
                                                       long long h_stride, double* __restrict__ X,
                                                       const JobParams* __restrict__ jobs, int d, int d_pad) {
-  __shared__ double t[32][33];
+  __shared__ double t[64][65];
   const int job = blockIdx.z;
   const int bi = blockIdx.y, bj = blockIdx.x;
   const double* Hj = H + (long long)job * h_stride;
   double* Xj = X + (long long)job * d_pad * (long long)d_pad;
   const double s = jobs[job].s, alpha = jobs[job].alpha;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4
   const int ri = min(bi, bj), rj = max(bi, bj);           // source tile in the upper triangle
-  for (int y = ty; y < 32; y += 8) {
-    const int gi = ri * 32 + y, gj = rj * 32 + tx;
-    t[y][tx] = (gi < d && gj < d && gi <= gj) ? Hj[(long long)gi * ldh + gj] : 0.0;
+  double v[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int gi = ri * 64 + ty + 4 * u, gj = rj * 64 + tx;
+    v[u] = (gi < d && gj < d && gi <= gj) ? Hj[(long long)gi * ldh + gj] : 0.0;
   }
+#pragma unroll
+  for (int u = 0; u < 16; ++u) t[ty + 4 * u][tx] = v[u];
   __syncthreads();
-  for (int y = ty; y < 32; y += 8) {
-    const int gi = bi * 32 + y, gj = bj * 32 + tx;
-    double v = 0.0;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int gi = bi * 64 + ty + 4 * u, gj = bj * 64 + tx;
+    double x = 0.0;
     if (gi < d && gj < d) {
-      const double h = (gi <= gj) ? t[gi - ri * 32][gj - rj * 32] : t[gj - ri * 32][gi - rj * 32];
-      v = (gi == gj) ? (h - s) / alpha : h / alpha;
+      const double h = (gi <= gj) ? t[gi - ri * 64][gj - rj * 64] : t[gj - ri * 64][gi - rj * 64];
+      x = (gi == gj) ? (h - s) / alpha : h / alpha;
     }
-    Xj[(long long)gi * d_pad + gj] = v;
+    Xj[(long long)gi * d_pad + gj] = x;
   }
 }
 
@@ -79,7 +86,11 @@ template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     ns_product_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
                       const ProdParams p) {
-  const int job = blockIdx.y;
+  int job = blockIdx.y;
+  if (p.job_list != nullptr) {                          // batched: compacted list of active jobs
+    if ((int)blockIdx.y >= *p.n_job_list) return;
+    job = p.job_list[blockIdx.y];
+  }
   if (p.state != nullptr && p.state[job].done) return;  // uniform per CTA
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -358,7 +369,11 @@ template <int MODE>
 __global__ void __launch_bounds__(k64Threads, k64Stages == 2 ? 3 : 2)
     ns_product64_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
                         const ProdParams p) {
-  const int job = blockIdx.y;
+  int job = blockIdx.y;
+  if (p.job_list != nullptr) {
+    if ((int)blockIdx.y >= *p.n_job_list) return;
+    job = p.job_list[blockIdx.y];
+  }
   if (p.state != nullptr && p.state[job].done) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -691,14 +706,56 @@ __global__ void ns_zero_state_kernel(DevState* state, int batch, int* n_active) 
 }
 
 // R = X_{steps}: buffer chosen on device from state.j (ping-pong parity).
+// R_job (d x d, leading dimension ldr) <- the returned iterate, 8 independent elements (or double2
+// pairs when rows are 16-B aligned) per thread in flight over the flattened d*d range.
+template <bool V2>
 __global__ void __launch_bounds__(256) ns_copy_out_kernel(const double* __restrict__ Xa, const double* __restrict__ Xb,
                                                           int d, int d_pad, const DevState* __restrict__ state,
                                                           double* __restrict__ R, long long ldr, long long r_stride) {
-  const int job = blockIdx.z;
+  const int job = blockIdx.y;
   const double* X = ((state[job].j & 1) ? Xb : Xa) + (long long)job * d_pad * d_pad;
-  const int i = blockIdx.y;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < d; c += gridDim.x * blockDim.x)
-    R[(long long)job * r_stride + (long long)i * ldr + c] = X[(long long)i * d_pad + c];
+  double* Rj = R + (long long)job * r_stride;
+  const int cols = V2 ? d / 2 : d;
+  const long long per = (long long)d * cols;
+  for (long long base = (long long)blockIdx.x * 2048; base < per; base += (long long)gridDim.x * 2048) {
+    if (V2) {
+      double2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const long long e = base + u * 256 + threadIdx.x;
+        if (e < per) {
+          const long long i = e / cols, c = e - i * cols;
+          v[u] = *reinterpret_cast<const double2*>(X + i * d_pad + 2 * c);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const long long e = base + u * 256 + threadIdx.x;
+        if (e < per) {
+          const long long i = e / cols, c = e - i * cols;
+          *reinterpret_cast<double2*>(Rj + i * ldr + 2 * c) = v[u];
+        }
+      }
+    } else {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const long long e = base + u * 256 + threadIdx.x;
+        if (e < per) {
+          const long long i = e / cols, c = e - i * cols;
+          v[u] = X[i * d_pad + c];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const long long e = base + u * 256 + threadIdx.x;
+        if (e < per) {
+          const long long i = e / cols, c = e - i * cols;
+          Rj[i * ldr + c] = v[u];
+        }
+      }
+    }
+  }
 }
 
 // --------------------------------------------------------------------------------------
@@ -706,7 +763,7 @@ __global__ void __launch_bounds__(256) ns_copy_out_kernel(const double* __restri
 // --------------------------------------------------------------------------------------
 cudaError_t launch_init(const double* H, long long ldh, long long h_stride, double* X, const JobParams* jobs,
                         int d, int d_pad, int batch, cudaStream_t st) {
-  dim3 grid(d_pad / 32, d_pad / 32, batch);
+  dim3 grid(d_pad / 64, d_pad / 64, batch);
   ns_init_kernel<<<grid, 256, 0, st>>>(H, ldh, h_stride, X, jobs, d, d_pad);
   return cudaGetLastError();
 }
@@ -769,9 +826,51 @@ cudaError_t launch_decide(DevState* state, const JobParams* jobs, const double* 
 
 cudaError_t launch_copy_out(const double* Xa, const double* Xb, int d, int d_pad, const DevState* state,
                             double* R, long long ldr, long long r_stride, int batch, cudaStream_t st) {
-  const int bx = (d + 255) / 256 < 8 ? (d + 255) / 256 : 8;
-  dim3 grid(bx, d, batch);
-  ns_copy_out_kernel<<<grid, 256, 0, st>>>(Xa, Xb, d, d_pad, state, R, ldr, r_stride);
+  const bool v2 = (d % 2 == 0) && (ldr % 2 == 0) && (r_stride % 2 == 0) && ((reinterpret_cast<uintptr_t>(R) & 15) == 0);
+  const long long per = (long long)d * (v2 ? d / 2 : d);
+  dim3 grid((unsigned)std::min<long long>((per + 2047) / 2048, 1 << 20), batch);
+  if (v2) ns_copy_out_kernel<true><<<grid, 256, 0, st>>>(Xa, Xb, d, d_pad, state, R, ldr, r_stride);
+  else ns_copy_out_kernel<false><<<grid, 256, 0, st>>>(Xa, Xb, d, d_pad, state, R, ldr, r_stride);
+  return cudaGetLastError();
+}
+
+// Stable compaction of the active jobs (batched loop): one CTA, 1024 jobs per pass, warp ballots + a
+// scan of the 32 warp counts.  The product kernels then launch only ~n_active CTA rows instead of the
+// whole batch (at the tail of configs[1] most rows would otherwise start and exit at once: ~86 us
+// per launch for 6144 x 10 empty CTAs).
+__global__ void __launch_bounds__(1024) ns_compact_kernel(const DevState* __restrict__ state, int batch,
+                                                          int* __restrict__ list, int* __restrict__ n_list) {
+  __shared__ int wsum[32];
+  __shared__ int carry;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) carry = 0;
+  for (int base = 0; base < batch; base += 1024) {
+    __syncthreads();
+    const int j = base + tid;
+    const bool a = j < batch && !state[j].done;
+    const unsigned m = __ballot_sync(0xffffffffu, a);
+    if (lane == 0) wsum[warp] = __popc(m);
+    __syncthreads();
+    if (warp == 0) {
+      int v = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+      }
+      wsum[lane] = v;                       // inclusive
+    }
+    __syncthreads();
+    if (a) list[carry + (warp ? wsum[warp - 1] : 0) + __popc(m & ((1u << lane) - 1u))] = j;
+    __syncthreads();
+    if (tid == 0) carry += wsum[31];
+  }
+  __syncthreads();
+  if (tid == 0) *n_list = carry;
+}
+
+cudaError_t launch_compact(const DevState* state, int batch, int* list, int* n_list, cudaStream_t st) {
+  ns_compact_kernel<<<1, 1024, 0, st>>>(state, batch, list, n_list);
   return cudaGetLastError();
 }
 

@@ -110,6 +110,9 @@ struct ProdParams {
   double* const* dst_part = nullptr;
   int n_dst = 0;
   int gt_off = 0, gt_stride = 1, n_tiles_total = 0;
+  // batched: CTA row blockIdx.y runs job job_list[blockIdx.y] (rows >= *n_job_list exit); nullptr = job blockIdx.y
+  const int* job_list = nullptr;
+  const int* n_job_list = nullptr;
   int diag_tri = 1;        // 64x64-tile kernel: diagonal tiles compute only their upper 8x8 blocks (NS_DIAG_TRI=0: full)
 };
 
@@ -259,5 +262,7 @@ cudaError_t launch_shard_sum(const double* v, int n, double* out, cudaStream_t s
 cudaError_t launch_copy_out(const double* Xa, const double* Xb, int d, int d_pad, const DevState* state,
                             double* R, long long ldr, long long r_stride, int batch, cudaStream_t st);
 cudaError_t launch_zero_state(DevState* state, int batch, int* n_active, cudaStream_t st);
+// list[0..*n_list) = the jobs with !state[job].done in ascending order (one CTA, stable)
+cudaError_t launch_compact(const DevState* state, int batch, int* list, int* n_list, cudaStream_t st);
 
 }  // namespace nsr

@@ -390,6 +390,28 @@ def test_sharded_cfg4_subproblem(nsr, comm1):
     assert o["steps"] == res["steps"] and checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= TOL_R
 
 
+def test_sharded_cfg4_full_size(nsr, comm1):
+    """configs[4] at its full size (d = 49152, k = 4096) on the sharded path as one GPU runs it (P = 1):
+    step count = scalar-recurrence prediction, certificate, sampled columns vs the closed-form
+    Householder reflector, R symmetric and an involution on a probe.  ~100 s."""
+    p = workloads.cfg4_sharded(form=False)
+    H = workloads.householder_form_fast(p.Vh, p.lam, device=_dev())
+    R, res = nsr.ns_reflector_sharded(comm1, H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    del H
+    steps_pred = scalar.predict_run((p.lam - p.s) / p.alpha, 100, 1e-10, True)[0]
+    assert res["steps"] == steps_pred and res["cert"] == 4096 and res["flags"] == ons.CONVERGED
+    cols = np.array([0, 4095, 4096, 30000, 49151])
+    Rc = closed_form.householder_reflector_columns(p.Vh, p.lam, 0.0, cols)
+    Rg = R[:, torch.as_tensor(cols, device=_dev())].cpu().numpy()
+    assert np.max(np.abs(Rg - Rc)) <= 1e-12
+    rows = R[torch.as_tensor(cols, device=_dev()), :].cpu().numpy()
+    assert np.array_equal(rows.T, Rg)                       # R bitwise symmetric on the sampled lines
+    g = torch.Generator(device=_dev()).manual_seed(3)
+    v = torch.randn(p.d, dtype=torch.float64, device=_dev(), generator=g)
+    assert float(torch.linalg.vector_norm(R @ (R @ v) - v) / torch.linalg.vector_norm(v)) <= 1e-10
+    assert abs(res["trace"] - (p.d - 2 * p.k)) <= 1e-5     # sum |x_i - sgn(x_i)| <= sqrt(d) ||X^2 - I||_F
+
+
 def test_small_path_batched(nsr):
     """d <= 96 runs the fused one-CTA-per-problem kernel; batched problems stop independently."""
     probs = []
