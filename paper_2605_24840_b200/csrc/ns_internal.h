@@ -216,10 +216,19 @@ cudaError_t launch_outer(const double* Q, int d, const int* k, const double* x0,
 constexpr int kOzSlices = 7;                           // balanced base-256 int8 digits per entry (54 bits)
 constexpr int kOzChunkKb = 256;                        // k-blocks (x64) per INT32 chunk: exact for any d
 constexpr int kOzMaxD = 65536;
-constexpr int kOzStages = 2;
+#ifndef NS_OZ_KH
+#define NS_OZ_KH 64
+#endif
+// K bytes per ring stage: 64 (64-byte swizzle, 2 stages of 84 KB; default) or 32 (one UMMA K step,
+// 32-byte swizzle, 4 stages of 42 KB, -DNS_OZ_KH=32).  The operand feed (L2 -> SMEM over TMA) and the
+// tensor pipe take about equally long per k-block here (32 ms each for a d = 16384 product when
+// measured alone, 39 ms together), so finer stages were tried for a better overlap: measured A/B they
+// are 12% slower (twice the TMA requests of half the width).
+constexpr int kOzKH = NS_OZ_KH;
+constexpr int kOzStages = kOzKH == 32 ? 4 : 2;
 constexpr int kOzThreads = 320;                        // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
-constexpr int kOzSlabA = kTile * 64;                   // 128 rows x 64 int8
-constexpr int kOzSlabB = 64 * 64;                      // 64 rows x 64 int8
+constexpr int kOzSlabA = kTile * kOzKH;                // 128 rows x kOzKH int8
+constexpr int kOzSlabB = 64 * kOzKH;                   // 64 rows x kOzKH int8
 constexpr int kOzStageBytes = kOzSlices * (kOzSlabA + kOzSlabB);
 constexpr int kOzSmemBytes = kOzStages * kOzStageBytes + 1024 + 256 + 8 * 32 * 17 * 8;   // + epilogue staging
 
@@ -241,6 +250,7 @@ struct OzParams {
   double cb = -0.5;
   int kb0 = 0;             // first k-block of this launch (K segments, see launch_ozaki_product)
   int pm = 0;              // 0 whole K; K segments: 1 first (C = raw sums), 2 middle (C += raw), 3 last (C + raw -> epilogue)
+  int dbg = 0;             // experiments only (NS_OZ_DBG): 1 = stream operands without issuing the UMMAs
 };
 constexpr int kOzBadRow = 1 << 20;   // row exponent marking a non-finite row (its products become NaN)
 constexpr int kOzSegKb = 256;   // k-blocks per K segment (K = 16384): one launch per segment for larger d

@@ -146,9 +146,11 @@ __device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t adesc, uint64_
       : "memory");
 }
 
-// K-major operand, 64-byte swizzle: rows of 64 B, 8-row atoms 512 B apart (SBO), version 1.
+// K-major operand, kOzKH-byte swizzle: rows of kOzKH bytes, 8-row atoms 8 * kOzKH bytes apart (SBO),
+// version 1; layout type 4 = 64-byte swizzle, 6 = 32-byte swizzle.
 __device__ __forceinline__ uint64_t sdesc_k64(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFFu) | (1ull << 16) | (32ull << 32) | (1ull << 46) | (4ull << 61);
+  constexpr uint64_t sbo = (8ull * kOzKH) >> 4, lay = kOzKH == 32 ? 6ull : 4ull;
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | (1ull << 16) | (sbo << 32) | (1ull << 46) | (lay << 61);
 }
 
 template <int MODE, bool MC>
@@ -203,12 +205,14 @@ __global__ void __launch_bounds__(kOzThreads, 1)
     if (lane == 0) {
       tma_prefetch_desc(&tmA);
       tma_prefetch_desc(&tmB);
-      uint32_t kbg = 0;                    // k-blocks issued by this CTA so far (ring position)
+      uint32_t kbg = 0;                    // stages issued by this CTA so far (ring position)
+      constexpr int kSub = 64 / kOzKH;     // stages per 64-wide k-block
       for (int item = item0; item < n_items; item += istride) {
         const int job = item / p.n_tiles;
         if (p.state != nullptr && p.state[job].done) continue;
         const int2 tile = tile_of(item, job);
-        for (int kb = 0; kb < p.nkb; ++kb, ++kbg) {
+        for (int kb = 0; kb < p.nkb * kSub; ++kb, ++kbg) {
+          const int kx = p.kb0 * 64 + kb * kOzKH;   // k coordinate (bytes) of this stage
           const int s = kbg % kOzStages;
           if (kbg >= kOzStages) mbar_wait(&empty[s], ((kbg / kOzStages) & 1u) ^ 1u);
           uint8_t* st = smem + s * kOzStageBytes;
@@ -217,16 +221,16 @@ __global__ void __launch_bounds__(kOzThreads, 1)
 #pragma unroll
             for (int q = 0; q < kOzSlices; ++q)
               if ((q & 1) == rank)
-                tma_load_3d_mc(st + q * kOzSlabA, &tmA, (p.kb0 + kb) * 64, tile.x * kTile, job * kOzSlices + q,
+                tma_load_3d_mc(st + q * kOzSlabA, &tmA, kx, tile.x * kTile, job * kOzSlices + q,
                                &full[s], 0x3);
           } else {
 #pragma unroll
             for (int q = 0; q < kOzSlices; ++q)
-              tma_load_3d(st + q * kOzSlabA, &tmA, (p.kb0 + kb) * 64, tile.x * kTile, job * kOzSlices + q, &full[s]);
+              tma_load_3d(st + q * kOzSlabA, &tmA, kx, tile.x * kTile, job * kOzSlices + q, &full[s]);
           }
 #pragma unroll
           for (int q = 0; q < kOzSlices; ++q)
-            tma_load_3d(st + kOzSlices * kOzSlabA + q * kOzSlabB, &tmB, (p.kb0 + kb) * 64, tile.y * 64, job * kOzSlices + q,
+            tma_load_3d(st + kOzSlices * kOzSlabA + q * kOzSlabB, &tmB, kx, tile.y * 64, job * kOzSlices + q,
                         &full[s]);
         }
       }
@@ -241,13 +245,15 @@ __global__ void __launch_bounds__(kOzThreads, 1)
       for (int c = 0; c < n_chunks; ++c, ++cg) {
         if (cg >= 1) mbar_wait(tempty, (cg - 1) & 1u);   // accumulators folded by the epilogue
         tc_fence_after();
-        const int kb0 = c * kOzChunkKb, kb1 = min(p.nkb, kb0 + kOzChunkKb);
+        constexpr int kSub = 64 / kOzKH;
+        const int kb0 = c * kOzChunkKb * kSub, kb1 = min(p.nkb * kSub, kb0 + kOzChunkKb * kSub);
         for (int kb = kb0; kb < kb1; ++kb, ++kbg) {
           const int s = kbg % kOzStages;
           mbar_wait(&full[s], (kbg / kOzStages) & 1u);
           tc_fence_after();
           if (elect_one()) {
             const uint32_t a0 = smem_u32(smem + s * kOzStageBytes);
+            if (!p.dbg) {
             const uint32_t b0 = a0 + kOzSlices * kOzSlabA;
             const uint32_t first = (kb == kb0) ? 0u : 1u;
             // Digit pairs (sa, sb), sb = sb0 .. sb0+n-1, share the A digit: the B digit slabs are stored
@@ -255,7 +261,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
             // N = 64 n whose output columns are exactly the group accumulators sa+sb0 .. sa+sb0+n-1.
             // 28 pairs become 10 UMMAs (N = 64..256) per K=32 half, with the same MACs.
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < kOzKH / 32; ++h) {
 #pragma unroll
               for (int sa = 0; sa < kOzSlices; ++sa) {
 #pragma unroll
@@ -266,6 +272,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
                           sdesc_k64(b0 + sb0 * kOzSlabB + 32 * h), idesc, (sa == 0 && h == 0) ? first : 1u);
                 }
               }
+            }
             }
             if (MC) umma_commit_mc(&empty[s], 0x3);   // release the slot in both CTAs
             else umma_commit(&empty[s]);
@@ -433,6 +440,15 @@ cudaError_t launch_ozaki_product(const CUtensorMap& tmA, const CUtensorMap& tmB,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     if (n_sm <= 0) n_sm = 148;
+  }
+  static const int dbg = [] {
+    const char* e = getenv("NS_OZ_DBG");
+    return e ? atoi(e) : 0;
+  }();
+  if (dbg != p.dbg) {
+    OzParams q = p;
+    q.dbg = dbg;
+    return launch_ozaki_product(tmA, tmB, q, batch, st);
   }
   if (p.pm == 0 && p.nkb > kOzSegKb) {
     // K segments of kOzSegKb k-blocks, one launch each: every segment streams a K range that the
