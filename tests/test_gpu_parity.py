@@ -213,6 +213,25 @@ def test_deterministic_batched_full_occupancy(nsr):
         assert torch.equal(R1, R2) and o1 == o2
 
 
+def test_batched_compaction_matches_single_runs(nsr):
+    """Problems that stop at very different steps (the batched loop compacts the active jobs and bounds
+    the product grids by the count): every sampled problem's R, steps and residual equal the same
+    problem run alone, bitwise (the per-tile arithmetic does not depend on the CTA that runs it)."""
+    probs = workloads.cfg1_batched(seed=3, n_matrices=2048, count=96)
+    H = torch.from_numpy(np.stack([p.H for p in probs])).to(_dev())
+    R, outs = nsr.ns_reflector_batched(H, [p.s for p in probs], [p.alpha for p in probs], [p.k for p in probs],
+                                       100, 1e-12)
+    steps = np.array([o["steps"] for o in outs])
+    assert steps.max() - steps.min() >= 6
+    pick = sorted({int(np.argmin(steps)), int(np.argmax(steps)), 0, 17, 50, len(probs) - 1})
+    for i in pick:
+        p = probs[i]
+        R1, o1 = nsr.ns_reflector_batched(H[i:i + 1].clone(), [p.s], [p.alpha], [p.k], 100, 1e-12)
+        assert torch.equal(R1[0], R[i]), i
+        for key in ("steps", "flags", "residual", "trace", "cert"):
+            assert o1[0][key] == outs[i][key], (i, key)
+
+
 # ------------------------------------------------------------------ full size (bench launch configuration)
 def test_cfg3_full_size_sampled(nsr):
     """configs[3] at d=16384 exactly as bench.py runs it: steps == scalar-recurrence prediction,
