@@ -301,6 +301,26 @@ HostRing& ring() {
   return r;
 }
 
+// Side stream + events of the speculative result copy (host entry, one per thread)
+struct SpecCtx {
+  cudaStream_t side = nullptr;
+  cudaEvent_t upd = nullptr, cp[2] = {nullptr, nullptr}, end = nullptr;
+  bool ok = false;
+};
+
+SpecCtx& spec_ctx() {
+  static thread_local SpecCtx c;
+  if (!c.ok) {
+    if (cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking) != cudaSuccess) return c;
+    cudaEventCreateWithFlags(&c.upd, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c.cp[0], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c.cp[1], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c.end, cudaEventDisableTiming);
+    c.ok = true;
+  }
+  return c;
+}
+
 ns_status_t check_common(int64_t d, int32_t max_steps, double tol, ns_tolmode_t tm, ns_precision_t prec) {
   if (d < 1 || d > 65536) return fail(NS_ERR_INVALID_ARG, "d must be in [1, 65536], got %lld", (long long)d);
   if (max_steps < 0) return fail(NS_ERR_INVALID_ARG, "max_steps must be >= 0");
@@ -319,6 +339,11 @@ struct Opts {
   int lookahead = 0;
   int polish = 0;                 // mixed path: 0 = FP64 DMMA re-anchor / polish, 1 = Ozaki INT8
   double ca = 1.5, cb = -0.5;
+  // host entry: the caller's pinned R (device-accessible address) for the speculative result copy;
+  // run_loop sets *spec_hit when R already holds the returned iterate
+  double* spec_R = nullptr;
+  long long spec_ldr = 0;
+  bool* spec_hit = nullptr;
 };
 
 Opts to_opts(const ns_options_t* o) {
@@ -440,6 +465,17 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
 
   LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0, -1, 0};
   const long long job_stride = (long long)L.d_pad * L.d_pad;
+  // Speculative result copy (host entry, one problem): after update j a side-stream kernel copies
+  // X_{j+1} to the caller's pinned R if the decide of step j predicted it final (DevState.spec), so the
+  // PCIe transfer of the result hides behind the square product that confirms it.  Update j + 2 (which
+  // overwrites X_{j+1}'s buffer) waits for that copy.
+  SpecCtx* sc = nullptr;
+  if (opt.spec_R != nullptr && opt.spec_hit != nullptr && batch == 1 && L.d % 2 == 0 && opt.spec_ldr % 2 == 0 &&
+      (reinterpret_cast<uintptr_t>(opt.spec_R) & 15) == 0) {
+    SpecCtx& c = spec_ctx();
+    if (c.ok) sc = &c;
+  }
+  int spec_last = 0;                 // largest jn whose copy kernel was enqueued
   // look-ahead: how many steps may be in flight before the host checks the counter
   const double step_flops = 2.0 * (double)L.n_tiles * kTile * kTile * (double)L.d_pad * batch;
   const int LA = step_flops > 2e10 ? 2 : 8;
@@ -474,10 +510,19 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
     }
     if (j < max_steps) {
       ProdParams up{tiles, n_t, L.d_pad / kBK, L.d, L.d_pad, job_stride, Xn, Xc, trp, state, 1, opt.ca, opt.cb};
+      if (sc && j >= 2) NS_CUDA(cudaStreamWaitEvent(st, sc->cp[(j - 1) & 1], 0));   // copy of X_{j-1} done
       if (pf.on) NS_CUDA(cudaEventRecord(pf.get(4 * j + 2), st));
       NS_CUDA(product(tmC, tmY, up));
       if (pf.on) NS_CUDA(cudaEventRecord(pf.get(4 * j + 3), st));
       nl += 1;
+      if (sc) {
+        NS_CUDA(cudaEventRecord(sc->upd, st));
+        NS_CUDA(cudaStreamWaitEvent(sc->side, sc->upd, 0));
+        NS_CUDA(launch_spec_copy(state, j + 1, Xn, L.d, L.d_pad, opt.spec_R, opt.spec_ldr, sc->side));
+        NS_CUDA(cudaEventRecord(sc->cp[(j + 1) & 1], sc->side));
+        spec_last = j + 1;
+        nl += 1;
+      }
     }
     const int slot = j % 16;
     NS_CUDA(cudaMemcpyAsync(&rg.slots[slot], n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -485,9 +530,15 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
   }
   NS_CUDA(launch_copy_out(Xa, Xb, L.d, L.d_pad, state, R, ldr, r_stride, batch, st));
   nl += 1;
+  if (sc) {
+    NS_CUDA(cudaEventRecord(sc->end, sc->side));
+    NS_CUDA(cudaStreamWaitEvent(st, sc->end, 0));
+  }
   states.resize(batch);
   NS_CUDA(cudaMemcpyAsync(states.data(), state, sizeof(DevState) * batch, cudaMemcpyDeviceToHost, st));
   NS_CUDA(cudaStreamSynchronize(st));
+  if (sc)   // R already holds X_{j} iff the copy kernel for jn = j ran (spec == j at the end)
+    *opt.spec_hit = states[0].done && states[0].j >= 1 && states[0].spec == states[0].j && states[0].j <= spec_last;
   if (launches) *launches = nl;
   if (pf.on) {
     // launches that did work: squares j = 0..max_j, updates j = 0..max_j-1 (max over jobs)
@@ -1386,8 +1437,31 @@ ns_status_t ns_reflector_host(const double* H_host, int64_t d, int64_t ldh, doub
     st = run_mixed(L, w, stage, d, jobs[0], max_steps, tol, tm, stage, d, cs, Opts{}, states[0], &nl, tf32);
   else if (ozaki)
     st = run_ozaki(L, w, stage, d, jobs[0], max_steps, tol, tm, stage, d, cs, Opts{}, states[0], &nl);
-  else
-    st = run_loop(L, w, stage, d, 0, jobs, max_steps, tol, tm, stage, d, 0, cs, states, &nl);
+  else {
+    // FP64 path: if R_host is pinned (device-accessible), the result may be copied speculatively
+    // behind the last square product (run_loop); otherwise one D2H copy after the loop
+    Opts o;
+    bool hit = false;
+    cudaPointerAttributes pa{};
+    static const bool spec_on = [] {
+      const char* e = getenv("NS_SPEC_COPY");   // 0: always copy R after the loop (A/B knob)
+      return !(e && e[0] == '0');
+    }();
+    if (spec_on && cudaPointerGetAttributes(&pa, R_host) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+        pa.devicePointer != nullptr) {
+      o.spec_R = static_cast<double*>(pa.devicePointer);
+      o.spec_ldr = ldr;
+      o.spec_hit = &hit;
+    } else {
+      (void)cudaGetLastError();   // pageable memory: clear the query's error state
+    }
+    st = run_loop(L, w, stage, d, 0, jobs, max_steps, tol, tm, stage, d, 0, cs, states, &nl, o);
+    if (st != NS_OK) return st;
+    if (hit) {
+      fill_result(states[0], nl, out);
+      return NS_OK;
+    }
+  }
   if (st != NS_OK) return st;
   NS_CUDA(cudaMemcpy2DAsync(R_host, (size_t)ldr * 8, stage, (size_t)d * 8, (size_t)d * 8, (size_t)d,
                             cudaMemcpyDeviceToHost, cs));

@@ -41,7 +41,7 @@ struct DevState {
   int64_t cert;       // round((d - tr)/2)
   double sw_residual; // mixed path: low-precision residual at the switch
   int32_t sw_step;    // mixed path: j at the switch (-1 = none)
-  int32_t pad1;
+  int32_t spec;       // index j+1 of the iterate the decide at step j predicts to be final (0 = none)
 };
 
 // Per-problem scalar inputs (device copy).
@@ -272,6 +272,10 @@ cudaError_t launch_shard_sum(const double* v, int n, double* out, cudaStream_t s
 cudaError_t launch_copy_out(const double* Xa, const double* Xb, int d, int d_pad, const DevState* state,
                             double* R, long long ldr, long long r_stride, int batch, cudaStream_t st);
 cudaError_t launch_zero_state(DevState* state, int batch, int* n_active, cudaStream_t st);
+// If state->spec == jn: copy X (d x d inside d_pad) to R (device-accessible pinned host memory, leading
+// dimension ldr) -- the speculative result copy of the host entry (ns_api.cu run_loop)
+cudaError_t launch_spec_copy(const DevState* state, int jn, const double* X, int d, int d_pad, double* R,
+                             long long ldr, cudaStream_t st);
 // list[0..*n_list) = the jobs with !state[job].done in ascending order (one CTA, stable)
 cudaError_t launch_compact(const DevState* state, int batch, int* list, int* n_list, cudaStream_t st);
 

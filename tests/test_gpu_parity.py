@@ -192,6 +192,26 @@ def test_host_entry_matches_device(nsr):
     assert np.array_equal(Rh.numpy(), Rd.cpu().numpy()) and rh == rd
 
 
+@pytest.mark.parametrize("case", ["tol", "fixed", "zero_steps", "odd_d", "nan"])
+def test_host_entry_pinned_speculative_copy(nsr, case):
+    """Pinned host buffers: the FP64 loop copies the iterate its decide predicts final straight to R
+    behind the confirming square (DevState.spec); R, steps and residual equal the device entry's bitwise,
+    also where the prediction has nothing to do (no update, odd d: copy disabled, non-finite input)."""
+    d = 1001 if case == "odd_d" else 1024
+    p = workloads.cfg3_dense(d=d, k=64)
+    H = p.H.copy()
+    if case == "nan":
+        H[3, 5] = H[5, 3] = np.nan
+    steps, tol = {"fixed": (9, 0.0), "zero_steps": (0, p.tol)}.get(case, (p.max_steps, p.tol))
+    Hp = torch.from_numpy(H).pin_memory()
+    Rp = torch.full((d, d), float("nan"), dtype=torch.float64).pin_memory()
+    Rh, rh = nsr.ns_reflector_host(Hp, p.s, p.alpha, p.k, steps, tol, p.tol_mode, R=Rp)
+    Rd, rd = nsr.ns_reflector(torch.from_numpy(H).to(_dev()), p.s, p.alpha, p.k, steps, tol, p.tol_mode)
+    assert torch.equal(Rh, Rd.cpu()) or (case == "nan" and rh["flags"] & ons.NONFINITE)
+    for key in ("steps", "flags", "residual", "trace", "cert"):
+        assert rh[key] == rd[key] or (rh[key] != rh[key] and rd[key] != rd[key]), key
+
+
 def test_deterministic(nsr):
     p = workloads.cfg3_dense(d=768, k=48)
     Hg = torch.from_numpy(p.H).to(_dev())
