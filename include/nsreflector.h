@@ -161,7 +161,11 @@ ns_status_t ns_reflector_ex(const double* H, int64_t d, int64_t ldh, double s, d
  * ns_reflector_host — same computation with HOST H and R (end-to-end entry point):
  * copies H (host, ldh) to the device workspace, runs ns_reflector, copies R back to
  * host memory (ldr).  Pinned host buffers give full PCIe bandwidth; pageable works.
- * The workspace must hold ns_workspace_bytes_host(d, prec) bytes.
+ * FP64 path with pinned R, even d and even ldr: the device may write R during the call
+ * (the iterate its stop rule predicts final is streamed to R behind the confirming
+ * square product; if the prediction fails R is simply overwritten by the returned
+ * iterate) -- R must not be read or reused by the caller before the call returns.
+ * Set NS_SPEC_COPY=0 to disable.  The workspace must hold ns_workspace_bytes_host(d, prec) bytes.
  */
 size_t ns_workspace_bytes_host(int64_t d, ns_precision_t prec);
 ns_status_t ns_reflector_host(const double* H_host, int64_t d, int64_t ldh, double s, double alpha,
