@@ -11,6 +11,8 @@ C3; 12 NS updates = 25 symmetric products).  value = algorithmic TFLOP/s =
 
 N > 1 (torchrun): configs[3] does not shard ("replicas only"), so
 every rank computes its own reflector; value = all ranks' flops / max-over-ranks time.
+--sharded (opt-in): ONE reflector sharded over the N ranks (ns_reflector_sharded, exchange fused
+into the product epilogue over CUDA-IPC peer memory), "scaling": "strong"; --d 49152 = configs[4].
 --impl reference times the CPU oracle (oracle/ns.py) on a bounded sample of the same
 workload (one NS step per bench step) on the host cores; rank 0 only.
 """
@@ -50,11 +52,18 @@ def parse():
     ap.add_argument("--d", type=int, default=16384)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="strong scaling: ONE reflector sharded over all ranks (ns_reflector_sharded, peer-memory "
+                         "exchange) instead of one replica per rank; with --d 49152 this is configs[4]")
     return ap.parse_args()
 
 
 def workload(args):
     import workloads
+    if args.d == 49152:
+        p = workloads.cfg4_sharded(form=False)
+        return p, ("configs[4]: d=49152 k=4096 Q=32 Householders, lambda in [-1,-0.02]u[0.02,1], s=0, alpha=1.05, FP64, "
+                   "run-to-tol ||X^2-I||_F/sqrt(d)<1e-10")
     k = 1024 if args.d == 16384 else max(1, args.d // 16)
     p = workloads.cfg3_dense(d=args.d, k=k, form=False, mode=args.mode)
     desc = (f"configs[3]: d={p.d} k={p.k} Q=64 Householders, lambda in [-1,-0.05]u[0.05,1], s=0, alpha=1.05, FP64, "
@@ -182,9 +191,22 @@ def run_ours(args):
     prec = {"fp64": nsr.NS_PREC_FP64, "mixed": nsr.NS_PREC_MIXED_BF16X3, "ozaki": nsr.NS_PREC_FP64_OZAKI}[args.prec]
     if prec != nsr.NS_PREC_FP64:
         wsbuf = nsr.alloc_workspace(nsr.ns_workspace_bytes(d, prec), dev)
+    comm = None
+    if args.sharded:
+        if prec != nsr.NS_PREC_FP64:
+            raise SystemExit("--sharded runs the FP64 path")
+        uid = [nsr.ns_comm_get_unique_id() if rank == 0 else None]
+        if pg:
+            pg.broadcast_object_list(uid, src=0)
+        comm = nsr.ns_comm_init(rank, ws, uid[0])
+        del wsbuf
+        wsbuf = nsr.alloc_workspace(nsr.ns_workspace_bytes_sharded(d, ws), dev)
 
     def call(pr=None, options=None):
         pr = prec if pr is None else pr
+        if comm is not None and pr == nsr.NS_PREC_FP64 and options is None:
+            return nsr.ns_reflector_sharded(comm, H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode, R=R,
+                                            ws=wsbuf, stream=stream)
         return nsr.ns_reflector(H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode, R=R, ws=wsbuf, stream=stream,
                                 prec=pr, options=options)
 
@@ -221,7 +243,8 @@ def run_ours(args):
         pg.barrier()
     steps_ns = results[-1]["steps"]
     flops_call = (2 * steps_ns + 1) * float(d) ** 3
-    value = ws * args.steps * flops_call / (ms * 1e-3) / 1e12
+    n_refl = 1 if args.sharded else ws          # reflectors computed per bench step by all ranks together
+    value = n_refl * args.steps * flops_call / (ms * 1e-3) / 1e12
     launches = int(sum(r["launches"] for r in results))
 
     # ---- roofline of the dominant kernel (the symmetric product): algorithmic d^3 flops per launch
@@ -245,7 +268,7 @@ def run_ours(args):
 
     # ---- end to end through the public host-buffer entry (H2D + D2H inside the timed region)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not args.sharded:
         Hh = H.cpu().pin_memory()
         Rh = torch.empty((d, d), dtype=torch.float64).pin_memory()
         wsh = wsbuf
@@ -295,7 +318,7 @@ def run_ours(args):
                 "speedup_vs_fp64": (ms / args.steps) / mms, "launches": rm["launches"]}
 
     mixed_oz = None
-    if args.prec == "fp64" and not args.no_mixed:
+    if args.prec == "fp64" and not args.no_mixed and not args.sharded:
         mixed = secondary(nsr.NS_PREC_MIXED_BF16X3)
         # the same mixed path with its re-anchor products and polishing steps on the Ozaki INT8 products
         mixed_oz = secondary(nsr.NS_PREC_MIXED_BF16X3, nsr.ns_options(polish=1))
@@ -303,7 +326,7 @@ def run_ours(args):
             ozaki = secondary(nsr.NS_PREC_FP64_OZAKI)
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.sharded:
         from oracle import ns as ons
         Hc = H.cpu().numpy()
         t, threads = ons.timed_ns_steps(Hc, p.s, p.alpha, 1)
@@ -314,19 +337,24 @@ def run_ours(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if args.sharded else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "d": d, "k": p.k, "ns_steps": steps_ns, "products": 2 * steps_ns + 1,
                        "algorithmic_flops_per_reflector": flops_call, "l2": "inputs larger than L2 (3 x 2 GiB FP64 "
-                       "matrices per step vs 126 MB L2)", "parallelism": f"replicas x{ws}" if ws > 1 else "single",
+                       "matrices per step vs 126 MB L2)",
+                       "parallelism": (f"sharded x{ws} (peer-memory exchange)" if args.sharded
+                                       else (f"replicas x{ws}" if ws > 1 else "single")),
                        "frac_of_fp64_peak": value / ws / FP64_PEAK_TFLOPS},
-            "time_to_R_ms": ms / args.steps, "reflectors_per_s": ws * args.steps / (ms * 1e-3),
+            "time_to_R_ms": ms / args.steps, "reflectors_per_s": n_refl * args.steps / (ms * 1e-3),
             "result": {"steps": steps_ns, "cert": results[-1]["cert"], "flags": results[-1]["flags"],
                        "residual": results[-1]["residual"]},
             "gpu_launches": launches, "clocks": clocks, "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
             "mixed_mode": mixed, "mixed_ozaki_polish_mode": mixed_oz, "ozaki_mode": ozaki, "precision": args.prec,
         }
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        nsr.ns_comm_destroy(comm)
     if pg:
         pg.destroy_process_group()
     return 0
