@@ -24,6 +24,10 @@
 #include <type_traits>
 
 #include "ns_internal.h"
+
+#ifndef NS_K64_ROT0
+#define NS_K64_ROT0 0   // 1: square launches rotate K the same way (measured: no gain, 3.53 vs 3.51 ms at cfg1)
+#endif
 #include "ns_ptx.cuh"
 
 namespace nsr {
@@ -395,14 +399,27 @@ __global__ void __launch_bounds__(k64Threads, k64Stages == 2 ? 3 : 2)
   }
   __syncthreads();
   const int nst = p.nk / kSPS;
+  // MODE 1 walks K starting after the tile's own column block J (stage units 2J, 2J+1 of 32 columns
+  // come last), so when the loop ends the ring still holds X_j[I rows][J columns] -- the tile the
+  // update epilogue needs -- and no global re-read of X_j is required.
+  const int koff = (MODE == 1 || NS_K64_ROT0) ? (2 * J + 2) % nst : 0;
   auto issue = [&](int kt) {
     const int s = kt % k64Stages;
+    const int kb = (kt + koff) % nst;
     mbar_arrive_expect_tx(&full[s], k64StageBytes);
 #pragma unroll
     for (int u = 0; u < kSPS; ++u) {
-      tma_load_3d(sA + (s * kSPS + u) * k64Tile * kBK, &tmP, (kt * kSPS + u) * kBK, I * k64Tile, job, &full[s]);
-      tma_load_3d(sB + (s * kSPS + u) * k64Tile * kBK, &tmQ, (kt * kSPS + u) * kBK, J * k64Tile, job, &full[s]);
+      tma_load_3d(sA + (s * kSPS + u) * k64Tile * kBK, &tmP, (kb * kSPS + u) * kBK, I * k64Tile, job, &full[s]);
+      tma_load_3d(sB + (s * kSPS + u) * k64Tile * kBK, &tmQ, (kb * kSPS + u) * kBK, J * k64Tile, job, &full[s]);
     }
+  };
+  // X_j(r, c..c+1) of this tile (c even) from the ring after the K loop: columns [0, 32) sit in the slot
+  // of stage nst-2, [32, 64) in that of nst-1; 128-B swizzle (16-B chunk q of row r at q ^ (r & 7))
+  auto x_ring = [&](int r, int c) -> double2 {
+    const int slot = (c < 32) ? (nst - 2) % k64Stages : (nst - 1) % k64Stages;
+    const int cs = c & 31;
+    const double* slab = sA + (slot * kSPS + (cs >> 4)) * (k64Tile * kBK);
+    return *reinterpret_cast<const double2*>(slab + r * kBK + ((((cs & 15) >> 1) ^ (r & 7)) << 1));
   };
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmP);
@@ -415,19 +432,10 @@ __global__ void __launch_bounds__(k64Threads, k64Stages == 2 ? 3 : 2)
   const uint32_t off_h1 = static_cast<uint32_t>(((2 * t + 1) ^ g) << 4);
   const uint32_t sA_u32 = smem_u32(sA), sB_u32 = smem_u32(sB);
   const bool diag = (I == J);
-  const int pf_kt = nst > 8 ? nst - 8 : 0;
   // K loop: ring bookkeeping around a per-warp compute step on stage s
   auto mainloop = [&](auto&& compute) {
     for (int kt = 0; kt < nst; ++kt) {
       const int s = kt % k64Stages;
-      if (MODE == 1 && kt == pf_kt) {           // X_j tile for the epilogue: ask L2 early
-        const double* Xt = p.Xold + (long long)job * p.job_stride + (long long)(I * k64Tile) * p.ld + J * k64Tile;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int l = threadIdx.x * 4 + u;     // 512 lines of 64 B: row l >> 3 (0..63), 8-double chunk l & 7
-          prefetch_l2(Xt + (long long)(l >> 3) * p.ld + (l & 7) * 8);
-        }
-      }
       if (threadIdx.x == 0 && kt >= 1 && kt - 1 + k64Stages < nst) {
         const int sp = (kt - 1) % k64Stages;
         mbar_wait(&empty[sp], static_cast<uint32_t>((kt - 1) / k64Stages) & 1u);
@@ -473,6 +481,16 @@ __global__ void __launch_bounds__(k64Threads, k64Stages == 2 ? 3 : 2)
             for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi][e], b[ni][e]);
       }
     });
+    if (MODE == 1) {   // X_{j+1} = ca X_j + cb Z in registers, X_j from the ring (read before S reuses it)
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+          const double2 x = x_ring(wm * 32 + mi * 8 + g, wn * 32 + ni * 8 + 2 * t);
+          acc[mi][ni][0] = fma(p.cb, acc[mi][ni][0], p.ca * x.x);
+          acc[mi][ni][1] = fma(p.cb, acc[mi][ni][1], p.ca * x.y);
+        }
+    }
     __syncthreads();
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
@@ -516,6 +534,20 @@ __global__ void __launch_bounds__(k64Threads, k64Stages == 2 ? 3 : 2)
           }
         }
       });
+      if (MODE == 1) {
+#pragma unroll
+        for (int i = 0; i < N0; ++i) {
+          const double2 x = x_ring(R0 * 8 + g, (R0 + i) * 8 + 2 * t);
+          c0[i][0] = fma(p.cb, c0[i][0], p.ca * x.x);
+          c0[i][1] = fma(p.cb, c0[i][1], p.ca * x.y);
+        }
+#pragma unroll
+        for (int i = 0; i < N1; ++i) {
+          const double2 x = x_ring(R1 * 8 + g, (R1 + i) * 8 + 2 * t);
+          c1[i][0] = fma(p.cb, c1[i][0], p.ca * x.x);
+          c1[i][1] = fma(p.cb, c1[i][1], p.ca * x.y);
+        }
+      }
       __syncthreads();
 #pragma unroll
       for (int i = 0; i < N0; ++i) {
@@ -546,27 +578,7 @@ __global__ void __launch_bounds__(k64Threads, k64Stages == 2 ? 3 : 2)
   const int i0 = I * k64Tile, j0 = J * k64Tile;
   double part = 0.0;
   constexpr int NE = k64Tile * k64Tile;          // 4096 elements, 32 per thread
-  if (MODE == 1) {
-    const double* X = p.Xold + base;
-    for (int idx0 = tid; idx0 < NE; idx0 += 8 * k64Threads) {
-      double xv[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int idx = idx0 + u * k64Threads, r = idx >> 6, c = idx & 63;
-        xv[u] = (!diag || r <= c) ? X[(long long)(i0 + r) * ld + j0 + c] : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int idx = idx0 + u * k64Threads, r = idx >> 6, c = idx & 63;
-        if (!diag || r <= c) {
-          const double v = fma(p.cb, S[r * EP + c], p.ca * xv[u]);
-          S[r * EP + c] = v;
-          if (diag && r == c && i0 + r < p.d) part += v;
-        }
-      }
-    }
-    __syncthreads();
-  }
+  if (MODE == 1 && diag && tid < k64Tile && i0 + tid < p.d) part = S[tid * EP + tid];   // trace partial
   if (!diag) {
     for (int idx = tid; idx < NE; idx += k64Threads) {
       const int r = idx >> 6, c = idx & 63;
