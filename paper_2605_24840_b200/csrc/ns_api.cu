@@ -52,7 +52,8 @@ struct Layout {
   size_t off_xa = 0, off_xb = 0, off_y = 0, off_res = 0, off_tr = 0, off_tiles = 0, off_jobs = 0,
          off_state = 0, off_active = 0, off_px = 0, off_py = 0, off_full = 0, off_pxb = 0, off_ahat = 0,
          off_r = 0, off_p = 0, off_cgpart = 0, off_cgsc = 0, off_ozx = 0, off_ozy = 0, off_oex = 0, off_oey = 0,
-         off_ores = 0, off_otr = 0, off_otiles = 0, off_ptiles = 0, off_pfull = 0, off_jlist = 0, total = 0;
+         off_ores = 0, off_otr = 0, off_otiles = 0, off_ptiles = 0, off_pfull = 0, off_jlist = 0, off_tperm = 0,
+         off_tslot = 0, total = 0;
 };
 
 Layout make_layout(int64_t d, int64_t batch, bool mixed = false, bool ozaki = false, bool tf32 = false) {
@@ -72,6 +73,8 @@ Layout make_layout(int64_t d, int64_t batch, bool mixed = false, bool ozaki = fa
   L.off_res = o; o = align256(o + sizeof(double) * nt_max * batch);
   L.off_tr = o; o = align256(o + sizeof(double) * n64 * batch);
   L.off_tiles = o; o = align256(o + sizeof(int2) * nt_max);
+  L.off_tperm = o; o = align256(o + sizeof(int2) * nt_max);   // first square of the host entry: tiles by H chunk
+  L.off_tslot = o; o = align256(o + sizeof(int) * nt_max);    // ... and their partial slots
   L.off_jobs = o; o = align256(o + sizeof(JobParams) * (size_t)batch);
   L.off_state = o; o = align256(o + sizeof(DevState) * (size_t)batch);
   L.off_active = o; o = align256(o + 256);
@@ -304,7 +307,7 @@ HostRing& ring() {
 // Side stream + events of the speculative result copy (host entry, one per thread)
 struct SpecCtx {
   cudaStream_t side = nullptr;
-  cudaEvent_t upd = nullptr, cp[2] = {nullptr, nullptr}, end = nullptr;
+  cudaEvent_t upd = nullptr, cp[2] = {nullptr, nullptr}, end = nullptr, chunk[8] = {};
   bool ok = false;
 };
 
@@ -316,6 +319,7 @@ SpecCtx& spec_ctx() {
     cudaEventCreateWithFlags(&c.cp[0], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c.cp[1], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c.end, cudaEventDisableTiming);
+    for (cudaEvent_t& e : c.chunk) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     c.ok = true;
   }
   return c;
@@ -344,6 +348,10 @@ struct Opts {
   double* spec_R = nullptr;
   long long spec_ldr = 0;
   bool* spec_hit = nullptr;
+  // host entry, one problem: H is still on the host (h_host, leading dimension h_ldh); run_loop stages
+  // it in row chunks on the side stream and starts the first square's tiles as their rows arrive
+  const double* h_host = nullptr;
+  long long h_ldh = 0;
 };
 
 Opts to_opts(const ns_options_t* o) {
@@ -456,10 +464,74 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
 
   NS_CUDA(launch_zero_state(state, batch, n_active, st));
   if (compact) NS_CUDA(launch_compact(state, batch, jlist, jlist + batch, st));
-  NS_CUDA(launch_init(H, ldh, h_stride, Xa, djobs, L.d, L.d_pad, batch, st));
-  if (t64) NS_CUDA(cudaMemsetAsync(trp, 0, sizeof(double) * nb * batch, st));
-  NS_CUDA(launch_trace_partials(Xa, L.d, L.d_pad, batch, trp, st, nb));   // 128-block sums, stride nb
   int nl = compact ? 4 : 3;
+  // Host entry (H on the host): H is staged in row chunks into X_b's buffer (dead until update 0) on the
+  // side stream; chunk c's rows of X_0 are formed as soon as it lands, and the tiles of the first square
+  // whose rows and columns all lie in chunks <= c are launched right after (each CTA writes its partial
+  // to the tile's slot of the full list: the decide's sum is unchanged), so the transfer of H overlaps
+  // the first product instead of preceding it.
+  const bool chunked = opt.h_host != nullptr && batch == 1 && spec_ctx().ok;
+  const Layout* Lp = &L;
+  ProdParams sq0{tiles, n_t, L.d_pad / kBK, L.d, L.d_pad, (long long)L.d_pad * L.d_pad, Y, nullptr, res, state, 0};
+  if (chunked) {
+    SpecCtx& c = spec_ctx();
+    const int nch = std::min(8, nb);
+    std::vector<int> cb(nch + 1);                   // chunk c = tile blocks [cb[c], cb[c+1])
+    for (int q = 0; q <= nch; ++q) cb[q] = (int)((long long)q * nb / nch);
+    std::vector<int> chunk_of(nb);
+    for (int q = 0; q < nch; ++q)
+      for (int b = cb[q]; b < cb[q + 1]; ++b) chunk_of[b] = q;
+    std::vector<int2> perm;
+    std::vector<int> slot, gstart(nch + 1, 0);
+    for (int q = 0; q < nch; ++q) {
+      gstart[q] = (int)perm.size();
+      for (int t = 0; t < n_t; ++t)
+        if (chunk_of[std::max(tl[t].x, tl[t].y)] == q) {
+          perm.push_back(tl[t]);
+          slot.push_back(t);
+        }
+    }
+    gstart[nch] = (int)perm.size();
+    int2* dperm = reinterpret_cast<int2*>(ws + Lp->off_tperm);
+    int* dslot = reinterpret_cast<int*>(ws + Lp->off_tslot);
+    NS_CUDA(cudaMemcpyAsync(dperm, perm.data(), perm.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+    NS_CUDA(cudaMemcpyAsync(dslot, slot.data(), slot.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    NS_CUDA(cudaEventRecord(c.upd, st));             // side stream: X_b is free once the previous call is done
+    NS_CUDA(cudaStreamWaitEvent(c.side, c.upd, 0));
+    for (int q = 0; q < nch; ++q) {
+      const int r0 = cb[q] * tile_rows, r1 = std::min(L.d, cb[q + 1] * tile_rows);
+      if (r1 > r0)
+        NS_CUDA(cudaMemcpy2DAsync(Xb + (size_t)r0 * L.d_pad, (size_t)L.d_pad * 8, opt.h_host + (size_t)r0 * opt.h_ldh,
+                                  (size_t)opt.h_ldh * 8, (size_t)L.d * 8, (size_t)(r1 - r0), cudaMemcpyHostToDevice,
+                                  c.side));
+      NS_CUDA(cudaEventRecord(c.chunk[q], c.side));
+    }
+    CUtensorMap tA0;
+    ns_status_t s0 = encode_map(&tA0, Xa, L.d_pad, 1, tile_rows);
+    if (s0 != NS_OK) return s0;
+    for (int q = 0; q < nch; ++q) {
+      NS_CUDA(cudaStreamWaitEvent(st, c.chunk[q], 0));
+      NS_CUDA(launch_init(Xb, L.d_pad, 0, Xa, djobs, L.d, L.d_pad, 1, st, cb[q] * tile_rows / 64,
+                          cb[q + 1] * tile_rows / 64));
+      nl += 1;
+      if (q == nch - 1) {
+        if (t64) NS_CUDA(cudaMemsetAsync(trp, 0, sizeof(double) * nb, st));
+        NS_CUDA(launch_trace_partials(Xa, L.d, L.d_pad, 1, trp, st, nb));
+      }
+      if (gstart[q + 1] > gstart[q]) {
+        ProdParams g = sq0;
+        g.tiles = dperm + gstart[q];
+        g.n_tiles = gstart[q + 1] - gstart[q];
+        g.part_slot = dslot + gstart[q];
+        NS_CUDA(t64 ? launch_product64(tA0, tA0, g, 1, st) : launch_product(tA0, tA0, g, 1, st));
+        nl += 1;
+      }
+    }
+  } else {
+    NS_CUDA(launch_init(H, ldh, h_stride, Xa, djobs, L.d, L.d_pad, batch, st));
+    if (t64) NS_CUDA(cudaMemsetAsync(trp, 0, sizeof(double) * nb * batch, st));
+    NS_CUDA(launch_trace_partials(Xa, L.d, L.d_pad, batch, trp, st, nb));   // 128-block sums, stride nb
+  }
   Profiler& pf = prof();
   // event slots: 4 per step (square begin/end, update begin/end)
 
@@ -500,10 +572,10 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
 
     ProdParams sq{tiles, n_t, L.d_pad / kBK, L.d, L.d_pad, job_stride, Y, nullptr, res, state, 0};
     if (pf.on) NS_CUDA(cudaEventRecord(pf.get(4 * j + 0), st));
-    NS_CUDA(product(tmC, tmC, sq));
+    if (!(chunked && j == 0)) NS_CUDA(product(tmC, tmC, sq));   // chunked: the first square already ran
     if (pf.on) NS_CUDA(cudaEventRecord(pf.get(4 * j + 1), st));
     NS_CUDA(launch_decide(state, djobs, res, n_t, trp, nb, lp, batch, n_active, st));
-    nl += 2;
+    nl += (chunked && j == 0) ? 1 : 2;
     if (compact) {
       NS_CUDA(launch_compact(state, batch, jlist, jlist + batch, st));
       nl += 1;
@@ -1426,10 +1498,17 @@ ns_status_t ns_reflector_host(const double* H_host, int64_t d, int64_t ldh, doub
     return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   uint8_t* w = static_cast<uint8_t*>(ws);
-  // H staged in the Y buffer (dead until the first square), R staged there after the loop.
+  // H staged in the Y buffer (dead until the first square), R staged there after the loop.  FP64 path
+  // with d >= 1024: run_loop stages H itself, in row chunks overlapped with the first square product.
   double* stage = reinterpret_cast<double*>(w + L.off_y);
-  NS_CUDA(cudaMemcpy2DAsync(stage, (size_t)d * 8, H_host, (size_t)ldh * 8, (size_t)d * 8, (size_t)d,
-                            cudaMemcpyHostToDevice, cs));
+  static const bool chunks_on = [] {
+    const char* e = getenv("NS_H2D_CHUNKS");   // 0: stage H in one copy before the loop (A/B knob)
+    return !(e && e[0] == '0');
+  }();
+  const bool fp64_chunked = chunks_on && !mixed && !ozaki && small_dpad(d) == 0 && d >= 1024;
+  if (!fp64_chunked)
+    NS_CUDA(cudaMemcpy2DAsync(stage, (size_t)d * 8, H_host, (size_t)ldh * 8, (size_t)d * 8, (size_t)d,
+                              cudaMemcpyHostToDevice, cs));
   std::vector<JobParams> jobs{JobParams{s, alpha, k, 0}};
   std::vector<DevState> states(1);
   int nl = 0;
@@ -1442,6 +1521,10 @@ ns_status_t ns_reflector_host(const double* H_host, int64_t d, int64_t ldh, doub
     // behind the last square product (run_loop); otherwise one D2H copy after the loop
     Opts o;
     bool hit = false;
+    if (fp64_chunked) {
+      o.h_host = H_host;
+      o.h_ldh = ldh;
+    }
     cudaPointerAttributes pa{};
     static const bool spec_on = [] {
       const char* e = getenv("NS_SPEC_COPY");   // 0: always copy R after the loop (A/B knob)

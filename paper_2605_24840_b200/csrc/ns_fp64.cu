@@ -39,10 +39,10 @@ namespace nsr {
 // --------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) ns_init_kernel(const double* __restrict__ H, long long ldh,
                                                       long long h_stride, double* __restrict__ X,
-                                                      const JobParams* __restrict__ jobs, int d, int d_pad) {
+                                                      const JobParams* __restrict__ jobs, int d, int d_pad, int rb0) {
   __shared__ double t[64][65];
   const int job = blockIdx.z;
-  const int bi = blockIdx.y, bj = blockIdx.x;
+  const int bi = blockIdx.y + rb0, bj = blockIdx.x;
   const double* Hj = H + (long long)job * h_stride;
   double* Xj = X + (long long)job * d_pad * (long long)d_pad;
   const double s = jobs[job].s, alpha = jobs[job].alpha;
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __threadfence_system();
     } else if (MODE == 0) {
-      p.partial[(long long)job * p.n_tiles + blockIdx.x] = s;
+      p.partial[(long long)job * p.n_tiles + (p.part_slot ? p.part_slot[blockIdx.x] : (int)blockIdx.x)] = s;
     } else if (diag) {
       p.partial[(long long)job * (p.ld / kTile) + I] = s;
     }
@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(k64Threads, k64Stages == 2 ? 3 : 2)
     double sum = 0.0;
 #pragma unroll
     for (int w = 0; w < k64Threads / 32; ++w) sum += red[w];
-    if (MODE == 0) p.partial[(long long)job * p.n_tiles + blockIdx.x] = sum;
+    if (MODE == 0) p.partial[(long long)job * p.n_tiles + (p.part_slot ? p.part_slot[blockIdx.x] : (int)blockIdx.x)] = sum;
     else if (diag) p.partial[(long long)job * (p.ld / k64Tile) + I] = sum;
   }
 }
@@ -779,9 +779,11 @@ __global__ void __launch_bounds__(256) ns_copy_out_kernel(const double* __restri
 // launchers
 // --------------------------------------------------------------------------------------
 cudaError_t launch_init(const double* H, long long ldh, long long h_stride, double* X, const JobParams* jobs,
-                        int d, int d_pad, int batch, cudaStream_t st) {
-  dim3 grid(d_pad / 64, d_pad / 64, batch);
-  ns_init_kernel<<<grid, 256, 0, st>>>(H, ldh, h_stride, X, jobs, d, d_pad);
+                        int d, int d_pad, int batch, cudaStream_t st, int rb0, int rb1) {
+  if (rb1 < 0) rb1 = d_pad / 64;
+  if (rb1 <= rb0) return cudaSuccess;
+  dim3 grid(d_pad / 64, rb1 - rb0, batch);
+  ns_init_kernel<<<grid, 256, 0, st>>>(H, ldh, h_stride, X, jobs, d, d_pad, rb0);
   return cudaGetLastError();
 }
 

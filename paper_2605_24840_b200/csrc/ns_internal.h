@@ -113,6 +113,9 @@ struct ProdParams {
   // batched: CTA row blockIdx.y runs job job_list[blockIdx.y] (rows >= *n_job_list exit); nullptr = job blockIdx.y
   const int* job_list = nullptr;
   const int* n_job_list = nullptr;
+  // mode 0, batch 1: partial slot of CTA x is part_slot[x] (a sub-list of the tile list launched on its
+  // own keeps the slots of the full list, so the decide's fixed-order sum is unchanged); nullptr = x
+  const int* part_slot = nullptr;
   int diag_tri = 1;        // 64x64-tile kernel: diagonal tiles compute only their upper 8x8 blocks (NS_DIAG_TRI=0: full)
 };
 
@@ -167,7 +170,7 @@ cudaError_t launch_mx2_product(const CUtensorMap& tmP, const CUtensorMap& tmQ64,
 
 // Host-side launchers (ns_fp64.cu).
 cudaError_t launch_init(const double* H, long long ldh, long long h_stride, double* X, const JobParams* jobs,
-                        int d, int d_pad, int batch, cudaStream_t st);
+                        int d, int d_pad, int batch, cudaStream_t st, int rb0 = 0, int rb1 = -1);   // 64-row blocks [rb0, rb1)
 cudaError_t launch_trace_partials(const double* X, int d, int d_pad, int batch, double* tr_partial,
                                   cudaStream_t st, int job_stride = 0);
 // Raise a kernel's dynamic shared-memory limit once per device: `mask` is that kernel's static set of

@@ -192,12 +192,14 @@ def test_host_entry_matches_device(nsr):
     assert np.array_equal(Rh.numpy(), Rd.cpu().numpy()) and rh == rd
 
 
-@pytest.mark.parametrize("case", ["tol", "fixed", "zero_steps", "odd_d", "nan"])
+@pytest.mark.parametrize("case", ["tol", "fixed", "zero_steps", "odd_d", "nan", "ragged"])
 def test_host_entry_pinned_speculative_copy(nsr, case):
-    """Pinned host buffers: the FP64 loop copies the iterate its decide predicts final straight to R
-    behind the confirming square (DevState.spec); R, steps and residual equal the device entry's bitwise,
-    also where the prediction has nothing to do (no update, odd d: copy disabled, non-finite input)."""
-    d = 1001 if case == "odd_d" else 1024
+    """Pinned host buffers: H arrives in row chunks overlapped with the first square (tiles launched as
+    their rows land, partials in the full list's slots) and the FP64 loop copies the iterate its decide
+    predicts final straight to R behind the confirming square (DevState.spec); R, steps and residual
+    equal the device entry's bitwise, also where the prediction has nothing to do (no update, odd d:
+    copy disabled, non-finite input) and for a ragged d on 64-tiles."""
+    d = {"odd_d": 1001, "ragged": 3000}.get(case, 1024)
     p = workloads.cfg3_dense(d=d, k=64)
     H = p.H.copy()
     if case == "nan":
