@@ -10,3 +10,8 @@ python bench.py --steps 1 --warmup 3 --no-mixed --no-cpu-baseline --no-e2e > /de
   bash tools/ncu_launches.sh 400 "ns_" python bench.py --steps 1 --warmup 3 --no-mixed --no-cpu-baseline --no-e2e \
   > gpurun_out/${T}_launches.txt 2>&1
 cat gpurun_out/${T}_pytest.txt
+# full ncu capture of one full-batch 64-tile launch (cfg1 square + update), after the same command ran clean
+python tools/cfg1_prof.py > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on \
+  -k "regex:ns_product64_kernel" -s 2 -c 2 -o gpurun_out/${T}_p64 python tools/cfg1_prof.py > gpurun_out/${T}_p64.log 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.txt 2>&1
+python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/${T}_reference.json 2>/dev/null
