@@ -291,8 +291,11 @@ struct HostRing {
   bool ok = false;
 };
 
-HostRing& ring() {
-  static thread_local HostRing r;
+HostRing& ring() {   // per host thread and device (events and mapped memory belong to one device)
+  static thread_local HostRing rings[32];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  HostRing& r = rings[dev & 31];
   if (!r.ok) {
     if (cudaHostAlloc(&r.slots, 16 * sizeof(int), cudaHostAllocDefault) != cudaSuccess) return r;
     if (cudaHostAlloc(&r.pstate, sizeof(DevState), cudaHostAllocMapped) != cudaSuccess) r.pstate = nullptr;
@@ -311,8 +314,11 @@ struct SpecCtx {
   bool ok = false;
 };
 
-SpecCtx& spec_ctx() {
-  static thread_local SpecCtx c;
+SpecCtx& spec_ctx() {   // per host thread and device
+  static thread_local SpecCtx ctxs[32];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SpecCtx& c = ctxs[dev & 31];
   if (!c.ok) {
     if (cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking) != cudaSuccess) return c;
     cudaEventCreateWithFlags(&c.upd, cudaEventDisableTiming);
