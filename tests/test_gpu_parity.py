@@ -812,3 +812,75 @@ def test_batched_nonfinite_problem_is_isolated(nsr, prec):
         if not _tie_band(o["hist_residual"], 1e-12, o["steps"]):
             assert outs[i]["steps"] == o["steps"]
         assert outs[i]["cert"] == p.k and checks.frob_per_sqrt_d(R[i], o["R"]) <= TOL_R
+
+
+# ------------------------------------------------------------------ seeded random sweep
+def _random_problem(seed):
+    """Random size (ragged, 1..320), index, relative gap (log-uniform 1e-3..0.3), shift inside the gap,
+    scale factor (0.8 = too small -> SCALING_SUSPECT / divergence; else >= the bound), tolerance mode,
+    tolerance and step cap.  Generator only (Haar Q, spectrum); no Newton–Schulz arithmetic."""
+    rng = np.random.default_rng(1000 + seed)
+    d = int(rng.choice([1, 2, 3, 7, 31, 64, 65, 96, 97, 127, 129, 200, 255, 257, 320]))
+    k = int(rng.integers(0, d + 1))
+    g = 10.0 ** rng.uniform(-3, math.log10(0.3))
+    lam = np.concatenate([-rng.uniform(g / 2, 1.0, k), rng.uniform(g / 2, 1.0, d - k)])
+    Q = workloads.haar_q(rng, d)
+    H = (Q * lam[None, :]) @ Q.T
+    H = 0.5 * (H + H.T)
+    s = float(rng.uniform(-0.4, 0.4) * g)
+    bound = float(np.max(np.abs(lam - s)))
+    alpha = bound * float(rng.choice([0.8, 1.0, 1.05, 1.3]))
+    tm = int(rng.integers(0, 2))
+    tol = float(rng.choice([1e-8, 1e-10, 1e-12]))
+    max_steps = int(rng.choice([3, 10, 100]))
+    return H, s, alpha, k, max_steps, tol, tm
+
+
+@pytest.mark.parametrize("seed", range(48))
+def test_random_sweep_fp64(nsr, seed):
+    """FP64 path vs the oracle on seeded random problems (sizes, gaps, shifts, scales, tolerance modes and
+    step caps drawn at random): steps, flags, certificate, trace and R (tie-band rule C9)."""
+    H, s, alpha, k, max_steps, tol, tm = _random_problem(seed)
+    _compare(nsr, H, s, alpha, k, max_steps, tol, tm)
+
+
+@pytest.mark.parametrize("seed", range(0, 24, 3))
+def test_random_sweep_ozaki_and_batched(nsr, seed):
+    """The same random problems (well scaled) on the Ozaki INT8 path, and a batch of 6 of one size
+    through the batched entry: steps and certificate equal the oracle's outside the tie band, R within
+    1e-10 per sqrt(d)."""
+    H, s, alpha, k, max_steps, tol, tm = _random_problem(seed)
+    d = H.shape[0]
+    alpha = max(alpha, float(np.linalg.norm(H - s * np.eye(d), 2)))
+    o = ons.ns_reflector(H, s, alpha, k, max_steps, tol, tm, trace_residuals=True)
+    tie = _tie_band(o["hist_residual"], tol if tm == 0 else tol * math.sqrt(d), o["steps"])
+    R, res = nsr.ns_reflector(torch.from_numpy(H).to(_dev()), s, alpha, k, max_steps, tol, tm,
+                              prec=nsr.NS_PREC_FP64_OZAKI)
+    assert res["cert"] == o["cert"]
+    if not tie:
+        assert res["steps"] == o["steps"]
+        assert checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= TOL_R
+    # batched: 6 problems of this size with their own shifts and scales
+    rng = np.random.default_rng(seed)
+    probs = []
+    for b in range(6):
+        Hb, sb, ab, kb, _, _, _ = _random_problem(seed * 7 + 100 + b)
+        if Hb.shape[0] != d:           # keep the size: rescale a fresh problem of size d
+            lam = np.sort(rng.uniform(-1, 1, d))
+            Q = workloads.haar_q(rng, d)
+            Hb = 0.5 * (((Q * lam[None, :]) @ Q.T) + ((Q * lam[None, :]) @ Q.T).T)
+            kb = int(np.sum(lam < 0))
+            sb = float(0.5 * (lam[kb - 1] + lam[kb])) if 0 < kb < d else (-2.0 if kb == 0 else 2.0)
+            ab = float(np.max(np.abs(lam - sb)))
+        ab = max(ab, float(np.linalg.norm(Hb - sb * np.eye(d), 2)))
+        probs.append((Hb, sb, ab, kb))
+    Hs = torch.from_numpy(np.stack([p_[0] for p_ in probs])).to(_dev())
+    Rb, outs = nsr.ns_reflector_batched(Hs, [p_[1] for p_ in probs], [p_[2] for p_ in probs],
+                                        [p_[3] for p_ in probs], max_steps, tol, tm)
+    Rb = Rb.cpu().numpy()
+    for b, (Hb, sb, ab, kb) in enumerate(probs):
+        ob = ons.ns_reflector(Hb, sb, ab, kb, max_steps, tol, tm, trace_residuals=True)
+        assert outs[b]["cert"] == ob["cert"]
+        if not _tie_band(ob["hist_residual"], tol if tm == 0 else tol * math.sqrt(d), ob["steps"]):
+            assert outs[b]["steps"] == ob["steps"], b
+            assert checks.frob_per_sqrt_d(Rb[b], ob["R"]) <= TOL_R, b
