@@ -307,6 +307,16 @@ HostRing& ring() {   // per host thread and device (events and mapped memory bel
   return r;
 }
 
+// Relative residual at which the re-anchor's CG solve stops (remaining launches of the capped loop
+// return at once); NS_CG_TOL overrides (experiments)
+double cg_tol() {
+  static const double v = [] {
+    const char* e = getenv("NS_CG_TOL");
+    return e ? atof(e) : kCgTol;
+  }();
+  return v;
+}
+
 // Side stream + events of the speculative result copy (host entry, one per thread)
 struct SpecCtx {
   cudaStream_t side = nullptr;
@@ -344,7 +354,7 @@ ns_status_t check_common(int64_t d, int32_t max_steps, double tol, ns_tolmode_t 
 
 struct Opts {
   double switch_tol = 1e-4;
-  int cg_iters = 24;
+  int cg_iters = 96;              // cap; the solve stops at the relative residual cg_tol()
   int stop_at_switch = 0;
   int lookahead = 0;
   int polish = 0;                 // mixed path: 0 = FP64 DMMA re-anchor / polish, 1 = Ozaki INT8
@@ -879,14 +889,15 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
       int np = 0;
       double* E = Ahat;
       NS_CUDA(launch_cg_init(Y, Rc, Pc, E, cgpart, L.d_pad, st, &np));
-      NS_CUDA(launch_cg_scalar(cgsc, cgpart, np, 0, st));
+      NS_CUDA(launch_cg_scalar(cgsc, cgpart, np, 0, st, cg_tol() * cg_tol()));
       NS_CUDA(launch_split_planes(Pc, PXa, L.d_pad, 1, st, tf32));
       nl += 4;
       for (int it = 0; it < opt.cg_iters; ++it) {
         // W = |A| P (BF16x3 tcgen05, every tile) -> Xo
         MxParams pw{mx_full, mx_nfull, mx_nkb, L.d, L.d_pad, 0, Xo, nullptr, nullptr, nullptr, nullptr, 2, tf32 ? 1 : 0};
+        pw.skip = &cgsc->done;
         NS_CUDA(mx_product(tmPY, tqPXa, pw));
-        NS_CUDA(launch_cg_pw(Pc, Xo, cgpart, L.d_pad, st));
+        NS_CUDA(launch_cg_pw(Pc, Xo, cgpart, L.d_pad, st, cgsc));
         NS_CUDA(launch_cg_scalar(cgsc, cgpart, kEwBlocks, 1, st));
         NS_CUDA(launch_cg_update(E, Rc, Pc, Xo, cgsc, cgpart, L.d_pad, st, &np));
         NS_CUDA(launch_cg_scalar(cgsc, cgpart, np, 2, st));
@@ -898,6 +909,13 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
       }
       NS_CUDA(launch_apply_correction(Xt, E, L.d_pad, st));
       nl += 1;
+      if (getenv("NS_CG_DEBUG")) {
+        CgScalars h{};
+        NS_CUDA(cudaMemcpyAsync(&h, cgsc, sizeof(CgScalars), cudaMemcpyDeviceToHost, st));
+        NS_CUDA(cudaStreamSynchronize(st));
+        fprintf(stderr, "re-anchor CG: %d iterations, |r|/|r0| = %.3e (tol %.1e, cap %d)\n", h.iters,
+                h.rr0 > 0 ? sqrt(h.rr / h.rr0) : 0.0, cg_tol(), opt.cg_iters);
+      }
     }
     // ---------------- phase 2: FP64-class steps from j0 to tolerance ----------------
     LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0, -1, 0};
@@ -1422,7 +1440,7 @@ void ns_options_default(ns_options_t* o) {
   if (!o) return;
   *o = ns_options_t{};
   o->switch_tol = 1e-4;
-  o->cg_iters = 24;
+  o->cg_iters = 96;
   o->stop_at_switch = 0;
   o->lookahead = 0;
   o->filter_a = 1.5;

@@ -72,15 +72,22 @@ struct CgScalars {
   double pw;      // <P, W>,  W = |A| P
   double alpha;
   double beta;
+  double rr0;     // <R, R> of the initial residual
+  double tol2;    // stop once rr <= tol2 * rr0 (relative residual tol, squared)
+  int done;       // set by the scalar kernel; every later CG launch returns at once
+  int iters;      // iterations performed
 };
+constexpr double kCgTol = 1e-6;      // re-anchor CG: stop at |R| <= kCgTol |R_0| (within the iteration cap)
 constexpr int kEwBlocks = 148 * 8;   // fixed grid of the elementwise CG kernels (fixed-order partial sums)
 
 cudaError_t launch_commutator(const double* M, double* C, void* abs_planes, int d_pad, cudaStream_t st,
                               bool tf32 = false);
 cudaError_t launch_cg_init(const double* Fp, double* R, double* P, double* E, double* partial, int d_pad,
                            cudaStream_t st, int* n_partial);
-cudaError_t launch_cg_pw(const double* P, const double* W, double* partial, int d_pad, cudaStream_t st);
-cudaError_t launch_cg_scalar(CgScalars* sc, const double* partial, int n_partial, int which, cudaStream_t st);
+cudaError_t launch_cg_pw(const double* P, const double* W, double* partial, int d_pad, cudaStream_t st,
+                         const CgScalars* sc);
+cudaError_t launch_cg_scalar(CgScalars* sc, const double* partial, int n_partial, int which, cudaStream_t st,
+                             double tol2 = 0.0);
 cudaError_t launch_cg_update(double* E, double* R, const double* P, const double* W, const CgScalars* sc,
                              double* partial, int d_pad, cudaStream_t st, int* n_partial);
 cudaError_t launch_cg_direction(double* P, const double* R, const CgScalars* sc, void* p_planes, int d_pad,
@@ -157,6 +164,7 @@ struct MxParams {
   int mode;                // 0 square (+res, mirror), 1 update (+trace, mirror), 2 dense tile (no mirror)
   int tf32 = 0;            // 0: BF16x3 (kind::f16), 1: TF32x3 (kind::tf32); nkb = d_pad / (tf32 ? 32 : 64)
   unsigned long long* trace = nullptr;   // diagnostics: per-CTA %globaltimer stamps (start, mainloop done, end)
+  const int* skip = nullptr;             // CG operator products: return at once if *skip (solve converged)
 };
 
 cudaError_t launch_split_planes(const double* X, void* planes, int d_pad, int batch, cudaStream_t st,

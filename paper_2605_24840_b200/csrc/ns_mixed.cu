@@ -196,6 +196,7 @@ __global__ void __launch_bounds__(kMxThreads, 1)
   constexpr int kKB = TF32 ? 32 : kMxBK;   // elements per 128-byte k-block row
   const int job = blockIdx.y;
   if (p.state != nullptr && (p.state[job].done || p.state[job].sw)) return;   // low-precision phase over
+  if (p.skip != nullptr && *p.skip) return;                                    // CG solve already converged
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -363,6 +364,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kMxThreads, 1)
   constexpr int kKB = TF32 ? 32 : kMxBK;
   const int job = blockIdx.y;
   if (p.state != nullptr && (p.state[job].done || p.state[job].sw)) return;   // same for both CTAs
+  if (p.skip != nullptr && *p.skip) return;                                    // CG solve already converged
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));

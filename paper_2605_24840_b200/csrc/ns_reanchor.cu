@@ -146,17 +146,21 @@ __global__ void __launch_bounds__(256) ns_cg_init_kernel(const double* __restric
 
 // partial <P, W> over all entries (grid-stride, fixed grid kEwBlocks).
 __global__ void __launch_bounds__(256) ns_cg_pw_kernel(const double* __restrict__ P, const double* __restrict__ W,
-                                                       double* __restrict__ partial, long long n) {
+                                                       double* __restrict__ partial, long long n,
+                                                       const CgScalars* __restrict__ sc) {
+  if (sc->done) return;
   double acc = 0.0;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     acc = fma(P[i], W[i], acc);
   block_partial(acc, partial);
 }
 
-// which = 0: rr = sum;  1: pw = sum, alpha = rr / (2 pw);  2: beta = sum / rr, rr = sum.
+// which = 0: rr = rr0 = sum (tol2 set by the host);  1: pw = sum, alpha = rr / (2 pw);
+// 2: beta = sum / rr, rr = sum, done once rr <= tol2 rr0 (the remaining launches of the solve return at once).
 __global__ void __launch_bounds__(256) ns_cg_scalar_kernel(CgScalars* sc, const double* __restrict__ partial, int n,
-                                                           int which) {
+                                                           int which, double tol2) {
   __shared__ double red[8];
+  if (which != 0 && sc->done) return;
   double s = 0.0;
   for (int i = threadIdx.x; i < n; i += 256) s += partial[i];
 #pragma unroll
@@ -168,12 +172,18 @@ __global__ void __launch_bounds__(256) ns_cg_scalar_kernel(CgScalars* sc, const 
   for (int w = 0; w < 8; ++w) t += red[w];
   if (which == 0) {
     sc->rr = t;
+    sc->rr0 = t;
+    sc->tol2 = tol2;
+    sc->done = (t == 0.0) ? 1 : 0;
+    sc->iters = 0;
   } else if (which == 1) {
     sc->pw = t;
     sc->alpha = (t != 0.0) ? sc->rr / (2.0 * t) : 0.0;   // <P, L(P)> = <P, W + W^T> = 2 <P, W>
   } else {
     sc->beta = (sc->rr != 0.0) ? t / sc->rr : 0.0;
     sc->rr = t;
+    sc->iters += 1;
+    if (!(t > sc->tol2 * sc->rr0)) sc->done = 1;
   }
 }
 
@@ -183,6 +193,7 @@ __global__ void __launch_bounds__(256) ns_cg_update_kernel(double* __restrict__ 
                                                            const CgScalars* __restrict__ sc,
                                                            double* __restrict__ partial, int d_pad) {
   __shared__ double ta[32][33], tb[32][33];
+  if (sc->done) return;
   const int nb = d_pad / 32;
   int bi, bj;
   tile_pair(blockIdx.x, nb, bi, bj);
@@ -214,6 +225,7 @@ template <bool TF32>
 __global__ void __launch_bounds__(256) ns_cg_direction_kernel(double* __restrict__ P, const double* __restrict__ R,
                                                               const CgScalars* __restrict__ sc,
                                                               void* __restrict__ planes, long long n) {
+  if (sc->done) return;
   const double beta = sc->beta;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const double p = fma(beta, P[i], R[i]);
@@ -247,13 +259,15 @@ cudaError_t launch_cg_init(const double* Fp, double* R, double* P, double* E, do
   return cudaGetLastError();
 }
 
-cudaError_t launch_cg_pw(const double* P, const double* W, double* partial, int d_pad, cudaStream_t st) {
-  ns_cg_pw_kernel<<<kEwBlocks, 256, 0, st>>>(P, W, partial, (long long)d_pad * d_pad);
+cudaError_t launch_cg_pw(const double* P, const double* W, double* partial, int d_pad, cudaStream_t st,
+                         const CgScalars* sc) {
+  ns_cg_pw_kernel<<<kEwBlocks, 256, 0, st>>>(P, W, partial, (long long)d_pad * d_pad, sc);
   return cudaGetLastError();
 }
 
-cudaError_t launch_cg_scalar(CgScalars* sc, const double* partial, int n_partial, int which, cudaStream_t st) {
-  ns_cg_scalar_kernel<<<1, 256, 0, st>>>(sc, partial, n_partial, which);
+cudaError_t launch_cg_scalar(CgScalars* sc, const double* partial, int n_partial, int which, cudaStream_t st,
+                             double tol2) {
+  ns_cg_scalar_kernel<<<1, 256, 0, st>>>(sc, partial, n_partial, which, tol2);
   return cudaGetLastError();
 }
 

@@ -884,3 +884,28 @@ def test_random_sweep_ozaki_and_batched(nsr, seed):
         if not _tie_band(ob["hist_residual"], tol if tm == 0 else tol * math.sqrt(d), ob["steps"]):
             assert outs[b]["steps"] == ob["steps"], b
             assert checks.frob_per_sqrt_d(Rb[b], ob["R"]) <= TOL_R, b
+
+
+@pytest.mark.parametrize("seed,prec", [(s_, p_) for s_ in range(6) for p_ in (1, 2)])
+def test_random_sweep_mixed(nsr, seed, prec):
+    """Mixed BF16x3 / TF32x3 path on random well-scaled problems (d 130..512, gaps 1e-2..0.3, run to
+    tolerance): after re-anchor + FP64 polish, steps and certificate equal the oracle's (outside the tie
+    band) and R is within 1e-10 per sqrt(d)."""
+    rng = np.random.default_rng(2000 + seed)
+    d = int(rng.choice([130, 200, 256, 300, 512]))
+    k = int(rng.integers(1, d))
+    g = 10.0 ** rng.uniform(-2, math.log10(0.3))
+    lam = np.concatenate([-rng.uniform(g / 2, 1.0, k), rng.uniform(g / 2, 1.0, d - k)])
+    Q = workloads.haar_q(rng, d)
+    H = (Q * lam[None, :]) @ Q.T
+    H = 0.5 * (H + H.T)
+    s = float(rng.uniform(-0.3, 0.3) * g)
+    alpha = float(np.linalg.norm(H - s * np.eye(d), 2)) * 1.02
+    tol, tm = 1e-10, 1
+    o = ons.ns_reflector(H, s, alpha, k, 100, tol, tm, trace_residuals=True)
+    R, res = nsr.ns_reflector(torch.from_numpy(H).to(_dev()), s, alpha, k, 100, tol, tm, prec=prec)
+    assert res["cert"] == o["cert"] == k
+    assert res["flags"] & ons.CONVERGED
+    if not _tie_band(o["hist_residual"], tol * math.sqrt(d), o["steps"]):
+        assert res["steps"] == o["steps"], (res, o["steps"])
+    assert checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= TOL_R
