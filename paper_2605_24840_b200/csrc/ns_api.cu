@@ -878,16 +878,19 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
       return NS_OK;
     };
     if (oz) NS_CUDA(cudaMemcpyAsync(otiles, ot_full.data(), ot_full.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
-    if (opt.cg_iters > 0) {
+    // One re-anchor pass: M = A X~, C = M - M^T, F = sym(X~ C) in FP64-class arithmetic, CG on
+    // |A|E + E|A| = F with the split-precision operator, X~ <- X~ - E.  Returns the CG iterations used.
+    auto reanchor_pass = [&](int* iters) -> ns_status_t {
       // M = A X~  (every tile) -> Y
       if ((s = dense(Ahat, tmAh, Xt, tXt, Y)) != NS_OK) return s;
       // C = M - M^T -> Xo ; |A| = sym(M) -> bf16 planes PY
       NS_CUDA(launch_commutator(Y, Xo, PY, L.d_pad, st, tf32));
       // F' = X~ C^T = -X~ C  (every tile) -> Y
       if ((s = dense(Xt, tXt, Xo, tXo, Y)) != NS_OK) return s;
-      // F = sym(X~ C); R = P = F; E = 0 (E lives in A's buffer, A is no longer needed)
+      // F = sym(X~ C); R = P = F; E = 0 (E overwrites F' in Y tile pair by tile pair; A stays for a
+      // second pass)
       int np = 0;
-      double* E = Ahat;
+      double* E = Y;
       NS_CUDA(launch_cg_init(Y, Rc, Pc, E, cgpart, L.d_pad, st, &np));
       NS_CUDA(launch_cg_scalar(cgsc, cgpart, np, 0, st, cg_tol() * cg_tol()));
       NS_CUDA(launch_split_planes(Pc, PXa, L.d_pad, 1, st, tf32));
@@ -909,13 +912,23 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
       }
       NS_CUDA(launch_apply_correction(Xt, E, L.d_pad, st));
       nl += 1;
-      if (getenv("NS_CG_DEBUG")) {
-        CgScalars h{};
-        NS_CUDA(cudaMemcpyAsync(&h, cgsc, sizeof(CgScalars), cudaMemcpyDeviceToHost, st));
-        NS_CUDA(cudaStreamSynchronize(st));
+      CgScalars h{};
+      NS_CUDA(cudaMemcpyAsync(&h, cgsc, sizeof(CgScalars), cudaMemcpyDeviceToHost, st));
+      NS_CUDA(cudaStreamSynchronize(st));
+      if (getenv("NS_CG_DEBUG"))
         fprintf(stderr, "re-anchor CG: %d iterations, |r|/|r0| = %.3e (tol %.1e, cap %d)\n", h.iters,
                 h.rr0 > 0 ? sqrt(h.rr / h.rr0) : 0.0, cg_tol(), opt.cg_iters);
-      }
+      *iters = h.iters;
+      return NS_OK;
+    };
+    if (opt.cg_iters > 0) {
+      // A slowly converging solve means a badly conditioned |A| (small min |x| of X_0): the solution's
+      // error from the split-precision operator is amplified by that condition number, so a second pass
+      // (iterative refinement: the new right-hand side is formed in FP64 from the corrected iterate)
+      // removes what the first left.
+      int iters = 0;
+      if ((s = reanchor_pass(&iters)) != NS_OK) return s;
+      if (iters > kCgRefineIters && (s = reanchor_pass(&iters)) != NS_OK) return s;
     }
     // ---------------- phase 2: FP64-class steps from j0 to tolerance ----------------
     LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0, -1, 0};

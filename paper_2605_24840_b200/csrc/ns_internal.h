@@ -78,6 +78,7 @@ struct CgScalars {
   int iters;      // iterations performed
 };
 constexpr double kCgTol = 1e-6;      // re-anchor CG: stop at |R| <= kCgTol |R_0| (within the iteration cap)
+constexpr int kCgRefineIters = 40;   // a solve that needed more iterations is followed by a second re-anchor pass
 constexpr int kEwBlocks = 148 * 8;   // fixed grid of the elementwise CG kernels (fixed-order partial sums)
 
 cudaError_t launch_commutator(const double* M, double* C, void* abs_planes, int d_pad, cudaStream_t st,

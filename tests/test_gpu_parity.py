@@ -886,15 +886,17 @@ def test_random_sweep_ozaki_and_batched(nsr, seed):
             assert checks.frob_per_sqrt_d(Rb[b], ob["R"]) <= TOL_R, b
 
 
-@pytest.mark.parametrize("seed,prec", [(s_, p_) for s_ in range(6) for p_ in (1, 2)])
+@pytest.mark.parametrize("seed,prec", [(s_, p_) for s_ in range(10) for p_ in (1, 2)])
 def test_random_sweep_mixed(nsr, seed, prec):
-    """Mixed BF16x3 / TF32x3 path on random well-scaled problems (d 130..512, gaps 1e-2..0.3, run to
-    tolerance): after re-anchor + FP64 polish, steps and certificate equal the oracle's (outside the tie
-    band) and R is within 1e-10 per sqrt(d)."""
+    """Mixed BF16x3 / TF32x3 path on random well-scaled problems (d 130..512, gaps 1e-3..0.3, run to
+    tolerance): after re-anchor + FP64 polish, the certificate equals the oracle's, R is within 1e-10 per
+    sqrt(d), and the step count equals the oracle's (outside the tie band) -- or exceeds it by one when
+    the oracle's residual at the mixed path's switch step was already below the switch threshold
+    (1e-4 sqrt(d)), which the split-precision residual cannot resolve (DESIGN reading C16b)."""
     rng = np.random.default_rng(2000 + seed)
     d = int(rng.choice([130, 200, 256, 300, 512]))
     k = int(rng.integers(1, d))
-    g = 10.0 ** rng.uniform(-2, math.log10(0.3))
+    g = 10.0 ** rng.uniform(-3 if seed >= 6 else -2, math.log10(0.3))
     lam = np.concatenate([-rng.uniform(g / 2, 1.0, k), rng.uniform(g / 2, 1.0, d - k)])
     Q = workloads.haar_q(rng, d)
     H = (Q * lam[None, :]) @ Q.T
@@ -907,5 +909,7 @@ def test_random_sweep_mixed(nsr, seed, prec):
     assert res["cert"] == o["cert"] == k
     assert res["flags"] & ons.CONVERGED
     if not _tie_band(o["hist_residual"], tol * math.sqrt(d), o["steps"]):
-        assert res["steps"] == o["steps"], (res, o["steps"])
+        late_switch = (res["steps"] == o["steps"] + 1 and 0 <= res["switch_step"] <= o["steps"]
+                       and o["hist_residual"][res["switch_step"]] / math.sqrt(d) < 1e-4)
+        assert res["steps"] == o["steps"] or late_switch, (res, o["steps"])
     assert checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= TOL_R
