@@ -913,3 +913,44 @@ def test_random_sweep_mixed(nsr, seed, prec):
                        and o["hist_residual"][res["switch_step"]] / math.sqrt(d) < 1e-4)
         assert res["steps"] == o["steps"] or late_switch, (res, o["steps"])
     assert checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= TOL_R
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_sweep_sharded_host_filters(nsr, seed):
+    """Random problems through the remaining entries: P ranks emulated on one GPU (random P, ragged d),
+    the pinned host entry (chunked staging + speculative copy, d >= 1024), and a random odd cubic filter
+    at fixed depth on the tiled path -- each against the oracle (or the device entry, bitwise)."""
+    from oracle import setup
+    rng = np.random.default_rng(4000 + seed)
+    H, s, alpha, k, max_steps, tol, tm = _random_problem(seed + 50)
+    d = H.shape[0]
+    alpha = max(alpha, float(np.linalg.norm(H - s * np.eye(d), 2)))
+    o = ons.ns_reflector(H, s, alpha, k, max_steps, tol, tm, trace_residuals=True)
+    P = int(rng.integers(2, 9))
+    Re, re_ = nsr.ns_reflector_sharded_emulated(P, torch.from_numpy(H).to(_dev()), s, alpha, k, max_steps, tol, tm)
+    assert re_["cert"] == o["cert"]
+    if not _tie_band(o["hist_residual"], tol if tm == 0 else tol * math.sqrt(d), o["steps"]):
+        assert re_["steps"] == o["steps"]
+        assert checks.frob_per_sqrt_d(Re.cpu().numpy(), o["R"]) <= TOL_R
+    # host entry at a size that takes the chunked / speculative path
+    dh = int(rng.choice([1024, 1100, 1536, 2048]))
+    lam = np.concatenate([-rng.uniform(0.02, 1.0, dh // 3), rng.uniform(0.02, 1.0, dh - dh // 3)])
+    Q = workloads.haar_q(rng, dh)
+    Hh = (Q * lam[None, :]) @ Q.T
+    Hh = 0.5 * (Hh + Hh.T)
+    Hp = torch.from_numpy(Hh).pin_memory()
+    Rp = torch.empty((dh, dh), dtype=torch.float64).pin_memory()
+    Rh, rh = nsr.ns_reflector_host(Hp, 0.0, 1.01, dh // 3, 100, 1e-10, 1, R=Rp)
+    Rd, rd = nsr.ns_reflector(torch.from_numpy(Hh).to(_dev()), 0.0, 1.01, dh // 3, 100, 1e-10, 1)
+    assert torch.equal(Rh, Rd.cpu()) and rh["steps"] == rd["steps"] and rh["cert"] == dh // 3
+    # fixed-depth odd cubic filter phi_m with random coefficients (sign-preserving range, P:278-289)
+    a = float(rng.uniform(1.2, 1.9))
+    b = 1.0 - a                                   # phi(1) = 1
+    m = int(rng.integers(1, 7))
+    dd = int(rng.choice([200, 384, 515]))
+    p = workloads.cfg0_controlled(seed=seed, d=dd, k=max(1, dd // 10))
+    R, res = nsr.ns_reflector(torch.from_numpy(p.H).to(_dev()), p.s, p.alpha, p.k, m, 0.0,
+                              options=nsr.ns_options(filter_a=a, filter_b=b))
+    Xo = setup.filter_fixed_depth(p.H, p.s, p.alpha, m, a, b)
+    assert res["steps"] == m
+    assert checks.frob_per_sqrt_d(R.cpu().numpy(), Xo) <= 1e-13
