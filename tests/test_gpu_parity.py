@@ -954,3 +954,28 @@ def test_random_sweep_sharded_host_filters(nsr, seed):
     Xo = setup.filter_fixed_depth(p.H, p.s, p.alpha, m, a, b)
     assert res["steps"] == m
     assert checks.frob_per_sqrt_d(R.cpu().numpy(), Xo) <= 1e-13
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_symm_products(nsr, seed):
+    """Kernel-level random sweep: random (ragged) d, mode 0/1/2, FP64 DMMA / Ozaki INT8 / BF16x3 cores vs
+    numpy FP64 products; symmetric modes bitwise symmetric; error bounds per arithmetic (FP64 and Ozaki
+    ~1e-13 relative to |A||B|, BF16x3 ~1e-5)."""
+    rng = np.random.default_rng(5000 + seed)
+    d = int(rng.integers(1, 700))
+    mode = int(rng.integers(0, 3))
+    prec = int(rng.choice([0, 3, 1]))
+    A = rng.standard_normal((d, d)) * 10.0 ** rng.uniform(-3, 3)
+    A = 0.5 * (A + A.T)
+    # mode 0 is the square (symmetric result: upper tiles + mirror), mode 1 needs B commuting with A
+    # (the NS update Z = X Y with Y = X^2), mode 2 is a general dense product of symmetric operands
+    B = A.copy() if mode == 0 else (A @ A if mode == 1 else rng.standard_normal((d, d)))
+    B = 0.5 * (B + B.T)
+    Ag, Bg = torch.from_numpy(A).to(_dev()), torch.from_numpy(B).to(_dev())
+    C = nsr.ns_symm_product(Ag, Bg, mode=mode, prec=prec).cpu().numpy()
+    ref = (1.5 * A - 0.5 * (A @ B)) if mode == 1 else (A @ B)
+    scale = np.max(np.abs(A)) * np.max(np.abs(B)) * d + (1.5 * np.max(np.abs(A)) if mode == 1 else 0.0)
+    tol = {0: 1e-14, 3: 1e-14, 1: 2e-5}[prec]
+    assert np.max(np.abs(C - ref)) <= tol * scale, (d, mode, prec)
+    if mode != 2:
+        assert np.array_equal(C, C.T)
