@@ -486,7 +486,7 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
   // whose rows and columns all lie in chunks <= c are launched right after (each CTA writes its partial
   // to the tile's slot of the full list: the decide's sum is unchanged), so the transfer of H overlaps
   // the first product instead of preceding it.
-  const bool chunked = opt.h_host != nullptr && batch == 1 && spec_ctx().ok;
+  const bool chunked = opt.h_host != nullptr;   // the host entry checked batch == 1 and the side stream
   const Layout* Lp = &L;
   ProdParams sq0{tiles, n_t, L.d_pad / kBK, L.d, L.d_pad, (long long)L.d_pad * L.d_pad, Y, nullptr, res, state, 0};
   if (chunked) {
@@ -1542,7 +1542,7 @@ ns_status_t ns_reflector_host(const double* H_host, int64_t d, int64_t ldh, doub
     const char* e = getenv("NS_H2D_CHUNKS");   // 0: stage H in one copy before the loop (A/B knob)
     return !(e && e[0] == '0');
   }();
-  const bool fp64_chunked = chunks_on && !mixed && !ozaki && small_dpad(d) == 0 && d >= 1024;
+  const bool fp64_chunked = chunks_on && !mixed && !ozaki && small_dpad(d) == 0 && d >= 1024 && spec_ctx().ok;
   if (!fp64_chunked)
     NS_CUDA(cudaMemcpy2DAsync(stage, (size_t)d * 8, H_host, (size_t)ldh * 8, (size_t)d * 8, (size_t)d,
                               cudaMemcpyHostToDevice, cs));
