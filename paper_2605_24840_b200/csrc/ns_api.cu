@@ -534,11 +534,15 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
         if (t64) NS_CUDA(cudaMemsetAsync(trp, 0, sizeof(double) * nb, st));
         NS_CUDA(launch_trace_partials(Xa, L.d, L.d_pad, 1, trp, st, nb));
       }
-      if (gstart[q + 1] > gstart[q]) {
+      // groups of the first half of the chunks run while the rest of H is in flight; the tiles of the
+      // later chunks go out as one launch once H is complete (separate launches per chunk would each
+      // end in a partial wave)
+      const int g0 = (q < nch / 2) ? q : nch / 2, g1 = (q < nch / 2) ? q + 1 : nch;
+      if ((q < nch / 2 || q == nch - 1) && gstart[g1] > gstart[g0]) {
         ProdParams g = sq0;
-        g.tiles = dperm + gstart[q];
-        g.n_tiles = gstart[q + 1] - gstart[q];
-        g.part_slot = dslot + gstart[q];
+        g.tiles = dperm + gstart[g0];
+        g.n_tiles = gstart[g1] - gstart[g0];
+        g.part_slot = dslot + gstart[g0];
         NS_CUDA(t64 ? launch_product64(tA0, tA0, g, 1, st) : launch_product(tA0, tA0, g, 1, st));
         nl += 1;
       }
