@@ -979,3 +979,57 @@ def test_random_symm_products(nsr, seed):
     assert np.max(np.abs(C - ref)) <= tol * scale, (d, mode, prec)
     if mode != 2:
         assert np.array_equal(C, C.T)
+
+
+@pytest.mark.parametrize("prec", [0, 1, 3])
+@pytest.mark.parametrize("d", [50, 300])
+def test_strided_inputs_and_outputs(nsr, prec, d):
+    """ldh > d and ldr > d (views into larger buffers): the result equals the contiguous call bitwise, and
+    the padding of R's buffer is left untouched."""
+    p = workloads.cfg0_controlled(seed=3, d=d, k=max(1, d // 10))
+    Hc = torch.from_numpy(p.H).to(_dev())
+    big = torch.full((d + 7, d + 37), float("nan"), dtype=torch.float64, device=_dev())
+    big[3:3 + d, 5:5 + d] = Hc
+    Hv = big[3:3 + d, 5:5 + d]
+    Rbig = torch.full((d + 3, d + 19), -7.0, dtype=torch.float64, device=_dev())
+    Rv = Rbig[1:1 + d, 2:2 + d]
+    Rv_out, r1 = nsr.ns_reflector(Hv, p.s, p.alpha, p.k, 100, 1e-12, R=Rv, prec=prec)
+    R2, r2 = nsr.ns_reflector(Hc, p.s, p.alpha, p.k, 100, 1e-12, prec=prec)
+    assert torch.equal(Rv, R2) and r1["steps"] == r2["steps"] and r1["cert"] == r2["cert"] == p.k
+    mask = torch.ones_like(Rbig, dtype=torch.bool)
+    mask[1:1 + d, 2:2 + d] = False
+    assert torch.all(Rbig[mask] == -7.0)
+    if prec == 0:   # host entry with strided host buffers
+        Hh = big.cpu()[3:3 + d, 5:5 + d]
+        Rh_big = torch.full((d + 3, d + 19), -7.0, dtype=torch.float64)
+        Rh, rh = nsr.ns_reflector_host(Hh, p.s, p.alpha, p.k, 100, 1e-12, R=Rh_big[1:1 + d, 2:2 + d])
+        assert torch.equal(Rh, R2.cpu()) and torch.all(Rh_big[mask.cpu()] == -7.0)
+
+
+@pytest.mark.parametrize("d", [1, 2, 95, 96, 97, 128, 129])
+def test_batched_size_boundaries(nsr, d):
+    """Batched entry around the fused small kernel's limit (d <= 96) and the tile edges: every problem
+    matches the oracle (steps / certificate / R) with its own shift and scale."""
+    rng = np.random.default_rng(6000 + d)
+    probs = []
+    for b in range(5):
+        lam = np.sort(rng.uniform(-1, 1, d))
+        lam[np.abs(lam) < 0.05] = 0.05
+        lam = np.sort(lam)
+        Q = workloads.haar_q(rng, d)
+        H = (Q * lam[None, :]) @ Q.T
+        H = 0.5 * (H + H.T)
+        kb = int(np.sum(lam < 0))
+        s = 0.0
+        alpha = float(np.max(np.abs(lam))) * float(rng.uniform(1.0, 1.3))
+        probs.append((H, s, alpha, kb))
+    Hs = torch.from_numpy(np.stack([p_[0] for p_ in probs])).to(_dev())
+    R, outs = nsr.ns_reflector_batched(Hs, [p_[1] for p_ in probs], [p_[2] for p_ in probs],
+                                       [p_[3] for p_ in probs], 100, 1e-12)
+    R = R.cpu().numpy()
+    for b, (H, s, alpha, kb) in enumerate(probs):
+        o = ons.ns_reflector(H, s, alpha, kb, 100, 1e-12, 0, trace_residuals=True)
+        assert outs[b]["cert"] == o["cert"] == kb
+        if not _tie_band(o["hist_residual"], 1e-12, o["steps"]):
+            assert outs[b]["steps"] == o["steps"], (b, outs[b], o["steps"])
+            assert checks.frob_per_sqrt_d(R[b], o["R"]) <= TOL_R
