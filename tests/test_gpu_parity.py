@@ -1033,3 +1033,16 @@ def test_batched_size_boundaries(nsr, d):
         if not _tie_band(o["hist_residual"], 1e-12, o["steps"]):
             assert outs[b]["steps"] == o["steps"], (b, outs[b], o["steps"])
             assert checks.frob_per_sqrt_d(R[b], o["R"]) <= TOL_R
+
+
+@pytest.mark.parametrize("scale", [1e-150, 1e150])
+@pytest.mark.parametrize("prec", [0, 1, 3])
+def test_extreme_value_scales(nsr, scale, prec):
+    """H, s and alpha scaled by 1e+-150: X_0 = (H - sI)/alpha is the same up to rounding, so the steps,
+    certificate and R match the unscaled run (no overflow / underflow anywhere on the path)."""
+    p = workloads.cfg0_controlled(seed=1, d=200, k=20)
+    R1, r1 = nsr.ns_reflector(torch.from_numpy(p.H).to(_dev()), p.s, p.alpha, p.k, 100, 1e-10, 1, prec=prec)
+    R2, r2 = nsr.ns_reflector(torch.from_numpy(p.H * scale).to(_dev()), p.s * scale, p.alpha * scale, p.k, 100,
+                              1e-10, 1, prec=prec)
+    assert r2["cert"] == r1["cert"] == p.k and r2["steps"] == r1["steps"] and r2["flags"] == r1["flags"]
+    assert checks.frob_per_sqrt_d(R2.cpu().numpy(), R1.cpu().numpy()) <= 1e-12
