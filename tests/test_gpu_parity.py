@@ -1046,3 +1046,25 @@ def test_extreme_value_scales(nsr, scale, prec):
                               1e-10, 1, prec=prec)
     assert r2["cert"] == r1["cert"] == p.k and r2["steps"] == r1["steps"] and r2["flags"] == r1["flags"]
     assert checks.frob_per_sqrt_d(R2.cpu().numpy(), R1.cpu().numpy()) <= 1e-12
+
+
+def test_cfg1_full_size(nsr):
+    """configs[1] at its full size exactly as tools/bench_configs.py times it: 2048 matrices x 3 shifts =
+    6144 problems of d = 256 in one batched call.  Every step count equals the scalar-recurrence
+    prediction on its spectrum (outside the +-1 tie band of C9), every certificate equals k, the midpoint
+    shift needs strictly fewer steps than both offset shifts, and the direction error vs the closed form
+    (prop:direrr) is <= 1e-12 on a sample of 64 problems."""
+    probs = workloads.cfg1_batched(seed=0, n_matrices=2048)
+    assert len(probs) == 6144
+    H = torch.from_numpy(np.stack([p_.H for p_ in probs])).to(_dev())
+    R, outs = nsr.ns_reflector_batched(H, [p_.s for p_ in probs], [p_.alpha for p_ in probs],
+                                       [p_.k for p_ in probs], 100, 1e-12)
+    steps = np.array([o_["steps"] for o_ in outs])
+    pred = np.array([scalar.predict_run((p_.lam - p_.s) / p_.alpha, 100, 1e-12, False)[0] for p_ in probs])
+    assert np.all(np.abs(steps - pred) <= 1) and np.mean(steps == pred) >= 0.99
+    assert all(o_["cert"] == p_.k for o_, p_ in zip(outs, probs))
+    assert np.all(steps[0::3] < np.minimum(steps[1::3], steps[2::3]))
+    for i in range(0, 6144, 96):
+        Ri = R[i].cpu().numpy()
+        Rc = closed_form.reflector_explicit_q(probs[i].Q, probs[i].lam, probs[i].s)
+        assert np.linalg.norm((Ri - Rc) @ probs[i].extra["probe"]) <= 1e-12, i
