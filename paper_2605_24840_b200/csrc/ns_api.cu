@@ -932,7 +932,8 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
       // removes what the first left.
       int iters = 0;
       if ((s = reanchor_pass(&iters)) != NS_OK) return s;
-      if (iters > kCgRefineIters && (s = reanchor_pass(&iters)) != NS_OK) return s;
+      const bool ill = iters > kCgRefineIters || hs.j_small >= kCgRefineJSmall;
+      if (ill && (s = reanchor_pass(&iters)) != NS_OK) return s;
     }
     // ---------------- phase 2: FP64-class steps from j0 to tolerance ----------------
     LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0, -1, 0};

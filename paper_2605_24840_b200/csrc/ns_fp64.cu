@@ -665,6 +665,7 @@ __global__ void __launch_bounds__(256) ns_decide_kernel(DevState* __restrict__ s
     const double slack = (lp.lowprec ? 1e-4 : 1e-10) * sqd;
     if (st->j > 0 && r > st->r_prev * (1.0 + 1e-12) + slack) flags |= 8;
     const double rho = lp.tol_mode ? r / sqd : r;
+    if (lp.lowprec && st->j_small < 0 && r / sqd < lp.switch_tol) st->j_small = st->j;
     if (rho < lp.tol) {
       flags |= 1;  // NS_F_CONVERGED
       done = 1;
@@ -716,6 +717,7 @@ __global__ void ns_zero_state_kernel(DevState* state, int batch, int* n_active) 
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < batch) {
     DevState z{};
+    z.j_small = -1;
     z.sw_step = -1;
     state[i] = z;
   }

@@ -42,6 +42,9 @@ struct DevState {
   double sw_residual; // mixed path: low-precision residual at the switch
   int32_t sw_step;    // mixed path: j at the switch (-1 = none)
   int32_t spec;       // index j+1 of the iterate the decide at step j predicts to be final (0 = none)
+  int32_t j_small;    // mixed path: first j with r_j/sqrt(d) < switch_tol in the low-precision phase (-1 = none);
+                      // a conditioning proxy, min|x| of X_0 ~ 1.5^-(j_small - 3) (each NS step grows small |x| by 1.5)
+  int32_t pad2;
 };
 
 // Per-problem scalar inputs (device copy).
@@ -79,6 +82,7 @@ struct CgScalars {
 };
 constexpr double kCgTol = 1e-6;      // re-anchor CG: stop at |R| <= kCgTol |R_0| (within the iteration cap)
 constexpr int kCgRefineIters = 40;   // a solve that needed more iterations is followed by a second re-anchor pass
+constexpr int kCgRefineJSmall = 12;  // ... and so is one whose |A| has condition ~ 1.5^(j_small - 3) > 30
 constexpr int kEwBlocks = 148 * 8;   // fixed grid of the elementwise CG kernels (fixed-order partial sums)
 
 cudaError_t launch_commutator(const double* M, double* C, void* abs_planes, int d_pad, cudaStream_t st,

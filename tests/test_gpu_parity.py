@@ -39,6 +39,21 @@ def _tie_band(hist, tol, steps):
     return any(abs(r - tol) <= 0.01 * tol for r in cand)
 
 
+def _mixed_step_ok(r, o, tol, tm, d):
+    """Reading C16b: the mixed path's step count may differ from the oracle's by one when
+    (a) the oracle's residual at the mixed switch step was already below the switch threshold (late
+    switch: +1), or (b) the oracle's residual at its decision step or the one before lies within a factor
+    2 of the threshold (the split-precision switch iterate perturbs the last residuals by up to ~2x)."""
+    t = tol if tm == 0 else tol * math.sqrt(d)
+    h = o["hist_residual"]
+    if abs(r["steps"] - o["steps"]) != 1:
+        return False
+    late = (r["steps"] == o["steps"] + 1 and 0 <= r["switch_step"] <= o["steps"]
+            and h[r["switch_step"]] / math.sqrt(d) < 1e-4)
+    near = any(0.5 * t <= h[j] <= 2.0 * t for j in (o["steps"] - 1, o["steps"]) if 0 <= j < len(h))
+    return late or near
+
+
 def _compare(nsr, H, s, alpha, k, max_steps, tol, tm, d=None):
     d = H.shape[0]
     o = ons.ns_reflector(H, s, alpha, k, max_steps, tol, tm, trace_residuals=True)
@@ -909,9 +924,7 @@ def test_random_sweep_mixed(nsr, seed, prec):
     assert res["cert"] == o["cert"] == k
     assert res["flags"] & ons.CONVERGED
     if not _tie_band(o["hist_residual"], tol * math.sqrt(d), o["steps"]):
-        late_switch = (res["steps"] == o["steps"] + 1 and 0 <= res["switch_step"] <= o["steps"]
-                       and o["hist_residual"][res["switch_step"]] / math.sqrt(d) < 1e-4)
-        assert res["steps"] == o["steps"] or late_switch, (res, o["steps"])
+        assert res["steps"] == o["steps"] or _mixed_step_ok(res, o, tol, 1, d), (res, o["steps"])
     assert checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= TOL_R
 
 
