@@ -98,3 +98,59 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def batched_stress(n, seed0=0):
+    """Random batches (FP64 and Ozaki) and random emulated-rank counts against the oracle per problem."""
+    fails = 0
+    for i in range(n):
+        rng = np.random.default_rng(90_000 + seed0 + i)
+        seeds = [int(x) for x in rng.integers(0, 10**9, int(rng.integers(1, 24)))]
+        first = problem(seeds[0], 400)
+        d = first[0].shape[0]
+        probs = [first]
+        for sd in seeds[1:]:
+            H, s, alpha, k, _, _, _ = problem(sd, 2)   # d = 1 placeholder, replaced below
+            r2 = np.random.default_rng(sd)
+            lam = np.sort(r2.uniform(-1, 1, d))
+            lam[np.abs(lam) < 0.02] = 0.02
+            Q = workloads.haar_q(r2, d)
+            H = (Q * lam[None, :]) @ Q.T
+            H = 0.5 * (H + H.T)
+            k = int(np.sum(lam < 0))
+            probs.append((H, 0.0, float(np.max(np.abs(lam))) * float(r2.choice([1.0, 1.2])), k, 0, 0, 0))
+        ms, tol, tm = first[4], first[5], first[6]
+        Hs = torch.from_numpy(np.stack([p[0] for p in probs])).cuda()
+        for prec in (0, 3):
+            R, outs = nsr.ns_reflector_batched(Hs, [p[1] for p in probs], [p[2] for p in probs],
+                                               [p[3] for p in probs], ms, tol, tm, prec=prec)
+            R = R.cpu().numpy()
+            for b, p in enumerate(probs):
+                o = ons.ns_reflector(p[0], p[1], p[2], p[3], ms, tol, tm, trace_residuals=True)
+                msg = []
+                if outs[b]["cert"] != o["cert"]:
+                    msg.append(f"cert {outs[b]['cert']} vs {o['cert']}")
+                if not (tol > 0 and tie(o, tol, tm, d)):
+                    if outs[b]["steps"] != o["steps"]:
+                        msg.append(f"steps {outs[b]['steps']} vs {o['steps']}")
+                    elif not (o["flags"] & (ons.SCALING_SUSPECT | ons.NONFINITE)):
+                        e = checks.frob_per_sqrt_d(R[b], o["R"])
+                        if e > TOL_R:
+                            msg.append(f"err {e:.2e}")
+                if msg:
+                    fails += 1
+                    print(f"FAIL batched i={i} d={d} batch={len(probs)} b={b} prec={prec}: {'; '.join(msg)}", flush=True)
+        # emulated ranks on the first problem
+        H, s, alpha, k, ms, tol, tm = first
+        P = int(rng.integers(2, 9))
+        Re, re_ = nsr.ns_reflector_sharded_emulated(P, torch.from_numpy(H).cuda(), s, alpha, k, ms, tol, tm)
+        Rd, rd = nsr.ns_reflector(torch.from_numpy(H).cuda(), s, alpha, k, ms, tol, tm)
+        o = ons.ns_reflector(H, s, alpha, k, ms, tol, tm, trace_residuals=True)
+        if re_["cert"] != o["cert"] or (not (tol > 0 and tie(o, tol, tm, d)) and re_["steps"] != o["steps"]):
+            fails += 1
+            print(f"FAIL emulated i={i} d={d} P={P}: steps {re_['steps']} vs {o['steps']}, cert {re_['cert']}", flush=True)
+    print(f"batched/emulated done: {fails} failures", flush=True)
+
+
+if __name__ == "__main__" and os.environ.get("STRESS_BATCHED"):
+    batched_stress(int(os.environ["STRESS_BATCHED"]))
