@@ -61,7 +61,9 @@ def problem(seed, dmax):
 def main():
     n64, noz, nmx, s0 = [int(x) for x in (sys.argv[1:] + ["120", "40", "30", "0"])[:4]]
     fails = 0
-    for path, n, dmax, precs in (("fp64", n64, 400, [0]), ("ozaki", noz, 400, [3]), ("mixed", nmx, 600, [1, 2])):
+    dm = int(os.environ.get("STRESS_DMAX", "0"))   # larger sizes (2-SM split-precision kernel, 128-tile paths)
+    for path, n, dmax, precs in (("fp64", n64, dm or 400, [0]), ("ozaki", noz, dm or 400, [3]),
+                                 ("mixed", nmx, dm or 600, [1, 2])):
         for i in range(n):
             seed = 10_000 * (1 + precs[0]) + s0 + i
             H, s, alpha, k, ms, tol, tm = problem(seed, dmax)
