@@ -320,7 +320,8 @@ def run_ours(args):
     mixed_oz = None
     if args.prec == "fp64" and not args.no_mixed and not args.sharded:
         mixed = secondary(nsr.NS_PREC_MIXED_BF16X3)
-        # the same mixed path with its re-anchor products and polishing steps on the Ozaki INT8 products
+        # mixed_mode: the default (re-anchor products on the Ozaki INT8 cores, FP64 DMMA polishing steps);
+        # the same mixed path with the polishing steps on the Ozaki INT8 products as well
         mixed_oz = secondary(nsr.NS_PREC_MIXED_BF16X3, nsr.ns_options(polish=1))
         if d <= 65536:
             ozaki = secondary(nsr.NS_PREC_FP64_OZAKI)

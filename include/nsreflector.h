@@ -107,8 +107,9 @@ typedef struct {
  *                  no FP64 steps); flags then carry neither CONVERGED nor MAX_STEPS.
  *   lookahead      steps enqueued before the host reads the stop flag (0 = default).
  *   polish         mixed path: arithmetic of the re-anchor's two dense products and of the
- *                  polishing steps: 0 = FP64 DMMA (default), 1 = FP64 emulated on the INT8 tensor
- *                  cores (the Ozaki products of NS_PREC_FP64_OZAKI).
+ *                  polishing steps: 0 = both FP64 DMMA, 1 = both FP64 emulated on the INT8 tensor
+ *                  cores (the Ozaki products of NS_PREC_FP64_OZAKI), 2 (default) = the
+ *                  re-anchor products emulated on INT8, the polishing steps FP64 DMMA.
  *   filter_a/b     the step X_{j+1} = a X_j + b X_j^3 (generic odd sign-preserving
  *                  filters; with tol = 0 and max_steps = m it is the fixed-depth filter phi_m).
  */

@@ -357,7 +357,7 @@ struct Opts {
   int cg_iters = 96;              // cap; the solve stops at the relative residual cg_tol()
   int stop_at_switch = 0;
   int lookahead = 0;
-  int polish = 0;                 // mixed path: 0 = FP64 DMMA re-anchor / polish, 1 = Ozaki INT8
+  int polish = 2;                 // mixed path: 0 = all FP64 DMMA, 1 = all Ozaki INT8, 2 = Ozaki re-anchor + DMMA polish
   double ca = 1.5, cb = -0.5;
   // host entry: the caller's pinned R (device-accessible address) for the speculative result copy;
   // run_loop sets *spec_hit when R already holds the returned iterate
@@ -849,8 +849,10 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
     const CUtensorMap& tXt = (j0 & 1) ? tmB : tmA;
     const CUtensorMap& tXo = (j0 & 1) ? tmA : tmB;
     const int nk = L.d_pad / kBK;
-    // polish = 1: the FP64-class products below run as Ozaki INT8 products (same operands / outputs)
-    const bool oz = (opt.polish == 1);
+    // polish 1: re-anchor products and polishing steps on the Ozaki INT8 products; 2: only the re-anchor's
+    // two dense products (the polishing steps stay FP64 DMMA)
+    const bool oz = (opt.polish >= 1);
+    const bool oz_steps = (opt.polish == 1);
     int8_t* slX = reinterpret_cast<int8_t*>(ws + L.off_ozx);
     int8_t* slY = reinterpret_cast<int8_t*>(ws + L.off_ozy);
     int* eX = reinterpret_cast<int*>(ws + L.off_oex);
@@ -939,7 +941,7 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
     LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0, -1, 0};
     const int one = 1;
     NS_CUDA(cudaMemcpyAsync(n_active, &one, sizeof(int), cudaMemcpyHostToDevice, st));
-    if (oz) {
+    if (oz_steps) {
       // Ozaki steps (as run_ozaki): symmetric 128x64 tile list, its residual / trace partial layouts
       const std::vector<int2> ot = oz_tile_list(L.n, true);
       const int nt = (int)ot.size(), npart = oz_partials(ot), ndiag = 2 * L.n;
@@ -971,7 +973,7 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
         NS_CUDA(cudaEventRecord(rg.ev[j % 16], st));
       }
     }
-    if (!oz) {
+    if (!oz_steps) {
     NS_CUDA(launch_trace_partials(Xt, L.d, L.d_pad, 1, trp, st));
     nl += 1;
     for (int j = j0; j <= max_steps; ++j) {
@@ -1461,6 +1463,7 @@ void ns_options_default(ns_options_t* o) {
   o->cg_iters = 96;
   o->stop_at_switch = 0;
   o->lookahead = 0;
+  o->polish = 2;
   o->filter_a = 1.5;
   o->filter_b = -0.5;
 }
@@ -1487,7 +1490,7 @@ ns_status_t ns_reflector_ex(const double* H, int64_t d, int64_t ldh, double s, d
   if (ws_bytes < L.total)
     return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
   const Opts o = to_opts(opts);
-  if (mixed && (!(o.switch_tol >= 0.0) || o.cg_iters < 0 || o.polish < 0 || o.polish > 1))
+  if (mixed && (!(o.switch_tol >= 0.0) || o.cg_iters < 0 || o.polish < 0 || o.polish > 2))
     return fail(NS_ERR_INVALID_ARG, "bad mixed options");
   if (!std::isfinite(o.ca) || !std::isfinite(o.cb)) return fail(NS_ERR_INVALID_ARG, "filter coefficients must be finite");
   if (mixed && (o.ca != 1.5 || o.cb != -0.5))

@@ -116,7 +116,7 @@ def cfg3(mode="tol", prec=nsr.NS_PREC_FP64, reps=3, polish=0):
     err = float(np.sqrt(np.mean(np.sum((Rg - Rc) ** 2, axis=0))))
     tf = (2 * res["steps"] + 1) * float(p.d) ** 3 / (ms * 1e-3) / 1e12
     emit({"config": "cfg3", "mode": mode, "prec": {0: "fp64", 1: "mixed_bf16x3", 2: "mixed_tf32x3",
-                                                   3: "fp64_ozaki_int8"}[prec] + ("+ozaki_polish" if polish else ""),
+                                                   3: "fp64_ozaki_int8"}[prec] + {0: "", 1: "+ozaki_polish", 2: "+ozaki_reanchor"}[polish],
           "d": p.d,
           "time_to_R_ms": ms, "steps": res["steps"], "cert": res["cert"], "flags": res["flags"],
           "switch_step": res["switch_step"], "tflops": tf, "frac_fp64_peak": tf / PEAK, "err_vs_closed_form": err,
@@ -193,6 +193,8 @@ def main():
             cfg3("fixed30", nsr.NS_PREC_MIXED_BF16X3, reps=1)
         elif w == "cfg3mixedoz":
             cfg3("tol", nsr.NS_PREC_MIXED_BF16X3, polish=1)
+        elif w == "cfg3mixedoz2":
+            cfg3("tol", nsr.NS_PREC_MIXED_BF16X3, polish=2)
         elif w == "cfg3fixedmixedoz":
             cfg3("fixed30", nsr.NS_PREC_MIXED_BF16X3, reps=1, polish=1)
         elif w == "cfg3tf32":
