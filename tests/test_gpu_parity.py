@@ -1081,3 +1081,25 @@ def test_cfg1_full_size(nsr):
         Ri = R[i].cpu().numpy()
         Rc = closed_form.reflector_explicit_q(probs[i].Q, probs[i].lam, probs[i].s)
         assert np.linalg.norm((Ri - Rc) @ probs[i].extra["probe"]) <= 1e-12, i
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_graded_matrices(nsr, seed):
+    """Graded H = D A D (D over 6 decades: rows of very different magnitude, which the Ozaki split scales
+    row by row), shift at the midpoint of a random gap: FP64 and Ozaki paths vs the oracle."""
+    rng = np.random.default_rng(70_000 + seed)
+    d = int(rng.integers(50, 300))
+    Dg = 10.0 ** rng.uniform(-6, 0, d)
+    A = rng.standard_normal((d, d))
+    H = (Dg[:, None] * (0.5 * (A + A.T))) * Dg[None, :]
+    lam = np.linalg.eigvalsh(H)
+    k = int(np.argmax(np.diff(lam)[: d - 1])) + 1          # the widest gap: converges within the cap
+    s = 0.5 * (lam[k - 1] + lam[k])
+    alpha = float(np.max(np.abs(lam - s))) * 1.01
+    o = ons.ns_reflector(H, s, alpha, k, 200, 1e-10, 1, trace_residuals=True)
+    for prec in (0, 3):
+        R, r = nsr.ns_reflector(torch.from_numpy(H).to(_dev()), s, alpha, k, 200, 1e-10, 1, prec=prec)
+        assert r["cert"] == o["cert"] == k
+        if not _tie_band(o["hist_residual"], 1e-10 * math.sqrt(d), o["steps"]):
+            assert r["steps"] == o["steps"]
+            assert checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= TOL_R

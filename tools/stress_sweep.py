@@ -156,3 +156,42 @@ def batched_stress(n, seed0=0):
 
 if __name__ == "__main__" and os.environ.get("STRESS_BATCHED"):
     batched_stress(int(os.environ["STRESS_BATCHED"]))
+
+
+def graded_stress(n, seed0=0):
+    """Graded matrices H = D A D (D log-uniform over 6 decades, A a random symmetric matrix): rows of very
+    different magnitude (the Ozaki split scales per row); shift at the midpoint of a random spectral gap."""
+    fails = 0
+    for i in range(n):
+        rng = np.random.default_rng(70_000 + seed0 + i)
+        d = int(rng.integers(2, 400))
+        Dg = 10.0 ** rng.uniform(-6, 0, d)
+        A = rng.standard_normal((d, d))
+        H = (Dg[:, None] * (0.5 * (A + A.T))) * Dg[None, :]
+        lam = np.linalg.eigvalsh(H)
+        k = int(rng.integers(1, d))
+        s = 0.5 * (lam[k - 1] + lam[k])
+        alpha = float(np.max(np.abs(lam - s))) * 1.01
+        tol, tm = 1e-10, 1
+        o = ons.ns_reflector(H, s, alpha, k, 200, tol, tm, trace_residuals=True)
+        for prec in (0, 3):
+            R, r = nsr.ns_reflector(torch.from_numpy(H).cuda(), s, alpha, k, 200, tol, tm, prec=prec)
+            msg = []
+            if r["cert"] != o["cert"]:
+                msg.append(f"cert {r['cert']} vs {o['cert']}")
+            if not tie(o, tol, tm, d):
+                if r["steps"] != o["steps"]:
+                    msg.append(f"steps {r['steps']} vs {o['steps']}")
+                elif o["flags"] & ons.CONVERGED:
+                    e = checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"])
+                    if e > TOL_R:
+                        msg.append(f"err {e:.2e}")
+            if msg:
+                fails += 1
+                print(f"FAIL graded i={i} d={d} k={k} prec={prec} flags={r['flags']}/{o['flags']}: {'; '.join(msg)}",
+                      flush=True)
+    print(f"graded done: {fails} failures", flush=True)
+
+
+if __name__ == "__main__" and os.environ.get("STRESS_GRADED"):
+    graded_stress(int(os.environ["STRESS_GRADED"]))
