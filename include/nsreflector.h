@@ -102,7 +102,7 @@ typedef struct {
  *                  ||X_j^2 - I||_F / sqrt(d) < switch_tol (default 1e-4, reading C16).
  *   cg_iters       mixed path: maximum conjugate-gradient iterations of the re-anchor solve
  *                  |A|E + E|A| = sym(X~ [A, X~]); the solve stops earlier once its residual
- *                  has dropped by 1e-6 (default cap 96; 0 = polish without re-anchor).
+ *                  has dropped by 1e-6 (default cap 512; 0 = polish without re-anchor).
  *   stop_at_switch mixed path: return the pre-polish iterate X_switch as R (no re-anchor,
  *                  no FP64 steps); flags then carry neither CONVERGED nor MAX_STEPS.
  *   lookahead      steps enqueued before the host reads the stop flag (0 = default).

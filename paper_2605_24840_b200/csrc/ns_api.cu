@@ -354,7 +354,7 @@ ns_status_t check_common(int64_t d, int32_t max_steps, double tol, ns_tolmode_t 
 
 struct Opts {
   double switch_tol = 1e-4;
-  int cg_iters = 96;              // cap; the solve stops at the relative residual cg_tol()
+  int cg_iters = 512;             // cap; the solve stops at the relative residual cg_tol()
   int stop_at_switch = 0;
   int lookahead = 0;
   int polish = 2;                 // mixed path: 0 = all FP64 DMMA, 1 = all Ozaki INT8, 2 = Ozaki re-anchor + DMMA polish
@@ -901,7 +901,15 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
       NS_CUDA(launch_cg_scalar(cgsc, cgpart, np, 0, st, cg_tol() * cg_tol()));
       NS_CUDA(launch_split_planes(Pc, PXa, L.d_pad, 1, st, tf32));
       nl += 4;
+      // The host stops enqueuing iterations kCgLag iterations after the device flagged convergence (the
+      // flag is read back through the status ring); launches already queued return at once.
+      constexpr int kCgLag = 2;
       for (int it = 0; it < opt.cg_iters; ++it) {
+        if (it >= kCgLag) {
+          const int slot = (it - kCgLag) % 16;
+          NS_CUDA(cudaEventSynchronize(rg.ev[slot]));
+          if (rg.slots[slot] != 0) break;
+        }
         // W = |A| P (BF16x3 tcgen05, every tile) -> Xo
         MxParams pw{mx_full, mx_nfull, mx_nkb, L.d, L.d_pad, 0, Xo, nullptr, nullptr, nullptr, nullptr, 2, tf32 ? 1 : 0};
         pw.skip = &cgsc->done;
@@ -915,6 +923,8 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
           NS_CUDA(launch_cg_direction(Pc, Rc, cgsc, PXa, L.d_pad, st, tf32));
           nl += 1;
         }
+        NS_CUDA(cudaMemcpyAsync(&rg.slots[it % 16], &cgsc->done, sizeof(int), cudaMemcpyDeviceToHost, st));
+        NS_CUDA(cudaEventRecord(rg.ev[it % 16], st));
       }
       NS_CUDA(launch_apply_correction(Xt, E, L.d_pad, st));
       nl += 1;
@@ -934,7 +944,10 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
       // removes what the first left.
       int iters = 0;
       if ((s = reanchor_pass(&iters)) != NS_OK) return s;
-      const bool ill = iters > kCgRefineIters || hs.j_small >= kCgRefineJSmall;
+      // ... and for d <= kCgRefineMaxD always: there a pass costs a few ms, and the split-precision
+      // operator's error floor can reach 1e-10 even at cfg3-like conditioning (randomised stress: d = 278,
+      // min|x| = 0.048, 1.3e-10 after one pass, 4e-14 after two)
+      const bool ill = iters > kCgRefineIters || hs.j_small >= kCgRefineJSmall || L.d <= kCgRefineMaxD;
       if (ill && (s = reanchor_pass(&iters)) != NS_OK) return s;
     }
     // ---------------- phase 2: FP64-class steps from j0 to tolerance ----------------
@@ -1460,7 +1473,7 @@ void ns_options_default(ns_options_t* o) {
   if (!o) return;
   *o = ns_options_t{};
   o->switch_tol = 1e-4;
-  o->cg_iters = 96;
+  o->cg_iters = 512;
   o->stop_at_switch = 0;
   o->lookahead = 0;
   o->polish = 2;

@@ -82,11 +82,13 @@ struct CgScalars {
 };
 constexpr double kCgTol = 1e-6;      // re-anchor CG: stop at |R| <= kCgTol |R_0| (within the iteration cap)
 constexpr int kCgRefineIters = 40;   // a solve that needed more iterations is followed by a second re-anchor pass
-constexpr int kCgRefineJSmall = 12;  // ... and so is one whose |A| has condition ~ 1.5^(j_small - 3) > 30
+constexpr int kCgRefineJSmall = 12;
+constexpr int kCgRefineMaxD = 2048;  // ... and every run with d <= this (the second pass is cheap there)  // ... and so is one whose |A| has condition ~ 1.5^(j_small - 3) > 30
 constexpr int kEwBlocks = 148 * 8;   // fixed grid of the elementwise CG kernels (fixed-order partial sums)
 
+// C = M - M^T, |A| = sym(M) planes; with partial: per-block ||C||_F^2 partials (n_partial of them)
 cudaError_t launch_commutator(const double* M, double* C, void* abs_planes, int d_pad, cudaStream_t st,
-                              bool tf32 = false);
+                              bool tf32 = false, double* partial = nullptr, int* n_partial = nullptr);
 cudaError_t launch_cg_init(const double* Fp, double* R, double* P, double* E, double* partial, int d_pad,
                            cudaStream_t st, int* n_partial);
 cudaError_t launch_cg_pw(const double* P, const double* W, double* partial, int d_pad, cudaStream_t st,

@@ -84,7 +84,8 @@ __device__ __forceinline__ void tile_pair(int b, int nb, int& bi, int& bj) {
 // C = M - M^T,  |A| = (M + M^T)/2 -> bf16 hi/lo planes (the CG operator's left factor).
 template <bool TF32>
 __global__ void __launch_bounds__(256) ns_commutator_kernel(const double* __restrict__ M, double* __restrict__ C,
-                                                            void* __restrict__ abs_planes, int d_pad) {
+                                                            void* __restrict__ abs_planes, int d_pad,
+                                                            double* __restrict__ partial) {
   __shared__ double ta[32][33], tb[32][33];
   const int nb = d_pad / 32;
   int bi, bj;
@@ -96,12 +97,14 @@ __global__ void __launch_bounds__(256) ns_commutator_kernel(const double* __rest
     tb[y][tx] = M[(long long)(bj * 32 + y) * d_pad + bi * 32 + tx];
   }
   __syncthreads();
+  double acc = 0.0;
   for (int y = ty; y < 32; y += 8) {
     // element (bi*32+y, bj*32+tx): M_ij = ta[y][tx], M_ji = tb[tx][y]
     const double mij = ta[y][tx], mji = tb[tx][y];
     const long long g1 = (long long)(bi * 32 + y) * d_pad + bj * 32 + tx;
     const long long g2 = (long long)(bj * 32 + y) * d_pad + bi * 32 + tx;
     C[g1] = mij - mji;
+    acc += (bi == bj ? 1.0 : 2.0) * (mij - mji) * (mij - mji);   // ||C||_F^2: the mirror tile counts once more
     put_planes<TF32>(0.5 * (mij + mji), abs_planes, g1, np);
     if (bi != bj) {
       const double nij = tb[y][tx], nji = ta[tx][y];   // element (bj*32+y, bi*32+tx)
@@ -109,6 +112,7 @@ __global__ void __launch_bounds__(256) ns_commutator_kernel(const double* __rest
       put_planes<TF32>(0.5 * (nij + nji), abs_planes, g2, np);
     }
   }
+  if (partial != nullptr) block_partial(acc, partial);
 }
 
 // F = -(F' + F'^T)/2 with F' = X~ C^T = -X~ C;  R = P = F, E = 0;  partial <R, R>.
@@ -246,9 +250,11 @@ static int n_pairs(int d_pad) {
   return nb * (nb + 1) / 2;
 }
 
-cudaError_t launch_commutator(const double* M, double* C, void* abs_planes, int d_pad, cudaStream_t st, bool tf32) {
-  if (tf32) ns_commutator_kernel<true><<<n_pairs(d_pad), 256, 0, st>>>(M, C, abs_planes, d_pad);
-  else ns_commutator_kernel<false><<<n_pairs(d_pad), 256, 0, st>>>(M, C, abs_planes, d_pad);
+cudaError_t launch_commutator(const double* M, double* C, void* abs_planes, int d_pad, cudaStream_t st, bool tf32,
+                              double* partial, int* n_partial) {
+  if (n_partial) *n_partial = n_pairs(d_pad);
+  if (tf32) ns_commutator_kernel<true><<<n_pairs(d_pad), 256, 0, st>>>(M, C, abs_planes, d_pad, partial);
+  else ns_commutator_kernel<false><<<n_pairs(d_pad), 256, 0, st>>>(M, C, abs_planes, d_pad, partial);
   return cudaGetLastError();
 }
 

@@ -12,7 +12,7 @@ import paper_2605_24840_b200 as nsr  # noqa: E402
 from oracle import checks, ns as ons  # noqa: E402
 from stress_sweep import problem  # noqa: E402
 for seed in [int(x) for x in sys.argv[1:]]:
-    H, s, alpha, k, ms, tol, tm = problem(seed, 600)
+    H, s, alpha, k, ms, tol, tm = problem(seed, int(os.environ.get("STRESS_DMAX", "600")))
     d = H.shape[0]
     alpha = max(alpha, float(np.linalg.norm(H - s * np.eye(d), 2)) * 1.01)
     ev = np.linalg.eigvalsh((H - s * np.eye(d)) / alpha)
