@@ -83,7 +83,11 @@ def main():
                 msg = []
                 if r["cert"] != o["cert"]:
                     msg.append(f"cert {r['cert']} vs {o['cert']}")
-                if not (tol > 0 and tie(o, tol, tm, d)):
+                # the Ozaki products' residual floor is ~1.5e-15 d (absolute; FP64 DMMA: ~3e-17 d, DESIGN Ozaki
+                # section): tolerances within 10x of it are not expected to give the oracle's step count
+                t_abs = tol if tm == 0 else tol * math.sqrt(d)
+                below_floor = path == "ozaki" and tol > 0 and t_abs < 1.5e-14 * d
+                if not (tol > 0 and tie(o, tol, tm, d)) and not below_floor:
                     ok_steps = r["steps"] == o["steps"] or (path == "mixed" and mixed_step_ok(r, o, tol, tm, d))
                     if not ok_steps:
                         msg.append(f"steps {r['steps']} vs {o['steps']}")
@@ -195,3 +199,35 @@ def graded_stress(n, seed0=0):
 
 if __name__ == "__main__" and os.environ.get("STRESS_GRADED"):
     graded_stress(int(os.environ["STRESS_GRADED"]))
+
+
+def host_stress(n, seed0=0):
+    """Host entry (pinned: chunked staging + speculative copy; pageable: plain copies) vs the device entry,
+    bitwise, on random problems of the chunked-path sizes."""
+    fails = 0
+    for i in range(n):
+        rng = np.random.default_rng(80_000 + seed0 + i)
+        H, s, alpha, k, ms, tol, tm = problem(80_000 + seed0 + i, 2)
+        d = int(rng.integers(1024, 3000))
+        lam = np.concatenate([-rng.uniform(0.01, 1.0, d // 4), rng.uniform(0.01, 1.0, d - d // 4)])
+        Q = workloads.haar_q(rng, d)
+        H = (Q * lam[None, :]) @ Q.T
+        H = 0.5 * (H + H.T)
+        s, alpha, k = 0.0, 1.0 * float(rng.choice([1.0, 1.3])), d // 4
+        ms, tol, tm = int(rng.choice([5, 30, 100])), float(rng.choice([0.0, 1e-10, 1e-12])), int(rng.integers(0, 2))
+        pinned = bool(rng.integers(0, 2))
+        Hh = torch.from_numpy(H)
+        Rh = torch.empty((d, d), dtype=torch.float64)
+        if pinned:
+            Hh, Rh = Hh.pin_memory(), Rh.pin_memory()
+        Rh, rh = nsr.ns_reflector_host(Hh, s, alpha, k, ms, tol, tm, R=Rh)
+        Rd, rd = nsr.ns_reflector(torch.from_numpy(H).cuda(), s, alpha, k, ms, tol, tm)
+        same = torch.equal(Rh, Rd.cpu()) and all(rh[q] == rd[q] for q in ("steps", "flags", "cert", "residual"))
+        if not same:
+            fails += 1
+            print(f"FAIL host i={i} d={d} pinned={pinned} ms={ms} tol={tol}: {rh} vs {rd}", flush=True)
+    print(f"host done: {fails} failures", flush=True)
+
+
+if __name__ == "__main__" and os.environ.get("STRESS_HOST"):
+    host_stress(int(os.environ["STRESS_HOST"]))
