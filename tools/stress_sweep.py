@@ -220,12 +220,13 @@ def host_stress(n, seed0=0):
         Rh = torch.empty((d, d), dtype=torch.float64)
         if pinned:
             Hh, Rh = Hh.pin_memory(), Rh.pin_memory()
-        Rh, rh = nsr.ns_reflector_host(Hh, s, alpha, k, ms, tol, tm, R=Rh)
-        Rd, rd = nsr.ns_reflector(torch.from_numpy(H).cuda(), s, alpha, k, ms, tol, tm)
+        prec = int(rng.choice([0, 0, 1, 3]))
+        Rh, rh = nsr.ns_reflector_host(Hh, s, alpha, k, ms, tol, tm, R=Rh, prec=prec)
+        Rd, rd = nsr.ns_reflector(torch.from_numpy(H).cuda(), s, alpha, k, ms, tol, tm, prec=prec)
         same = torch.equal(Rh, Rd.cpu()) and all(rh[q] == rd[q] for q in ("steps", "flags", "cert", "residual"))
         if not same:
             fails += 1
-            print(f"FAIL host i={i} d={d} pinned={pinned} ms={ms} tol={tol}: {rh} vs {rd}", flush=True)
+            print(f"FAIL host i={i} d={d} prec={prec} pinned={pinned} ms={ms} tol={tol}: {rh} vs {rd}", flush=True)
     print(f"host done: {fails} failures", flush=True)
 
 
