@@ -232,6 +232,9 @@ cudaError_t launch_outer(const double* Q, int d, const int* k, const double* x0,
 
 // ---------------- Ozaki-split FP64 products on INT8 tensor cores (ns_ozaki.cu) ----------------
 constexpr int kOzSlices = 7;                           // balanced base-256 int8 digits per entry (54 bits)
+// digit-pair groups kept per launch (OzParams.groups, pairs s + t < groups): 7 keeps the 28 pairs of weight
+// >= 2^-48; 8 adds the six pairs of weight 2^-56 (+21% MACs; the eighth INT32 group fills TMEM columns
+// 448..511), which lowers the dropped-pair residual floor from ~1.5e-15 d to ~4e-17 d (FP64 DMMA: 3e-17 d)
 constexpr int kOzChunkKb = 256;                        // k-blocks (x64) per INT32 chunk: exact for any d
 constexpr int kOzMaxD = 65536;
 #ifndef NS_OZ_KH
@@ -269,6 +272,7 @@ struct OzParams {
   int kb0 = 0;             // first k-block of this launch (K segments, see launch_ozaki_product)
   int pm = 0;              // 0 whole K; K segments: 1 first (C = raw sums), 2 middle (C += raw), 3 last (C + raw -> epilogue)
   int dbg = 0;             // experiments only (NS_OZ_DBG): 1 = stream operands without issuing the UMMAs
+  int groups = 7;          // digit-pair groups kept (7 or 8, see kOzSlices)
 };
 constexpr int kOzBadRow = 1 << 20;   // row exponent marking a non-finite row (its products become NaN)
 constexpr int kOzSegKb = 256;   // k-blocks per K segment (K = 16384): one launch per segment for larger d

@@ -153,7 +153,7 @@ __device__ __forceinline__ uint64_t sdesc_k64(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | (1ull << 16) | (sbo << 32) | (1ull << 46) | (lay << 61);
 }
 
-template <int MODE, bool MC>
+template <int MODE, bool MC, int G>
 __global__ void __launch_bounds__(kOzThreads, 1)
     ns_ozaki_product_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                             const OzParams p, int n_items) {
@@ -259,17 +259,29 @@ __global__ void __launch_bounds__(kOzThreads, 1)
             // Digit pairs (sa, sb), sb = sb0 .. sb0+n-1, share the A digit: the B digit slabs are stored
             // back to back (64 rows each), so rows [64 sb0, 64 (sb0+n)) form ONE K-major operand of
             // N = 64 n whose output columns are exactly the group accumulators sa+sb0 .. sa+sb0+n-1.
-            // 28 pairs become 10 UMMAs (N = 64..256) per K=32 half, with the same MACs.
+            // 28 pairs (34 with the eighth group) become 10 (15) UMMAs (N = 64..256) per K=32 half.
 #pragma unroll
             for (int h = 0; h < kOzKH / 32; ++h) {
 #pragma unroll
               for (int sa = 0; sa < kOzSlices; ++sa) {
-#pragma unroll
-                for (int sb0 = 0; sb0 < kOzSlices - sa; sb0 += 4) {
-                  const int n = min(4, kOzSlices - sa - sb0);
+                const int nb = min(kOzSlices, G - sa);   // B digits paired with A digit sa (s + t < G)
+                auto issue = [&](int sb, int n, uint32_t acc) {
                   const uint32_t idesc = idesc_base | ((uint32_t)(64 * n >> 3) << 17);
-                  umma_i8(tmem + (uint32_t)(64 * (sa + sb0)), sdesc_k64(a0 + sa * kOzSlabA + 32 * h),
-                          sdesc_k64(b0 + sb0 * kOzSlabB + 32 * h), idesc, (sa == 0 && h == 0) ? first : 1u);
+                  umma_i8(tmem + (uint32_t)(64 * (sa + sb)), sdesc_k64(a0 + sa * kOzSlabA + 32 * h),
+                          sdesc_k64(b0 + sb * kOzSlabB + 32 * h), idesc, acc);
+                };
+#pragma unroll
+                for (int sb0 = 0; sb0 < nb; sb0 += 4) {
+                  const int n = min(4, nb - sb0);
+                  const uint32_t acc = (sa == 0 && h == 0) ? first : 1u;
+                  if (G > kOzSlices && sa == 1 && sb0 + n == nb) {
+                    // the eighth group (s + t = 7) is first written by pair (1, 6): that column block
+                    // starts the chunk on its own UMMA, the rest of the range accumulates
+                    if (n > 1) issue(sb0, n - 1, acc);
+                    issue(nb - 1, 1, h == 0 ? first : 1u);
+                  } else {
+                    issue(sb0, n, acc);
+                  }
                 }
               }
             }
@@ -299,7 +311,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
         mbar_wait(tfull, cg & 1u);
         tc_fence_after();
 #pragma unroll 1
-        for (int g = kOzSlices - 1; g >= 0; --g) {      // smallest weights first
+        for (int g = G - 1; g >= 0; --g) {      // smallest weights first
           const double w = ldexp(1.0, -8 * g);
           uint32_t v[32];
           tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(g * 64 + hc * 32), v);   // one wait per group
@@ -431,9 +443,34 @@ cudaError_t launch_ozaki_slice(const double* X, int8_t* slices, int* expo, int d
   return cudaGetLastError();
 }
 
+// one persistent launch of the product kernel; MC: clusters of 2 CTAs on 128 x 128 tiles (p.tiles holds
+// (I, J) of 128-column blocks)
+template <int MODE, bool MC, int G>
+static cudaError_t oz_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const OzParams& p, int n_items, dim3 grid,
+                             cudaStream_t st) {
+  static unsigned long long attr = 0;
+  smem_attr(ns_ozaki_product_kernel<MODE, MC, G>, kOzSmemBytes, attr);
+  if (MC) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kOzThreads);
+    cfg.dynamicSmemBytes = kOzSmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, ns_ozaki_product_kernel<MODE, MC, G>, tmA, tmB, p, n_items);
+  }
+  ns_ozaki_product_kernel<MODE, MC, G><<<grid, kOzThreads, kOzSmemBytes, st>>>(tmA, tmB, p, n_items);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_ozaki_product(const CUtensorMap& tmA, const CUtensorMap& tmB, const OzParams& p, int batch,
                                  cudaStream_t st) {
-  static unsigned long long attr[3] = {0, 0, 0}, attr_mc[3] = {0, 0, 0};
   static int n_sm = 0;
   if (n_sm == 0) {
     int dev = 0;
@@ -466,49 +503,23 @@ cudaError_t launch_ozaki_product(const CUtensorMap& tmA, const CUtensorMap& tmB,
     return cudaSuccess;
   }
   const int n_items = p.n_tiles * batch;
-  if (use_oz_mc()) {
-    // clusters of 2 CTAs on 128 x 128 tiles (p.tiles holds (I, J) of 128-column blocks); persistent
-    const int n_cl = std::min(n_items, n_sm / 2);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * n_cl);
-    cfg.blockDim = dim3(kOzThreads);
-    cfg.dynamicSmemBytes = kOzSmemBytes;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    switch (p.mode) {
-      case 0:
-        smem_attr(ns_ozaki_product_kernel<0, true>, kOzSmemBytes, attr_mc[0]);
-        return cudaLaunchKernelEx(&cfg, ns_ozaki_product_kernel<0, true>, tmA, tmB, p, n_items);
-      case 1:
-        smem_attr(ns_ozaki_product_kernel<1, true>, kOzSmemBytes, attr_mc[1]);
-        return cudaLaunchKernelEx(&cfg, ns_ozaki_product_kernel<1, true>, tmA, tmB, p, n_items);
-      default:
-        smem_attr(ns_ozaki_product_kernel<2, true>, kOzSmemBytes, attr_mc[2]);
-        return cudaLaunchKernelEx(&cfg, ns_ozaki_product_kernel<2, true>, tmA, tmB, p, n_items);
-    }
+  const bool mc = use_oz_mc();
+  const dim3 grid = mc ? dim3(2 * std::min(n_items, n_sm / 2)) : dim3(std::min(n_items, n_sm));
+  const int g8 = (p.groups > kOzSlices) ? 1 : 0;
+  switch ((p.mode == 0 ? 0 : p.mode == 1 ? 1 : 2) * 4 + (mc ? 2 : 0) + g8) {
+    case 0: return oz_launch<0, false, 7>(tmA, tmB, p, n_items, grid, st);
+    case 1: return oz_launch<0, false, 8>(tmA, tmB, p, n_items, grid, st);
+    case 2: return oz_launch<0, true, 7>(tmA, tmB, p, n_items, grid, st);
+    case 3: return oz_launch<0, true, 8>(tmA, tmB, p, n_items, grid, st);
+    case 4: return oz_launch<1, false, 7>(tmA, tmB, p, n_items, grid, st);
+    case 5: return oz_launch<1, false, 8>(tmA, tmB, p, n_items, grid, st);
+    case 6: return oz_launch<1, true, 7>(tmA, tmB, p, n_items, grid, st);
+    case 7: return oz_launch<1, true, 8>(tmA, tmB, p, n_items, grid, st);
+    case 8: return oz_launch<2, false, 7>(tmA, tmB, p, n_items, grid, st);
+    case 9: return oz_launch<2, false, 8>(tmA, tmB, p, n_items, grid, st);
+    case 10: return oz_launch<2, true, 7>(tmA, tmB, p, n_items, grid, st);
+    default: return oz_launch<2, true, 8>(tmA, tmB, p, n_items, grid, st);
   }
-  const dim3 grid(std::min(n_items, n_sm));   // persistent: one CTA per SM
-  switch (p.mode) {
-    case 0:
-      smem_attr(ns_ozaki_product_kernel<0, false>, kOzSmemBytes, attr[0]);
-      ns_ozaki_product_kernel<0, false><<<grid, kOzThreads, kOzSmemBytes, st>>>(tmA, tmB, p, n_items);
-      break;
-    case 1:
-      smem_attr(ns_ozaki_product_kernel<1, false>, kOzSmemBytes, attr[1]);
-      ns_ozaki_product_kernel<1, false><<<grid, kOzThreads, kOzSmemBytes, st>>>(tmA, tmB, p, n_items);
-      break;
-    default:
-      smem_attr(ns_ozaki_product_kernel<2, false>, kOzSmemBytes, attr[2]);
-      ns_ozaki_product_kernel<2, false><<<grid, kOzThreads, kOzSmemBytes, st>>>(tmA, tmB, p, n_items);
-      break;
-  }
-  return cudaGetLastError();
 }
 
 }  // namespace nsr

@@ -86,7 +86,7 @@ def main():
                 # the Ozaki products' residual floor is ~1.5e-15 d (absolute; FP64 DMMA: ~3e-17 d, DESIGN Ozaki
                 # section): tolerances within 10x of it are not expected to give the oracle's step count
                 t_abs = tol if tm == 0 else tol * math.sqrt(d)
-                below_floor = path == "ozaki" and tol > 0 and t_abs < 1.5e-14 * d
+                below_floor = path == "ozaki" and tol > 0 and t_abs < 5e-16 * d   # 8-group floor ~4e-17 d
                 if not (tol > 0 and tie(o, tol, tm, d)) and not below_floor:
                     ok_steps = r["steps"] == o["steps"] or (path == "mixed" and mixed_step_ok(r, o, tol, tm, d))
                     if not ok_steps:
