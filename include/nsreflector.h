@@ -54,8 +54,11 @@ typedef enum {
   NS_PREC_FP64 = 0,          /* FP64 DMMA contraction (accuracy path) */
   NS_PREC_MIXED_BF16X3 = 1,  /* tcgen05 BF16x3 steps -> switch -> re-anchor -> FP64 steps (C16) */
   NS_PREC_MIXED_TF32X3 = 2,  /* as MIXED_BF16X3 with TF32 hi/lo splits (tcgen05 kind::tf32; more margin, half rate) */
-  NS_PREC_FP64_OZAKI = 3     /* FP64-accurate products emulated on tcgen05 INT8 (Ozaki split, 7 slices);
-                                SURVEY N4; single problem, d <= 16384 (INT32 group sums stay exact) */
+  NS_PREC_FP64_OZAKI = 3     /* FP64-accurate products emulated on tcgen05 INT8 (Ozaki split, 7 balanced
+                                base-256 digits, 28 digit pairs -- 34 when the tolerance is below 1e-13 d
+                                in absolute terms, which lowers the residual floor from ~1.5e-15 d to
+                                ~4e-17 d); single or batched, d <= 65536 (K segments of 16384
+                                keep the INT32 group sums exact) */
 } ns_precision_t;
 
 typedef enum {
