@@ -152,19 +152,29 @@ def _check(st):
         raise NsError(f"{lib.ns_status_string(st).decode()}: {lib.ns_last_error().decode()}")
 
 
+_TORCH = None
+_RAW_STREAM = None
+
+
 def _torch():
-    import torch
-    return torch
+    global _TORCH
+    if _TORCH is None:      # imported lazily (the package itself does not need torch), then cached:
+        import torch        # this sits on the small-d latency path, several calls per reflector
+        _TORCH = torch
+    return _TORCH
 
 
 def _stream_ptr(stream, device=None):
     """cudaStream_t of `stream`, or of torch's current stream on `device` (the raw-handle query avoids
     building a torch.cuda.Stream object: ~3 us per call on the small-d latency path)."""
+    global _RAW_STREAM
     torch = _torch()
     if stream is not None:
         return ctypes.c_void_p(stream.cuda_stream)
-    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
-    if raw is not None:
+    if _RAW_STREAM is None:
+        _RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", False)
+    raw = _RAW_STREAM
+    if raw:
         idx = device.index if device is not None and device.index is not None else torch.cuda.current_device()
         return ctypes.c_void_p(raw(idx))
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
