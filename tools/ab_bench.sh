@@ -1,3 +1,4 @@
+# needs a second build: git worktree add build_ab/old <rev> && (cd build_ab/old && python paper_2605_24840_b200/build.py)
 # alternate the in-tree library and build_ab/old's on the bench (FP64 cfg3), printing product kernel times
 for v in new old new old; do
   if [ $v = new ]; then L=paper_2605_24840_b200/libnsreflector.so; else L=build_ab/old/paper_2605_24840_b200/libnsreflector.so; fi
