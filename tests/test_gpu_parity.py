@@ -1103,3 +1103,40 @@ def test_graded_matrices(nsr, seed):
         if not _tie_band(o["hist_residual"], 1e-10 * math.sqrt(d), o["steps"]):
             assert r["steps"] == o["steps"]
             assert checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= TOL_R
+
+
+def test_ozaki_tight_absolute_tolerance(nsr):
+    """An absolute tolerance below the 7-group Ozaki residual floor (~1.5e-15 d): the run keeps the eighth
+    digit-pair group and converges in the oracle's step count (d = 2048, tol 1e-12 absolute)."""
+    rng = np.random.default_rng(81)
+    d = 2048
+    lam = np.concatenate([-rng.uniform(0.02, 1.0, d // 4), rng.uniform(0.02, 1.0, d - d // 4)])
+    Q = workloads.haar_q(rng, d)
+    H = (Q * lam[None, :]) @ Q.T
+    H = 0.5 * (H + H.T)
+    o = ons.ns_reflector(H, 0.0, 1.01, d // 4, 100, 1e-12, 0, trace_residuals=True)
+    R, r = nsr.ns_reflector(torch.from_numpy(H).to(_dev()), 0.0, 1.01, d // 4, 100, 1e-12, 0,
+                            prec=nsr.NS_PREC_FP64_OZAKI)
+    assert r["flags"] & ons.CONVERGED and r["cert"] == d // 4
+    if not _tie_band(o["hist_residual"], 1e-12, o["steps"]):
+        assert r["steps"] == o["steps"]
+    assert checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= 1e-12
+
+
+@pytest.mark.parametrize("prec", [1, 2])
+def test_mixed_ill_conditioned(nsr, prec):
+    """Mixed path with min|x| of X_0 ~ 1e-4 (|A| condition ~1e4): the re-anchor CG needs far more than the
+    cfg3 count of iterations and a second pass; R stays within 1e-10 of the oracle."""
+    rng = np.random.default_rng(82)
+    d = 600
+    k = 211
+    lam = np.concatenate([-rng.uniform(1e-4, 1.0, k), rng.uniform(1e-4, 1.0, d - k)])
+    Q = workloads.haar_q(rng, d)
+    H = (Q * lam[None, :]) @ Q.T
+    H = 0.5 * (H + H.T)
+    alpha = float(np.max(np.abs(lam))) * 1.01
+    o = ons.ns_reflector(H, 0.0, alpha, k, 100, 1e-10, 1, trace_residuals=True)
+    R, r = nsr.ns_reflector(torch.from_numpy(H).to(_dev()), 0.0, alpha, k, 100, 1e-10, 1, prec=prec)
+    assert r["cert"] == k and r["flags"] & ons.CONVERGED
+    assert r["steps"] == o["steps"] or _mixed_step_ok(r, o, 1e-10, 1, d)
+    assert checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= TOL_R
