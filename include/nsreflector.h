@@ -108,7 +108,9 @@ typedef struct {
  *                  has dropped by 1e-6 (default cap 512; 0 = polish without re-anchor).
  *   stop_at_switch mixed path: return the pre-polish iterate X_switch as R (no re-anchor,
  *                  no FP64 steps); flags then carry neither CONVERGED nor MAX_STEPS.
- *   lookahead      steps enqueued before the host reads the stop flag (0 = default).
+ *   lookahead      steps enqueued before the host reads the stop flag (0 = default: 2 for large
+ *                  problems, 8 for small or batched ones); clamped to 15 (the status ring has 16
+ *                  slots).  Honoured by the FP64, Ozaki and mixed single-problem paths.
  *   polish         mixed path: arithmetic of the re-anchor's two dense products and of the
  *                  polishing steps: 0 = both FP64 DMMA, 1 = both FP64 emulated on the INT8 tensor
  *                  cores (the Ozaki products of NS_PREC_FP64_OZAKI), 2 (default) = the
@@ -202,6 +204,8 @@ ns_status_t ns_reflector_batched(const double* H, int64_t d, int64_t batch, int6
  *   (H - sI)/alpha_out has its spectrum in [-1, 1] (lem:NSsign).  Device H (upper triangle read),
  *   device workspace >= ns_workspace_bytes_setup(d) bytes; alpha_out is host memory.  Also bounds the
  *   endpoint drift of prop:reuse_refresh: |lambda_i(H') - lambda_i(H)| <= ||H' - H||_inf (Weyl).
+ *   A NaN/Inf entry of H - sI propagates into alpha_out (never dropped by the max) and the call
+ *   returns NS_ERR_INVALID_ARG after writing it.
  * ns_shift_certificate (host only): prop:reuse_refresh.  Given endpoint estimates
  *   lam_k_hat, lam_k1_hat with error <= eps, a shift s and a next-step drift bound delta:
  *     margin_hat  = min(s - lam_k_hat, lam_k1_hat - s)

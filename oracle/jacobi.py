@@ -17,11 +17,21 @@ _LIB = os.path.join(_HERE, "libjacobi.so")
 _lib = None
 
 
+_CMD = ["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"]
+
+
 def build(force=False):
-    """Compile oracle/jacobi.c -> oracle/libjacobi.so (gcc, OpenMP, no FMA contraction)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fPIC", "-shared",
-                               "-o", _LIB, _SRC, "-lm"])
+    """Compile oracle/jacobi.c -> oracle/libjacobi.so (gcc, OpenMP, no FMA contraction).
+    Rebuilt whenever the sha256 of the source and command differs from the stamp next to the library."""
+    import hashlib
+    with open(_SRC, "rb") as f:
+        digest = hashlib.sha256(f.read() + " ".join(_CMD).encode()).hexdigest()
+    stamp = _LIB + ".sha256"
+    if not force and os.path.exists(_LIB) and os.path.exists(stamp) and open(stamp).read().strip() == digest:
+        return _LIB
+    subprocess.check_call(_CMD)
+    with open(stamp, "w") as f:
+        f.write(digest + "\n")
     return _LIB
 
 

@@ -124,9 +124,12 @@ def ns_fixed_depth(A, alpha, m):
     return X
 
 
-def timed_ns_steps(H, s, alpha, n_steps):
-    """CPU-baseline helper: run exactly n_steps NS updates (2 products each) and
-    return (seconds, threads).  Same arithmetic as ns_reflector, no stop test."""
+def timed_ns_steps(H, s, alpha, n_steps, return_iterate=False):
+    """CPU-baseline helper (bench.py cpu_baseline / --impl reference): time exactly n_steps NS updates
+    (2 products each) of the same loop as ns_reflector, without its stop test.  Returns (seconds,
+    threads), plus X_{n_steps} when return_iterate (pinned in tests/test_oracle_ns.py: bitwise equal to
+    ns_reflector's iterate after n_steps fixed steps).  The products are numpy/OpenBLAS FP64 matmuls,
+    so the time is a "library CPU" number on the host's cores, not a hand-written-loop one."""
     import os
     X = initial_iterate(H, s, alpha)
     t0 = time.perf_counter()
@@ -137,4 +140,6 @@ def timed_ns_steps(H, s, alpha, n_steps):
         X = 0.5 * (X + X.T)
     t1 = time.perf_counter()
     threads = int(os.environ.get("OPENBLAS_NUM_THREADS", os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)))
+    if return_iterate:
+        return t1 - t0, threads, X
     return t1 - t0, threads

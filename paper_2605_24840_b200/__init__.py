@@ -180,10 +180,39 @@ def _stream_ptr(stream, device=None):
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+class _NullCtx:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *a):
+        return False
+
+
+_NULL = _NullCtx()
+
+
+def _on(dev):
+    """Make `dev` the current CUDA device for one C call: the library launches on the current device and
+    queries no tensor's device itself.  A no-op (no torch context object) when it already is current, which
+    keeps the small-d latency path free of the device switch."""
+    torch = _torch()
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    if idx == torch.cuda.current_device():
+        return _NULL
+    return torch.cuda.device(idx)
+
+
 def _require_cuda_f64(t, name):
     torch = _torch()
     if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64):
         raise NsError(f"{name} must be a CUDA float64 tensor (no CPU fallback)")
+
+
+def _same_device(*ts):
+    dev = ts[0].device
+    for t in ts[1:]:
+        if t.device != dev:
+            raise NsError(f"all tensors of one call must be on the same device ({dev} vs {t.device})")
 
 
 def ns_workspace_bytes(d, prec=NS_PREC_FP64):
@@ -227,10 +256,12 @@ def ns_reflector(H, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_ABS, prec=NS_PR
     args = (ctypes.c_void_p(H.data_ptr()), d, H.stride(0), float(s), float(alpha), int(k), int(max_steps), float(tol),
             int(tol_mode), int(prec), ctypes.c_void_p(R.data_ptr()), R.stride(0), ctypes.c_void_p(ws.data_ptr()),
             ws.numel(), _stream_ptr(stream, H.device))
-    if options is None:
-        st = lib.ns_reflector(*args, ctypes.byref(res))
-    else:
-        st = lib.ns_reflector_ex(*args, ctypes.byref(options), ctypes.byref(res))
+    _same_device(H, R, ws)
+    with _on(H.device):
+        if options is None:
+            st = lib.ns_reflector(*args, ctypes.byref(res))
+        else:
+            st = lib.ns_reflector_ex(*args, ctypes.byref(options), ctypes.byref(res))
     _check(st)
     return R, res.as_dict()
 
@@ -250,11 +281,15 @@ def ns_reflector_host(H, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_ABS, prec=
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
     if ws is None:
         ws = alloc_workspace(lib.ns_workspace_bytes_host(d, prec), dev)
+    if ws.device.type != "cuda":
+        raise NsError("the workspace must be device memory")
+    dev = ws.device
     res = NsResult()
-    st = lib.ns_reflector_host(ctypes.c_void_p(H.data_ptr()), d, H.stride(0), float(s), float(alpha), int(k),
-                               int(max_steps), float(tol), int(tol_mode), int(prec), ctypes.c_void_p(R.data_ptr()),
-                               R.stride(0), ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream),
-                               ctypes.byref(res))
+    with _on(dev):
+        st = lib.ns_reflector_host(ctypes.c_void_p(H.data_ptr()), d, H.stride(0), float(s), float(alpha), int(k),
+                                   int(max_steps), float(tol), int(tol_mode), int(prec), ctypes.c_void_p(R.data_ptr()),
+                                   R.stride(0), ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream, dev),
+                                   ctypes.byref(res))
     _check(st)
     return R, res.as_dict()
 
@@ -276,11 +311,15 @@ def ns_reflector_batched(H, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_ABS, pr
     _require_cuda_f64(R, "R")
     if ws is None:
         ws = alloc_workspace(lib.ns_workspace_bytes_batched(d, b, prec), H.device)
+    if R.shape != H.shape or not R.is_contiguous():
+        raise NsError("R must be a contiguous tensor of H's shape")
+    _same_device(H, R, ws)
     outs = (NsResult * b)()
-    st = lib.ns_reflector_batched(ctypes.c_void_p(H.data_ptr()), d, b, H.stride(0), s_a.ctypes.data,
-                                  a_a.ctypes.data, k_a.ctypes.data, int(max_steps), float(tol), int(tol_mode),
-                                  int(prec), ctypes.c_void_p(R.data_ptr()), R.stride(0),
-                                  ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream), outs)
+    with _on(H.device):
+        st = lib.ns_reflector_batched(ctypes.c_void_p(H.data_ptr()), d, b, H.stride(0), s_a.ctypes.data,
+                                      a_a.ctypes.data, k_a.ctypes.data, int(max_steps), float(tol), int(tol_mode),
+                                      int(prec), ctypes.c_void_p(R.data_ptr()), R.stride(0),
+                                      ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream, H.device), outs)
     _check(st)
     return R, [o.as_dict() for o in outs]
 
@@ -293,15 +332,26 @@ def ns_symm_product(A, B, mode=0, C=None, ws=None, stream=None, prec=NS_PREC_FP6
     _require_cuda_f64(A, "A")
     _require_cuda_f64(B, "B")
     d = A.shape[0]
+    for name, t in (("A", A), ("B", B)):
+        if t.dim() != 2 or tuple(t.shape) != (d, d) or t.stride(1) != 1:
+            raise NsError(f"{name} must be a (d, d) row-major (stride(1) == 1) matrix")
     if A.stride(0) != B.stride(0):
         raise NsError("A and B must share a leading dimension")
+    ld = A.stride(0)
     if C is None:
-        C = torch.empty_like(A)
+        # the library writes C with A's leading dimension: allocate exactly that layout (rows of ld doubles;
+        # torch.empty_strided sizes the storage for the last row's d elements, not a full pitch)
+        C = torch.empty_strided((d, d), (ld, 1), dtype=torch.float64, device=A.device)
+    _require_cuda_f64(C, "C")
+    if C.dim() != 2 or tuple(C.shape) != (d, d) or C.stride(1) != 1 or C.stride(0) != ld:
+        raise NsError("C must be a (d, d) row-major matrix with A's leading dimension")
     if ws is None:
         ws = alloc_workspace(lib.ns_workspace_bytes(d, prec), A.device)
-    st = lib.ns_symm_product(ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()),
-                             ctypes.c_void_p(C.data_ptr()), d, A.stride(0), int(mode), int(prec),
-                             ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream))
+    _same_device(A, B, C, ws)
+    with _on(A.device):
+        st = lib.ns_symm_product(ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()),
+                                 ctypes.c_void_p(C.data_ptr()), d, ld, int(mode), int(prec),
+                                 ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream, A.device))
     _check(st)
     return C
 
@@ -319,7 +369,8 @@ def ns_reflector_sharded_emulated(nranks, H, s, alpha, k, max_steps, tol, tol_mo
     if ws is None:
         ws = alloc_workspace(lib.ns_workspace_bytes_sharded_emulated(d, nranks), H.device)
     res = NsResult()
-    st = lib.ns_reflector_sharded_emulated(int(nranks), ctypes.c_void_p(H.data_ptr()), d, H.stride(0), float(s),
+    with _on(H.device):
+        st = lib.ns_reflector_sharded_emulated(int(nranks), ctypes.c_void_p(H.data_ptr()), d, H.stride(0), float(s),
                                            float(alpha), int(k), int(max_steps), float(tol), int(tol_mode),
                                            ctypes.c_void_p(R.data_ptr()), R.stride(0), ctypes.c_void_p(ws.data_ptr()),
                                            ws.numel(), _stream_ptr(stream, H.device), ctypes.byref(res))
@@ -339,10 +390,12 @@ def ns_symm_product_shard(A, B, C_list, rank, nranks, mode=0, ws=None, stream=No
     if ws is None:
         ws = alloc_workspace(lib.ns_workspace_bytes(d, NS_PREC_FP64), A.device)
     arr = (ctypes.c_void_p * len(C_list))(*[C.data_ptr() for C in C_list])
-    st = lib.ns_symm_product_shard(ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()), arr, len(C_list), d,
+    with _on(A.device):
+        st = lib.ns_symm_product_shard(ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(B.data_ptr()), arr, len(C_list), d,
                                    int(mode), int(rank), int(nranks), ctypes.c_void_p(ws.data_ptr()), ws.numel(),
-                                   _stream_ptr(stream))
+                                   _stream_ptr(stream, A.device))
     _check(st)
+
 
 def ns_profile_enable(on=True):
     load_library().ns_profile_enable(1 if on else 0)
@@ -410,9 +463,11 @@ def ns_reflector_sharded(comm, H, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_A
     if ws is None:
         ws = alloc_workspace(lib.ns_workspace_bytes_sharded(d, nranks or 1), H.device)
     res = NsResult()
-    st = lib.ns_reflector_sharded(comm, ctypes.c_void_p(H.data_ptr()), d, H.stride(0), float(s), float(alpha), int(k),
+    with _on(H.device):
+        st = lib.ns_reflector_sharded(comm, ctypes.c_void_p(H.data_ptr()), d, H.stride(0), float(s), float(alpha), int(k),
                                   int(max_steps), float(tol), int(tol_mode), ctypes.c_void_p(R.data_ptr()), R.stride(0),
-                                  ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream), ctypes.byref(res))
+                                  ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream, H.device),
+                                  ctypes.byref(res))
     _check(st)
     return R, res.as_dict()
 
@@ -425,8 +480,10 @@ def ns_scale_bound(H, s, ws=None, stream=None):
     if ws is None:
         ws = alloc_workspace(lib.ns_workspace_bytes_setup(d), H.device)
     out = ctypes.c_double()
-    _check(lib.ns_scale_bound(ctypes.c_void_p(H.data_ptr()), d, H.stride(0), float(s), ctypes.c_void_p(ws.data_ptr()),
-                              ws.numel(), _stream_ptr(stream), ctypes.byref(out)))
+    with _on(H.device):
+        st = lib.ns_scale_bound(ctypes.c_void_p(H.data_ptr()), d, H.stride(0), float(s), ctypes.c_void_p(ws.data_ptr()),
+                                ws.numel(), _stream_ptr(stream, H.device), ctypes.byref(out))
+    _check(st)
     return out.value
 
 
@@ -454,10 +511,13 @@ def ns_alg1_rotated_quartic(Q, k, x0, m, eta, max_iters, grad_tol, x_out=None, w
     if ws is None:
         ws = alloc_workspace(lib.ns_workspace_bytes_alg1(nruns), x0.device)
     outs = (NsAlg1Result * nruns)()
-    _check(lib.ns_alg1_rotated_quartic(ctypes.c_void_p(Q.data_ptr()), d, nruns, k_a.ctypes.data,
+    with _on(x0.device):
+        st = lib.ns_alg1_rotated_quartic(ctypes.c_void_p(Q.data_ptr()), d, nruns, k_a.ctypes.data,
                                        ctypes.c_void_p(x0.data_ptr()), int(m), float(eta), int(max_iters),
                                        float(grad_tol), ctypes.c_void_p(x_out.data_ptr()),
-                                       ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream), outs))
+                                         ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream, x0.device),
+                                         outs)
+    _check(st)
     return x_out, [dict(iters=o.iters, morse_index=o.morse_index, success=bool(o.success), grad_norm=o.grad_norm)
                    for o in outs]
 

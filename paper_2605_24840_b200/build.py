@@ -1,4 +1,5 @@
 """Build libnsreflector.so in-tree with nvcc for sm_100a (no JIT, no torch extension)."""
+import hashlib
 import os
 import subprocess
 import sys
@@ -22,18 +23,35 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
 
-def build(force=False, verbose=False):
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [
+STAMP = LIB + ".sha256"
+
+
+def _source_hash(cmd_tail):
+    """sha256 over every source the library is built from (csrc/*, the public header) and the compile
+    command: the staleness test (mtimes are not trusted -- a shipped .so newer than edited sources, or
+    sources restored with old mtimes, must still rebuild)."""
+    h = hashlib.sha256()
+    deps = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC)) + [
         os.path.join(HERE, "..", "include", "nsreflector.h")]
-    if not force and os.path.exists(LIB):
-        t = os.path.getmtime(LIB)
-        if all(os.path.getmtime(d) <= t for d in deps):
-            return LIB
+    for d in deps:
+        h.update(os.path.basename(d).encode())
+        with open(d, "rb") as f:
+            h.update(f.read())
+    h.update(" ".join(cmd_tail).encode())
+    return h.hexdigest()
+
+
+def build(force=False, verbose=False):
     nccl = _nccl_dir()
     link = ["-I" + os.path.join(nccl, "include"), "-L" + os.path.join(nccl, "lib"), "-l:libnccl.so.2",
             "-Xlinker", "-rpath=" + os.path.join(nccl, "lib")]
     extra = os.environ.get("NS_NVCC_EXTRA", "").split()   # developer experiments (e.g. -DNS_OZ_A_TMEM=0)
     cmd = [NVCC] + FLAGS + extra + ["-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES] + link
+    digest = _source_hash(FLAGS + extra + SOURCES)
+    if not force and os.path.exists(LIB) and os.path.exists(STAMP):
+        with open(STAMP) as f:
+            if f.read().strip() == digest:
+                return LIB
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:
@@ -41,6 +59,8 @@ def build(force=False, verbose=False):
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed building libnsreflector.so (see %s)" % log)
+    with open(STAMP, "w") as f:
+        f.write(digest + "\n")
     if verbose:
         print(res.stderr)
     return LIB

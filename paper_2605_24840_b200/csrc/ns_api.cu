@@ -570,7 +570,7 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
   int spec_last = 0;                 // largest jn whose copy kernel was enqueued
   // look-ahead: how many steps may be in flight before the host checks the counter
   const double step_flops = 2.0 * (double)L.n_tiles * kTile * kTile * (double)L.d_pad * batch;
-  const int LA = step_flops > 2e10 ? 2 : 8;
+  const int LA = opt.lookahead > 0 ? std::min(opt.lookahead, 15) : (step_flops > 2e10 ? 2 : 8);
 
   for (int j = 0; j <= max_steps; ++j) {
     if (j >= LA) {
@@ -703,7 +703,7 @@ ns_status_t run_ozaki_batch(const Layout& L, uint8_t* ws, const double* H, long 
   NS_CUDA(launch_trace_partials(Xa, L.d, L.d_pad, batch, trp, st, ndiag));
   nl += 3;
   LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0, -1, 0};
-  const int LA = batch > 1 ? 8 : 2;
+  const int LA = opt.lookahead > 0 ? std::min(opt.lookahead, 15) : (batch > 1 ? 8 : 2);
   for (int j = 0; j <= max_steps; ++j) {
     if (j >= LA) {
       const int slot = (j - LA) % 16;
@@ -1942,6 +1942,7 @@ ns_status_t ns_scale_bound(const double* H, int64_t d, int64_t ldh, double s, vo
   NS_CUDA(launch_scale_bound(H, ldh, (int)d, s, part, dout, cs));
   NS_CUDA(cudaMemcpyAsync(alpha_out, dout, sizeof(double), cudaMemcpyDeviceToHost, cs));
   NS_CUDA(cudaStreamSynchronize(cs));
+  if (!std::isfinite(*alpha_out)) return fail(NS_ERR_INVALID_ARG, "H - sI has a non-finite entry: no scale bound");
   return NS_OK;
 }
 

@@ -39,17 +39,21 @@ __global__ void __launch_bounds__(256) ns_colsum_upper_kernel(const double* __re
   part[j] += acc;
 }
 
+// max that propagates NaN (fmax drops a NaN operand, which would turn a NaN row sum into a finite,
+// wrong bound: the Gershgorin guarantee alpha >= ||H - sI||_2 must not silently fail)
+__device__ __forceinline__ double nan_max(double a, double b) { return (a != a || b != b) ? (a + b) : fmax(a, b); }
+
 __global__ void __launch_bounds__(256) ns_max_kernel(const double* __restrict__ v, int n, double* out) {
   __shared__ double red[8];
   double m = 0.0;
-  for (int i = threadIdx.x; i < n; i += 256) m = fmax(m, v[i]);
+  for (int i = threadIdx.x; i < n; i += 256) m = nan_max(m, v[i]);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  for (int o = 16; o > 0; o >>= 1) m = nan_max(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int w = 0; w < 8; ++w) t = fmax(t, red[w]);
+    for (int w = 0; w < 8; ++w) t = nan_max(t, red[w]);
     out[0] = t;
   }
 }

@@ -129,6 +129,33 @@ def test_householder_closed_form_and_generator():
     assert np.max(np.abs(Rc - R[:, cols])) <= 1e-14
 
 
+def test_householder_iterate_columns_match_ns_loop():
+    """thm:generic: the m-step iterate of the NS loop on H = Q diag(lam) Q^T equals
+    Q diag(p_m((lam - s)/alpha)) Q^T; the Householder column routine is that closed form (two routes:
+    matrix products vs. scalar polynomial + reflector applications)."""
+    lam, Vh = workloads.householder_spectrum(3, 200, 12, 0.05, 10)
+    H = workloads.householder_form_numpy(Vh, lam)
+    cols = [0, 3, 99, 199]
+    for m in (0, 1, 3, 7):
+        Xm = ns.ns_fixed_depth(H - 0.1 * np.eye(200), 1.2, m)
+        Xc = closed_form.householder_iterate_columns(Vh, lam, 0.1, 1.2, m, cols)
+        assert np.max(np.abs(Xm[:, cols] - Xc)) <= 1e-13, m
+    # m large: the closed-form iterate is the reflector (prop:exact)
+    Xc = closed_form.householder_iterate_columns(Vh, lam, 0.1, 1.2, 40, cols)
+    assert np.max(np.abs(Xc - closed_form.householder_reflector_columns(Vh, lam, 0.1, cols))) <= 1e-13
+
+
+def test_timed_ns_steps_is_the_ns_loop():
+    """The cpu_baseline helper runs the same arithmetic as ns_reflector: after n fixed steps its iterate is
+    bitwise ns_reflector's (tol = 0, max_steps = n, reading C5)."""
+    p = workloads.cfg0_controlled(seed=4, d=96, k=5)
+    for n in (1, 3):
+        t, threads, X = ns.timed_ns_steps(p.H, p.s, p.alpha, n, return_iterate=True)
+        o = ns.ns_reflector(p.H, p.s, p.alpha, p.k, n, 0.0)
+        assert o["steps"] == n and np.array_equal(X, o["R"])
+        assert t >= 0.0 and threads >= 1
+
+
 def test_householder_fast_formation():
     """The WY formation used for large-d inputs equals the inside-out rank-2 recipe (C13)."""
     lam, Vh = workloads.householder_spectrum(1, 300, 20, 0.05, 16)

@@ -92,3 +92,16 @@ def test_min_depth_cap():
         scalar.min_depth(1e-30, 1e-12, cap=10)
     with pytest.raises(ValueError):
         scalar.eps_m(0.0, 1)
+
+
+def test_scaled_margin_closed_form():
+    """gamma = min_i |lambda_i - s| / alpha (disc:spectral_compression P:484-490, divide form C1): the
+    configs[3] spectrum edges give 0.05/1.05; the margin is the one prop:NSerr's bound uses, so the
+    closed-form iterate's worst eigenvalue error equals eps_m(gamma) when an eigenvalue sits at the edge."""
+    lam = np.array([-1.0, -0.05, 0.05, 0.3, 1.0])
+    assert scalar.scaled_margin(lam, 0.0, 1.05) == 0.05 / 1.05
+    assert abs(scalar.scaled_margin(lam, 0.1, 2.0) - 0.025) <= 1e-17
+    g = scalar.scaled_margin(lam, 0.0, 1.05)
+    mu = lam / 1.05
+    for m in (1, 4, 9):
+        assert abs(scalar.spectral_operator_error(mu, m) - scalar.eps_m(g, m)) <= 1e-15
