@@ -9,10 +9,14 @@ C3; 12 NS updates = 25 symmetric products).  value = algorithmic TFLOP/s =
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--mode tol|fixed30]
 
-N > 1 (torchrun): configs[3] does not shard ("replicas only"), so
-every rank computes its own reflector; value = all ranks' flops / max-over-ranks time.
---sharded (opt-in): ONE reflector sharded over the N ranks (ns_reflector_sharded, exchange fused
-into the product epilogue over CUDA-IPC peer memory), "scaling": "strong"; --d 49152 = configs[4].
+N > 1 (torchrun): ONE reflector sharded over the N ranks (strong scaling, "scaling": "strong"):
+ns_reflector_sharded_rows, each rank holding only its block-row panel of H and receiving the same
+rows of R; every rank computes 1/N of the upper 128x128 tiles of each symmetric product and its
+product kernel's epilogue stores them into all ranks' buffers over NVLink (CUDA-IPC peer memory),
+so N = 1 is the BENCH workload and N > 1 measures north_star's strong-scaling target on configs[3];
+--d 49152 runs configs[4] (the sharded large-d case).  value = the one reflector's algorithmic
+flops / max-over-ranks time.  --replicas: the old weak-scaling mode (one independent configs[3]
+reflector per rank).
 --impl reference times the CPU oracle (oracle/ns.py) on a bounded sample of the same
 workload (one NS step per bench step) on the host cores; rank 0 only.
 """
@@ -36,6 +40,9 @@ METRIC = "Newton–Schulz reflector TFLOP/s & time-to-R_k at d=16384 FP64 (frac 
 # max under FP64 load (no power cap), so burst == sustained.  MEASURED_PEAKS.json has no FP64 entry.
 FP64_PEAK_TFLOPS = 36.97
 FP64_PEAK_SOURCE = "measured: DMMA.8x8x4 microbenchmark, profiles/r01_calib_fp64.log (cuBLAS DGEMM 36.15)"
+# B200 datasheet FP64 / FP64-tensor figure (NVIDIA HGX B200 specification, per GPU; not in B200_PROFILING.md,
+# whose table lists no FP64 entry): reported as a second denominator next to the measured one.
+FP64_DATASHEET_TFLOPS = 40.0
 
 
 def parse():
@@ -53,8 +60,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sharded", action="store_true",
-                    help="strong scaling: ONE reflector sharded over all ranks (ns_reflector_sharded, peer-memory "
-                         "exchange) instead of one replica per rank; with --d 49152 this is configs[4]")
+                    help="force the sharded rows entry also at N = 1 (N > 1 always runs it unless --replicas)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: one independent reflector per rank (weak scaling) instead of one sharded reflector")
     return ap.parse_args()
 
 
@@ -167,14 +175,40 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------------- our arm
+def _timed(call, stream, steps, dev, pg):
+    """K calls between CUDA events on the launching stream; barrier + synchronize on both sides; max over ranks."""
+    import torch
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    out = [call() for _ in range(steps)]
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    if pg:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        ms = float(t.item())
+        pg.barrier()
+    return ms, out
+
+
 def run_ours(args):
     import torch
     ws, rank, local = dist_setup()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
+    sharded = (ws > 1 and not args.replicas) or args.sharded
     if ws > 1:
         import torch.distributed as dist
+        # communicator lines (NCCL INIT: nranks, NVLS / P2P transports) on stderr, so stdout keeps one JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=dev)
         pg = dist
     import paper_2605_24840_b200 as nsr
@@ -184,29 +218,35 @@ def run_ours(args):
     p, desc = workload(args)
     d = p.d
     H = workloads.householder_form_fast(p.Vh, p.lam, device=dev)
-    R = torch.empty_like(H)
-    wsbuf = nsr.alloc_workspace(nsr.ns_workspace_bytes(d), dev)
     stream = torch.cuda.current_stream(dev)
-
     prec = {"fp64": nsr.NS_PREC_FP64, "mixed": nsr.NS_PREC_MIXED_BF16X3, "ozaki": nsr.NS_PREC_FP64_OZAKI}[args.prec]
-    if prec != nsr.NS_PREC_FP64:
-        wsbuf = nsr.alloc_workspace(nsr.ns_workspace_bytes(d, prec), dev)
+
     comm = None
-    if args.sharded:
+    if sharded:
         if prec != nsr.NS_PREC_FP64:
-            raise SystemExit("--sharded runs the FP64 path")
+            raise SystemExit("the sharded path runs FP64")
+        if d % ws:
+            raise SystemExit(f"d = {d} is not divisible by the {ws} ranks")
         uid = [nsr.ns_comm_get_unique_id() if rank == 0 else None]
         if pg:
             pg.broadcast_object_list(uid, src=0)
         comm = nsr.ns_comm_init(rank, ws, uid[0])
-        del wsbuf
+        r0, r1 = nsr.ns_shard_rows(d, ws, rank)
+        H_rows = H[r0:r1].clone()          # this rank's block-row panel of H: the only H it keeps
+        del H
+        torch.cuda.empty_cache()
+        H = None
+        R_rows = torch.empty_like(H_rows)
         wsbuf = nsr.alloc_workspace(nsr.ns_workspace_bytes_sharded(d, ws), dev)
+    else:
+        R = torch.empty_like(H)
+        wsbuf = nsr.alloc_workspace(nsr.ns_workspace_bytes(d, prec), dev)
 
     def call(pr=None, options=None):
         pr = prec if pr is None else pr
-        if comm is not None and pr == nsr.NS_PREC_FP64 and options is None:
-            return nsr.ns_reflector_sharded(comm, H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode, R=R,
-                                            ws=wsbuf, stream=stream)
+        if comm is not None:
+            return nsr.ns_reflector_sharded_rows(comm, H_rows, d, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode,
+                                                 R_rows=R_rows, ws=wsbuf, stream=stream, nranks=ws)
         return nsr.ns_reflector(H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode, R=R, ws=wsbuf, stream=stream,
                                 prec=pr, options=options)
 
@@ -218,107 +258,106 @@ def run_ours(args):
     sampler = ClockSampler(local)
     nsr.ns_profile_reset()
     nsr.ns_profile_enable(True)
-    if pg:
-        pg.barrier()
-    torch.cuda.synchronize(dev)
     sampler.start()
     time.sleep(0.3)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    results = []
-    for _ in range(args.steps):
-        _, res = call()
-        results.append(res)
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
+    ms, outs = _timed(call, stream, args.steps, dev, pg)
+    results = [o[1] for o in outs]
     clocks = sampler.stop()
     nsr.ns_profile_enable(False)
     prof = nsr.ns_profile_get()
-    ms = e0.elapsed_time(e1)
-    if pg:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        ms = float(t.item())
-        pg.barrier()
     steps_ns = results[-1]["steps"]
     flops_call = (2 * steps_ns + 1) * float(d) ** 3
-    n_refl = 1 if args.sharded else ws          # reflectors computed per bench step by all ranks together
+    n_refl = 1 if sharded else ws          # reflectors computed per bench step by all ranks together
     value = n_refl * args.steps * flops_call / (ms * 1e-3) / 1e12
     launches = int(sum(r["launches"] for r in results))
 
-    # ---- roofline of the dominant kernel (the symmetric product): algorithmic d^3 flops per launch
+    # ---- roofline of the dominant kernel (the symmetric product): algorithmic d^3 flops per launch, or its
+    # 1/N share of the tiles on the sharded path (the kernel time excludes the barrier)
     n_prod = prof["n_square"] + prof["n_update"]
     avg_ms = (prof["ms_square"] + prof["ms_update"]) / max(1, n_prod)
-    achieved = float(d) ** 3 / (avg_ms * 1e-3) / 1e12 if n_prod else None
+    share = 1.0 / ws if sharded else 1.0
+    achieved = share * float(d) ** 3 / (avg_ms * 1e-3) / 1e12 if n_prod else None
+    if pg and achieved is not None:   # report the slowest rank's kernel
+        t = torch.tensor([avg_ms], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        avg_ms = float(t.item())
+        achieved = share * float(d) ** 3 / (avg_ms * 1e-3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and not sharded:
         with open(tpath) as f:
             tj = json.load(f)
         traffic = tj.get(str(d), {}).get("bytes_per_launch")
     roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": traffic,
-                "kernel": "ns_product_kernel (FP64 DMMA, symmetric 128x128 tiles)",
-                "flops_per_launch": float(d) ** 3, "avg_launch_ms": avg_ms, "launches_timed": n_prod,
+                "kernel": "ns_product_kernel (FP64 DMMA, symmetric 128x128 tiles"
+                          + (f", 1/{ws} of the tiles per rank, peer-store epilogue)" if sharded else ")"),
+                "flops_per_launch": share * float(d) ** 3, "avg_launch_ms": avg_ms, "launches_timed": n_prod,
                 "square_ms": prof["ms_square"] / max(1, prof["n_square"]),
                 "update_ms": prof["ms_update"] / max(1, prof["n_update"]),
                 "kernel_share_of_step": (prof["ms_square"] + prof["ms_update"]) / ms if ms else None,
-                "peak_source": FP64_PEAK_SOURCE}
+                "peak_source": FP64_PEAK_SOURCE,
+                "frac_of_datasheet_fp64": (achieved / FP64_DATASHEET_TFLOPS) if achieved else None,
+                "datasheet_fp64_tflops": FP64_DATASHEET_TFLOPS}
 
-    # ---- end to end through the public host-buffer entry (H2D + D2H inside the timed region)
+    # ---- end to end through the public entry with HOST buffers (H2D of the inputs and D2H of the result
+    # inside the timed region)
     e2e = None
-    if not args.no_e2e and not args.sharded:
-        Hh = H.cpu().pin_memory()
-        Rh = torch.empty((d, d), dtype=torch.float64).pin_memory()
-        wsh = wsbuf
-        nsr.ns_reflector_host(Hh, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode, R=Rh, ws=wsh, stream=stream,
-                              prec=prec)
-        if pg:
-            pg.barrier()
-        torch.cuda.synchronize(dev)
-        f0 = torch.cuda.Event(enable_timing=True)
-        f1 = torch.cuda.Event(enable_timing=True)
-        f0.record(stream)
-        for _ in range(args.steps):
-            _, rh = nsr.ns_reflector_host(Hh, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode, R=Rh, ws=wsh,
-                                          stream=stream, prec=prec)
-        f1.record(stream)
-        torch.cuda.synchronize(dev)
-        ems = f0.elapsed_time(f1)
-        if pg:
-            t = torch.tensor([ems], dtype=torch.float64, device=dev)
-            pg.all_reduce(t, op=pg.ReduceOp.MAX)
-            ems = float(t.item())
-        e2e = {"value": ws * args.steps * (2 * rh["steps"] + 1) * float(d) ** 3 / (ems * 1e-3) / 1e12,
-               "unit": "TFLOP/s", "h2d_bytes_per_step": d * d * 8, "d2h_bytes_per_step": d * d * 8,
-               "ms_per_step": ems / args.steps, "entry": "ns_reflector_host (pinned host H, R)"}
+    if not args.no_e2e:
+        if sharded:
+            Hh = H_rows.cpu().pin_memory()
+            Rh = torch.empty(tuple(H_rows.shape), dtype=torch.float64).pin_memory()
+
+            def e2e_call():
+                H_rows.copy_(Hh, non_blocking=True)
+                out = call()
+                Rh.copy_(R_rows, non_blocking=True)
+                return out
+            e2e_call()
+            ems, eo = _timed(e2e_call, stream, args.steps, dev, pg)
+            rh = eo[-1][1]
+            e2e = {"value": args.steps * (2 * rh["steps"] + 1) * float(d) ** 3 / (ems * 1e-3) / 1e12,
+                   "unit": "TFLOP/s", "h2d_bytes_per_step": d * d * 8, "d2h_bytes_per_step": d * d * 8,
+                   "ms_per_step": ems / args.steps,
+                   "entry": f"ns_reflector_sharded_rows with pinned host panels (each rank copies its {d // ws} "
+                            f"rows of H in and of R out; bytes summed over ranks)"}
+        else:
+            Hh = H.cpu().pin_memory()
+            Rh = torch.empty((d, d), dtype=torch.float64).pin_memory()
+            nsr.ns_reflector_host(Hh, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode, R=Rh, ws=wsbuf,
+                                  stream=stream, prec=prec)
+            ems, eo = _timed(lambda: nsr.ns_reflector_host(Hh, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode,
+                                                           R=Rh, ws=wsbuf, stream=stream, prec=prec),
+                             stream, args.steps, dev, pg)
+            rh = eo[-1][1]
+            e2e = {"value": ws * args.steps * (2 * rh["steps"] + 1) * float(d) ** 3 / (ems * 1e-3) / 1e12,
+                   "unit": "TFLOP/s", "h2d_bytes_per_step": ws * d * d * 8, "d2h_bytes_per_step": ws * d * d * 8,
+                   "ms_per_step": ems / args.steps, "entry": "ns_reflector_host (pinned host H, R)"}
         del Hh, Rh
 
     # ---- secondary: the same reflector through the mixed BF16x3 -> re-anchor -> FP64 mode and the
     # Ozaki-split FP64 emulation on the INT8 tensor cores (same metric, FP64-equivalent algorithmic flops)
-    mixed = ozaki = None
+    mixed = ozaki = mixed_oz = None
 
     def secondary(pr, options=None):
         nonlocal wsbuf
         wsbuf = nsr.alloc_workspace(nsr.ns_workspace_bytes(d, pr), dev)
-        _, rm = call(pr, options)
-        torch.cuda.synchronize(dev)
-        g0 = torch.cuda.Event(enable_timing=True)
-        g1 = torch.cuda.Event(enable_timing=True)
-        g0.record(stream)
-        for _ in range(args.steps):
-            _, rm = call(pr, options)
-        g1.record(stream)
-        torch.cuda.synchronize(dev)
-        mms = g0.elapsed_time(g1) / args.steps
-        return {"time_to_R_ms": mms, "value": (2 * rm["steps"] + 1) * float(d) ** 3 / (mms * 1e-3) / 1e12,
-                "unit": "TFLOP/s (FP64-equivalent algorithmic)", "steps": rm["steps"], "switch_step": rm["switch_step"],
-                "pre_polish_residual": rm["pre_polish_residual"], "cert": rm["cert"], "flags": rm["flags"],
-                "speedup_vs_fp64": (ms / args.steps) / mms, "launches": rm["launches"]}
+        call(pr, options)
+        nsr.ns_profile_reset()
+        nsr.ns_profile_enable(True)
+        mms, mo = _timed(lambda: call(pr, options), stream, args.steps, dev, pg)
+        nsr.ns_profile_enable(False)
+        pf = nsr.ns_profile_get()
+        rm = mo[-1][1]
+        mms /= args.steps
+        out = {"time_to_R_ms": mms, "value": (2 * rm["steps"] + 1) * float(d) ** 3 / (mms * 1e-3) / 1e12,
+               "unit": "TFLOP/s (FP64-equivalent algorithmic)", "steps": rm["steps"], "switch_step": rm["switch_step"],
+               "pre_polish_residual": rm["pre_polish_residual"], "cert": rm["cert"], "flags": rm["flags"],
+               "speedup_vs_fp64": (ms / args.steps) / mms, "launches": rm["launches"]}
+        out["executed_roofline"] = executed_roofline(pf, args.steps)
+        return out
 
-    mixed_oz = None
-    if args.prec == "fp64" and not args.no_mixed and not args.sharded:
+    if args.prec == "fp64" and not args.no_mixed and not sharded:
         mixed = secondary(nsr.NS_PREC_MIXED_BF16X3)
         # mixed_mode: the default (re-anchor products on the Ozaki INT8 cores, FP64 DMMA polishing steps);
         # the same mixed path with the polishing steps on the Ozaki INT8 products as well
@@ -327,30 +366,41 @@ def run_ours(args):
             ozaki = secondary(nsr.NS_PREC_FP64_OZAKI)
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.sharded:
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and not sharded:
         from oracle import ns as ons
         Hc = H.cpu().numpy()
         t, threads = ons.timed_ns_steps(Hc, p.s, p.alpha, 1)
         cpu = {"value": 2.0 * float(d) ** 3 / t / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
-               "sample": f"one oracle NS step (2 numpy FP64 products + update) on the same d={d} matrix, {t:.1f} s",
+               "sample": f"one oracle NS step (2 numpy/OpenBLAS FP64 products + update: a library-CPU number) on "
+                         f"the same d={d} matrix, {t:.1f} s; {_cpu_model()}",
                "seconds": t}
 
     if rank == 0:
+        nvlink = None
+        if sharded and ws > 1:
+            n_tiles = (-(-d // 128)) * (-(-d // 128) + 1) // 2
+            n_my = -(-n_tiles // ws)
+            per_product = n_my * 128 * 128 * 8 * (ws - 1)          # upper tiles only (receivers mirror)
+            nvlink = {"bytes_out_per_rank_per_step": 2 * per_product,
+                      "bytes_out_per_rank_per_reflector": (2 * steps_ns + 1) * per_product,
+                      "note": "peer stores of each rank's upper tiles into the other ranks (receiver-side mirror)"}
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if args.sharded else "weak",
+            "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "d": d, "k": p.k, "ns_steps": steps_ns, "products": 2 * steps_ns + 1,
                        "algorithmic_flops_per_reflector": flops_call, "l2": "inputs larger than L2 (3 x 2 GiB FP64 "
                        "matrices per step vs 126 MB L2)",
-                       "parallelism": (f"sharded x{ws} (peer-memory exchange)" if args.sharded
-                                       else (f"replicas x{ws}" if ws > 1 else "single")),
-                       "frac_of_fp64_peak": value / ws / FP64_PEAK_TFLOPS},
+                       "parallelism": (f"sharded x{ws} (block-row panels, upper tiles split, peer-memory exchange)"
+                                       if sharded else (f"replicas x{ws}" if ws > 1 else "single")),
+                       "frac_of_fp64_peak": value / ws / FP64_PEAK_TFLOPS,
+                       "frac_of_datasheet_fp64": value / ws / FP64_DATASHEET_TFLOPS},
             "time_to_R_ms": ms / args.steps, "reflectors_per_s": n_refl * args.steps / (ms * 1e-3),
             "result": {"steps": steps_ns, "cert": results[-1]["cert"], "flags": results[-1]["flags"],
                        "residual": results[-1]["residual"]},
             "gpu_launches": launches, "clocks": clocks, "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
+            "nvlink": nvlink,
             "mixed_mode": mixed, "mixed_ozaki_polish_mode": mixed_oz, "ozaki_mode": ozaki, "precision": args.prec,
         }
         print(json.dumps(line), flush=True)
@@ -359,6 +409,49 @@ def run_ours(args):
     if pg:
         pg.destroy_process_group()
     return 0
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return "CPU: " + ln.split(":", 1)[1].strip() + f", {os.cpu_count()} logical cores"
+    except OSError:
+        pass
+    return f"{os.cpu_count()} logical cores"
+
+
+def executed_roofline(pf, steps):
+    """Roofline of the secondaries' tensor-core work in the arithmetic they EXECUTE (not FP64-equivalent):
+    BF16 flops of the split products against MEASURED_PEAKS.json's bf16 figure, INT8 ops of the Ozaki digit
+    products against the bf16 figure x 2 (the guide's nominal int8/fp8 : bf16 ratio, 4.5 : 2.25)."""
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mp = json.load(f)
+        peaks = {"bf16": mp.get("bf16_tflops_sustained") or mp.get("bf16_tflops"), "bf16_burst": mp.get("bf16_tflops")}
+    except (OSError, ValueError):
+        peaks = {"bf16": None, "bf16_burst": None}
+    out = {}
+    if pf.get("n_lowp"):
+        a = pf["lowp_flops"] / (pf["ms_lowp"] * 1e-3) / 1e12
+        out["bf16"] = {"kernel": "ns_mx2_product_kernel (BF16x3 split, tcgen05 cta_group::2)", "launches": pf["n_lowp"],
+                       "achieved": a, "unit": "TFLOP/s", "peak": peaks["bf16"],
+                       "frac": a / peaks["bf16"] if peaks["bf16"] else None,
+                       "frac_of_burst": a / peaks["bf16_burst"] if peaks["bf16_burst"] else None,
+                       "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"}
+    if pf.get("n_oz"):
+        a = pf["oz_ops"] / (pf["ms_oz"] * 1e-3) / 1e12
+        # burst: the INT8 kernel exceeds 2 x the power-limited SUSTAINED bf16 GEMM rate (it draws less power
+        # per op), so the sustained x 2 figure is no ceiling for it; the burst x 2 figure is
+        pk = 2.0 * peaks["bf16_burst"] if peaks["bf16_burst"] else None
+        pks = 2.0 * peaks["bf16"] if peaks["bf16"] else None
+        out["int8"] = {"kernel": "ns_ozaki_product_kernel (INT8 digit pairs, tcgen05 kind::i8)", "launches": pf["n_oz"],
+                       "achieved": a, "unit": "TOP/s", "peak": pk, "frac": a / pk if pk else None,
+                       "frac_of_sustained_x2": a / pks if pks else None,
+                       "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst) x 2 (nominal int8 : bf16 = 4.5 : 2.25)"}
+    return out
 
 
 def main():

@@ -258,33 +258,59 @@ ns_status_t ns_alg1_rotated_quartic(const double* Q, int64_t d, int32_t nruns, c
 
 /*
  * ---------------- multi-GPU (one process per GPU, NCCL over NVLink/NVSwitch) ----------------
- * configs[4] (d = 49152) on P GPUs.  Every rank keeps the full FP64 iterate and
- * computes only its share of the upper 128x128 tiles of each symmetric product (tile t of the
- * library's upper-tile order belongs to rank t % P); after each product the ranks exchange their
- * tiles with one ncclAllGather and the per-rank residual sums with a second (P doubles, summed in
- * rank order so every rank takes the identical stop decision).
+ * configs[4] (d = 49152) and configs[3] strong scaling on P GPUs (the paper motivates
+ * accelerator execution of the dense sign iteration).  Every rank keeps the full FP64
+ * iterate (X_j, X_{j+1} and Y = X_j^2, 3 x 8 d_pad^2 bytes: the symmetric work split below needs any
+ * rank to read any row panel) and computes only its share of the upper 128x128 tiles of each symmetric
+ * product: tile t of the library's upper-tile order belongs to rank t % P (balanced to one tile).
+ * Exchange (default): every rank's workspace is mapped into every process (CUDA IPC; the mapping check
+ * is collective on every call), and the product kernels' epilogues store each finished tile (upper
+ * half only; the receivers mirror it locally after the barrier -- NS_SHARD_MIRROR=sender stores the
+ * mirror remotely too) and its residual / trace partial straight into all ranks' buffers over NVLink,
+ * so the transfer overlaps the contraction tile by tile; one one-double all-reduce per product is the
+ * barrier.  Every rank sums the same partials in the same fixed order: identical stop decisions.
+ * Fallback (a rank cannot map, e.g. VMM memory, or NS_SHARD_P2P=0): chunked NCCL all-gathers of the
+ * tiles overlapped with the contraction, per-rank residual sums gathered and summed in rank order.
  *
  * ns_comm_get_unique_id  rank 0 creates the 128-byte NCCL id (ship it to the other ranks, e.g.
  *                        with torch.distributed.broadcast).
  * ns_comm_init           every rank, with its CUDA device current; collective (blocks until all
  *                        ranks joined).  nranks >= 1 (1 = single-GPU communicator).
+ * ns_comm_init_host      a communicator WITHOUT NCCL: the library's collectives (IPC record exchange,
+ *                        barriers, the fallback's all-gathers) call `allgather(send, recv, bytes, user)`,
+ *                        which must all-gather `bytes` host bytes from every rank into recv (nranks *
+ *                        bytes, rank order) and return 0 (e.g. torch.distributed over gloo).  The device
+ *                        path (IPC mappings, peer-store epilogues) is unchanged; each barrier becomes a
+ *                        stream synchronisation plus the callback, so no kernel ever waits on another
+ *                        rank's kernel.  Used by the tests to run several ranks as processes sharing
+ *                        one GPU, which NCCL does not allow.
  * ns_shard_plan          host-only: the (I, J) tile pairs rank `rank` computes for dimension d
  *                        (tiles_ij[2*i], tiles_ij[2*i+1]); returns the count via n_out; writes at
  *                        most `cap` pairs.  Lets callers/tests check balance and coverage.
+ * ns_shard_rows          host-only: the block-row panel [row0, row1) rank `rank` owns in the rows entry
+ *                        (d / nranks rows each; NS_ERR_INVALID_ARG unless nranks divides d).
  * ns_reflector_sharded   same arguments and result as ns_reflector (FP64 only); H (full, upper
  *                        triangle read) and R (full) are device buffers on every rank; all ranks
  *                        must call it with identical scalars.  The workspace must hold
- *                        ns_workspace_bytes_sharded(d, nranks) bytes.  Exchange: every rank's
- *                        workspace is mapped into every process (CUDA IPC, collective, cached per
- *                        workspace) and the product kernels store their tiles straight into all
- *                        ranks' buffers (one small all-reduce per product as the barrier); if any
- *                        rank cannot map (e.g. VMM memory) or NS_SHARD_P2P=0, tiles are exchanged with
- *                        chunked NCCL all-gathers overlapped with the contraction.
+ *                        ns_workspace_bytes_sharded(d, nranks) bytes.
+ * ns_reflector_sharded_rows  SURVEY §8(b)'s sharded entry: rank r passes only its block-row panel of H,
+ *                        H_rows = rows [row0, row1) of H (ns_shard_rows; (d/P) x d, leading dimension
+ *                        ldh >= d, device memory; in each row i only the elements j >= i are read) and
+ *                        receives only the same rows of R in R_rows ((d/P) x d, ldr >= d, every element
+ *                        written).  X_0 is assembled on every rank from all ranks' panels (peer stores,
+ *                        or an all-gather of the panels on the fallback path).  prec must be NS_PREC_FP64
+ *                        (else NS_ERR_UNSUPPORTED); d must be divisible by nranks (else
+ *                        NS_ERR_INVALID_ARG); all ranks call it with identical scalars; the result
+ *                        (steps, flags, residual, trace, certificate) is identical on every rank.
+ *                        Workspace: ns_workspace_bytes_sharded(d, nranks).
  */
+typedef int (*ns_host_allgather_fn)(const void* send, void* recv, size_t bytes, void* user);
 typedef struct ns_comm ns_comm_t;
 ns_status_t ns_comm_get_unique_id(uint8_t id[128]);
 ns_status_t ns_comm_init(int rank, int nranks, const uint8_t id[128], ns_comm_t** comm);
+ns_status_t ns_comm_init_host(int rank, int nranks, ns_host_allgather_fn allgather, void* user, ns_comm_t** comm);
 ns_status_t ns_comm_destroy(ns_comm_t* comm);
+ns_status_t ns_shard_rows(int64_t d, int nranks, int rank, int64_t* row0, int64_t* row1);
 ns_status_t ns_shard_plan(int64_t d, int nranks, int rank, int32_t* tiles_ij, int32_t cap, int32_t* n_out);
 
 /*
@@ -310,17 +336,23 @@ ns_status_t ns_shard_chunks(int64_t d, int nranks, int32_t* n_chunks, int32_t* c
  * replica), each replica deciding on its own data.  No kernel waits on another.  Returns
  * NS_ERR_CUDA ("emulated ranks diverged") if the replicas' final states differ in any bit.  Same
  * arguments and result as ns_reflector (FP64); device H and R; workspace >=
- * ns_workspace_bytes_sharded_emulated(d, nranks).
+ * ns_workspace_bytes_sharded_emulated(d, nranks).  flags: bit 0 = block-row input (replica r forms
+ * X_0 from rows [r d/P, (r+1) d/P) of H with the rows entry's peer-store init and writes the same
+ * rows of R), bit 1 = sender-mirror epilogue (default 0: receivers mirror).
  */
 size_t ns_workspace_bytes_sharded_emulated(int64_t d, int nranks);
 ns_status_t ns_reflector_sharded_emulated(int32_t nranks, const double* H, int64_t d, int64_t ldh, double s,
                                           double alpha, int32_t k, int32_t max_steps, double tol, ns_tolmode_t tm,
                                           double* R, int64_t ldr, void* ws, size_t ws_bytes, void* stream,
-                                          ns_result_t* out);
+                                          int32_t flags, ns_result_t* out);
 size_t ns_workspace_bytes_sharded(int64_t d, int nranks);
 ns_status_t ns_reflector_sharded(ns_comm_t* comm, const double* H, int64_t d, int64_t ldh, double s, double alpha,
                                  int32_t k, int32_t max_steps, double tol, ns_tolmode_t tm, double* R, int64_t ldr,
                                  void* ws, size_t ws_bytes, void* stream, ns_result_t* out);
+ns_status_t ns_reflector_sharded_rows(ns_comm_t* comm, const double* H_rows, int64_t d, int64_t ldh, double s,
+                                      double alpha, int32_t k, int32_t max_steps, double tol, ns_tolmode_t tm,
+                                      ns_precision_t prec, double* R_rows, int64_t ldr, void* ws, size_t ws_bytes,
+                                      void* stream, ns_result_t* out);
 
 /*
  * ns_symm_product — kernel-level entry used by tests (the contraction core alone).
@@ -349,6 +381,16 @@ typedef struct {
   double ms_square;     /* summed device time of those launches */
   double ms_update;
   int64_t n_calls;
+  /* split-precision (BF16x3) and Ozaki (INT8 digit-pair) product launches of the mixed and Ozaki paths,
+   * with the arithmetic they EXECUTE (for a roofline in their own precision): launches that exited at
+   * once (queued past a stop, or a converged CG) are excluded (device time < 1/4 of the longest launch
+   * of the same shape in the call). */
+  int64_t n_lowp;       /* BF16x3 product launches that did work */
+  double ms_lowp;       /* their summed device time */
+  double lowp_flops;    /* executed BF16 flops: 3 GEMMs x 2 x 128 x 128 x d_pad per 128x128 output tile computed */
+  int64_t n_oz;         /* Ozaki INT8 product launches that did work (K segments count separately) */
+  double ms_oz;
+  double oz_ops;        /* executed INT8 ops: digit pairs (28 or 34) x 2 x 128 x 128 x K per 128x128 output tile */
 } ns_profile_t;
 void ns_profile_enable(int on);
 void ns_profile_reset(void);

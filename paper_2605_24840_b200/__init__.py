@@ -27,6 +27,7 @@ EXPORTED_SYMBOLS = (
     "ns_workspace_bytes_sharded", "ns_reflector_sharded", "ns_shard_chunks", "ns_workspace_bytes_setup", "ns_scale_bound",
     "ns_shift_certificate", "ns_workspace_bytes_alg1", "ns_alg1_rotated_quartic", "ns_debug_mx_trace",
     "ns_symm_product_shard", "ns_workspace_bytes_sharded_emulated", "ns_reflector_sharded_emulated",
+    "ns_comm_init_host", "ns_shard_rows", "ns_reflector_sharded_rows",
 )
 
 
@@ -49,7 +50,9 @@ class NsOptions(ctypes.Structure):
 
 class NsProfile(ctypes.Structure):
     _fields_ = [("n_square", ctypes.c_int64), ("n_update", ctypes.c_int64), ("ms_square", ctypes.c_double),
-                ("ms_update", ctypes.c_double), ("n_calls", ctypes.c_int64)]
+                ("ms_update", ctypes.c_double), ("n_calls", ctypes.c_int64),
+                ("n_lowp", ctypes.c_int64), ("ms_lowp", ctypes.c_double), ("lowp_flops", ctypes.c_double),
+                ("n_oz", ctypes.c_int64), ("ms_oz", ctypes.c_double), ("oz_ops", ctypes.c_double)]
 
 
 class NsShiftCert(ctypes.Structure):
@@ -65,6 +68,11 @@ class NsAlg1Result(ctypes.Structure):
 
 class NsError(RuntimeError):
     pass
+
+
+# int allgather(const void* send, void* recv, size_t bytes, void* user)   (ns_host_allgather_fn)
+HOST_ALLGATHER = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+_HOST_CALLBACKS = {}     # comm handle value -> CFUNCTYPE object (kept alive while the communicator exists)
 
 
 _lib = None
@@ -104,7 +112,15 @@ def load_library(path=LIB_PATH):
     lib.ns_workspace_bytes_sharded_emulated.argtypes = [c_i64, ctypes.c_int]
     lib.ns_reflector_sharded_emulated.restype = ctypes.c_int
     lib.ns_reflector_sharded_emulated.argtypes = [c_i32, c_vp, c_i64, c_i64, c_dbl, c_dbl, c_i32, c_i32, c_dbl,
-                                                  ctypes.c_int, c_vp, c_i64, c_vp, c_sz, c_vp, c_vp]
+                                                  ctypes.c_int, c_vp, c_i64, c_vp, c_sz, c_vp, c_i32, c_vp]
+    lib.ns_comm_init_host.restype = ctypes.c_int
+    lib.ns_comm_init_host.argtypes = [ctypes.c_int, ctypes.c_int, HOST_ALLGATHER, c_vp, ctypes.POINTER(c_vp)]
+    lib.ns_shard_rows.restype = ctypes.c_int
+    lib.ns_shard_rows.argtypes = [c_i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]
+    lib.ns_reflector_sharded_rows.restype = ctypes.c_int
+    lib.ns_reflector_sharded_rows.argtypes = [c_vp, c_vp, c_i64, c_i64, c_dbl, c_dbl, c_i32, c_i32, c_dbl,
+                                              ctypes.c_int, ctypes.c_int, c_vp, c_i64, c_vp, c_sz, c_vp,
+                                              ctypes.POINTER(NsResult)]
     lib.ns_symm_product_shard.restype = ctypes.c_int
     lib.ns_symm_product_shard.argtypes = [c_vp, c_vp, c_vp, c_i32, c_i64, c_i32, c_i32, c_i32, c_vp, c_sz, c_vp]
     lib.ns_build_info.restype = ctypes.c_char_p
@@ -358,7 +374,7 @@ def ns_symm_product(A, B, mode=0, C=None, ws=None, stream=None, prec=NS_PREC_FP6
 
 
 def ns_reflector_sharded_emulated(nranks, H, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_ABS, R=None, ws=None,
-                                  stream=None):
+                                  stream=None, rows=False, sender_mirror=False):
     """The sharded algorithm with `nranks` ranks emulated on one GPU (C-ABI ns_reflector_sharded_emulated)."""
     torch = _torch()
     lib = load_library()
@@ -373,7 +389,8 @@ def ns_reflector_sharded_emulated(nranks, H, s, alpha, k, max_steps, tol, tol_mo
         st = lib.ns_reflector_sharded_emulated(int(nranks), ctypes.c_void_p(H.data_ptr()), d, H.stride(0), float(s),
                                            float(alpha), int(k), int(max_steps), float(tol), int(tol_mode),
                                            ctypes.c_void_p(R.data_ptr()), R.stride(0), ctypes.c_void_p(ws.data_ptr()),
-                                           ws.numel(), _stream_ptr(stream, H.device), ctypes.byref(res))
+                                           ws.numel(), _stream_ptr(stream, H.device),
+                                           (1 if rows else 0) | (2 if sender_mirror else 0), ctypes.byref(res))
     _check(st)
     return R, res.as_dict()
 
@@ -408,8 +425,7 @@ def ns_profile_reset():
 def ns_profile_get():
     p = NsProfile()
     load_library().ns_profile_get(ctypes.byref(p))
-    return dict(n_square=p.n_square, n_update=p.n_update, ms_square=p.ms_square, ms_update=p.ms_update,
-                n_calls=p.n_calls)
+    return {f: getattr(p, f) for f, _ in NsProfile._fields_}
 
 
 def ns_comm_get_unique_id():
@@ -426,8 +442,37 @@ def ns_comm_init(rank, nranks, uid):
     return h
 
 
+def ns_comm_init_host(rank, nranks, allgather):
+    """Communicator without NCCL (C-ABI ns_comm_init_host): `allgather(data: bytes) -> list[bytes]` must
+    all-gather one bytes object per rank (e.g. over a gloo process group).  Lets several processes share one
+    GPU in tests: the library's barriers become stream syncs + this host exchange."""
+    def _cb(send, recv, nbytes, user):
+        try:
+            parts = allgather(ctypes.string_at(send, nbytes))
+            buf = b"".join(parts)
+            if len(buf) != nbytes * nranks:
+                return 1
+            ctypes.memmove(recv, buf, len(buf))
+            return 0
+        except Exception:      # noqa: BLE001 -- an exception must not cross the C frame
+            return 1
+    fn = HOST_ALLGATHER(_cb)
+    h = ctypes.c_void_p()
+    _check(load_library().ns_comm_init_host(int(rank), int(nranks), fn, None, ctypes.byref(h)))
+    _HOST_CALLBACKS[h.value] = fn
+    return h
+
+
 def ns_comm_destroy(comm):
     _check(load_library().ns_comm_destroy(comm))
+    _HOST_CALLBACKS.pop(getattr(comm, "value", None), None)
+
+
+def ns_shard_rows(d, nranks, rank):
+    """[row0, row1) of the block-row panel rank `rank` owns in the rows entry (host-only)."""
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    _check(load_library().ns_shard_rows(int(d), int(nranks), int(rank), ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
 
 
 def ns_shard_plan(d, nranks, rank):
@@ -470,6 +515,34 @@ def ns_reflector_sharded(comm, H, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_A
                                   ctypes.byref(res))
     _check(st)
     return R, res.as_dict()
+
+
+def ns_reflector_sharded_rows(comm, H_rows, d, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_ABS, R_rows=None,
+                              ws=None, stream=None, nranks=None, prec=NS_PREC_FP64):
+    """Multi-GPU reflector on block-row panels (C-ABI ns_reflector_sharded_rows): H_rows = this rank's rows
+    [row0, row1) of H ((d/P, d) CUDA float64, stride(1) == 1); returns (R_rows, result)."""
+    torch = _torch()
+    lib = load_library()
+    _require_cuda_f64(H_rows, "H_rows")
+    if H_rows.dim() != 2 or H_rows.shape[1] != d or H_rows.stride(1) != 1:
+        raise NsError("H_rows must be a (rows, d) row-major matrix")
+    if R_rows is None:
+        R_rows = torch.empty(tuple(H_rows.shape), dtype=torch.float64, device=H_rows.device)
+    _require_cuda_f64(R_rows, "R_rows")
+    if tuple(R_rows.shape) != tuple(H_rows.shape) or R_rows.stride(1) != 1:
+        raise NsError("R_rows must have H_rows' shape, row-major")
+    if ws is None:
+        ws = alloc_workspace(lib.ns_workspace_bytes_sharded(d, nranks or 1), H_rows.device)
+    _same_device(H_rows, R_rows, ws)
+    res = NsResult()
+    with _on(H_rows.device):
+        st = lib.ns_reflector_sharded_rows(comm, ctypes.c_void_p(H_rows.data_ptr()), int(d), H_rows.stride(0),
+                                           float(s), float(alpha), int(k), int(max_steps), float(tol), int(tol_mode),
+                                           int(prec), ctypes.c_void_p(R_rows.data_ptr()), R_rows.stride(0),
+                                           ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                                           _stream_ptr(stream, H_rows.device), ctypes.byref(res))
+    _check(st)
+    return R_rows, res.as_dict()
 
 
 def ns_scale_bound(H, s, ws=None, stream=None):

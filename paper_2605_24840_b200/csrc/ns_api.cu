@@ -14,6 +14,7 @@
 #include <string>
 #include <vector>
 #include <algorithm>
+#include <array>
 
 #include "../../include/nsreflector.h"
 #include "ns_internal.h"
@@ -281,6 +282,69 @@ struct Profiler {
 Profiler& prof() {
   static thread_local Profiler p;
   return p;
+}
+
+// Split-precision / Ozaki product launches, timed when profiling is on (bench.py's executed-arithmetic
+// rooflines).  kind: 0/1 = BF16x3 symmetric / dense tile lists, 2/3 = Ozaki symmetric / dense.
+struct XProf {
+  struct Rec {
+    cudaEvent_t a, b;
+    int kind;
+    double work;
+  };
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<Rec> recs;
+  cudaEvent_t ev() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+};
+XProf& xprof() {
+  static thread_local XProf x;
+  return x;
+}
+template <class F>
+cudaError_t xtimed(cudaStream_t st, int kind, double work, F&& launch) {
+  if (!prof().on) return launch();
+  XProf& x = xprof();
+  cudaEvent_t a = x.ev(), b = x.ev();
+  cudaEventRecord(a, st);
+  const cudaError_t e = launch();
+  cudaEventRecord(b, st);
+  x.recs.push_back({a, b, kind, work});
+  return e;
+}
+// After the call's final stream synchronisation: add the launches that did work to the accumulators.
+void xprof_flush() {
+  XProf& x = xprof();
+  if (x.recs.empty()) return;
+  std::vector<float> ms(x.recs.size(), 0.f);
+  float mx[4] = {0.f, 0.f, 0.f, 0.f};
+  for (size_t i = 0; i < x.recs.size(); ++i) {
+    cudaEventElapsedTime(&ms[i], x.recs[i].a, x.recs[i].b);
+    mx[x.recs[i].kind] = std::max(mx[x.recs[i].kind], ms[i]);
+  }
+  ns_profile_t& acc = prof().acc;
+  for (size_t i = 0; i < x.recs.size(); ++i) {
+    const XProf::Rec& r = x.recs[i];
+    if (ms[i] < 0.25f * mx[r.kind]) continue;        // exited at once (past a stop / converged CG)
+    if (r.kind < 2) {
+      acc.n_lowp += 1;
+      acc.ms_lowp += ms[i];
+      acc.lowp_flops += r.work;
+    } else {
+      acc.n_oz += 1;
+      acc.ms_oz += ms[i];
+      acc.oz_ops += r.work;
+    }
+  }
+  x.recs.clear();
+  x.used = 0;
 }
 
 struct HostRing {
@@ -652,6 +716,13 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
   return NS_OK;
 }
 
+// An Ozaki product launch (all its K segments), timed for the executed-INT8 roofline when profiling.
+cudaError_t oz_product(const CUtensorMap& ta, const CUtensorMap& tb, const OzParams& p, int batch, cudaStream_t st) {
+  const int pairs = p.groups >= 8 ? 34 : 28;
+  const double work = (double)pairs * 2.0 * kTile * (use_oz_mc() ? kTile : 64) * (double)p.ld * p.n_tiles * batch;
+  return xtimed(st, p.mode == 2 ? 3 : 2, work, [&] { return launch_ozaki_product(ta, tb, p, batch, st); });
+}
+
 // Ozaki path (single problem): the FP64 loop with every product on the INT8 tensor cores.
 // Ozaki path: L.batch problems (H + b*h_stride, R + b*r_stride), every product on the INT8 tensor cores.
 // Digit-pair groups for an Ozaki run: 8 when the stopping tolerance is within reach of the 7-group
@@ -716,14 +787,14 @@ ns_status_t run_ozaki_batch(const Layout& L, uint8_t* ws, const double* H, long 
     NS_CUDA(launch_ozaki_slice(Xc, slX, eX, L.d_pad, batch, st));
     OzParams sq{otiles, nt, L.d_pad / 64, L.d, L.d_pad, js, Y, nullptr, eX, eX, res, state, 0};
     sq.groups = oz_groups(tol, tm, L.d);
-    NS_CUDA(launch_ozaki_product(tXa, tXb, sq, batch, st));
+    NS_CUDA(oz_product(tXa, tXb, sq, batch, st));
     NS_CUDA(launch_decide(state, djobs, res, npart, trp, ndiag, lp, batch, n_active, st));
     nl += 3;
     if (j < max_steps) {
       NS_CUDA(launch_ozaki_slice(Y, slY, eY, L.d_pad, batch, st));
       OzParams up{otiles, nt, L.d_pad / 64, L.d, L.d_pad, js, Xn, Xc, eX, eY, trp, state, 1, opt.ca, opt.cb};
       up.groups = sq.groups;
-      NS_CUDA(launch_ozaki_product(tXa, tY, up, batch, st));
+      NS_CUDA(oz_product(tXa, tY, up, batch, st));
       nl += 2;
     }
     NS_CUDA(cudaMemcpyAsync(&rg.slots[j % 16], n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -809,7 +880,11 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
   if ((s = encode_map_bf16(&tqPXb, PXb, L.d_pad, 2, tf32, qrows)) != NS_OK) return s;
   if ((s = encode_map_bf16(&tqPY, PY, L.d_pad, 2, tf32, qrows)) != NS_OK) return s;
   auto mx_product = [&](const CUtensorMap& tP, const CUtensorMap& tQ, const MxParams& mp) {
-    return mx2 ? launch_mx2_product(tP, tQ, mp, 1, st) : launch_mx_product(tP, tQ, mp, 1, st);
+    // executed low-precision flops: 3 GEMMs (hi*hi, hi*lo, lo*hi) on every 128x128 output tile computed
+    const double work = tf32 ? 0.0 : 3.0 * 2.0 * kTile * kTile * (double)L.d_pad * mp.n_tiles;
+    return xtimed(st, mp.mode == 2 ? 1 : 0, work, [&] {
+      return mx2 ? launch_mx2_product(tP, tQ, mp, 1, st) : launch_mx_product(tP, tQ, mp, 1, st);
+    });
   };
 
   int nl = 0;
@@ -888,7 +963,7 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
         NS_CUDA(launch_ozaki_slice(P, slX, eX, L.d_pad, 1, st));
         NS_CUDA(launch_ozaki_slice(Q, slY, eY, L.d_pad, 1, st));
         OzParams pp{otiles, (int)ot_full.size(), L.d_pad / 64, L.d, L.d_pad, 0, C, nullptr, eX, eY, nullptr, nullptr, 2};
-        NS_CUDA(launch_ozaki_product(tOa, tOy, pp, 1, st));
+        NS_CUDA(oz_product(tOa, tOy, pp, 1, st));
         nl += 3;
       } else {
         ProdParams pp{full, L.n * L.n, nk, L.d, L.d_pad, 0, C, nullptr, nullptr, nullptr, 2};
@@ -988,14 +1063,14 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
         NS_CUDA(launch_ozaki_slice(Xc, slX, eX, L.d_pad, 1, st));
         OzParams sq{otiles, nt, L.d_pad / 64, L.d, L.d_pad, 0, Y, nullptr, eX, eX, ores, state, 0};
         sq.groups = oz_groups(tol, tm, L.d);
-        NS_CUDA(launch_ozaki_product(tOa, tOb, sq, 1, st));
+        NS_CUDA(oz_product(tOa, tOb, sq, 1, st));
         NS_CUDA(launch_decide(state, djobs, ores, npart, otr, ndiag, lp, 1, n_active, st));
         nl += 3;
         if (j < max_steps) {
           NS_CUDA(launch_ozaki_slice(Y, slY, eY, L.d_pad, 1, st));
           OzParams up{otiles, nt, L.d_pad / 64, L.d, L.d_pad, 0, Xn, Xc, eX, eY, otr, state, 1, opt.ca, opt.cb};
           up.groups = sq.groups;
-          NS_CUDA(launch_ozaki_product(tOa, tOy, up, 1, st));
+          NS_CUDA(oz_product(tOa, tOy, up, 1, st));
           nl += 2;
         }
         NS_CUDA(cudaMemcpyAsync(&rg.slots[j % 16], n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1079,15 +1154,26 @@ std::vector<int2> shard_tiles(const std::vector<int2>& all, int nranks, int rank
     if (r_ != ncclSuccess) return fail(NS_ERR_NCCL, "%s failed: %s", #x, ncclGetErrorString(r_)); \
   } while (0)
 
+// Host control plane (ns_comm_init_host): the library's collectives go through a caller-supplied
+// all-gather of host bytes instead of NCCL (tests: several processes sharing one GPU, where NCCL refuses
+// duplicate devices).  Every device-side exchange step then becomes stream sync + host all-gather; the
+// peer-memory path (CUDA IPC mappings + the product kernels' peer stores) is unchanged, and no kernel ever
+// waits on another process's kernel (the barrier is a host sync + the callback).
+typedef int (*HostAllGather)(const void* send, void* recv, size_t bytes, void* user);
+
 struct CommCtx {
-  ncclComm_t comm;
-  cudaStream_t cst;                    // communication stream (pack / all-gather / unpack)
+  ncclComm_t comm = nullptr;
+  HostAllGather host_fn = nullptr;
+  void* host_user = nullptr;
+  int rank = 0, nranks = 1;
+  cudaStream_t cst = nullptr;          // communication stream (pack / all-gather / unpack)
   std::vector<cudaEvent_t> ev;         // chunk-ready events (compute -> comm), + 1 "exchange done" (comm -> compute)
   // peer-memory exchange: every rank's workspace mapped into this process (CUDA IPC over NVLink)
-  const void* peer_ws_key = nullptr;   // workspace the mappings below belong to
+  std::vector<std::array<uint8_t, 96>> keys;   // [rank] -> (IPC handle, offset, size) the mappings belong to
   std::vector<uint8_t*> peer_ws;       // [rank] -> that rank's workspace (own entry: local pointer)
   std::vector<void*> opened;           // IPC mappings to close
   bool p2p = false;
+  bool valid = false;                  // keys / peer_ws / p2p describe the current mappings
 };
 
 typedef CUresult (*AddrRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
@@ -1107,33 +1193,95 @@ void close_peers(CommCtx& cc) {
   for (void* p : cc.opened) cudaIpcCloseMemHandle(p);
   cc.opened.clear();
   cc.peer_ws.clear();
-  cc.peer_ws_key = nullptr;
+  cc.keys.clear();
   cc.p2p = false;
+  cc.valid = false;
 }
 
-// Map every rank's workspace into this process (collective).  The exchange runs through NCCL on the
-// device; all ranks take the peer-memory path only if every rank could export and open the mappings
-// (torch's caching allocator memory can be IPC-exported; VMM/expandable segments cannot), else the
-// NCCL all-gather path is used everywhere.  NS_SHARD_P2P=0 forces the NCCL path.
-ns_status_t setup_peers(CommCtx& cc, int rank, int nranks, uint8_t* ws, uint8_t* scratch, cudaStream_t st) {
-  if (cc.peer_ws_key == ws) return NS_OK;
-  close_peers(cc);
+// All-gather of `bytes` HOST bytes per rank (recv: nranks * bytes, rank order).  dscratch: device scratch of
+// (nranks + 1) * bytes for the NCCL path.  Synchronises `st`.
+ns_status_t comm_allgather_host(CommCtx& cc, const void* send, void* recv, size_t bytes, uint8_t* dscratch,
+                                cudaStream_t st) {
+  if (cc.nranks == 1) {
+    memcpy(recv, send, bytes);
+    return NS_OK;
+  }
+  if (cc.host_fn) {
+    NS_CUDA(cudaStreamSynchronize(st));
+    if (cc.host_fn(send, recv, bytes, cc.host_user) != 0) return fail(NS_ERR_NCCL, "host all-gather callback failed");
+    return NS_OK;
+  }
+  NS_CUDA(cudaMemcpyAsync(dscratch, send, bytes, cudaMemcpyHostToDevice, st));
+  NS_NCCL(ncclAllGather(dscratch, dscratch + bytes, bytes, ncclUint8, cc.comm, st));
+  NS_CUDA(cudaMemcpyAsync(recv, dscratch + bytes, bytes * cc.nranks, cudaMemcpyDeviceToHost, st));
+  NS_CUDA(cudaStreamSynchronize(st));
+  return NS_OK;
+}
+
+// All-gather of DEVICE buffers (ncclAllGather semantics: recv holds nranks * bytes in rank order; in place
+// when send == recv + rank * bytes), enqueued on `st`.  Host control plane: staged through host memory.
+ns_status_t comm_allgather_dev(CommCtx& cc, const void* dsend, void* drecv, size_t bytes, cudaStream_t st) {
+  if (cc.host_fn) {
+    std::vector<uint8_t> hs(bytes), hr(bytes * (size_t)cc.nranks);
+    NS_CUDA(cudaMemcpyAsync(hs.data(), dsend, bytes, cudaMemcpyDeviceToHost, st));
+    NS_CUDA(cudaStreamSynchronize(st));
+    if (cc.host_fn(hs.data(), hr.data(), bytes, cc.host_user) != 0)
+      return fail(NS_ERR_NCCL, "host all-gather callback failed");
+    NS_CUDA(cudaMemcpyAsync(drecv, hr.data(), hr.size(), cudaMemcpyHostToDevice, st));
+    NS_CUDA(cudaStreamSynchronize(st));
+    return NS_OK;
+  }
+  NS_NCCL(ncclAllGather(dsend, drecv, bytes, ncclUint8, cc.comm, st));
+  return NS_OK;
+}
+
+// Cross-rank barrier in stream order: every rank's work enqueued on its `st` before this point (including its
+// kernels' peer stores, made visible by __threadfence_system) is complete before anything after it runs.
+// NCCL: a one-double all-reduce on the stream; host control plane: stream sync + a one-byte all-gather.
+ns_status_t comm_barrier(CommCtx& cc, double* dscratch, cudaStream_t st) {
+  if (cc.nranks == 1) return NS_OK;
+  if (cc.host_fn) {
+    NS_CUDA(cudaStreamSynchronize(st));
+    uint8_t b = 1;
+    std::vector<uint8_t> all(cc.nranks);
+    if (cc.host_fn(&b, all.data(), 1, cc.host_user) != 0) return fail(NS_ERR_NCCL, "host barrier callback failed");
+    return NS_OK;
+  }
+  NS_NCCL(ncclAllReduce(dscratch, dscratch, 1, ncclDouble, ncclSum, cc.comm, st));
+  return NS_OK;
+}
+
+// Map every rank's workspace into this process (collective, on EVERY call).  Each rank all-gathers its record
+// (IPC handle of the allocation holding ws, ws's offset in it, the allocation size, "can export"); since all
+// ranks see the same gathered records, the decision to reuse the cached mappings (every rank's record equals
+// the one the mappings were opened for) or to re-open them is identical on every rank -- a workspace that
+// moved on one rank only, or a peer that re-allocated, re-maps everywhere instead of desynchronising the
+// collectives or storing through stale mappings.  All ranks take the peer-memory path only if every rank could
+// export and open (torch's caching-allocator memory can be IPC-exported; VMM/expandable segments cannot), else
+// the NCCL all-gather path everywhere.  NS_SHARD_P2P=0 forces the NCCL path.
+// The gather also serves as the call's entry barrier: no rank stores into a peer before that peer has finished
+// its previous call (its copy-out precedes its contribution in stream order).
+ns_status_t setup_peers(CommCtx& cc, uint8_t* ws, uint8_t* scratch, cudaStream_t st) {
   static const bool allow = [] {
     const char* e = getenv("NS_SHARD_P2P");
     return !(e && e[0] == '0');
   }();
-  cc.peer_ws.assign(nranks, nullptr);
-  cc.peer_ws[rank] = ws;
+  const int nranks = cc.nranks, rank = cc.rank;
   if (nranks == 1) {
-    cc.p2p = allow;
-    cc.peer_ws_key = ws;
+    if (!cc.valid || cc.peer_ws.size() != 1 || cc.peer_ws[0] != ws) {
+      close_peers(cc);
+      cc.peer_ws.assign(1, ws);
+      cc.keys.assign(1, {});
+      cc.p2p = allow;
+      cc.valid = true;
+    }
     return NS_OK;
   }
   struct Rec {
-    cudaIpcMemHandle_t h;
-    unsigned long long off;
+    cudaIpcMemHandle_t h;              // 64 bytes
+    unsigned long long off, size;      // 16
     int ok;
-    int pad[13];
+    int pad[11];
   };
   static_assert(sizeof(Rec) == 128, "IPC record size");
   Rec mine{};
@@ -1147,11 +1295,21 @@ ns_status_t setup_peers(CommCtx& cc, int rank, int nranks, uint8_t* ws, uint8_t*
     mine.ok = 0;
   }
   mine.off = mine.ok ? (unsigned long long)(reinterpret_cast<uintptr_t>(ws) - (uintptr_t)base) : 0ull;
-  NS_CUDA(cudaMemcpyAsync(scratch, &mine, sizeof(Rec), cudaMemcpyHostToDevice, st));
-  NS_NCCL(ncclAllGather(scratch, scratch + sizeof(Rec), sizeof(Rec), ncclUint8, cc.comm, st));
+  mine.size = mine.ok ? (unsigned long long)size : 0ull;
   std::vector<Rec> all(nranks);
-  NS_CUDA(cudaMemcpyAsync(all.data(), scratch + sizeof(Rec), sizeof(Rec) * nranks, cudaMemcpyDeviceToHost, st));
-  NS_CUDA(cudaStreamSynchronize(st));
+  ns_status_t s = comm_allgather_host(cc, &mine, all.data(), sizeof(Rec), scratch, st);
+  if (s != NS_OK) return s;
+  auto key_of = [](const Rec& r) {
+    std::array<uint8_t, 96> k{};
+    memcpy(k.data(), &r, 84);          // handle, off, size, ok
+    return k;
+  };
+  bool same = cc.valid && (int)cc.keys.size() == nranks && cc.peer_ws.size() == (size_t)nranks && cc.peer_ws[rank] == ws;
+  for (int r = 0; r < nranks && same; ++r) same = (cc.keys[r] == key_of(all[r]));
+  if (same) return NS_OK;              // identical decision on every rank (same gathered records)
+  close_peers(cc);
+  cc.peer_ws.assign(nranks, nullptr);
+  cc.peer_ws[rank] = ws;
   int ok = 1;
   for (const Rec& r : all) ok &= r.ok;
   if (ok) {
@@ -1168,26 +1326,40 @@ ns_status_t setup_peers(CommCtx& cc, int rank, int nranks, uint8_t* ws, uint8_t*
     }
   }
   // agree on the outcome (an open can fail on one rank only)
-  double* flag = reinterpret_cast<double*>(scratch);
-  const double mine_ok = ok ? 1.0 : 0.0;
-  NS_CUDA(cudaMemcpyAsync(flag, &mine_ok, sizeof(double), cudaMemcpyHostToDevice, st));
-  NS_NCCL(ncclAllReduce(flag, flag, 1, ncclDouble, ncclMin, cc.comm, st));
-  double all_ok = 0.0;
-  NS_CUDA(cudaMemcpyAsync(&all_ok, flag, sizeof(double), cudaMemcpyDeviceToHost, st));
-  NS_CUDA(cudaStreamSynchronize(st));
-  cc.p2p = (all_ok == 1.0);
+  std::vector<int> oks(nranks);
+  s = comm_allgather_host(cc, &ok, oks.data(), sizeof(int), scratch, st);
+  if (s != NS_OK) return s;
+  int all_ok = 1;
+  for (int v : oks) all_ok &= v;
+  cc.p2p = all_ok != 0;
   if (!cc.p2p) {
     for (void* p : cc.opened) cudaIpcCloseMemHandle(p);
     cc.opened.clear();
   }
-  cc.peer_ws_key = ws;
+  cc.keys.resize(nranks);
+  for (int r = 0; r < nranks; ++r) cc.keys[r] = key_of(all[r]);
+  cc.valid = true;
   return NS_OK;
 }
 
-ns_status_t run_sharded(CommCtx& cc, const ShardLayout& SL, uint8_t* ws, const double* H, long long ldh,
-                        const JobParams& jp, int32_t max_steps, double tol, ns_tolmode_t tm, double* R, long long ldr,
-                        cudaStream_t st, DevState& out_state, int* launches) {
-  ncclComm_t comm = cc.comm;
+// Mirror mode of the peer-store epilogue: 0 = receiver mirrors (default: each rank sends only the upper tile,
+// half the NVLink bytes; a local transpose pass after the barrier), 1 = sender stores the mirror too.
+int shard_sender_mirror() {
+  static const int v = [] {
+    const char* e = getenv("NS_SHARD_MIRROR");
+    return (e && (e[0] == 's' || e[0] == '1')) ? 1 : 0;
+  }();
+  return v;
+}
+
+// One sharded run.  H_full != nullptr: every rank passes the full H (upper triangle read) and forms X_0 locally.
+// Otherwise rows mode: H_rows holds rows [r0, r1) of H; X_0 is assembled on every rank from all ranks' rows
+// (peer stores from ns_init_rows_kernel, or an all-gather of the row panels on the NCCL path) and the rank
+// receives rows [r0, r1) of R in R (ldr).
+ns_status_t run_sharded(CommCtx& cc, const ShardLayout& SL, uint8_t* ws, const double* H_full, const double* H_rows,
+                        long long ldh, long long r0, long long r1, const JobParams& jp, int32_t max_steps, double tol,
+                        ns_tolmode_t tm, double* R, long long ldr, cudaStream_t st, DevState& out_state,
+                        int* launches, int sender_mirror) {
   const Layout& L = SL.base;
   double* Xa = reinterpret_cast<double*>(ws + L.off_xa);
   double* Xb = reinterpret_cast<double*>(ws + L.off_xb);
@@ -1205,6 +1377,11 @@ ns_status_t run_sharded(CommCtx& cc, const ShardLayout& SL, uint8_t* ws, const d
   int* n_active = reinterpret_cast<int*>(ws + L.off_active);
   HostRing& rg = ring();
   if (!rg.ok) return fail(NS_ERR_CUDA, "pinned status ring allocation failed");
+
+  // entry: the collective peer-mapping check (also the entry barrier, see setup_peers)
+  ns_status_t ps = setup_peers(cc, ws, ws + SL.off_ipc, st);
+  if (ps != NS_OK) return ps;
+  const bool p2p = cc.p2p;
 
   std::vector<int2> tl = make_tiles(L.n);
   std::vector<int2> mt = shard_tiles(tl, SL.nranks, SL.rank);
@@ -1226,8 +1403,8 @@ ns_status_t run_sharded(CommCtx& cc, const ShardLayout& SL, uint8_t* ws, const d
     cc.ev.push_back(e);
   }
   int nl = 0;
-  // One symmetric product on the rank's tiles, chunk by chunk, with the exchange of chunk c on the
-  // communication stream overlapping the computation of chunk c+1.
+  // NCCL fallback: one symmetric product on the rank's tiles, chunk by chunk, with the exchange of chunk c on
+  // the communication stream overlapping the computation of chunk c+1.
   auto product_and_exchange = [&](const CUtensorMap& tP, const CUtensorMap& tQ, double* C, const double* Xold,
                                   double* partial, int mode) -> ns_status_t {
     for (int c = 0; c < SL.n_chunks; ++c) {
@@ -1242,8 +1419,9 @@ ns_status_t run_sharded(CommCtx& cc, const ShardLayout& SL, uint8_t* ws, const d
       NS_CUDA(cudaEventRecord(cc.ev[c], st));
       NS_CUDA(cudaStreamWaitEvent(cc.cst, cc.ev[c], 0));
       if (cnt > 0) NS_CUDA(launch_pack_tiles(C, my + s0, cnt, send + (size_t)s0 * tile_elems, L.d_pad, cc.cst));
-      NS_NCCL(ncclAllGather(send + (size_t)s0 * tile_elems, recv + (size_t)c * SL.nranks * chunk_elems, chunk_elems,
-                            ncclDouble, comm, cc.cst));
+      ns_status_t e = comm_allgather_dev(cc, send + (size_t)s0 * tile_elems, recv + (size_t)c * SL.nranks * chunk_elems,
+                                         chunk_elems * sizeof(double), cc.cst);
+      if (e != NS_OK) return e;
       NS_CUDA(launch_unpack_tiles(C, tiles, L.n_tiles, recv + (size_t)c * SL.nranks * chunk_elems, SL.cs, s0,
                                   SL.nranks, SL.rank, L.d_pad, cc.cst));
       nl += 2;
@@ -1253,15 +1431,13 @@ ns_status_t run_sharded(CommCtx& cc, const ShardLayout& SL, uint8_t* ws, const d
     return NS_OK;
   };
 
-  // Peer-memory exchange (default): the product kernel's epilogue stores each tile (+ mirror, + its
-  // residual / trace partial) straight into every rank's buffers through the IPC mappings, so the
-  // exchange rides on the contraction tile by tile; one tiny NCCL all-reduce per product is the
-  // cross-rank barrier (all peers' stores done) before anything reads the full matrix.
-  ns_status_t ps = setup_peers(cc, SL.rank, SL.nranks, ws, ws + SL.off_ipc, st);
-  if (ps != NS_OK) return ps;
-  const bool p2p = cc.p2p;
-  // [6][P]: Y, Xa, Xb, res, tr (even steps), tr (odd steps).  The trace partials alternate by step
-  // parity: a fast rank's update j (writing tr X_{j+1}) may overlap a slow rank's decide j (reading tr X_j).
+  // Peer-memory exchange (default): the product kernel's epilogue stores each tile (and, in sender-mirror mode,
+  // its mirror) plus its residual / trace partial straight into every rank's buffers through the IPC mappings,
+  // so the exchange rides on the contraction tile by tile; one tiny all-reduce per product is the cross-rank
+  // barrier (all peers' stores done) before anything reads the full matrix; in receiver-mirror mode each rank
+  // then fills the lower halves of its peers' tiles locally.
+  // [7][P]: Y, Xa, Xb, res, tr (even steps), tr (odd steps), Xa again (init targets).  The trace partials
+  // alternate by step parity: a fast rank's update j (writing tr X_{j+1}) may overlap a slow rank's decide j.
   double** dptr = reinterpret_cast<double**>(ws + SL.off_ptrs);
   if (p2p) {
     std::vector<double*> h(6 * (size_t)SL.nranks);
@@ -1276,8 +1452,12 @@ ns_status_t run_sharded(CommCtx& cc, const ShardLayout& SL, uint8_t* ws, const d
     }
     NS_CUDA(cudaMemcpyAsync(dptr, h.data(), h.size() * sizeof(double*), cudaMemcpyHostToDevice, st));
   }
+  Profiler& pf = prof();
+  int n_prof = 0;                      // event pairs recorded (kernel only, not the barrier)
+  std::vector<int> prof_mode;
   auto product_p2p = [&](const CUtensorMap& tP, const CUtensorMap& tQ, double* C, int which_c, const double* Xold,
                          double* partial, int which_part, int mode) -> ns_status_t {
+    if (pf.on) NS_CUDA(cudaEventRecord(pf.get(2 * n_prof), st));
     if (n_my > 0) {
       ProdParams pp{my, n_my, L.d_pad / kBK, L.d, L.d_pad, (long long)L.d_pad * L.d_pad, C, Xold, partial, state, mode};
       pp.dst = dptr + (size_t)which_c * SL.nranks;
@@ -1286,17 +1466,54 @@ ns_status_t run_sharded(CommCtx& cc, const ShardLayout& SL, uint8_t* ws, const d
       pp.gt_off = SL.rank;
       pp.gt_stride = SL.nranks;
       pp.n_tiles_total = L.n_tiles;
+      pp.remote_mirror = sender_mirror;
       NS_CUDA(launch_product(tP, tQ, pp, 1, st));
       nl += 1;
     }
-    if (SL.nranks > 1) NS_NCCL(ncclAllReduce(rsend, rsend, 1, ncclDouble, ncclSum, comm, st));   // barrier
+    if (pf.on) {
+      NS_CUDA(cudaEventRecord(pf.get(2 * n_prof + 1), st));
+      prof_mode.push_back(mode);
+      ++n_prof;
+    }
+    ns_status_t e = comm_barrier(cc, rsend, st);
+    if (e != NS_OK) return e;
+    if (!sender_mirror && SL.nranks > 1) {
+      NS_CUDA(launch_mirror_remote(C, tiles, L.n_tiles, SL.nranks, SL.rank, L.d_pad, st));
+      nl += 1;
+    }
     return NS_OK;
   };
 
   NS_CUDA(launch_zero_state(state, 1, n_active, st));
-  NS_CUDA(launch_init(H, ldh, 0, Xa, djobs, L.d, L.d_pad, 1, st));
+  nl += 1;
+  if (H_full) {
+    NS_CUDA(launch_init(H_full, ldh, 0, Xa, djobs, L.d, L.d_pad, 1, st));
+    nl += 1;
+  } else if (p2p) {
+    // every rank stores its rows' upper parts and their mirrors into every rank's X_0; the padding (never
+    // written remotely) is zeroed locally
+    if (L.d_pad > L.d) {
+      NS_CUDA(cudaMemset2DAsync(Xa + L.d, (size_t)L.d_pad * 8, 0, (size_t)(L.d_pad - L.d) * 8, (size_t)L.d, st));
+      NS_CUDA(cudaMemsetAsync(Xa + (size_t)L.d * L.d_pad, 0, (size_t)(L.d_pad - L.d) * L.d_pad * 8, st));
+    }
+    NS_CUDA(launch_init_rows(H_rows, ldh, r0, r1, dptr + 1 * (size_t)SL.nranks, SL.nranks, jp.s, jp.alpha, L.d,
+                             L.d_pad, st));
+    nl += 1;
+    ns_status_t e = comm_barrier(cc, rsend, st);
+    if (e != NS_OK) return e;
+  } else {
+    // NCCL path: all-gather the row panels of H into Y (free until the first square), then form X_0 locally
+    const long long rows = r1 - r0;
+    if (rows > 0)
+      NS_CUDA(cudaMemcpy2DAsync(Y + (size_t)r0 * L.d_pad, (size_t)L.d_pad * 8, H_rows, (size_t)ldh * 8, (size_t)L.d * 8,
+                                (size_t)rows, cudaMemcpyDeviceToDevice, st));
+    ns_status_t e = comm_allgather_dev(cc, Y + (size_t)r0 * L.d_pad, Y, (size_t)rows * L.d_pad * sizeof(double), st);
+    if (e != NS_OK) return e;
+    NS_CUDA(launch_init(Y, L.d_pad, 0, Xa, djobs, L.d, L.d_pad, 1, st));
+    nl += 1;
+  }
   NS_CUDA(launch_trace_partials(Xa, L.d, L.d_pad, 1, trp, st));
-  nl += 3;
+  nl += 1;
   LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0, -1, 0};
   const int LA = 2;
   for (int j = 0; j <= max_steps; ++j) {
@@ -1325,7 +1542,8 @@ ns_status_t run_sharded(CommCtx& cc, const ShardLayout& SL, uint8_t* ws, const d
       ns_status_t e1 = product_and_exchange(tmC, tmC, Y, nullptr, res, 0);
       if (e1 != NS_OK) return e1;
       NS_CUDA(launch_shard_sum(res, n_my, rsend, st));
-      NS_NCCL(ncclAllGather(rsend, rrecv, 1, ncclDouble, comm, st));
+      e1 = comm_allgather_dev(cc, rsend, rrecv, sizeof(double), st);
+      if (e1 != NS_OK) return e1;
       // decide (identical on all ranks)
       NS_CUDA(launch_decide(state, djobs, res, 0, trp, L.n, lp, 1, n_active, st, rrecv, SL.nranks));
       nl += 2;
@@ -1339,11 +1557,31 @@ ns_status_t run_sharded(CommCtx& cc, const ShardLayout& SL, uint8_t* ws, const d
     NS_CUDA(cudaMemcpyAsync(&rg.slots[j % 16], n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
     NS_CUDA(cudaEventRecord(rg.ev[j % 16], st));
   }
-  NS_CUDA(launch_copy_out(Xa, Xb, L.d, L.d_pad, state, R, ldr, 0, 1, st));
+  if (H_full) NS_CUDA(launch_copy_out(Xa, Xb, L.d, L.d_pad, state, R, ldr, 0, 1, st));
+  else NS_CUDA(launch_copy_out(Xa, Xb, L.d, L.d_pad, state, R, ldr, 0, 1, st, (int)r0, (int)(r1 - r0)));
   nl += 1;
   NS_CUDA(cudaMemcpyAsync(&out_state, state, sizeof(DevState), cudaMemcpyDeviceToHost, st));
   NS_CUDA(cudaStreamSynchronize(st));
   if (launches) *launches = nl;
+  if (pf.on) {   // products that did work: squares 0..j, updates 0..j-1 (launches past the stop exit at once)
+    int sq = 0, up = 0;
+    for (int q = 0; q < n_prof; ++q) {
+      const bool is_sq = prof_mode[q] == 0;
+      if (is_sq ? sq > out_state.j : up >= out_state.j) continue;
+      float ms = 0.f;
+      NS_CUDA(cudaEventElapsedTime(&ms, pf.get(2 * q), pf.get(2 * q + 1)));
+      if (is_sq) {
+        pf.acc.ms_square += ms;
+        pf.acc.n_square += 1;
+        ++sq;
+      } else {
+        pf.acc.ms_update += ms;
+        pf.acc.n_update += 1;
+        ++up;
+      }
+    }
+    pf.acc.n_calls += 1;
+  }
   return NS_OK;
 }
 
@@ -1353,9 +1591,13 @@ ns_status_t run_sharded(CommCtx& cc, const ShardLayout& SL, uint8_t* ws, const d
 // on another (stream order replaces the cross-rank barrier), so this is safe on one device; it checks
 // the partitioning, the global partial slots, the trace-parity buffers and that all ranks take
 // identical decisions (their final states must agree bit for bit).
+// flags: bit 0 = block-row input (replica r forms its share of X_0 from rows [r d/P, (r+1) d/P) of H with the
+// rows entry's init kernel, storing into every replica); bit 1 = sender-mirror epilogue (default: receivers mirror).
 ns_status_t run_sharded_emulated(int64_t d, int P, uint8_t* ws, size_t stride, const double* H, long long ldh,
                                  const JobParams& jp, int32_t max_steps, double tol, ns_tolmode_t tm, double* R,
-                                 long long ldr, cudaStream_t st, DevState& out_state, int* launches) {
+                                 long long ldr, cudaStream_t st, DevState& out_state, int* launches, int flags) {
+  const bool rows_mode = (flags & 1) != 0;
+  const int sender_mirror = (flags & 2) ? 1 : 0;
   std::vector<ShardLayout> sl;
   std::vector<uint8_t*> w(P);
   for (int r = 0; r < P; ++r) {
@@ -1384,6 +1626,7 @@ ns_status_t run_sharded_emulated(int64_t d, int P, uint8_t* ws, size_t stride, c
   NS_CUDA(cudaMemcpyAsync(dptr, h.data(), h.size() * sizeof(double*), cudaMemcpyHostToDevice, st));
   int nl = 0;
   for (int r = 0; r < P; ++r) {
+    NS_CUDA(cudaMemcpyAsync(w[r] + L.off_tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
     mt[r] = shard_tiles(tl, P, r);
     int2* my = reinterpret_cast<int2*>(w[r] + sl[r].off_my);
     if (!mt[r].empty()) NS_CUDA(cudaMemcpyAsync(my, mt[r].data(), mt[r].size() * sizeof(int2), cudaMemcpyHostToDevice, st));
@@ -1394,9 +1637,26 @@ ns_status_t run_sharded_emulated(int64_t d, int P, uint8_t* ws, size_t stride, c
     DevState* state = reinterpret_cast<DevState*>(w[r] + L.off_state);
     int* n_active = reinterpret_cast<int*>(w[r] + L.off_active);
     NS_CUDA(launch_zero_state(state, 1, n_active, st));
-    NS_CUDA(launch_init(H, ldh, 0, ptr(r, L.off_xa), reinterpret_cast<JobParams*>(w[r] + L.off_jobs), L.d, L.d_pad, 1, st));
+    nl += 1;
+    if (!rows_mode) {
+      NS_CUDA(launch_init(H, ldh, 0, ptr(r, L.off_xa), reinterpret_cast<JobParams*>(w[r] + L.off_jobs), L.d, L.d_pad, 1, st));
+      nl += 1;
+    } else if (L.d_pad > L.d) {
+      double* Xa = ptr(r, L.off_xa);
+      NS_CUDA(cudaMemset2DAsync(Xa + L.d, (size_t)L.d_pad * 8, 0, (size_t)(L.d_pad - L.d) * 8, (size_t)L.d, st));
+      NS_CUDA(cudaMemsetAsync(Xa + (size_t)L.d * L.d_pad, 0, (size_t)(L.d_pad - L.d) * L.d_pad * 8, st));
+    }
+  }
+  if (rows_mode) {   // each replica's row panel into every replica's X_0 (the rows entry's peer-store init)
+    for (int r = 0; r < P; ++r) {
+      const long long r0 = d * r / P, r1 = d * (r + 1) / P;
+      NS_CUDA(launch_init_rows(H + r0 * ldh, ldh, r0, r1, dptr + 1 * (size_t)P, P, jp.s, jp.alpha, L.d, L.d_pad, st));
+      nl += 1;
+    }
+  }
+  for (int r = 0; r < P; ++r) {
     NS_CUDA(launch_trace_partials(ptr(r, L.off_xa), L.d, L.d_pad, 1, ptr(r, L.off_tr), st));
-    nl += 3;
+    nl += 1;
   }
   auto products = [&](bool odd, int mode) -> ns_status_t {
     for (int r = 0; r < P; ++r) {
@@ -1416,9 +1676,17 @@ ns_status_t run_sharded_emulated(int64_t d, int P, uint8_t* ws, size_t stride, c
       pp.gt_off = r;
       pp.gt_stride = P;
       pp.n_tiles_total = L.n_tiles;
+      pp.remote_mirror = sender_mirror;
       NS_CUDA(launch_product(tC, mode == 0 ? tC : tY[r], pp, 1, st));
       nl += 1;
     }
+    // (stream order is the barrier) receivers mirror their peers' tiles
+    if (!sender_mirror && P > 1)
+      for (int r = 0; r < P; ++r) {
+        double* C = (mode == 0) ? ptr(r, L.off_y) : ptr(r, odd ? L.off_xa : L.off_xb);
+        NS_CUDA(launch_mirror_remote(C, reinterpret_cast<int2*>(w[r] + L.off_tiles), L.n_tiles, P, r, L.d_pad, st));
+        nl += 1;
+      }
     return NS_OK;
   };
   LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0, -1, 0};
@@ -1441,9 +1709,19 @@ ns_status_t run_sharded_emulated(int64_t d, int P, uint8_t* ws, size_t stride, c
     NS_CUDA(cudaMemcpyAsync(&rg.slots[j % 16], w[0] + L.off_active, sizeof(int), cudaMemcpyDeviceToHost, st));
     NS_CUDA(cudaEventRecord(rg.ev[j % 16], st));
   }
-  NS_CUDA(launch_copy_out(ptr(0, L.off_xa), ptr(0, L.off_xb), L.d, L.d_pad, reinterpret_cast<DevState*>(w[0] + L.off_state),
-                          R, ldr, 0, 1, st));
-  nl += 1;
+  if (!rows_mode) {
+    NS_CUDA(launch_copy_out(ptr(0, L.off_xa), ptr(0, L.off_xb), L.d, L.d_pad,
+                            reinterpret_cast<DevState*>(w[0] + L.off_state), R, ldr, 0, 1, st));
+    nl += 1;
+  } else {   // every replica writes its own row block of R (the rows entry's output)
+    for (int r = 0; r < P; ++r) {
+      const long long r0 = d * r / P, r1 = d * (r + 1) / P;
+      NS_CUDA(launch_copy_out(ptr(r, L.off_xa), ptr(r, L.off_xb), L.d, L.d_pad,
+                              reinterpret_cast<DevState*>(w[r] + L.off_state), R + r0 * ldr, ldr, 0, 1, st, (int)r0,
+                              (int)(r1 - r0)));
+      nl += 1;
+    }
+  }
   std::vector<DevState> states(P);
   for (int r = 0; r < P; ++r)
     NS_CUDA(cudaMemcpyAsync(&states[r], w[r] + L.off_state, sizeof(DevState), cudaMemcpyDeviceToHost, st));
@@ -1532,6 +1810,7 @@ ns_status_t ns_reflector_ex(const double* H, int64_t d, int64_t ldh, double s, d
                            static_cast<cudaStream_t>(stream), o, ds, &nl, tf32)
                : run_ozaki(L, static_cast<uint8_t*>(ws), H, ldh, jobs[0], max_steps, tol, tm, R, ldr,
                            static_cast<cudaStream_t>(stream), o, ds, &nl);
+    xprof_flush();
     if (st != NS_OK) return st;
     fill_result(ds, nl, out);
     return NS_OK;
@@ -1586,11 +1865,13 @@ ns_status_t ns_reflector_host(const double* H_host, int64_t d, int64_t ldh, doub
   std::vector<JobParams> jobs{JobParams{s, alpha, k, 0}};
   std::vector<DevState> states(1);
   int nl = 0;
-  if (mixed)
+  if (mixed) {
     st = run_mixed(L, w, stage, d, jobs[0], max_steps, tol, tm, stage, d, cs, Opts{}, states[0], &nl, tf32);
-  else if (ozaki)
+    xprof_flush();
+  } else if (ozaki) {
     st = run_ozaki(L, w, stage, d, jobs[0], max_steps, tol, tm, stage, d, cs, Opts{}, states[0], &nl);
-  else {
+    xprof_flush();
+  } else {
     // FP64 path: if R_host is pinned (device-accessible), the result may be copied speculatively
     // behind the last square product (run_loop); otherwise one D2H copy after the loop
     Opts o;
@@ -1654,10 +1935,11 @@ ns_status_t ns_reflector_batched(const double* H, int64_t d, int64_t batch, int6
     return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
   std::vector<DevState> states;
   int nl = 0;
-  if (ozaki)
+  if (ozaki) {
     st = run_ozaki_batch(L, static_cast<uint8_t*>(ws), H, d, stride_h, jobs, max_steps, tol, tm, R, d, stride_r,
                          static_cast<cudaStream_t>(stream), Opts{}, states, &nl);
-  else
+    xprof_flush();
+  } else
     st = run_loop(L, static_cast<uint8_t*>(ws), H, d, stride_h, jobs, max_steps, tol, tm, R, d, stride_r,
                   static_cast<cudaStream_t>(stream), states, &nl);
   if (st != NS_OK) return st;
@@ -1715,7 +1997,7 @@ ns_status_t ns_symm_product(const double* A, const double* B, double* C, int64_t
     if ((s = encode_map_i8(&tB, slB, L.d_pad, kOzSlices, 64)) != NS_OK) return s;
     double* opart = reinterpret_cast<double*>(w + (mode == 0 ? L.off_ores : L.off_otr));
     OzParams p{otiles, (int)ot.size(), L.d_pad / 64, L.d, L.d_pad, 0, Pc, Pa, eA, eB, opart, nullptr, mode};
-    NS_CUDA(launch_ozaki_product(tA, tB, p, 1, cs));
+    NS_CUDA(oz_product(tA, tB, p, 1, cs));
   } else if (!mixed) {
     CUtensorMap tA, tB;
     if ((s = encode_map(&tA, Pa, L.d_pad, 1)) != NS_OK) return s;
@@ -1778,8 +2060,27 @@ ns_status_t ns_comm_init(int rank, int nranks, const uint8_t id[128], ns_comm_t*
     return fail(NS_ERR_NCCL, "ncclCommInitRank failed: %s", ncclGetErrorString(r));
   }
   c->ctx.comm = c->comm;
+  c->ctx.rank = rank;
+  c->ctx.nranks = nranks;
   if (cudaStreamCreateWithFlags(&c->ctx.cst, cudaStreamNonBlocking) != cudaSuccess) {
     ncclCommDestroy(c->comm);
+    delete c;
+    return fail(NS_ERR_CUDA, "communication stream creation failed");
+  }
+  *comm = c;
+  return NS_OK;
+}
+
+ns_status_t ns_comm_init_host(int rank, int nranks, ns_host_allgather_fn allgather, void* user, ns_comm_t** comm) {
+  g_last_error.clear();
+  if (!allgather || !comm) return fail(NS_ERR_INVALID_ARG, "null argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(NS_ERR_INVALID_ARG, "bad rank/nranks");
+  ns_comm_t* c = new ns_comm_t{nullptr, rank, nranks, CommCtx{}};
+  c->ctx.host_fn = allgather;
+  c->ctx.host_user = user;
+  c->ctx.rank = rank;
+  c->ctx.nranks = nranks;
+  if (cudaStreamCreateWithFlags(&c->ctx.cst, cudaStreamNonBlocking) != cudaSuccess) {
     delete c;
     return fail(NS_ERR_CUDA, "communication stream creation failed");
   }
@@ -1793,7 +2094,7 @@ ns_status_t ns_comm_destroy(ns_comm_t* comm) {
   close_peers(comm->ctx);
   for (cudaEvent_t e : comm->ctx.ev) cudaEventDestroy(e);
   if (comm->ctx.cst) cudaStreamDestroy(comm->ctx.cst);
-  ncclResult_t r = ncclCommDestroy(comm->comm);
+  ncclResult_t r = comm->comm ? ncclCommDestroy(comm->comm) : ncclSuccess;
   delete comm;
   if (r != ncclSuccess) return fail(NS_ERR_NCCL, "ncclCommDestroy failed: %s", ncclGetErrorString(r));
   return NS_OK;
@@ -1850,11 +2151,12 @@ size_t ns_workspace_bytes_sharded_emulated(int64_t d, int nranks) {
 ns_status_t ns_reflector_sharded_emulated(int32_t nranks, const double* H, int64_t d, int64_t ldh, double s,
                                           double alpha, int32_t k, int32_t max_steps, double tol, ns_tolmode_t tm,
                                           double* R, int64_t ldr, void* ws, size_t ws_bytes, void* stream,
-                                          ns_result_t* out) {
+                                          int32_t flags, ns_result_t* out) {
   g_last_error.clear();
   ns_status_t st = check_common(d, max_steps, tol, tm, NS_PREC_FP64);
   if (st != NS_OK) return st;
   if (nranks < 1 || nranks > 64) return fail(NS_ERR_INVALID_ARG, "nranks must be in [1, 64]");
+  if (flags & ~3) return fail(NS_ERR_INVALID_ARG, "flags: bit 0 = block-row input, bit 1 = sender mirror");
   if (!H || !R || !ws || !out) return fail(NS_ERR_INVALID_ARG, "null pointer argument");
   if (ldh < d || ldr < d) return fail(NS_ERR_INVALID_ARG, "leading dimensions must be >= d");
   if (!std::isfinite(s)) return fail(NS_ERR_INVALID_ARG, "shift s must be finite");
@@ -1867,7 +2169,7 @@ ns_status_t ns_reflector_sharded_emulated(int32_t nranks, const double* H, int64
   DevState ds;
   int nl = 0;
   st = run_sharded_emulated(d, nranks, static_cast<uint8_t*>(ws), stride, H, ldh, JobParams{s, alpha, k, 0},
-                            max_steps, tol, tm, R, ldr, static_cast<cudaStream_t>(stream), ds, &nl);
+                            max_steps, tol, tm, R, ldr, static_cast<cudaStream_t>(stream), ds, &nl, flags);
   if (st != NS_OK) return st;
   fill_result(ds, nl, out);
   return NS_OK;
@@ -1920,8 +2222,51 @@ ns_status_t ns_reflector_sharded(ns_comm_t* comm, const double* H, int64_t d, in
     return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, SL.total);
   DevState ds;
   int nl = 0;
-  st = run_sharded(comm->ctx, SL, static_cast<uint8_t*>(ws), H, ldh, JobParams{s, alpha, k, 0}, max_steps, tol, tm,
-                   R, ldr, static_cast<cudaStream_t>(stream), ds, &nl);
+  st = run_sharded(comm->ctx, SL, static_cast<uint8_t*>(ws), H, nullptr, ldh, 0, d, JobParams{s, alpha, k, 0},
+                   max_steps, tol, tm, R, ldr, static_cast<cudaStream_t>(stream), ds, &nl, shard_sender_mirror());
+  if (st != NS_OK) return st;
+  fill_result(ds, nl, out);
+  return NS_OK;
+}
+
+ns_status_t ns_shard_rows(int64_t d, int nranks, int rank, int64_t* row0, int64_t* row1) {
+  g_last_error.clear();
+  if (d < 1 || nranks < 1 || rank < 0 || rank >= nranks || !row0 || !row1)
+    return fail(NS_ERR_INVALID_ARG, "bad arguments");
+  if (d % nranks != 0) return fail(NS_ERR_INVALID_ARG, "d = %lld is not divisible by nranks = %d", (long long)d, nranks);
+  *row0 = d / nranks * rank;
+  *row1 = d / nranks * (rank + 1);
+  return NS_OK;
+}
+
+ns_status_t ns_reflector_sharded_rows(ns_comm_t* comm, const double* H_rows, int64_t d, int64_t ldh, double s,
+                                      double alpha, int32_t k, int32_t max_steps, double tol, ns_tolmode_t tm,
+                                      ns_precision_t prec, double* R_rows, int64_t ldr, void* ws, size_t ws_bytes,
+                                      void* stream, ns_result_t* out) {
+  g_last_error.clear();
+  if (!comm) return fail(NS_ERR_INVALID_ARG, "null communicator");
+  ns_status_t st = check_common(d, max_steps, tol, tm, prec);
+  if (st != NS_OK) return st;
+  if (prec != NS_PREC_FP64)
+    return fail(NS_ERR_UNSUPPORTED, "the sharded path runs FP64 DMMA products only (prec = %d)", (int)prec);
+  if (d % comm->nranks != 0)
+    return fail(NS_ERR_INVALID_ARG, "d = %lld is not divisible by nranks = %d", (long long)d, comm->nranks);
+  const long long rows = d / comm->nranks, r0 = rows * comm->rank, r1 = r0 + rows;
+  if ((!H_rows || !R_rows) && rows > 0) return fail(NS_ERR_INVALID_ARG, "null H_rows / R_rows");
+  if (!ws || !out) return fail(NS_ERR_INVALID_ARG, "null pointer argument");
+  if (ldh < d || ldr < d) return fail(NS_ERR_INVALID_ARG, "leading dimensions must be >= d");
+  if (!std::isfinite(s)) return fail(NS_ERR_INVALID_ARG, "shift s must be finite");
+  if (!(alpha > 0.0) || !std::isfinite(alpha)) return fail(NS_ERR_INVALID_ARG, "alpha must be finite and > 0");
+  if (k < 0 || k > d) return fail(NS_ERR_INVALID_ARG, "k must lie in [0, d]");
+  if (R_rows == H_rows) return fail(NS_ERR_INVALID_ARG, "R_rows must not alias H_rows");
+  if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(NS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+  const ShardLayout SL = make_shard_layout(d, comm->nranks, comm->rank);
+  if (ws_bytes < SL.total)
+    return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, SL.total);
+  DevState ds;
+  int nl = 0;
+  st = run_sharded(comm->ctx, SL, static_cast<uint8_t*>(ws), nullptr, H_rows, ldh, r0, r1, JobParams{s, alpha, k, 0},
+                   max_steps, tol, tm, R_rows, ldr, static_cast<cudaStream_t>(stream), ds, &nl, shard_sender_mirror());
   if (st != NS_OK) return st;
   fill_result(ds, nl, out);
   return NS_OK;

@@ -313,8 +313,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (MODE == 2) return;
   if (p.n_dst > 0) {
-    // peer-memory exchange: the same tile (and mirror) into every other destination; S holds the final
-    // values (MODE 1 updated it in place; diagonal tiles are valid on and above the diagonal)
+    // peer-memory exchange: the same tile (and, if remote_mirror, its mirror) into every other destination;
+    // S holds the final values (MODE 1 updated it in place; diagonal tiles are valid on and above the diagonal)
     named_bar_sync(1, 32 * kConsumerWarps);
     for (int q = 0; q < p.n_dst; ++q) {
       double* Cq = p.dst[q] + base;
@@ -324,10 +324,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int r = idx >> 7, c = idx & 127;
           Cq[(long long)(I * kTile + r) * ld + J * kTile + c] = S[r * kEpiPitch + c];
         }
-        for (int idx = tid; idx < kTile * kTile; idx += 256) {
-          const int r = idx >> 7, c = idx & 127;
-          Cq[(long long)(J * kTile + r) * ld + I * kTile + c] = S[c * kEpiPitch + r];
-        }
+        if (p.remote_mirror)   // else the receiver mirrors its peers' off-diagonal tiles after the barrier
+          for (int idx = tid; idx < kTile * kTile; idx += 256) {
+            const int r = idx >> 7, c = idx & 127;
+            Cq[(long long)(J * kTile + r) * ld + I * kTile + c] = S[c * kEpiPitch + r];
+          }
       } else {
         for (int idx = tid; idx < kTile * kTile; idx += 256) {
           const int r = idx >> 7, c = idx & 127;
@@ -730,12 +731,13 @@ __global__ void ns_zero_state_kernel(DevState* state, int batch, int* n_active) 
 template <bool V2>
 __global__ void __launch_bounds__(256) ns_copy_out_kernel(const double* __restrict__ Xa, const double* __restrict__ Xb,
                                                           int d, int d_pad, const DevState* __restrict__ state,
-                                                          double* __restrict__ R, long long ldr, long long r_stride) {
+                                                          double* __restrict__ R, long long ldr, long long r_stride,
+                                                          int row0, int rows) {
   const int job = blockIdx.y;
-  const double* X = ((state[job].j & 1) ? Xb : Xa) + (long long)job * d_pad * d_pad;
+  const double* X = ((state[job].j & 1) ? Xb : Xa) + (long long)job * d_pad * d_pad + (long long)row0 * d_pad;
   double* Rj = R + (long long)job * r_stride;
   const int cols = V2 ? d / 2 : d;
-  const long long per = (long long)d * cols;
+  const long long per = (long long)rows * cols;
   for (long long base = (long long)blockIdx.x * 2048; base < per; base += (long long)gridDim.x * 2048) {
     if (V2) {
       double2 v[8];
@@ -846,12 +848,15 @@ cudaError_t launch_decide(DevState* state, const JobParams* jobs, const double* 
 }
 
 cudaError_t launch_copy_out(const double* Xa, const double* Xb, int d, int d_pad, const DevState* state,
-                            double* R, long long ldr, long long r_stride, int batch, cudaStream_t st) {
+                            double* R, long long ldr, long long r_stride, int batch, cudaStream_t st, int row0,
+                            int rows) {
+  if (rows < 0) rows = d - row0;
+  if (rows <= 0) return cudaSuccess;
   const bool v2 = (d % 2 == 0) && (ldr % 2 == 0) && (r_stride % 2 == 0) && ((reinterpret_cast<uintptr_t>(R) & 15) == 0);
-  const long long per = (long long)d * (v2 ? d / 2 : d);
+  const long long per = (long long)rows * (v2 ? d / 2 : d);
   dim3 grid((unsigned)std::min<long long>((per + 2047) / 2048, 1 << 20), batch);
-  if (v2) ns_copy_out_kernel<true><<<grid, 256, 0, st>>>(Xa, Xb, d, d_pad, state, R, ldr, r_stride);
-  else ns_copy_out_kernel<false><<<grid, 256, 0, st>>>(Xa, Xb, d, d_pad, state, R, ldr, r_stride);
+  if (v2) ns_copy_out_kernel<true><<<grid, 256, 0, st>>>(Xa, Xb, d, d_pad, state, R, ldr, r_stride, row0, rows);
+  else ns_copy_out_kernel<false><<<grid, 256, 0, st>>>(Xa, Xb, d, d_pad, state, R, ldr, r_stride, row0, rows);
   return cudaGetLastError();
 }
 

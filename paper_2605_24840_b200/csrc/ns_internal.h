@@ -131,6 +131,8 @@ struct ProdParams {
   // own keeps the slots of the full list, so the decide's fixed-order sum is unchanged); nullptr = x
   const int* part_slot = nullptr;
   int diag_tri = 1;        // 64x64-tile kernel: diagonal tiles compute only their upper 8x8 blocks (NS_DIAG_TRI=0: full)
+  int remote_mirror = 1;   // peer-store epilogue: also store the mirrored tile into the other destinations (0: the
+                           // receivers mirror remote tiles themselves, launch_mirror_remote; half the NVLink bytes)
 };
 
 // ---------------- mixed path (tcgen05 BF16x3, ns_mixed.cu) ----------------
@@ -291,8 +293,19 @@ cudaError_t launch_pack_tiles(const double* M, const int2* my_tiles, int n_my, d
 cudaError_t launch_unpack_tiles(double* M, const int2* all_tiles, int n_tiles, const double* recv_chunk, int cs,
                                 int slot0, int nranks, int my_rank, int d_pad, cudaStream_t st);
 cudaError_t launch_shard_sum(const double* v, int n, double* out, cudaStream_t st);
+// R (rows row0 .. row0 + rows - 1 of the returned iterate; rows < 0: to d) <- X_steps
 cudaError_t launch_copy_out(const double* Xa, const double* Xb, int d, int d_pad, const DevState* state,
-                            double* R, long long ldr, long long r_stride, int batch, cudaStream_t st);
+                            double* R, long long ldr, long long r_stride, int batch, cudaStream_t st, int row0 = 0,
+                            int rows = -1);
+// Receiver-side mirror (sharded path, remote_mirror = 0): for every off-diagonal upper tile of the global
+// list NOT computed by my_rank (t % nranks != my_rank), M[J-block][I-block] <- M[I-block][J-block]^T.
+cudaError_t launch_mirror_remote(double* M, const int2* all_tiles, int n_tiles, int nranks, int my_rank, int d_pad,
+                                 cudaStream_t st);
+// Block-row input (sharded rows entry): rows [r0, r1) of H (local buffer H_rows, leading dimension ldh, only
+// elements j >= i read) -> X_0 = (H - sI)/alpha elements (i, j) and (j, i) into every destination X in dst[0..n_dst)
+// (device array of base pointers, d_pad x d_pad).  Elements of other ranks' rows and the padding are not written.
+cudaError_t launch_init_rows(const double* H_rows, long long ldh, long long r0, long long r1, double* const* dst,
+                             int n_dst, double s, double alpha, int d, int d_pad, cudaStream_t st);
 cudaError_t launch_zero_state(DevState* state, int batch, int* n_active, cudaStream_t st);
 // If state->spec == jn: copy X (d x d inside d_pad) to R (device-accessible pinned host memory, leading
 // dimension ldr) -- the speculative result copy of the host entry (ns_api.cu run_loop)

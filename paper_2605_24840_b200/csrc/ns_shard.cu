@@ -91,6 +91,90 @@ __global__ void __launch_bounds__(256) ns_shard_sum_kernel(const double* __restr
   }
 }
 
+// Receiver-side mirror: the peer-store epilogue (remote_mirror = 0) sends only the upper tile (I, J) to the
+// other ranks; after the barrier each rank fills M[J-block][I-block] = M[I-block][J-block]^T for the tiles it
+// did not compute itself (its own tiles were mirrored by its own epilogue).  One CTA per tile of the global
+// list, 32x32 shared-memory transposes (coalesced reads and writes).
+__global__ void __launch_bounds__(256) ns_mirror_remote_kernel(double* __restrict__ M, const int2* __restrict__ all_tiles,
+                                                               int nranks, int my_rank, int d_pad) {
+  __shared__ double t[32][33];
+  const int gt = blockIdx.x;
+  if (gt % nranks == my_rank) return;
+  const int2 tl = all_tiles[gt];
+  if (tl.x == tl.y) return;
+  const double* src = M + (long long)tl.x * kTile * d_pad + (long long)tl.y * kTile;
+  double* dst = M + (long long)tl.y * kTile * d_pad + (long long)tl.x * kTile;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int bi = 0; bi < 4; ++bi)
+    for (int bj = 0; bj < 4; ++bj) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = src[(long long)(bi * 32 + ty + 8 * u) * d_pad + bj * 32 + tx];
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < 4; ++u) t[ty + 8 * u][tx] = v[u];
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dst[(long long)(bj * 32 + ty + 8 * u) * d_pad + bi * 32 + tx] = t[tx][ty + 8 * u];
+    }
+}
+
+// Block-row initial iterate (ns_reflector_sharded_rows): rank r holds rows [r0, r1) of H.  Block (bj, by)
+// covers the 64x64 tile (bi, bj), bi = r0/64 + by, of the global matrix; only tiles with bj >= bi and only
+// elements (i, j) with r0 <= i < r1, i <= j < d are read (the upper triangle of the rank's rows).  Each
+// element x = (H_ij - s delta_ij)/alpha is stored at (i, j) and (j, i) in every destination (every rank's
+// X_0 through the peer mappings), so after the barrier all ranks hold the full symmetric X_0.
+__global__ void __launch_bounds__(256) ns_init_rows_kernel(const double* __restrict__ Hr, long long ldh, long long r0,
+                                                           long long r1, double* const* __restrict__ dst, int n_dst,
+                                                           double s, double alpha, int d, int d_pad) {
+  __shared__ double t[64][65];
+  const int bj = blockIdx.x;
+  const int bi = (int)(r0 / 64) + blockIdx.y;
+  if (bj < bi) return;
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;   // 64 x 4
+  double v[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const long long gi = (long long)bi * 64 + ty + 4 * u, gj = (long long)bj * 64 + tx;
+    double x = 0.0;
+    if (gi >= r0 && gi < r1 && gj >= gi && gj < d) {
+      const double h = Hr[(gi - r0) * ldh + gj];
+      x = (gi == gj) ? (h - s) / alpha : h / alpha;
+    }
+    v[u] = x;
+    t[ty + 4 * u][tx] = x;
+  }
+  __syncthreads();
+  for (int q = 0; q < n_dst; ++q) {
+    double* X = dst[q];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {   // direct: (i, j), j >= i
+      const long long gi = (long long)bi * 64 + ty + 4 * u, gj = (long long)bj * 64 + tx;
+      if (gi >= r0 && gi < r1 && gj >= gi && gj < d) X[gi * d_pad + gj] = v[u];
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {   // mirror: row j = bj*64 + ty + 4u, column i = bi*64 + tx, for j > i
+      const long long gj = (long long)bj * 64 + ty + 4 * u, gi = (long long)bi * 64 + tx;
+      if (gi >= r0 && gi < r1 && gj > gi && gj < d) X[gj * d_pad + gi] = t[tx][ty + 4 * u];
+    }
+  }
+}
+
+cudaError_t launch_mirror_remote(double* M, const int2* all_tiles, int n_tiles, int nranks, int my_rank, int d_pad,
+                                 cudaStream_t st) {
+  if (nranks > 1 && n_tiles > 0) ns_mirror_remote_kernel<<<n_tiles, 256, 0, st>>>(M, all_tiles, nranks, my_rank, d_pad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_rows(const double* H_rows, long long ldh, long long r0, long long r1, double* const* dst,
+                             int n_dst, double s, double alpha, int d, int d_pad, cudaStream_t st) {
+  if (r1 <= r0) return cudaSuccess;
+  const int rb0 = (int)(r0 / 64), rb1 = (int)((r1 + 63) / 64);
+  dim3 grid(d_pad / 64, rb1 - rb0);
+  ns_init_rows_kernel<<<grid, 256, 0, st>>>(H_rows, ldh, r0, r1, dst, n_dst, s, alpha, d, d_pad);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_pack_tiles(const double* M, const int2* my_tiles, int n_my, double* send, int d_pad,
                               cudaStream_t st) {
   if (n_my > 0) ns_pack_tiles_kernel<<<n_my, 256, 0, st>>>(M, my_tiles, send, d_pad);

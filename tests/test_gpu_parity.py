@@ -429,6 +429,14 @@ def test_sharded_p1_matches_single_and_oracle(nsr, comm1):
     o = ons.ns_reflector(p.H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
     assert rs["steps"] == o["steps"] and rs["cert"] == o["cert"]
     assert checks.frob_per_sqrt_d(Rs.cpu().numpy(), o["R"]) <= TOL_R
+    # the block-row entry on the same one-rank NCCL communicator (rows [0, d), prec argument)
+    Rr, rr = nsr.ns_reflector_sharded_rows(comm1, Hg, p.d, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    assert torch.equal(Rr, Rd)
+    for key in ("steps", "flags", "residual", "trace", "cert"):
+        assert rr[key] == rd[key], key
+    with pytest.raises(nsr.NsError, match="UNSUPPORTED|unsupported|FP64"):
+        nsr.ns_reflector_sharded_rows(comm1, Hg, p.d, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode,
+                                      prec=nsr.NS_PREC_FP64_OZAKI)
 
 
 def test_sharded_cfg4_subproblem(nsr, comm1):
@@ -759,26 +767,32 @@ def test_peer_exchange_products(nsr, d, mode, P):
         assert torch.equal(C, ref)
 
 
-@pytest.mark.parametrize("P", [2, 3, 8])
-def test_sharded_emulated_ranks_match_single(nsr, P):
+@pytest.mark.parametrize("P,rows,sender", [(2, False, False), (3, False, False), (8, False, False),
+                                           (2, True, False), (8, True, False), (3, False, True), (4, True, True)])
+def test_sharded_emulated_ranks_match_single(nsr, P, rows, sender):
     """The whole sharded run with P ranks emulated on one GPU (P workspace replicas, each rank's product
     kernels storing into every replica, every replica deciding on its own): all replicas end in the
     same state (the library checks this bit for bit) and R equals the single-GPU result bitwise
-    (d = 2048: both use 128x128 tiles)."""
+    (d = 2048: both use 128x128 tiles).  rows: X_0 assembled from the replicas' block-row panels by the
+    rows entry's peer-store init and R written panel by panel; sender: the epilogue also stores mirrors
+    remotely (default: receivers mirror)."""
     p = workloads.cfg3_dense(d=2048, k=128)
     Hg = torch.from_numpy(p.H).to(_dev())
-    Re, re_ = nsr.ns_reflector_sharded_emulated(P, Hg, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    Re, re_ = nsr.ns_reflector_sharded_emulated(P, Hg, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode,
+                                                rows=rows, sender_mirror=sender)
     Rd, rd = nsr.ns_reflector(Hg, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
     assert torch.equal(Re, Rd)
     for key in ("steps", "flags", "residual", "trace", "cert"):
         assert re_[key] == rd[key], key
 
 
-def test_sharded_emulated_ragged_vs_oracle(nsr):
-    """Ragged d (not a tile multiple) with more ranks than some tile rows: parity with the oracle."""
+@pytest.mark.parametrize("rows", [False, True])
+def test_sharded_emulated_ragged_vs_oracle(nsr, rows):
+    """Ragged d (not a tile multiple) with more ranks than some tile rows, row panels not aligned to the
+    64-row init blocks: parity with the oracle."""
     p = workloads.cfg3_dense(d=1000, k=77)
     Hg = torch.from_numpy(p.H).to(_dev())
-    R, res = nsr.ns_reflector_sharded_emulated(5, Hg, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
+    R, res = nsr.ns_reflector_sharded_emulated(5, Hg, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode, rows=rows)
     o = ons.ns_reflector(p.H, p.s, p.alpha, p.k, p.max_steps, p.tol, p.tol_mode)
     assert res["steps"] == o["steps"] and res["cert"] == o["cert"] == 77
     assert checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= TOL_R
