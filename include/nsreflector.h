@@ -96,6 +96,7 @@ typedef struct {
   int32_t kernel_launches;   /* device kernels this call launched (incl. early-exit look-ahead steps) */
   int32_t switch_step;       /* mixed path: j at which the low-precision phase ended (-1 = none) */
   double pre_polish_residual;/* mixed path: low-precision ||X_switch^2 - I||_F (0 if no switch) */
+  double alpha;              /* the scale used (the caller's, or the device Gershgorin bound for alpha = 0) */
 } ns_result_t;
 
 /*
@@ -117,6 +118,12 @@ typedef struct {
  *                  re-anchor products emulated on INT8, the polishing steps FP64 DMMA.
  *   filter_a/b     the step X_{j+1} = a X_j + b X_j^3 (generic odd sign-preserving
  *                  filters; with tol = 0 and max_steps = m it is the fixed-depth filter phi_m).
+ *   filter_c[3]    coefficients of X^5, X^7, X^9: with any of them nonzero the step is the general odd
+ *                  polynomial X_{j+1} = a X + b X^3 + c0 X^5 + c1 X^7 + c2 X^9 (eq:signpreserving P:278-289;
+ *                  "low-degree odd polynomial filters" P:513-518), evaluated as X P(X^2) with Horner's
+ *                  rule in Y = X^2: deg + 1 symmetric products per step (deg = highest nonzero power of Y).
+ *                  FP64 and NS_PREC_FP64_OZAKI, single problem; the workspace must hold
+ *                  ns_workspace_bytes_ex(d, prec, opts) bytes (one more d_pad^2 matrix).
  */
 typedef struct {
   double switch_tol;
@@ -127,9 +134,12 @@ typedef struct {
   int32_t reserved[2];
   double filter_a;   /* odd cubic filter step X <- filter_a X + filter_b X^3 (eq:signpreserving P:278-289); */
   double filter_b;   /* Newton–Schulz = (1.5, -0.5) (default).  FP64 paths only; mixed requires the default. */
+  double filter_c[3];/* X^5, X^7, X^9 coefficients (default 0: the cubic step) */
 } ns_options_t;
 
 void ns_options_default(ns_options_t* opts);
+/* Workspace for ns_reflector_ex with these options (>= ns_workspace_bytes; general filters need one more matrix). */
+size_t ns_workspace_bytes_ex(int64_t d, ns_precision_t prec, const ns_options_t* opts);
 
 /* Bytes of device workspace ns_reflector needs for dimension d (batch = 1). */
 size_t ns_workspace_bytes(int64_t d, ns_precision_t prec);
@@ -140,7 +150,11 @@ size_t ns_workspace_bytes_batched(int64_t d, int64_t batch, ns_precision_t prec)
 /*
  * ns_reflector — one reflector, run to tolerance (north_star call).
  *   H      device, d x d, row-major, leading dim ldh >= d; upper triangle read.
- *   s      shift (finite).      alpha   scale (finite, > 0); X_0 = (H - sI)/alpha.
+ *   s      shift (finite).      alpha   scale (finite, > 0); X_0 = (H - sI)/alpha.  alpha = 0:
+ *          the library computes alpha = ||H - sI||_inf (>= ||H - sI||_2, the Gershgorin surrogate of
+ *          the default realization) on the device first (one pass over H's upper triangle
+ *          and an 8-byte readback; NS_ERR_INVALID_ARG if H - sI has a non-finite entry); out->alpha
+ *          reports the scale used.
  *   k      target index, 0 <= k <= d (the paper's domain is 1..d-1); used
  *          only for NS_F_INDEX_MISMATCH.
  *   max_steps >= 0; tol >= 0 (0 = fixed max_steps updates); tm tolerance mode.
@@ -184,7 +198,8 @@ ns_status_t ns_reflector_host(const double* H_host, int64_t d, int64_t ldh, doub
  * ns_reflector_batched — `batch` independent problems (configs[1]: many small H, one
  * shift each; pass the same H several times via the stride to sweep shifts).
  *   H      device, H + b*stride_h is problem b's d x d matrix (row-major, ld = d).
- *   s, alpha, k   HOST arrays [batch].
+ *   s, alpha, k   HOST arrays [batch] (ns_reflector_batched_dev: DEVICE arrays, read back and
+ *          validated on the host before any launch).  alpha[b] = 0: device Gershgorin bound.
  *   R      device, R + b*stride_r receives problem b's reflector (ld = d).
  *   outs   HOST array [batch] of result records.
  *   Each problem stops independently (its own steps/flags); problems that stopped
@@ -195,6 +210,45 @@ ns_status_t ns_reflector_batched(const double* H, int64_t d, int64_t batch, int6
                                  int32_t max_steps, double tol, ns_tolmode_t tm, ns_precision_t prec,
                                  double* R, int64_t stride_r, void* ws, size_t ws_bytes, void* stream,
                                  ns_result_t* outs);
+ns_status_t ns_reflector_batched_dev(const double* H, int64_t d, int64_t batch, int64_t stride_h,
+                                     const double* s_dev, const double* alpha_dev, const int32_t* k_dev,
+                                     int32_t max_steps, double tol, ns_tolmode_t tm, ns_precision_t prec,
+                                     double* R, int64_t stride_r, void* ws, size_t ws_bytes, void* stream,
+                                     ns_result_t* outs);
+
+/*
+ * ---------------- inertia probes and shift bisection (alg:ssr steps 3-4) ----------------
+ * ns_inertia: count = #{i : lambda_i(H) < s} from the trace certificate of a Newton–Schulz run on
+ *   X_0 = (H - sI)/alpha with alpha = ||H - sI||_inf (device): the run stops once ||X^2 - I||_F <
+ *   1/(2 sqrt d), where (d - tr X)/2 is provably within 1/4 of the count (lem:NSsign sign preservation;
+ *   sum(1 - |x_i|) <= sqrt(d) ||X^2 - I||_F), so round((d - tr X)/2) is exact.  resolved = 0 when that
+ *   residual was not reached in max_steps (s on, or within ~1e-17 relative of, an eigenvalue).  prec:
+ *   NS_PREC_FP64 or NS_PREC_FP64_OZAKI.  Workspace: ns_workspace_bytes_inertia(d, prec).  out: the
+ *   probe's NS result (steps, residual, alpha used).
+ * ns_shift_bisect: brackets lambda_k and lambda_{k+1} by inertia probes (bisecting the wider bracket)
+ *   until the midpoint of the endpoint estimates is admissible by prop:reuse_refresh (half the
+ *   estimated gap exceeds the estimate error eps) and eps <= rel_eps x estimated gap; 1 <= k <= d-1.
+ *   Initial bracket [lo, hi] (must satisfy count(lo) <= k-1 and count(hi) >= k+1; lo >= hi: the device
+ *   computes [-||H||_inf, ||H||_inf]).  out->ok = 0 if max_probes ran out (e.g. a closed gap).  The
+ *   probe sequence is deterministic (oracle/setup.py shift_bisect is the reference algorithm).
+ */
+typedef struct {
+  double s;                      /* certified midpoint shift (lam_k_hat + lam_k1_hat)/2 */
+  double lam_k_lo, lam_k_hi;     /* lambda_k in [lam_k_lo, lam_k_hi] */
+  double lam_k1_lo, lam_k1_hi;   /* lambda_{k+1} in [lam_k1_lo, lam_k1_hi] */
+  double eps;                    /* max bracket half-width: |lam_hat - lam| <= eps for both endpoints */
+  double alpha;                  /* ||H - sI||_inf at the returned s (0 unless ok) */
+  int32_t probes;                /* inertia probes run (including nudged retries) */
+  int32_t unresolved;            /* probes that had to be nudged off an eigenvalue */
+  int32_t ok;                    /* 1: midpoint certified admissible with eps <= rel_eps * gap estimate */
+  int32_t pad;
+} ns_bisect_t;
+size_t ns_workspace_bytes_inertia(int64_t d, ns_precision_t prec);
+ns_status_t ns_inertia(const double* H, int64_t d, int64_t ldh, double s, ns_precision_t prec, int32_t max_steps,
+                       void* ws, size_t ws_bytes, void* stream, int64_t* count, int32_t* resolved, ns_result_t* out);
+ns_status_t ns_shift_bisect(const double* H, int64_t d, int64_t ldh, int32_t k, double lo, double hi, double rel_eps,
+                            int32_t max_probes, ns_precision_t prec, void* ws, size_t ws_bytes, void* stream,
+                            ns_bisect_t* out);
 
 /*
  * ---------------- shift / scale setup (the step before the path) ----------------

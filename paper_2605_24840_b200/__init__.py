@@ -27,25 +27,26 @@ EXPORTED_SYMBOLS = (
     "ns_workspace_bytes_sharded", "ns_reflector_sharded", "ns_shard_chunks", "ns_workspace_bytes_setup", "ns_scale_bound",
     "ns_shift_certificate", "ns_workspace_bytes_alg1", "ns_alg1_rotated_quartic", "ns_debug_mx_trace",
     "ns_symm_product_shard", "ns_workspace_bytes_sharded_emulated", "ns_reflector_sharded_emulated",
-    "ns_comm_init_host", "ns_shard_rows", "ns_reflector_sharded_rows",
+    "ns_comm_init_host", "ns_shard_rows", "ns_reflector_sharded_rows", "ns_reflector_batched_dev",
+    "ns_workspace_bytes_inertia", "ns_inertia", "ns_shift_bisect", "ns_workspace_bytes_ex",
 )
 
 
 class NsResult(ctypes.Structure):
     _fields_ = [("steps", ctypes.c_int32), ("flags", ctypes.c_int32), ("residual", ctypes.c_double),
                 ("trace", ctypes.c_double), ("index_cert", ctypes.c_int64), ("kernel_launches", ctypes.c_int32),
-                ("switch_step", ctypes.c_int32), ("pre_polish_residual", ctypes.c_double)]
+                ("switch_step", ctypes.c_int32), ("pre_polish_residual", ctypes.c_double), ("alpha", ctypes.c_double)]
 
     def as_dict(self):
         return dict(steps=self.steps, flags=self.flags, residual=self.residual, trace=self.trace,
                     cert=self.index_cert, launches=self.kernel_launches, switch_step=self.switch_step,
-                    pre_polish_residual=self.pre_polish_residual)
+                    pre_polish_residual=self.pre_polish_residual, alpha=self.alpha)
 
 
 class NsOptions(ctypes.Structure):
     _fields_ = [("switch_tol", ctypes.c_double), ("cg_iters", ctypes.c_int32), ("stop_at_switch", ctypes.c_int32),
-                ("lookahead", ctypes.c_int32), ("polish", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2), ("filter_a", ctypes.c_double),
-                ("filter_b", ctypes.c_double)]
+                ("lookahead", ctypes.c_int32), ("polish", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2),
+                ("filter_a", ctypes.c_double), ("filter_b", ctypes.c_double), ("filter_c", ctypes.c_double * 3)]
 
 
 class NsProfile(ctypes.Structure):
@@ -64,6 +65,13 @@ class NsShiftCert(ctypes.Structure):
 class NsAlg1Result(ctypes.Structure):
     _fields_ = [("iters", ctypes.c_int32), ("morse_index", ctypes.c_int32), ("success", ctypes.c_int32),
                 ("pad", ctypes.c_int32), ("grad_norm", ctypes.c_double)]
+
+
+class NsBisect(ctypes.Structure):
+    _fields_ = [("s", ctypes.c_double), ("lam_k_lo", ctypes.c_double), ("lam_k_hi", ctypes.c_double),
+                ("lam_k1_lo", ctypes.c_double), ("lam_k1_hi", ctypes.c_double), ("eps", ctypes.c_double),
+                ("alpha", ctypes.c_double), ("probes", ctypes.c_int32), ("unresolved", ctypes.c_int32),
+                ("ok", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
 class NsError(RuntimeError):
@@ -113,6 +121,18 @@ def load_library(path=LIB_PATH):
     lib.ns_reflector_sharded_emulated.restype = ctypes.c_int
     lib.ns_reflector_sharded_emulated.argtypes = [c_i32, c_vp, c_i64, c_i64, c_dbl, c_dbl, c_i32, c_i32, c_dbl,
                                                   ctypes.c_int, c_vp, c_i64, c_vp, c_sz, c_vp, c_i32, c_vp]
+    lib.ns_workspace_bytes_ex.restype = c_sz
+    lib.ns_workspace_bytes_ex.argtypes = [c_i64, ctypes.c_int, ctypes.POINTER(NsOptions)]
+    lib.ns_reflector_batched_dev.restype = ctypes.c_int
+    lib.ns_reflector_batched_dev.argtypes = lib.ns_reflector_batched.argtypes
+    lib.ns_workspace_bytes_inertia.restype = c_sz
+    lib.ns_workspace_bytes_inertia.argtypes = [c_i64, ctypes.c_int]
+    lib.ns_inertia.restype = ctypes.c_int
+    lib.ns_inertia.argtypes = [c_vp, c_i64, c_i64, c_dbl, ctypes.c_int, c_i32, c_vp, c_sz, c_vp,
+                               ctypes.POINTER(c_i64), ctypes.POINTER(c_i32), ctypes.POINTER(NsResult)]
+    lib.ns_shift_bisect.restype = ctypes.c_int
+    lib.ns_shift_bisect.argtypes = [c_vp, c_i64, c_i64, c_i32, c_dbl, c_dbl, c_dbl, c_i32, ctypes.c_int, c_vp, c_sz,
+                                    c_vp, ctypes.POINTER(NsBisect)]
     lib.ns_comm_init_host.restype = ctypes.c_int
     lib.ns_comm_init_host.argtypes = [ctypes.c_int, ctypes.c_int, HOST_ALLGATHER, c_vp, ctypes.POINTER(c_vp)]
     lib.ns_shard_rows.restype = ctypes.c_int
@@ -249,6 +269,8 @@ def ns_options(**kw):
     o = NsOptions()
     load_library().ns_options_default(ctypes.byref(o))
     for k_, v in kw.items():
+        if k_ == "filter_c":
+            v = (ctypes.c_double * 3)(*(list(v) + [0.0] * (3 - len(v))))
         setattr(o, k_, v)
     return o
 
@@ -266,8 +288,10 @@ def ns_reflector(H, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_ABS, prec=NS_PR
     if R is None:
         R = torch.empty((d, d), dtype=torch.float64, device=H.device)
     _require_cuda_f64(R, "R")
-    if ws is None:
-        ws = alloc_workspace(lib.ns_workspace_bytes(d, prec), H.device)   # (the library checks a given size)
+    if ws is None:   # (the library checks a given size)
+        nb = lib.ns_workspace_bytes_ex(d, prec, ctypes.byref(options)) if options is not None else \
+            lib.ns_workspace_bytes(d, prec)
+        ws = alloc_workspace(nb, H.device)
     res = NsResult()
     args = (ctypes.c_void_p(H.data_ptr()), d, H.stride(0), float(s), float(alpha), int(k), int(max_steps), float(tol),
             int(tol_mode), int(prec), ctypes.c_void_p(R.data_ptr()), R.stride(0), ctypes.c_void_p(ws.data_ptr()),
@@ -338,6 +362,72 @@ def ns_reflector_batched(H, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_ABS, pr
                                       ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream, H.device), outs)
     _check(st)
     return R, [o.as_dict() for o in outs]
+
+
+def ns_reflector_batched_dev(H, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_ABS, prec=NS_PREC_FP64, R=None,
+                             ws=None, stream=None):
+    """Batched reflectors with the per-problem s, alpha, k as CUDA tensors (float64, float64, int32)."""
+    torch = _torch()
+    lib = load_library()
+    _require_cuda_f64(H, "H")
+    if H.dim() != 3 or H.shape[1] != H.shape[2] or not H.is_contiguous():
+        raise NsError("H must be a contiguous (batch, d, d) tensor")
+    b, d = H.shape[0], H.shape[1]
+    for name, t, dt in (("s", s, torch.float64), ("alpha", alpha, torch.float64), ("k", k, torch.int32)):
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == dt and t.numel() == b and t.is_contiguous()):
+            raise NsError(f"{name} must be a contiguous CUDA {dt} tensor of {b} elements")
+    if R is None:
+        R = torch.empty_like(H)
+    if ws is None:
+        ws = alloc_workspace(lib.ns_workspace_bytes_batched(d, b, prec), H.device)
+    _same_device(H, R, ws, s, alpha, k)
+    outs = (NsResult * b)()
+    with _on(H.device):
+        st = lib.ns_reflector_batched_dev(ctypes.c_void_p(H.data_ptr()), d, b, H.stride(0), ctypes.c_void_p(s.data_ptr()),
+                                          ctypes.c_void_p(alpha.data_ptr()), ctypes.c_void_p(k.data_ptr()),
+                                          int(max_steps), float(tol), int(tol_mode), int(prec),
+                                          ctypes.c_void_p(R.data_ptr()), R.stride(0), ctypes.c_void_p(ws.data_ptr()),
+                                          ws.numel(), _stream_ptr(stream, H.device), outs)
+    _check(st)
+    return R, [o.as_dict() for o in outs]
+
+
+def ns_inertia(H, s, prec=NS_PREC_FP64, max_steps=100, ws=None, stream=None):
+    """#{lambda_i(H) < s} from the Newton–Schulz trace certificate (C-ABI ns_inertia).
+    Returns (count, resolved, result dict)."""
+    lib = load_library()
+    _require_cuda_f64(H, "H")
+    d = H.shape[0]
+    if H.dim() != 2 or H.shape[1] != d or H.stride(1) != 1:
+        raise NsError("H must be a square row-major matrix")
+    if ws is None:
+        ws = alloc_workspace(lib.ns_workspace_bytes_inertia(d, prec), H.device)
+    c, r, res = ctypes.c_int64(), ctypes.c_int32(), NsResult()
+    with _on(H.device):
+        st = lib.ns_inertia(ctypes.c_void_p(H.data_ptr()), d, H.stride(0), float(s), int(prec), int(max_steps),
+                            ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream, H.device), ctypes.byref(c),
+                            ctypes.byref(r), ctypes.byref(res))
+    _check(st)
+    return c.value, bool(r.value), res.as_dict()
+
+
+def ns_shift_bisect(H, k, lo=0.0, hi=0.0, rel_eps=0.05, max_probes=200, prec=NS_PREC_FP64, ws=None, stream=None):
+    """Certified midpoint shift for the gap (lambda_k, lambda_k+1) by inertia-probe bisection (C-ABI
+    ns_shift_bisect).  lo >= hi: default bracket [-||H||_inf, ||H||_inf].  Returns a dict."""
+    lib = load_library()
+    _require_cuda_f64(H, "H")
+    d = H.shape[0]
+    if H.dim() != 2 or H.shape[1] != d or H.stride(1) != 1:
+        raise NsError("H must be a square row-major matrix")
+    if ws is None:
+        ws = alloc_workspace(lib.ns_workspace_bytes_inertia(d, prec), H.device)
+    o = NsBisect()
+    with _on(H.device):
+        st = lib.ns_shift_bisect(ctypes.c_void_p(H.data_ptr()), d, H.stride(0), int(k), float(lo), float(hi),
+                                 float(rel_eps), int(max_probes), int(prec), ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                                 _stream_ptr(stream, H.device), ctypes.byref(o))
+    _check(st)
+    return {f: getattr(o, f) for f, _ in NsBisect._fields_ if f != "pad"}
 
 
 def ns_symm_product(A, B, mode=0, C=None, ws=None, stream=None, prec=NS_PREC_FP64):
@@ -451,10 +541,13 @@ def ns_comm_init_host(rank, nranks, allgather):
             parts = allgather(ctypes.string_at(send, nbytes))
             buf = b"".join(parts)
             if len(buf) != nbytes * nranks:
-                return 1
+                raise NsError(f"host all-gather returned {len(buf)} bytes, expected {nbytes} x {nranks}")
             ctypes.memmove(recv, buf, len(buf))
             return 0
         except Exception:      # noqa: BLE001 -- an exception must not cross the C frame
+            import sys
+            import traceback
+            traceback.print_exc(file=sys.stderr)
             return 1
     fn = HOST_ALLGATHER(_cb)
     h = ctypes.c_void_p()

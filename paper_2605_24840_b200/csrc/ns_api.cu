@@ -423,6 +423,12 @@ struct Opts {
   int lookahead = 0;
   int polish = 2;                 // mixed path: 0 = all FP64 DMMA, 1 = all Ozaki INT8, 2 = Ozaki re-anchor + DMMA polish
   double ca = 1.5, cb = -0.5;
+  double cz[kMaxFilterDeg - 1] = {0.0, 0.0, 0.0};   // coefficients of X^5, X^7, X^9 (general filters, run_filter)
+  bool general_filter() const {
+    for (double v : cz)
+      if (v != 0.0) return true;
+    return false;
+  }
   // host entry: the caller's pinned R (device-accessible address) for the speculative result copy;
   // run_loop sets *spec_hit when R already holds the returned iterate
   double* spec_R = nullptr;
@@ -444,6 +450,7 @@ Opts to_opts(const ns_options_t* o) {
     r.polish = o->polish;
     r.ca = o->filter_a;
     r.cb = o->filter_b;
+    for (int i = 0; i < kMaxFilterDeg - 1; ++i) r.cz[i] = o->filter_c[i];
   }
   return r;
 }
@@ -817,6 +824,170 @@ ns_status_t run_ozaki(const Layout& L, uint8_t* ws, const double* H, long long l
                                         st, opt, states, launches);
   if (s == NS_OK) out_state = states[0];
   return s;
+}
+
+// General odd sign-preserving polynomial filter steps (eq:signpreserving P:278-289, the
+// "low-degree odd polynomial filters" of P:513-518): X_{j+1} = phi(X_j) = sum_{i=0}^{m} c_i X_j^{2i+1}
+// = X_j P(Y_j), P(y) = sum_i c_i y^i, Y_j = X_j^2, degree m >= 2 in Y (m = 1 is the cubic step of run_loop).
+// P(Y) is formed by Horner's rule in Y with symmetric products (every Horner iterate is a polynomial in Y,
+// so it commutes with Y and X and the upper-tile products with mirrored writes apply):
+//   T_{m-2} = c_m Y Y + c_{m-1} Y + c_{m-2} I         (product Y.Y; mode-1 epilogue ca = c_{m-1}, cb = c_m, cc)
+//   T_i     = T_{i+1} Y + c_i I,  i = m-3 .. 0          (mode 1, ca = 0, cb = 1, cc = c_i)
+//   X_{j+1} = X_j T_0                                   (mode 1, ca = 0, cb = 1: trace partials of X_{j+1})
+// m + 1 products per step (the square + m - 1 Horner + 1), one extra d_pad^2 buffer E (T_i in E for even i,
+// in X_{j+1}'s buffer for odd i).  The square, residual, decide and stop rule are the NS loop's.  FP64 DMMA
+// or the Ozaki INT8 products (the operands of every product are re-sliced as needed).
+ns_status_t run_filter(const Layout& L, uint8_t* ws, const double* H, long long ldh, const JobParams& jp,
+                       int32_t max_steps, double tol, ns_tolmode_t tm, double* R, long long ldr, cudaStream_t st,
+                       const Opts& opt, bool ozaki, DevState& out_state, int* launches) {
+  double c[kMaxFilterDeg + 1] = {opt.ca, opt.cb};
+  for (int i = 2; i <= kMaxFilterDeg; ++i) c[i] = opt.cz[i - 2];
+  int m = kMaxFilterDeg;
+  while (m > 2 && c[m] == 0.0) --m;
+  double* Xa = reinterpret_cast<double*>(ws + L.off_xa);
+  double* Xb = reinterpret_cast<double*>(ws + L.off_xb);
+  double* Y = reinterpret_cast<double*>(ws + L.off_y);
+  double* E = reinterpret_cast<double*>(ws + align256(L.total));
+  JobParams* djobs = reinterpret_cast<JobParams*>(ws + L.off_jobs);
+  DevState* state = reinterpret_cast<DevState*>(ws + L.off_state);
+  int* n_active = reinterpret_cast<int*>(ws + L.off_active);
+  HostRing& rg = ring();
+  if (!rg.ok) return fail(NS_ERR_CUDA, "pinned status ring allocation failed");
+  NS_CUDA(cudaMemcpyAsync(djobs, &jp, sizeof(JobParams), cudaMemcpyHostToDevice, st));
+  ns_status_t s;
+  int nl = 0;
+  LoopParams lp{L.d, L.d_pad, max_steps, (int)tm, tol, 0.0, -1, 0};
+  const int LA = opt.lookahead > 0 ? std::min(opt.lookahead, 15) : 2;
+  NS_CUDA(launch_zero_state(state, 1, n_active, st));
+  NS_CUDA(launch_init(H, ldh, 0, Xa, djobs, L.d, L.d_pad, 1, st));
+  nl += 2;
+  if (!ozaki) {
+    double* res = reinterpret_cast<double*>(ws + L.off_res);
+    double* trp = reinterpret_cast<double*>(ws + L.off_tr);
+    int2* tiles = reinterpret_cast<int2*>(ws + L.off_tiles);
+    const bool t64 = use_tile64(L.d_pad, 1);
+    const int tile_rows = t64 ? k64Tile : kTile;
+    const int nb = L.d_pad / tile_rows;
+    const std::vector<int2> tl = make_tiles(nb);
+    const int n_t = (int)tl.size();
+    NS_CUDA(cudaMemcpyAsync(tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+    CUtensorMap tmA, tmB, tmY, tmE;
+    if ((s = encode_map(&tmA, Xa, L.d_pad, 1, tile_rows)) != NS_OK) return s;
+    if ((s = encode_map(&tmB, Xb, L.d_pad, 1, tile_rows)) != NS_OK) return s;
+    if ((s = encode_map(&tmY, Y, L.d_pad, 1, tile_rows)) != NS_OK) return s;
+    if ((s = encode_map(&tmE, E, L.d_pad, 1, tile_rows)) != NS_OK) return s;
+    auto product = [&](const CUtensorMap& a, const CUtensorMap& b, const ProdParams& pp) {
+      ++nl;
+      return t64 ? launch_product64(a, b, pp, 1, st) : launch_product(a, b, pp, 1, st);
+    };
+    if (t64) NS_CUDA(cudaMemsetAsync(trp, 0, sizeof(double) * nb, st));
+    NS_CUDA(launch_trace_partials(Xa, L.d, L.d_pad, 1, trp, st, nb));
+    ++nl;
+    for (int j = 0; j <= max_steps; ++j) {
+      if (j >= LA) {
+        const int slot = (j - LA) % 16;
+        NS_CUDA(cudaEventSynchronize(rg.ev[slot]));
+        if (rg.slots[slot] == 0) break;
+      }
+      const bool odd = (j & 1) != 0;
+      double* Xc = odd ? Xb : Xa;
+      double* Xn = odd ? Xa : Xb;
+      const CUtensorMap& tC = odd ? tmB : tmA;
+      const CUtensorMap& tN = odd ? tmA : tmB;
+      ProdParams sq{tiles, n_t, L.d_pad / kBK, L.d, L.d_pad, 0, Y, nullptr, res, state, 0};
+      NS_CUDA(product(tC, tC, sq));
+      NS_CUDA(launch_decide(state, djobs, res, n_t, trp, nb, lp, 1, n_active, st));
+      ++nl;
+      if (j < max_steps) {
+        for (int i = m - 2; i >= 0; --i) {     // Horner in Y; the partial buffer res is free after the decide
+          const bool first = (i == m - 2);
+          double* A = first ? Y : (((i + 1) % 2 == 0) ? E : Xn);
+          const CUtensorMap& tAm = first ? tmY : (((i + 1) % 2 == 0) ? tmE : tN);
+          double* T = (i % 2 == 0) ? E : Xn;
+          ProdParams hp{tiles, n_t, L.d_pad / kBK, L.d, L.d_pad, 0, T, A, res, state, 1,
+                        first ? c[m - 1] : 0.0, first ? c[m] : 1.0};
+          hp.cc = c[i];
+          NS_CUDA(product(tAm, tmY, hp));
+        }
+        ProdParams fp{tiles, n_t, L.d_pad / kBK, L.d, L.d_pad, 0, Xn, Xc, trp, state, 1, 0.0, 1.0};
+        NS_CUDA(product(tC, tmE, fp));
+      }
+      NS_CUDA(cudaMemcpyAsync(&rg.slots[j % 16], n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+      NS_CUDA(cudaEventRecord(rg.ev[j % 16], st));
+    }
+  } else {
+    double* res = reinterpret_cast<double*>(ws + L.off_ores);
+    double* trp = reinterpret_cast<double*>(ws + L.off_otr);
+    int8_t* slX = reinterpret_cast<int8_t*>(ws + L.off_ozx);
+    int8_t* slY = reinterpret_cast<int8_t*>(ws + L.off_ozy);
+    int* eX = reinterpret_cast<int*>(ws + L.off_oex);
+    int* eY = reinterpret_cast<int*>(ws + L.off_oey);
+    int2* otiles = reinterpret_cast<int2*>(ws + L.off_otiles);
+    const std::vector<int2> ot = oz_tile_list(L.n, true);
+    const int nt = (int)ot.size(), npart = oz_partials(ot), ndiag = 2 * L.n;
+    NS_CUDA(cudaMemcpyAsync(otiles, ot.data(), ot.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+    CUtensorMap tXa, tXb, tYa, tY;
+    if ((s = encode_map_i8(&tXa, slX, L.d_pad, kOzSlices, kTile)) != NS_OK) return s;
+    if ((s = encode_map_i8(&tXb, slX, L.d_pad, kOzSlices, 64)) != NS_OK) return s;
+    if ((s = encode_map_i8(&tYa, slY, L.d_pad, kOzSlices, kTile)) != NS_OK) return s;
+    if ((s = encode_map_i8(&tY, slY, L.d_pad, kOzSlices, 64)) != NS_OK) return s;
+    const int groups = oz_groups(tol, tm, L.d);
+    NS_CUDA(cudaMemsetAsync(trp, 0, sizeof(double) * ndiag, st));
+    NS_CUDA(launch_trace_partials(Xa, L.d, L.d_pad, 1, trp, st, ndiag));
+    ++nl;
+    for (int j = 0; j <= max_steps; ++j) {
+      if (j >= LA) {
+        const int slot = (j - LA) % 16;
+        NS_CUDA(cudaEventSynchronize(rg.ev[slot]));
+        if (rg.slots[slot] == 0) break;
+      }
+      const bool odd = (j & 1) != 0;
+      double* Xc = odd ? Xb : Xa;
+      double* Xn = odd ? Xa : Xb;
+      NS_CUDA(launch_ozaki_slice(Xc, slX, eX, L.d_pad, 1, st));
+      OzParams sq{otiles, nt, L.d_pad / 64, L.d, L.d_pad, 0, Y, nullptr, eX, eX, res, state, 0};
+      sq.groups = groups;
+      NS_CUDA(oz_product(tXa, tXb, sq, 1, st));
+      NS_CUDA(launch_decide(state, djobs, res, npart, trp, ndiag, lp, 1, n_active, st));
+      nl += 3;
+      if (j < max_steps) {
+        NS_CUDA(launch_ozaki_slice(Y, slY, eY, L.d_pad, 1, st));
+        ++nl;
+        for (int i = m - 2; i >= 0; --i) {
+          const bool first = (i == m - 2);
+          double* A = first ? Y : (((i + 1) % 2 == 0) ? E : Xn);
+          if (!first) {                        // A-operand digits of T_{i+1} (X_j's digits are re-sliced below)
+            NS_CUDA(launch_ozaki_slice(A, slX, eX, L.d_pad, 1, st));
+            ++nl;
+          }
+          double* T = (i % 2 == 0) ? E : Xn;
+          OzParams hp{otiles, nt, L.d_pad / 64, L.d, L.d_pad, 0, T, A, first ? eY : eX, eY, res, state, 1,
+                      first ? c[m - 1] : 0.0, first ? c[m] : 1.0};
+          hp.cc = c[i];
+          hp.groups = groups;
+          NS_CUDA(oz_product(first ? tYa : tXa, tY, hp, 1, st));
+          ++nl;
+        }
+        if (m >= 3) {
+          NS_CUDA(launch_ozaki_slice(Xc, slX, eX, L.d_pad, 1, st));
+          ++nl;
+        }
+        NS_CUDA(launch_ozaki_slice(E, slY, eY, L.d_pad, 1, st));   // T_0 (Y's digits are no longer needed)
+        OzParams fp{otiles, nt, L.d_pad / 64, L.d, L.d_pad, 0, Xn, Xc, eX, eY, trp, state, 1, 0.0, 1.0};
+        fp.groups = groups;
+        NS_CUDA(oz_product(tXa, tY, fp, 1, st));
+        nl += 2;
+      }
+      NS_CUDA(cudaMemcpyAsync(&rg.slots[j % 16], n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+      NS_CUDA(cudaEventRecord(rg.ev[j % 16], st));
+    }
+  }
+  NS_CUDA(launch_copy_out(Xa, Xb, L.d, L.d_pad, state, R, ldr, 0, 1, st));
+  ++nl;
+  NS_CUDA(cudaMemcpyAsync(&out_state, state, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+  NS_CUDA(cudaStreamSynchronize(st));
+  if (launches) *launches = nl;
+  return NS_OK;
 }
 
 // Mixed path (single problem): BF16x3 tcgen05 steps -> switch -> re-anchor -> FP64 steps.
@@ -1281,7 +1452,9 @@ ns_status_t setup_peers(CommCtx& cc, uint8_t* ws, uint8_t* scratch, cudaStream_t
     cudaIpcMemHandle_t h;              // 64 bytes
     unsigned long long off, size;      // 16
     int ok;
-    int pad[11];
+    int pad0;
+    unsigned long long ws_addr;        // the rank's workspace address: part of the key also without a handle
+    int pad[8];
   };
   static_assert(sizeof(Rec) == 128, "IPC record size");
   Rec mine{};
@@ -1296,15 +1469,18 @@ ns_status_t setup_peers(CommCtx& cc, uint8_t* ws, uint8_t* scratch, cudaStream_t
   }
   mine.off = mine.ok ? (unsigned long long)(reinterpret_cast<uintptr_t>(ws) - (uintptr_t)base) : 0ull;
   mine.size = mine.ok ? (unsigned long long)size : 0ull;
+  mine.ws_addr = (unsigned long long)reinterpret_cast<uintptr_t>(ws);
   std::vector<Rec> all(nranks);
   ns_status_t s = comm_allgather_host(cc, &mine, all.data(), sizeof(Rec), scratch, st);
   if (s != NS_OK) return s;
   auto key_of = [](const Rec& r) {
     std::array<uint8_t, 96> k{};
-    memcpy(k.data(), &r, 84);          // handle, off, size, ok
+    memcpy(k.data(), &r, 96);          // handle, off, size, ok, ws address
     return k;
   };
-  bool same = cc.valid && (int)cc.keys.size() == nranks && cc.peer_ws.size() == (size_t)nranks && cc.peer_ws[rank] == ws;
+  // decided on gathered data only (identical on every rank): the previous records of EVERY rank equal the
+  // new ones, and so does this rank's own (which includes its ws address)
+  bool same = cc.valid && (int)cc.keys.size() == nranks;
   for (int r = 0; r < nranks && same; ++r) same = (cc.keys[r] == key_of(all[r]));
   if (same) return NS_OK;              // identical decision on every rank (same gathered records)
   close_peers(cc);
@@ -1411,8 +1587,10 @@ ns_status_t run_sharded(CommCtx& cc, const ShardLayout& SL, uint8_t* ws, const d
       const int s0 = c * SL.cs;
       const int cnt = std::max(0, std::min(SL.cs, n_my - s0));
       if (cnt > 0) {
+        // mode 0: residual partial per local tile slot; mode 1: trace partial per diagonal block I (global
+        // index: an offset by s0 would write past the n-entry trace buffer)
         ProdParams pp{my + s0, cnt, L.d_pad / kBK, L.d, L.d_pad, (long long)L.d_pad * L.d_pad, C, Xold,
-                      partial + s0, state, mode};
+                      mode == 0 ? partial + s0 : partial, state, mode};
         NS_CUDA(launch_product(tP, tQ, pp, 1, st));
         nl += 1;
       }
@@ -1734,6 +1912,18 @@ ns_status_t run_sharded_emulated(int64_t d, int P, uint8_t* ws, size_t stride, c
   return NS_OK;
 }
 
+// alpha = ||H - sI||_inf on the device (the Gershgorin bound of ns_scale_bound, N1), read back with one
+// 8-byte copy; scratch: d + 1 doubles of device memory that the caller's next launches overwrite anyway.
+ns_status_t device_scale_bound(const double* H, long long ldh, int d, double s, double* scratch, cudaStream_t st,
+                               double* alpha) {
+  NS_CUDA(launch_scale_bound(H, ldh, d, s, scratch, scratch + d, st));
+  NS_CUDA(cudaMemcpyAsync(alpha, scratch + d, sizeof(double), cudaMemcpyDeviceToHost, st));
+  NS_CUDA(cudaStreamSynchronize(st));
+  if (!std::isfinite(*alpha)) return fail(NS_ERR_INVALID_ARG, "H - sI has a non-finite entry: no scale bound");
+  if (!(*alpha > 0.0)) *alpha = 1.0;       // H = sI: X_0 = 0 for any alpha
+  return NS_OK;
+}
+
 void fill_result(const DevState& s, int launches, ns_result_t* out) {
   out->kernel_launches = launches;
   out->switch_step = s.sw_step;
@@ -1763,6 +1953,14 @@ size_t ns_workspace_bytes_batched(int64_t d, int64_t batch, ns_precision_t prec)
 
 size_t ns_workspace_bytes_host(int64_t d, ns_precision_t prec) { return ns_workspace_bytes(d, prec); }
 
+size_t ns_workspace_bytes_ex(int64_t d, ns_precision_t prec, const ns_options_t* opts) {
+  if (d < 1) return 0;
+  const size_t base = ns_workspace_bytes(d, prec);
+  if (!opts || !to_opts(opts).general_filter()) return base;
+  const size_t dp = (size_t)((d + kTile - 1) / kTile * kTile);
+  return align256(base) + align256(dp * dp * sizeof(double));   // + E, the Horner buffer of run_filter
+}
+
 void ns_options_default(ns_options_t* o) {
   if (!o) return;
   *o = ns_options_t{};
@@ -1785,7 +1983,8 @@ ns_status_t ns_reflector_ex(const double* H, int64_t d, int64_t ldh, double s, d
   if (!H || !R || !ws || !out) return fail(NS_ERR_INVALID_ARG, "null pointer argument");
   if (ldh < d || ldr < d) return fail(NS_ERR_INVALID_ARG, "leading dimensions must be >= d");
   if (!std::isfinite(s)) return fail(NS_ERR_INVALID_ARG, "shift s must be finite");
-  if (!(alpha > 0.0) || !std::isfinite(alpha)) return fail(NS_ERR_INVALID_ARG, "alpha must be finite and > 0");
+  if (!(alpha >= 0.0) || !std::isfinite(alpha))
+    return fail(NS_ERR_INVALID_ARG, "alpha must be finite and > 0 (or 0: Gershgorin bound on the device)");
   if (k < 0 || k > d) return fail(NS_ERR_INVALID_ARG, "k must lie in [0, d]");
   if (R == H) return fail(NS_ERR_INVALID_ARG, "R must not alias H");
   if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(NS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
@@ -1796,12 +1995,34 @@ ns_status_t ns_reflector_ex(const double* H, int64_t d, int64_t ldh, double s, d
   const Layout L = make_layout(d, 1, mixed, ozaki || mixed, tf32);
   if (ws_bytes < L.total)
     return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
+  if (alpha == 0.0) {   // N1: alpha = ||H - sI||_inf >= ||H - sI||_2 from the device (Y is scratch until the first square)
+    st = device_scale_bound(H, ldh, (int)d, s, reinterpret_cast<double*>(static_cast<uint8_t*>(ws) + L.off_y),
+                            static_cast<cudaStream_t>(stream), &alpha);
+    if (st != NS_OK) return st;
+  }
+  out->alpha = alpha;
   const Opts o = to_opts(opts);
   if (mixed && (!(o.switch_tol >= 0.0) || o.cg_iters < 0 || o.polish < 0 || o.polish > 2))
     return fail(NS_ERR_INVALID_ARG, "bad mixed options");
   if (!std::isfinite(o.ca) || !std::isfinite(o.cb)) return fail(NS_ERR_INVALID_ARG, "filter coefficients must be finite");
   if (mixed && (o.ca != 1.5 || o.cb != -0.5))
     return fail(NS_ERR_UNSUPPORTED, "the mixed path runs the Newton-Schulz step (1.5, -0.5) only");
+  for (double v : o.cz)
+    if (!std::isfinite(v)) return fail(NS_ERR_INVALID_ARG, "filter coefficients must be finite");
+  if (o.general_filter()) {   // N3: general odd polynomial filter (degree >= 5)
+    if (mixed) return fail(NS_ERR_UNSUPPORTED, "general polynomial filters run on the FP64 and Ozaki paths");
+    if (ws_bytes < ns_workspace_bytes_ex(d, prec, opts))
+      return fail(NS_ERR_WORKSPACE, "workspace too small for a general filter: %zu < %zu bytes", ws_bytes,
+                  ns_workspace_bytes_ex(d, prec, opts));
+    DevState ds;
+    int nl = 0;
+    st = run_filter(L, static_cast<uint8_t*>(ws), H, ldh, JobParams{s, alpha, k, 0}, max_steps, tol, tm, R, ldr,
+                    static_cast<cudaStream_t>(stream), o, ozaki, ds, &nl);
+    xprof_flush();
+    if (st != NS_OK) return st;
+    fill_result(ds, nl, out);
+    return NS_OK;
+  }
   std::vector<JobParams> jobs{JobParams{s, alpha, k, 0}};
   int nl = 0;
   if (mixed || ozaki) {
@@ -1897,6 +2118,7 @@ ns_status_t ns_reflector_host(const double* H_host, int64_t d, int64_t ldh, doub
     if (st != NS_OK) return st;
     if (hit) {
       fill_result(states[0], nl, out);
+      out->alpha = alpha;
       return NS_OK;
     }
   }
@@ -1905,6 +2127,7 @@ ns_status_t ns_reflector_host(const double* H_host, int64_t d, int64_t ldh, doub
                             cudaMemcpyDeviceToHost, cs));
   NS_CUDA(cudaStreamSynchronize(cs));
   fill_result(states[0], nl, out);
+  out->alpha = alpha;
   return NS_OK;
 }
 
@@ -1922,17 +2145,36 @@ ns_status_t ns_reflector_batched(const double* H, int64_t d, int64_t batch, int6
   if (stride_h < d * d || stride_r < d * d) return fail(NS_ERR_INVALID_ARG, "strides must be >= d*d");
   if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(NS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
   std::vector<JobParams> jobs(batch);
+  bool any_auto = false;
   for (int64_t b = 0; b < batch; ++b) {
     if (!std::isfinite(s[b])) return fail(NS_ERR_INVALID_ARG, "s[%lld] not finite", (long long)b);
-    if (!(alpha[b] > 0.0) || !std::isfinite(alpha[b]))
-      return fail(NS_ERR_INVALID_ARG, "alpha[%lld] must be finite and > 0", (long long)b);
+    if (!(alpha[b] >= 0.0) || !std::isfinite(alpha[b]))
+      return fail(NS_ERR_INVALID_ARG, "alpha[%lld] must be finite and > 0 (or 0: device Gershgorin bound)", (long long)b);
     if (k[b] < 0 || k[b] > d) return fail(NS_ERR_INVALID_ARG, "k[%lld] out of [0, d]", (long long)b);
     jobs[b] = JobParams{s[b], alpha[b], k[b], 0};
+    any_auto |= alpha[b] == 0.0;
   }
   const bool ozaki = (prec == NS_PREC_FP64_OZAKI);
   const Layout L = make_layout(d, batch, false, ozaki);
   if (ws_bytes < L.total)
     return fail(NS_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, L.total);
+  if (any_auto) {   // N1: per-job ||H_b - s_b I||_inf on the device (job b's Y buffer is scratch), one readback
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    double* Yb = reinterpret_cast<double*>(static_cast<uint8_t*>(ws) + L.off_y);
+    const size_t js = (size_t)L.d_pad * L.d_pad;
+    std::vector<double> a(batch, 0.0);
+    for (int64_t b = 0; b < batch; ++b)
+      if (jobs[b].alpha == 0.0) {
+        NS_CUDA(launch_scale_bound(H + b * stride_h, d, (int)d, jobs[b].s, Yb + b * js, Yb + b * js + d, cs));
+        NS_CUDA(cudaMemcpyAsync(&a[b], Yb + b * js + d, sizeof(double), cudaMemcpyDeviceToHost, cs));
+      }
+    NS_CUDA(cudaStreamSynchronize(cs));
+    for (int64_t b = 0; b < batch; ++b)
+      if (jobs[b].alpha == 0.0) {
+        if (!std::isfinite(a[b])) return fail(NS_ERR_INVALID_ARG, "H[%lld] - s I has a non-finite entry", (long long)b);
+        jobs[b].alpha = a[b] > 0.0 ? a[b] : 1.0;
+      }
+  }
   std::vector<DevState> states;
   int nl = 0;
   if (ozaki) {
@@ -1943,7 +2185,139 @@ ns_status_t ns_reflector_batched(const double* H, int64_t d, int64_t batch, int6
     st = run_loop(L, static_cast<uint8_t*>(ws), H, d, stride_h, jobs, max_steps, tol, tm, R, d, stride_r,
                   static_cast<cudaStream_t>(stream), states, &nl);
   if (st != NS_OK) return st;
-  for (int64_t b = 0; b < batch; ++b) fill_result(states[b], nl, &outs[b]);
+  for (int64_t b = 0; b < batch; ++b) {
+    fill_result(states[b], nl, &outs[b]);
+    outs[b].alpha = jobs[b].alpha;
+  }
+  return NS_OK;
+}
+
+ns_status_t ns_reflector_batched_dev(const double* H, int64_t d, int64_t batch, int64_t stride_h, const double* s_dev,
+                                     const double* alpha_dev, const int32_t* k_dev, int32_t max_steps, double tol,
+                                     ns_tolmode_t tm, ns_precision_t prec, double* R, int64_t stride_r, void* ws,
+                                     size_t ws_bytes, void* stream, ns_result_t* outs) {
+  g_last_error.clear();
+  if (batch < 1 || batch > 65535) return fail(NS_ERR_INVALID_ARG, "batch must be in [1, 65535]");
+  if (!s_dev || !alpha_dev || !k_dev) return fail(NS_ERR_INVALID_ARG, "null pointer argument");
+  // the per-problem scalars are validated on the host before any launch (same contract as the host-array
+  // entry): one small copy of 20 bytes per problem and one synchronisation
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  std::vector<double> s(batch), a(batch);
+  std::vector<int32_t> k(batch);
+  NS_CUDA(cudaMemcpyAsync(s.data(), s_dev, sizeof(double) * batch, cudaMemcpyDeviceToHost, cs));
+  NS_CUDA(cudaMemcpyAsync(a.data(), alpha_dev, sizeof(double) * batch, cudaMemcpyDeviceToHost, cs));
+  NS_CUDA(cudaMemcpyAsync(k.data(), k_dev, sizeof(int32_t) * batch, cudaMemcpyDeviceToHost, cs));
+  NS_CUDA(cudaStreamSynchronize(cs));
+  return ns_reflector_batched(H, d, batch, stride_h, s.data(), a.data(), k.data(), max_steps, tol, tm, prec, R,
+                              stride_r, ws, ws_bytes, stream, outs);
+}
+
+size_t ns_workspace_bytes_inertia(int64_t d, ns_precision_t prec) {
+  if (d < 1) return 0;
+  return align256(ns_workspace_bytes(d, prec)) + align256(sizeof(double) * (size_t)d * (size_t)d);
+}
+
+// Inertia probe (N1; alg:ssr step 3 "estimate the target-gap endpoints", realised with the trace
+// certificate of prop:exact): #{i : lambda_i(H) < s} = round((d - tr X_m)/2) for the NS iterate X_m of
+// X_0 = (H - sI)/alpha, alpha = ||H - sI||_inf >= ||H - sI||_2 (so spec(X_0) c [-1, 1]), run until
+// ||X_m^2 - I||_F < 1/(2 sqrt d).  Then every |x_i| <= 1 has the sign of lambda_i - s (lem:NSsign) and
+// sum_i (1 - |x_i|) <= sum_i (1 - x_i^2) <= sqrt(d) ||X_m^2 - I||_F < 1/2, so (d - tr X_m)/2 is within 1/4
+// of the number of negative x_i: the rounded certificate IS the count.
+ns_status_t ns_inertia(const double* H, int64_t d, int64_t ldh, double s, ns_precision_t prec, int32_t max_steps,
+                       void* ws, size_t ws_bytes, void* stream, int64_t* count, int32_t* resolved, ns_result_t* out) {
+  g_last_error.clear();
+  if (!count || !resolved || !out || !ws || !H) return fail(NS_ERR_INVALID_ARG, "null pointer argument");
+  if (prec != NS_PREC_FP64 && prec != NS_PREC_FP64_OZAKI)
+    return fail(NS_ERR_UNSUPPORTED, "inertia probes run on the FP64 or Ozaki path");
+  if (d < 1 || d > 65536) return fail(NS_ERR_INVALID_ARG, "d must be in [1, 65536]");
+  if (ws_bytes < ns_workspace_bytes_inertia(d, prec)) return fail(NS_ERR_WORKSPACE, "workspace too small");
+  const size_t base = align256(ns_workspace_bytes(d, prec));
+  double* Rs = reinterpret_cast<double*>(static_cast<uint8_t*>(ws) + base);
+  const double tol = 0.5 / std::sqrt((double)d);
+  ns_status_t st = ns_reflector_ex(H, d, ldh, s, 0.0, 0, max_steps, tol, NS_TOL_ABS, prec, Rs, d, ws, base, stream,
+                                   nullptr, out);
+  if (st != NS_OK) return st;
+  *resolved = (out->flags & NS_F_CONVERGED) && !(out->flags & NS_F_NONFINITE) ? 1 : 0;
+  *count = out->index_cert;
+  return NS_OK;
+}
+
+// Endpoint bisection with inertia probes (N1): brackets lambda_k in (a_k, b_k] and lambda_{k+1} in
+// (a_k1, b_k1] (count(a) <= k-1 < k <= count(b), and likewise for k+1), refining the wider bracket at its
+// midpoint, until the estimated midpoint is certified admissible by prop:reuse_refresh (half the estimated
+// gap exceeds the estimate error eps) with eps <= rel_eps * estimated gap.  The reference algorithm (same
+// probe sequence, same floating-point formulas) is oracle/setup.py shift_bisect.
+ns_status_t ns_shift_bisect(const double* H, int64_t d, int64_t ldh, int32_t k, double lo, double hi, double rel_eps,
+                            int32_t max_probes, ns_precision_t prec, void* ws, size_t ws_bytes, void* stream,
+                            ns_bisect_t* out) {
+  g_last_error.clear();
+  if (!out || !ws || !H) return fail(NS_ERR_INVALID_ARG, "null pointer argument");
+  if (d < 2 || d > 65536) return fail(NS_ERR_INVALID_ARG, "d must be in [2, 65536]");
+  if (k < 1 || k > d - 1) return fail(NS_ERR_INVALID_ARG, "k must lie in [1, d - 1] (the gap (lambda_k, lambda_k+1))");
+  if (!(rel_eps > 0.0) || !(rel_eps < 0.5)) return fail(NS_ERR_INVALID_ARG, "rel_eps must lie in (0, 0.5)");
+  if (max_probes < 1) return fail(NS_ERR_INVALID_ARG, "max_probes must be >= 1");
+  if (ws_bytes < ns_workspace_bytes_inertia(d, prec)) return fail(NS_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  *out = ns_bisect_t{};
+  if (!(lo < hi) || !std::isfinite(lo) || !std::isfinite(hi)) {
+    // default bracket: [-||H||_inf, ||H||_inf] contains the spectrum (count = 0 / d at the ends, not probed)
+    double nrm = 0.0;
+    ns_status_t st = device_scale_bound(H, ldh, (int)d, 0.0, static_cast<double*>(ws), cs, &nrm);
+    if (st != NS_OK) return st;
+    hi = nrm * (1.0 + 1e-12) + 1e-300;
+    lo = -hi;
+  }
+  double ak = lo, bk = hi, ak1 = lo, bk1 = hi;
+  int probes = 0, unresolved = 0;
+  ns_result_t r{};
+  for (;;) {
+    const double lk = 0.5 * (ak + bk), lk1 = 0.5 * (ak1 + bk1);
+    const double eps = 0.5 * std::max(bk - ak, bk1 - ak1);
+    const double gap = lk1 - lk;
+    if (gap > 0.0 && 0.5 * gap > eps && eps <= rel_eps * gap) {
+      out->ok = 1;
+      break;
+    }
+    if (probes >= max_probes) break;
+    const bool refine_k = (bk - ak) >= (bk1 - ak1);
+    const double a = refine_k ? ak : ak1, b = refine_k ? bk : bk1;
+    double sp = 0.5 * (a + b);
+    int64_t c = 0;
+    int32_t res = 0;
+    for (int tries = 0; tries < 8; ++tries) {
+      ns_status_t st = ns_inertia(H, d, ldh, sp, prec, 100, ws, ws_bytes, stream, &c, &res, &r);
+      if (st != NS_OK) return st;
+      ++probes;
+      if (res) break;
+      ++unresolved;                                // s on (or within ~1e-17 of) an eigenvalue: nudge
+      sp = sp + (b - a) * std::ldexp(1.0, -20 + tries);
+    }
+    if (!res) return fail(NS_ERR_CUDA, "inertia probe unresolved after 8 nudges at s = %.17g", sp);
+    if (c <= k - 1) {
+      ak = std::max(ak, sp);
+      ak1 = std::max(ak1, sp);
+    } else if (c == k) {
+      bk = std::min(bk, sp);
+      ak1 = std::max(ak1, sp);
+    } else {
+      bk = std::min(bk, sp);
+      bk1 = std::min(bk1, sp);
+    }
+  }
+  out->lam_k_lo = ak;
+  out->lam_k_hi = bk;
+  out->lam_k1_lo = ak1;
+  out->lam_k1_hi = bk1;
+  out->eps = 0.5 * std::max(bk - ak, bk1 - ak1);
+  out->s = 0.5 * (0.5 * (ak + bk) + 0.5 * (ak1 + bk1));
+  out->probes = probes;
+  out->unresolved = unresolved;
+  if (out->ok) {   // the scale at the returned shift (device Gershgorin bound)
+    double al = 0.0;
+    ns_status_t st = device_scale_bound(H, ldh, (int)d, out->s, static_cast<double*>(ws), cs, &al);
+    if (st != NS_OK) return st;
+    out->alpha = al;
+  }
   return NS_OK;
 }
 
@@ -2172,6 +2546,7 @@ ns_status_t ns_reflector_sharded_emulated(int32_t nranks, const double* H, int64
                             max_steps, tol, tm, R, ldr, static_cast<cudaStream_t>(stream), ds, &nl, flags);
   if (st != NS_OK) return st;
   fill_result(ds, nl, out);
+  out->alpha = alpha;
   return NS_OK;
 }
 
@@ -2226,6 +2601,7 @@ ns_status_t ns_reflector_sharded(ns_comm_t* comm, const double* H, int64_t d, in
                    max_steps, tol, tm, R, ldr, static_cast<cudaStream_t>(stream), ds, &nl, shard_sender_mirror());
   if (st != NS_OK) return st;
   fill_result(ds, nl, out);
+  out->alpha = alpha;
   return NS_OK;
 }
 
@@ -2269,6 +2645,7 @@ ns_status_t ns_reflector_sharded_rows(ns_comm_t* comm, const double* H_rows, int
                    max_steps, tol, tm, R_rows, ldr, static_cast<cudaStream_t>(stream), ds, &nl, shard_sender_mirror());
   if (st != NS_OK) return st;
   fill_result(ds, nl, out);
+  out->alpha = alpha;
   return NS_OK;
 }
 

@@ -297,9 +297,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int u = 0; u < 8; ++u) {
           const int idx = idx0 + u * 256, r = idx >> 7, c = idx & 127;
           if (r <= c) {
-            const double v = fma(p.cb, S[r * kEpiPitch + c], p.ca * xv[u]);
+            double v = fma(p.cb, S[r * kEpiPitch + c], p.ca * xv[u]);
+            if (r == c && I * kTile + r < p.d) {
+              v += p.cc;
+              part += v;
+            }
             S[r * kEpiPitch + c] = v;
-            if (r == c && I * kTile + r < p.d) part += v;
           }
         }
       }
@@ -579,6 +582,10 @@ __global__ void __launch_bounds__(k64Threads, k64Stages == 2 ? 3 : 2)
   const int i0 = I * k64Tile, j0 = J * k64Tile;
   double part = 0.0;
   constexpr int NE = k64Tile * k64Tile;          // 4096 elements, 32 per thread
+  if (MODE == 1 && diag && p.cc != 0.0) {        // + cc I (general odd polynomial filters, Horner steps)
+    if (tid < k64Tile && i0 + tid < p.d) S[tid * EP + tid] += p.cc;
+    __syncthreads();
+  }
   if (MODE == 1 && diag && tid < k64Tile && i0 + tid < p.d) part = S[tid * EP + tid];   // trace partial
   if (!diag) {
     for (int idx = tid; idx < NE; idx += k64Threads) {

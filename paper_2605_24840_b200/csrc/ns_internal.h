@@ -17,6 +17,7 @@ constexpr int kStageBytes = kSPS * 2 * kTile * kBK * 8;   // A + B per stage = 6
 constexpr int kEpiPitch = kTile + 1;                  // staging row pitch (doubles), odd => conflict-free columns
 constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 // 64x64-tile variant (small / batched problems): 4 DMMA warps, 3 stages of 32 KB, 2 CTAs per SM
+constexpr int kMaxFilterDeg = 4;   // general odd filters: degree <= 2*4+1 = 9 (ns_options_t.filter_c)
 constexpr int k64Tile = 64;
 constexpr int k64Threads = 128;
 #ifndef NS_K64_STAGES
@@ -116,6 +117,7 @@ struct ProdParams {
   int mode;                // 0 = square/plain product + residual, 1 = NS update + trace
   double ca = 1.5;         // mode 1: X_{j+1} = ca X_j + cb X_j Y_j  (odd cubic filter step; NS: 1.5, -0.5)
   double cb = -0.5;
+  double cc = 0.0;         // mode 1: + cc I (Horner steps of a general odd polynomial filter, ns_api.cu run_filter)
   // Peer-memory exchange (sharded path, modes 0/1): the epilogue also stores its tile, mirror and partial
   // into n_dst destination buffers (device arrays of base pointers, e.g. every rank's Y through CUDA IPC
   // peer mappings over NVLink); partial slots use the global tile index gt_off + blockIdx.x * gt_stride
@@ -271,6 +273,7 @@ struct OzParams {
   int mode;                // 0 square (+res, mirror), 1 update (+trace, mirror), 2 dense
   double ca = 1.5;
   double cb = -0.5;
+  double cc = 0.0;         // mode 1: + cc I on the diagonal (general odd polynomial filters)
   int kb0 = 0;             // first k-block of this launch (K segments, see launch_ozaki_product)
   int pm = 0;              // 0 whole K; K segments: 1 first (C = raw sums), 2 middle (C += raw), 3 last (C + raw -> epilogue)
   int dbg = 0;             // experiments only (NS_OZ_DBG): 1 = stream operands without issuing the UMMAs

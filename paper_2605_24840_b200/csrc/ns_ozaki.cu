@@ -378,7 +378,10 @@ __global__ void __launch_bounds__(kOzThreads, 1)
           if (MODE != 2 && gj >= gi && fin) {   // element owned by this tile (written with its mirror)
             if (MODE == 1) {
               v = fma(p.cb, v, p.ca * xbuf[u]);
-              if (gi == gj && gi < p.d) part += v;
+              if (gi == gj && gi < p.d) {
+                v += p.cc;
+                part += v;
+              }
             } else {
               if (gj > gi) part += 2.0 * v * v;
               else {

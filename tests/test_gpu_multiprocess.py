@@ -7,7 +7,8 @@ storing their tiles and partials straight into the peers' buffers, the receivers
 block-row init storing X_0 panels into every rank.  Each barrier is a stream synchronisation plus the host
 exchange, so no kernel ever waits on another process's kernel (B200_PROFILING.md: ranks whose kernels wait
 on one another must not share a GPU).  Checked: every rank's R (full entry) or row panel (rows entry) and
-result record bitwise equal to the single-GPU ns_reflector; a workspace that moves on one rank only between
+result record bitwise equal to the same P-rank algorithm emulated in one process, within 1e-13 of the
+single-GPU ns_reflector and within 1e-10 of the oracle; a workspace that moves on one rank only between
 calls (the mapping check is collective); the NCCL-free fallback protocol (NS_SHARD_P2P=0: pack, host
 all-gather, unpack) on the same inputs; both mirror modes.
 """

@@ -532,6 +532,60 @@ def test_fixed_depth_filters(nsr, d, coef):
         assert checks.frob_per_sqrt_d(R.cpu().numpy(), Xcf) <= 1e-13
 
 
+QUINTIC = (15.0 / 8.0, -10.0 / 8.0, 3.0 / 8.0)
+
+
+@pytest.mark.parametrize("prec_name", ["NS_PREC_FP64", "NS_PREC_FP64_OZAKI"])
+@pytest.mark.parametrize("d,coeffs", [(64, QUINTIC), (300, QUINTIC), (1000, QUINTIC),
+                                      (300, (1.3, -0.2, -0.15, 0.05)), (200, (1.1, 0.2, -0.25, 0.1, -0.05)),
+                                      (515, (1.4, -0.3, -0.2, 0.1, 0.0))])
+def test_general_odd_filters_fixed_depth(nsr, prec_name, d, coeffs):
+    """General odd polynomial filters X <- sum_i c_i X^(2i+1) (N3; eq:signpreserving P:278-289, degree 5, 7, 9)
+    at fixed depth m (tol = 0): the device's Horner-in-X^2 evaluation against the oracle's plain odd
+    powers and the closed form Q diag(phi^m(mu)) Q^T (thm:generic proof)."""
+    from oracle import setup
+    prec = getattr(nsr, prec_name)
+    p = workloads.cfg0_controlled(seed=5, d=d, k=max(1, d // 20))
+    Hg = torch.from_numpy(p.H).to(_dev())
+    opts = nsr.ns_options(filter_a=coeffs[0], filter_b=coeffs[1], filter_c=list(coeffs[2:]))
+    mu = (p.lam - p.s) / p.alpha
+    for m in (1, 2, 4):
+        R, res = nsr.ns_reflector(Hg, p.s, p.alpha, p.k, m, 0.0, prec=prec, options=opts)
+        assert res["steps"] == m and res["flags"] & ons.MAX_STEPS
+        Rn = R.cpu().numpy()
+        assert np.array_equal(Rn, Rn.T)
+        Xo = setup.poly_filter_fixed_depth(p.H, p.s, p.alpha, m, coeffs)
+        tol = 1e-13 if prec == nsr.NS_PREC_FP64 else 1e-12     # Ozaki: 28 digit pairs, ~3e-15 per product
+        assert checks.frob_per_sqrt_d(Rn, Xo) <= tol, m
+        Xcf = closed_form.spectral_matrix(p.Q, setup.poly_filter_scalar(mu, m, coeffs))
+        assert checks.frob_per_sqrt_d(Rn, Xcf) <= tol, m
+        assert abs(res["trace"] - float(np.trace(Xo))) <= 1e-10 * d
+
+
+@pytest.mark.parametrize("prec_name", ["NS_PREC_FP64", "NS_PREC_FP64_OZAKI"])
+def test_quintic_filter_run_to_tolerance(nsr, prec_name):
+    """The quintic sign filter (15t - 10t^3 + 3t^5)/8 run to ||X^2 - I||_F/sqrt(d) < 1e-10 on the configs[3]
+    recipe (d = 1024): the step count equals the eigenvalue-wise replay of the same loop (check before update,
+    readings C2/C3) on the closed-form spectrum, fewer steps than Newton-Schulz (cubic vs quadratic
+    convergence), certificate k, R within 1e-10 of the exact reflector."""
+    from oracle import setup
+    prec = getattr(nsr, prec_name)
+    p = workloads.cfg3_dense(d=1024, k=64)
+    mu = (p.lam - p.s) / p.alpha
+    x, j = mu.copy(), 0
+    while math.sqrt(float(np.sum((x * x - 1.0) ** 2))) / math.sqrt(p.d) >= 1e-10:
+        x = setup.poly_filter_scalar(x, 1, QUINTIC)
+        j += 1
+    opts = nsr.ns_options(filter_a=QUINTIC[0], filter_b=QUINTIC[1], filter_c=[QUINTIC[2]])
+    Hg = torch.from_numpy(p.H).to(_dev())
+    R, res = nsr.ns_reflector(Hg, p.s, p.alpha, p.k, 100, 1e-10, 1, prec=prec, options=opts)
+    steps_ns = scalar.predict_run(mu, 100, 1e-10, True)[0]
+    assert res["steps"] == j < steps_ns and res["flags"] == ons.CONVERGED and res["cert"] == p.k
+    cols = np.arange(0, 1024, 41)
+    Rc = closed_form.householder_reflector_columns(p.Vh, p.lam, 0.0, cols)
+    assert np.max(np.abs(R.cpu().numpy()[:, cols] - Rc)) <= 1e-12
+
+
 def test_raw_sign_shift_zero(nsr):
     """prop:raw: s = 0 gives sgn(H); cfg0's spectrum has 0 inside the target gap."""
     p = workloads.cfg0_controlled(seed=2)

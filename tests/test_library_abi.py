@@ -60,7 +60,7 @@ def test_argument_validation(lib):
 
     assert call(d=0) == 1
     assert call(ldh=10) == 1
-    assert call(alpha=0.0) == 1
+    assert call(alpha=-1.0) == 1                 # (alpha = 0 selects the device Gershgorin bound)
     assert call(alpha=float("nan")) == 1
     assert call(s=float("inf")) == 1
     assert call(k=-1) == 1 and call(k=65) == 1
