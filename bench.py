@@ -61,6 +61,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="force the sharded rows entry also at N = 1 (N > 1 always runs it unless --replicas)")
+    ap.add_argument("--per-config", action="store_true",
+                    help="with --impl reference: time the CPU oracle on every BASELINE config (one JSON line each; "
+                         "cfg0/cfg1/cfg2 NS in full, cfg3 one step extrapolated, cfg4 extrapolated and flagged, "
+                         "Jacobi and closed-form verification timed separately)")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: one independent reflector per rank (weak scaling) instead of one sharded reflector")
     return ap.parse_args()
@@ -142,10 +146,85 @@ def dist_setup():
 
 
 # ---------------------------------------------------------------------------------- reference arm
+def _oracle_cfg1_worker(args):
+    from oracle import ns as ons
+    H, s, alpha, k = args
+    return ons.ns_reflector(H, s, alpha, k, 100, 1e-12, ons.TOL_ABS)["steps"]
+
+
+def run_reference_per_config(args):
+    """The CPU oracle (numpy/OpenBLAS FP64 products: a "library CPU" number; plain-C cyclic Jacobi) timed on
+    every BASELINE config on this host, one JSON line each -- reported next to the GPU numbers, not targeted."""
+    import multiprocessing as mp
+    from oracle import closed_form, jacobi, ns as ons
+    import workloads
+    cpu = _cpu_model()
+    threads = int(os.environ.get("OPENBLAS_NUM_THREADS", os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)))
+
+    def emit(rec):
+        rec.update({"impl": "reference", "kind": "oracle (numpy/OpenBLAS FP64 products; library CPU)", "cpu": cpu})
+        print(json.dumps(rec), flush=True)
+
+    # configs[0]: 5 seeds, full NS run each
+    ts = []
+    for seed in range(5):
+        p = workloads.cfg0_controlled(seed)
+        t0 = time.perf_counter()
+        o = ons.ns_reflector(p.H, p.s, p.alpha, p.k, 100, 1e-12, 0)
+        ts.append(time.perf_counter() - t0)
+    emit({"config": "cfg0", "what": "NS run to 1e-12, 5 seeds", "ms_median": 1e3 * float(np.median(ts)),
+          "steps": o["steps"], "cores": threads})
+    # configs[1]: all 6144 problems, one process per core (single-threaded BLAS each)
+    probs = workloads.cfg1_batched(seed=0, n_matrices=2048)
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(os.cpu_count()) as pool:
+        steps = pool.map(_oracle_cfg1_worker, [(q.H, q.s, q.alpha, q.k) for q in probs], chunksize=16)
+    t1 = time.perf_counter() - t0
+    emit({"config": "cfg1", "what": "NS on all 6144 problems (process pool)", "seconds": t1,
+          "reflectors_per_s": len(probs) / t1, "steps_total": int(sum(steps)), "cores": os.cpu_count(),
+          "tflops": float(np.sum(2 * np.array(steps) + 1)) * 256.0 ** 3 / t1 / 1e12})
+    del os.environ["OPENBLAS_NUM_THREADS"]
+    t0 = time.perf_counter()
+    for q in probs[:24:3]:
+        jacobi.jacobi_eigh(q.H)
+    tj = (time.perf_counter() - t0) / 8
+    emit({"config": "cfg1", "what": "cyclic Jacobi (plain C, OpenMP) per d=256 matrix, 8 sampled; x2048 extrapolated",
+          "seconds_per_matrix": tj, "seconds_2048_extrapolated": 2048 * tj, "extrapolated": True, "cores": threads})
+    # configs[2]: seed 0 NS in full (s, alpha from the oracle's Jacobi, tests/golden)
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "cfg2_seed0.json")))
+    prob = workloads.cfg2_allen_cahn(seed=0, s=g["s"])
+    t0 = time.perf_counter()
+    o = ons.ns_reflector(prob.H, g["s"], g["alpha"], 5, 100, 1e-12, 0)
+    t2 = time.perf_counter() - t0
+    emit({"config": "cfg2", "what": "NS run, seed 0 (d=4096)", "seconds": t2, "steps": o["steps"], "cores": threads,
+          "tflops": (2 * o["steps"] + 1) * 4096.0 ** 3 / t2 / 1e12})
+    emit({"config": "cfg2", "what": "cyclic Jacobi d=4096 (the shift's source), recorded by tools/make_golden_cfg2.py",
+          "seconds": g["seconds"]["jacobi"], "threads": g.get("threads"), "recorded_not_rerun": True,
+          "where": "the build container's CPU (not this host)"})
+    # configs[3]: one NS step, extrapolated to the 12-step run and the 30-step fixed run
+    p = workloads.cfg3_dense(form=False)
+    H = workloads.householder_form_fast(p.Vh, p.lam)
+    t, thr = ons.timed_ns_steps(H, p.s, p.alpha, 1)
+    emit({"config": "cfg3", "what": "one NS step (2 products + update), d=16384", "seconds": t, "cores": thr,
+          "tflops": 2.0 * 16384.0 ** 3 / t / 1e12, "seconds_run_to_tol_extrapolated": 12.5 * t,
+          "seconds_fixed30_extrapolated": 30.5 * t, "extrapolated": True})
+    t0 = time.perf_counter()
+    closed_form.householder_reflector_columns(p.Vh, p.lam, 0.0, np.arange(0, 16384, 256))
+    emit({"config": "cfg3", "what": "closed-form verification: 64 columns of Q sgn(Lambda) Q^T (64 Householders)",
+          "seconds": time.perf_counter() - t0, "cores": threads})
+    # configs[4]: extrapolated (d ratio 3: 27x per product; 29 products vs 25)
+    emit({"config": "cfg4", "what": "NS run d=49152, extrapolated from the cfg3 step: 27 x per product, 29 products",
+          "seconds_extrapolated": 27.0 * 14.5 * t, "extrapolated": True, "cores": thr})
+    return 0
+
+
 def run_reference(args):
     ws, rank, _ = dist_setup()
     if rank != 0:
         return 0  # the oracle runs on rank 0's host cores only
+    if args.per_config:
+        return run_reference_per_config(args)
     from oracle import ns as ons
     import workloads
     p, desc = workload(args)

@@ -417,7 +417,7 @@ ns_status_t check_common(int64_t d, int32_t max_steps, double tol, ns_tolmode_t 
 }
 
 struct Opts {
-  double switch_tol = 1e-4;
+  double switch_tol = 1e-3;   // reading C16b: 10x above the split-precision residual's noise floor
   int cg_iters = 512;             // cap; the solve stops at the relative residual cg_tol()
   int stop_at_switch = 0;
   int lookahead = 0;
@@ -1964,7 +1964,7 @@ size_t ns_workspace_bytes_ex(int64_t d, ns_precision_t prec, const ns_options_t*
 void ns_options_default(ns_options_t* o) {
   if (!o) return;
   *o = ns_options_t{};
-  o->switch_tol = 1e-4;
+  o->switch_tol = 1e-3;
   o->cg_iters = 512;
   o->stop_at_switch = 0;
   o->lookahead = 0;

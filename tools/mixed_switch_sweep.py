@@ -40,9 +40,10 @@ def problem(seed):
 
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 40
+    first = int(sys.argv[2]) if len(sys.argv) > 2 else 0
     dev = torch.device("cuda:0")
     nsr.load_library()
-    for seed in range(n):
+    for seed in range(first, first + n):
         H, s, alpha, k = problem(seed)
         d = H.shape[0]
         thr = 1e-10 * math.sqrt(d)
@@ -57,7 +58,11 @@ def main():
                                   dsteps=r["steps"] - o["steps"], switch=r["switch_step"],
                                   margin_dec=h[o["steps"]] / thr, margin_prev=h[o["steps"] - 1] / thr,
                                   r_switch_oracle=(h[r["switch_step"]] / math.sqrt(d)) if 0 <= r["switch_step"] < len(h)
-                                  else None, err=err, cert_ok=r["cert"] == k)), flush=True)
+                                  else None, err=err, cert_ok=r["cert"] == k,
+                                  res_ratio=(r["residual"] / o["residual"]) if r["steps"] == o["steps"] else None,
+                                  res_ratio_prev=None)), flush=True)
+    if os.environ.get("NO_CFG3"):
+        return
     # configs[3] timing per tau
     p = workloads.cfg3_dense(form=False)
     Hc = workloads.householder_form_fast(p.Vh, p.lam, device=dev)
