@@ -464,6 +464,10 @@ const char* ns_build_info(void);
  * 12 x CTAs entries; NULL turns the stamps off (default).
  */
 void ns_debug_mx_trace(void* device_buffer);
+/* Diagnostics (builds with -DNS_SMALL_TRACE=1; else returns 0): the fused small-d kernel's clock64 stamps
+ * of its last launch (block 0): [0] start, [1] X_0 formed, [2 + p] after product p, [100] loop end,
+ * [128 + w] warp w's DMMA loop end in product 0.  Copies n <= 256 values to host memory and clears them. */
+int ns_debug_small_trace(unsigned long long* out, int n);
 const char* ns_status_string(ns_status_t st);
 /* Thread-local message for the last non-NS_OK status on this thread ("" if none). */
 const char* ns_last_error(void);

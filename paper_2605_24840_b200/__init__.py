@@ -278,31 +278,41 @@ def ns_options(**kw):
 def ns_reflector(H, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_ABS, prec=NS_PREC_FP64, R=None, ws=None,
                  stream=None, options=None):
     """R = sgn(H - sI) by Newton–Schulz on the GPU (C-ABI ns_reflector / ns_reflector_ex when options
-    are given).  Returns (R, result dict)."""
+    are given).  Returns (R, result dict).  (Written for the small-d latency path: device checks on integer
+    indices, the raw stream handle, no context object unless a device switch is needed.)"""
     torch = _torch()
-    lib = load_library()
-    _require_cuda_f64(H, "H")
+    lib = _lib if _lib is not None else load_library()
+    dev = H.get_device() if isinstance(H, torch.Tensor) else -1
+    if dev < 0 or H.dtype != torch.float64:
+        raise NsError("H must be a CUDA float64 tensor (no CPU fallback)")
     d = H.shape[0]
     if H.dim() != 2 or H.shape[1] != d or H.stride(1) != 1:
         raise NsError("H must be a square row-major (stride(1)==1) matrix")
     if R is None:
         R = torch.empty((d, d), dtype=torch.float64, device=H.device)
-    _require_cuda_f64(R, "R")
+    elif not isinstance(R, torch.Tensor) or R.get_device() != dev or R.dtype != torch.float64:
+        raise NsError("R must be a CUDA float64 tensor on H's device")
     if ws is None:   # (the library checks a given size)
         nb = lib.ns_workspace_bytes_ex(d, prec, ctypes.byref(options)) if options is not None else \
             lib.ns_workspace_bytes(d, prec)
         ws = alloc_workspace(nb, H.device)
+    elif ws.get_device() != dev:
+        raise NsError("the workspace must be on H's device")
     res = NsResult()
+    if stream is not None:
+        sp = ctypes.c_void_p(stream.cuda_stream)
+    else:
+        sp = _stream_ptr(None, H.device)
     args = (ctypes.c_void_p(H.data_ptr()), d, H.stride(0), float(s), float(alpha), int(k), int(max_steps), float(tol),
             int(tol_mode), int(prec), ctypes.c_void_p(R.data_ptr()), R.stride(0), ctypes.c_void_p(ws.data_ptr()),
-            ws.numel(), _stream_ptr(stream, H.device))
-    _same_device(H, R, ws)
-    with _on(H.device):
+            ws.numel(), sp)
+    with (_NULL if dev == torch._C._cuda_getDevice() else torch.cuda.device(dev)):
         if options is None:
             st = lib.ns_reflector(*args, ctypes.byref(res))
         else:
             st = lib.ns_reflector_ex(*args, ctypes.byref(options), ctypes.byref(res))
-    _check(st)
+    if st != NS_OK:
+        _check(st)
     return R, res.as_dict()
 
 

@@ -2321,6 +2321,8 @@ ns_status_t ns_shift_bisect(const double* H, int64_t d, int64_t ldh, int32_t k, 
   return NS_OK;
 }
 
+int ns_debug_small_trace(unsigned long long* out, int n) { return small_trace_read(out, n); }
+
 void ns_debug_mx_trace(void* device_buffer) { g_mx_trace = static_cast<unsigned long long*>(device_buffer); }
 
 ns_status_t ns_symm_product(const double* A, const double* B, double* C, int64_t d, int64_t ld, int32_t mode,

@@ -213,6 +213,7 @@ cudaError_t launch_decide(DevState* state, const JobParams* jobs, const double* 
 
 // ---------------- small-d fused path (ns_small.cu): d <= 96, whole loop in one CTA per problem ----------------
 int small_dpad(int d);
+int small_trace_read(unsigned long long* out, int n);   // NS_SMALL_TRACE diagnostics
 cudaError_t launch_small(const double* H, long long ldh, long long h_stride, const JobParams* jobs, JobParams job0,
                          LoopParams lp, double* R, long long ldr, long long r_stride, DevState* state, int batch,
                          cudaStream_t st);

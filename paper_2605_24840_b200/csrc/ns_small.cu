@@ -17,7 +17,26 @@
 #include "ns_ptx.cuh"
 #include "ns_small.cuh"
 
+#ifndef NS_SMALL_SQ_MODE1
+#define NS_SMALL_SQ_MODE1 0   // experiment: the square through the update's epilogue code (timing only)
+#endif
+#ifndef NS_SMALL_SQ_COPY
+#define NS_SMALL_SQ_COPY 0   // experiment (tools/small_trace.py): the square reads its B operand from a copy of X
+#endif
+#ifndef NS_SMALL_TRACE
+#define NS_SMALL_TRACE 0   // 1: thread 0 records %globaltimer at phase boundaries (tools/small_trace.py)
+#endif
+
 namespace nsr {
+
+#if NS_SMALL_TRACE
+__device__ unsigned long long g_small_trace[256];   // [0] start, [1] init done, [2 + p] after product p (clock64);
+                                                    // [128 + w], [160 + w]: warp w's DMMA loop end in
+                                                    // products 0, 1; [250]: product counter
+#define NS_STRACE(i) do { if (threadIdx.x == 0 && blockIdx.x == 0) g_small_trace[(i)] = clock64(); } while (0)
+#else
+#define NS_STRACE(i) do { } while (0)
+#endif
 
 // one warp per work unit (a pair of upper fragments sharing their A rows, see small_ns_product):
 // 6 / 20 / 42 units for d_pad 32 / 64 / 96 (d_pad 96: 14 warps x 3 units, within the register file)
@@ -148,6 +167,9 @@ __device__ __forceinline__ double small_ns_product(const double* __restrict__ A,
         }
       }
     }
+#if NS_SMALL_TRACE
+    if (lane == 0 && blockIdx.x == 0 && g_small_trace[250] < 2) g_small_trace[128 + 32 * (int)g_small_trace[250] + warp] = clock64();
+#endif
 #pragma unroll
     for (int f = 0; f < 2; ++f) {
       if (f == 1 && !two) continue;
@@ -156,31 +178,6 @@ __device__ __forceinline__ double small_ns_product(const double* __restrict__ A,
     }
   }
   return acc;
-}
-
-// Sum of (a, b) over the CTA; one barrier (callers separate consecutive uses by another barrier).
-// The per-warp partials are summed by every warp with the same shuffle tree, so all threads hold
-// identical bits (one LDS per lane instead of NW per thread).
-template <int NW>
-__device__ __forceinline__ void block_sum2(double& a, double& b, double (*red)[2]) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    a += __shfl_xor_sync(0xffffffffu, a, o);
-    b += __shfl_xor_sync(0xffffffffu, b, o);
-  }
-  const int lane = threadIdx.x & 31;
-  if (lane == 0) {
-    red[threadIdx.x >> 5][0] = a;
-    red[threadIdx.x >> 5][1] = b;
-  }
-  __syncthreads();
-  a = lane < NW ? red[lane][0] : 0.0;
-  b = lane < NW ? red[lane][1] : 0.0;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    a += __shfl_xor_sync(0xffffffffu, a, o);
-    b += __shfl_xor_sync(0xffffffffu, b, o);
-  }
 }
 
 template <int DP>
@@ -195,74 +192,159 @@ __global__ void __launch_bounds__(small_threads<DP>(), 1)
   double* Xn = sm + DP * P;        // X_{j+1}
   double* Y = sm + 2 * DP * P;     // Y_j = X_j^2
   __shared__ double red[NT / 32][2];
+  __shared__ double dec_r, dec_tr;            // warp 0's stop decision of the current step
+  __shared__ int dec_flags, dec_stop;
   __shared__ int2 units[small_units<DP>()];
+  NS_STRACE(0);
   small_fill_units<DP>(units);             // visible after the first barrier below
   const int job = blockIdx.x;
   const double* Hj = H + (long long)job * h_stride;
   const JobParams jp = jobs ? jobs[job] : job0;   // batch of one: parameters by value (no H2D copy)
   const double s = jp.s, alpha = jp.alpha;
   const int d = lp.d;
-  // X_0 = (H - sI)/alpha from the upper triangle, zero padded; tr X_0 partials
+  // X_0 = (H - sI)/alpha from the upper triangle, zero padded; tr X_0 partials.  Two passes, no integer
+  // division: (1) warp w reads rows w, w + NW, ... of H's upper triangle (coalesced, every load of the
+  // thread issued before the first use) into a pitch-(DP+1) staging copy in Y's buffer (free until the
+  // first square); (2) element (i, j) takes staging[min][max] -- the transposed reads for j < i run down a
+  // column of an odd-pitch array, conflict-free -- and is divided and stored row-wise into X.  (A flat-index
+  // loop with per-element divisions and strided global reads of the lower half spent ~6400 cycles here.)
   double tpart = 0.0;
-  for (int e = threadIdx.x; e < DP * DP; e += NT) X[(e / DP) * P + e % DP] = 0.0;   // padding
-  __syncthreads();
-  // row-major (coalesced) reads, 8 independent loads in flight per thread (the loop is otherwise a chain
-  // of global-memory latencies: ~9 us of a 48 us configs[0] kernel); the upper triangle is kept
-  for (int e0 = threadIdx.x; e0 < d * d; e0 += 8 * NT) {
-    double h[8];
+  {
+    constexpr int NW = NT / 32, RPW = (DP + NW - 1) / NW, CPL = DP / 32, SP = DP + 1;
+    double* Sg = Y;                        // staging, DP x SP <= DP x P
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    double v[RPW][CPL];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int e = e0 + q * NT;
-      h[q] = (e < d * d) ? Hj[(long long)(e / d) * ldh + e % d] : 0.0;
-    }
+    for (int q = 0; q < RPW; ++q)
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int e = e0 + q * NT;
-      const int i = e / d, j = e % d;
-      if (e >= d * d || i > j) continue;
-      const double v = (i == j) ? (h[q] - s) / alpha : h[q] / alpha;
-      if (i == j) tpart += v;
-      X[i * P + j] = v;
-      X[j * P + i] = v;
-    }
+      for (int c = 0; c < CPL; ++c) {
+        const int i = w + q * NW, jj = ln + 32 * c;
+        v[q][c] = (i < d && jj < d && jj >= i) ? Hj[(long long)i * ldh + jj] : 0.0;
+      }
+#pragma unroll
+    for (int q = 0; q < RPW; ++q)
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int i = w + q * NW, jj = ln + 32 * c;
+        if (i < DP) Sg[i * SP + jj] = v[q][c];
+      }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < RPW; ++q)
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int i = w + q * NW, jj = ln + 32 * c;
+        if (i >= DP) continue;
+        double x = 0.0;
+        if (i < d && jj < d) {
+          const double h = (jj >= i) ? Sg[i * SP + jj] : Sg[jj * SP + i];
+          x = (i == jj) ? (h - s) / alpha : h / alpha;
+          if (i == jj) tpart += x;
+        }
+        X[i * P + jj] = x;
+      }
   }
   __syncthreads();
+  NS_STRACE(1);
   const double sqd = sqrt((double)d);
   int j = 0, flags = 0;
   double r = 0.0, r_prev = 0.0, tr = 0.0;
   while (true) {
+#if NS_SMALL_SQ_COPY
+    // experiment: the square's B operand from a copy of X in Xn's (free) buffer instead of X itself
+    for (int e = threadIdx.x; e < DP * P; e += NT) Xn[e] = X[e];
+    __syncthreads();
+    NS_STRACE(200 + j);
+    double part = small_ns_product<DP, 0>(X, Xn, Y, d, 0.0, 0.0, units);
+#elif NS_SMALL_SQ_MODE1
+    // experiment: the square through the update's code path (epilogue ca = 0, cb = 1; no residual)
+    double part = small_ns_product<DP, 1>(X, X, Y, d, 0.0, 1.0, units);
+    part = 1.0;
+#else
     double part = small_ns_product<DP, 0>(X, X, Y, d, 0.0, 0.0, units);   // Y_j = X_j^2, ||Y_j - I||_F^2 share
-    block_sum2<NT / 32>(part, tpart, red);                          // barrier: Y_j complete
-    r = sqrt(part);
-    tr = tpart;
-    if (!isfinite(r)) {
-      flags |= 16;
-      break;
+#endif
+    // Stop rule (ns_decide_kernel's) evaluated once, by warp 0, instead of redundantly by every thread: the
+    // square root, the division and the comparisons in all 20 warps cost ~1000 cycles of FP64 issue per step
+    // (tools/small_trace.py).  Warp partials -> barrier (Y_j complete) -> warp 0 reduces in a fixed order and
+    // decides -> barrier -> everyone reads the decision.
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      part += __shfl_xor_sync(0xffffffffu, part, o);
+      tpart += __shfl_xor_sync(0xffffffffu, tpart, o);
     }
-    if (j > 0 && r > r_prev * (1.0 + 1e-12) + 1e-10 * sqd) flags |= 8;
-    const double rho = lp.tol_mode ? r / sqd : r;
-    if (rho < lp.tol) {
-      flags |= 1;
-      break;
+    if ((threadIdx.x & 31) == 0) {
+      red[threadIdx.x >> 5][0] = part;
+      red[threadIdx.x >> 5][1] = tpart;
     }
-    if (j >= lp.max_steps) {
-      flags |= 2;
-      break;
+    __syncthreads();                                                // Y_j complete, partials in red
+    NS_STRACE(2 + 2 * j);
+#if NS_SMALL_TRACE
+    if (threadIdx.x == 0 && blockIdx.x == 0 && g_small_trace[250] == 0) g_small_trace[250] = 1;   // stamps: products 0, 1
+#endif
+    if (threadIdx.x < 32) {
+      double a = threadIdx.x < NT / 32 ? red[threadIdx.x][0] : 0.0;
+      double b = threadIdx.x < NT / 32 ? red[threadIdx.x][1] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+      }
+      if (threadIdx.x == 0) {
+        const double rr = sqrt(a);
+        int fl = flags, stop = 0;
+        if (!isfinite(rr)) {
+          fl |= 16;
+          stop = 1;
+        } else {
+          if (j > 0 && rr > r_prev * (1.0 + 1e-12) + 1e-10 * sqd) fl |= 8;
+          const double rho = lp.tol_mode ? rr / sqd : rr;
+          if (rho < lp.tol) {
+            fl |= 1;
+            stop = 1;
+          } else if (j >= lp.max_steps) {
+            fl |= 2;
+            stop = 1;
+          }
+        }
+        dec_r = rr;
+        dec_tr = b;
+        dec_flags = fl;
+        dec_stop = stop;
+      }
     }
-    tpart = small_ns_product<DP, 1>(X, Y, Xn, d, lp.ca, lp.cb, units);      // X_{j+1} = ca X_j + cb X_j Y_j
-    __syncthreads();                                                 // X_{j+1} complete
+    // The update runs speculatively while warp 0 takes the decision (its sequential square root, division and
+    // comparisons, ~1500 cycles, hide behind the other warps' DMMAs; warp 0 holds a single-fragment unit).
+    // If the decision was to stop, X_j is returned and the extra X_{j+1} in Xn is simply not used.
+    const double tpart_n = small_ns_product<DP, 1>(X, Y, Xn, d, lp.ca, lp.cb, units);   // ca X_j + cb X_j Y_j
+    __syncthreads();                                                 // X_{j+1} complete, decision visible
+    NS_STRACE(3 + 2 * j);
+#if NS_SMALL_TRACE
+    if (threadIdx.x == 0 && blockIdx.x == 0 && g_small_trace[250] == 1) g_small_trace[250] = 2;
+#endif
+    r = dec_r;
+    tr = dec_tr;
+    flags = dec_flags;
+    if (dec_stop) break;
+    tpart = tpart_n;
     double* tmp = X;
     X = Xn;
     Xn = tmp;
     r_prev = r;
     ++j;
   }
-  // R = X_j
+  // R = X_j (warp w: rows w, w + NW, ...; coalesced row stores, no integer division)
   double* Rj = R + (long long)job * r_stride;
-  for (int e = threadIdx.x; e < d * d; e += NT) {
-    const int i = e / d, c = e % d;
-    Rj[(long long)i * ldr + c] = X[i * P + c];
+  {
+    constexpr int NW = NT / 32;
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    for (int i = w; i < d; i += NW)
+#pragma unroll
+      for (int c = 0; c < DP / 32; ++c) {
+        const int jj = ln + 32 * c;
+        if (jj < d) Rj[(long long)i * ldr + jj] = X[i * P + jj];
+      }
   }
+  NS_STRACE(100);
   if (threadIdx.x == 0) {
     DevState st{};
     st.j = j;
@@ -283,6 +365,20 @@ __global__ void __launch_bounds__(small_threads<DP>(), 1)
     st.flags = flags;
     state[job] = st;
   }
+}
+
+// Diagnostics (NS_SMALL_TRACE builds): copy the phase stamps of the last traced launch to the host and clear them.
+int small_trace_read(unsigned long long* out, int n) {
+#if NS_SMALL_TRACE
+  if (cudaMemcpyFromSymbol(out, g_small_trace, sizeof(unsigned long long) * (n < 256 ? n : 256)) != cudaSuccess) return -1;
+  static const unsigned long long zero[256] = {};
+  cudaMemcpyToSymbol(g_small_trace, zero, sizeof(zero));
+  return n < 256 ? n : 256;
+#else
+  (void)out;
+  (void)n;
+  return 0;
+#endif
 }
 
 int small_dpad(int d) { return d <= 32 ? 32 : d <= 64 ? 64 : d <= 96 ? 96 : 0; }

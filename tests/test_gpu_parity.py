@@ -1053,6 +1053,47 @@ def test_random_symm_products(nsr, seed):
         assert np.array_equal(C, C.T)
 
 
+@pytest.mark.parametrize("prec", [0, 3])
+def test_symm_product_strided_views(nsr, prec):
+    """ns_symm_product on strided views A = big[:d, :d] (ld > d): the default C gets A's leading dimension (no
+    write past its storage), an explicit C with that layout is filled in place (its padding untouched), and
+    a C with the wrong layout, dtype or device is rejected before any launch (advisor finding)."""
+    rng = np.random.default_rng(77)
+    d, D = 200, 264
+    big = torch.zeros((D, D), dtype=torch.float64, device=_dev())
+    A = rng.standard_normal((d, d))
+    A = 0.5 * (A + A.T)
+    big[:d, :d] = torch.from_numpy(A)
+    Av = big[:d, :d]
+    C = nsr.ns_symm_product(Av, Av, mode=0, prec=prec)
+    assert C.stride(0) == D and C.shape == (d, d)
+    ref = nsr.ns_symm_product(Av.contiguous(), Av.contiguous(), mode=0, prec=prec)
+    assert torch.equal(C, ref)
+    cbig = torch.full((D, D), 7.0, dtype=torch.float64, device=_dev())
+    nsr.ns_symm_product(Av, Av, mode=0, prec=prec, C=cbig[:d, :d])
+    assert torch.equal(cbig[:d, :d], ref)
+    assert torch.all(cbig[:, d:] == 7.0) and torch.all(cbig[d:, :] == 7.0)
+    with pytest.raises(nsr.NsError):
+        nsr.ns_symm_product(Av, Av, C=torch.empty((d, d), dtype=torch.float64, device=_dev()))   # ld d != D
+    with pytest.raises(nsr.NsError):
+        nsr.ns_symm_product(Av, Av, C=torch.empty((D, D), dtype=torch.float32, device=_dev())[:d, :d])
+    with pytest.raises(nsr.NsError):
+        nsr.ns_symm_product(Av, Av, C=torch.empty((D, D), dtype=torch.float64)[:d, :d])
+
+
+def test_scale_bound_propagates_nan(nsr):
+    """A NaN entry of H makes the Gershgorin bound NaN and the call fail (the max never drops a NaN row sum,
+    so a finite alpha is never a false upper bound of ||H - sI||_2); alpha = 0 in ns_reflector likewise."""
+    p = workloads.cfg0_controlled(seed=3, d=300, k=10)
+    H = p.H.copy()
+    H[17, 250] = H[250, 17] = np.nan
+    Hg = torch.from_numpy(H).to(_dev())
+    with pytest.raises(nsr.NsError, match="non-finite"):
+        nsr.ns_scale_bound(Hg, p.s)
+    with pytest.raises(nsr.NsError, match="non-finite"):
+        nsr.ns_reflector(Hg, p.s, 0.0, p.k, 100, 1e-12)
+
+
 @pytest.mark.parametrize("prec", [0, 1, 3])
 @pytest.mark.parametrize("d", [50, 300])
 def test_strided_inputs_and_outputs(nsr, prec, d):
