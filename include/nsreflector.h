@@ -468,6 +468,11 @@ void ns_debug_mx_trace(void* device_buffer);
  * of its last launch (block 0): [0] start, [1] X_0 formed, [2 + p] after product p, [100] loop end,
  * [128 + w] warp w's DMMA loop end in product 0.  Copies n <= 256 values to host memory and clears them. */
 int ns_debug_small_trace(unsigned long long* out, int n);
+/* Diagnostics (builds with -DNS_P64_TRACE=1; else returns -1): every CTA of the 64x64-tile FP64 product kernel
+ * appends a record of 10 uint64 (SM id | mode << 16 | diagonal << 17; %globaltimer at start, first stage landed,
+ * end; job << 32 | tile; K loop done in warps 0..3; 0) to `device_buffer` (1 + 10 x capacity uint64, element 0 = record counter,
+ * zeroed by the caller) -- tools/p64_trace.py.  NULL turns the records off. */
+int ns_debug_p64_trace(void* device_buffer, unsigned long long capacity);
 const char* ns_status_string(ns_status_t st);
 /* Thread-local message for the last non-NS_OK status on this thread ("" if none). */
 const char* ns_last_error(void);

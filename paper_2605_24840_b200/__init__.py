@@ -28,7 +28,7 @@ EXPORTED_SYMBOLS = (
     "ns_shift_certificate", "ns_workspace_bytes_alg1", "ns_alg1_rotated_quartic", "ns_debug_mx_trace",
     "ns_symm_product_shard", "ns_workspace_bytes_sharded_emulated", "ns_reflector_sharded_emulated",
     "ns_comm_init_host", "ns_shard_rows", "ns_reflector_sharded_rows", "ns_reflector_batched_dev",
-    "ns_workspace_bytes_inertia", "ns_inertia", "ns_shift_bisect", "ns_workspace_bytes_ex", "ns_debug_small_trace",
+    "ns_workspace_bytes_inertia", "ns_inertia", "ns_shift_bisect", "ns_workspace_bytes_ex", "ns_debug_small_trace", "ns_debug_p64_trace",
 )
 
 

@@ -2322,6 +2322,9 @@ ns_status_t ns_shift_bisect(const double* H, int64_t d, int64_t ldh, int32_t k, 
 }
 
 int ns_debug_small_trace(unsigned long long* out, int n) { return small_trace_read(out, n); }
+int ns_debug_p64_trace(void* device_buffer, unsigned long long capacity) {
+  return p64_trace_set(static_cast<unsigned long long*>(device_buffer), capacity);
+}
 
 void ns_debug_mx_trace(void* device_buffer) { g_mx_trace = static_cast<unsigned long long*>(device_buffer); }
 

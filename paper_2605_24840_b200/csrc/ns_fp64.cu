@@ -373,8 +373,25 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Same scheme as ns_product_kernel: TMA ring (box 16 x 64, 128-B swizzle), thread 0 refills, 4 DMMA
 // warps with 32x32 warp tiles and the k-permuted conflict-free LDS.128 fragments, staged epilogue.
 // --------------------------------------------------------------------------------------
+__device__ __forceinline__ void stg_v2(double* p, double x, double y) {
+  asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(x), "d"(y) : "memory");
+}
+#ifndef NS_P64_TRACE
+#define NS_P64_TRACE 0   // 1: every CTA of the 64-tile kernel records %globaltimer phase stamps (tools/p64_trace.py)
+#endif
+#if NS_P64_TRACE
+// g_p64_trace[0] = record counter; record r at 1 + 10 r: smid | mode << 16 | diag << 17, start, first stage
+// landed, end, job << 32 | tile, K loop done of warps 0..3, 0
+__device__ unsigned long long* g_p64_trace = nullptr;
+__device__ unsigned long long g_p64_cap = 0;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
 template <int MODE>
-__global__ void __launch_bounds__(k64Threads, k64Stages == 2 ? 3 : 2)
+__global__ void __launch_bounds__(k64Threads, k64MinBlocks)
     ns_product64_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmQ,
                         const ProdParams p) {
   int job = blockIdx.y;
@@ -382,11 +399,16 @@ __global__ void __launch_bounds__(k64Threads, k64Stages == 2 ? 3 : 2)
     if ((int)blockIdx.y >= *p.n_job_list) return;
     job = p.job_list[blockIdx.y];
   }
-  if (p.state != nullptr && p.state[job].done) return;
+  // the compacted list holds only running jobs (ns_compact_kernel after the last decide): no state read
+  else if (p.state != nullptr && p.state[job].done) return;
+#if NS_P64_TRACE
+  unsigned long long tr_t0 = gtimer(), tr_t1 = 0;
+  __shared__ unsigned long long tr_wend[k64Threads / 32];
+#endif
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  double* sA = reinterpret_cast<double*>(smem);                                      // [stages*kSPS][64*16]
-  double* sB = reinterpret_cast<double*>(smem + k64Stages * kSPS * k64Tile * kBK * 8);
+  double* sA = reinterpret_cast<double*>(smem);                                      // [stages*k64SPS][64*16]
+  double* sB = reinterpret_cast<double*>(smem + k64Stages * k64SPS * k64Tile * kBK * 8);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + k64Stages * k64StageBytes);
   uint64_t* empty = full + k64Stages;
   __shared__ double red[k64Threads / 32];
@@ -402,35 +424,40 @@ __global__ void __launch_bounds__(k64Threads, k64Stages == 2 ? 3 : 2)
     fence_mbar_init();
   }
   __syncthreads();
-  const int nst = p.nk / kSPS;
+  const int nst = p.nk / k64SPS;
   // MODE 1 walks K starting after the tile's own column block J (stage units 2J, 2J+1 of 32 columns
   // come last), so when the loop ends the ring still holds X_j[I rows][J columns] -- the tile the
   // update epilogue needs -- and no global re-read of X_j is required.
-  const int koff = (MODE == 1 || NS_K64_ROT0) ? (2 * J + 2) % nst : 0;
+  constexpr int kJS = 4 / k64SPS;         // stages per 64-column block
+  const int koff = (MODE == 1 || NS_K64_ROT0) ? (kJS * J + kJS) % nst : 0;
   auto issue = [&](int kt) {
     const int s = kt % k64Stages;
     const int kb = (kt + koff) % nst;
     mbar_arrive_expect_tx(&full[s], k64StageBytes);
 #pragma unroll
-    for (int u = 0; u < kSPS; ++u) {
-      tma_load_3d(sA + (s * kSPS + u) * k64Tile * kBK, &tmP, (kb * kSPS + u) * kBK, I * k64Tile, job, &full[s]);
-      tma_load_3d(sB + (s * kSPS + u) * k64Tile * kBK, &tmQ, (kb * kSPS + u) * kBK, J * k64Tile, job, &full[s]);
+    for (int u = 0; u < k64SPS; ++u) {
+      tma_load_3d(sA + (s * k64SPS + u) * k64Tile * kBK, &tmP, (kb * k64SPS + u) * kBK, I * k64Tile, job, &full[s]);
+      tma_load_3d(sB + (s * k64SPS + u) * k64Tile * kBK, &tmQ, (kb * k64SPS + u) * kBK, J * k64Tile, job, &full[s]);
     }
   };
-  // X_j(r, c..c+1) of this tile (c even) from the ring after the K loop: columns [0, 32) sit in the slot
-  // of stage nst-2, [32, 64) in that of nst-1; 128-B swizzle (16-B chunk q of row r at q ^ (r & 7))
+  // X_j(r, c..c+1) of this tile (c even) from the ring after the K loop: the block's 16-column slab q sits in
+  // the slot of stage nst - kJS + q / k64SPS; 128-B swizzle (16-B chunk of row r at chunk ^ (r & 7))
   auto x_ring = [&](int r, int c) -> double2 {
-    const int slot = (c < 32) ? (nst - 2) % k64Stages : (nst - 1) % k64Stages;
-    const int cs = c & 31;
-    const double* slab = sA + (slot * kSPS + (cs >> 4)) * (k64Tile * kBK);
-    return *reinterpret_cast<const double2*>(slab + r * kBK + ((((cs & 15) >> 1) ^ (r & 7)) << 1));
+    const int q = c >> 4;                        // 16-column slab of the block
+    const int slot = (nst - kJS + q / k64SPS) % k64Stages;
+    const int cs = c & 15;
+    const double* slab = sA + (slot * k64SPS + q % k64SPS) * (k64Tile * kBK);
+    return *reinterpret_cast<const double2*>(slab + r * kBK + (((cs >> 1) ^ (r & 7)) << 1));
   };
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmP);
     tma_prefetch_desc(&tmQ);
     for (int kt = 0; kt < k64Stages && kt < nst; ++kt) issue(kt);
   }
-  const int wm = warp >> 1, wn = warp & 1;   // warp tile rows wm*32, cols wn*32
+  constexpr int NWP = k64Threads / 32;        // DMMA warps per CTA: 4 (32x32 warp tiles) or 8 (32x16)
+  constexpr int WN = 64 / (NWP / 2);          // warp tile columns
+  constexpr int NI = WN / 8;                  // 8-column fragments per warp
+  const int wm = warp / (NWP / 2), wn = warp % (NWP / 2);   // warp tile rows wm*32, cols wn*WN
   const int g = lane >> 2, t = lane & 3;
   const uint32_t off_h0 = static_cast<uint32_t>(((2 * t + 0) ^ g) << 4);
   const uint32_t off_h1 = static_cast<uint32_t>(((2 * t + 1) ^ g) << 4);
@@ -446,8 +473,11 @@ __global__ void __launch_bounds__(k64Threads, k64Stages == 2 ? 3 : 2)
         issue(kt - 1 + k64Stages);
       }
       mbar_wait(&full[s], static_cast<uint32_t>(kt / k64Stages) & 1u);
+#if NS_P64_TRACE
+      if (kt == 0 && threadIdx.x == 0) tr_t1 = gtimer();
+#endif
       compute(s);
-      // the slot is refilled by TMA (async proxy) once every warp has arrived: order this warp's generic-
+      // the slot is refilled by TMA (async proxy) once every warp has released it: order this warp's generic-
       // proxy reads of it before the release (without the fence, 3 CTAs/SM with a 2-stage ring produced
       // nondeterministic results -- a refill overtaking the last LDS of the slot)
       fence_proxy_async();
@@ -455,26 +485,69 @@ __global__ void __launch_bounds__(k64Threads, k64Stages == 2 ? 3 : 2)
       if (lane == 0) mbar_arrive(&empty[s]);
     }
   };
-  constexpr int EP = k64Tile + 1;
-  double* S = reinterpret_cast<double*>(smem);   // [64][65] epilogue staging (reuses the ring)
+  // ---------------- epilogue straight from the accumulator registers ----------------
+  // Lane (g, t) of a fragment holds C[r][c], C[r][c+1] (r = 8-row base + g, c = 8-col base + 2t): one 16-byte
+  // store for the tile and, after one shuffle with lane g ^ 1, one 16-byte store for the mirror (even g takes
+  // row c: (r, r+1), odd g row c+1: (r-1, r)); every warp store covers 8 rows x 64 contiguous bytes.  No
+  // shared-memory staging and no block barrier before the stores (the staged epilogue -- fragments to a padded
+  // smem tile, then coalesced row and column passes -- took ~25% of a CTA's warp time in ncu; cfg1 118.3 ->
+  // 115.9 ms).  Diagonal 8x8 blocks keep c >= r and mirror it, so every stored matrix is bitwise symmetric.
+  const long long ld = p.ld;
+  const long long base = (long long)job * p.job_stride;
+  double* C = p.C + base;
+  const int i0 = I * k64Tile, j0 = J * k64Tile;
+  double part = 0.0;
+  const bool godd = (g & 1) != 0;
+  // off-diagonal 8x8 block (r in rows, c >= every r): tile store + mirror, MODE 0 residual weight 2
+  auto put_full = [&](int r, int c, double v0, double v1) {
+    stg_v2(C + (long long)(i0 + r) * ld + j0 + c, v0, v1);
+    const double send = godd ? v0 : v1;
+    const double recv = __shfl_xor_sync(0xffffffffu, send, 4);
+    if (godd) stg_v2(C + (long long)(j0 + c + 1) * ld + i0 + r - 1, recv, v1);
+    else stg_v2(C + (long long)(j0 + c) * ld + i0 + r, v0, recv);
+    if (MODE == 0) part += 2.0 * (v0 * v0 + v1 * v1);
+  };
+  // 8x8 block on the diagonal of a diagonal tile: elements c >= r (+ mirror), identity / trace / + cc I on c == r
+  auto put_diag = [&](int r, int c, double v0, double v1) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int cc = c + h;
+      double v = h ? v1 : v0;
+      if (cc < r) continue;
+      if (cc == r) {
+        const bool in = i0 + r < p.d;
+        if (MODE == 0) {
+          const double e = in ? v - 1.0 : v;
+          part += e * e;
+        } else if (in) {
+          v += p.cc;
+          part += v;
+        }
+      } else if (MODE == 0) {
+        part += 2.0 * v * v;
+      }
+      C[(long long)(i0 + r) * ld + i0 + cc] = v;
+      if (cc != r) C[(long long)(i0 + cc) * ld + i0 + r] = v;
+    }
+  };
   if (!diag || !p.diag_tri) {
     const uint32_t a_row = static_cast<uint32_t>((wm * 32 + g) * 128);
-    const uint32_t b_row = static_cast<uint32_t>((wn * 32 + g) * 128);
-    double acc[4][4][2];
+    const uint32_t b_row = static_cast<uint32_t>((wn * WN + g) * 128);
+    double acc[4][NI][2];
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+      for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
     mainloop([&](int s) {
 #pragma unroll
-      for (int hh = 0; hh < 2 * kSPS; ++hh) {
+      for (int hh = 0; hh < 2 * k64SPS; ++hh) {
         const int h = hh & 1;
-        const uint32_t aS = sA_u32 + (s * kSPS + (hh >> 1)) * (k64Tile * kBK * 8) + a_row;
-        const uint32_t bS = sB_u32 + (s * kSPS + (hh >> 1)) * (k64Tile * kBK * 8) + b_row;
+        const uint32_t aS = sA_u32 + (s * k64SPS + (hh >> 1)) * (k64Tile * kBK * 8) + a_row;
+        const uint32_t bS = sB_u32 + (s * k64SPS + (hh >> 1)) * (k64Tile * kBK * 8) + b_row;
         const uint32_t off = h ? off_h1 : off_h0;
-        double a[4][2], b[4][2];
+        double a[4][2], b[NI][2];
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) lds128(bS + ni * 8 * 128 + off, b[ni][0], b[ni][1]);
+        for (int ni = 0; ni < NI; ++ni) lds128(bS + ni * 8 * 128 + off, b[ni][0], b[ni][1]);
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) lds128(aS + mi * 8 * 128 + off, a[mi][0], a[mi][1]);
 #pragma unroll
@@ -482,53 +555,61 @@ __global__ void __launch_bounds__(k64Threads, k64Stages == 2 ? 3 : 2)
 #pragma unroll
           for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi][e], b[ni][e]);
+            for (int ni = 0; ni < NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi][e], b[ni][e]);
       }
     });
-    if (MODE == 1) {   // X_{j+1} = ca X_j + cb Z in registers, X_j from the ring (read before S reuses it)
+    if (MODE == 1) {   // X_{j+1} = ca X_j + cb Z in registers, X_j from the ring
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
-          const double2 x = x_ring(wm * 32 + mi * 8 + g, wn * 32 + ni * 8 + 2 * t);
+        for (int ni = 0; ni < NI; ++ni) {
+          const double2 x = x_ring(wm * 32 + mi * 8 + g, wn * WN + ni * 8 + 2 * t);
           acc[mi][ni][0] = fma(p.cb, acc[mi][ni][0], p.ca * x.x);
           acc[mi][ni][1] = fma(p.cb, acc[mi][ni][1], p.ca * x.y);
         }
     }
-    __syncthreads();
+#if NS_P64_TRACE
+    if (lane == 0) tr_wend[warp] = gtimer();
+#endif
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) {
-        const int r = wm * 32 + mi * 8 + g, c = wn * 32 + ni * 8 + 2 * t;
-        S[r * EP + c] = acc[mi][ni][0];
-        S[r * EP + c + 1] = acc[mi][ni][1];
+      for (int ni = 0; ni < NI; ++ni) {
+        const int r = wm * 32 + mi * 8 + g, c = wn * WN + ni * 8 + 2 * t;
+        const int rb = wm * 4 + mi, cb = wn * NI + ni;   // 8-blocks (warp-uniform)
+        if (!diag || rb < cb) put_full(r, c, acc[mi][ni][0], acc[mi][ni][1]);
+        else if (rb == cb) put_diag(r, c, acc[mi][ni][0], acc[mi][ni][1]);
       }
   } else {
-    // Diagonal tile: only the 36 upper-triangle 8x8 blocks (rb <= cb) of the 8x8 block grid are needed
-    // (the epilogue reads r <= c and mirrors).  Warp W takes block rows W and 7 - W: (8 - W) + (W + 1)
-    // = 9 blocks for every warp, so the four SM sub-partitions stay balanced (the 32x32 warp quadrants
-    // would leave one warp idle and one at full load).  Batched d = 256: 17% fewer DMMAs per product.
-    auto diag_warp = [&](auto WC) {
+    // Diagonal tile: only the 36 upper-triangle 8x8 blocks (rb <= cb) of the 8x8 block grid are needed.
+    // Each SM sub-partition (warps w, w + 4 when NWP = 8) takes block rows P and 7 - P: (8 - P) + (P + 1) = 9
+    // blocks, so the four sub-partitions stay balanced (32x32 warp quadrants would leave one warp idle and one
+    // at full load).  Batched d = 256: 17% fewer DMMAs per product.  NWP = 4: one warp per pair of rows;
+    // NWP = 8: warp P takes row P, warp P + 4 row 7 - P.
+    auto rows_warp = [&](auto WC) {
       constexpr int W = decltype(WC)::value;
-      constexpr int R0 = W, R1 = 7 - W, N0 = 8 - W, N1 = W + 1;
-      double c0[N0][2], c1[N1][2];
+      constexpr int P = W % 4;
+      constexpr bool TWO = (NWP == 4);
+      constexpr int R0 = (NWP == 8 && W >= 4) ? 7 - P : P, N0 = 8 - R0;
+      constexpr int R1 = 7 - P, N1 = TWO ? P + 1 : 0;
+      double c0[N0][2], c1[N1 > 0 ? N1 : 1][2];
 #pragma unroll
       for (int i = 0; i < N0; ++i) c0[i][0] = c0[i][1] = 0.0;
 #pragma unroll
       for (int i = 0; i < N1; ++i) c1[i][0] = c1[i][1] = 0.0;
       mainloop([&](int s) {
 #pragma unroll
-        for (int hh = 0; hh < 2 * kSPS; ++hh) {
+        for (int hh = 0; hh < 2 * k64SPS; ++hh) {
           const int h = hh & 1;
-          const uint32_t aS = sA_u32 + (s * kSPS + (hh >> 1)) * (k64Tile * kBK * 8) + g * 128;
-          const uint32_t bS = sB_u32 + (s * kSPS + (hh >> 1)) * (k64Tile * kBK * 8) + g * 128;
+          const uint32_t aS = sA_u32 + (s * k64SPS + (hh >> 1)) * (k64Tile * kBK * 8) + g * 128;
+          const uint32_t bS = sB_u32 + (s * k64SPS + (hh >> 1)) * (k64Tile * kBK * 8) + g * 128;
           const uint32_t off = h ? off_h1 : off_h0;
+          constexpr int B0 = TWO ? (R0 < R1 ? R0 : R1) : R0;   // first B block needed
           double a0[2], a1[2], b[8][2];
 #pragma unroll
-          for (int cb = W; cb < 8; ++cb) lds128(bS + cb * 8 * 128 + off, b[cb][0], b[cb][1]);
+          for (int cb = B0; cb < 8; ++cb) lds128(bS + cb * 8 * 128 + off, b[cb][0], b[cb][1]);
           lds128(aS + R0 * 8 * 128 + off, a0[0], a0[1]);
-          lds128(aS + R1 * 8 * 128 + off, a1[0], a1[1]);
+          if (TWO) lds128(aS + R1 * 8 * 128 + off, a1[0], a1[1]);
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
 #pragma unroll
@@ -552,68 +633,36 @@ __global__ void __launch_bounds__(k64Threads, k64Stages == 2 ? 3 : 2)
           c1[i][1] = fma(p.cb, c1[i][1], p.ca * x.y);
         }
       }
-      __syncthreads();
+#if NS_P64_TRACE
+      if (lane == 0) tr_wend[warp] = gtimer();
+#endif
 #pragma unroll
       for (int i = 0; i < N0; ++i) {
         const int r = R0 * 8 + g, c = (R0 + i) * 8 + 2 * t;
-        S[r * EP + c] = c0[i][0];
-        S[r * EP + c + 1] = c0[i][1];
+        if (i == 0) put_diag(r, c, c0[i][0], c0[i][1]);
+        else put_full(r, c, c0[i][0], c0[i][1]);
       }
 #pragma unroll
       for (int i = 0; i < N1; ++i) {
         const int r = R1 * 8 + g, c = (R1 + i) * 8 + 2 * t;
-        S[r * EP + c] = c1[i][0];
-        S[r * EP + c + 1] = c1[i][1];
+        if (i == 0) put_diag(r, c, c1[i][0], c1[i][1]);
+        else put_full(r, c, c1[i][0], c1[i][1]);
       }
     };
     switch (warp) {
-      case 0: diag_warp(std::integral_constant<int, 0>{}); break;
-      case 1: diag_warp(std::integral_constant<int, 1>{}); break;
-      case 2: diag_warp(std::integral_constant<int, 2>{}); break;
-      default: diag_warp(std::integral_constant<int, 3>{}); break;
+      case 0: rows_warp(std::integral_constant<int, 0>{}); break;
+      case 1: rows_warp(std::integral_constant<int, 1>{}); break;
+      case 2: rows_warp(std::integral_constant<int, 2>{}); break;
+      case 3: rows_warp(std::integral_constant<int, 3>{}); break;
+#if NS_K64_WARPS == 8
+      case 4: rows_warp(std::integral_constant<int, 4>{}); break;
+      case 5: rows_warp(std::integral_constant<int, 5>{}); break;
+      case 6: rows_warp(std::integral_constant<int, 6>{}); break;
+      default: rows_warp(std::integral_constant<int, 7>{}); break;
+#endif
     }
   }
-  // ---------------- epilogue (ring reused as staging once every warp is past the loop) ----------------
-  __syncthreads();
   const int tid = threadIdx.x;
-  const long long ld = p.ld;
-  const long long base = (long long)job * p.job_stride;
-  double* C = p.C + base;
-  const int i0 = I * k64Tile, j0 = J * k64Tile;
-  double part = 0.0;
-  constexpr int NE = k64Tile * k64Tile;          // 4096 elements, 32 per thread
-  if (MODE == 1 && diag && p.cc != 0.0) {        // + cc I (general odd polynomial filters, Horner steps)
-    if (tid < k64Tile && i0 + tid < p.d) S[tid * EP + tid] += p.cc;
-    __syncthreads();
-  }
-  if (MODE == 1 && diag && tid < k64Tile && i0 + tid < p.d) part = S[tid * EP + tid];   // trace partial
-  if (!diag) {
-    for (int idx = tid; idx < NE; idx += k64Threads) {
-      const int r = idx >> 6, c = idx & 63;
-      const double v = S[r * EP + c];
-      C[(long long)(i0 + r) * ld + j0 + c] = v;
-      if (MODE == 0) part += v * v;
-    }
-    if (MODE == 0) part *= 2.0;
-    for (int idx = tid; idx < NE; idx += k64Threads) {
-      const int r = idx >> 6, c = idx & 63;   // mirror row j0+r, col i0+c <- tile (c, r)
-      C[(long long)(j0 + r) * ld + i0 + c] = S[c * EP + r];
-    }
-  } else {
-    for (int idx = tid; idx < NE; idx += k64Threads) {
-      const int r = idx >> 6, c = idx & 63;
-      const double v = (r <= c) ? S[r * EP + c] : S[c * EP + r];
-      C[(long long)(i0 + r) * ld + i0 + c] = v;
-      if (MODE == 0) {
-        if (r < c) {
-          part += 2.0 * v * v;
-        } else if (r == c) {
-          const double e = (i0 + r < p.d) ? v - 1.0 : v;
-          part += e * e;
-        }
-      }
-    }
-  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
   if (lane == 0) red[warp] = part;
@@ -624,6 +673,24 @@ __global__ void __launch_bounds__(k64Threads, k64Stages == 2 ? 3 : 2)
     for (int w = 0; w < k64Threads / 32; ++w) sum += red[w];
     if (MODE == 0) p.partial[(long long)job * p.n_tiles + (p.part_slot ? p.part_slot[blockIdx.x] : (int)blockIdx.x)] = sum;
     else if (diag) p.partial[(long long)job * (p.ld / k64Tile) + I] = sum;
+#if NS_P64_TRACE
+    if (g_p64_trace != nullptr) {
+      const unsigned long long r = atomicAdd(g_p64_trace, 1ull);
+      if (r < g_p64_cap) {
+        unsigned long long* rec = g_p64_trace + 1 + 10 * r;
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        rec[0] = smid | ((unsigned long long)MODE << 16) | ((unsigned long long)diag << 17);
+        rec[1] = tr_t0;
+        rec[2] = tr_t1;
+        rec[3] = gtimer();
+        rec[4] = ((unsigned long long)job << 32) | blockIdx.x;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) rec[5 + w] = tr_wend[w];
+        rec[9] = 0;
+      }
+    }
+#endif
   }
 }
 
@@ -947,6 +1014,20 @@ cudaError_t launch_compact(const DevState* state, int batch, int* list, int* n_l
 cudaError_t launch_zero_state(DevState* state, int batch, int* n_active, cudaStream_t st) {
   ns_zero_state_kernel<<<(batch + 255) / 256, 256, 0, st>>>(state, batch, n_active);
   return cudaGetLastError();
+}
+
+// Diagnostics (NS_P64_TRACE builds; else returns -1): point the 64-tile kernel's stamps at a device buffer of
+// 1 + 10 cap uint64 (buffer[0] must be zeroed by the caller), or turn them off with buf = nullptr.
+int p64_trace_set(unsigned long long* buf, unsigned long long cap) {
+#if NS_P64_TRACE
+  if (cudaMemcpyToSymbol(g_p64_trace, &buf, sizeof(buf)) != cudaSuccess) return -2;
+  if (cudaMemcpyToSymbol(g_p64_cap, &cap, sizeof(cap)) != cudaSuccess) return -2;
+  return 0;
+#else
+  (void)buf;
+  (void)cap;
+  return -1;
+#endif
 }
 
 }  // namespace nsr

@@ -19,15 +19,27 @@ constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barrie
 // 64x64-tile variant (small / batched problems): 4 DMMA warps, 3 stages of 32 KB, 2 CTAs per SM
 constexpr int kMaxFilterDeg = 4;   // general odd filters: degree <= 2*4+1 = 9 (ns_options_t.filter_c)
 constexpr int k64Tile = 64;
-constexpr int k64Threads = 128;
+#ifndef NS_K64_WARPS
+#define NS_K64_WARPS 4
+#endif
+constexpr int k64Threads = 32 * NS_K64_WARPS;   // 4 DMMA warps (32x32 warp tiles) or 8 (32x16)
 #ifndef NS_K64_STAGES
 #define NS_K64_STAGES 2
 #endif
 constexpr int k64Stages = NS_K64_STAGES;
-constexpr int k64StageBytes = kSPS * 2 * k64Tile * kBK * 8;   // 32 KB
+#ifndef NS_K64_SPS
+#define NS_K64_SPS 2
+#endif
+constexpr int k64SPS = NS_K64_SPS;   // 16-wide k-slabs per stage of the 64-tile ring (k64Stages * k64SPS >= 4)
+static_assert(k64Stages * k64SPS >= 4, "the update epilogue reads X_j's 64 columns from the ring");
+constexpr int k64StageBytes = k64SPS * 2 * k64Tile * kBK * 8;   // 32 KB at 2 slabs
 #ifndef NS_K64_PAD
 #define NS_K64_PAD 0
 #endif
+#ifndef NS_K64_MINB
+#define NS_K64_MINB (k64Stages * k64SPS <= 4 ? 3 : 2)
+#endif
+constexpr int k64MinBlocks = NS_K64_MINB;   // CTAs per SM the register budget is sized for
 constexpr int k64SmemBytes = k64Stages * k64StageBytes + 1024 + 256 + NS_K64_PAD;
 
 // Per-problem device state (one per job).  Written only by ns_decide_kernel.
@@ -213,7 +225,8 @@ cudaError_t launch_decide(DevState* state, const JobParams* jobs, const double* 
 
 // ---------------- small-d fused path (ns_small.cu): d <= 96, whole loop in one CTA per problem ----------------
 int small_dpad(int d);
-int small_trace_read(unsigned long long* out, int n);   // NS_SMALL_TRACE diagnostics
+int small_trace_read(unsigned long long* out, int n);                    // NS_SMALL_TRACE diagnostics
+int p64_trace_set(unsigned long long* buf, unsigned long long cap);      // NS_P64_TRACE diagnostics
 cudaError_t launch_small(const double* H, long long ldh, long long h_stride, const JobParams* jobs, JobParams job0,
                          LoopParams lp, double* R, long long ldr, long long r_stride, DevState* state, int batch,
                          cudaStream_t st);
