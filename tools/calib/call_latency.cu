@@ -11,6 +11,13 @@
 
 #include "nsreflector.h"
 
+__global__ void empty_kernel(int* flag) {
+  if (flag && threadIdx.x == 0) {
+    __threadfence_system();
+    *(volatile int*)flag = 1;
+  }
+}
+
 int main() {
   const int d = 64;
   std::vector<double> h(d * d, 0.0);
@@ -33,6 +40,33 @@ int main() {
     printf("C ABI ns_reflector d=64 max_steps=%d: %.1f us per call (steps %d cert %lld)\n", m,
            std::chrono::duration<double, std::micro>(t1 - t0).count() / n, res.steps, (long long)res.index_cert);
   }
-  // bare launch + sync latency of an empty kernel for reference
+  // bare launch + sync latency of an empty kernel, and launch + host spin on a flag the kernel writes to mapped
+  // pinned memory, for reference
+  {
+    const int n = 2000;
+    for (int i = 0; i < 20; ++i) empty_kernel<<<1, 32>>>(nullptr);
+    cudaDeviceSynchronize();
+    auto t0 = std::chrono::steady_clock::now();
+    for (int i = 0; i < n; ++i) {
+      empty_kernel<<<1, 32>>>(nullptr);
+      cudaStreamSynchronize(nullptr);
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    printf("empty kernel launch + cudaStreamSynchronize: %.1f us\n", std::chrono::duration<double, std::micro>(t1 - t0).count() / n);
+    volatile int* hflag;
+    int* dflag;
+    cudaHostAlloc((void**)&hflag, 4, cudaHostAllocMapped);
+    cudaHostGetDevicePointer((void**)&dflag, (void*)hflag, 0);
+    t0 = std::chrono::steady_clock::now();
+    for (int i = 0; i < n; ++i) {
+      *hflag = 0;
+      empty_kernel<<<1, 32>>>(dflag);
+      while (*hflag == 0) {
+      }
+    }
+    t1 = std::chrono::steady_clock::now();
+    cudaDeviceSynchronize();
+    printf("empty kernel launch + host spin on a mapped flag: %.1f us\n", std::chrono::duration<double, std::micro>(t1 - t0).count() / n);
+  }
   return 0;
 }
