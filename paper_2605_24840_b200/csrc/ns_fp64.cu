@@ -442,8 +442,13 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
   };
   // X_j(r, c..c+1) of this tile (c even) from the ring after the K loop: the block's 16-column slab q sits in
   // the slot of stage nst - kJS + q / k64SPS; 128-B swizzle (16-B chunk of row r at chunk ^ (r & 7))
+  // (a ring shallower than the block, k64Stages * k64SPS < 4, has overwritten its first slabs: those come from
+  // L2 instead)
   auto x_ring = [&](int r, int c) -> double2 {
     const int q = c >> 4;                        // 16-column slab of the block
+    if (k64Stages * k64SPS < 4 && q < 4 - k64Stages * k64SPS)
+      return *reinterpret_cast<const double2*>(p.Xold + (long long)job * p.job_stride +
+                                               (long long)(I * k64Tile + r) * p.ld + J * k64Tile + c);
     const int slot = (nst - kJS + q / k64SPS) % k64Stages;
     const int cs = c & 15;
     const double* slab = sA + (slot * k64SPS + q % k64SPS) * (k64Tile * kBK);

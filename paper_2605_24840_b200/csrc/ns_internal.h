@@ -31,7 +31,6 @@ constexpr int k64Stages = NS_K64_STAGES;
 #define NS_K64_SPS 2
 #endif
 constexpr int k64SPS = NS_K64_SPS;   // 16-wide k-slabs per stage of the 64-tile ring (k64Stages * k64SPS >= 4)
-static_assert(k64Stages * k64SPS >= 4, "the update epilogue reads X_j's 64 columns from the ring");
 constexpr int k64StageBytes = k64SPS * 2 * k64Tile * kBK * 8;   // 32 KB at 2 slabs
 #ifndef NS_K64_PAD
 #define NS_K64_PAD 0
