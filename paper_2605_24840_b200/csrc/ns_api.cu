@@ -2736,7 +2736,7 @@ void ns_profile_get(ns_profile_t* out) {
 }
 
 const char* ns_build_info(void) {
-  return "libnsreflector FP64 DMMA/TMA path; target sm_100a; tile 128x128x16, 6-stage TMA ring, 8 DMMA warps";
+  return "libnsreflector FP64 DMMA/TMA path; target sm_100a; 128x128 tiles (3 x 64 KB TMA ring, 8 DMMA warps), 64x64 batched tiles, tcgen05 BF16x3 / INT8 Ozaki paths";
 }
 
 const char* ns_status_string(ns_status_t st) {

@@ -1241,3 +1241,22 @@ def test_mixed_ill_conditioned(nsr, prec):
     if not _tie_band(o["hist_residual"], 1e-10 * math.sqrt(d), o["steps"]):
         assert r["steps"] == o["steps"], (r, o["steps"])
     assert checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= TOL_R
+
+
+@pytest.mark.parametrize("d,tol_mode", [(64, 0), (64, 1), (40, 0), (96, 1), (200, 0), (200, 1)])
+def test_stop_rule_exact_threshold(nsr, d, tol_mode):
+    """The stop rule rho_j < tol (C4, strict) at a threshold equal to the path's own residual: the fused small-d
+    kernel (d <= 96) decides on the squared residual with an exact re-test inside a +-1e-14 band, the tiled path on
+    r_j itself; both must take the rounded comparison's decision bit for bit.  tol = rho_j must NOT stop at j
+    (not strictly less), tol = nextafter(rho_j, +inf) must."""
+    p = workloads.cfg3_dense(d=d, k=max(1, d // 16), n_house=8, seed=3, form=True)
+    Hg = torch.from_numpy(p.H).to(_dev())
+    j = 6
+    _, res = nsr.ns_reflector(Hg, p.s, p.alpha, p.k, j, 0.0, tol_mode)     # fixed steps: residual of X_j
+    assert res["steps"] == j
+    rho = res["residual"] / math.sqrt(d) if tol_mode else res["residual"]
+    _, at = nsr.ns_reflector(Hg, p.s, p.alpha, p.k, 100, rho, tol_mode)
+    assert at["steps"] == j + 1 and at["flags"] & 1, (rho, at)
+    _, above = nsr.ns_reflector(Hg, p.s, p.alpha, p.k, 100, float(np.nextafter(rho, np.inf)), tol_mode)
+    assert above["steps"] == j and above["flags"] & 1, (rho, above)
+    assert above["residual"] == res["residual"]
