@@ -23,18 +23,15 @@ def tie(o, tol, tm, d):
 
 
 def mixed_step_ok(r, o, tol, tm, d):
-    """Reading C16b: the mixed path's step count may differ by one from the oracle's when (a) the oracle's
-    residual at the mixed switch step was already below the switch threshold (late switch, +1), or (b) the
-    oracle's residual at its decision step or the one before lies within a factor 2 of the threshold (the
-    split-precision switch iterate perturbs the last residuals by up to ~2x: a wider tie band than C9's)."""
+    """Reading C16b (round 2: switch at r/sqrt(d) < 1e-3): the mixed path must take the oracle's step count; a
+    difference of one is reported separately (not a failure) only when the oracle's residual at its decision step
+    or the one before lies within 3% of the threshold -- the measured predicate DESIGN C16b names (never observed
+    in the 440-problem sweep)."""
     t = tol if tm == 0 else tol * math.sqrt(d)
     h = o["hist_residual"]
     if abs(r["steps"] - o["steps"]) != 1:
         return False
-    late = (r["steps"] == o["steps"] + 1 and 0 <= r["switch_step"] <= o["steps"]
-            and h[r["switch_step"]] / math.sqrt(d) < 1e-4)
-    near = any(0.5 * t <= h[j] <= 2.0 * t for j in (o["steps"] - 1, o["steps"]) if 0 <= j < len(h))
-    return late or near
+    return any(0.97 * t <= h[j] <= 1.03 * t for j in (o["steps"] - 1, o["steps"]) if 0 <= j < len(h))
 
 
 def problem(seed, dmax):
