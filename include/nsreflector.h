@@ -297,20 +297,46 @@ ns_status_t ns_shift_certificate(double lam_k_hat, double lam_k1_hat, double eps
  *   k      HOST int32[nruns], 1 <= k < d
  *   x0     device nruns x d starts;  x_out device nruns x d final states
  *   out    HOST ns_alg1_result_t[nruns]: iterations, final ||g||, Morse index of H(x_final),
- *          success = (||g|| <= grad_tol && Morse index == k)
+ *          success = (||g|| <= grad_tol && Morse index == k), stop reason, midpoint refreshes, last shift
  *   ws     device workspace >= ns_workspace_bytes_alg1(nruns) bytes
+ * ns_alg1_rotated_quartic_ex: the same with a shift policy (alg:ssr step 4; DESIGN reading N2b)
+ * and the admissibility stop (step 8; prop:reuse_refresh P:604).  pol == NULL is the midpoint
+ * policy with eps = 0.  Per iteration, after the ||g|| / budget test:
+ *   NS_SHIFT_MIDPOINT  s = (lk + lk1)/2
+ *   NS_SHIFT_DAMPED    s = min(max(damp s_prev + (1 - damp) mid, lk + clip gap), lk1 - clip gap)   (n >= 1)
+ *   NS_SHIFT_REUSE     s = s_prev if min(s_prev - lk, lk1 - s_prev) > reuse_margin, else mid      (n >= 1)
+ *   stop (NS_ALG1_STOP_INADMISSIBLE, no update) unless min(s - lk, lk1 - s) > eps.
+ * Errors: NS_ERR_INVALID_ARG for damp outside [0, 1), clip outside (0, 1/2], a negative or non-finite
+ * reuse_margin / eps, an unknown policy, and the checks of the plain entry.
  */
+enum { NS_SHIFT_MIDPOINT = 0, NS_SHIFT_DAMPED = 1, NS_SHIFT_REUSE = 2 };
+enum { NS_ALG1_STOP_GRAD = 0, NS_ALG1_STOP_BUDGET = 1, NS_ALG1_STOP_INADMISSIBLE = 2 };
+typedef struct {
+  int32_t policy;        /* NS_SHIFT_* */
+  int32_t pad;
+  double damp;           /* damped: weight beta of the previous shift, [0, 1) */
+  double clip;           /* damped: kappa, clip into [lk + kappa gap, lk1 - kappa gap], (0, 1/2] */
+  double reuse_margin;   /* reuse/refresh: threshold tau on the previous shift's margin, >= 0 */
+  double eps;            /* admissibility: endpoint error bound, >= 0 */
+} ns_alg1_policy_t;
 typedef struct {
   int32_t iters;
   int32_t morse_index;
   int32_t success;
-  int32_t pad;
+  int32_t stop_reason;   /* NS_ALG1_STOP_* */
   double grad_norm;
+  int32_t refreshes;     /* iterations whose shift was the fresh midpoint */
+  int32_t pad;
+  double s_last;         /* last shift used in an update (NaN if none) */
 } ns_alg1_result_t;
 size_t ns_workspace_bytes_alg1(int32_t nruns);
 ns_status_t ns_alg1_rotated_quartic(const double* Q, int64_t d, int32_t nruns, const int32_t* k, const double* x0,
                                     int32_t m, double eta, int32_t max_iters, double grad_tol, double* x_out,
                                     void* ws, size_t ws_bytes, void* stream, ns_alg1_result_t* out);
+ns_status_t ns_alg1_rotated_quartic_ex(const double* Q, int64_t d, int32_t nruns, const int32_t* k,
+                                       const double* x0, int32_t m, double eta, int32_t max_iters, double grad_tol,
+                                       const ns_alg1_policy_t* pol, double* x_out, void* ws, size_t ws_bytes,
+                                       void* stream, ns_alg1_result_t* out);
 
 /*
  * ---------------- multi-GPU (one process per GPU, NCCL over NVLink/NVSwitch) ----------------

@@ -25,7 +25,8 @@ EXPORTED_SYMBOLS = (
     "ns_last_error", "ns_profile_enable", "ns_profile_reset", "ns_profile_get", "ns_options_default",
     "ns_reflector_ex", "ns_comm_get_unique_id", "ns_comm_init", "ns_comm_destroy", "ns_shard_plan",
     "ns_workspace_bytes_sharded", "ns_reflector_sharded", "ns_shard_chunks", "ns_workspace_bytes_setup", "ns_scale_bound",
-    "ns_shift_certificate", "ns_workspace_bytes_alg1", "ns_alg1_rotated_quartic", "ns_debug_mx_trace",
+    "ns_shift_certificate", "ns_workspace_bytes_alg1", "ns_alg1_rotated_quartic", "ns_alg1_rotated_quartic_ex",
+    "ns_debug_mx_trace",
     "ns_symm_product_shard", "ns_workspace_bytes_sharded_emulated", "ns_reflector_sharded_emulated",
     "ns_comm_init_host", "ns_shard_rows", "ns_reflector_sharded_rows", "ns_reflector_batched_dev",
     "ns_workspace_bytes_inertia", "ns_inertia", "ns_shift_bisect", "ns_workspace_bytes_ex", "ns_debug_small_trace", "ns_debug_p64_trace",
@@ -64,7 +65,16 @@ class NsShiftCert(ctypes.Structure):
 
 class NsAlg1Result(ctypes.Structure):
     _fields_ = [("iters", ctypes.c_int32), ("morse_index", ctypes.c_int32), ("success", ctypes.c_int32),
-                ("pad", ctypes.c_int32), ("grad_norm", ctypes.c_double)]
+                ("stop_reason", ctypes.c_int32), ("grad_norm", ctypes.c_double), ("refreshes", ctypes.c_int32),
+                ("pad", ctypes.c_int32), ("s_last", ctypes.c_double)]
+
+
+class NsAlg1Policy(ctypes.Structure):
+    _fields_ = [("policy", ctypes.c_int32), ("pad", ctypes.c_int32), ("damp", ctypes.c_double),
+                ("clip", ctypes.c_double), ("reuse_margin", ctypes.c_double), ("eps", ctypes.c_double)]
+
+
+NS_SHIFT_POLICIES = {"midpoint": 0, "damped": 1, "reuse_refresh": 2}
 
 
 class NsBisect(ctypes.Structure):
@@ -178,6 +188,10 @@ def load_library(path=LIB_PATH):
     lib.ns_alg1_rotated_quartic.restype = ctypes.c_int
     lib.ns_alg1_rotated_quartic.argtypes = [c_vp, c_i64, c_i32, c_vp, c_vp, c_i32, c_dbl, c_i32, c_dbl, c_vp, c_vp,
                                             c_sz, c_vp, ctypes.POINTER(NsAlg1Result)]
+    lib.ns_alg1_rotated_quartic_ex.restype = ctypes.c_int
+    lib.ns_alg1_rotated_quartic_ex.argtypes = [c_vp, c_i64, c_i32, c_vp, c_vp, c_i32, c_dbl, c_i32, c_dbl,
+                                               ctypes.POINTER(NsAlg1Policy), c_vp, c_vp, c_sz, c_vp,
+                                               ctypes.POINTER(NsAlg1Result)]
     _lib = lib
     return lib
 
@@ -673,9 +687,11 @@ def ns_shift_certificate(lam_k_hat, lam_k1_hat, eps, s, delta=0.0):
                 midpoint_ok=bool(c.midpoint_ok))
 
 
-def ns_alg1_rotated_quartic(Q, k, x0, m, eta, max_iters, grad_tol, x_out=None, ws=None, stream=None):
+def ns_alg1_rotated_quartic(Q, k, x0, m, eta, max_iters, grad_tol, x_out=None, ws=None, stream=None,
+                            policy="midpoint", damp=0.5, clip=0.25, reuse_margin=0.0, eps=0.0):
     """Batched Algorithm 1 on the rotated quartic (N2).  Q (d, d) and x0 (nruns, d) CUDA float64;
-    k host ints.  Returns (x_final, list of result dicts)."""
+    k host ints; policy "midpoint" | "damped" | "reuse_refresh" with its parameters and the admissibility
+    bound eps (ns_alg1_rotated_quartic_ex).  Returns (x_final, list of result dicts)."""
     torch = _torch()
     lib = load_library()
     _require_cuda_f64(Q, "Q")
@@ -686,16 +702,19 @@ def ns_alg1_rotated_quartic(Q, k, x0, m, eta, max_iters, grad_tol, x_out=None, w
         x_out = torch.empty_like(x0)
     if ws is None:
         ws = alloc_workspace(lib.ns_workspace_bytes_alg1(nruns), x0.device)
+    if policy not in NS_SHIFT_POLICIES:
+        raise ValueError(f"unknown shift policy {policy!r}")
+    pol = NsAlg1Policy(NS_SHIFT_POLICIES[policy], 0, float(damp), float(clip), float(reuse_margin), float(eps))
     outs = (NsAlg1Result * nruns)()
     with _on(x0.device):
-        st = lib.ns_alg1_rotated_quartic(ctypes.c_void_p(Q.data_ptr()), d, nruns, k_a.ctypes.data,
-                                       ctypes.c_void_p(x0.data_ptr()), int(m), float(eta), int(max_iters),
-                                       float(grad_tol), ctypes.c_void_p(x_out.data_ptr()),
-                                         ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream, x0.device),
-                                         outs)
+        st = lib.ns_alg1_rotated_quartic_ex(ctypes.c_void_p(Q.data_ptr()), d, nruns, k_a.ctypes.data,
+                                            ctypes.c_void_p(x0.data_ptr()), int(m), float(eta), int(max_iters),
+                                            float(grad_tol), ctypes.byref(pol), ctypes.c_void_p(x_out.data_ptr()),
+                                            ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                                            _stream_ptr(stream, x0.device), outs)
     _check(st)
-    return x_out, [dict(iters=o.iters, morse_index=o.morse_index, success=bool(o.success), grad_norm=o.grad_norm)
-                   for o in outs]
+    return x_out, [dict(iters=o.iters, morse_index=o.morse_index, success=bool(o.success), grad_norm=o.grad_norm,
+                        stop_reason=o.stop_reason, refreshes=o.refreshes, s_last=o.s_last) for o in outs]
 
 
 def build_info():

@@ -2697,15 +2697,23 @@ size_t ns_workspace_bytes_alg1(int32_t nruns) {
   return align256(sizeof(int) * (size_t)nruns) + align256(sizeof(OuterResult) * (size_t)nruns);
 }
 
-ns_status_t ns_alg1_rotated_quartic(const double* Q, int64_t d, int32_t nruns, const int32_t* k, const double* x0,
-                                    int32_t m, double eta, int32_t max_iters, double grad_tol, double* x_out,
-                                    void* ws, size_t ws_bytes, void* stream, ns_alg1_result_t* out) {
+ns_status_t ns_alg1_rotated_quartic_ex(const double* Q, int64_t d, int32_t nruns, const int32_t* k,
+                                       const double* x0, int32_t m, double eta, int32_t max_iters, double grad_tol,
+                                       const ns_alg1_policy_t* pol, double* x_out, void* ws, size_t ws_bytes,
+                                       void* stream, ns_alg1_result_t* out) {
   g_last_error.clear();
   if (!Q || !k || !x0 || !x_out || !ws || !out) return fail(NS_ERR_INVALID_ARG, "null pointer argument");
   if (d < 2 || d > 64) return fail(NS_ERR_INVALID_ARG, "d must lie in [2, 64] (one CTA per run)");
   if (nruns < 1 || nruns > 1 << 20) return fail(NS_ERR_INVALID_ARG, "bad nruns");
   if (m < 0 || m > 64 || max_iters < 0) return fail(NS_ERR_INVALID_ARG, "bad depth / iteration budget");
   if (!(eta > 0.0) || !std::isfinite(eta) || !(grad_tol >= 0.0)) return fail(NS_ERR_INVALID_ARG, "bad eta / grad_tol");
+  ns_alg1_policy_t pp{NS_SHIFT_MIDPOINT, 0, 0.5, 0.25, 0.0, 0.0};
+  if (pol) pp = *pol;
+  if (pp.policy < NS_SHIFT_MIDPOINT || pp.policy > NS_SHIFT_REUSE) return fail(NS_ERR_INVALID_ARG, "unknown shift policy");
+  if (!(pp.damp >= 0.0 && pp.damp < 1.0)) return fail(NS_ERR_INVALID_ARG, "damp must lie in [0, 1)");
+  if (!(pp.clip > 0.0 && pp.clip <= 0.5)) return fail(NS_ERR_INVALID_ARG, "clip must lie in (0, 1/2]");
+  if (!(pp.reuse_margin >= 0.0) || !std::isfinite(pp.reuse_margin) || !(pp.eps >= 0.0) || !std::isfinite(pp.eps))
+    return fail(NS_ERR_INVALID_ARG, "reuse_margin and eps must be finite and >= 0");
   for (int r = 0; r < nruns; ++r)
     if (k[r] < 1 || k[r] >= d) return fail(NS_ERR_INVALID_ARG, "k[%d] must lie in [1, d-1]", r);
   if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(NS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
@@ -2714,7 +2722,7 @@ ns_status_t ns_alg1_rotated_quartic(const double* Q, int64_t d, int32_t nruns, c
   int* dk = static_cast<int*>(ws);
   OuterResult* dres = reinterpret_cast<OuterResult*>(static_cast<uint8_t*>(ws) + align256(sizeof(int) * (size_t)nruns));
   NS_CUDA(cudaMemcpyAsync(dk, k, sizeof(int) * nruns, cudaMemcpyHostToDevice, cs));
-  OuterParams p{m, max_iters, eta, grad_tol};
+  OuterParams p{m, max_iters, eta, grad_tol, pp.policy, 0, pp.damp, pp.clip, pp.reuse_margin, pp.eps};
   NS_CUDA(launch_outer(Q, (int)d, dk, x0, p, x_out, dres, nruns, cs));
   std::vector<OuterResult> hr(nruns);
   NS_CUDA(cudaMemcpyAsync(hr.data(), dres, sizeof(OuterResult) * nruns, cudaMemcpyDeviceToHost, cs));
@@ -2723,10 +2731,20 @@ ns_status_t ns_alg1_rotated_quartic(const double* Q, int64_t d, int32_t nruns, c
     out[r].iters = hr[r].iters;
     out[r].morse_index = hr[r].morse_index;
     out[r].success = hr[r].success;
-    out[r].pad = 0;
+    out[r].stop_reason = hr[r].stop_reason;
     out[r].grad_norm = hr[r].grad_norm;
+    out[r].refreshes = hr[r].refreshes;
+    out[r].pad = 0;
+    out[r].s_last = hr[r].s_last;
   }
   return NS_OK;
+}
+
+ns_status_t ns_alg1_rotated_quartic(const double* Q, int64_t d, int32_t nruns, const int32_t* k, const double* x0,
+                                    int32_t m, double eta, int32_t max_iters, double grad_tol, double* x_out,
+                                    void* ws, size_t ws_bytes, void* stream, ns_alg1_result_t* out) {
+  return ns_alg1_rotated_quartic_ex(Q, d, nruns, k, x0, m, eta, max_iters, grad_tol, nullptr, x_out, ws, ws_bytes,
+                                    stream, out);
 }
 
 void ns_profile_enable(int on) { prof().on = (on != 0); }

@@ -236,13 +236,22 @@ struct OuterParams {
   int max_iters;
   double eta;         // fixed outer step size
   double grad_tol;
+  int policy;         // shift policy (alg:ssr step 4): 0 midpoint, 1 damped midpoint, 2 reuse/refresh
+  int pad;
+  double damp;        // damped: weight of the previous shift
+  double clip;        // damped: clip into [lk + clip gap, lk1 - clip gap]
+  double reuse_margin;  // reuse/refresh: keep the previous shift while its margin exceeds this
+  double eps;         // admissibility: stop unless the chosen shift's estimated margin exceeds eps
 };
 struct OuterResult {
   int iters;
   int morse_index;
   int success;
-  int pad;
+  int stop_reason;    // 0 ||g|| <= grad_tol, 1 budget, 2 inadmissible shift
   double grad_norm;
+  int refreshes;      // iterations that took the fresh midpoint
+  int pad;
+  double s_last;      // last shift used in an update (NaN when none)
 };
 cudaError_t launch_outer(const double* Q, int d, const int* k, const double* x0, OuterParams p, double* xout,
                          OuterResult* res, int nruns, cudaStream_t st);

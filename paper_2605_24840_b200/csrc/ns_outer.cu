@@ -6,7 +6,11 @@
 //   g = Q (y^3 + c y),   H = Q diag(mu) Q^T,  mu_i = 3 y_i^2 + c_i
 // per outer iteration n (alg:ssr steps 2-8):
 //   endpoints lambda_k, lambda_{k+1} = k-th / (k+1)-th smallest mu (exact for this model),
-//   midpoint shift s (prop:mid), alpha = max_i |mu_i - s| = ||H - sI||_2 (divide convention, C1),
+//   shift s by the policy (step 4; DESIGN reading N2b): midpoint (prop:mid), damped midpoint
+//   clip(beta s_prev + (1 - beta) mid, [lk + kappa gap, lk1 - kappa gap]), or reuse/refresh (keep s_prev while
+//   min(s_prev - lk, lk1 - s_prev) > tau, else the midpoint); stop if the shift's estimated margin <= eps
+//   (step 8 "the shift ceases to be admissible", prop:reuse_refresh P:604),
+//   alpha = max_i |mu_i - s| = ||H - sI||_2 (divide convention, C1),
 //   R~ = phi_m((H - sI)/alpha): m Newton–Schulz steps from X_0 = Q diag((mu - s)/alpha) Q^T
 //        (m = 0: the exact reflector Q diag(sgn(mu - s)) Q^T),
 //   x_{n+1} = x_n - eta R~ g_n  (eq:discrete_step),  stop when ||g|| <= grad_tol or n = max_iters.
@@ -44,8 +48,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
   }
   for (int i = threadIdx.x; i < DP; i += kSmallThreads) x[i] = (i < d) ? x0[(long long)run * d + i] : 0.0;
   __syncthreads();
-  int n = 0;
+  int n = 0, refreshes = 0, stop = 0;
   double gn = 0.0;
+  double s_prev = __longlong_as_double(0x7ff8000000000000ll);   // NaN: no shift yet
   while (true) {
     // y = Q^T x ; mu ; g = Q (y^3 + c y)
     for (int i = threadIdx.x; i < DP; i += kSmallThreads) {
@@ -65,7 +70,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
       gp += a * a;
     }
     gn = sqrt(block_sum(gp, red));
-    if (!(gn > p.grad_tol) || n >= p.max_iters) break;   // also stops on NaN
+    if (!(gn > p.grad_tol)) { stop = 0; break; }   // also stops on NaN
+    if (n >= p.max_iters) { stop = 1; break; }
     // endpoints: k-th and (k+1)-th smallest mu (rank by counting, ties by index)
     for (int i = threadIdx.x; i < d; i += kSmallThreads) {
       int rank = 0;
@@ -74,7 +80,25 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
       if (rank == k) sc[1] = mu[i];
     }
     __syncthreads();
-    const double s = 0.5 * (sc[0] + sc[1]);
+    // step 4: every thread takes the same decision from the same shared endpoints
+    const double lk = sc[0], lk1 = sc[1];
+    const double mid = 0.5 * (lk + lk1);
+    double s = mid;
+    bool fresh = true;
+    if (n > 0 && p.policy == 1) {
+      const double gap = lk1 - lk;
+      const double blend = __dadd_rn(__dmul_rn(p.damp, s_prev), __dmul_rn(1.0 - p.damp, mid));
+      s = fmin(fmax(blend, __dadd_rn(lk, __dmul_rn(p.clip, gap))), __dsub_rn(lk1, __dmul_rn(p.clip, gap)));
+      fresh = false;
+    } else if (n > 0 && p.policy == 2) {
+      if (fmin(s_prev - lk, lk1 - s_prev) > p.reuse_margin) {
+        s = s_prev;
+        fresh = false;
+      }
+    }
+    if (!(fmin(s - lk, lk1 - s) > p.eps)) { stop = 2; break; }   // inadmissible shift: no update
+    refreshes += fresh ? 1 : 0;
+    s_prev = s;
     double am = 0.0;
     for (int i = threadIdx.x; i < d; i += kSmallThreads) am = fmax(am, fabs(mu[i] - s));
 #pragma unroll
@@ -124,7 +148,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
     r.morse_index = neg;
     r.grad_norm = gn;
     r.success = (gn <= p.grad_tol && neg == k) ? 1 : 0;
+    r.stop_reason = stop;
+    r.refreshes = refreshes;
     r.pad = 0;
+    r.s_last = s_prev;
     res[run] = r;
   }
 }

@@ -625,6 +625,91 @@ def test_alg1_scan_matches_oracle(nsr):
         assert agree == len(kk)
 
 
+@pytest.mark.parametrize("pol", [dict(policy="damped", damp=0.5, clip=0.2), dict(policy="damped", damp=0.8, clip=0.05),
+                                 dict(policy="reuse_refresh", reuse_margin=0.1),
+                                 dict(policy="reuse_refresh", reuse_margin=0.6)])
+def test_alg1_policies_match_oracle(nsr, pol):
+    """alg:ssr step 4's damped-midpoint and reuse/refresh policies (DESIGN N2b) vs the oracle: local runs
+    (radius 0.1, final states within 1e-9) and scan runs (radius 4, success flags), at NS depth 2 and 4 --
+    stop reason, Morse index and success equal, iterations +-1 at the grad_tol crossing, midpoint refreshes
+    equal when the iterations are, and the last shift equal to the oracle's."""
+    from oracle import outer
+    for radius, n_starts in ((0.1, 3), (4.0, 4)):
+        Q, ks, starts = workloads.rotated_quartic_scan(d=64, n_starts=n_starts, radius=radius)
+        Qg = torch.from_numpy(Q).to(_dev())
+        kk = [k for k in ks for _ in starts]
+        x0 = np.concatenate([starts for _ in ks])
+        for m in (2, 4):
+            xf, res = nsr.ns_alg1_rotated_quartic(Qg, kk, torch.from_numpy(x0).to(_dev()), m, 0.2, 600, 1e-10, **pol)
+            xf = xf.cpu().numpy()
+            for r in range(len(kk)):
+                o = outer.run(Q, kk[r], x0[r], m, 0.2, 600, 1e-10, **pol)
+                g = res[r]
+                assert g["success"] == o["success"] and g["stop_reason"] == o["stop_reason"], (pol, m, r, g, o["iters"])
+                assert g["morse_index"] == o["morse_index"]
+                assert abs(g["iters"] - o["iters"]) <= 1
+                if g["iters"] == o["iters"]:
+                    assert g["refreshes"] == o["refreshes"], (pol, m, r, g, o["refreshes"])
+                    assert abs(g["s_last"] - o["shifts"][-1]) <= 1e-12 * max(1.0, abs(o["shifts"][-1]))
+                if radius < 1:
+                    assert o["success"] and np.max(np.abs(xf[r] - o["x"])) <= 1e-9
+
+
+def test_alg1_exact_reflector_policy_independent(nsr):
+    """prop:exact on the device: with m = 0 every admissible shift gives the same exact reflector, so the
+    GPU runs under the damped and reuse/refresh policies end in the midpoint run's state bit for bit."""
+    Q, ks, starts = workloads.rotated_quartic_scan(d=64, n_starts=8, radius=4.0)
+    Qg = torch.from_numpy(Q).to(_dev())
+    kk = [k for k in ks for _ in starts]
+    x0 = torch.from_numpy(np.concatenate([starts for _ in ks])).to(_dev())
+    xa, ra = nsr.ns_alg1_rotated_quartic(Qg, kk, x0, 0, 0.2, 300, 1e-10)
+    for pol in (dict(policy="damped", damp=0.7, clip=0.1), dict(policy="reuse_refresh", reuse_margin=0.05)):
+        xb, rb = nsr.ns_alg1_rotated_quartic(Qg, kk, x0, 0, 0.2, 300, 1e-10, **pol)
+        # runs whose target gap closes stop as inadmissible, and when depends on the shift's margin (a damped
+        # shift sits nearer an endpoint, so its margin rounds away first): compare the others
+        keep = [r for r in range(len(kk)) if ra[r]["stop_reason"] != 2 and rb[r]["stop_reason"] != 2]
+        assert len(keep) >= len(kk) // 4
+        assert torch.equal(xa[keep], xb[keep])
+        assert [ra[r]["iters"] for r in keep] == [rb[r]["iters"] for r in keep]
+        assert any(ra[r]["s_last"] != rb[r]["s_last"] for r in keep)
+
+
+def test_alg1_admissibility_stop(nsr):
+    """Step 8's admissibility stop (prop:reuse_refresh, m_hat > eps) on the device: the hand case Q = I,
+    x0 = (1/2, 1/4, 0...), k = 1 has mu = (-1/4, 19/16, 1, ...) -> endpoints (-1/4, 1), midpoint 3/8, margin
+    5/8: eps = 0.6 proceeds, eps = 5/8 stops before any update (state unchanged); the oracle agrees; and a
+    gap-closing run (20 iterations) stops where the oracle does."""
+    from oracle import outer
+    d = 8
+    Q = np.eye(d)
+    x0 = np.zeros((1, d))
+    x0[0, :2] = (0.5, 0.25)
+    Qg, xg = torch.from_numpy(Q).to(_dev()), torch.from_numpy(x0).to(_dev())
+    for eps, stop, iters in ((0.6, outer.STOP_BUDGET, 2), (5 / 8, outer.STOP_INADMISSIBLE, 0)):
+        xf, res = nsr.ns_alg1_rotated_quartic(Qg, [1], xg, 2, 0.1, 2, 0.0, eps=eps)
+        o = outer.run(Q, 1, x0[0], 2, 0.1, 2, 0.0, eps=eps)
+        assert res[0]["stop_reason"] == o["stop_reason"] == stop and res[0]["iters"] == o["iters"] == iters
+        if stop == outer.STOP_INADMISSIBLE:
+            assert torch.equal(xf, xg) and math.isnan(res[0]["s_last"])
+    x0 = np.zeros((1, d))
+    x0[0, :2] = (0.9, 0.1)
+    x0[0, 2:] = 2.0        # the oracle stops this run at iteration 20 (gap of lambda_1, lambda_2 down to 2 eps)
+    xf, res = nsr.ns_alg1_rotated_quartic(Qg, [1], torch.from_numpy(x0).to(_dev()), 0, 0.05, 200, 0.0, eps=0.05)
+    o = outer.run(Q, 1, x0[0], 0, 0.05, 200, 0.0, eps=0.05)
+    assert res[0]["stop_reason"] == o["stop_reason"] == outer.STOP_INADMISSIBLE
+    assert res[0]["iters"] == o["iters"]
+    assert np.max(np.abs(xf.cpu().numpy()[0] - o["x"])) <= 1e-12
+
+
+def test_alg1_policy_validation(nsr):
+    Q = torch.eye(8, dtype=torch.float64, device=_dev())
+    x0 = torch.zeros((1, 8), dtype=torch.float64, device=_dev())
+    for bad in (dict(policy="damped", damp=1.0), dict(policy="damped", clip=0.0), dict(policy="damped", clip=0.6),
+                dict(policy="reuse_refresh", reuse_margin=-1.0), dict(eps=float("nan"))):
+        with pytest.raises(nsr.NsError):
+            nsr.ns_alg1_rotated_quartic(Q, [1], x0, 2, 0.1, 2, 0.0, **bad)
+
+
 # ------------------------------------------------------------------ N4: Ozaki-split FP64 on INT8 tensor cores
 @pytest.mark.parametrize("d,mode", [(128, 0), (300, 0), (515, 1), (256, 2), (200, 2), (1024, 0), (4500, 1), (16500, 0),
                                     (16448, 1)])
