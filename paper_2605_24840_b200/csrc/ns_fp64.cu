@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
   else if (p.state != nullptr && p.state[job].done) return;
 #if NS_P64_TRACE
   unsigned long long tr_t0 = gtimer(), tr_t1 = 0;
-  __shared__ unsigned long long tr_wend[k64Threads / 32];
+  __shared__ unsigned long long tr_wend[k64Threads / 32], tr_wst[k64Threads / 32];
 #endif
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -668,6 +668,9 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
     }
   }
   const int tid = threadIdx.x;
+#if NS_P64_TRACE
+  if (lane == 0) tr_wst[warp] = gtimer();
+#endif
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
   if (lane == 0) red[warp] = part;
@@ -692,7 +695,9 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
         rec[4] = ((unsigned long long)job << 32) | blockIdx.x;
 #pragma unroll
         for (int w = 0; w < 4; ++w) rec[5 + w] = tr_wend[w];
-        rec[9] = 0;
+        unsigned long long wst = 0;
+        for (int w = 0; w < 4; ++w) wst = tr_wst[w] > wst ? tr_wst[w] : wst;
+        rec[9] = wst;   // last warp's stores issued
       }
     }
 #endif

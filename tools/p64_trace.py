@@ -75,6 +75,7 @@ if a.trace:
     t0, t1, t3, we = t0 - base, t1 - base, t3 - base, we - base
     t2 = we.max(1)                      # the CTA's K loop ends with its last warp
     t2f = we.min(1)
+    tst = rec[:, 9].astype(np.int64) - base   # last warp's epilogue stores issued
     print(f"{n} CTAs traced; span {(t3.max()) / 1e6:.2f} ms")
     for m in (0, 1):
         for dg in (0, 1):
@@ -82,7 +83,7 @@ if a.trace:
             if k.any():
                 print(f"  mode {m} diag {dg}: n={k.sum():7d}  prologue {np.median(t1[k] - t0[k]) / 1e3:6.2f} us  "
                       f"K loop (first..last warp) {np.median(t2f[k] - t1[k]) / 1e3:6.2f}..{np.median(t2[k] - t1[k]) / 1e3:6.2f} us  "
-                      f"epilogue {np.median(t3[k] - t2[k]) / 1e3:6.2f} us  total {np.median(t3[k] - t0[k]) / 1e3:6.2f} us; "
+                      f"epilogue {np.median(t3[k] - t2[k]) / 1e3:6.2f} us (stores issued +{np.median(tst[k] - t2[k]) / 1e3:5.2f})  total {np.median(t3[k] - t0[k]) / 1e3:6.2f} us; "
                       f"warp w ends last: {np.bincount(np.argmax(we[k], 1), minlength=4) / k.sum()}")
     # per SM: fraction of the busy span in which >= 1 CTA is inside its K loop
     res = [], []
