@@ -560,6 +560,7 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
   const bool chunked = opt.h_host != nullptr;   // the host entry checked batch == 1 and the side stream
   const Layout* Lp = &L;
   ProdParams sq0{tiles, n_t, L.d_pad / kBK, L.d, L.d_pad, (long long)L.d_pad * L.d_pad, Y, nullptr, res, state, 0};
+  sq0.same_pq = 1;
   if (chunked) {
     SpecCtx& c = spec_ctx();
     const int nch = std::min(8, nb);
@@ -662,6 +663,7 @@ ns_status_t run_loop(const Layout& L, uint8_t* ws, const double* H, long long ld
     const CUtensorMap& tmC = odd ? tmB : tmA;
 
     ProdParams sq{tiles, n_t, L.d_pad / kBK, L.d, L.d_pad, job_stride, Y, nullptr, res, state, 0};
+    sq.same_pq = 1;
     if (pf.on) NS_CUDA(cudaEventRecord(pf.get(4 * j + 0), st));
     if (!(chunked && j == 0)) NS_CUDA(product(tmC, tmC, sq));   // chunked: the first square already ran
     if (pf.on) NS_CUDA(cudaEventRecord(pf.get(4 * j + 1), st));

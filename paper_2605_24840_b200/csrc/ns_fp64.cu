@@ -430,14 +430,17 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
   // update epilogue needs -- and no global re-read of X_j is required.
   constexpr int kJS = 4 / k64SPS;         // stages per 64-column block
   const int koff = (MODE == 1 || NS_K64_ROT0) ? (kJS * J + kJS) % nst : 0;
+  // a diagonal tile of a square (P == Q) needs one row panel, not two: the B fragments come from sA
+  const bool share = (MODE == 0) && (I == J) && p.diag_tri && p.same_pq;
   auto issue = [&](int kt) {
     const int s = kt % k64Stages;
     const int kb = (kt + koff) % nst;
-    mbar_arrive_expect_tx(&full[s], k64StageBytes);
+    mbar_arrive_expect_tx(&full[s], share ? k64StageBytes / 2 : k64StageBytes);
 #pragma unroll
     for (int u = 0; u < k64SPS; ++u) {
       tma_load_3d(sA + (s * k64SPS + u) * k64Tile * kBK, &tmP, (kb * k64SPS + u) * kBK, I * k64Tile, job, &full[s]);
-      tma_load_3d(sB + (s * k64SPS + u) * k64Tile * kBK, &tmQ, (kb * k64SPS + u) * kBK, J * k64Tile, job, &full[s]);
+      if (!share)
+        tma_load_3d(sB + (s * k64SPS + u) * k64Tile * kBK, &tmQ, (kb * k64SPS + u) * kBK, J * k64Tile, job, &full[s]);
     }
   };
   // X_j(r, c..c+1) of this tile (c even) from the ring after the K loop: the block's 16-column slab q sits in
@@ -502,15 +505,27 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
   double* C = p.C + base;
   const int i0 = I * k64Tile, j0 = J * k64Tile;
   double part = 0.0;
+  // MODE 0: off-diagonal squares in four independent DFMA chains (weight 2 applied once at the end): the FP64
+  // pipe is busy with the other CTAs' DMMAs, so the epilogue issues as few, and as independent, FP64
+  // instructions as it can
+  double sq0 = 0.0, sq1 = 0.0, sq2 = 0.0, sq3 = 0.0;
   const bool godd = (g & 1) != 0;
   // off-diagonal 8x8 block (r in rows, c >= every r): tile store + mirror, MODE 0 residual weight 2
-  auto put_full = [&](int r, int c, double v0, double v1) {
+  auto put_full = [&](int r, int c, double v0, double v1, int ch) {
+    if (MODE == 0) {
+      if (ch & 1) {
+        sq2 = fma(v0, v0, sq2);
+        sq3 = fma(v1, v1, sq3);
+      } else {
+        sq0 = fma(v0, v0, sq0);
+        sq1 = fma(v1, v1, sq1);
+      }
+    }
     stg_v2(C + (long long)(i0 + r) * ld + j0 + c, v0, v1);
     const double send = godd ? v0 : v1;
     const double recv = __shfl_xor_sync(0xffffffffu, send, 4);
     if (godd) stg_v2(C + (long long)(j0 + c + 1) * ld + i0 + r - 1, recv, v1);
     else stg_v2(C + (long long)(j0 + c) * ld + i0 + r, v0, recv);
-    if (MODE == 0) part += 2.0 * (v0 * v0 + v1 * v1);
   };
   // 8x8 block on the diagonal of a diagonal tile: elements c >= r (+ mirror), identity / trace / + cc I on c == r
   auto put_diag = [&](int r, int c, double v0, double v1) {
@@ -523,13 +538,14 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
         const bool in = i0 + r < p.d;
         if (MODE == 0) {
           const double e = in ? v - 1.0 : v;
-          part += e * e;
+          part = fma(e, e, part);
         } else if (in) {
           v += p.cc;
           part += v;
         }
       } else if (MODE == 0) {
-        part += 2.0 * v * v;
+        if (h) sq1 = fma(v, v, sq1);
+        else sq0 = fma(v, v, sq0);
       }
       C[(long long)(i0 + r) * ld + i0 + cc] = v;
       if (cc != r) C[(long long)(i0 + cc) * ld + i0 + r] = v;
@@ -582,7 +598,7 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
       for (int ni = 0; ni < NI; ++ni) {
         const int r = wm * 32 + mi * 8 + g, c = wn * WN + ni * 8 + 2 * t;
         const int rb = wm * 4 + mi, cb = wn * NI + ni;   // 8-blocks (warp-uniform)
-        if (!diag || rb < cb) put_full(r, c, acc[mi][ni][0], acc[mi][ni][1]);
+        if (!diag || rb < cb) put_full(r, c, acc[mi][ni][0], acc[mi][ni][1], mi * NI + ni);
         else if (rb == cb) put_diag(r, c, acc[mi][ni][0], acc[mi][ni][1]);
       }
   } else {
@@ -591,8 +607,9 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
     // blocks, so the four sub-partitions stay balanced (32x32 warp quadrants would leave one warp idle and one
     // at full load).  Batched d = 256: 17% fewer DMMAs per product.  NWP = 4: one warp per pair of rows;
     // NWP = 8: warp P takes row P, warp P + 4 row 7 - P.
-    auto rows_warp = [&](auto WC) {
+    auto rows_warp = [&](auto WC, auto SC) {
       constexpr int W = decltype(WC)::value;
+      constexpr bool SHARE = decltype(SC)::value;   // B fragments from sA; the A fragments are B fragments
       constexpr int P = W % 4;
       constexpr bool TWO = (NWP == 4);
       constexpr int R0 = (NWP == 8 && W >= 4) ? 7 - P : P, N0 = 8 - R0;
@@ -607,14 +624,23 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
         for (int hh = 0; hh < 2 * k64SPS; ++hh) {
           const int h = hh & 1;
           const uint32_t aS = sA_u32 + (s * k64SPS + (hh >> 1)) * (k64Tile * kBK * 8) + g * 128;
-          const uint32_t bS = sB_u32 + (s * k64SPS + (hh >> 1)) * (k64Tile * kBK * 8) + g * 128;
+          const uint32_t bS = SHARE ? aS : sB_u32 + (s * k64SPS + (hh >> 1)) * (k64Tile * kBK * 8) + g * 128;
           const uint32_t off = h ? off_h1 : off_h0;
           constexpr int B0 = TWO ? (R0 < R1 ? R0 : R1) : R0;   // first B block needed
           double a0[2], a1[2], b[8][2];
 #pragma unroll
           for (int cb = B0; cb < 8; ++cb) lds128(bS + cb * 8 * 128 + off, b[cb][0], b[cb][1]);
-          lds128(aS + R0 * 8 * 128 + off, a0[0], a0[1]);
-          if (TWO) lds128(aS + R1 * 8 * 128 + off, a1[0], a1[1]);
+          if (SHARE) {   // same panel, same k-permutation: row block R's A fragment is its B fragment
+            a0[0] = b[R0][0];
+            a0[1] = b[R0][1];
+            if (TWO) {
+              a1[0] = b[R1][0];
+              a1[1] = b[R1][1];
+            }
+          } else {
+            lds128(aS + R0 * 8 * 128 + off, a0[0], a0[1]);
+            if (TWO) lds128(aS + R1 * 8 * 128 + off, a1[0], a1[1]);
+          }
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
 #pragma unroll
@@ -645,32 +671,37 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
       for (int i = 0; i < N0; ++i) {
         const int r = R0 * 8 + g, c = (R0 + i) * 8 + 2 * t;
         if (i == 0) put_diag(r, c, c0[i][0], c0[i][1]);
-        else put_full(r, c, c0[i][0], c0[i][1]);
+        else put_full(r, c, c0[i][0], c0[i][1], i);
       }
 #pragma unroll
       for (int i = 0; i < N1; ++i) {
         const int r = R1 * 8 + g, c = (R1 + i) * 8 + 2 * t;
         if (i == 0) put_diag(r, c, c1[i][0], c1[i][1]);
-        else put_full(r, c, c1[i][0], c1[i][1]);
+        else put_full(r, c, c1[i][0], c1[i][1], i + 1);
       }
     };
-    switch (warp) {
-      case 0: rows_warp(std::integral_constant<int, 0>{}); break;
-      case 1: rows_warp(std::integral_constant<int, 1>{}); break;
-      case 2: rows_warp(std::integral_constant<int, 2>{}); break;
-      case 3: rows_warp(std::integral_constant<int, 3>{}); break;
+    auto rows_any = [&](auto SC) {
+      switch (warp) {
+        case 0: rows_warp(std::integral_constant<int, 0>{}, SC); break;
+        case 1: rows_warp(std::integral_constant<int, 1>{}, SC); break;
+        case 2: rows_warp(std::integral_constant<int, 2>{}, SC); break;
+        case 3: rows_warp(std::integral_constant<int, 3>{}, SC); break;
 #if NS_K64_WARPS == 8
-      case 4: rows_warp(std::integral_constant<int, 4>{}); break;
-      case 5: rows_warp(std::integral_constant<int, 5>{}); break;
-      case 6: rows_warp(std::integral_constant<int, 6>{}); break;
-      default: rows_warp(std::integral_constant<int, 7>{}); break;
+        case 4: rows_warp(std::integral_constant<int, 4>{}, SC); break;
+        case 5: rows_warp(std::integral_constant<int, 5>{}, SC); break;
+        case 6: rows_warp(std::integral_constant<int, 6>{}, SC); break;
+        default: rows_warp(std::integral_constant<int, 7>{}, SC); break;
 #endif
-    }
+      }
+    };
+    if (MODE == 0 && share) rows_any(std::true_type{});
+    else rows_any(std::false_type{});
   }
   const int tid = threadIdx.x;
 #if NS_P64_TRACE
   if (lane == 0) tr_wst[warp] = gtimer();
 #endif
+  if (MODE == 0) part = fma(2.0, (sq0 + sq1) + (sq2 + sq3), part);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
   if (lane == 0) red[warp] = part;

@@ -144,6 +144,7 @@ struct ProdParams {
   // own keeps the slots of the full list, so the decide's fixed-order sum is unchanged); nullptr = x
   const int* part_slot = nullptr;
   int diag_tri = 1;        // 64x64-tile kernel: diagonal tiles compute only their upper 8x8 blocks (NS_DIAG_TRI=0: full)
+  int same_pq = 0;         // mode 0: P and Q are the same matrix (diagonal tiles then load one panel, not two)
   int remote_mirror = 1;   // peer-store epilogue: also store the mirrored tile into the other destinations (0: the
                            // receivers mirror remote tiles themselves, launch_mirror_remote; half the NVLink bytes)
 };

@@ -99,6 +99,12 @@ int main() {
   run<8, 4>("64x32 warp tile", 2, 6, out);
   run<4, 2>("32x16 warp tile", 8, 3, out);
   run<2, 4>("16x32 warp tile", 4, 3, out);
+  // one and two K-loop warps per SM sub-partition (what a CTA sustains while its co-residents are outside their K loops)
+  run<4, 4>("32x32 warp tile, 1 warp/SMSP", 4, 1, out);
+  run<4, 4>("32x32 warp tile, 2 warps/SMSP", 4, 2, out);
+  run<8, 4>("64x32 warp tile, 1 warp/SMSP", 4, 1, out);
+  run<4, 8>("32x64 warp tile, 1 warp/SMSP", 4, 1, out);
+  run<4, 8>("32x64 warp tile, 2 warps/SMSP", 4, 2, out);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) printf("CUDA error %s\n", cudaGetErrorString(e));
   return 0;
