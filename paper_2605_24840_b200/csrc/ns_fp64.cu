@@ -505,13 +505,32 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
   double* C = p.C + base;
   const int i0 = I * k64Tile, j0 = J * k64Tile;
   double part = 0.0;
+  unsigned dbg_x = 0;
+  auto dbg_epilogue = [&]() {   // sensitivity experiments: idle time vs issued instructions in a CTA's epilogue
+    if (p.dbg_sleep > 0) __nanosleep(p.dbg_sleep);
+    if (p.dbg_int) {
+      unsigned x0 = lane, x1 = 7, x2 = 9, x3 = 11;
+      for (int i = 0; i < p.dbg_int; ++i) {
+        asm volatile("lop3.b32 %0, %0, %1, 0x5a5a5a5a, 0x96;" : "+r"(x0) : "r"(x1));
+        asm volatile("add.u32 %0, %0, %1;" : "+r"(x1) : "r"(x2));
+        asm volatile("lop3.b32 %0, %0, %1, 0x33333333, 0x96;" : "+r"(x2) : "r"(x3));
+        asm volatile("add.u32 %0, %0, %1;" : "+r"(x3) : "r"(x0));
+      }
+      dbg_x = x0 + x1 + x2 + x3;
+    }
+  };
   // MODE 0: off-diagonal squares in four independent DFMA chains (weight 2 applied once at the end): the FP64
   // pipe is busy with the other CTAs' DMMAs, so the epilogue issues as few, and as independent, FP64
   // instructions as it can
   double sq0 = 0.0, sq1 = 0.0, sq2 = 0.0, sq3 = 0.0;
   const bool godd = (g & 1) != 0;
   // off-diagonal 8x8 block (r in rows, c >= every r): tile store + mirror, MODE 0 residual weight 2
-  auto put_full = [&](int r, int c, double v0, double v1, int ch) {
+  // tp = &C[r][c] and mp = this lane's mirror address (even g: &C[c][r], odd g: &C[c+1][r-1]) are formed by the
+  // callers from per-warp base pointers with constant strides: next to a saturated DMMA stream every issued
+  // integer instruction costs ~0.5 clk of DMMA time (profiles/r02_dmma_issue.txt), and the per-fragment 64-bit
+  // address arithmetic was most of this epilogue's ~45 instructions per fragment
+  const long long ld8 = 8 * ld;
+  auto put_full = [&](double* tp, double* mp, double v0, double v1, int ch) {
     if (MODE == 0) {
       if (ch & 1) {
         sq2 = fma(v0, v0, sq2);
@@ -521,11 +540,10 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
         sq1 = fma(v1, v1, sq1);
       }
     }
-    stg_v2(C + (long long)(i0 + r) * ld + j0 + c, v0, v1);
+    stg_v2(tp, v0, v1);
     const double send = godd ? v0 : v1;
     const double recv = __shfl_xor_sync(0xffffffffu, send, 4);
-    if (godd) stg_v2(C + (long long)(j0 + c + 1) * ld + i0 + r - 1, recv, v1);
-    else stg_v2(C + (long long)(j0 + c) * ld + i0 + r, v0, recv);
+    stg_v2(mp, godd ? recv : v0, godd ? v1 : recv);
   };
   // 8x8 block on the diagonal of a diagonal tile: elements c >= r (+ mirror), identity / trace / + cc I on c == r
   auto put_diag = [&](int r, int c, double v0, double v1) {
@@ -579,6 +597,16 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
             for (int ni = 0; ni < NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi][e], b[ni][e]);
       }
     });
+    dbg_epilogue();
+    if (p.dbg_sleep < 0) {   // timing only: no epilogue at all (one store keeps the accumulators live)
+      double sum = 0.0;
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) sum += acc[mi][ni][0] + acc[mi][ni][1];
+      if (sum == 1.2345e300) C[0] = sum;
+      return;
+    }
     if (MODE == 1) {   // X_{j+1} = ca X_j + cb Z in registers, X_j from the ring
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
@@ -592,15 +620,26 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
 #if NS_P64_TRACE
     if (lane == 0) tr_wend[warp] = gtimer();
 #endif
+    double* const T0 = C + (long long)(i0 + wm * 32 + g) * ld + j0 + wn * WN + 2 * t;
+    double* const M0 = C + (long long)(j0 + wn * WN + 2 * t + (godd ? 1 : 0)) * ld + i0 + wm * 32 + g - (godd ? 1 : 0);
+    if (!diag) {
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+      for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < NI; ++ni) {
-        const int r = wm * 32 + mi * 8 + g, c = wn * WN + ni * 8 + 2 * t;
-        const int rb = wm * 4 + mi, cb = wn * NI + ni;   // 8-blocks (warp-uniform)
-        if (!diag || rb < cb) put_full(r, c, acc[mi][ni][0], acc[mi][ni][1], mi * NI + ni);
-        else if (rb == cb) put_diag(r, c, acc[mi][ni][0], acc[mi][ni][1]);
-      }
+        for (int ni = 0; ni < NI; ++ni)
+          put_full(T0 + mi * ld8 + ni * 8, M0 + ni * ld8 + mi * 8, acc[mi][ni][0], acc[mi][ni][1], mi * NI + ni);
+    } else {   // full diagonal tile (NS_DIAG_TRI=0 only): upper 8x8 blocks + the blocks on the diagonal
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) {
+          const int rb = wm * 4 + mi, cb = wn * NI + ni;   // 8-blocks (warp-uniform)
+          if (rb < cb)
+            put_full(T0 + mi * ld8 + ni * 8, M0 + ni * ld8 + mi * 8, acc[mi][ni][0], acc[mi][ni][1], ni);
+          else if (rb == cb)
+            put_diag(wm * 32 + mi * 8 + g, wn * WN + ni * 8 + 2 * t, acc[mi][ni][0], acc[mi][ni][1]);
+        }
+    }
   } else {
     // Diagonal tile: only the 36 upper-triangle 8x8 blocks (rb <= cb) of the 8x8 block grid are needed.
     // Each SM sub-partition (warps w, w + 4 when NWP = 8) takes block rows P and 7 - P: (8 - P) + (P + 1) = 9
@@ -667,17 +706,20 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
 #if NS_P64_TRACE
       if (lane == 0) tr_wend[warp] = gtimer();
 #endif
+      // block row R: fragment i is the 8x8 block (R, R + i) of this diagonal tile
+      double* const TR0 = C + (long long)(i0 + R0 * 8 + g) * ld + i0 + R0 * 8 + 2 * t;
+      double* const MR0 = C + (long long)(i0 + R0 * 8 + 2 * t + (godd ? 1 : 0)) * ld + i0 + R0 * 8 + g - (godd ? 1 : 0);
 #pragma unroll
       for (int i = 0; i < N0; ++i) {
-        const int r = R0 * 8 + g, c = (R0 + i) * 8 + 2 * t;
-        if (i == 0) put_diag(r, c, c0[i][0], c0[i][1]);
-        else put_full(r, c, c0[i][0], c0[i][1], i);
+        if (i == 0) put_diag(R0 * 8 + g, R0 * 8 + 2 * t, c0[i][0], c0[i][1]);
+        else put_full(TR0 + i * 8, MR0 + i * ld8, c0[i][0], c0[i][1], i);
       }
+      double* const TR1 = C + (long long)(i0 + R1 * 8 + g) * ld + i0 + R1 * 8 + 2 * t;
+      double* const MR1 = C + (long long)(i0 + R1 * 8 + 2 * t + (godd ? 1 : 0)) * ld + i0 + R1 * 8 + g - (godd ? 1 : 0);
 #pragma unroll
       for (int i = 0; i < N1; ++i) {
-        const int r = R1 * 8 + g, c = (R1 + i) * 8 + 2 * t;
-        if (i == 0) put_diag(r, c, c1[i][0], c1[i][1]);
-        else put_full(r, c, c1[i][0], c1[i][1], i + 1);
+        if (i == 0) put_diag(R1 * 8 + g, R1 * 8 + 2 * t, c1[i][0], c1[i][1]);
+        else put_full(TR1 + i * 8, MR1 + i * ld8, c1[i][0], c1[i][1], i + 1);
       }
     };
     auto rows_any = [&](auto SC) {
@@ -702,6 +744,7 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
   if (lane == 0) tr_wst[warp] = gtimer();
 #endif
   if (MODE == 0) part = fma(2.0, (sq0 + sq1) + (sq2 + sq3), part);
+  if (dbg_x == 0x12345678u) part += 1.0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
   if (lane == 0) red[warp] = part;
@@ -926,6 +969,10 @@ cudaError_t launch_product64(const CUtensorMap& tmP, const CUtensorMap& tmQ, con
   static unsigned long long attr[2] = {0, 0};
   ProdParams p = p_in;
   p.diag_tri = diag_tri_env();
+  static const int dbg_sleep = [] { const char* e = getenv("NS_P64_DBG_SLEEP"); return e ? atoi(e) : 0; }();
+  static const int dbg_int = [] { const char* e = getenv("NS_P64_DBG_INT"); return e ? atoi(e) : 0; }();
+  p.dbg_sleep = dbg_sleep;
+  p.dbg_int = dbg_int;
   dim3 grid(p.n_tiles, batch);
   if (p.mode == 0) {
     smem_attr(ns_product64_kernel<0>, k64SmemBytes, attr[0]);

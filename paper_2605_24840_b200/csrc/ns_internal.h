@@ -145,6 +145,8 @@ struct ProdParams {
   const int* part_slot = nullptr;
   int diag_tri = 1;        // 64x64-tile kernel: diagonal tiles compute only their upper 8x8 blocks (NS_DIAG_TRI=0: full)
   int same_pq = 0;         // mode 0: P and Q are the same matrix (diagonal tiles then load one panel, not two)
+  int dbg_sleep = 0;       // experiments (NS_P64_DBG_SLEEP, ns): every DMMA warp idles this long before its epilogue
+  int dbg_int = 0;         // experiments (NS_P64_DBG_INT): ... and issues this many x4 extra integer instructions
   int remote_mirror = 1;   // peer-store epilogue: also store the mirrored tile into the other destinations (0: the
                            // receivers mirror remote tiles themselves, launch_mirror_remote; half the NVLink bytes)
 };

@@ -861,10 +861,11 @@ def test_cfg2_seed1_golden(nsr, golden_dir):
 
 
 # ------------------------------------------------------------------ kernel-selection alternatives
-@pytest.mark.parametrize("env", [{"NS_MX2": "0"}, {"NS_TILE64": "0"}, {"NS_TILE64": "1"}, {"NS_SHARD_P2P": "0"}])
+@pytest.mark.parametrize("env", [{"NS_MX2": "0"}, {"NS_TILE64": "0"}, {"NS_TILE64": "1"}, {"NS_SHARD_P2P": "0"},
+                                 {"NS_TILE64": "1", "NS_DIAG_TRI": "0"}])
 def test_alternative_kernels(nsr, env):
-    """The one-SM split-precision kernel (NS_MX2=0) and the forced 128- / 64-tile FP64 kernels give the
-    same answers as the defaults (the knobs are read once per process: run in a subprocess)."""
+    """The one-SM split-precision kernel (NS_MX2=0), the forced 128- / 64-tile FP64 kernels and the 64-tile kernel
+    with full diagonal tiles (NS_DIAG_TRI=0) give the same answers as the defaults (the knobs are read once per process: run in a subprocess)."""
     import json
     import subprocess
     import sys
