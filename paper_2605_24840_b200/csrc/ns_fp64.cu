@@ -376,6 +376,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 __device__ __forceinline__ void stg_v2(double* p, double x, double y) {
   asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(x), "d"(y) : "memory");
 }
+#ifndef NS_K64_MIRROR8
+#define NS_K64_MIRROR8 1   // 0: mirror by one 16-byte store after a lane shuffle (8 rows x 64 B per warp store)
+#endif
 #ifndef NS_P64_TRACE
 #define NS_P64_TRACE 0   // 1: every CTA of the 64-tile kernel records %globaltimer phase stamps (tools/p64_trace.py)
 #endif
@@ -530,6 +533,7 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
   // integer instruction costs ~0.5 clk of DMMA time (profiles/r02_dmma_issue.txt), and the per-fragment 64-bit
   // address arithmetic was most of this epilogue's ~45 instructions per fragment
   const long long ld8 = 8 * ld;
+  constexpr int kGo = NS_K64_MIRROR8 ? 0 : 1;   // 16-byte mirror stores: odd g stores row c + 1 from column r - 1
   auto put_full = [&](double* tp, double* mp, double v0, double v1, int ch) {
     if (MODE == 0) {
       if (ch & 1) {
@@ -541,9 +545,16 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
       }
     }
     stg_v2(tp, v0, v1);
+#if NS_K64_MIRROR8
+    // mirror by two 8-byte stores (C[c][r] and C[c+1][r]; a warp store covers 4 rows x 64 contiguous bytes): no
+    // shuffle and no lane-parity selects -- 3 instead of 10 instructions per fragment next to the DMMA stream
+    mp[0] = v0;
+    mp[ld] = v1;
+#else
     const double send = godd ? v0 : v1;
     const double recv = __shfl_xor_sync(0xffffffffu, send, 4);
     stg_v2(mp, godd ? recv : v0, godd ? v1 : recv);
+#endif
   };
   // 8x8 block on the diagonal of a diagonal tile: elements c >= r (+ mirror), identity / trace / + cc I on c == r
   auto put_diag = [&](int r, int c, double v0, double v1) {
@@ -621,7 +632,7 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
     if (lane == 0) tr_wend[warp] = gtimer();
 #endif
     double* const T0 = C + (long long)(i0 + wm * 32 + g) * ld + j0 + wn * WN + 2 * t;
-    double* const M0 = C + (long long)(j0 + wn * WN + 2 * t + (godd ? 1 : 0)) * ld + i0 + wm * 32 + g - (godd ? 1 : 0);
+    double* const M0 = C + (long long)(j0 + wn * WN + 2 * t + kGo * (godd ? 1 : 0)) * ld + i0 + wm * 32 + g - kGo * (godd ? 1 : 0);
     if (!diag) {
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
@@ -708,14 +719,14 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
 #endif
       // block row R: fragment i is the 8x8 block (R, R + i) of this diagonal tile
       double* const TR0 = C + (long long)(i0 + R0 * 8 + g) * ld + i0 + R0 * 8 + 2 * t;
-      double* const MR0 = C + (long long)(i0 + R0 * 8 + 2 * t + (godd ? 1 : 0)) * ld + i0 + R0 * 8 + g - (godd ? 1 : 0);
+      double* const MR0 = C + (long long)(i0 + R0 * 8 + 2 * t + kGo * (godd ? 1 : 0)) * ld + i0 + R0 * 8 + g - kGo * (godd ? 1 : 0);
 #pragma unroll
       for (int i = 0; i < N0; ++i) {
         if (i == 0) put_diag(R0 * 8 + g, R0 * 8 + 2 * t, c0[i][0], c0[i][1]);
         else put_full(TR0 + i * 8, MR0 + i * ld8, c0[i][0], c0[i][1], i);
       }
       double* const TR1 = C + (long long)(i0 + R1 * 8 + g) * ld + i0 + R1 * 8 + 2 * t;
-      double* const MR1 = C + (long long)(i0 + R1 * 8 + 2 * t + (godd ? 1 : 0)) * ld + i0 + R1 * 8 + g - (godd ? 1 : 0);
+      double* const MR1 = C + (long long)(i0 + R1 * 8 + 2 * t + kGo * (godd ? 1 : 0)) * ld + i0 + R1 * 8 + g - kGo * (godd ? 1 : 0);
 #pragma unroll
       for (int i = 0; i < N1; ++i) {
         if (i == 0) put_diag(R1 * 8 + g, R1 * 8 + 2 * t, c1[i][0], c1[i][1]);
