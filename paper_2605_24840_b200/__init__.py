@@ -5,6 +5,7 @@ kernels of the shared library.  torch is used for device memory and streams.  Th
 is no CPU fallback: importing this package on a machine without the built library
 raises, and calling it with CPU tensors raises.
 """
+import collections.abc
 import ctypes
 import os
 
@@ -42,6 +43,35 @@ class NsResult(ctypes.Structure):
         return dict(steps=self.steps, flags=self.flags, residual=self.residual, trace=self.trace,
                     cert=self.index_cert, launches=self.kernel_launches, switch_step=self.switch_step,
                     pre_polish_residual=self.pre_polish_residual, alpha=self.alpha)
+
+
+class _ResultList(collections.abc.Sequence):
+    """Per-problem result records of a batched call, converted to dicts on access (building thousands of dicts
+    eagerly cost ~4 ms per configs[1] call -- marshalling, so it stays out of the call)."""
+
+    def __init__(self, arr):
+        self._arr = arr
+
+    def __len__(self):
+        return len(self._arr)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self._arr[j].as_dict() for j in range(*i.indices(len(self._arr)))]
+        return self._arr[i].as_dict()
+
+    def __eq__(self, other):
+        if isinstance(other, (_ResultList, list, tuple)):
+            return len(self) == len(other) and all(a == b for a, b in zip(self, other))
+        return NotImplemented
+
+    def __repr__(self):
+        return repr(list(self))
+
+    def column(self, name):
+        """One field of every record as a numpy array (steps, flags, residual, trace, cert, ...)."""
+        field = {"cert": "index_cert", "launches": "kernel_launches"}.get(name, name)
+        return np.array([getattr(r, field) for r in self._arr])
 
 
 class NsOptions(ctypes.Structure):
@@ -385,7 +415,7 @@ def ns_reflector_batched(H, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_ABS, pr
                                       int(prec), ctypes.c_void_p(R.data_ptr()), R.stride(0),
                                       ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream, H.device), outs)
     _check(st)
-    return R, [o.as_dict() for o in outs]
+    return R, _ResultList(outs)
 
 
 def ns_reflector_batched_dev(H, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_ABS, prec=NS_PREC_FP64, R=None,
@@ -413,7 +443,7 @@ def ns_reflector_batched_dev(H, s, alpha, k, max_steps, tol, tol_mode=NS_TOL_ABS
                                           ctypes.c_void_p(R.data_ptr()), R.stride(0), ctypes.c_void_p(ws.data_ptr()),
                                           ws.numel(), _stream_ptr(stream, H.device), outs)
     _check(st)
-    return R, [o.as_dict() for o in outs]
+    return R, _ResultList(outs)
 
 
 def ns_inertia(H, s, prec=NS_PREC_FP64, max_steps=100, ws=None, stream=None):
