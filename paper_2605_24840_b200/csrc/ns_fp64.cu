@@ -376,6 +376,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 __device__ __forceinline__ void stg_v2(double* p, double x, double y) {
   asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(x), "d"(y) : "memory");
 }
+#ifndef NS_K64_HH_UNROLL
+#define NS_K64_HH_UNROLL 4   // half-slabs of a ring stage unrolled in the K loop (4 = the whole stage)
+#endif
+constexpr int kHHUnroll = NS_K64_HH_UNROLL;
 #ifndef NS_K64_MIRROR8
 #define NS_K64_MIRROR8 1   // 0: mirror by one 16-byte store after a lane shuffle (8 rows x 64 B per warp store)
 #endif
@@ -589,7 +593,7 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
 #pragma unroll
       for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
     mainloop([&](int s) {
-#pragma unroll
+#pragma unroll(kHHUnroll)
       for (int hh = 0; hh < 2 * k64SPS; ++hh) {
         const int h = hh & 1;
         const uint32_t aS = sA_u32 + (s * k64SPS + (hh >> 1)) * (k64Tile * kBK * 8) + a_row;
@@ -670,7 +674,7 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
 #pragma unroll
       for (int i = 0; i < N1; ++i) c1[i][0] = c1[i][1] = 0.0;
       mainloop([&](int s) {
-#pragma unroll
+#pragma unroll(kHHUnroll)
         for (int hh = 0; hh < 2 * k64SPS; ++hh) {
           const int h = hh & 1;
           const uint32_t aS = sA_u32 + (s * k64SPS + (hh >> 1)) * (k64Tile * kBK * 8) + g * 128;
