@@ -85,3 +85,23 @@ def test_product_path_has_no_oracle_or_fallback():
                     src = f.read()
                 assert "oracle" not in src.replace("oracle/", ""), fn
                 assert "import numpy.linalg" not in src and "np.linalg" not in src, fn
+
+
+def test_batched_result_records_are_a_sequence_of_dicts():
+    """The batched entries return their per-problem records as a sequence that builds each dict on access
+    (marshalling only: no arithmetic); it indexes, slices, iterates and compares like the list of dicts it replaces."""
+    import paper_2605_24840_b200 as nsr
+    n = 5
+    raw = (nsr.NsResult * n)()
+    for i in range(n):
+        raw[i].steps, raw[i].flags, raw[i].index_cert, raw[i].residual = i + 1, 1, 7 - i, 0.5 * i
+    outs = nsr._ResultList(raw)
+    assert len(outs) == n and outs[2]["steps"] == 3 and outs[-1]["cert"] == 3
+    assert [o["steps"] for o in outs] == [1, 2, 3, 4, 5]
+    assert outs[1:3] == [outs[1], outs[2]] and isinstance(outs[1:3], list)
+    assert outs == list(outs) and outs == nsr._ResultList(raw)
+    other = (nsr.NsResult * n)()
+    assert outs != nsr._ResultList(other)
+    assert outs.column("steps").tolist() == [1, 2, 3, 4, 5] and outs.column("cert").tolist() == [7, 6, 5, 4, 3]
+    with pytest.raises(IndexError):
+        outs[n]
