@@ -1073,6 +1073,40 @@ def test_random_sweep_mixed(nsr, seed, prec):
     assert checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= TOL_R
 
 
+@pytest.mark.parametrize("seed,dmax,prec", [(20000, 600, 1), (20000, 600, 2), (20022, 600, 2), (20512, 3000, 1)])
+def test_mixed_late_switch(nsr, seed, dmax, prec):
+    """Problems on which quadratic convergence carries the residual from above the switch threshold to below the
+    split-precision noise floor in one step (found by tools/stress_sweep.py, whose generator this repeats): the
+    switch lands on an iterate as close to its reflector as the low-precision eigenvalue noise, and before the
+    late-switch redo step (DESIGN reading C16b) the mixed path took one step fewer (seeds 20000, 20022) or more
+    (20512) than the oracle.  With it: the oracle's step count, its decision residual to a few percent, and R far
+    inside the tolerance."""
+    rng = np.random.default_rng(seed)
+    d = int(rng.integers(1, dmax))
+    k = int(rng.integers(0, d + 1))
+    g = 10.0 ** rng.uniform(-3.5, math.log10(0.5))
+    cluster = rng.random() < 0.3
+    neg = -rng.uniform(g / 2, 1.0, k) if not cluster else -(g / 2 + rng.exponential(0.01, k))
+    pos = rng.uniform(g / 2, 1.0, d - k) if not cluster else g / 2 + rng.exponential(0.01, d - k)
+    lam = np.concatenate([neg, pos]) * 10.0 ** rng.uniform(-2, 2)
+    Q = workloads.haar_q(rng, d)
+    H = (Q * lam[None, :]) @ Q.T
+    H = 0.5 * (H + H.T)
+    scale = float(np.max(np.abs(lam)))
+    s = float(rng.uniform(-0.4, 0.4) * g * scale)
+    alpha = float(np.max(np.abs(lam - s))) * float(rng.choice([1.0, 1.001, 1.1, 2.0]))
+    alpha = max(alpha, float(np.linalg.norm(H - s * np.eye(d), 2)) * 1.01)
+    tol, tm = 1e-10, 1
+    o = ons.ns_reflector(H, s, alpha, k, 100, tol, tm, trace_residuals=True)
+    h, sqd = o["hist_residual"], math.sqrt(d)
+    R, res = nsr.ns_reflector(torch.from_numpy(H).to(_dev()), s, alpha, k, 100, tol, tm, prec=prec)
+    sw = res["switch_step"]
+    assert 1 <= sw < o["steps"] and h[sw - 1] / sqd >= 1e-3 and h[sw] / sqd < 1e-4   # a late switch
+    assert res["steps"] == o["steps"] and res["cert"] == o["cert"] == k and res["flags"] == o["flags"]
+    assert abs(res["residual"] - h[o["steps"]]) <= 0.1 * h[o["steps"]]
+    assert checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= 1e-12
+
+
 @pytest.mark.parametrize("seed", range(8))
 def test_random_sweep_sharded_host_filters(nsr, seed):
     """Random problems through the remaining entries: P ranks emulated on one GPU (random P, ragged d),

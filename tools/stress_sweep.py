@@ -24,14 +24,15 @@ def tie(o, tol, tm, d):
 
 def mixed_step_ok(r, o, tol, tm, d):
     """Reading C16b (round 2: switch at r/sqrt(d) < 1e-3): the mixed path must take the oracle's step count; a
-    difference of one is reported separately (not a failure) only when the oracle's residual at its decision step
-    or the one before lies within 3% of the threshold -- the measured predicate DESIGN C16b names (never observed
-    in the 440-problem sweep)."""
+    difference of one is not a failure only inside the predicate DESIGN C16b names: the oracle's residual at its
+    decision step or the one before within 3% of the threshold (a late switch is handled by the library: the last
+    low-precision step is redone in FP64-class arithmetic)."""
     t = tol if tm == 0 else tol * math.sqrt(d)
     h = o["hist_residual"]
     if abs(r["steps"] - o["steps"]) != 1:
         return False
-    return any(0.97 * t <= h[j] <= 1.03 * t for j in (o["steps"] - 1, o["steps"]) if 0 <= j < len(h))
+    band = 0.03
+    return any((1 - band) * t <= h[j] <= (1 + band) * t for j in (o["steps"] - 1, o["steps"]) if 0 <= j < len(h))
 
 
 def problem(seed, dmax):
