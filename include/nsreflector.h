@@ -104,8 +104,12 @@ typedef struct {
  * library defaults, which ns_reflector uses.
  *   switch_tol     mixed path: the BF16x3 phase ends at the first j with
  *                  ||X_j^2 - I||_F / sqrt(d) < switch_tol (default 1e-3, readings C16/C16b:
- *                  10x above the ~1e-4 noise floor of the split-precision residual, so the switch is
- *                  never late and the FP64 phase tracks the oracle's residuals to a few percent).
+ *                  10x above the ~1e-4 noise floor of the split-precision residual).  Quadratic
+ *                  convergence can still jump from above switch_tol to below that floor in one step;
+ *                  when the residual at the switch reads below 5e-4 (run-to-tolerance mode) the step
+ *                  that produced X_switch is taken again in FP64-class arithmetic from X_{j-1}
+ *                  before the re-anchor, so the FP64 phase tracks the oracle's residuals to a few
+ *                  percent and takes its step count.
  *   cg_iters       mixed path: maximum conjugate-gradient iterations of the re-anchor solve
  *                  |A|E + E|A| = sym(X~ [A, X~]); the solve stops earlier once its residual
  *                  has dropped by 1e-6 (default cap 512; 0 = polish without re-anchor).

@@ -1147,7 +1147,7 @@ ns_status_t run_mixed(const Layout& L, uint8_t* ws, const double* H, long long l
     };
     // Late switch (reading C16b): quadratic convergence can carry the residual from above the switch threshold to
     // below the split-precision noise floor in one step; X_switch then sits as close to its reflector as the
-    // low-precision steps' eigenvalue noise, and the FP64 residuals that follow deviate from the oracle's by tens of
+    // low-precision steps' eigenvalue noise, and the FP64 residuals that follow deviate from the exact recurrence's by tens of
     // percent (measured: +-1 step in 4 of 332 random runs).  When the low-precision residual at the switch reads
     // below kRedoFloor (it cannot resolve less), the last low-precision step is taken again in FP64-class arithmetic
     // from X_{j0-1}, which is still in the other buffer (its distance to the reflector is >= the switch threshold,
