@@ -1103,7 +1103,7 @@ def test_mixed_late_switch(nsr, seed, dmax, prec):
     sw = res["switch_step"]
     assert 1 <= sw < o["steps"] and h[sw - 1] / sqd >= 1e-3 and h[sw] / sqd < 1e-4   # a late switch
     assert res["steps"] == o["steps"] and res["cert"] == o["cert"] == k and res["flags"] == o["flags"]
-    assert abs(res["residual"] - h[o["steps"]]) <= 0.1 * h[o["steps"]]
+    assert abs(res["residual"] - h[o["steps"]]) <= 0.1 * h[o["steps"]] + 64 * 1.1e-16 * d   # + the rounding floor
     assert checks.frob_per_sqrt_d(R.cpu().numpy(), o["R"]) <= 1e-12
 
 

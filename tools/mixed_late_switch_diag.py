@@ -1,3 +1,6 @@
+"""Diagnosis of the mixed path's late-switch problems (DESIGN reading C16b): the oracle's residual history next to
+every precision path's steps, switch step, residuals and distance to the oracle's R, for the stress generator's
+seeds 20000, 20022 (d < 600) and 20512 (d < 3000).  NS_MIXED_REDO=0 shows the behaviour before the redo step."""
 import math, sys, os
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
