@@ -502,8 +502,9 @@ __global__ void __launch_bounds__(k64Threads, k64MinBlocks)
   };
   // ---------------- epilogue straight from the accumulator registers ----------------
   // Lane (g, t) of a fragment holds C[r][c], C[r][c+1] (r = 8-row base + g, c = 8-col base + 2t): one 16-byte
-  // store for the tile and, after one shuffle with lane g ^ 1, one 16-byte store for the mirror (even g takes
-  // row c: (r, r+1), odd g row c+1: (r-1, r)); every warp store covers 8 rows x 64 contiguous bytes.  No
+  // store for the tile (8 rows x 64 contiguous bytes per warp store) and two 8-byte stores for the mirror,
+  // C[c][r] and C[c+1][r] (4 rows x 64 bytes each; NS_K64_MIRROR8=0: one 16-byte store after a shuffle with lane
+  // g ^ 1 -- even g takes row c: (r, r+1), odd g row c+1: (r-1, r)).  No
   // shared-memory staging and no block barrier before the stores (the staged epilogue -- fragments to a padded
   // smem tile, then coalesced row and column passes -- took ~25% of a CTA's warp time in ncu; cfg1 118.3 ->
   // 115.9 ms).  Diagonal 8x8 blocks keep c >= r and mirror it, so every stored matrix is bitwise symmetric.
